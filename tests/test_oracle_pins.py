@@ -1,0 +1,303 @@
+"""Pins for the CPU oracle (oracle/messi_oracle.c) against things other than itself:
+textbook constants, independent library routines (scipy.special.ndtri / ndtr,
+statistics.NormalDist, numpy.searchsorted, scipy.ndimage filters, numpy argmin),
+paper invariants (Property 1; the LB_Keogh chain) and brute
+force over all warping paths on tiny inputs.  CPU only (no gpu marker).
+"""
+import itertools
+import json
+import math
+import os
+from statistics import NormalDist
+
+import numpy as np
+import pytest
+import scipy.ndimage as ndi
+import scipy.special as sps
+
+import oracle
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_pins.json")))
+
+
+def zwalks(rows, n, seed):
+    """z-normalised random walks -- numpy, test-local."""
+    rng = np.random.default_rng(seed)
+    x = np.cumsum(rng.standard_normal((rows, n)), axis=1)
+    x = (x - x.mean(1, keepdims=True)) / x.std(1, keepdims=True)
+    return x.astype(np.float32)
+
+
+# ------------------------------------------------------------------ breakpoints (O3)
+def test_breakpoints_match_independent_quantile_routines():
+    b64, b32 = oracle.breakpoints(256)
+    k = np.arange(1, 256)
+    ref = sps.ndtri(k / 256.0)
+    assert np.allclose(b64, ref, rtol=4e-15, atol=1e-15)
+    nd = NormalDist()
+    ref2 = np.array([nd.inv_cdf(kk / 256.0) for kk in k])
+    assert np.allclose(b64, ref2, rtol=4e-15, atol=1e-15)
+    # the fp32 table the symbols use is the correctly rounded float of the quantile
+    assert np.array_equal(b32, ref.astype(np.float32))
+    assert np.all(np.diff(b64) > 0)
+
+
+def test_breakpoints_closed_forms():
+    b64, _ = oracle.breakpoints(256)
+    q = GOLD["quartile_beta"]["value"]
+    assert b64[127] == 0.0  # beta_128 = median
+    assert abs(b64[191] - q) <= 2e-16 and abs(b64[63] + q) <= 2e-16
+    assert np.allclose(b64[::-1], -b64, rtol=0, atol=1e-15)  # symmetry beta_{256-k} = -beta_k
+    assert oracle.breakpoints(2)[0].tolist() == GOLD["card2_breakpoints"]["value"]
+    assert np.allclose(oracle.breakpoints(4)[0], GOLD["card4_breakpoints"]["value"], atol=1e-4)
+    for card in (2, 4, 8, 16, 32, 64, 128, 256):
+        bb, _ = oracle.breakpoints(card)
+        edges = np.concatenate([[-np.inf], bb, [np.inf]])
+        probs = np.diff(sps.ndtr(edges))
+        assert np.allclose(probs, 1.0 / card, atol=1e-14)  # equiprobable regions
+    with pytest.raises(ValueError):
+        oracle.breakpoints(3)
+
+
+# ----------------------------------------------------------------------- symbols (O4)
+def test_symbol_cases_and_prefix_property():
+    _, b32 = oracle.breakpoints(256)
+    for v, s in GOLD["symbols"]["cases"]:
+        assert oracle.symbol(v, b32) == s
+    # value exactly on a breakpoint goes to the region above; just below -> region below
+    assert oracle.symbol(b32[191], b32) == 192
+    assert oracle.symbol(np.nextafter(b32[191], np.float32(-np.inf)), b32) == 191
+    _, b4 = oracle.breakpoints(4)
+    assert oracle.symbol(0.2, b4, 4) == GOLD["symbols"]["card4_of_0.2"]
+    assert oracle.symbol(-5.0, b4, 4) == 0 and oracle.symbol(5.0, b4, 4) == 3
+    rng = np.random.default_rng(3)
+    xs = np.concatenate([rng.standard_normal(4000), b32, np.nextafter(b32, -np.inf)]).astype(np.float32)
+    tables = {c: oracle.breakpoints(c)[1] for c in (2, 4, 16, 256)}
+    for x in xs:
+        s256 = oracle.symbol(x, b32)
+        # independent library routine: count of breakpoints <= x
+        assert s256 == int(np.searchsorted(b32, x, side="right"))
+        for c, tb in tables.items():
+            # prefix soundness: the card-c symbol is the bit prefix of the 8-bit one
+            assert oracle.symbol(x, tb, c) == s256 >> (8 - int(math.log2(c)))
+
+
+# --------------------------------------------------------------------------- PAA (O2)
+def test_paa_examples():
+    g = GOLD["paa_spec"]
+    assert oracle.paa32(g["x"], g["w"]).tolist() == g["paa"]
+    assert np.all(oracle.paa32(np.full(64, 0.375, np.float32), 16) == np.float32(0.375))
+    g = GOLD["worked_isax"]
+    p, s = oracle.isax(g["x"], g["w"])
+    assert p.tolist() == g["paa"]
+    assert s.tolist() == g["sym256"]
+    # the symbols agree with floor(256 * Phi(paa)) from a normal table
+    assert [int(256 * v) for v in g["phi_of_paa"]] == g["sym256"]
+    assert (s >> 6).tolist() == g["card4_word"]
+    with pytest.raises(ValueError):
+        oracle.paa32(np.zeros(10, np.float32), 3)  # n % w != 0 rejected
+    with pytest.raises(ValueError):
+        oracle.paa32(np.zeros(4, np.float32), 8)  # w > n rejected
+
+
+def test_paa_matches_numpy_mean():
+    X = zwalks(200, 256, 7)
+    for x in X:
+        ref = x.astype(np.float64).reshape(16, 16).mean(1)
+        assert np.allclose(oracle.paa64(x, 16), ref, rtol=1e-14, atol=1e-15)
+        assert np.allclose(oracle.paa32(x, 16), ref.astype(np.float32), rtol=1e-6, atol=1e-7)
+
+
+# ----------------------------------------------------------------------- mindist (O6)
+def test_mindist_closed_form_and_zero_on_own_box():
+    g = GOLD["mindist_closed_form"]
+    rng = np.random.default_rng(5)
+    x = zwalks(1, 256, 11)[0]
+    qpaa = oracle.paa64(x, 16)
+    _, sym = oracle.isax(x, 16)
+    # a series' PAA lies inside its own boxes (up to the fp32 rounding of the PAA)
+    assert oracle.mindist2(oracle.paa32(x, 16).astype(np.float64), sym, 256) == 0.0
+    # closed form: query PAA 0 vs symbol 192 in segment 0, own boxes elsewhere
+    sym2 = sym.copy()
+    sym2[0] = g["sym_in_seg0"]
+    q2 = oracle.paa32(x, 16).astype(np.float64)
+    q2[0] = g["qpaa_seg0"]
+    got = oracle.mindist2(q2, sym2, 256)
+    # box edges are the fp32-rounded breakpoints (reading R5): 16 * fl32(z_0.75)^2 exactly
+    edge = float(np.float32(GOLD["quartile_beta"]["value"]))
+    assert math.isclose(got, 16.0 * edge * edge, rel_tol=1e-15)
+    assert math.isclose(got, g["value"], rel_tol=2e-7)  # the real-valued closed form
+    # worked example: zero query vs the worked iSAX word, m = 2: lower edges from a normal table
+    nd = NormalDist()
+    gw = GOLD["worked_isax"]
+    exp = 2 * (nd.inv_cdf(41 / 256) ** 2 + nd.inv_cdf(177 / 256) ** 2 + nd.inv_cdf(238 / 256) ** 2)
+    got = oracle.mindist2(np.zeros(4), np.array(gw["sym256"], np.uint8), 8)
+    assert math.isclose(got, exp, rel_tol=1e-6)
+    assert got <= oracle.ed2(gw["x"], np.zeros(8, np.float32))
+
+
+def test_property1_lower_bound():
+    """Property 1: mindist(PAA(q), iSAX(c)) <= ED^2(q, c), 10k pairs."""
+    X = zwalks(100, 256, 1)
+    Q = zwalks(100, 256, 2)
+    P, S = oracle.isax_rows(X)
+    for q in Q:
+        qp = oracle.paa64(q, 16)
+        d = oracle.ed2_rows(X, q)
+        for k in range(X.shape[0]):
+            assert oracle.mindist2(qp, S[k], 256) <= d[k]
+
+
+# ------------------------------------------------------------------------------- ED (O7)
+def test_ed_examples_and_library():
+    g = GOLD["ed_spec"]
+    assert oracle.ed2(g["a"], g["b"]) == g["ed2"]
+    X = zwalks(50, 256, 4)
+    assert oracle.ed2(X[0], X[0]) == 0.0
+    for a, b in zip(X[:-1], X[1:]):
+        ref = float(np.sum((a.astype(np.float64) - b.astype(np.float64)) ** 2))
+        assert math.isclose(oracle.ed2(a, b), ref, rel_tol=1e-13)
+        assert oracle.ed2(a, b) == oracle.ed2(b, a)
+
+
+# ---------------------------------------------------------------- envelope / LB_Keogh
+def test_envelope_examples_and_library():
+    g = GOLD["envelope_spec"]
+    U, L = oracle.envelope(g["q"], g["r"])
+    assert U.tolist() == g["U"] and L.tolist() == g["L"]
+    q = zwalks(1, 256, 9)[0]
+    U0, L0 = oracle.envelope(q, 0)
+    assert np.array_equal(U0, q) and np.array_equal(L0, q)
+    for r in (1, 5, 25, 255, 256):
+        U, L = oracle.envelope(q, r)
+        assert np.array_equal(U, ndi.maximum_filter1d(q, 2 * r + 1, mode="nearest"))
+        assert np.array_equal(L, ndi.minimum_filter1d(q, 2 * r + 1, mode="nearest"))
+        assert np.all(L <= q) and np.all(q <= U)
+    with pytest.raises(ValueError):
+        oracle.envelope(q, 257)
+
+
+def test_lb_keogh_hand_and_r0():
+    g = GOLD["lb_keogh_hand"]
+    U, L = oracle.envelope(g["q"], g["r"])
+    assert oracle.lb_keogh2(U, L, g["c"]) == g["lbk2"]
+    assert oracle.ed2(g["q"], g["c"]) == g["ed2"]
+    assert oracle.dtw2(g["q"], g["c"], g["r"]) == g["dtw2"]
+    X = zwalks(20, 256, 12)
+    for a, b in zip(X[:-1], X[1:]):
+        U, L = oracle.envelope(a, 0)
+        assert oracle.lb_keogh2(U, L, b) == oracle.ed2(a, b)  # r = 0: LB_Keogh == ED^2
+        U, L = oracle.envelope(a, 25)
+        assert oracle.lb_keogh2(U, L, a) == 0.0  # a series lies inside its own envelope
+
+
+# ------------------------------------------------------------------------------ DTW (O12)
+def brute_dtw(q, c, r):
+    """min over every warping path inside the band of the summed squared cost."""
+    n = len(q)
+    best = math.inf
+
+    def walk(i, j, acc):
+        nonlocal best
+        acc += (float(q[i]) - float(c[j])) ** 2
+        if acc >= best:
+            return
+        if i == n - 1 and j == n - 1:
+            best = acc
+            return
+        for di, dj in ((1, 1), (1, 0), (0, 1)):
+            a, b = i + di, j + dj
+            if a < n and b < n and abs(a - b) <= r:
+                walk(a, b, acc)
+
+    walk(0, 0, 0.0)
+    return best
+
+
+def test_dtw_hand_values():
+    g = GOLD["dtw_hand"]
+    assert oracle.dtw2(g["q"], g["c"], 0) == g["r0"]
+    assert oracle.dtw2(g["q"], g["c"], 1) == g["r1"]
+
+
+def test_dtw_brute_force_tiny():
+    rng = np.random.default_rng(21)
+    for trial in range(60):
+        n = int(rng.integers(1, 8))
+        q = rng.standard_normal(n).astype(np.float32)
+        c = rng.standard_normal(n).astype(np.float32)
+        for r in range(0, n + 1):
+            assert math.isclose(oracle.dtw2(q, c, r), brute_dtw(q, c, r), rel_tol=1e-12, abs_tol=1e-12)
+
+
+def test_dtw_invariants():
+    X = zwalks(30, 256, 13)
+    for a, b in zip(X[:-1], X[1:]):
+        e = oracle.ed2(a, b)
+        assert oracle.dtw2(a, b, 0) == e  # r = 0 is the diagonal: bit-identical to ED^2
+        prev = e
+        for r in (1, 2, 5, 12, 25, 51, 128, 255):
+            d = oracle.dtw2(a, b, r)
+            assert d <= prev  # monotone non-increasing in the reach
+            prev = d
+        assert oracle.dtw2(a, b, 255) == oracle.dtw2(a, b, 256)
+        assert math.isclose(oracle.dtw2(a, b, 25), oracle.dtw2(b, a, 25), rel_tol=1e-12)
+        assert oracle.dtw2(a, a, 25) == 0.0
+
+
+def test_lower_bound_chain_dtw():
+    """LB_envPAA <= LB_Keogh <= DTW <= ED^2 (Alg. 10), r = 25, 2,500 pairs."""
+    X = zwalks(50, 256, 14)
+    Q = zwalks(50, 256, 15)
+    _, S = oracle.isax_rows(X)
+    for q in Q:
+        U, L = oracle.envelope(q, 25)
+        Up, Lp = oracle.paa64(U, 16), oracle.paa64(L, 16)
+        for k in range(X.shape[0]):
+            lbp = oracle.lb_env_paa2(Up, Lp, S[k], 256)
+            lbk = oracle.lb_keogh2(U, L, X[k])
+            d = oracle.dtw2(q, X[k], 25)
+            assert lbp <= lbk <= d <= oracle.ed2(q, X[k])
+    # r = 0: the envelope PAA bound equals the ED mindist
+    q = Q[0]
+    U, L = oracle.envelope(q, 0)
+    Up, Lp = oracle.paa64(U, 16), oracle.paa64(L, 16)
+    qp = oracle.paa64(q, 16)
+    for k in range(X.shape[0]):
+        assert oracle.lb_env_paa2(Up, Lp, S[k], 256) == oracle.mindist2(qp, S[k], 256)
+
+
+# ------------------------------------------------------------------------- 1-NN (O8/O13)
+def test_nn_ed_vs_numpy_scan_and_threads():
+    X = zwalks(3000, 256, 31)
+    Q = zwalks(8, 256, 32)
+    d2, ids = oracle.nn("ed", X, Q, threads=1, chunk=1 << 20)
+    d2b, idsb = oracle.nn("ed", X, Q, threads=8, chunk=257)
+    assert np.array_equal(ids, idsb) and np.array_equal(d2, d2b)
+    D = ((X[None, :, :].astype(np.float64) - Q[:, None, :].astype(np.float64)) ** 2).sum(-1)
+    assert np.array_equal(ids, D.argmin(1))
+    assert np.allclose(d2, D.min(1), rtol=1e-13)
+
+
+def test_nn_ties_lowest_id_and_exact_match():
+    X = zwalks(500, 64, 33)
+    X[400] = X[17]
+    X[450] = X[17]
+    d2, ids = oracle.nn("ed", X, X[[17, 400, 3]], threads=4, chunk=64)
+    assert ids.tolist() == [17, 17, 3] and d2.tolist() == [0.0, 0.0, 0.0]
+    d2, ids = oracle.nn("dtw", X, X[[450]], r=6, threads=4, chunk=64)
+    assert ids.tolist() == [17] and d2.tolist() == [0.0]
+    d2, ids = oracle.nn("ed", X, X[[17]], row_begin=1000, threads=2, chunk=100)
+    assert ids.tolist() == [1017]
+
+
+def test_nn_dtw_vs_brute_paths_tiny():
+    rng = np.random.default_rng(41)
+    X = rng.standard_normal((40, 6)).astype(np.float32)
+    Q = rng.standard_normal((3, 6)).astype(np.float32)
+    for r in (0, 1, 2, 5):
+        d2, ids = oracle.nn("dtw", X, Q, r=r, threads=3, chunk=7)
+        for qi, q in enumerate(Q):
+            ref = [brute_dtw(q, x, r) for x in X]
+            assert ids[qi] == int(np.argmin(ref))
+            assert math.isclose(d2[qi], min(ref), rel_tol=1e-12, abs_tol=1e-12)
