@@ -1,0 +1,134 @@
+/*
+ * messi.h -- C-ABI of the B200-native MESSI exact 1-NN hot path (libmessi.so).
+ *
+ * Paper: Peng, Fatourou, Palpanas, "Fast Data Series Indexing for In-Memory Data",
+ * arXiv 2110.07519; "P:<line>" cites /root/reference/PAPER.md (section / algorithm).
+ *
+ * The operation (sec. 2.1): "given a query series S_q of length n, and a
+ * collection S of sequences of the same length, n, identify the series S_c in S that has
+ * the smallest distance to S_q", under Euclidean distance or DTW with a
+ * Sakoe-Chiba band of reach r (sec. 3.4).  The index is the iSAX
+ * summary of every series (PAA means -> 8-bit N(0,1)-region symbols) plus an
+ * approximate-search order (Alg. 5 line "approxSearch").  Answers are EXACT:
+ * the id is the lexicographic minimum of (squared distance in fp64, id) over all rows
+ * (ties -> lowest id), and dist = sqrt of that fp64 squared distance (R11-R13).
+ *
+ * Conventions for every call:
+ *   - returns messi_status; MESSI_OK == 0; never aborts; on failure a thread-local message
+ *     is available from messi_last_error().
+ *   - pointers named *_dev are CUDA device pointers on the index's device; *_host are host
+ *     pointers; "query" pointers may be either (detected with cudaPointerGetAttributes).
+ *   - work is enqueued on cfg.stream (a cudaStream_t, e.g. torch's current stream); the
+ *     non-batch calls synchronise that stream before returning.
+ *   - float data is row-major fp32 [count][length]; ids are 0-based, global ids are
+ *     cfg.row_begin + local row.
+ */
+#ifndef MESSI_H
+#define MESSI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MESSI_OK = 0,
+    MESSI_EINVAL = 1, /* null pointer, bad length/segments/card_bits, reach outside [0, n], count too large */
+    MESSI_EEMPTY = 2, /* count == 0 (empty dataset is an error) */
+    MESSI_ENOMEM = 3, /* device allocation failed */
+    MESSI_ECUDA = 4   /* any other CUDA error (message in messi_last_error()) */
+} messi_status;
+
+typedef struct messi_index messi_index; /* opaque; owned by the library until messi_free */
+
+typedef struct {
+    int32_t length;    /* n: points per series; n >= 16, n % segments == 0, n <= 8192 */
+    int32_t segments;  /* w: PAA segments; 16 only ("w is fixed to 16") */
+    int32_t card_bits; /* bits per iSAX symbol; 8 only (256 symbols) */
+    int32_t window;    /* approximate-search leaf size; 0 -> 2000 (P:2064-2065 leaf capacity) */
+    int32_t device;    /* CUDA ordinal that holds rows_dev and runs every kernel */
+    int32_t keep_paa;  /* 1: also keep the fp32 PAA [count][16] (tests); 0: symbols only */
+    int64_t row_begin; /* global id of local row 0 (row sharding over GPUs; 0 unsharded) */
+    void* stream;      /* cudaStream_t to enqueue on; NULL = legacy default stream */
+} messi_config;
+
+typedef struct {
+    double dist;      /* sqrt of d2 (fp64, correctly rounded) */
+    int64_t id;       /* global id of the nearest series; -1 only if no row has a finite distance */
+    double d2;        /* the exact fp64 squared distance (ED^2 or DTW^2): the cross-shard merge key */
+    int64_t reserved; /* 0 */
+} messi_result;
+
+typedef struct {
+    int64_t lb_computed;  /* rows whose iSAX lower bound was evaluated (= count: flat scan) */
+    int64_t candidates;   /* rows with LB <= BSF0 * (1 + eps) after the scan */
+    int64_t lbk_pass;     /* DTW: candidates whose raw LB_Keogh <= BSF * (1 + eps) */
+    int64_t refined;      /* real distances computed (fp32) in the refine step */
+    int64_t abandoned;    /* real distance computations abandoned early */
+    int64_t near_best;    /* fp32 near-ties re-ranked exactly in fp64 */
+    double seed_d2;       /* BSF0: squared distance found by the approximate search */
+    double bsf_d2;        /* final fp32 best-so-far (squared) before the exact re-rank */
+} messi_stats;
+
+/* Build the index over `count` rows of length cfg->length (device pointer, borrowed: the
+ * caller keeps it alive and unmodified until messi_free; no copy is made).  Runs the iSAX
+ * summarisation (Alg. 3, ConvertToiSAX P:710) and the approximate-search key
+ * sort on the device.  count must be < 2^31.  *out receives the new index. */
+messi_status messi_build(const float* rows_dev, int64_t count, const messi_config* cfg, messi_index** out);
+
+/* Exact 1-NN under ED (Alg. 5 ExactSearch P:933-961 with Alg. 9) of one query
+ * of length n (host or device pointer).  *local_best (host) receives this index's best;
+ * stats (host, nullable) the per-query counters.  Synchronous. */
+messi_status messi_query_ed(messi_index* idx, const float* query, messi_result* local_best, messi_stats* stats);
+
+/* Exact 1-NN under DTW with reach `reach` points, 0 <= reach <= n (Alg. 10). */
+messi_status messi_query_dtw(messi_index* idx, const float* query, int32_t reach, messi_result* local_best,
+                             messi_stats* stats);
+
+/* Batched, asynchronous forms: nq queries [nq][n] in device memory, answered one after the
+ * other (the paper's sequential query model) entirely on cfg.stream with no
+ * host synchronisation; results_dev[nq] and stats_dev[nq] (nullable) are device arrays.
+ * The caller synchronises the stream before reading them. */
+messi_status messi_query_ed_batch(messi_index* idx, const float* queries_dev, int32_t nq,
+                                  messi_result* results_dev, messi_stats* stats_dev);
+messi_status messi_query_dtw_batch(messi_index* idx, const float* queries_dev, int32_t nq, int32_t reach,
+                                   messi_result* results_dev, messi_stats* stats_dev);
+
+/* Release everything the library allocated for idx.  NULL-safe. */
+void messi_free(messi_index* idx);
+
+/* Thread-local text of the last failure ("" if none). */
+const char* messi_last_error(void);
+
+/* Kernel launches the library enqueued so far on this index (for bench accounting). */
+int64_t messi_launch_count(const messi_index* idx);
+
+/* ---- inspection entry points (tests / bench; same kernels as the query path) ---------- */
+
+/* The 255 fp32 N(0,1) breakpoints the device derived (O3 reading), into host memory. */
+messi_status messi_debug_breakpoints(int32_t device, float* beta32_host);
+
+/* iSAX symbols [count][16] (u8) and, if cfg.keep_paa, PAA [count][16] (fp32) of every row,
+ * de-tiled into caller device buffers (paa_dev may be NULL). */
+messi_status messi_debug_summaries(messi_index* idx, uint8_t* sym_dev, float* paa_dev);
+
+/* Sorted approximate-search keys and the row permutation (device pointers owned by idx). */
+messi_status messi_debug_order(messi_index* idx, const uint64_t** skey_dev, const uint32_t** perm_dev);
+
+/* Lower bound of every row against one query (device pointer): reach < 0 -> ED mindist
+ * (Property 1); reach >= 0 -> DTW envelope-PAA bound.  Squared,
+ * fp32 rounded down, written to lb_dev[count]. */
+messi_status messi_debug_lower_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
+
+/* For `k` local row ids: fp32 squared distance as computed by the refine kernels (no
+ * abandoning), the exact fp64 squared distance of the re-rank kernel, and (reach >= 0)
+ * the fp32 raw LB_Keogh of the filter kernel.  reach < 0 -> ED, else DTW with that reach.
+ * Any output pointer may be NULL. */
+messi_status messi_debug_distances(messi_index* idx, const float* query_dev, int32_t reach, const uint32_t* ids_dev,
+                                   int32_t k, float* d32_dev, double* d64_dev, float* lbk_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MESSI_H */

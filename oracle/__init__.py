@@ -59,6 +59,8 @@ def lib():
         L.oracle_symbol.restype = _c_int
         L.oracle_isax.argtypes = [_f32p, _c_int, _c_int, _f32p, _c_int, _f32p, _u8p]
         L.oracle_isax.restype = _c_int
+        L.oracle_isax_rows.argtypes = [_f32p, _c_i64, _c_int, _c_int, _f32p, _c_int, _f32p, _u8p]
+        L.oracle_isax_rows.restype = _c_int
         L.oracle_mindist2.argtypes = [_f64p, _u8p, _c_int, _c_int, _f32p, _c_int]
         L.oracle_mindist2.restype = _c_d
         L.oracle_ed2.argtypes = [_f32p, _f32p, _c_int]
@@ -135,12 +137,13 @@ def isax(x, w: int = 16, card: int = 256, beta32=None):
 
 
 def isax_rows(data, w: int = 16, card: int = 256):
+    """(paa32[rows, w], sym[rows, w]) of every row (O2 + O4)."""
     data = _f32(data)
     beta32 = breakpoints(card)[1]
     P = np.zeros((data.shape[0], w), np.float32)
     S = np.zeros((data.shape[0], w), np.uint8)
-    for k in range(data.shape[0]):
-        P[k], S[k] = isax(data[k], w, card, beta32)
+    if lib().oracle_isax_rows(data, data.shape[0], data.shape[1], w, _f32(beta32), card, P, S):
+        raise ValueError("need 0 < w <= n and n % w == 0")
     return P, S
 
 

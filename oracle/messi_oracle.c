@@ -307,3 +307,14 @@ void oracle_dtw2_rows(const float* data, int64_t rows, int n, const float* q, in
 {
     for (int64_t k = 0; k < rows; ++k) out[k] = oracle_dtw2(q, data + (size_t)k * (size_t)n, n, r);
 }
+
+/* O2 + O4 for `rows` consecutive series (a loop over oracle_isax; no new arithmetic). */
+int oracle_isax_rows(const float* data, int64_t rows, int n, int w, const float* beta32, int card, float* paa32,
+                     uint8_t* sym)
+{
+    for (int64_t k = 0; k < rows; ++k)
+        if (oracle_isax(data + (size_t)k * (size_t)n, n, w, beta32, card, paa32 + (size_t)k * (size_t)w,
+                        sym + (size_t)k * (size_t)w))
+            return -1;
+    return 0;
+}

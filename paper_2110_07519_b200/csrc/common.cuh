@@ -1,0 +1,85 @@
+// common.cuh -- shared device definitions of libmessi (the CUDA product path).
+// Independent of oracle/ (no shared code, tables or constants).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define MESSI_W 16                 // PAA segments ("w is fixed to 16")
+#define MESSI_CARD 256             // 8-bit iSAX symbols
+#define MESSI_TILE_ROWS 512        // series per symbol tile (32 blocks x 16 series)
+#define MESSI_TILE_BYTES 8192      // 16 tile rows x 512 B
+#define MESSI_MAX_N 8192
+
+namespace messi {
+
+// Relative slack on every prune / abandon / near-tie test:
+// thr = BSF * (1 + 2^-12), rounded up.  > 10x the fp32 error of any distance we compare.
+__device__ __forceinline__ float slack_up(float bsf) { return __fmul_ru(bsf, 1.000244140625f); }
+
+// Per-query device state.  bsf_bits holds a non-negative fp32 whose bit pattern orders
+// like the value, so atomicMin on the bits is a monotone BSF update (Observation 1,
+// BSF only decreases).  The resolve kernel re-arms it for the next query.
+struct QState {
+    unsigned bsf_bits;      // current best-so-far (fp32 bits), +inf when armed
+    unsigned seed_bits;     // BSF0 after the approximate search
+    unsigned cand_count;    // LB survivors appended by the scan
+    unsigned list2_count;   // DTW: LB_Keogh survivors
+    unsigned near_count;    // near-best entries (d32 <= thr at refine time)
+    unsigned refined;       // real distances started
+    unsigned abandoned;     // real distances abandoned early
+    unsigned work;          // work-stealing cursor (DTW refine)
+    unsigned long long qkey;  // query's approximate-search key
+    int window_start;       // first sorted position of the approximate-search window
+    int window_len;
+};
+
+struct NearEntry { unsigned id; float d32; };
+
+__device__ __forceinline__ void arm_state(QState* st)
+{
+    st->bsf_bits = 0x7f800000u;
+    st->seed_bits = 0x7f800000u;
+    st->cand_count = 0;
+    st->list2_count = 0;
+    st->near_count = 0;
+    st->refined = 0;
+    st->abandoned = 0;
+    st->work = 0;
+}
+
+__device__ __forceinline__ float warp_sum(float v)
+{
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ float warp_min(float v)
+{
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ float ld_bsf(const QState* st)
+{
+    return __uint_as_float(*(volatile const unsigned*)&st->bsf_bits);
+}
+
+__device__ __forceinline__ void bsf_update(QState* st, float d)
+{
+    if (d >= 0.0f) atomicMin(&st->bsf_bits, __float_as_uint(d));
+}
+
+// Symbol of a fp32 PAA value: #{k : beta32_k <= x} over the 255 ascending breakpoints
+// (reading R3/R4: ascending, ties go to the region above).  Branch-free binary search.
+__device__ __forceinline__ int symbol_of(float x, const float* beta)
+{
+    int pos = 0;
+#pragma unroll
+    for (int step = 128; step; step >>= 1)
+        if (pos + step <= 255 && beta[pos + step - 1] <= x) pos += step;
+    return pos;
+}
+
+}  // namespace messi

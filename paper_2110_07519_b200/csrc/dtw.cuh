@@ -1,0 +1,179 @@
+// dtw.cuh -- real-distance engines: fp32 ED (warp), fp32/fp64 banded DTW (warp
+// wavefront), fp32 banded DTW (one thread per candidate, band in registers), raw
+// LB_Keogh (warp), and the canonical fp64 ED used for the exact re-rank.
+#pragma once
+#include "common.cuh"
+
+namespace messi {
+
+// Squared ED in fp32, one warp: lane handles float4 chunks lane*4 + 128k, then a butterfly
+// sum (commutative pairs -> every lane holds the same total).  RealDist_SIMD.
+__device__ __forceinline__ float ed2_warp(const float* __restrict__ q_s, const float* __restrict__ c, int n, int lane)
+{
+    float acc = 0.0f;
+    for (int j = lane * 4; j < n; j += 128) {
+        float4 cv = __ldg(reinterpret_cast<const float4*>(c + j));
+        float4 qv = *reinterpret_cast<const float4*>(q_s + j);
+        float d;
+        d = qv.x - cv.x; acc = fmaf(d, d, acc);
+        d = qv.y - cv.y; acc = fmaf(d, d, acc);
+        d = qv.z - cv.z; acc = fmaf(d, d, acc);
+        d = qv.w - cv.w; acc = fmaf(d, d, acc);
+    }
+    return warp_sum(acc);
+}
+
+// Canonical fp64 squared ED: d = sum_i ((double)q_i - (double)c_i)^2, sequential in i,
+// explicit round-to-nearest ops (no FMA contraction).  The exact re-rank of near-ties.
+__device__ __forceinline__ double ed2_exact(const float* __restrict__ q, const float* __restrict__ c, int n)
+{
+    double sum = 0.0;
+    for (int i = 0; i < n; ++i) {
+        double d = __dsub_rn((double)q[i], (double)c[i]);
+        sum = __dadd_rn(sum, __dmul_rn(d, d));
+    }
+    return sum;
+}
+
+template <typename T> __device__ __forceinline__ T inf_of();
+template <> __device__ __forceinline__ float inf_of<float>() { return INFINITY; }
+template <> __device__ __forceinline__ double inf_of<double>() { return (double)INFINITY; }
+
+__device__ __forceinline__ float cell_cost_add(float q, float c, float m) { float d = q - c; return fmaf(d, d, m); }
+__device__ __forceinline__ double cell_cost_add(float q, float c, double m)
+{
+    double d = __dsub_rn((double)q, (double)c);
+    return __dadd_rn(__dmul_rn(d, d), m);
+}
+
+// Banded DTW (reach r: |i - j| <= r; D(0,0) = cost; D = cost + min(diag, up, left)),
+// P:323-324 / P:1379, one warp, anti-diagonal wavefront: anti-diagonal t = i + j holds the
+// cells i in [ilo, ihi]; lanes take them 32 at a time; three rotating buffers indexed by i
+// (buf: 3*n of T).  Cells just outside the band are written +inf so later reads see +inf.
+// With T = double and cell_cost_add's _rn ops every cell is fl(fl(d*d) + min(...)): the
+// same value in any evaluation order, i.e. bit-identical to a row-by-row DP.
+template <typename T>
+__device__ T dtw_warp(const float* __restrict__ q, const float* __restrict__ c, int n, int r, T* buf, int lane)
+{
+    T* Dm2 = buf;
+    T* Dm1 = buf + n;
+    T* D0 = buf + 2 * n;
+    const T INF = inf_of<T>();
+    for (int t = 0; t <= 2 * n - 2; ++t) {
+        const int ilo = max(max(0, t - (n - 1)), (t - r + 1) >> 1);
+        const int ihi = min(min(n - 1, t), (t + r) >> 1);
+        for (int i = ilo - 1 + lane; i <= ihi + 1; i += 32) {
+            if (i < 0 || i >= n) continue;
+            T val = INF;
+            if (i >= ilo && i <= ihi) {
+                const int j = t - i;
+                T mn;
+                if (t == 0) {
+                    mn = (T)0;
+                } else {
+                    T up = i > 0 ? Dm1[i - 1] : INF;
+                    T left = j > 0 ? Dm1[i] : INF;
+                    T diag = (i > 0 && j > 0) ? Dm2[i - 1] : INF;
+                    mn = diag < up ? diag : up;
+                    mn = left < mn ? left : mn;
+                }
+                val = cell_cost_add(q[i], c[j], mn);
+            }
+            D0[i] = val;
+        }
+        __syncwarp();
+        T* tmp = Dm2;
+        Dm2 = Dm1;
+        Dm1 = D0;
+        D0 = tmp;
+    }
+    T out = Dm1[n - 1];
+    __syncwarp();
+    return out;
+}
+
+// Raw LB_Keogh, squared, fp32, one warp: sum_i (c_i - U_i)^2 [c_i > U_i] +
+// (c_i - L_i)^2 [c_i < L_i].  Alg. 10 line LB_Keogh.
+__device__ __forceinline__ float lbk_warp(const float* __restrict__ U, const float* __restrict__ L,
+                                          const float* __restrict__ c, int n, int lane)
+{
+    float acc = 0.0f;
+    for (int j = lane * 4; j < n; j += 128) {
+        float4 cv = __ldg(reinterpret_cast<const float4*>(c + j));
+        float4 uv = *reinterpret_cast<const float4*>(U + j);
+        float4 lv = *reinterpret_cast<const float4*>(L + j);
+        float e[4] = {cv.x, cv.y, cv.z, cv.w}, u[4] = {uv.x, uv.y, uv.z, uv.w}, l[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            float d = e[k] > u[k] ? e[k] - u[k] : (e[k] < l[k] ? e[k] - l[k] : 0.0f);
+            acc = fmaf(d, d, acc);
+        }
+    }
+    return warp_sum(acc);
+}
+
+// Banded DTW in fp32, ONE THREAD per candidate, band of width W = 2R+1 held in registers.
+// Row i, band slot d <-> column j = i + d - R.  D[d] is updated in place left to right:
+// before the update D[d] = D(i-1, j-1), D[d+1] = D(i-1, j), `left` = D(i, j-1).  Columns
+// outside [0, n) read c = +inf, so their cells are +inf without branches.  Rows advance
+// four at a time over a sliding register window cw[e] = c[i - R + e], e < W + 3.
+// Early abandon (Alg. 10's "< BSF" test, exact for non-negative costs): after every 4 rows,
+// if min_d D > thr every warping path already exceeds thr.  Returns +inf when abandoned.
+template <int R>
+struct DtwThread {
+    static constexpr int W = 2 * R + 1;
+    static constexpr int CW = W + 3;
+    float D[W + 1];
+    float cw[CW];
+    int i;
+
+    __device__ __forceinline__ void start(const float* __restrict__ c, int n)
+    {
+#pragma unroll
+        for (int d = 0; d <= W; ++d) D[d] = INFINITY;
+        D[R] = 0.0f;  // virtual D(-1, -1) = 0 so that D(0, 0) = cost(0, 0)
+#pragma unroll
+        for (int e = 0; e < CW; ++e) {
+            int j = e - R;
+            cw[e] = (j >= 0 && j < n) ? __ldg(c + j) : INFINITY;
+        }
+        i = 0;
+    }
+
+    // Four rows i..i+3; returns the row-minimum of the last one.
+    __device__ __forceinline__ float step4(const float* __restrict__ c, int n, const float* __restrict__ q_s)
+    {
+        float nx[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            int j = i + 4 + R + u;
+            nx[u] = j < n ? __ldg(c + j) : INFINITY;
+        }
+        const float4 qv = *reinterpret_cast<const float4*>(q_s + i);
+        const float qq[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            float left = INFINITY;
+#pragma unroll
+            for (int d = 0; d < W; ++d) {
+                float mn = fminf(fminf(D[d], D[d + 1]), left);
+                float df = qq[u] - cw[d + u];
+                left = fmaf(df, df, mn);
+                D[d] = left;
+            }
+        }
+        float mn = D[0];
+#pragma unroll
+        for (int d = 1; d < W; ++d) mn = fminf(mn, D[d]);
+#pragma unroll
+        for (int e = 0; e < CW - 4; ++e) cw[e] = cw[e + 4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cw[CW - 4 + u] = nx[u];
+        i += 4;
+        return mn;
+    }
+
+    __device__ __forceinline__ float result() const { return D[R]; }
+};
+
+}  // namespace messi

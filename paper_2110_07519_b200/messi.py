@@ -1,0 +1,288 @@
+"""ctypes binding of libmessi.so (include/messi.h) -- argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of ``csrc/``; this module passes
+pointers, sizes and the caller's CUDA stream through the C-ABI and raises on a non-zero
+status.  There is no CPU fallback: importing it without the built library raises.
+
+Function names follow the C-ABI (``messi_build``, ``messi_query_ed``, ``messi_query_dtw``,
+``messi_free`` and the batch / inspection calls).  ``Index`` is a small convenience owner
+around them for torch tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmessi.so")
+
+MESSI_OK, MESSI_EINVAL, MESSI_EEMPTY, MESSI_ENOMEM, MESSI_ECUDA = range(5)
+_STATUS = {1: "EINVAL", 2: "EEMPTY", 3: "ENOMEM", 4: "ECUDA"}
+
+
+class MessiError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"MESSI_{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("length", ctypes.c_int32), ("segments", ctypes.c_int32), ("card_bits", ctypes.c_int32),
+                ("window", ctypes.c_int32), ("device", ctypes.c_int32), ("keep_paa", ctypes.c_int32),
+                ("row_begin", ctypes.c_int64), ("stream", ctypes.c_void_p)]
+
+
+class Result(ctypes.Structure):
+    _fields_ = [("dist", ctypes.c_double), ("id", ctypes.c_int64), ("d2", ctypes.c_double),
+                ("reserved", ctypes.c_int64)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("lb_computed", ctypes.c_int64), ("candidates", ctypes.c_int64), ("lbk_pass", ctypes.c_int64),
+                ("refined", ctypes.c_int64), ("abandoned", ctypes.c_int64), ("near_best", ctypes.c_int64),
+                ("seed_d2", ctypes.c_double), ("bsf_d2", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+STATS_FIELDS = [k for k, _ in Stats._fields_]
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                               "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        L.messi_build.argtypes = [vp, i64, ctypes.POINTER(Config), ctypes.POINTER(vp)]
+        L.messi_query_ed.argtypes = [vp, vp, ctypes.POINTER(Result), vp]
+        L.messi_query_dtw.argtypes = [vp, vp, i32, ctypes.POINTER(Result), vp]
+        L.messi_query_ed_batch.argtypes = [vp, vp, i32, vp, vp]
+        L.messi_query_dtw_batch.argtypes = [vp, vp, i32, i32, vp, vp]
+        L.messi_free.argtypes = [vp]
+        L.messi_free.restype = None
+        L.messi_last_error.restype = ctypes.c_char_p
+        L.messi_launch_count.argtypes = [vp]
+        L.messi_launch_count.restype = i64
+        L.messi_debug_breakpoints.argtypes = [i32, vp]
+        L.messi_debug_summaries.argtypes = [vp, vp, vp]
+        L.messi_debug_order.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]
+        L.messi_debug_lower_bounds.argtypes = [vp, vp, i32, vp]
+        L.messi_debug_distances.argtypes = [vp, vp, i32, vp, i32, vp, vp, vp]
+        for f in ("messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_batch",
+                  "messi_query_dtw_batch", "messi_debug_breakpoints", "messi_debug_summaries",
+                  "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances"):
+            getattr(L, f).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_batch", "messi_query_dtw_batch",
+            "messi_free", "messi_last_error", "messi_launch_count", "messi_debug_breakpoints",
+            "messi_debug_summaries", "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances"]
+
+
+def _check(status: int):
+    if status != MESSI_OK:
+        raise MessiError(status, lib().messi_last_error().decode(errors="replace"))
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_handle(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+# ------------------------------------------------------------------ C-ABI, same names
+def messi_build(rows_dev: torch.Tensor, *, window: int = 0, keep_paa: bool = False, row_begin: int = 0,
+                stream=None, segments: int = 16, card_bits: int = 8, length: int | None = None):
+    """Build over a [count, n] float32 CUDA tensor (borrowed: keep it alive); returns a handle."""
+    if not (rows_dev.is_cuda and rows_dev.dtype == torch.float32 and rows_dev.is_contiguous()):
+        raise MessiError(MESSI_EINVAL, "rows must be a contiguous float32 CUDA tensor")
+    count = rows_dev.shape[0] if rows_dev.dim() == 2 else 0
+    n = length if length is not None else (rows_dev.shape[1] if rows_dev.dim() == 2 else 0)
+    cfg = Config(length=n, segments=segments, card_bits=card_bits, window=window,
+                 device=rows_dev.device.index or 0, keep_paa=int(keep_paa), row_begin=row_begin,
+                 stream=_stream_handle(stream))
+    h = ctypes.c_void_p()
+    _check(lib().messi_build(_ptr(rows_dev) if rows_dev.numel() else None, count, ctypes.byref(cfg), ctypes.byref(h)))
+    return h
+
+
+def messi_query_ed(handle, query, with_stats: bool = False):
+    """query: host (numpy / CPU tensor) or CUDA tensor of n float32.  Returns (dist, id, d2[, stats])."""
+    q, keep = _query_ptr(query)
+    res, st = Result(), Stats()
+    _check(lib().messi_query_ed(handle, q, ctypes.byref(res), ctypes.byref(st) if with_stats else None))
+    return (res.dist, res.id, res.d2, st.as_dict()) if with_stats else (res.dist, res.id, res.d2)
+
+
+def messi_query_dtw(handle, query, reach: int, with_stats: bool = False):
+    q, keep = _query_ptr(query)
+    res, st = Result(), Stats()
+    _check(lib().messi_query_dtw(handle, q, int(reach), ctypes.byref(res), ctypes.byref(st) if with_stats else None))
+    return (res.dist, res.id, res.d2, st.as_dict()) if with_stats else (res.dist, res.id, res.d2)
+
+
+def messi_query_ed_batch(handle, queries_dev: torch.Tensor, results_dev: torch.Tensor, stats_dev=None):
+    """Asynchronous on the build stream.  results_dev: uint8 CUDA tensor of nq*32 bytes (see
+    ``result_buffer``); stats_dev: optional nq*64 bytes (``stats_buffer``)."""
+    _check(lib().messi_query_ed_batch(handle, _ptr(queries_dev), queries_dev.shape[0], _ptr(results_dev),
+                                      _ptr(stats_dev)))
+
+
+def messi_query_dtw_batch(handle, queries_dev: torch.Tensor, reach: int, results_dev: torch.Tensor, stats_dev=None):
+    _check(lib().messi_query_dtw_batch(handle, _ptr(queries_dev), queries_dev.shape[0], int(reach),
+                                       _ptr(results_dev), _ptr(stats_dev)))
+
+
+def messi_free(handle):
+    if handle:
+        lib().messi_free(handle)
+
+
+def messi_launch_count(handle) -> int:
+    return int(lib().messi_launch_count(handle))
+
+
+def messi_debug_breakpoints(device: int = 0):
+    import numpy as np
+    out = np.zeros(255, np.float32)
+    _check(lib().messi_debug_breakpoints(device, out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def messi_debug_summaries(handle, count: int, device, with_paa: bool = False):
+    sym = torch.empty((count, 16), dtype=torch.uint8, device=device)
+    paa = torch.empty((count, 16), dtype=torch.float32, device=device) if with_paa else None
+    _check(lib().messi_debug_summaries(handle, _ptr(sym), _ptr(paa)))
+    return sym, paa
+
+
+def messi_debug_order(handle, count: int, device):
+    """(sorted keys as int64 view, permutation) copied into torch tensors."""
+    k, p = ctypes.c_void_p(), ctypes.c_void_p()
+    _check(lib().messi_debug_order(handle, ctypes.byref(k), ctypes.byref(p)))
+    keys = torch.empty(count, dtype=torch.int64, device=device)
+    perm = torch.empty(count, dtype=torch.int32, device=device)
+    torch.cuda.synchronize(device)
+    keys.copy_(_wrap_dev(k.value, count * 8, device).view(torch.int64))
+    perm.copy_(_wrap_dev(p.value, count * 4, device).view(torch.int32))
+    return keys, perm
+
+
+def messi_debug_lower_bounds(handle, query_dev: torch.Tensor, reach: int, count: int):
+    lb = torch.empty(count, dtype=torch.float32, device=query_dev.device)
+    _check(lib().messi_debug_lower_bounds(handle, _ptr(query_dev), int(reach), _ptr(lb)))
+    return lb
+
+
+def messi_debug_distances(handle, query_dev: torch.Tensor, reach: int, ids_dev: torch.Tensor):
+    k = ids_dev.numel()
+    dev = query_dev.device
+    d32 = torch.empty(k, dtype=torch.float32, device=dev)
+    d64 = torch.empty(k, dtype=torch.float64, device=dev)
+    lbk = torch.empty(k, dtype=torch.float32, device=dev) if reach >= 0 else None
+    ids = ids_dev.to(torch.int32).contiguous()
+    _check(lib().messi_debug_distances(handle, _ptr(query_dev), int(reach), _ptr(ids), k, _ptr(d32), _ptr(d64),
+                                       _ptr(lbk)))
+    return d32, d64, lbk
+
+
+# ----------------------------------------------------------------------------- helpers
+def _query_ptr(query):
+    import numpy as np
+    if isinstance(query, torch.Tensor):
+        if query.is_cuda:
+            q = query.contiguous().to(torch.float32)
+            return ctypes.c_void_p(q.data_ptr()), q
+        query = query.numpy()
+    q = np.ascontiguousarray(query, dtype=np.float32)
+    return q.ctypes.data_as(ctypes.c_void_p), q
+
+
+def _wrap_dev(ptr: int, nbytes: int, device):
+    """A uint8 CUDA tensor viewing library-owned device memory (no copy, not owned)."""
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+                                    "strides": None}
+    return torch.as_tensor(_Arr(), device=device)
+
+
+RESULT_BYTES, STATS_BYTES = 32, 64
+
+
+def result_buffer(nq: int, device) -> torch.Tensor:
+    return torch.empty(nq * RESULT_BYTES, dtype=torch.uint8, device=device)
+
+
+def stats_buffer(nq: int, device) -> torch.Tensor:
+    return torch.empty(nq * 64, dtype=torch.uint8, device=device)
+
+
+def decode_results(buf: torch.Tensor):
+    """(dist float64[nq], id int64[nq], d2 float64[nq]) from a result buffer (copied to host)."""
+    raw = buf.view(-1, RESULT_BYTES).cpu()
+    return (raw[:, 0:8].contiguous().view(torch.float64).flatten(), raw[:, 8:16].contiguous().view(torch.int64).flatten(),
+            raw[:, 16:24].contiguous().view(torch.float64).flatten())
+
+
+def decode_stats(buf: torch.Tensor):
+    raw = buf.view(-1, 64).cpu()
+    ints = raw[:, :48].contiguous().view(torch.int64)
+    dbl = raw[:, 48:].contiguous().view(torch.float64)
+    return [dict(zip(STATS_FIELDS, list(map(int, i.tolist())) + list(map(float, d.tolist()))))
+            for i, d in zip(ints, dbl)]
+
+
+class Index:
+    """Owner of one messi index over a [count, n] float32 CUDA tensor (kept alive here)."""
+
+    def __init__(self, rows: torch.Tensor, *, window: int = 0, keep_paa: bool = False, row_begin: int = 0,
+                 stream=None):
+        self.rows = rows
+        self.count, self.n = rows.shape
+        self.device = rows.device
+        self.row_begin = row_begin
+        self.stream = stream if stream is not None else torch.cuda.current_stream(rows.device)
+        self.handle = messi_build(rows, window=window, keep_paa=keep_paa, row_begin=row_begin, stream=self.stream)
+
+    def query_ed(self, q, with_stats=False):
+        return messi_query_ed(self.handle, q, with_stats)
+
+    def query_dtw(self, q, reach, with_stats=False):
+        return messi_query_dtw(self.handle, q, reach, with_stats)
+
+    def query_batch(self, queries_dev: torch.Tensor, reach: int | None = None, results=None, stats=None):
+        """Enqueue nq queries (ED if reach is None) on the index stream; returns the buffers."""
+        nq = queries_dev.shape[0]
+        results = results if results is not None else result_buffer(nq, self.device)
+        if reach is None:
+            messi_query_ed_batch(self.handle, queries_dev, results, stats)
+        else:
+            messi_query_dtw_batch(self.handle, queries_dev, reach, results, stats)
+        return results, stats
+
+    def launches(self) -> int:
+        return messi_launch_count(self.handle)
+
+    def close(self):
+        if self.handle:
+            messi_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

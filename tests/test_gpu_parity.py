@@ -1,0 +1,332 @@
+"""Parity of the CUDA path (through the C-ABI) with the CPU oracle, element by element on
+the same seeded inputs (device-generated rows copied back to the host for the oracle).
+
+Bars:
+  * symbols, PAA, breakpoints: bit-exact (integer / byte work and a fixed fp64 op order);
+  * nearest-neighbour id: bit-exact, ties -> lowest id; d2 bit-exact (canonical fp64
+    re-rank); dist within 1e-12 relative (it is sqrt(d2) on both sides);
+  * fp32 per-row quantities (refine distances, LB_Keogh): 2^-16 relative of the oracle;
+  * lower bounds: GPU LB <= true distance always (Property 1), and within
+    the widened-box / round-down tolerance of the oracle's mindist (derived in the test).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+def messi():
+    from paper_2110_07519_b200 import messi as m
+    return m
+
+
+def gen_rows(N, n, seed=datagen.DATA_SEED, row_begin=0):
+    x = torch.empty((N, n), dtype=torch.float32, device=DEV)
+    if N:
+        datagen.walks_cuda(x, row_begin, seed=seed)
+    torch.cuda.synchronize()
+    return x
+
+
+@pytest.fixture(scope="module")
+def c1():
+    """Config 1: 100,000 x 256 random walks (seed 0), 10 queries (seed 1); 195.3 tiles."""
+    X = gen_rows(100_000, 256)
+    Q = gen_rows(10, 256, seed=datagen.QUERY_SEED)
+    idx = messi().Index(X, keep_paa=True)
+    yield X, Q, idx, X.cpu().numpy(), Q.cpu().numpy()
+    idx.close()
+
+
+# ------------------------------------------------------------------------ build (A1/A2)
+def test_breakpoints_bit_exact():
+    b = messi().messi_debug_breakpoints(0)
+    assert np.array_equal(b, oracle.breakpoints(256)[1])
+
+
+def test_summaries_bit_exact(c1):
+    X, Q, idx, Xh, Qh = c1
+    sym, paa = messi().messi_debug_summaries(idx.handle, X.shape[0], X.device, with_paa=True)
+    P, S = oracle.isax_rows(Xh)
+    assert np.array_equal(paa.cpu().numpy().view(np.uint32), P.view(np.uint32))
+    assert np.array_equal(sym.cpu().numpy(), S)
+
+
+def _interleave_key(S):
+    key = np.zeros(S.shape[0], np.uint64)
+    for bit in range(7, 3, -1):
+        plane = np.zeros(S.shape[0], np.uint64)
+        for s in range(16):
+            plane |= ((S[:, s].astype(np.uint64) >> np.uint64(bit)) & np.uint64(1)) << np.uint64(s)
+        key = (key << np.uint64(16)) | plane
+    return key
+
+
+def test_approximate_search_order_is_valid(c1):
+    """The approximate-search order (reading R14, parity unpinned for the seed itself):
+    keys sorted, perm a permutation, key(perm[i]) = bit-plane interleave of the symbols."""
+    X, Q, idx, Xh, Qh = c1
+    keys, perm = messi().messi_debug_order(idx.handle, X.shape[0], X.device)
+    k = keys.cpu().numpy().view(np.uint64)
+    p = perm.cpu().numpy().astype(np.int64)
+    assert np.all(k[1:] >= k[:-1])
+    assert np.array_equal(np.sort(p), np.arange(X.shape[0]))
+    _, S = oracle.isax_rows(Xh)
+    assert np.array_equal(k, _interleave_key(S)[p])
+
+
+# ------------------------------------------------------------------ lower bounds (A3/A5)
+def _lb_tol(d_seg, m):
+    # GPU boxes are widened by one fp32 ulp (<= 4.8e-7 for |beta| < 4) and summed rounding
+    # down: |GPU - oracle| <= m * sum_s (2 d_s u + u^2) + 2^-20 * LB
+    u = 4.8e-7
+    return m * (2 * d_seg.sum(1) * u + 16 * u * u)
+
+
+def test_lower_bounds_ed(c1):
+    X, Q, idx, Xh, Qh = c1
+    _, S = oracle.isax_rows(Xh)
+    b32 = oracle.breakpoints()[1]
+    lo = np.concatenate([[-np.inf], b32]).astype(np.float64)
+    hi = np.concatenate([b32, [np.inf]]).astype(np.float64)
+    for qi in range(3):
+        lb = messi().messi_debug_lower_bounds(idx.handle, Q[qi].contiguous(), -1, X.shape[0]).cpu().numpy()
+        qp = oracle.paa64(Qh[qi])
+        rows = np.random.default_rng(qi).choice(X.shape[0], 3000, replace=False)
+        ref = np.array([oracle.mindist2(qp, S[r], 256) for r in rows])
+        d_seg = np.maximum(0, np.maximum(lo[S[rows]] - qp, qp - hi[S[rows]]))
+        tol = _lb_tol(d_seg, 16) + 2.0 ** -20 * ref
+        assert np.all(np.abs(lb[rows] - ref) <= tol)
+        # Property 1: LB <= true ED^2, for every row of the collection
+        ed = oracle.ed2_rows(Xh, Qh[qi])
+        assert np.all(lb.astype(np.float64) <= ed)
+
+
+def test_lower_bounds_dtw(c1):
+    X, Q, idx, Xh, Qh = c1
+    _, S = oracle.isax_rows(Xh[:4000])
+    r = 25
+    for qi in range(2):
+        lb = messi().messi_debug_lower_bounds(idx.handle, Q[qi].contiguous(), r, X.shape[0]).cpu().numpy()
+        U, L = oracle.envelope(Qh[qi], r)
+        Up, Lp = oracle.paa64(U), oracle.paa64(L)
+        rows = np.arange(0, 4000, 7)
+        ref = np.array([oracle.lb_env_paa2(Up, Lp, S[k], 256) for k in rows])
+        assert np.all(lb[rows] <= ref * (1 + 1e-6) + 1e-9)
+        assert np.all(lb[rows] >= ref * (1 - 1e-4) - 1e-3)
+        for k in rows[:200]:  # the chain LB_envPAA <= LB_Keogh <= DTW holds on the GPU bound
+            assert lb[k] <= oracle.lb_keogh2(U, L, Xh[k]) <= oracle.dtw2(Qh[qi], Xh[k], r)
+
+
+# -------------------------------------------------------------- real distances (A7-A9)
+@pytest.mark.parametrize("reach", [-1, 0, 3, 12, 25, 40])
+def test_distances_elementwise(c1, reach):
+    X, Q, idx, Xh, Qh = c1
+    ids = np.random.default_rng(7 + reach).choice(X.shape[0], 300, replace=False).astype(np.int32)
+    d32, d64, lbk = messi().messi_debug_distances(idx.handle, Q[1].contiguous(), reach,
+                                                  torch.from_numpy(ids).to(DEV))
+    d32, d64 = d32.cpu().numpy().astype(np.float64), d64.cpu().numpy()
+    if reach < 0:
+        ref = np.array([oracle.ed2(Qh[1], Xh[i]) for i in ids])
+    else:
+        ref = np.array([oracle.dtw2(Qh[1], Xh[i], reach) for i in ids])
+        U, L = oracle.envelope(Qh[1], reach)
+        lref = np.array([oracle.lb_keogh2(U, L, Xh[i]) for i in ids])
+        assert np.allclose(lbk.cpu().numpy(), lref, rtol=2.0 ** -16, atol=1e-6)
+    assert np.array_equal(d64, ref)  # canonical fp64: bit-exact
+    assert np.allclose(d32, ref, rtol=2.0 ** -16, atol=1e-6)
+
+
+# --------------------------------------------------------------------- 1-NN end to end
+def check_nn(got, ref_d2, ref_id):
+    dist, gid, d2 = got[:3]
+    assert gid == ref_id, (gid, ref_id, d2, ref_d2)
+    assert d2 == ref_d2
+    assert math.isclose(dist, math.sqrt(ref_d2), rel_tol=1e-12, abs_tol=1e-300)
+
+
+def test_nn_ed_config1(c1):
+    X, Q, idx, Xh, Qh = c1
+    d2, ids = oracle.nn("ed", Xh, Qh)
+    for qi in range(Q.shape[0]):
+        got = idx.query_ed(Q[qi], with_stats=True)
+        check_nn(got, d2[qi], ids[qi])
+        st = got[3]
+        assert st["lb_computed"] == X.shape[0]
+        assert st["seed_d2"] >= st["bsf_d2"] >= 0  # BSF only decreases (Obs. 1)
+        assert st["near_best"] >= 1 and st["candidates"] >= st["refined"] >= 1
+
+
+def test_nn_ed_host_query_and_batch(c1):
+    X, Q, idx, Xh, Qh = c1
+    d2, ids = oracle.nn("ed", Xh, Qh)
+    m = messi()
+    res, stats = m.result_buffer(Q.shape[0], DEV), m.stats_buffer(Q.shape[0], DEV)
+    idx.query_batch(Q, None, res, stats)
+    torch.cuda.synchronize()
+    dist_b, id_b, d2_b = m.decode_results(res)
+    assert np.array_equal(id_b.numpy(), ids) and np.array_equal(d2_b.numpy(), d2)
+    for qi in range(3):  # host pointer path
+        check_nn(idx.query_ed(Qh[qi]), d2[qi], ids[qi])
+
+
+@pytest.mark.parametrize("reach", [25, 7])
+def test_nn_dtw(c1, reach):
+    X, Q, idx, Xh, Qh = c1
+    sub = 20_000
+    X2 = X[:sub].contiguous()
+    idx2 = messi().Index(X2)
+    try:
+        d2, ids = oracle.nn("dtw", Xh[:sub], Qh[:3], r=reach)
+        for qi in range(3):
+            got = idx2.query_dtw(Q[qi], reach, with_stats=True)
+            check_nn(got, d2[qi], ids[qi])
+            st = got[3]
+            assert st["candidates"] >= st["lbk_pass"] >= 1
+        res = messi().result_buffer(3, DEV)
+        idx2.query_batch(Q[:3].contiguous(), reach, res)
+        torch.cuda.synchronize()
+        _, id_b, d2_b = messi().decode_results(res)
+        assert np.array_equal(id_b.numpy(), ids) and np.array_equal(d2_b.numpy(), d2)
+    finally:
+        idx2.close()
+
+
+# ------------------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("N,n", [(1, 256), (7, 64), (513, 128), (2500, 16), (3000, 2048), (1025, 48)])
+def test_nn_sizes_and_ragged(N, n):
+    X = gen_rows(N, n, seed=5)
+    Q = gen_rows(3, n, seed=6)
+    Xh, Qh = X.cpu().numpy(), Q.cpu().numpy()
+    idx = messi().Index(X)
+    try:
+        d2, ids = oracle.nn("ed", Xh, Qh)
+        for qi in range(3):
+            check_nn(idx.query_ed(Q[qi]), d2[qi], ids[qi])
+        sub_rows = 400 if n <= 256 else 40
+        for r in sorted({0, 2, min(5, n), n}):
+            d2, ids = oracle.nn("dtw", Xh[:sub_rows], Qh[:1], r=r)
+            sub = messi().Index(X[:sub_rows].contiguous())
+            try:
+                check_nn(sub.query_dtw(Q[0], r), d2[0], ids[0])
+            finally:
+                sub.close()
+    finally:
+        idx.close()
+
+
+def test_duplicates_ties_lowest_id_and_zero_distance():
+    N, n = 5000, 128
+    X = gen_rows(N, n, seed=9)
+    X[3000] = X[41]
+    X[4999] = X[41]
+    X[1234] = X[17]
+    torch.cuda.synchronize()
+    idx = messi().Index(X, row_begin=1000)
+    try:
+        for src, want in ((41, 41), (3000, 41), (4999, 41), (1234, 17)):
+            dist, gid, d2 = idx.query_ed(X[src])
+            assert (gid, d2, dist) == (1000 + want, 0.0, 0.0)
+            dist, gid, d2 = idx.query_dtw(X[src], 12)
+            assert (gid, d2) == (1000 + want, 0.0)
+    finally:
+        idx.close()
+
+
+def test_all_rows_identical_and_constant_rows():
+    N, n = 3000, 64
+    base = gen_rows(1, n, seed=11)
+    X = base.repeat(N, 1).contiguous()
+    Q = gen_rows(2, n, seed=12)
+    idx = messi().Index(X)
+    try:
+        d2, _ = oracle.nn("ed", X[:1].cpu().numpy(), Q.cpu().numpy())
+        for qi in range(2):
+            dist, gid, got = idx.query_ed(Q[qi])
+            assert gid == 0 and got == d2[qi]
+        dist, gid, got = idx.query_dtw(Q[0], 5)
+        assert gid == 0
+    finally:
+        idx.close()
+    Z = torch.zeros((700, n), dtype=torch.float32, device=DEV)  # constant (z-norm -> 0) rows
+    Z[500] = gen_rows(1, n, seed=13)[0]
+    idx = messi().Index(Z)
+    try:
+        q = gen_rows(1, n, seed=14)[0]
+        d2, ids = oracle.nn("ed", Z.cpu().numpy(), q.cpu().numpy()[None])
+        check_nn(idx.query_ed(q), d2[0], ids[0])
+        dist, gid, got = idx.query_ed(torch.zeros(n, device=DEV))
+        assert gid == 0 and got == 0.0
+    finally:
+        idx.close()
+
+
+def test_near_tie_one_ulp():
+    """Two rows differing in one ulp at one point: the fp32 refine cannot separate them,
+    the exact fp64 re-rank must."""
+    N, n = 4000, 256
+    X = gen_rows(N, n, seed=15)
+    q = gen_rows(1, n, seed=16)[0]
+    d2, ids = oracle.nn("ed", X.cpu().numpy(), q.cpu().numpy()[None])
+    nn = int(ids[0])
+    twin = X[nn].clone()
+    j = 100
+    # move one point of the twin one ulp towards the query (strictly closer) and put the
+    # twin at a HIGHER id than the original
+    twin[j] = torch.from_numpy(np.nextafter(X[nn, j].cpu().numpy(), q[j].cpu().numpy()).reshape(())).to(DEV)
+    X[3999] = twin
+    torch.cuda.synchronize()
+    Xh = X.cpu().numpy()
+    d2, ids = oracle.nn("ed", Xh, q.cpu().numpy()[None])
+    idx = messi().Index(X)
+    try:
+        check_nn(idx.query_ed(q), d2[0], ids[0])
+    finally:
+        idx.close()
+
+
+def test_noisy_queries_config5_shape():
+    """Config 5's query workload at small scale: n = 128, sigma = 0.1."""
+    N, n = 60_000, 128
+    X = gen_rows(N, n)
+    Q = torch.empty((20, n), dtype=torch.float32, device=DEV)
+    datagen.noisy_queries_cuda(Q, N, sigma=0.1)
+    torch.cuda.synchronize()
+    d2, ids = oracle.nn("ed", X.cpu().numpy(), Q.cpu().numpy())
+    idx = messi().Index(X)
+    try:
+        src = datagen.noisy_rows(20, N)
+        hits = 0
+        for qi in range(20):
+            got = idx.query_ed(Q[qi])
+            check_nn(got, d2[qi], ids[qi])
+            hits += int(got[1] == src[qi])
+        assert hits >= 15  # sigma = 0.1 noise: the source row is (almost always) the NN
+    finally:
+        idx.close()
+
+
+def test_errors():
+    m = messi()
+    X = gen_rows(10, 64)
+    with pytest.raises(m.MessiError) as e:
+        m.messi_build(X[:0])
+    assert e.value.status == m.MESSI_EEMPTY
+    with pytest.raises(m.MessiError) as e:
+        m.messi_build(gen_rows(10, 40))
+    assert e.value.status == m.MESSI_EINVAL
+    idx = m.Index(X)
+    try:
+        with pytest.raises(m.MessiError) as e:
+            idx.query_dtw(X[0], 65)
+        assert e.value.status == m.MESSI_EINVAL
+    finally:
+        idx.close()
