@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 MESSI exact 1-NN hot path (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode ed|dtw]
+
+One STEP = a batch of Q queries (default 100, the paper's query-set size) answered
+one after the other (the paper's sequential model) by the whole hot path
+(A3-A10: prologue/approximate search, LB scan + compaction, refine, exact re-rank, and for
+N > 1 the cross-GPU merge) over the workload's collection, inputs resident in HBM.  The
+index build (A1 summarise + A2 key sort) runs once per collection and is reported in
+"build".  N = 1 workload: config 3 (100M x 256, ED) -- the collection the metric is quoted
+on -- fits one B200; for N > 1 the same collection is row-sharded (strong scaling).  DTW
+(config 4: 10M x 256, reach 25) is reported in "dtw" (or as the headline with --mode dtw).
+
+--impl reference times the CPU oracle (the reference arm for this tier) on a bounded row
+sample of the same workload, on the host's cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "exact 1-NN queries/sec (ED & DTW, 100M×256 fp32) at 1/2/4/8 B200; % HBM roofline"
+PAPER_QPS = 20.0  # ~50 ms per exact ED 1-NN query on 100M x 256, 2x Xeon E5-2650 v4
+
+CONFIGS = {
+    "c1": dict(N=100_000, n=256, Q=10, reach=None, name="C1 ED exact 1-NN tiny: 100,000 x 256 random walks"),
+    "c2": dict(N=10_000_000, n=256, Q=100, reach=None, name="C2 ED exact 1-NN: 10,000,000 x 256 random walks"),
+    "c3": dict(N=100_000_000, n=256, Q=100, reach=None,
+               name="C3 ED exact 1-NN: 100,000,000 x 256 z-normalised random walks (seed 0), 100 random-walk "
+                    "queries (seed 1), iSAX w=16 card 256, row-sharded over the GPUs"),
+    "c4": dict(N=10_000_000, n=256, Q=100, reach=25,
+               name="C4 DTW exact 1-NN: 10,000,000 x 256 random walks, Sakoe-Chiba reach 25 (10%), 100 queries"),
+    "c5": dict(N=100_000_000, n=128, Q=1000, reach=None, noisy=True,
+               name="C5 ED exact 1-NN tight pruning: 100,000,000 x 128, 1,000 noisy dataset queries (sigma 0.1)"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="ed", choices=["ed", "dtw"])
+    ap.add_argument("--config", default=None, help="c1..c5 (default: c3 for ed, c4 for dtw)")
+    ap.add_argument("--rows", type=int, default=None, help="override the collection size")
+    ap.add_argument("--queries", type=int, default=None, help="override queries per step")
+    ap.add_argument("--no-dtw", action="store_true", help="skip the secondary DTW measurement")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
+    ap.add_argument("--cpu-rows", type=int, default=2_000_000, help="row sample of the oracle timing")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------ dist plumbing
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi-equivalent NVML sampling of SM clock and throttle reasons while running."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# --------------------------------------------------------------------------- our arm
+def gen_collection(cfg, rank, world, dev):
+    import torch
+    import datagen
+    from paper_2110_07519_b200.dist import shard_range
+    b, e = shard_range(cfg["N"], world, rank)
+    X = torch.empty((e - b, cfg["n"]), dtype=torch.float32, device=dev)
+    datagen.walks_cuda(X, b, seed=datagen.DATA_SEED)
+    Q = torch.empty((cfg["Q"], cfg["n"]), dtype=torch.float32, device=dev)
+    if cfg.get("noisy"):
+        datagen.noisy_queries_cuda(Q, cfg["N"], sigma=0.1)
+    else:
+        datagen.walks_cuda(Q, 0, seed=datagen.QUERY_SEED)
+    torch.cuda.synchronize()
+    return X, Q, b
+
+
+def run_arm(cfg, args, world, rank, dev, stream, time_steps, warmup):
+    """Build + time `time_steps` steps of cfg's queries.  Returns a dict of measurements."""
+    import torch
+    from paper_2110_07519_b200 import messi as M
+    from paper_2110_07519_b200.dist import merge_results
+
+    X, Q, row_begin = gen_collection(cfg, rank, world, dev)
+    reach = cfg["reach"]
+    with torch.cuda.stream(stream):
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        idx = M.Index(X, row_begin=row_begin, stream=stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        build_ms = t0.elapsed_time(t1)
+        nq = Q.shape[0]
+        res = M.result_buffer(nq, dev)
+        stats = M.stats_buffer(nq, dev)
+
+        def step():
+            idx.query_batch(Q, reach, res, stats)
+            if world > 1:
+                dist_, gid, d2 = M.decode_results_device(res)
+                merge_results(d2, gid)
+
+        for _ in range(warmup):
+            step()
+        torch.cuda.synchronize()
+        barrier(world)
+        torch.cuda.synchronize()
+        launches0 = idx.launches()
+        M.messi_profile_enable(idx.handle, True)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        with ClockSampler(dev.index or 0) as clk:
+            ev0.record(stream)
+            for _ in range(time_steps):
+                step()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+        barrier(world)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        launches = idx.launches() - launches0
+        prof = {k: M.messi_profile_read(idx.handle, k) for k in ("seed", "scan", "refine", "lbk", "resolve")}
+        M.messi_profile_enable(idx.handle, False)
+        st = M.decode_stats(stats)
+
+        # e2e: the same steps through the public API with HOST buffers: pinned host queries
+        # -> H2D, the batch call, D2H of the results (and the merge for N > 1), every step.
+        qh = Q.cpu().pin_memory()
+        rh = torch.empty(res.numel(), dtype=torch.uint8).pin_memory()
+        qd = torch.empty_like(Q)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier(world)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(time_steps):
+            qd.copy_(qh, non_blocking=True)
+            idx.query_batch(qd, reach, res, None)
+            if world > 1:
+                dist_, gid, d2 = M.decode_results_device(res)
+                merge_results(d2, gid)
+            rh.copy_(res, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        e2e_ms = e0.elapsed_time(e1)
+    out = dict(ms=ms, build_ms=build_ms, launches=launches, prof=prof, stats=st, clocks=clk.summary(),
+               e2e_ms=e2e_ms, nq=nq, N_local=X.shape[0], n=cfg["n"], h2d=qh.numel() * 4, d2h=rh.numel())
+    idx.close()
+    del X, Q
+    torch.cuda.empty_cache()
+    return out
+
+
+def cpu_baseline(cfg, args, dev, kind):
+    """The oracle, as it stands, timed on this host's cores over a bounded row sample of the
+    workload (rows copied back from the device generator), scaled to the full collection."""
+    import numpy as np
+    import torch
+    import datagen
+    import oracle
+    rows = min(cfg["N"], args.cpu_rows if cfg["reach"] is None else max(20_000, args.cpu_rows // 200))
+    X = torch.empty((rows, cfg["n"]), dtype=torch.float32, device=dev)
+    datagen.walks_cuda(X, 0, seed=datagen.DATA_SEED)
+    Qd = torch.empty((2, cfg["n"]), dtype=torch.float32, device=dev)
+    datagen.walks_cuda(Qd, 0, seed=datagen.QUERY_SEED)
+    Xh, Qh = X.cpu().numpy(), Qd.cpu().numpy()
+    del X
+    cores = len(os.sched_getaffinity(0))
+    nq = 2 if cfg["reach"] is None else 1
+    t = time.perf_counter()
+    if cfg["reach"] is None:
+        oracle.nn("ed", Xh, Qh[:nq], threads=cores, chunk=max(1, rows // (4 * cores)))
+    else:
+        oracle.nn("dtw", Xh, Qh[:nq], r=cfg["reach"], threads=cores, chunk=max(1, rows // (4 * cores)))
+    dt = time.perf_counter() - t
+    qps = nq / (dt * cfg["N"] / rows)
+    return {"value": qps, "unit": "queries/s", "cores": cores, "kind": "oracle",
+            "sample": f"{nq} queries x first {rows:,} of {cfg['N']:,} rows in {dt:.2f} s, linearly scaled to the "
+                      f"full collection; plain fp64 brute force ({kind}), one serial call per row chunk on "
+                      f"{cores} threads", "seconds": dt}
+
+
+def ours(args):
+    import torch
+    world, rank, local = dist_init(args)
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(dev)
+    cname = args.config or ("c3" if args.mode == "ed" else "c4")
+    cfg = dict(CONFIGS[cname])
+    if args.rows:
+        cfg["N"] = args.rows
+    if args.queries:
+        cfg["Q"] = args.queries
+    if args.mode == "dtw" and cfg["reach"] is None:
+        cfg["reach"] = 25
+    pk = peaks()
+    main = run_arm(cfg, args, world, rank, dev, stream, args.steps, args.warmup)
+    ms = max_over_ranks(main["ms"], world)
+    e2e_ms = max_over_ranks(main["e2e_ms"], world)
+    scan_ms, scan_n = main["prof"]["scan"]
+    scan_ms = max_over_ranks(scan_ms, world)
+    K, nq = args.steps, main["nq"]
+    value = K * nq / (ms / 1e3)
+    # roofline of the dominant kernel: the LB scan, algorithmic bytes = 16 B of symbols per
+    # local series + 8 B per compacted candidate; achieved over its own time
+    st = main["stats"]
+    mean = lambda k: sum(s[k] for s in st) / len(st)  # noqa: E731
+    scan_bytes = 16 * main["N_local"] + 8 * mean("candidates")
+    achieved = scan_bytes * scan_n / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
+    peak = pk.get("hbm_gbs", 6650.0)
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic = tr.get(f"{cname}_{args.mode}_scan_bytes_per_launch")
+    except Exception:
+        pass
+    per_query_bytes = 16 * main["N_local"] + 4 * main["n"] * mean("refined") + 4 * main["n"] * min(2000, main["N_local"])
+    steps_total = {k: max_over_ranks(v[0], world) for k, v in main["prof"].items()}
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": value / PAPER_QPS if args.mode == "ed" and cname == "c3" else None,
+        "dtype": "f32", "data": "synthetic (seeded device Philox random walks, z-normalised)",
+        "config": {"workload": cfg["name"], "mode": args.mode, "rows": cfg["N"], "length": cfg["n"],
+                   "queries_per_step": nq, "reach": cfg["reach"], "parallelism": f"row-shard x{world}",
+                   "l2": "inputs larger than L2: every query streams %.2f GB of symbols per GPU" % (16 * main["N_local"] / 1e9),
+                   "query_model": "sequential queries (P:2024-2026), batch call per step"},
+        "roofline": {"bound": "hbm", "kernel": "k_scan (LB scan + compaction)", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in pk else "fallback",
+                     "algorithmic_bytes_per_launch": scan_bytes, "launches": scan_n,
+                     "share_of_step": scan_ms / ms if ms else None},
+        "query_roofline": {"bytes_per_query_per_gpu": per_query_bytes,
+                           "qps_at_peak": peak * 1e9 / per_query_bytes,
+                           "frac": value / (peak * 1e9 / per_query_bytes)},
+        "kernel_ms_per_step": {k: v / K for k, v in steps_total.items()},
+        "e2e": {"value": K * nq / (e2e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": main["h2d"],
+                "d2h_bytes_per_step": main["d2h"]},
+        "gpu_launches": main["launches"],
+        "clocks": main["clocks"],
+        "build": {"ms": main["build_ms"], "rows_per_s": main["N_local"] / (main["build_ms"] / 1e3),
+                  "what": "summarise (PAA + iSAX + key) + CUB key sort, per GPU"},
+        "stats_mean": {k: mean(k) for k in ("candidates", "lbk_pass", "refined", "abandoned", "near_best",
+                                             "seed_d2", "bsf_d2")},
+    }
+    if args.mode == "ed" and not args.no_dtw:
+        c4 = dict(CONFIGS["c4"])
+        k4 = max(1, min(2, K))
+        d = run_arm(c4, args, world, rank, dev, stream, k4, 1)
+        dms = max_over_ranks(d["ms"], world)
+        dst = d["stats"]
+        dm = lambda k: sum(s[k] for s in dst) / len(dst)  # noqa: E731
+        line["dtw"] = {"value": k4 * d["nq"] / (dms / 1e3), "unit": "queries/s", "workload": c4["name"],
+                       "steps": k4, "ms_per_step": dms / k4,
+                       "kernel_ms_per_step": {k: v[0] / k4 for k, v in d["prof"].items()},
+                       "stats_mean": {k: dm(k) for k in ("candidates", "lbk_pass", "refined", "abandoned",
+                                                         "near_best", "seed_d2", "bsf_d2")},
+                       "gpu_launches": d["launches"]}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, args, dev, "ED" if cfg["reach"] is None else "DTW")
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def reference(args):
+    """The reference arm for this tier: the CPU oracle on the host cores, rank 0 only."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import datagen
+    import oracle
+    cname = args.config or ("c3" if args.mode == "ed" else "c4")
+    cfg = dict(CONFIGS[cname])
+    if args.rows:
+        cfg["N"] = args.rows
+    if args.mode == "dtw" and cfg["reach"] is None:
+        cfg["reach"] = 25
+    rows = min(cfg["N"], 1_000_000 if cfg["reach"] is None else 10_000)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            X = torch.empty((rows, cfg["n"]), dtype=torch.float32, device="cuda")
+            datagen.walks_cuda(X, 0)
+            Xh = X.cpu().numpy()
+            del X
+        else:
+            Xh = datagen.walks_cpu(0, rows, cfg["n"])
+    except Exception:
+        Xh = datagen.walks_cpu(0, rows, cfg["n"])
+    Qh = datagen.walks_cpu(0, args.warmup + args.steps, cfg["n"], seed=datagen.QUERY_SEED)
+    cores = len(os.sched_getaffinity(0))
+    kind = "ed" if cfg["reach"] is None else "dtw"
+
+    def step(i):
+        oracle.nn(kind, Xh, Qh[i:i + 1], r=cfg["reach"] or 0, threads=cores, chunk=max(1, rows // (4 * cores)))
+
+    for i in range(args.warmup):
+        step(i)
+    t = time.perf_counter()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    dt = time.perf_counter() - t
+    scale = cfg["N"] / rows
+    value = args.steps / (dt * scale)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * scale * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded random walks, z-normalised)",
+            "config": {"workload": cfg["name"], "mode": args.mode, "rows": cfg["N"], "length": cfg["n"]},
+            "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "oracle",
+                             "sample": f"each step: 1 query over the first {rows:,} of {cfg['N']:,} rows, "
+                                       f"time scaled x{scale:g} to the full collection"},
+            "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference(args)
+    else:
+        ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -104,6 +104,14 @@ const char* messi_last_error(void);
 /* Kernel launches the library enqueued so far on this index (for bench accounting). */
 int64_t messi_launch_count(const messi_index* idx);
 
+/* Per-kernel device timing (bench accounting): when enabled, the library brackets every
+ * launch of the query path with CUDA events on the index stream.  kind: 0 seed (prologue +
+ * approximate search), 1 lower-bound scan, 2 refine (ED or DTW), 3 DTW LB_Keogh filter,
+ * 4 exact resolve.  messi_profile_enable resets the accumulators; messi_profile_read
+ * synchronises the stream and returns the summed milliseconds and the launch count. */
+messi_status messi_profile_enable(messi_index* idx, int32_t enable);
+messi_status messi_profile_read(messi_index* idx, int32_t kind, double* total_ms, int64_t* launches);
+
 /* ---- inspection entry points (tests / bench; same kernels as the query path) ---------- */
 
 /* The 255 fp32 N(0,1) breakpoints the device derived (O3 reading), into host memory. */

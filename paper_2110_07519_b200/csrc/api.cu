@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "../../include/messi.h"
 #include "common.cuh"
@@ -39,6 +40,47 @@ struct messi_index {
     messi_result* res1 = nullptr;
     messi_stats* stats1 = nullptr;
     long long launches = 0;
+    // optional per-kernel event timing
+    bool prof = false;
+    struct Ev { int kind; cudaEvent_t a, b; };
+    std::vector<Ev> evs;
+    std::vector<cudaEvent_t> pool;
+};
+
+enum { K_SEED = 0, K_SCAN = 1, K_REFINE = 2, K_LBK = 3, K_RESOLVE = 4, K_KINDS = 5 };
+
+static cudaEvent_t pool_get(messi_index* idx)
+{
+    if (!idx->pool.empty()) {
+        cudaEvent_t e = idx->pool.back();
+        idx->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Brackets one launch with events when profiling is on.
+struct ProfScope {
+    messi_index* idx;
+    int kind;
+    cudaEvent_t a = nullptr;
+    ProfScope(messi_index* i, int k) : idx(i), kind(k)
+    {
+        if (idx->prof) {
+            a = pool_get(idx);
+            cudaEventRecord(a, idx->stream);
+        }
+    }
+    ~ProfScope()
+    {
+        if (idx->prof && a) {
+            cudaEvent_t b = pool_get(idx);
+            cudaEventRecord(b, idx->stream);
+            idx->evs.push_back({kind, a, b});
+        }
+    }
 };
 
 static_assert(sizeof(messi_result) == 32, "messi_result layout");
@@ -218,12 +260,50 @@ extern "C" void messi_free(messi_index* idx)
                     idx->st,    idx->res1,  idx->stats1};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (auto& e : idx->evs) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    for (auto e : idx->pool) cudaEventDestroy(e);
     delete idx;
 }
 
 extern "C" const char* messi_last_error(void) { return g_err; }
 
 extern "C" int64_t messi_launch_count(const messi_index* idx) { return idx ? idx->launches : 0; }
+
+extern "C" messi_status messi_profile_enable(messi_index* idx, int32_t enable)
+{
+    if (!idx) return fail(MESSI_EINVAL, "NULL index");
+    CK(cudaSetDevice(idx->device));
+    CK(cudaStreamSynchronize(idx->stream));
+    for (auto& e : idx->evs) {
+        idx->pool.push_back(e.a);
+        idx->pool.push_back(e.b);
+    }
+    idx->evs.clear();
+    idx->prof = enable != 0;
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_profile_read(messi_index* idx, int32_t kind, double* total_ms, int64_t* launches)
+{
+    if (!idx || !total_ms || !launches || kind < 0 || kind >= K_KINDS) return fail(MESSI_EINVAL, "bad argument");
+    CK(cudaSetDevice(idx->device));
+    CK(cudaStreamSynchronize(idx->stream));
+    double ms = 0.0;
+    long long cnt = 0;
+    for (auto& e : idx->evs) {
+        if (e.kind != kind) continue;
+        float t = 0.0f;
+        CK(cudaEventElapsedTime(&t, e.a, e.b));
+        ms += t;
+        ++cnt;
+    }
+    *total_ms = ms;
+    *launches = cnt;
+    return MESSI_OK;
+}
 
 // ---------------------------------------------------------------------------- queries
 static int scan_grid(const messi_index* idx)
@@ -242,16 +322,28 @@ static messi_status run_ed(messi_index* idx, const float* q_dev, messi_result* r
     int len = (int)(idx->window < idx->N ? idx->window : idx->N);
     int seed_grid = (len + 7) / 8;
     if (seed_grid > 256) seed_grid = 256;
-    k_seed_ed<<<seed_grid, 256, qsm, st>>>(q_dev, n, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32,
-                                           idx->lo_w, idx->hi_w, idx->lut, idx->st);
-    LAUNCHED(idx);
-    k_scan<false><<<scan_grid(idx), 256, scan_smem(), st>>>(idx->tiles, idx->ntiles, idx->N, idx->lut, idx->st, idx->cand,
-                                                            nullptr);
-    LAUNCHED(idx);
-    k_refine_ed<<<idx->sms * 4, 256, qsm, st>>>(idx->rows, n, q_dev, idx->cand, idx->st, idx->near);
-    LAUNCHED(idx);
-    k_resolve_ed<<<1, 256, 0, st>>>(idx->rows, n, q_dev, idx->near, idx->st, idx->N, idx->row_begin, res, stats);
-    LAUNCHED(idx);
+    {
+        ProfScope ps(idx, K_SEED);
+        k_seed_ed<<<seed_grid, 256, qsm, st>>>(q_dev, n, idx->rows, idx->skey, idx->perm, idx->N, idx->window,
+                                               idx->beta32, idx->lo_w, idx->hi_w, idx->lut, idx->st);
+        LAUNCHED(idx);
+    }
+    {
+        ProfScope ps(idx, K_SCAN);
+        k_scan<false><<<scan_grid(idx), 256, scan_smem(), st>>>(idx->tiles, idx->ntiles, idx->N, idx->lut, idx->st,
+                                                                idx->cand, nullptr);
+        LAUNCHED(idx);
+    }
+    {
+        ProfScope ps(idx, K_REFINE);
+        k_refine_ed<<<idx->sms * 4, 256, qsm, st>>>(idx->rows, n, q_dev, idx->cand, idx->st, idx->near);
+        LAUNCHED(idx);
+    }
+    {
+        ProfScope ps(idx, K_RESOLVE);
+        k_resolve_ed<<<1, 256, 0, st>>>(idx->rows, n, q_dev, idx->near, idx->st, idx->N, idx->row_begin, res, stats);
+        LAUNCHED(idx);
+    }
     return MESSI_OK;
 }
 
@@ -265,20 +357,30 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     const int wf = wavefront_warps(n, sizeof(float), 8);
     int seed_grid = (len + wf - 1) / wf;
     if (seed_grid > idx->sms * 4) seed_grid = idx->sms * 4;
-    k_seed_dtw<<<seed_grid, 32 * wf, qsm + (size_t)wf * 3 * n * sizeof(float), st>>>(
-        q_dev, n, reach, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32, idx->lo_w, idx->hi_w, idx->lut,
-        idx->U, idx->L, idx->st);
-    LAUNCHED(idx);
-    k_scan<false><<<scan_grid(idx), 256, scan_smem(), st>>>(idx->tiles, idx->ntiles, idx->N, idx->lut, idx->st, idx->cand,
-                                                            nullptr);
-    LAUNCHED(idx);
-    k_lbk_filter<<<idx->sms * 4, 256, 2 * qsm, st>>>(idx->rows, n, idx->U, idx->L, idx->cand, idx->st, idx->list2);
-    LAUNCHED(idx);
+    {
+        ProfScope ps(idx, K_SEED);
+        k_seed_dtw<<<seed_grid, 32 * wf, qsm + (size_t)wf * 3 * n * sizeof(float), st>>>(
+            q_dev, n, reach, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32, idx->lo_w, idx->hi_w,
+            idx->lut, idx->U, idx->L, idx->st);
+        LAUNCHED(idx);
+    }
+    {
+        ProfScope ps(idx, K_SCAN);
+        k_scan<false><<<scan_grid(idx), 256, scan_smem(), st>>>(idx->tiles, idx->ntiles, idx->N, idx->lut, idx->st,
+                                                                idx->cand, nullptr);
+        LAUNCHED(idx);
+    }
+    {
+        ProfScope ps(idx, K_LBK);
+        k_lbk_filter<<<idx->sms * 4, 256, 2 * qsm, st>>>(idx->rows, n, idx->U, idx->L, idx->cand, idx->st, idx->list2);
+        LAUNCHED(idx);
+    }
+    ProfScope* ref_scope = new ProfScope(idx, K_REFINE);
     bool launched = false;
 #define LAUNCH_R(R)                                                                                           \
     if (!launched && reach == R) {                                                                            \
         k_refine_dtw<R><<<idx->sms * 8, 128, qsm, st>>>(idx->rows, n, q_dev, idx->list2, idx->st, idx->near); \
-        LAUNCHED(idx);                                                                                        \
+        ++idx->launches;                                                                                      \
         launched = true;                                                                                      \
     }
     MESSI_DTW_REACHES(LAUNCH_R)
@@ -286,12 +388,17 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     if (!launched) {
         k_refine_dtw_warp<<<idx->sms * 4, 32 * wf, qsm + (size_t)wf * 3 * n * sizeof(float), st>>>(
             idx->rows, n, reach, q_dev, idx->list2, idx->st, idx->near);
+        ++idx->launches;
+    }
+    delete ref_scope;
+    CK(cudaGetLastError());
+    const int wr = wavefront_warps(n, sizeof(double), 8);
+    {
+        ProfScope ps(idx, K_RESOLVE);
+        k_resolve_dtw<<<1, 32 * wr, (size_t)wr * 3 * n * sizeof(double), st>>>(idx->rows, n, reach, q_dev, idx->near,
+                                                                              idx->st, idx->N, idx->row_begin, res, stats);
         LAUNCHED(idx);
     }
-    const int wr = wavefront_warps(n, sizeof(double), 8);
-    k_resolve_dtw<<<1, 32 * wr, (size_t)wr * 3 * n * sizeof(double), st>>>(idx->rows, n, reach, q_dev, idx->near, idx->st,
-                                                                          idx->N, idx->row_begin, res, stats);
-    LAUNCHED(idx);
     return MESSI_OK;
 }
 

@@ -71,13 +71,15 @@ def lib():
         L.messi_last_error.restype = ctypes.c_char_p
         L.messi_launch_count.argtypes = [vp]
         L.messi_launch_count.restype = i64
+        L.messi_profile_enable.argtypes = [vp, i32]
+        L.messi_profile_read.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
         L.messi_debug_breakpoints.argtypes = [i32, vp]
         L.messi_debug_summaries.argtypes = [vp, vp, vp]
         L.messi_debug_order.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]
         L.messi_debug_lower_bounds.argtypes = [vp, vp, i32, vp]
         L.messi_debug_distances.argtypes = [vp, vp, i32, vp, i32, vp, vp, vp]
         for f in ("messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_batch",
-                  "messi_query_dtw_batch", "messi_debug_breakpoints", "messi_debug_summaries",
+                  "messi_query_dtw_batch", "messi_profile_enable", "messi_profile_read", "messi_debug_breakpoints", "messi_debug_summaries",
                   "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
@@ -85,7 +87,8 @@ def lib():
 
 
 EXPORTED = ["messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_batch", "messi_query_dtw_batch",
-            "messi_free", "messi_last_error", "messi_launch_count", "messi_debug_breakpoints",
+            "messi_free", "messi_last_error", "messi_launch_count", "messi_profile_enable", "messi_profile_read",
+            "messi_debug_breakpoints",
             "messi_debug_summaries", "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances"]
 
 
@@ -153,6 +156,21 @@ def messi_free(handle):
 
 def messi_launch_count(handle) -> int:
     return int(lib().messi_launch_count(handle))
+
+
+KERNEL_KINDS = {"seed": 0, "scan": 1, "refine": 2, "lbk": 3, "resolve": 4}
+
+
+def messi_profile_enable(handle, enable: bool = True):
+    _check(lib().messi_profile_enable(handle, int(enable)))
+
+
+def messi_profile_read(handle, kind):
+    """(total milliseconds, launches) of one kernel kind since messi_profile_enable."""
+    ms, cnt = ctypes.c_double(), ctypes.c_int64()
+    k = KERNEL_KINDS[kind] if isinstance(kind, str) else int(kind)
+    _check(lib().messi_profile_read(handle, k, ctypes.byref(ms), ctypes.byref(cnt)))
+    return ms.value, cnt.value
 
 
 def messi_debug_breakpoints(device: int = 0):
@@ -233,6 +251,13 @@ def stats_buffer(nq: int, device) -> torch.Tensor:
 def decode_results(buf: torch.Tensor):
     """(dist float64[nq], id int64[nq], d2 float64[nq]) from a result buffer (copied to host)."""
     raw = buf.view(-1, RESULT_BYTES).cpu()
+    return (raw[:, 0:8].contiguous().view(torch.float64).flatten(), raw[:, 8:16].contiguous().view(torch.int64).flatten(),
+            raw[:, 16:24].contiguous().view(torch.float64).flatten())
+
+
+def decode_results_device(buf: torch.Tensor):
+    """(dist, id, d2) views of a result buffer, kept on the device (for the NCCL merge)."""
+    raw = buf.view(-1, RESULT_BYTES)
     return (raw[:, 0:8].contiguous().view(torch.float64).flatten(), raw[:, 8:16].contiguous().view(torch.int64).flatten(),
             raw[:, 16:24].contiguous().view(torch.float64).flatten())
 

@@ -281,7 +281,7 @@ def test_near_tie_one_ulp():
     j = 100
     # move one point of the twin one ulp towards the query (strictly closer) and put the
     # twin at a HIGHER id than the original
-    twin[j] = torch.from_numpy(np.nextafter(X[nn, j].cpu().numpy(), q[j].cpu().numpy()).reshape(())).to(DEV)
+    twin[j] = float(np.nextafter(np.float32(X[nn, j].item()), np.float32(q[j].item())))
     X[3999] = twin
     torch.cuda.synchronize()
     Xh = X.cpu().numpy()
