@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--queries", type=int, default=None, help="override queries per step")
     ap.add_argument("--no-dtw", action="store_true", help="skip the secondary DTW measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
-    ap.add_argument("--cpu-rows", type=int, default=2_000_000, help="row sample of the oracle timing")
+    ap.add_argument("--cpu-rows", type=int, default=4_000_000, help="row sample of the oracle timing")
+    ap.add_argument("--cpu-queries", type=int, default=32, help="queries of the oracle timing sample")
     return ap.parse_args()
 
 
@@ -251,12 +252,12 @@ def cpu_baseline(cfg, args, dev, kind):
     rows = min(cfg["N"], args.cpu_rows if cfg["reach"] is None else max(20_000, args.cpu_rows // 200))
     X = torch.empty((rows, cfg["n"]), dtype=torch.float32, device=dev)
     datagen.walks_cuda(X, 0, seed=datagen.DATA_SEED)
-    Qd = torch.empty((2, cfg["n"]), dtype=torch.float32, device=dev)
+    nq = args.cpu_queries if cfg["reach"] is None else 1
+    Qd = torch.empty((nq, cfg["n"]), dtype=torch.float32, device=dev)
     datagen.walks_cuda(Qd, 0, seed=datagen.QUERY_SEED)
     Xh, Qh = X.cpu().numpy(), Qd.cpu().numpy()
     del X
     cores = len(os.sched_getaffinity(0))
-    nq = 2 if cfg["reach"] is None else 1
     t = time.perf_counter()
     if cfg["reach"] is None:
         oracle.nn("ed", Xh, Qh[:nq], threads=cores, chunk=max(1, rows // (4 * cores)))
@@ -292,11 +293,12 @@ def ours(args):
     scan_ms = max_over_ranks(scan_ms, world)
     K, nq = args.steps, main["nq"]
     value = K * nq / (ms / 1e3)
-    # roofline of the dominant kernel: the LB scan, algorithmic bytes = 16 B of symbols per
-    # local series + 8 B per compacted candidate; achieved over its own time
+    # roofline of the dominant kernel: the coarse LB scan, algorithmic bytes = 8 B of coarse
+    # summary (16 top nibbles) per local series + 8 B per compacted coarse survivor
+    # (DESIGN.md "Roofline"); achieved = those bytes over the kernel's own event time
     st = main["stats"]
     mean = lambda k: sum(s[k] for s in st) / len(st)  # noqa: E731
-    scan_bytes = 16 * main["N_local"] + 8 * mean("candidates")
+    scan_bytes = 8 * main["N_local"] + 8 * mean("coarse_pass")
     achieved = scan_bytes * scan_n / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
     peak = pk.get("hbm_gbs", 6650.0)
     traffic = None
@@ -305,7 +307,10 @@ def ours(args):
         traffic = tr.get(f"{cname}_{args.mode}_scan_bytes_per_launch")
     except Exception:
         pass
-    per_query_bytes = 16 * main["N_local"] + 4 * main["n"] * mean("refined") + 4 * main["n"] * min(2000, main["N_local"])
+    # whole-query algorithmic bytes per GPU: coarse stream + one 32 B sector of 8-bit word per
+    # coarse survivor + the rows refined + the approximate-search window rows
+    per_query_bytes = (8 * main["N_local"] + 32 * mean("coarse_pass") + 4 * main["n"] * mean("refined")
+                       + 4 * main["n"] * min(2000, main["N_local"]))
     steps_total = {k: max_over_ranks(v[0], world) for k, v in main["prof"].items()}
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
@@ -314,9 +319,9 @@ def ours(args):
         "dtype": "f32", "data": "synthetic (seeded device Philox random walks, z-normalised)",
         "config": {"workload": cfg["name"], "mode": args.mode, "rows": cfg["N"], "length": cfg["n"],
                    "queries_per_step": nq, "reach": cfg["reach"], "parallelism": f"row-shard x{world}",
-                   "l2": "inputs larger than L2: every query streams %.2f GB of symbols per GPU" % (16 * main["N_local"] / 1e9),
+                   "l2": "inputs larger than L2: every query streams %.2f GB of coarse summaries per GPU" % (8 * main["N_local"] / 1e9),
                    "query_model": "sequential queries (P:2024-2026), batch call per step"},
-        "roofline": {"bound": "hbm", "kernel": "k_scan (LB scan + compaction)", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": "k_scan (coarse iSAX LB scan + compaction)", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in pk else "fallback",
                      "algorithmic_bytes_per_launch": scan_bytes, "launches": scan_n,
@@ -331,8 +336,8 @@ def ours(args):
         "clocks": main["clocks"],
         "build": {"ms": main["build_ms"], "rows_per_s": main["N_local"] / (main["build_ms"] / 1e3),
                   "what": "summarise (PAA + iSAX + key) + CUB key sort, per GPU"},
-        "stats_mean": {k: mean(k) for k in ("candidates", "lbk_pass", "refined", "abandoned", "near_best",
-                                             "seed_d2", "bsf_d2")},
+        "stats_mean": {k: mean(k) for k in ("coarse_pass", "candidates", "lbk_pass", "refined", "abandoned",
+                                             "near_best", "seed_d2", "bsf_d2")},
     }
     if args.mode == "ed" and not args.no_dtw:
         c4 = dict(CONFIGS["c4"])
@@ -344,8 +349,8 @@ def ours(args):
         line["dtw"] = {"value": k4 * d["nq"] / (dms / 1e3), "unit": "queries/s", "workload": c4["name"],
                        "steps": k4, "ms_per_step": dms / k4,
                        "kernel_ms_per_step": {k: v[0] / k4 for k, v in d["prof"].items()},
-                       "stats_mean": {k: dm(k) for k in ("candidates", "lbk_pass", "refined", "abandoned",
-                                                         "near_best", "seed_d2", "bsf_d2")},
+                       "stats_mean": {k: dm(k) for k in ("coarse_pass", "candidates", "lbk_pass", "refined",
+                                                         "abandoned", "near_best", "seed_d2", "bsf_d2")},
                        "gpu_launches": d["launches"]}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, args, dev, "ED" if cfg["reach"] is None else "DTW")

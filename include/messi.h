@@ -62,7 +62,8 @@ typedef struct {
 
 typedef struct {
     int64_t lb_computed;  /* rows whose iSAX lower bound was evaluated (= count: flat scan) */
-    int64_t candidates;   /* rows with LB <= BSF0 * (1 + eps) after the scan */
+    int64_t coarse_pass;  /* rows whose cardinality-16 (4-bit prefix) bound <= BSF0 * (1 + eps) */
+    int64_t candidates;   /* of those, rows whose exact 8-bit bound <= BSF * (1 + eps) */
     int64_t lbk_pass;     /* DTW: candidates whose raw LB_Keogh <= BSF * (1 + eps) */
     int64_t refined;      /* real distances computed (fp32) in the refine step */
     int64_t abandoned;    /* real distance computations abandoned early */
@@ -124,10 +125,15 @@ messi_status messi_debug_summaries(messi_index* idx, uint8_t* sym_dev, float* pa
 /* Sorted approximate-search keys and the row permutation (device pointers owned by idx). */
 messi_status messi_debug_order(messi_index* idx, const uint64_t** skey_dev, const uint32_t** perm_dev);
 
+/* Pair bytes of the coarse summary, [count][8]: byte p = hi(sym_2p) << 4 | hi(sym_2p+1). */
+messi_status messi_debug_coarse_summaries(messi_index* idx, uint8_t* pairs_dev);
+
 /* Lower bound of every row against one query (device pointer): reach < 0 -> ED mindist
  * (Property 1); reach >= 0 -> DTW envelope-PAA bound.  Squared,
- * fp32 rounded down, written to lb_dev[count]. */
+ * fp32 rounded down, written to lb_dev[count].  _lower_bounds: the exact 8-bit words;
+ * _coarse_bounds: the same bound at cardinality 16 (top nibbles), what the scan streams. */
 messi_status messi_debug_lower_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
+messi_status messi_debug_coarse_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
 
 /* For `k` local row ids: fp32 squared distance as computed by the refine kernels (no
  * abandoning), the exact fp64 squared distance of the re-rank kernel, and (reach >= 0)

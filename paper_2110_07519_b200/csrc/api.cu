@@ -1,5 +1,14 @@
 // api.cu -- the C-ABI of libmessi (include/messi.h): argument checks, device memory,
-// kernel orchestration.  The only translation unit; the .cuh files hold the kernels.
+// stream/event orchestration of the kernels.  The only translation unit; the .cuh files
+// hold the kernels.
+//
+// Query pipeline (per query k, state slot k & 1, three streams):
+//   side   : seed(k)  -- prologue tables + approximate search -> BSF0      (latency-bound)
+//   main   : scan(k)  -- coarse iSAX lower bound of every series           (HBM-bound)
+//   refine : ED : fine bound + real distances + exact re-rank -> result(k)
+//            DTW: fine bound + LB_Keogh -> banded DTW -> exact re-rank -> result(k)
+// scan(k) waits for seed(k); refine(k) for scan(k); seed(k+2) for refine(k) (slot reuse).
+// So seed(k+1) and refine(k) overlap scan(k+1): the HBM stream on `main` is back to back.
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 
@@ -18,25 +27,36 @@
 
 using namespace messi;
 
+struct Slot {
+    QState* st = nullptr;
+    float *lut = nullptr, *lut2 = nullptr, *U = nullptr, *L = nullptr;
+    uint2* coarse = nullptr;  // coarse-scan survivors (id, coarse LB)
+    uint2* list2 = nullptr;   // DTW: LB_Keogh survivors (id, LBK)  [lazy]
+    NearEntry* near = nullptr;
+    cudaEvent_t ev_seed = nullptr, ev_scan = nullptr, ev_done = nullptr;
+};
+
 struct messi_index {
     int device = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;  // the caller's stream ("main": scans)
+    cudaStream_t side = nullptr;    // library-owned: seeds
+    cudaStream_t rstr = nullptr;    // library-owned: refine / resolve
+    cudaEvent_t ev_fork = nullptr;
     int n = 0, window = 2000, keep_paa = 0;
     long long N = 0, ntiles = 0, row_begin = 0;
     const float* rows = nullptr;
     int sms = 148;
     // summaries
-    uint4* tiles = nullptr;
+    uint4* tiles = nullptr;    // coarse tiles (4 KB per 512 series)
+    uint4* symrows = nullptr;  // [ntiles*512][16] u8
     float* paa = nullptr;
     unsigned long long* skey = nullptr;
     unsigned* perm = nullptr;
     float *beta32 = nullptr, *lo_w = nullptr, *hi_w = nullptr;
     // per-query scratch
-    float *lut = nullptr, *U = nullptr, *L = nullptr, *qbuf = nullptr;
-    uint2* cand = nullptr;
-    unsigned* list2 = nullptr;
-    NearEntry* near = nullptr;
-    QState* st = nullptr;
+    Slot slot[2];
+    unsigned long long qcount = 0;
+    float* qbuf = nullptr;
     messi_result* res1 = nullptr;
     messi_stats* stats1 = nullptr;
     long long launches = 0;
@@ -47,44 +67,10 @@ struct messi_index {
     std::vector<cudaEvent_t> pool;
 };
 
-enum { K_SEED = 0, K_SCAN = 1, K_REFINE = 2, K_LBK = 3, K_RESOLVE = 4, K_KINDS = 5 };
-
-static cudaEvent_t pool_get(messi_index* idx)
-{
-    if (!idx->pool.empty()) {
-        cudaEvent_t e = idx->pool.back();
-        idx->pool.pop_back();
-        return e;
-    }
-    cudaEvent_t e = nullptr;
-    cudaEventCreate(&e);
-    return e;
-}
-
-// Brackets one launch with events when profiling is on.
-struct ProfScope {
-    messi_index* idx;
-    int kind;
-    cudaEvent_t a = nullptr;
-    ProfScope(messi_index* i, int k) : idx(i), kind(k)
-    {
-        if (idx->prof) {
-            a = pool_get(idx);
-            cudaEventRecord(a, idx->stream);
-        }
-    }
-    ~ProfScope()
-    {
-        if (idx->prof && a) {
-            cudaEvent_t b = pool_get(idx);
-            cudaEventRecord(b, idx->stream);
-            idx->evs.push_back({kind, a, b});
-        }
-    }
-};
-
 static_assert(sizeof(messi_result) == 32, "messi_result layout");
-static_assert(sizeof(messi_stats) == 64, "messi_stats layout");
+static_assert(sizeof(messi_stats) == 72, "messi_stats layout");
+
+enum { K_SEED = 0, K_SCAN = 1, K_REFINE = 2, K_LBK = 3, K_RESOLVE = 4, K_KINDS = 5 };
 
 // ------------------------------------------------------------------------------ errors
 static thread_local char g_err[512] = "";
@@ -113,6 +99,12 @@ static messi_status fail(messi_status s, const char* fmt, ...)
         CK(cudaGetLastError());                                                                     \
     } while (0)
 
+#define TRY(x)                                                                                      \
+    do {                                                                                            \
+        messi_status s_ = (x);                                                                      \
+        if (s_ != MESSI_OK) return s_;                                                              \
+    } while (0)
+
 template <typename T> static messi_status dalloc(T** p, size_t count)
 {
     *p = nullptr;
@@ -121,39 +113,78 @@ template <typename T> static messi_status dalloc(T** p, size_t count)
     return MESSI_OK;
 }
 
-#define TRY(x)                                                                                      \
-    do {                                                                                            \
-        messi_status s_ = (x);                                                                      \
-        if (s_ != MESSI_OK) return s_;                                                              \
-    } while (0)
+static cudaEvent_t pool_get(messi_index* idx)
+{
+    if (!idx->pool.empty()) {
+        cudaEvent_t e = idx->pool.back();
+        idx->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Brackets one launch with events on its stream when profiling is on.
+struct ProfScope {
+    messi_index* idx;
+    int kind;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    ProfScope(messi_index* i, int k, cudaStream_t st) : idx(i), kind(k), s(st)
+    {
+        if (idx->prof) {
+            a = pool_get(idx);
+            cudaEventRecord(a, s);
+        }
+    }
+    ~ProfScope()
+    {
+        if (idx->prof && a) {
+            cudaEvent_t b = pool_get(idx);
+            cudaEventRecord(b, s);
+            idx->evs.push_back({kind, a, b});
+        }
+    }
+};
 
 // Reaches with a register-band DTW instantiation (DtwThread<R>); others use the warp path.
 #define MESSI_DTW_REACHES(X) X(2) X(5) X(12) X(25)
 
-static size_t scan_smem() { return (size_t)MESSI_CARD * 64 * sizeof(float); }
+static size_t scan_smem() { return kScanLutBytes; }
+static size_t lbk_smem(int n)
+{
+    return (size_t)MESSI_W * MESSI_CARD * sizeof(float) + 2 * (size_t)((n + 3) & ~3) * sizeof(float);
+}
 
 static messi_status setup_kernels()
 {
     static bool done = false;
     if (done) return MESSI_OK;
-    CK(cudaFuncSetAttribute(k_scan<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
-    CK(cudaFuncSetAttribute(k_scan<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
-    CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(k_refine_dtw_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(k_resolve_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(k_debug_dist<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-#define SET_ATTR(R) CK(cudaFuncSetAttribute(k_debug_dist<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    const int big = 200 * 1024;
+    CK(cudaFuncSetAttribute(k_scan<SCAN_COMPACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
+    CK(cudaFuncSetAttribute(k_scan<SCAN_ALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
+    CK(cudaFuncSetAttribute(k_fine_ed, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_lbk_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_refine_dtw_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_resolve_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_resolve_ed, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+#define SET_ATTR_R(R) CK(cudaFuncSetAttribute(k_refine_dtw<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    MESSI_DTW_REACHES(SET_ATTR_R)
+#undef SET_ATTR_R
+    CK(cudaFuncSetAttribute(k_debug_dist<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+#define SET_ATTR(R) CK(cudaFuncSetAttribute(k_debug_dist<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     MESSI_DTW_REACHES(SET_ATTR)
 #undef SET_ATTR
     done = true;
     return MESSI_OK;
 }
 
-// warps per CTA for kernels holding 3*n elements of `esize` bytes per warp in smem
-static int wavefront_warps(int n, size_t esize, int maxw)
+// Warps per CTA for wavefront kernels holding `per_warp` bytes of shared memory each.
+static int warps_for(size_t per_warp, int maxw)
 {
-    size_t per = 3 * (size_t)n * esize;
-    int w = (int)((96 * 1024) / per);
+    int w = (int)((96 * 1024) / (per_warp ? per_warp : 1));
     return w < 1 ? 1 : (w > maxw ? maxw : w);
 }
 
@@ -197,17 +228,28 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
 
     auto bail = [&](messi_status s) { messi_free(idx); return s; };
     const long long N = count;
+    const size_t npadrows = (size_t)idx->ntiles * MESSI_TILE_ROWS;
     messi_status s;
-    if ((s = dalloc(&idx->tiles, (size_t)idx->ntiles * (MESSI_TILE_BYTES / 16)))) return bail(s);
+    if ((s = dalloc(&idx->tiles, (size_t)idx->ntiles * (MESSI_TILE_BYTES / 16))) || (s = dalloc(&idx->symrows, npadrows)))
+        return bail(s);
     if (idx->keep_paa && (s = dalloc(&idx->paa, (size_t)N * MESSI_W))) return bail(s);
     if ((s = dalloc(&idx->skey, (size_t)N)) || (s = dalloc(&idx->perm, (size_t)N))) return bail(s);
     if ((s = dalloc(&idx->beta32, 256)) || (s = dalloc(&idx->lo_w, 256)) || (s = dalloc(&idx->hi_w, 256))) return bail(s);
-    if ((s = dalloc(&idx->lut, MESSI_W * MESSI_CARD)) || (s = dalloc(&idx->U, n)) || (s = dalloc(&idx->L, n)) ||
-        (s = dalloc(&idx->qbuf, n)))
-        return bail(s);
-    if ((s = dalloc(&idx->cand, (size_t)N)) || (s = dalloc(&idx->list2, (size_t)N)) || (s = dalloc(&idx->near, (size_t)N)))
-        return bail(s);
-    if ((s = dalloc(&idx->st, 1)) || (s = dalloc(&idx->res1, 1)) || (s = dalloc(&idx->stats1, 1))) return bail(s);
+    for (Slot& sl : idx->slot) {
+        if ((s = dalloc(&sl.st, 1)) || (s = dalloc(&sl.lut, MESSI_W * MESSI_CARD)) ||
+            (s = dalloc(&sl.lut2, MESSI_PAIRS * MESSI_CARD)) || (s = dalloc(&sl.U, n)) || (s = dalloc(&sl.L, n)) ||
+            (s = dalloc(&sl.coarse, (size_t)N)) || (s = dalloc(&sl.near, (size_t)N)))
+            return bail(s);
+        if (cudaEventCreateWithFlags(&sl.ev_seed, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sl.ev_scan, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sl.ev_done, cudaEventDisableTiming) != cudaSuccess)
+            return bail(fail(MESSI_ECUDA, "event creation failed"));
+    }
+    if ((s = dalloc(&idx->qbuf, n)) || (s = dalloc(&idx->res1, 1)) || (s = dalloc(&idx->stats1, 1))) return bail(s);
+    if (cudaStreamCreateWithFlags(&idx->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&idx->rstr, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&idx->ev_fork, cudaEventDisableTiming) != cudaSuccess)
+        return bail(fail(MESSI_ECUDA, "stream creation failed"));
 
     cudaStream_t st = idx->stream;
     unsigned long long* keys_in = nullptr;
@@ -225,8 +267,8 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
         ++idx->launches;
         if (cudaGetLastError() != cudaSuccess) { s = fail(MESSI_ECUDA, "k_breakpoints launch"); break; }
         long long grid = idx->ntiles < (long long)idx->sms * 8 ? idx->ntiles : (long long)idx->sms * 8;
-        k_summarise<<<(unsigned)grid, 256, 0, st>>>(rows_dev, N, n, idx->beta32, idx->tiles, idx->ntiles, keys_in,
-                                                    ids_in, idx->paa);
+        k_summarise<<<(unsigned)grid, 256, 0, st>>>(rows_dev, N, n, idx->beta32, idx->tiles, idx->symrows, idx->ntiles,
+                                                    keys_in, ids_in, idx->paa);
         ++idx->launches;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "k_summarise: %s", cudaGetErrorString(e)); break; }
@@ -237,8 +279,10 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
         e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, idx->skey, ids_in, idx->perm, (int)N, 0, 64, st);
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "cub sort: %s", cudaGetErrorString(e)); break; }
         idx->launches += 4;
-        k_arm<<<1, 1, 0, st>>>(idx->st);
-        ++idx->launches;
+        for (Slot& sl : idx->slot) {
+            k_arm<<<1, 1, 0, st>>>(sl.st);
+            ++idx->launches;
+        }
         e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "build: %s", cudaGetErrorString(e)); break; }
         s = MESSI_OK;
@@ -253,13 +297,25 @@ extern "C" void messi_free(messi_index* idx)
 {
     if (!idx) return;
     cudaSetDevice(idx->device);
+    if (idx->side) cudaStreamSynchronize(idx->side);
+    if (idx->rstr) cudaStreamSynchronize(idx->rstr);
     if (idx->stream) cudaStreamSynchronize(idx->stream);
     else cudaDeviceSynchronize();
-    void* ptrs[] = {idx->tiles, idx->paa,   idx->skey, idx->perm, idx->beta32, idx->lo_w,  idx->hi_w,
-                    idx->lut,   idx->U,     idx->L,    idx->qbuf, idx->cand,   idx->list2, idx->near,
-                    idx->st,    idx->res1,  idx->stats1};
+    void* ptrs[] = {idx->tiles, idx->symrows, idx->paa,  idx->skey, idx->perm,  idx->beta32,
+                    idx->lo_w,  idx->hi_w,    idx->qbuf, idx->res1, idx->stats1};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (Slot& sl : idx->slot) {
+        void* sp[] = {sl.st, sl.lut, sl.lut2, sl.U, sl.L, sl.coarse, sl.list2, sl.near};
+        for (void* p : sp)
+            if (p) cudaFree(p);
+        cudaEvent_t es[] = {sl.ev_seed, sl.ev_scan, sl.ev_done};
+        for (cudaEvent_t e : es)
+            if (e) cudaEventDestroy(e);
+    }
+    if (idx->ev_fork) cudaEventDestroy(idx->ev_fork);
+    if (idx->side) cudaStreamDestroy(idx->side);
+    if (idx->rstr) cudaStreamDestroy(idx->rstr);
     for (auto& e : idx->evs) {
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
@@ -272,11 +328,19 @@ extern "C" const char* messi_last_error(void) { return g_err; }
 
 extern "C" int64_t messi_launch_count(const messi_index* idx) { return idx ? idx->launches : 0; }
 
+static messi_status sync_all(messi_index* idx)
+{
+    CK(cudaStreamSynchronize(idx->stream));
+    CK(cudaStreamSynchronize(idx->side));
+    CK(cudaStreamSynchronize(idx->rstr));
+    return MESSI_OK;
+}
+
 extern "C" messi_status messi_profile_enable(messi_index* idx, int32_t enable)
 {
     if (!idx) return fail(MESSI_EINVAL, "NULL index");
     CK(cudaSetDevice(idx->device));
-    CK(cudaStreamSynchronize(idx->stream));
+    TRY(sync_all(idx));
     for (auto& e : idx->evs) {
         idx->pool.push_back(e.a);
         idx->pool.push_back(e.b);
@@ -290,7 +354,7 @@ extern "C" messi_status messi_profile_read(messi_index* idx, int32_t kind, doubl
 {
     if (!idx || !total_ms || !launches || kind < 0 || kind >= K_KINDS) return fail(MESSI_EINVAL, "bad argument");
     CK(cudaSetDevice(idx->device));
-    CK(cudaStreamSynchronize(idx->stream));
+    TRY(sync_all(idx));
     double ms = 0.0;
     long long cnt = 0;
     for (auto& e : idx->evs) {
@@ -308,97 +372,138 @@ extern "C" messi_status messi_profile_read(messi_index* idx, int32_t kind, doubl
 // ---------------------------------------------------------------------------- queries
 static int scan_grid(const messi_index* idx)
 {
-    long long need = (idx->ntiles + 7) / 8;
+    long long need = (idx->ntiles + kScanWarps - 1) / kScanWarps;
     long long cap = (long long)idx->sms * 2;
     return (int)(need < cap ? (need < 1 ? 1 : need) : cap);
 }
 
-// One ED query, fully on the stream: seed (+prologue) -> scan -> refine -> resolve.
+static int refine_grid(const messi_index* idx, int per_block_rows)
+{
+    long long need = (idx->N + per_block_rows - 1) / per_block_rows;
+    long long cap = (long long)idx->sms * 4;
+    return (int)(need < cap ? (need < 1 ? 1 : need) : cap);
+}
+
+// Orders the side and refine streams after everything already enqueued on the main stream
+// (query buffers written by the caller) -- once per API call, not between batch queries.
+static messi_status fork_streams(messi_index* idx)
+{
+    CK(cudaEventRecord(idx->ev_fork, idx->stream));
+    CK(cudaStreamWaitEvent(idx->side, idx->ev_fork, 0));
+    CK(cudaStreamWaitEvent(idx->rstr, idx->ev_fork, 0));
+    return MESSI_OK;
+}
+
+// The caller's stream waits for the results of every query enqueued so far.
+static messi_status join_streams(messi_index* idx)
+{
+    for (Slot& sl : idx->slot) CK(cudaStreamWaitEvent(idx->stream, sl.ev_done, 0));
+    return MESSI_OK;
+}
+
+static messi_status ensure_dtw_buffers(messi_index* idx)
+{
+    for (Slot& sl : idx->slot)
+        if (!sl.list2) TRY(dalloc(&sl.list2, (size_t)idx->N));
+    return MESSI_OK;
+}
+
+static messi_status launch_scan(messi_index* idx, Slot& sl)
+{
+    CK(cudaStreamWaitEvent(idx->stream, sl.ev_seed, 0));
+    {
+        ProfScope ps(idx, K_SCAN, idx->stream);
+        k_scan<SCAN_COMPACT><<<scan_grid(idx), 32 * kScanWarps, scan_smem(), idx->stream>>>(
+            idx->tiles, idx->ntiles, idx->N, sl.lut2, sl.st, sl.coarse, nullptr);
+        LAUNCHED(idx);
+    }
+    CK(cudaEventRecord(sl.ev_scan, idx->stream));
+    CK(cudaStreamWaitEvent(idx->rstr, sl.ev_scan, 0));
+    return MESSI_OK;
+}
+
 static messi_status run_ed(messi_index* idx, const float* q_dev, messi_result* res, messi_stats* stats)
 {
-    cudaStream_t st = idx->stream;
+    Slot& sl = idx->slot[idx->qcount++ & 1];
     const int n = idx->n;
     const size_t qsm = (size_t)((n + 3) & ~3) * sizeof(float);
     int len = (int)(idx->window < idx->N ? idx->window : idx->N);
     int seed_grid = (len + 7) / 8;
     if (seed_grid > 256) seed_grid = 256;
+    CK(cudaStreamWaitEvent(idx->side, sl.ev_done, 0));  // the slot's previous query is finished
     {
-        ProfScope ps(idx, K_SEED);
-        k_seed_ed<<<seed_grid, 256, qsm, st>>>(q_dev, n, idx->rows, idx->skey, idx->perm, idx->N, idx->window,
-                                               idx->beta32, idx->lo_w, idx->hi_w, idx->lut, idx->st);
+        ProfScope ps(idx, K_SEED, idx->side);
+        k_seed_ed<<<seed_grid, 256, qsm, idx->side>>>(q_dev, n, idx->rows, idx->skey, idx->perm, idx->N, idx->window,
+                                                      idx->beta32, idx->lo_w, idx->hi_w, sl.lut, sl.lut2, sl.st);
         LAUNCHED(idx);
     }
+    CK(cudaEventRecord(sl.ev_seed, idx->side));
+    TRY(launch_scan(idx, sl));
     {
-        ProfScope ps(idx, K_SCAN);
-        k_scan<false><<<scan_grid(idx), 256, scan_smem(), st>>>(idx->tiles, idx->ntiles, idx->N, idx->lut, idx->st,
-                                                                idx->cand, nullptr);
+        ProfScope ps(idx, K_REFINE, idx->rstr);
+        k_fine_ed<<<refine_grid(idx, 4096), 256, fine_ed_smem(n), idx->rstr>>>(
+            sl.coarse, idx->symrows, sl.lut, idx->rows, n, q_dev, sl.st, sl.near, idx->N, idx->row_begin, res, stats);
         LAUNCHED(idx);
     }
-    {
-        ProfScope ps(idx, K_REFINE);
-        k_refine_ed<<<idx->sms * 4, 256, qsm, st>>>(idx->rows, n, q_dev, idx->cand, idx->st, idx->near);
-        LAUNCHED(idx);
-    }
-    {
-        ProfScope ps(idx, K_RESOLVE);
-        k_resolve_ed<<<1, 256, 0, st>>>(idx->rows, n, q_dev, idx->near, idx->st, idx->N, idx->row_begin, res, stats);
-        LAUNCHED(idx);
-    }
+    CK(cudaEventRecord(sl.ev_done, idx->rstr));
     return MESSI_OK;
 }
 
 static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, messi_result* res, messi_stats* stats)
 {
-    cudaStream_t st = idx->stream;
+    Slot& sl = idx->slot[idx->qcount++ & 1];
+    cudaStream_t rs = idx->rstr;
     const int n = idx->n;
     const int npad = (n + 3) & ~3;
     const size_t qsm = (size_t)npad * sizeof(float);
     int len = (int)(idx->window < idx->N ? idx->window : idx->N);
-    const int wf = wavefront_warps(n, sizeof(float), 8);
+    const size_t seed_warp = (size_t)(npad + 3 * n) * sizeof(float);
+    const int wf = warps_for(seed_warp, 8);
     int seed_grid = (len + wf - 1) / wf;
     if (seed_grid > idx->sms * 4) seed_grid = idx->sms * 4;
+    CK(cudaStreamWaitEvent(idx->side, sl.ev_done, 0));
     {
-        ProfScope ps(idx, K_SEED);
-        k_seed_dtw<<<seed_grid, 32 * wf, qsm + (size_t)wf * 3 * n * sizeof(float), st>>>(
+        ProfScope ps(idx, K_SEED, idx->side);
+        k_seed_dtw<<<seed_grid, 32 * wf, qsm + wf * seed_warp, idx->side>>>(
             q_dev, n, reach, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32, idx->lo_w, idx->hi_w,
-            idx->lut, idx->U, idx->L, idx->st);
+            sl.lut, sl.U, sl.L, sl.lut2, sl.st);
+        LAUNCHED(idx);
+    }
+    CK(cudaEventRecord(sl.ev_seed, idx->side));
+    TRY(launch_scan(idx, sl));
+    {
+        ProfScope ps(idx, K_LBK, rs);
+        k_lbk_filter<<<refine_grid(idx, 2048), 256, lbk_smem(n), rs>>>(sl.coarse, idx->symrows, sl.lut, idx->rows, n,
+                                                                       sl.U, sl.L, sl.st, sl.list2);
         LAUNCHED(idx);
     }
     {
-        ProfScope ps(idx, K_SCAN);
-        k_scan<false><<<scan_grid(idx), 256, scan_smem(), st>>>(idx->tiles, idx->ntiles, idx->N, idx->lut, idx->st,
-                                                                idx->cand, nullptr);
-        LAUNCHED(idx);
-    }
-    {
-        ProfScope ps(idx, K_LBK);
-        k_lbk_filter<<<idx->sms * 4, 256, 2 * qsm, st>>>(idx->rows, n, idx->U, idx->L, idx->cand, idx->st, idx->list2);
-        LAUNCHED(idx);
-    }
-    ProfScope* ref_scope = new ProfScope(idx, K_REFINE);
-    bool launched = false;
+        ProfScope ps(idx, K_REFINE, rs);
+        bool launched = false;
 #define LAUNCH_R(R)                                                                                           \
     if (!launched && reach == R) {                                                                            \
-        k_refine_dtw<R><<<idx->sms * 8, 128, qsm, st>>>(idx->rows, n, q_dev, idx->list2, idx->st, idx->near); \
-        ++idx->launches;                                                                                      \
+        k_refine_dtw<R><<<idx->sms * 8, 128, 3 * qsm, rs>>>(idx->rows, n, q_dev, sl.U, sl.L, sl.list2, sl.st, \
+                                                            sl.near);                                         \
         launched = true;                                                                                      \
     }
-    MESSI_DTW_REACHES(LAUNCH_R)
+        MESSI_DTW_REACHES(LAUNCH_R)
 #undef LAUNCH_R
-    if (!launched) {
-        k_refine_dtw_warp<<<idx->sms * 4, 32 * wf, qsm + (size_t)wf * 3 * n * sizeof(float), st>>>(
-            idx->rows, n, reach, q_dev, idx->list2, idx->st, idx->near);
-        ++idx->launches;
-    }
-    delete ref_scope;
-    CK(cudaGetLastError());
-    const int wr = wavefront_warps(n, sizeof(double), 8);
-    {
-        ProfScope ps(idx, K_RESOLVE);
-        k_resolve_dtw<<<1, 32 * wr, (size_t)wr * 3 * n * sizeof(double), st>>>(idx->rows, n, reach, q_dev, idx->near,
-                                                                              idx->st, idx->N, idx->row_begin, res, stats);
+        if (!launched) {
+            const int wr = warps_for((size_t)4 * npad * sizeof(float), 8);
+            k_refine_dtw_warp<<<idx->sms * 4, 32 * wr, qsm + (size_t)wr * 4 * npad * sizeof(float), rs>>>(
+                idx->rows, n, reach, q_dev, sl.list2, sl.st, sl.near);
+        }
         LAUNCHED(idx);
     }
+    {
+        const size_t rw = (size_t)(3 * n + npad) * sizeof(double);
+        const int wr = warps_for(rw, 8);
+        ProfScope ps(idx, K_RESOLVE, rs);
+        k_resolve_dtw<<<1, 32 * wr, wr * rw, rs>>>(idx->rows, n, reach, q_dev, sl.near, sl.st, idx->N, idx->row_begin,
+                                                   res, stats);
+        LAUNCHED(idx);
+    }
+    CK(cudaEventRecord(sl.ev_done, rs));
     return MESSI_OK;
 }
 
@@ -416,6 +521,8 @@ static messi_status stage_query(messi_index* idx, const float* query, const floa
         *q_dev = query;
         return MESSI_OK;
     }
+    // the buffer may still be read by an earlier query on the refine stream
+    TRY(join_streams(idx));
     CK(cudaMemcpyAsync(idx->qbuf, query, (size_t)idx->n * sizeof(float), cudaMemcpyHostToDevice, idx->stream));
     *q_dev = idx->qbuf;
     return MESSI_OK;
@@ -423,6 +530,7 @@ static messi_status stage_query(messi_index* idx, const float* query, const floa
 
 static messi_status finish_single(messi_index* idx, messi_result* local_best, messi_stats* stats)
 {
+    TRY(join_streams(idx));
     CK(cudaMemcpyAsync(local_best, idx->res1, sizeof(messi_result), cudaMemcpyDeviceToHost, idx->stream));
     if (stats) CK(cudaMemcpyAsync(stats, idx->stats1, sizeof(messi_stats), cudaMemcpyDeviceToHost, idx->stream));
     CK(cudaStreamSynchronize(idx->stream));
@@ -436,6 +544,7 @@ extern "C" messi_status messi_query_ed(messi_index* idx, const float* query, mes
     CK(cudaSetDevice(idx->device));
     const float* q = nullptr;
     TRY(stage_query(idx, query, &q));
+    TRY(fork_streams(idx));
     TRY(run_ed(idx, q, idx->res1, idx->stats1));
     return finish_single(idx, local_best, stats);
 }
@@ -447,8 +556,10 @@ extern "C" messi_status messi_query_dtw(messi_index* idx, const float* query, in
     if (!idx || !query || !local_best) return fail(MESSI_EINVAL, "NULL argument");
     if (reach < 0 || reach > idx->n) return fail(MESSI_EINVAL, "reach %d outside [0, %d]", reach, idx->n);
     CK(cudaSetDevice(idx->device));
+    TRY(ensure_dtw_buffers(idx));
     const float* q = nullptr;
     TRY(stage_query(idx, query, &q));
+    TRY(fork_streams(idx));
     TRY(run_dtw(idx, q, reach, idx->res1, idx->stats1));
     return finish_single(idx, local_best, stats);
 }
@@ -459,9 +570,10 @@ extern "C" messi_status messi_query_ed_batch(messi_index* idx, const float* quer
     g_err[0] = 0;
     if (!idx || !queries_dev || !results_dev || nq < 0) return fail(MESSI_EINVAL, "bad argument");
     CK(cudaSetDevice(idx->device));
+    TRY(fork_streams(idx));
     for (int i = 0; i < nq; ++i)
         TRY(run_ed(idx, queries_dev + (size_t)i * idx->n, results_dev + i, stats_dev ? stats_dev + i : nullptr));
-    return MESSI_OK;
+    return join_streams(idx);
 }
 
 extern "C" messi_status messi_query_dtw_batch(messi_index* idx, const float* queries_dev, int32_t nq, int32_t reach,
@@ -471,9 +583,11 @@ extern "C" messi_status messi_query_dtw_batch(messi_index* idx, const float* que
     if (!idx || !queries_dev || !results_dev || nq < 0) return fail(MESSI_EINVAL, "bad argument");
     if (reach < 0 || reach > idx->n) return fail(MESSI_EINVAL, "reach %d outside [0, %d]", reach, idx->n);
     CK(cudaSetDevice(idx->device));
+    TRY(ensure_dtw_buffers(idx));
+    TRY(fork_streams(idx));
     for (int i = 0; i < nq; ++i)
         TRY(run_dtw(idx, queries_dev + (size_t)i * idx->n, reach, results_dev + i, stats_dev ? stats_dev + i : nullptr));
-    return MESSI_OK;
+    return join_streams(idx);
 }
 
 // ------------------------------------------------------------------------ inspection
@@ -498,11 +612,25 @@ extern "C" messi_status messi_debug_summaries(messi_index* idx, uint8_t* sym_dev
     if (!idx || !sym_dev) return fail(MESSI_EINVAL, "NULL argument");
     if (paa_dev && !idx->paa) return fail(MESSI_EINVAL, "index built without keep_paa");
     CK(cudaSetDevice(idx->device));
-    long long total = idx->N * MESSI_W;
-    k_detile<<<(unsigned)((total + 255) / 256), 256, 0, idx->stream>>>((const unsigned char*)idx->tiles, idx->N, sym_dev);
-    LAUNCHED(idx);
+    TRY(sync_all(idx));
+    CK(cudaMemcpyAsync(sym_dev, idx->symrows, (size_t)idx->N * MESSI_W, cudaMemcpyDeviceToDevice, idx->stream));
     if (paa_dev)
-        CK(cudaMemcpyAsync(paa_dev, idx->paa, (size_t)total * sizeof(float), cudaMemcpyDeviceToDevice, idx->stream));
+        CK(cudaMemcpyAsync(paa_dev, idx->paa, (size_t)idx->N * MESSI_W * sizeof(float), cudaMemcpyDeviceToDevice,
+                           idx->stream));
+    CK(cudaStreamSynchronize(idx->stream));
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_debug_coarse_summaries(messi_index* idx, uint8_t* pairs_dev)
+{
+    g_err[0] = 0;
+    if (!idx || !pairs_dev) return fail(MESSI_EINVAL, "NULL argument");
+    CK(cudaSetDevice(idx->device));
+    TRY(sync_all(idx));
+    long long total = idx->N * MESSI_PAIRS;
+    k_detile_coarse<<<(unsigned)((total + 255) / 256), 256, 0, idx->stream>>>((const unsigned char*)idx->tiles, idx->N,
+                                                                              pairs_dev);
+    LAUNCHED(idx);
     CK(cudaStreamSynchronize(idx->stream));
     return MESSI_OK;
 }
@@ -515,30 +643,54 @@ extern "C" messi_status messi_debug_order(messi_index* idx, const uint64_t** ske
     return MESSI_OK;
 }
 
+// Prologue only (tables, envelope) for `reach` into slot 0, which is left armed.
+static messi_status debug_prologue(messi_index* idx, const float* query_dev, int reach)
+{
+    cudaStream_t st = idx->stream;
+    Slot& sl = idx->slot[0];
+    const int n = idx->n;
+    const size_t qsm = (size_t)((n + 3) & ~3) * sizeof(float);
+    if (reach < 0) {
+        k_seed_ed<<<1, 256, qsm, st>>>(query_dev, n, idx->rows, idx->skey, idx->perm, idx->N, 1, idx->beta32, idx->lo_w,
+                                       idx->hi_w, sl.lut, sl.lut2, sl.st);
+    } else {
+        k_seed_dtw<<<1, 32, 2 * qsm + 3 * (size_t)n * sizeof(float), st>>>(query_dev, n, reach, idx->rows, idx->skey,
+                                                                          idx->perm, idx->N, 1, idx->beta32, idx->lo_w,
+                                                                          idx->hi_w, sl.lut, sl.U, sl.L, sl.lut2, sl.st);
+    }
+    LAUNCHED(idx);
+    k_arm<<<1, 1, 0, st>>>(sl.st);
+    LAUNCHED(idx);
+    return MESSI_OK;
+}
+
 extern "C" messi_status messi_debug_lower_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev)
 {
     g_err[0] = 0;
     if (!idx || !query_dev || !lb_dev) return fail(MESSI_EINVAL, "NULL argument");
     if (reach > idx->n) return fail(MESSI_EINVAL, "reach %d > n", reach);
     CK(cudaSetDevice(idx->device));
-    cudaStream_t st = idx->stream;
-    const int n = idx->n;
-    const size_t qsm = (size_t)((n + 3) & ~3) * sizeof(float);
-    if (reach < 0) {
-        k_seed_ed<<<1, 256, qsm, st>>>(query_dev, n, idx->rows, idx->skey, idx->perm, idx->N, 1, idx->beta32, idx->lo_w,
-                                       idx->hi_w, idx->lut, idx->st);
-    } else {
-        k_seed_dtw<<<1, 32, qsm + 3 * (size_t)n * sizeof(float), st>>>(query_dev, n, reach, idx->rows, idx->skey, idx->perm,
-                                                                      idx->N, 1, idx->beta32, idx->lo_w, idx->hi_w,
-                                                                      idx->lut, idx->U, idx->L, idx->st);
-    }
+    TRY(sync_all(idx));
+    TRY(debug_prologue(idx, query_dev, reach));
+    k_fine_all<<<idx->sms * 4, 256, 0, idx->stream>>>(idx->symrows, idx->N, idx->slot[0].lut, lb_dev);
     LAUNCHED(idx);
-    k_scan<true><<<scan_grid(idx), 256, scan_smem(), st>>>(idx->tiles, idx->ntiles, idx->N, idx->lut, idx->st, idx->cand,
-                                                           lb_dev);
+    CK(cudaStreamSynchronize(idx->stream));
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_debug_coarse_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev)
+{
+    g_err[0] = 0;
+    if (!idx || !query_dev || !lb_dev) return fail(MESSI_EINVAL, "NULL argument");
+    if (reach > idx->n) return fail(MESSI_EINVAL, "reach %d > n", reach);
+    CK(cudaSetDevice(idx->device));
+    TRY(sync_all(idx));
+    TRY(debug_prologue(idx, query_dev, reach));
+    Slot& sl = idx->slot[0];
+    k_scan<SCAN_ALL><<<scan_grid(idx), 32 * kScanWarps, scan_smem(), idx->stream>>>(idx->tiles, idx->ntiles, idx->N,
+                                                                                    sl.lut2, sl.st, nullptr, lb_dev);
     LAUNCHED(idx);
-    k_arm<<<1, 1, 0, st>>>(idx->st);
-    LAUNCHED(idx);
-    CK(cudaStreamSynchronize(st));
+    CK(cudaStreamSynchronize(idx->stream));
     return MESSI_OK;
 }
 
@@ -550,33 +702,29 @@ extern "C" messi_status messi_debug_distances(messi_index* idx, const float* que
     if (!idx || !query_dev || (!ids_dev && k > 0) || k < 0) return fail(MESSI_EINVAL, "bad argument");
     if (reach > idx->n) return fail(MESSI_EINVAL, "reach %d > n", reach);
     CK(cudaSetDevice(idx->device));
+    TRY(sync_all(idx));
     cudaStream_t st = idx->stream;
+    Slot& sl = idx->slot[0];
     const int n = idx->n;
     const int npad = (n + 3) & ~3;
-    if (reach >= 0) {  // envelope for LB_Keogh (prologue only)
-        k_seed_dtw<<<1, 32, (size_t)npad * sizeof(float) + 3 * (size_t)n * sizeof(float), st>>>(
-            query_dev, n, reach, idx->rows, idx->skey, idx->perm, idx->N, 1, idx->beta32, idx->lo_w, idx->hi_w, idx->lut,
-            idx->U, idx->L, idx->st);
-        LAUNCHED(idx);
-        k_arm<<<1, 1, 0, st>>>(idx->st);
-        LAUNCHED(idx);
-    }
-    const int wr = wavefront_warps(n, sizeof(double), 4);
-    const size_t smem = 3 * (size_t)npad * sizeof(float) + (size_t)wr * 3 * n * sizeof(double);
+    if (reach >= 0) TRY(debug_prologue(idx, query_dev, reach));  // envelope for LB_Keogh
+    const size_t per_warp = (size_t)(npad + 6 * n) * sizeof(float);
+    const int wr = warps_for(per_warp, 4);
+    const size_t smem = 3 * (size_t)npad * sizeof(float) + (size_t)wr * per_warp;
     int grid = (k + wr - 1) / wr;
     if (grid > idx->sms * 8) grid = idx->sms * 8;
     if (grid < 1) grid = 1;
     bool launched = false;
 #define LAUNCH_D(R)                                                                                          \
     if (!launched && reach == R) {                                                                           \
-        k_debug_dist<R><<<grid, 32 * wr, smem, st>>>(idx->rows, n, reach, query_dev, idx->U, idx->L, ids_dev, k, \
+        k_debug_dist<R><<<grid, 32 * wr, smem, st>>>(idx->rows, n, reach, query_dev, sl.U, sl.L, ids_dev, k,   \
                                                      d32_dev, d64_dev, lbk_dev);                             \
         launched = true;                                                                                     \
     }
     MESSI_DTW_REACHES(LAUNCH_D)
 #undef LAUNCH_D
     if (!launched)
-        k_debug_dist<-1><<<grid, 32 * wr, smem, st>>>(idx->rows, n, reach, query_dev, idx->U, idx->L, ids_dev, k, d32_dev,
+        k_debug_dist<-1><<<grid, 32 * wr, smem, st>>>(idx->rows, n, reach, query_dev, sl.U, sl.L, ids_dev, k, d32_dev,
                                                       d64_dev, lbk_dev);
     LAUNCHED(idx);
     CK(cudaStreamSynchronize(st));

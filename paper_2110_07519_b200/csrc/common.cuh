@@ -6,8 +6,9 @@
 
 #define MESSI_W 16                 // PAA segments ("w is fixed to 16")
 #define MESSI_CARD 256             // 8-bit iSAX symbols
-#define MESSI_TILE_ROWS 512        // series per symbol tile (32 blocks x 16 series)
-#define MESSI_TILE_BYTES 8192      // 16 tile rows x 512 B
+#define MESSI_TILE_ROWS 512        // series per coarse tile (32 blocks x 16 series)
+#define MESSI_TILE_BYTES 4096      // coarse tile: 8 tile rows x 512 B (one nibble pair per byte)
+#define MESSI_PAIRS 8              // segment pairs (2p, 2p+1) of the coarse summary
 #define MESSI_MAX_N 8192
 
 namespace messi {
@@ -27,7 +28,8 @@ struct QState {
     unsigned near_count;    // near-best entries (d32 <= thr at refine time)
     unsigned refined;       // real distances started
     unsigned abandoned;     // real distances abandoned early
-    unsigned work;          // work-stealing cursor (DTW refine)
+    unsigned coarse_count;  // coarse-scan survivors appended
+    unsigned done;          // CTAs of the fused ED scan that finished (last one resolves)
     unsigned long long qkey;  // query's approximate-search key
     int window_start;       // first sorted position of the approximate-search window
     int window_len;
@@ -44,7 +46,8 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->near_count = 0;
     st->refined = 0;
     st->abandoned = 0;
-    st->work = 0;
+    st->coarse_count = 0;
+    st->done = 0;
 }
 
 __device__ __forceinline__ float warp_sum(float v)

@@ -50,6 +50,7 @@ __device__ __forceinline__ double cell_cost_add(float q, float c, double m)
 // P:323-324 / P:1379, one warp, anti-diagonal wavefront: anti-diagonal t = i + j holds the
 // cells i in [ilo, ihi]; lanes take them 32 at a time; three rotating buffers indexed by i
 // (buf: 3*n of T).  Cells just outside the band are written +inf so later reads see +inf.
+// q and c must already be in shared memory (the step loop is latency-bound otherwise).
 // With T = double and cell_cost_add's _rn ops every cell is fl(fl(d*d) + min(...)): the
 // same value in any evaluation order, i.e. bit-identical to a row-by-row DP.
 template <typename T>
@@ -92,6 +93,54 @@ __device__ T dtw_warp(const float* __restrict__ q, const float* __restrict__ c, 
     return out;
 }
 
+// Same banded DTW with the anti-diagonal in REGISTERS: for reach r <= 30 an anti-diagonal
+// holds at most r+1 <= 31 band cells, so lane l owns cell i = ilo(t) + l of anti-diagonal t.
+// Its three predecessors live on anti-diagonals t-1 (up, left) and t-2 (diag) in lanes
+// shifted by the (warp-uniform) change of ilo: three shuffles per step, no shared memory,
+// no barriers.  Lanes outside [ilo, ihi] hold +inf, which is what out-of-band reads must
+// see.  Same cell arithmetic as dtw_warp (cell_cost_add), so the fp64 result is identical.
+constexpr int kShflMaxReach = 30;
+
+template <typename T>
+__device__ T dtw_warp_shfl(const float* __restrict__ q, const float* __restrict__ c, int n, int r, int lane)
+{
+    const T INF = inf_of<T>();
+    T cur = INF, prev = INF;  // this lane's cell on anti-diagonals t-1 and t-2
+    int ilo1 = 0, ilo2 = 0;   // ilo(t-1), ilo(t-2)
+    for (int t = 0; t <= 2 * n - 2; ++t) {
+        const int ilo = max(max(0, t - (n - 1)), (t - r + 1) >> 1);
+        const int ihi = min(min(n - 1, t), (t + r) >> 1);
+        const int i = ilo + lane, j = t - i;
+        const int su = lane + (ilo - ilo1) - 1;  // (i-1, j)   on t-1
+        const int sl = lane + (ilo - ilo1);      // (i,   j-1) on t-1
+        const int sd = lane + (ilo - ilo2) - 1;  // (i-1, j-1) on t-2
+        T up = __shfl_sync(0xffffffffu, cur, su & 31);
+        T left = __shfl_sync(0xffffffffu, cur, sl & 31);
+        T diag = __shfl_sync(0xffffffffu, prev, sd & 31);
+        up = su >= 0 && su < 32 ? up : INF;
+        left = sl < 32 ? left : INF;
+        diag = sd >= 0 && sd < 32 ? diag : INF;
+        T mn = diag < up ? diag : up;
+        mn = left < mn ? left : mn;
+        if (t == 0) mn = (T)0;
+        const bool valid = i <= ihi;
+        const T val = valid ? cell_cost_add(q[valid ? i : 0], c[valid ? j : 0], mn) : INF;
+        prev = cur;
+        cur = val;
+        ilo2 = ilo1;
+        ilo1 = ilo;
+    }
+    return __shfl_sync(0xffffffffu, cur, 0);  // t = 2n-2: ilo = n-1, lane 0 holds D(n-1, n-1)
+}
+
+// Dispatch: register wavefront when the band fits a warp, shared-memory wavefront otherwise.
+template <typename T>
+__device__ __forceinline__ T dtw_warp_any(const float* __restrict__ q, const float* __restrict__ c, int n, int r,
+                                          T* buf, int lane)
+{
+    return r <= kShflMaxReach ? dtw_warp_shfl<T>(q, c, n, r, lane) : dtw_warp<T>(q, c, n, r, buf, lane);
+}
+
 // Raw LB_Keogh, squared, fp32, one warp: sum_i (c_i - U_i)^2 [c_i > U_i] +
 // (c_i - L_i)^2 [c_i < L_i].  Alg. 10 line LB_Keogh.
 __device__ __forceinline__ float lbk_warp(const float* __restrict__ U, const float* __restrict__ L,
@@ -116,39 +165,74 @@ __device__ __forceinline__ float lbk_warp(const float* __restrict__ U, const flo
 // Row i, band slot d <-> column j = i + d - R.  D[d] is updated in place left to right:
 // before the update D[d] = D(i-1, j-1), D[d+1] = D(i-1, j), `left` = D(i, j-1).  Columns
 // outside [0, n) read c = +inf, so their cells are +inf without branches.  Rows advance
-// four at a time over a sliding register window cw[e] = c[i - R + e], e < W + 3.
-// Early abandon (Alg. 10's "< BSF" test, exact for non-negative costs): after every 4 rows,
-// if min_d D > thr every warping path already exceeds thr.  Returns +inf when abandoned.
+// four at a time over a sliding register window cw[e] = c[i - R + e], e < W + 3; the four
+// columns entering the window each step come from two aligned float4 blocks held in
+// registers, the block after them being loaded one step ahead.
+// Early abandon (Alg. 10's "< BSF" test, exact for non-negative costs): after rows i..i+3
+// every warping path still has to cross row i+3 (>= its row minimum) and every column
+// j >= i+R+4 (>= that column's LB_Keogh term against the query envelope), so
+// the candidate is dropped when rowmin + (LBK_total - LBK of the columns seen) exceeds the
+// threshold (the UCR-suite cumulative bound, with fp32 margins of 2^-10).
 template <int R>
 struct DtwThread {
     static constexpr int W = 2 * R + 1;
     static constexpr int CW = W + 3;
+    static constexpr int T = R & 3;  // offset of column i+R+4 inside its float4 block
     float D[W + 1];
     float cw[CW];
+    float4 hold, h2;
+    float seen;     // sum of the LB_Keogh terms of the columns that entered the window
+    float seen_lo;  // the same before the last step's four columns: columns < i + R (i after step4)
     int i;
 
-    __device__ __forceinline__ void start(const float* __restrict__ c, int n)
+    __device__ __forceinline__ static float4 block(const float* __restrict__ c, int n, int b)
+    {
+        return (b >= 0 && 4 * b < n) ? __ldg(reinterpret_cast<const float4*>(c) + b)
+                                     : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+    }
+
+    __device__ __forceinline__ static float lbk_term(float v, float u, float l)
+    {
+        float d = v > u ? v - u : (v < l ? v - l : 0.0f);
+        return d * d;
+    }
+
+    __device__ __forceinline__ void start(const float* __restrict__ c, int n, const float* __restrict__ U,
+                                          const float* __restrict__ L)
     {
 #pragma unroll
         for (int d = 0; d <= W; ++d) D[d] = INFINITY;
         D[R] = 0.0f;  // virtual D(-1, -1) = 0 so that D(0, 0) = cost(0, 0)
+        constexpr int NB = (R + 4 + 3) / 4;  // blocks covering columns 0 .. R+3
+        float f[NB * 4];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            float4 v = block(c, n, b);
+            f[4 * b] = v.x; f[4 * b + 1] = v.y; f[4 * b + 2] = v.z; f[4 * b + 3] = v.w;
+        }
+        seen = 0.0f;
+        seen_lo = 0.0f;
 #pragma unroll
         for (int e = 0; e < CW; ++e) {
-            int j = e - R;
-            cw[e] = (j >= 0 && j < n) ? __ldg(c + j) : INFINITY;
+            const int j = e - R;
+            cw[e] = j < 0 ? INFINITY : f[j];
+            if (j >= 0 && j < n) seen += lbk_term(f[j], U[j], L[j]);
         }
+        hold = block(c, n, (R + 4) >> 2);
+        h2 = block(c, n, ((R + 4) >> 2) + 1);
         i = 0;
     }
 
-    // Four rows i..i+3; returns the row-minimum of the last one.
-    __device__ __forceinline__ float step4(const float* __restrict__ c, int n, const float* __restrict__ q_s)
+    // Rows i..i+3.  Returns min over the band of row i+3 (+inf cells included).
+    __device__ __forceinline__ float step4(const float* __restrict__ c, int n, const float* __restrict__ q_s,
+                                           const float* __restrict__ U, const float* __restrict__ L)
     {
+        const int p = i + R + 4;  // first column entering the window
+        const float4 nx4 = block(c, n, (p >> 2) + 2);  // for the next step
+        const float hv[8] = {hold.x, hold.y, hold.z, hold.w, h2.x, h2.y, h2.z, h2.w};
         float nx[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            int j = i + 4 + R + u;
-            nx[u] = j < n ? __ldg(c + j) : INFINITY;
-        }
+        for (int u = 0; u < 4; ++u) nx[u] = hv[T + u];
         const float4 qv = *reinterpret_cast<const float4*>(q_s + i);
         const float qq[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
@@ -165,10 +249,17 @@ struct DtwThread {
         float mn = D[0];
 #pragma unroll
         for (int d = 1; d < W; ++d) mn = fminf(mn, D[d]);
+        seen_lo = seen;
 #pragma unroll
         for (int e = 0; e < CW - 4; ++e) cw[e] = cw[e + 4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) cw[CW - 4 + u] = nx[u];
+        for (int u = 0; u < 4; ++u) {
+            cw[CW - 4 + u] = nx[u];
+            const int j = p + u;
+            if (j < n) seen += lbk_term(nx[u], U[j], L[j]);
+        }
+        hold = h2;
+        h2 = nx4;
         i += 4;
         return mn;
     }

@@ -3,6 +3,7 @@
 #pragma once
 #include "common.cuh"
 #include "dtw.cuh"
+#include "scan.cuh"
 
 namespace messi {
 
@@ -12,69 +13,205 @@ __device__ __forceinline__ void append_near(QState* st, NearEntry* near, unsigne
     near[pos] = NearEntry{id, d};
 }
 
-// ED refine (Alg. 9; Alg. 8 BSF update P:1178-1186): one warp per candidate.
-// Skip when the candidate's LB already exceeds the current BSF (the BSF has dropped since
-// the scan); else the fp32 squared ED; a result <= BSF*(1+eps) lowers the BSF (atomicMin,
-// the lock-free form of the paper's BSF lock) and joins the near-best list.
-__global__ void __launch_bounds__(256) k_refine_ed(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
-                                                   const uint2* __restrict__ cand, QState* st, NearEntry* near)
+// ED refine (Alg. 9; Alg. 8 BSF update P:1178-1186), one warp: the lanes set
+// in `pass` hold a candidate id each; their rows' fp32 squared ED are computed four at a
+// time (4 KB per warp in flight).  A result <= BSF*(1+eps) lowers the BSF (atomicMin: the
+// lock-free form of the paper's BSF lock) and joins the near-best list.
+constexpr int kRefineGroup = 4;
+
+__device__ void refine_ed_pass(unsigned pass, unsigned my_id, const float* __restrict__ rows, int n,
+                               const float* __restrict__ q_s, QState* st, NearEntry* near, int lane)
 {
-    extern __shared__ __align__(16) float q_s[];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
-    __syncthreads();
-    const unsigned total = *(volatile unsigned*)&st->cand_count;
-    const int lane = threadIdx.x & 31;
-    const unsigned wpb = blockDim.x >> 5;
-    unsigned refined = 0;
-    for (unsigned k = blockIdx.x * wpb + (threadIdx.x >> 5); k < total; k += gridDim.x * wpb) {
-        const uint2 e = cand[k];
-        float thr = slack_up(ld_bsf(st));
-        if (__uint_as_float(e.y) > thr) continue;
-        const float d = ed2_warp(q_s, rows + (long long)e.x * n, n, lane);
-        ++refined;
-        thr = slack_up(ld_bsf(st));
-        if (lane == 0 && d <= thr) {
-            bsf_update(st, d);
-            append_near(st, near, e.x, d);
+    while (pass) {
+        unsigned id[kRefineGroup];
+        bool ok[kRefineGroup];
+#pragma unroll
+        for (int g = 0; g < kRefineGroup; ++g) {
+            ok[g] = pass != 0;
+            const int src = ok[g] ? __ffs(pass) - 1 : 0;
+            pass &= pass - 1;
+            id[g] = __shfl_sync(0xffffffffu, my_id, src);
+        }
+        float acc[kRefineGroup];
+#pragma unroll
+        for (int g = 0; g < kRefineGroup; ++g) acc[g] = 0.0f;
+#pragma unroll 2
+        for (int j = lane * 4; j < n; j += 128) {
+            const float4 qv = *reinterpret_cast<const float4*>(q_s + j);
+            float4 cv[kRefineGroup];
+#pragma unroll
+            for (int g = 0; g < kRefineGroup; ++g)
+                cv[g] = ok[g] ? __ldg(reinterpret_cast<const float4*>(rows + (long long)id[g] * n + j))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int g = 0; g < kRefineGroup; ++g) {
+                float d;
+                d = qv.x - cv[g].x; acc[g] = fmaf(d, d, acc[g]);
+                d = qv.y - cv[g].y; acc[g] = fmaf(d, d, acc[g]);
+                d = qv.z - cv[g].z; acc[g] = fmaf(d, d, acc[g]);
+                d = qv.w - cv[g].w; acc[g] = fmaf(d, d, acc[g]);
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < kRefineGroup; ++g) acc[g] = warp_sum(acc[g]);
+        const float thr = slack_up(ld_bsf(st));
+#pragma unroll
+        for (int g = 0; g < kRefineGroup; ++g) {
+            if (ok[g] && lane == 0 && acc[g] <= thr) {
+                bsf_update(st, acc[g]);
+                append_near(st, near, id[g], acc[g]);
+            }
         }
     }
-    if (lane == 0 && refined) atomicAdd(&st->refined, refined);
 }
 
-// DTW step 1 (Alg. 10 line LB_Keogh): raw LB_Keogh of each scan survivor against
-// the query envelope; survivors with LBK <= BSF*(1+eps) go to list2.  One warp per
-// candidate, 32 candidates per round, one atomicAdd per round.
-__global__ void __launch_bounds__(256) k_lbk_filter(const float* __restrict__ rows, int n, const float* __restrict__ U_g,
-                                                    const float* __restrict__ L_g, const uint2* __restrict__ cand,
-                                                    QState* st, unsigned* __restrict__ list2)
+struct Best { double d; long long id; };
+__device__ void resolve_ed_block(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
+                                 const NearEntry* __restrict__ near, QState* st, long long N, long long row_begin,
+                                 void* result, void* stats, double* sq, int wuse);
+
+// Dynamic shared memory of k_fine_ed: fine table + q, and room for >= 1 warp of the resolve.
+__host__ __device__ inline size_t fine_ed_smem(int n)
+{
+    size_t a = (size_t)MESSI_W * MESSI_CARD * sizeof(float) + (size_t)((n + 3) & ~3) * sizeof(float);
+    size_t b = (size_t)n * sizeof(double);
+    return a > b ? a : b;
+}
+
+// The ED refine stage of one query (runs on the refine stream, overlapping the next
+// query's scan).  Each warp takes 32 coarse survivors at a time: each lane loads its
+// series' 8-bit iSAX row (16 B) and evaluates the exact lower bound (fine_lb, Property 1
+// P:1766-1771) against the CURRENT BSF; the survivors' real distances follow
+// (refine_ed_pass).  The last CTA to finish re-ranks the near-best set exactly and writes
+// the query's result (A9).  Shared memory: fine table (16 KB) + q (n floats), reused by
+// the resolve.
+__global__ void __launch_bounds__(256) k_fine_ed(const uint2* __restrict__ coarse, const uint4* __restrict__ symrows,
+                                                 const float* __restrict__ lut_g, const float* __restrict__ rows, int n,
+                                                 const float* __restrict__ q_g, QState* st, NearEntry* near,
+                                                 long long N, long long row_begin, void* result, void* stats)
+{
+    extern __shared__ __align__(16) float fsm[];
+    float* T = fsm;
+    float* q_s = fsm + MESSI_W * MESSI_CARD;
+    for (int i = threadIdx.x; i < MESSI_W * MESSI_CARD; i += blockDim.x) T[i] = lut_g[i];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
+    __syncthreads();
+    const unsigned total = *(volatile unsigned*)&st->coarse_count;
+    const int lane = threadIdx.x & 31;
+    const unsigned wpb = blockDim.x >> 5;
+    unsigned n_fine = 0, n_ref = 0;
+    for (unsigned k0 = (blockIdx.x * wpb + (threadIdx.x >> 5)) * 32; k0 < total; k0 += gridDim.x * wpb * 32) {
+        const bool valid = k0 + lane < total;
+        const uint2 e = valid ? coarse[k0 + lane] : make_uint2(0u, 0x7f800000u);
+        const float thr = slack_up(ld_bsf(st));
+        bool ok = valid && __uint_as_float(e.y) <= thr;
+        if (ok) ok = fine_lb(symrows[e.x], T) <= thr;
+        const unsigned pass = __ballot_sync(0xffffffffu, ok);
+        n_fine += __popc(pass);
+        n_ref += __popc(pass);
+        refine_ed_pass(pass, e.x, rows, n, q_s, st, near, lane);
+    }
+    if (lane == 0 && n_fine) {
+        atomicAdd(&st->cand_count, n_fine);
+        atomicAdd(&st->refined, n_ref);
+    }
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&st->done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    extern __shared__ __align__(16) double dsq[];
+    int wuse = (int)(fine_ed_smem(n) / ((size_t)n * sizeof(double)));
+    wuse = wuse < 1 ? 1 : (wuse > (int)wpb ? (int)wpb : wuse);
+    resolve_ed_block(rows, n, q_g, near, st, N, row_begin, result, stats, dsq, wuse);
+}
+
+// DTW step 1 (Alg. 10 lines LowerBound_DTW_SIMD and LB_Keogh): each coarse
+// survivor first gets the exact 8-bit envelope-PAA bound from its symbol row; those with
+// LB <= BSF*(1+eps) (counted as candidates) get the raw LB_Keogh against the query
+// envelope, four rows in flight per warp; survivors go to list2 as (id, LBK).
+__global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ coarse, const uint4* __restrict__ symrows,
+                                                    const float* __restrict__ lut_g, const float* __restrict__ rows, int n,
+                                                    const float* __restrict__ U_g, const float* __restrict__ L_g,
+                                                    QState* st, uint2* __restrict__ list2)
 {
     extern __shared__ __align__(16) float env[];
-    float* U = env;
-    float* L = env + ((n + 3) & ~3);
+    float* T = env;
+    float* U = env + MESSI_W * MESSI_CARD;
+    float* L = U + ((n + 3) & ~3);
+    for (int i = threadIdx.x; i < MESSI_W * MESSI_CARD; i += blockDim.x) T[i] = lut_g[i];
     for (int i = threadIdx.x; i < n; i += blockDim.x) { U[i] = U_g[i]; L[i] = L_g[i]; }
     __syncthreads();
-    const unsigned total = *(volatile unsigned*)&st->cand_count;
+    const unsigned total = *(volatile unsigned*)&st->coarse_count;
     const int lane = threadIdx.x & 31;
     const unsigned wpb = blockDim.x >> 5;
     const float thr = slack_up(ld_bsf(st));
+    unsigned n_fine = 0;
     for (unsigned k0 = (blockIdx.x * wpb + (threadIdx.x >> 5)) * 32; k0 < total; k0 += gridDim.x * wpb * 32) {
-        const unsigned cnt = min(32u, total - k0);
-        const uint2 mine = lane < (int)cnt ? cand[k0 + lane] : make_uint2(0, 0x7f800000u);
-        unsigned pass = 0;
-        for (unsigned j = 0; j < cnt; ++j) {
-            const unsigned id = __shfl_sync(0xffffffffu, mine.x, j);
-            const float lb = __uint_as_float(__shfl_sync(0xffffffffu, mine.y, j));
-            if (lb > thr) continue;
-            const float v = lbk_warp(U, L, rows + (long long)id * n, n, lane);
-            if (v <= thr) pass |= 1u << j;
+        const bool valid = k0 + lane < total;
+        const uint2 e = valid ? coarse[k0 + lane] : make_uint2(0u, 0x7f800000u);
+        bool ok = valid && __uint_as_float(e.y) <= thr;
+        if (ok) ok = fine_lb(symrows[e.x], T) <= thr;
+        unsigned todo = __ballot_sync(0xffffffffu, ok);
+        n_fine += __popc(todo);
+        unsigned passmask = 0;
+        float mylbk = 0.0f;
+        while (todo) {
+            int src[kRefineGroup];
+            unsigned id[kRefineGroup];
+            bool gok[kRefineGroup];
+#pragma unroll
+            for (int g = 0; g < kRefineGroup; ++g) {
+                gok[g] = todo != 0;
+                src[g] = gok[g] ? __ffs(todo) - 1 : 0;
+                todo &= todo - 1;
+                id[g] = __shfl_sync(0xffffffffu, e.x, src[g]);
+            }
+            float acc[kRefineGroup];
+#pragma unroll
+            for (int g = 0; g < kRefineGroup; ++g) acc[g] = 0.0f;
+#pragma unroll 2
+            for (int j = lane * 4; j < n; j += 128) {
+                const float4 uv = *reinterpret_cast<const float4*>(U + j);
+                const float4 lv = *reinterpret_cast<const float4*>(L + j);
+                const float u[4] = {uv.x, uv.y, uv.z, uv.w}, l[4] = {lv.x, lv.y, lv.z, lv.w};
+                float4 cv[kRefineGroup];
+#pragma unroll
+                for (int g = 0; g < kRefineGroup; ++g)
+                    cv[g] = gok[g] ? __ldg(reinterpret_cast<const float4*>(rows + (long long)id[g] * n + j))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int g = 0; g < kRefineGroup; ++g) {
+                    const float c[4] = {cv[g].x, cv[g].y, cv[g].z, cv[g].w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        float d = c[k] > u[k] ? c[k] - u[k] : (c[k] < l[k] ? c[k] - l[k] : 0.0f);
+                        acc[g] = fmaf(d, d, acc[g]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < kRefineGroup; ++g) {
+                acc[g] = warp_sum(acc[g]);
+                if (gok[g] && acc[g] <= thr) {
+                    passmask |= 1u << src[g];
+                    if (lane == src[g]) mylbk = acc[g];
+                }
+            }
         }
-        if (pass) {
+        if (passmask) {
             unsigned base = 0;
-            if (lane == 0) base = atomicAdd(&st->list2_count, (unsigned)__popc(pass));
+            if (lane == 0) base = atomicAdd(&st->list2_count, (unsigned)__popc(passmask));
             base = __shfl_sync(0xffffffffu, base, 0);
-            if (pass & (1u << lane)) list2[base + __popc(pass & ((1u << lane) - 1))] = mine.x;
+            if (passmask & (1u << lane))
+                list2[base + __popc(passmask & ((1u << lane) - 1))] = make_uint2(e.x, __float_as_uint(mylbk));
         }
     }
+    if (lane == 0 && n_fine) atomicAdd(&st->cand_count, n_fine);
 }
 
 // DTW step 2 (Alg. 10 line RealDist, P:1425 / P:1453 "true DTW distance"): banded fp32
@@ -83,10 +220,15 @@ __global__ void __launch_bounds__(256) k_lbk_filter(const float* __restrict__ ro
 // a lane that abandons early simply starts its next candidate.
 template <int R>
 __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
-                                                    const unsigned* __restrict__ list2, QState* st, NearEntry* near)
+                                                    const float* __restrict__ U_g, const float* __restrict__ L_g,
+                                                    const uint2* __restrict__ list2, QState* st, NearEntry* near)
 {
-    extern __shared__ __align__(16) float q_s[];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
+    extern __shared__ __align__(16) float dsm[];
+    const int npad = (n + 3) & ~3;
+    float* q_s = dsm;
+    float* U = dsm + npad;
+    float* L = dsm + 2 * npad;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) { q_s[i] = q_g[i]; U[i] = U_g[i]; L[i] = L_g[i]; }
     __syncthreads();
     const unsigned total = *(volatile unsigned*)&st->list2_count;
     const unsigned nthreads = gridDim.x * blockDim.x;
@@ -95,20 +237,34 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
     bool have = k < total;
     const float* c = rows;
     unsigned id = 0, refined = 0, abandoned = 0;
+    float lbk_total = 0.0f;
+    // the lane's next candidate is fetched one candidate ahead and the head of its row
+    // prefetched, so a lane that restarts does not stall its warp on an HBM round trip
+    uint2 nxt = k + nthreads < total ? list2[k + nthreads] : make_uint2(0u, 0u);
+    auto prefetch_row = [&](unsigned rid) {
+        const char* pr = reinterpret_cast<const char*>(rows + (long long)rid * n);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(pr));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(pr + 128));
+    };
+    if (k + nthreads < total) prefetch_row(nxt.x);
     if (have) {
-        id = list2[k];
+        const uint2 e = list2[k];
+        id = e.x;
+        lbk_total = __uint_as_float(e.y);
         c = rows + (long long)id * n;
-        dp.start(c, n);
+        dp.start(c, n, U, L);
         ++refined;
     }
     float thr = slack_up(ld_bsf(st));
     while (__any_sync(0xffffffffu, have)) {
         if (have) {
-            const float rowmin = dp.step4(c, n, q_s);
+            const float rowmin = dp.step4(c, n, q_s, U, L);
+            const float tail = fmaxf(0.0f, lbk_total * 0.9990234375f - dp.seen_lo * 1.0009765625f);
+            const float bound = (rowmin + tail) * 0.9990234375f;
             bool done = false;
-            if (rowmin > thr) {
+            if (bound > thr) {
                 thr = slack_up(ld_bsf(st));
-                if (rowmin > thr) { done = true; ++abandoned; }
+                if (bound > thr) { done = true; ++abandoned; }
             }
             if (!done && dp.i >= n) {
                 done = true;
@@ -123,9 +279,14 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
                 k += nthreads;
                 have = k < total;
                 if (have) {
-                    id = list2[k];
+                    id = nxt.x;
+                    lbk_total = __uint_as_float(nxt.y);
                     c = rows + (long long)id * n;
-                    dp.start(c, n);
+                    if (k + nthreads < total) {
+                        nxt = list2[k + nthreads];
+                        prefetch_row(nxt.x);
+                    }
+                    dp.start(c, n, U, L);
                     ++refined;
                     thr = slack_up(ld_bsf(st));
                 }
@@ -140,22 +301,34 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
     }
 }
 
+// Stage one row into a warp's shared buffer (float4, n % 4 == 0).
+__device__ __forceinline__ void stage_row(float* dst, const float* __restrict__ src, int n, int lane)
+{
+    for (int j = lane * 4; j < n; j += 128)
+        *reinterpret_cast<float4*>(dst + j) = __ldg(reinterpret_cast<const float4*>(src + j));
+    __syncwarp();
+}
+
 // DTW step 2 for reaches without a register-band instantiation: one warp per candidate,
-// fp32 anti-diagonal wavefront (dtw_warp<float>).
+// fp32 anti-diagonal wavefront (dtw_warp<float>) over the row staged in shared memory.
+// Per-warp shared memory: n floats of row + 3n floats of anti-diagonals.
 __global__ void k_refine_dtw_warp(const float* __restrict__ rows, int n, int reach, const float* __restrict__ q_g,
-                                  const unsigned* __restrict__ list2, QState* st, NearEntry* near)
+                                  const uint2* __restrict__ list2, QState* st, NearEntry* near)
 {
     extern __shared__ __align__(16) float dsm[];
+    const int npad = (n + 3) & ~3;
     float* q_s = dsm;
     for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-    float* buf = dsm + ((n + 3) & ~3) + w * 3 * n;
+    float* c_s = dsm + npad + (size_t)w * 4 * npad;
+    float* buf = c_s + npad;
     const unsigned total = *(volatile unsigned*)&st->list2_count;
     unsigned refined = 0;
     for (unsigned k = blockIdx.x * wpb + w; k < total; k += gridDim.x * wpb) {
-        const unsigned id = list2[k];
-        const float d = dtw_warp<float>(q_s, rows + (long long)id * n, n, reach, buf, lane);
+        const unsigned id = list2[k].x;
+        stage_row(c_s, rows + (long long)id * n, n, lane);
+        const float d = dtw_warp_any<float>(q_s, c_s, n, reach, buf, lane);
         ++refined;
         const float thr = slack_up(ld_bsf(st));
         if (lane == 0 && d <= thr) {
@@ -167,7 +340,6 @@ __global__ void k_refine_dtw_warp(const float* __restrict__ rows, int n, int rea
 }
 
 // ------------------------------------------------------------------- exact resolution
-struct Best { double d; long long id; };
 
 __device__ __forceinline__ bool better(double d, long long id, double bd, long long bid)
 {
@@ -179,7 +351,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
                              void* result, void* stats)
 {
     struct R { double dist; long long id; double d2; long long reserved; };
-    struct S { long long lb, cand, lbk, refined, abandoned, near; double seed, bsf; };
+    struct S { long long lb, coarse, cand, lbk, refined, abandoned, near; double seed, bsf; };
     R* res = reinterpret_cast<R*>(result);
     res->dist = b.id >= 0 ? sqrt(b.d) : (double)INFINITY;
     res->id = b.id >= 0 ? row_begin + b.id : -1;
@@ -188,6 +360,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
     if (stats) {
         S* s = reinterpret_cast<S*>(stats);
         s->lb = N;
+        s->coarse = st->coarse_count;
         s->cand = st->cand_count;
         s->lbk = st->list2_count;
         s->refined = st->refined;
@@ -226,44 +399,73 @@ __device__ Best block_best(Best b, int* cnt_io)
 
 // ED: every near-best entry with d32 <= BSF_final*(1+eps) is recomputed canonically in
 // fp64; the lexicographic min over (d64, id) is the answer (reading R11/R12; Thm. 2
-// P:1881-1913 exactness).  One CTA.
-__global__ void __launch_bounds__(256) k_resolve_ed(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
-                                                    const NearEntry* __restrict__ near, QState* st, long long N,
-                                                    long long row_begin, void* result, void* stats)
+// P:1881-1913 exactness).  One CTA, one warp per entry: the warp stages the fp64 squared
+// differences in shared memory (elementwise, order-free), lane 0 sums them in index order
+// -- the oracle's sequential operation sequence.  `sq` holds n doubles per used warp.
+__device__ void resolve_ed_block(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
+                                 const NearEntry* __restrict__ near, QState* st, long long N, long long row_begin,
+                                 void* result, void* stats, double* sq, int wuse)
 {
     const float thr = slack_up(ld_bsf(st));
     const unsigned total = *(volatile unsigned*)&st->near_count;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     Best b{(double)INFINITY, -1};
     int cnt = 0;
-    for (unsigned k = threadIdx.x; k < total; k += blockDim.x) {
-        const NearEntry e = near[k];
-        if (!(e.d32 <= thr)) continue;
-        ++cnt;
-        const double d = ed2_exact(q_g, rows + (long long)e.id * n, n);
-        if (better(d, e.id, b.d, b.id)) { b.d = d; b.id = e.id; }
+    if (w < wuse) {
+        double* mine = sq + (size_t)w * n;
+        for (unsigned k = w; k < total; k += wuse) {
+            const NearEntry e = near[k];
+            if (!(e.d32 <= thr)) continue;
+            const float* c = rows + (long long)e.id * n;
+            for (int i = lane; i < n; i += 32) {
+                double d = __dsub_rn((double)q_g[i], (double)c[i]);
+                mine[i] = __dmul_rn(d, d);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                ++cnt;
+                double sum = 0.0;
+                for (int i = 0; i < n; ++i) sum = __dadd_rn(sum, mine[i]);
+                if (better(sum, e.id, b.d, b.id)) { b.d = sum; b.id = e.id; }
+            }
+            __syncwarp();
+        }
     }
     b = block_best(b, &cnt);
     if (threadIdx.x == 0) finish_query(b, (unsigned)cnt, st, N, row_begin, result, stats);
 }
 
+__global__ void k_resolve_ed(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
+                             const NearEntry* __restrict__ near, QState* st, long long N, long long row_begin,
+                             void* result, void* stats)
+{
+    extern __shared__ __align__(16) double sq[];
+    resolve_ed_block(rows, n, q_g, near, st, N, row_begin, result, stats, sq, blockDim.x >> 5);
+}
+
 // DTW: same, with the fp64 warp wavefront (bit-identical to the row-by-row DP of the
-// oracle: every cell is fl(fl(d*d) + min) whatever the order).  buf: 3*n doubles per warp.
+// oracle: every cell is fl(fl(d*d) + min) whatever the order).  Per-warp shared memory:
+// q and the row (2n floats) + 3n doubles.
 __global__ void k_resolve_dtw(const float* __restrict__ rows, int n, int reach, const float* __restrict__ q_g,
                               const NearEntry* __restrict__ near, QState* st, long long N, long long row_begin,
                               void* result, void* stats)
 {
     extern __shared__ __align__(16) double dbuf[];
+    const int npad = (n + 3) & ~3;
     const float thr = slack_up(ld_bsf(st));
     const unsigned total = *(volatile unsigned*)&st->near_count;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-    double* buf = dbuf + (size_t)w * 3 * n;
+    double* buf = dbuf + (size_t)w * (3 * n + npad);
+    float* qc = reinterpret_cast<float*>(buf + 3 * n);  // q then c
+    for (int i = lane; i < n; i += 32) qc[i] = q_g[i];
     Best b{(double)INFINITY, -1};
     int cnt = 0;
     for (unsigned k = w; k < total; k += wpb) {
         const NearEntry e = near[k];
         if (!(e.d32 <= thr)) continue;
         if (lane == 0) ++cnt;
-        const double d = dtw_warp<double>(q_g, rows + (long long)e.id * n, n, reach, buf, lane);
+        stage_row(qc + npad, rows + (long long)e.id * n, n, lane);
+        const double d = dtw_warp_any<double>(qc, qc + npad, n, reach, buf, lane);
         if (better(d, e.id, b.d, b.id)) { b.d = d; b.id = e.id; }
     }
     b = block_best(b, &cnt);
@@ -275,6 +477,7 @@ __global__ void k_arm(QState* st) { arm_state(st); }
 // --------------------------------------------------------------------- inspection
 // Per id: refine-kernel fp32 distance (no abandoning), exact fp64 distance, and (DTW) the
 // fp32 LB_Keogh -- the same device routines the query path runs.  One warp per id.
+// Shared memory: q, U, L (3 npad floats) + per warp: row (npad floats) + 3n doubles.
 template <int R>
 __global__ void k_debug_dist(const float* __restrict__ rows, int n, int reach, const float* __restrict__ q_g,
                              const float* __restrict__ U_g, const float* __restrict__ L_g,
@@ -286,7 +489,8 @@ __global__ void k_debug_dist(const float* __restrict__ rows, int n, int reach, c
     float* U = dsm + npad;
     float* L = dsm + 2 * npad;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-    double* buf = reinterpret_cast<double*>(dsm + 3 * npad) + (size_t)w * 3 * n;
+    float* c_s = dsm + 3 * npad + (size_t)w * (npad + 6 * n);
+    double* buf = reinterpret_cast<double*>(c_s + npad);
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         q_s[i] = q_g[i];
         if (reach >= 0) { U[i] = U_g[i]; L[i] = L_g[i]; }
@@ -294,11 +498,12 @@ __global__ void k_debug_dist(const float* __restrict__ rows, int n, int reach, c
     __syncthreads();
     for (int t = blockIdx.x * wpb + w; t < k; t += gridDim.x * wpb) {
         const float* c = rows + (long long)ids[t] * n;
+        stage_row(c_s, c, n, lane);
         if (reach < 0) {
             float v = ed2_warp(q_s, c, n, lane);
             if (lane == 0) {
                 if (d32) d32[t] = v;
-                if (d64) d64[t] = ed2_exact(q_s, c, n);
+                if (d64) d64[t] = ed2_exact(q_s, c_s, n);
             }
         } else {
             if (lbk) {
@@ -306,7 +511,7 @@ __global__ void k_debug_dist(const float* __restrict__ rows, int n, int reach, c
                 if (lane == 0) lbk[t] = v;
             }
             if (d64) {
-                double v = dtw_warp<double>(q_s, c, n, reach, buf, lane);
+                double v = dtw_warp_any<double>(q_s, c_s, n, reach, buf, lane);
                 if (lane == 0) d64[t] = v;
             }
             if (d32) {
@@ -315,16 +520,17 @@ __global__ void k_debug_dist(const float* __restrict__ rows, int n, int reach, c
                     v = INFINITY;
                     if (lane == 0) {
                         DtwThread<(R >= 0 ? R : 0)> dp;
-                        dp.start(c, n);
-                        while (dp.i < n) dp.step4(c, n, q_s);
+                        dp.start(c, n, U, L);
+                        while (dp.i < n) dp.step4(c, n, q_s, U, L);
                         v = dp.result();
                     }
                 } else {
-                    v = dtw_warp<float>(q_s, c, n, reach, reinterpret_cast<float*>(buf), lane);
+                    v = dtw_warp_any<float>(q_s, c_s, n, reach, reinterpret_cast<float*>(buf), lane);
                 }
                 if (lane == 0) d32[t] = v;
             }
         }
+        __syncwarp();
     }
 }
 

@@ -17,7 +17,7 @@ namespace messi {
 __device__ void prologue_block(const float* __restrict__ q, int n, int reach, const float* __restrict__ beta_g,
                                const float* __restrict__ lo_w, const float* __restrict__ hi_w,
                                float* __restrict__ lut_g, float* __restrict__ U_g, float* __restrict__ L_g,
-                               unsigned long long* key_out)
+                               unsigned long long* key_out, float* __restrict__ lut2_g)
 {
     __shared__ double ubar[MESSI_W], lbar[MESSI_W];
     __shared__ float beta[256];
@@ -67,6 +67,16 @@ __device__ void prologue_block(const float* __restrict__ q, int n, int reach, co
             double d = fmax(0.0, fmax(lo - ubar[s], lbar[s] - hi));
             lut_g[i] = __double2float_rd(md * d * d);
         }
+        // coarse table over nibble pairs: T2[p][h1 << 4 | h2] = the same bound at cardinality
+        // 16 (box of top nibble h = union of the 16 fine boxes 16h .. 16h+15) for segments
+        // 2p and 2p+1, summed in fp64 and rounded down: T2 <= T[2p][v1] + T[2p+1][v2].
+        for (int i = tid; i < MESSI_PAIRS * MESSI_CARD; i += blockDim.x) {
+            int pr = i >> 8, h1 = (i >> 4) & 15, hh = i & 15;
+            int s1 = 2 * pr, s2 = 2 * pr + 1;
+            double d1 = fmax(0.0, fmax((double)lo_w[16 * h1] - ubar[s1], lbar[s1] - (double)hi_w[16 * h1 + 15]));
+            double d2 = fmax(0.0, fmax((double)lo_w[16 * hh] - ubar[s2], lbar[s2] - (double)hi_w[16 * hh + 15]));
+            lut2_g[i] = __double2float_rd(md * d1 * d1 + md * d2 * d2);
+        }
     }
 }
 
@@ -102,13 +112,13 @@ __global__ void __launch_bounds__(256) k_seed_ed(const float* __restrict__ q_g, 
                                                  const unsigned* __restrict__ perm, long long N, int window,
                                                  const float* __restrict__ beta_g, const float* __restrict__ lo_w,
                                                  const float* __restrict__ hi_w, float* __restrict__ lut_g,
-                                                 QState* st)
+                                                 float* __restrict__ lut2_g, QState* st)
 {
     extern __shared__ __align__(16) float q_s[];
     __shared__ unsigned long long qkey_s;
     for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
     __syncthreads();
-    prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, blockIdx.x == 0 ? lut_g : nullptr, nullptr, nullptr, &qkey_s);
+    prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, blockIdx.x == 0 ? lut_g : nullptr, nullptr, nullptr, &qkey_s, lut2_g);
     __syncthreads();
     const unsigned long long qkey = qkey_s;
     long long a = block_lower_bound(skey, N, qkey);
@@ -132,12 +142,14 @@ __global__ void __launch_bounds__(256) k_seed_ed(const float* __restrict__ q_g, 
 }
 
 // DTW seed: prologue (envelope, envelope PAA, table) in CTA 0, then the window rows' fp32
-// banded DTW, one warp per row (anti-diagonal wavefront, dtw.cuh).
+// banded DTW, one warp per row (anti-diagonal wavefront, dtw.cuh) over the row staged in
+// shared memory.  Dynamic shared memory: q (npad) + per warp row (npad) + 3n floats.
 __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, const float* __restrict__ rows,
                            const unsigned long long* __restrict__ skey, const unsigned* __restrict__ perm,
                            long long N, int window, const float* __restrict__ beta_g,
                            const float* __restrict__ lo_w, const float* __restrict__ hi_w,
-                           float* __restrict__ lut_g, float* __restrict__ U_g, float* __restrict__ L_g, QState* st)
+                           float* __restrict__ lut_g, float* __restrict__ U_g, float* __restrict__ L_g,
+                           float* __restrict__ lut2_g, QState* st)
 {
     extern __shared__ __align__(16) float dsm[];
     float* q_s = dsm;
@@ -145,9 +157,9 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
     for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
     __syncthreads();
     if (blockIdx.x == 0)
-        prologue_block(q_s, n, reach, beta_g, lo_w, hi_w, lut_g, U_g, L_g, &qkey_s);
+        prologue_block(q_s, n, reach, beta_g, lo_w, hi_w, lut_g, U_g, L_g, &qkey_s, lut2_g);
     else
-        prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, nullptr, nullptr, nullptr, &qkey_s);
+        prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, nullptr, nullptr, nullptr, &qkey_s, nullptr);
     __syncthreads();
     const unsigned long long qkey = qkey_s;
     long long a = block_lower_bound(skey, N, qkey);
@@ -159,11 +171,16 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
         st->window_len = len;
     }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-    float* buf = dsm + ((n + 3) & ~3) + w * 3 * n;
+    const int npad = (n + 3) & ~3;
+    float* c_s = dsm + npad + (size_t)w * (npad + 3 * n);
+    float* buf = c_s + npad;
     float best = INFINITY;
     for (int k = blockIdx.x * wpb + w; k < len; k += gridDim.x * wpb) {
-        const float* c = rows + (long long)perm[start + k] * n;
-        best = fminf(best, dtw_warp<float>(q_s, c, n, reach, buf, lane));
+        for (int j = lane * 4; j < n; j += 128)
+            *reinterpret_cast<float4*>(c_s + j) =
+                __ldg(reinterpret_cast<const float4*>(rows + (long long)perm[start + k] * n + j));
+        __syncwarp();
+        best = fminf(best, dtw_warp_any<float>(q_s, c_s, n, reach, buf, lane));
     }
     if (lane == 0 && best < INFINITY) {
         bsf_update(st, best);
@@ -172,86 +189,110 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
 }
 
 // ---------------------------------------------------------------------- lower-bound scan
-// Every series' lower bound LB = sum_s T[s][sym_s] (round-down adds), kept iff
-// LB <= BSF0 * (1 + eps): Alg. 9 line LowerBound_SIMD / Alg. 10 line
-// LowerBound_DTW_SIMD over the whole summary array, like ParIS+'s SIMS scan
-// (P:432-443).  Shared-memory LUT, 64 KB: word v*64 + 16h + s holds T[s][v]; the lane that
-// owns block b = 2p + h reads segment s = (t + p) mod 16 at step t, so the 32 lanes hit 32
-// distinct banks for any symbol values.  PRMT builds the byte address (v << 8 | base) from
-// the packed symbols in one instruction.  Survivors are compacted with a warp ballot/scan
-// and one atomicAdd per warp-tile.  WRITE_ALL (inspection) writes every LB instead.
-template <bool WRITE_ALL>
+// The HBM-roofline step (A5): Alg. 9 line LowerBound_SIMD / Alg. 10 line
+// LowerBound_DTW_SIMD evaluated for EVERY series, like ParIS+'s SIMS scan
+// (P:432-443), in two resolutions of the same iSAX word.  This kernel streams the coarse
+// tiles (8 B per series: top nibbles, two segments per byte) and sums, per series, the 8
+// pair-table entries T2[p][byte] (round-down adds) -- the iSAX lower bound at cardinality
+// 16, which never exceeds the 8-bit one.  Series with coarse LB <= BSF*(1+eps) go to a
+// global list (warp ballot + prefix + one atomicAdd per warp-tile); the exact 8-bit bound
+// is applied to them by the refine stage (k_fine_ed / k_lbk_filter).
+// Shared-memory table: 64 KB, word v*64 + 8c + p holds T2[p][v] (4 copies c); the lane
+// owning block b reads pair p = (t + b) mod 8 at step t and uses copy c = b >> 3, so the 32
+// lanes hit 32 distinct banks for any byte values.  PRMT builds the byte address
+// (v << 8 | base) from the packed pair bytes in one instruction.
+//   SCAN_COMPACT: survivors -> global list;   SCAN_ALL: every coarse LB written (inspection).
+enum { SCAN_COMPACT = 0, SCAN_ALL = 1 };
+constexpr int kScanWarps = 8;
+constexpr size_t kScanLutBytes = (size_t)MESSI_CARD * 64 * sizeof(float);
+
+template <int MODE>
 __global__ void __launch_bounds__(256, 2) k_scan(const uint4* __restrict__ tiles, long long ntiles, long long N,
-                                                 const float* __restrict__ lut_g, QState* st,
-                                                 uint2* __restrict__ cand, float* __restrict__ lb_all)
+                                                 const float* __restrict__ lut2_g, QState* st,
+                                                 uint2* __restrict__ out, float* __restrict__ lb_all)
 {
     extern __shared__ __align__(16) float lut_s[];  // 256 * 64 floats
-    for (int i = threadIdx.x; i < MESSI_W * MESSI_CARD; i += blockDim.x) {
-        int s = i >> 8, v = i & 255;
-        float val = lut_g[i];
-        lut_s[v * 64 + s] = val;
-        lut_s[v * 64 + 16 + s] = val;
+    for (int i = threadIdx.x; i < MESSI_PAIRS * MESSI_CARD; i += blockDim.x) {
+        const int pr = i >> 8, v = i & 255;
+        const float val = lut2_g[i];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) lut_s[v * 64 + 8 * c + pr] = val;
     }
     __syncthreads();
-    const float thr = WRITE_ALL ? INFINITY : slack_up(ld_bsf(st));
+    const float thr = MODE == SCAN_ALL ? INFINITY : slack_up(ld_bsf(st));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int p = lane >> 1, h = lane & 1;
+    const int cpy = lane >> 3;
     const char* lbase = reinterpret_cast<const char*>(lut_s);
-    for (long long tl = (long long)blockIdx.x * 8 + warp; tl < ntiles; tl += (long long)gridDim.x * 8) {
+    for (long long tl = (long long)blockIdx.x * kScanWarps + warp; tl < ntiles; tl += (long long)gridDim.x * kScanWarps) {
         const uint4* tp = tiles + tl * (MESSI_TILE_BYTES / 16) + lane;
-        uint4 data[16];
+        uint4 data[8];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) data[t] = __ldcs(tp + t * 32);
+        for (int t = 0; t < 8; ++t) data[t] = __ldcs(tp + t * 32);
         float acc[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) acc[k] = 0.0f;
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-            const unsigned base = (unsigned)((16 * h + ((t + p) & 15)) * 4);
+        for (int t = 0; t < 8; ++t) {
+            const unsigned base = (unsigned)((8 * cpy + ((t + lane) & 7)) * 4);
             const unsigned wv[4] = {data[t].x, data[t].y, data[t].z, data[t].w};
 #pragma unroll
             for (int wi = 0; wi < 4; ++wi) {
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                    unsigned addr = __byte_perm(wv[wi], base, 0x5504 | (b << 4));
+                    const unsigned addr = __byte_perm(wv[wi], base, 0x5504 | (b << 4));
                     acc[wi * 4 + b] = __fadd_rd(acc[wi * 4 + b], *reinterpret_cast<const float*>(lbase + addr));
                 }
             }
         }
         const long long id0 = tl * MESSI_TILE_ROWS + lane * 16;
-        if (WRITE_ALL) {
+        if (MODE == SCAN_ALL) {
 #pragma unroll
             for (int k = 0; k < 16; ++k)
                 if (id0 + k < N) lb_all[id0 + k] = acc[k];
-        } else {
-            unsigned mask = 0;
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-                if (acc[k] <= thr && id0 + k < N) mask |= 1u << k;
-            if (__any_sync(0xffffffffu, mask)) {
-                int cnt = __popc(mask), incl = cnt;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    int y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                int total = __shfl_sync(0xffffffffu, incl, 31);
-                unsigned base = 0;
-                if (lane == 0) base = atomicAdd(&st->cand_count, (unsigned)total);
-                base = __shfl_sync(0xffffffffu, base, 0);
-                unsigned pos = base + incl - cnt;
-                while (mask) {
-                    int k = __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    float lb = 0.0f;
-#pragma unroll
-                    for (int kk = 0; kk < 16; ++kk)
-                        if (kk == k) lb = acc[kk];
-                    cand[pos++] = make_uint2((unsigned)(id0 + k), __float_as_uint(lb));
-                }
-            }
+            continue;
         }
+        unsigned mask = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (acc[k] <= thr && id0 + k < N) mask |= 1u << k;
+        if (!__any_sync(0xffffffffu, mask)) continue;
+        const int cnt = __popc(mask);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(&st->coarse_count, (unsigned)total);
+        unsigned pos = __shfl_sync(0xffffffffu, base, 0) + incl - cnt;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (mask & (1u << k)) out[pos++] = make_uint2((unsigned)(id0 + k), __float_as_uint(acc[k]));
     }
+}
+
+// Exact (8-bit) lower bound of one series from its symbol row: sum_s T[s][sym_s], s in
+// order, round-down adds.  T: the fine table [16][256] in shared memory.
+__device__ __forceinline__ float fine_lb(uint4 sr, const float* __restrict__ T)
+{
+    const unsigned w[4] = {sr.x, sr.y, sr.z, sr.w};
+    float acc = 0.0f;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) acc = __fadd_rd(acc, T[s * 256 + ((w[s >> 2] >> (8 * (s & 3))) & 255u)]);
+    return acc;
+}
+
+// Inspection: the fine bound of every row (one thread per row).
+__global__ void k_fine_all(const uint4* __restrict__ symrows, long long N, const float* __restrict__ lut_g,
+                           float* __restrict__ lb_all)
+{
+    __shared__ float T[MESSI_W * MESSI_CARD];
+    for (int i = threadIdx.x; i < MESSI_W * MESSI_CARD; i += blockDim.x) T[i] = lut_g[i];
+    __syncthreads();
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += (long long)gridDim.x * blockDim.x)
+        lb_all[r] = fine_lb(symrows[r], T);
 }
 
 }  // namespace messi

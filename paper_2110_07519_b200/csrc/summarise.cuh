@@ -27,16 +27,21 @@ __global__ void k_breakpoints(float* beta32, float* lo_w, float* hi_w)
     hi_w[v] = v == 255 ? INFINITY : nextafterf(b[v], INFINITY);
 }
 
-// Tile layout of the symbols (what the LB scan streams).  A tile holds 512 consecutive
-// rows = 32 blocks of 16 rows; block b = 2p + h (pair p = b>>1, half h = b&1).  Tile row t
-// (512 B) holds, for every block b, the 16 symbols of segment s = (t + p) mod 16 of that
-// block's 16 rows at byte offset 16*b.  So one warp reading tile row t with lane b loading
-// 16 B gets 16 different segments across the 16 pairs -- what makes the LUT lookups of the
-// scan bank-conflict free -- while the warp's load is one contiguous 512 B line set.
-__device__ __forceinline__ int tile_offset(int rr, int s)
+// Two resolutions of the same iSAX words (the bit-prefix property of variable-cardinality
+// iSAX, P:387-392 / P:408-417: the first b bits of an 8-bit symbol are the symbol at
+// cardinality 2^b):
+//  * symrows [Npad][16] u8: the full 8-bit word of every series, series-major (16 B).
+//  * coarse tiles (4 KB per 512 series): the top nibble of every symbol, two segments per
+//    byte -- byte = hi(sym_2p) << 4 | hi(sym_2p+1) for pair p -- 8 B per series, in a
+//    skewed tile layout.  Block b = 16 series (b < 32); tile row t (512 B) holds, at byte
+//    offset 16*b, the pair bytes of pair p = (t + b) mod 8 of block b's 16 series.  A warp
+//    reading tile row t (lane b loads 16 B) therefore gets 8 different pairs across each
+//    group of 8 lanes; with the coarse table replicated 4 times (copy b >> 3) the 32 lanes
+//    hit 32 distinct shared-memory banks whatever the symbol values.
+__device__ __forceinline__ int coarse_offset(int rr, int pair)
 {
-    int b = rr >> 4, k = rr & 15, p = b >> 1;
-    int t = (s - p) & 15;
+    int b = rr >> 4, k = rr & 15;
+    int t = (pair - b) & 7;
     return t * 512 + b * 16 + k;
 }
 
@@ -48,18 +53,18 @@ __device__ __forceinline__ int tile_offset(int rr, int s)
 // subtree of P:711 (one bit per segment), each further plane refines it like a split.
 __global__ void __launch_bounds__(256) k_summarise(const float* __restrict__ rows, int64_t N, int n,
                                                    const float* __restrict__ beta_g, uint4* __restrict__ tiles,
-                                                   int64_t ntiles, unsigned long long* __restrict__ keys,
-                                                   unsigned* __restrict__ ids, float* __restrict__ paa)
+                                                   uint4* __restrict__ symrows, int64_t ntiles,
+                                                   unsigned long long* __restrict__ keys, unsigned* __restrict__ ids,
+                                                   float* __restrict__ paa)
 {
     __shared__ float beta[256];
     __shared__ __align__(16) unsigned char tile[MESSI_TILE_BYTES];
+    __shared__ __align__(16) unsigned char srow[MESSI_TILE_ROWS * MESSI_W];
     const int m = n / MESSI_W;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int s = lane & 15, h2 = lane >> 4;
     if (threadIdx.x < 255) beta[threadIdx.x] = beta_g[threadIdx.x];
     for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-        for (int i = threadIdx.x; i < MESSI_TILE_BYTES / 16; i += blockDim.x)
-            reinterpret_cast<uint4*>(tile)[i] = make_uint4(0, 0, 0, 0);
         __syncthreads();
         const int64_t row0 = tl * MESSI_TILE_ROWS;
 #pragma unroll 2
@@ -85,8 +90,11 @@ __global__ void __launch_bounds__(256) k_summarise(const float* __restrict__ row
                 float p32 = __double2float_rn(__ddiv_rn(sum, (double)m));
                 sym = symbol_of(p32, beta);
                 if (paa) paa[row * MESSI_W + s] = p32;
-                tile[tile_offset(rr, s)] = (unsigned char)sym;
             }
+            srow[rr * MESSI_W + s] = (unsigned char)sym;
+            // pair byte: even lane s takes its odd neighbour's top nibble
+            const int nb = __shfl_down_sync(0xffffffffu, sym, 1);
+            if ((s & 1) == 0) tile[coarse_offset(rr, s >> 1)] = (unsigned char)((sym & 0xf0) | (nb >> 4));
             unsigned long long key = 0;
 #pragma unroll
             for (int bit = 7; bit >= 4; --bit) {
@@ -102,20 +110,20 @@ __global__ void __launch_bounds__(256) k_summarise(const float* __restrict__ row
         uint4* dst = tiles + tl * (MESSI_TILE_BYTES / 16);
         for (int i = threadIdx.x; i < MESSI_TILE_BYTES / 16; i += blockDim.x)
             dst[i] = reinterpret_cast<const uint4*>(tile)[i];
-        __syncthreads();
+        uint4* sdst = symrows + tl * MESSI_TILE_ROWS;
+        for (int i = threadIdx.x; i < MESSI_TILE_ROWS; i += blockDim.x)
+            sdst[i] = reinterpret_cast<const uint4*>(srow)[i];
     }
 }
 
-// Inverse of the tile layout, for inspection: sym[row][s].
-__global__ void k_detile(const unsigned char* __restrict__ tiles, int64_t N, unsigned char* __restrict__ sym)
+// Inverse of the coarse layout (inspection): the pair bytes of every row, [N][8].
+__global__ void k_detile_coarse(const unsigned char* __restrict__ tiles, int64_t N, unsigned char* __restrict__ out)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= N * MESSI_W) return;
-    int64_t row = i / MESSI_W;
-    int s = (int)(i % MESSI_W);
-    int64_t tl = row / MESSI_TILE_ROWS;
-    int rr = (int)(row % MESSI_TILE_ROWS);
-    sym[i] = tiles[tl * MESSI_TILE_BYTES + tile_offset(rr, s)];
+    if (i >= N * MESSI_PAIRS) return;
+    int64_t row = i / MESSI_PAIRS;
+    int pair = (int)(i % MESSI_PAIRS);
+    out[i] = tiles[(row / MESSI_TILE_ROWS) * MESSI_TILE_BYTES + coarse_offset((int)(row % MESSI_TILE_ROWS), pair)];
 }
 
 }  // namespace messi

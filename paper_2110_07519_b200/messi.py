@@ -40,7 +40,8 @@ class Result(ctypes.Structure):
 
 
 class Stats(ctypes.Structure):
-    _fields_ = [("lb_computed", ctypes.c_int64), ("candidates", ctypes.c_int64), ("lbk_pass", ctypes.c_int64),
+    _fields_ = [("lb_computed", ctypes.c_int64), ("coarse_pass", ctypes.c_int64), ("candidates", ctypes.c_int64),
+                ("lbk_pass", ctypes.c_int64),
                 ("refined", ctypes.c_int64), ("abandoned", ctypes.c_int64), ("near_best", ctypes.c_int64),
                 ("seed_d2", ctypes.c_double), ("bsf_d2", ctypes.c_double)]
 
@@ -77,10 +78,13 @@ def lib():
         L.messi_debug_summaries.argtypes = [vp, vp, vp]
         L.messi_debug_order.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]
         L.messi_debug_lower_bounds.argtypes = [vp, vp, i32, vp]
+        L.messi_debug_coarse_bounds.argtypes = [vp, vp, i32, vp]
+        L.messi_debug_coarse_summaries.argtypes = [vp, vp]
         L.messi_debug_distances.argtypes = [vp, vp, i32, vp, i32, vp, vp, vp]
         for f in ("messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_batch",
                   "messi_query_dtw_batch", "messi_profile_enable", "messi_profile_read", "messi_debug_breakpoints", "messi_debug_summaries",
-                  "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances"):
+                  "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances",
+                  "messi_debug_coarse_bounds", "messi_debug_coarse_summaries"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -89,7 +93,8 @@ def lib():
 EXPORTED = ["messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_batch", "messi_query_dtw_batch",
             "messi_free", "messi_last_error", "messi_launch_count", "messi_profile_enable", "messi_profile_read",
             "messi_debug_breakpoints",
-            "messi_debug_summaries", "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances"]
+            "messi_debug_summaries", "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances",
+            "messi_debug_coarse_bounds", "messi_debug_coarse_summaries"]
 
 
 def _check(status: int):
@@ -139,7 +144,7 @@ def messi_query_dtw(handle, query, reach: int, with_stats: bool = False):
 
 def messi_query_ed_batch(handle, queries_dev: torch.Tensor, results_dev: torch.Tensor, stats_dev=None):
     """Asynchronous on the build stream.  results_dev: uint8 CUDA tensor of nq*32 bytes (see
-    ``result_buffer``); stats_dev: optional nq*64 bytes (``stats_buffer``)."""
+    ``result_buffer``); stats_dev: optional nq*72 bytes (``stats_buffer``)."""
     _check(lib().messi_query_ed_batch(handle, _ptr(queries_dev), queries_dev.shape[0], _ptr(results_dev),
                                       _ptr(stats_dev)))
 
@@ -205,6 +210,18 @@ def messi_debug_lower_bounds(handle, query_dev: torch.Tensor, reach: int, count:
     return lb
 
 
+def messi_debug_coarse_bounds(handle, query_dev: torch.Tensor, reach: int, count: int):
+    lb = torch.empty(count, dtype=torch.float32, device=query_dev.device)
+    _check(lib().messi_debug_coarse_bounds(handle, _ptr(query_dev), int(reach), _ptr(lb)))
+    return lb
+
+
+def messi_debug_coarse_summaries(handle, count: int, device):
+    pairs = torch.empty((count, 8), dtype=torch.uint8, device=device)
+    _check(lib().messi_debug_coarse_summaries(handle, _ptr(pairs)))
+    return pairs
+
+
 def messi_debug_distances(handle, query_dev: torch.Tensor, reach: int, ids_dev: torch.Tensor):
     k = ids_dev.numel()
     dev = query_dev.device
@@ -237,7 +254,7 @@ def _wrap_dev(ptr: int, nbytes: int, device):
     return torch.as_tensor(_Arr(), device=device)
 
 
-RESULT_BYTES, STATS_BYTES = 32, 64
+RESULT_BYTES, STATS_BYTES = 32, 72
 
 
 def result_buffer(nq: int, device) -> torch.Tensor:
@@ -245,7 +262,7 @@ def result_buffer(nq: int, device) -> torch.Tensor:
 
 
 def stats_buffer(nq: int, device) -> torch.Tensor:
-    return torch.empty(nq * 64, dtype=torch.uint8, device=device)
+    return torch.empty(nq * STATS_BYTES, dtype=torch.uint8, device=device)
 
 
 def decode_results(buf: torch.Tensor):
@@ -263,9 +280,9 @@ def decode_results_device(buf: torch.Tensor):
 
 
 def decode_stats(buf: torch.Tensor):
-    raw = buf.view(-1, 64).cpu()
-    ints = raw[:, :48].contiguous().view(torch.int64)
-    dbl = raw[:, 48:].contiguous().view(torch.float64)
+    raw = buf.view(-1, STATS_BYTES).cpu()
+    ints = raw[:, :56].contiguous().view(torch.int64)
+    dbl = raw[:, 56:].contiguous().view(torch.float64)
     return [dict(zip(STATS_FIELDS, list(map(int, i.tolist())) + list(map(float, d.tolist()))))
             for i, d in zip(ints, dbl)]
 
