@@ -246,8 +246,10 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
             return bail(fail(MESSI_ECUDA, "event creation failed"));
     }
     if ((s = dalloc(&idx->qbuf, n)) || (s = dalloc(&idx->res1, 1)) || (s = dalloc(&idx->stats1, 1))) return bail(s);
-    if (cudaStreamCreateWithFlags(&idx->side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&idx->rstr, cudaStreamNonBlocking) != cudaSuccess ||
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (cudaStreamCreateWithPriority(&idx->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&idx->rstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&idx->ev_fork, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(MESSI_ECUDA, "stream creation failed"));
 

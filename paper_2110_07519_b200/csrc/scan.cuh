@@ -203,11 +203,75 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
 // (v << 8 | base) from the packed pair bytes in one instruction.
 //   SCAN_COMPACT: survivors -> global list;   SCAN_ALL: every coarse LB written (inspection).
 enum { SCAN_COMPACT = 0, SCAN_ALL = 1 };
-constexpr int kScanWarps = 8;
+#ifndef MESSI_SCAN_WARPS
+#define MESSI_SCAN_WARPS 8
+#endif
+#ifndef MESSI_SCAN_MINB
+#define MESSI_SCAN_MINB 2
+#endif
+#ifndef MESSI_SCAN_PREFETCH
+#define MESSI_SCAN_PREFETCH 0
+#endif
+constexpr int kScanWarps = MESSI_SCAN_WARPS;
 constexpr size_t kScanLutBytes = (size_t)MESSI_CARD * 64 * sizeof(float);
 
+// Coarse bound of the 16 series of one lane for one tile already in registers.
+__device__ __forceinline__ void coarse_tile(const uint4 (&data)[8], const char* lbase, int lane, float (&acc)[16])
+{
+    const int cpy = lane >> 3;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = 0.0f;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const unsigned base = (unsigned)((8 * cpy + ((t + lane) & 7)) * 4);
+        const unsigned wv[4] = {data[t].x, data[t].y, data[t].z, data[t].w};
+#pragma unroll
+        for (int wi = 0; wi < 4; ++wi) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const unsigned addr = __byte_perm(wv[wi], base, 0x5504 | (b << 4));
+                acc[wi * 4 + b] = __fadd_rd(acc[wi * 4 + b], *reinterpret_cast<const float*>(lbase + addr));
+            }
+        }
+    }
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(256, 2) k_scan(const uint4* __restrict__ tiles, long long ntiles, long long N,
+__device__ __forceinline__ void coarse_emit(const float (&acc)[16], long long tl, long long N, float thr, int lane,
+                                            QState* st, uint2* __restrict__ out, float* __restrict__ lb_all)
+{
+    const long long id0 = tl * MESSI_TILE_ROWS + lane * 16;
+    if (MODE == SCAN_ALL) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (id0 + k < N) lb_all[id0 + k] = acc[k];
+        return;
+    }
+    unsigned mask = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+        if (acc[k] <= thr && id0 + k < N) mask |= 1u << k;
+    if (!__any_sync(0xffffffffu, mask)) return;
+    const int cnt = __popc(mask);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(&st->coarse_count, (unsigned)total);
+    unsigned pos = __shfl_sync(0xffffffffu, base, 0) + incl - cnt;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+        if (mask & (1u << k)) out[pos++] = make_uint2((unsigned)(id0 + k), __float_as_uint(acc[k]));
+}
+
+// Each warp walks its tiles (grid-stride); with MESSI_SCAN_PREFETCH the NEXT tile's eight
+// 128-bit loads are issued before the current tile's lookups (8 KB per warp in flight).
+template <int MODE>
+__global__ void __launch_bounds__(32 * kScanWarps, MESSI_SCAN_MINB) k_scan(const uint4* __restrict__ tiles, long long ntiles, long long N,
                                                  const float* __restrict__ lut2_g, QState* st,
                                                  uint2* __restrict__ out, float* __restrict__ lb_all)
 {
@@ -221,55 +285,37 @@ __global__ void __launch_bounds__(256, 2) k_scan(const uint4* __restrict__ tiles
     __syncthreads();
     const float thr = MODE == SCAN_ALL ? INFINITY : slack_up(ld_bsf(st));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int cpy = lane >> 3;
     const char* lbase = reinterpret_cast<const char*>(lut_s);
-    for (long long tl = (long long)blockIdx.x * kScanWarps + warp; tl < ntiles; tl += (long long)gridDim.x * kScanWarps) {
-        const uint4* tp = tiles + tl * (MESSI_TILE_BYTES / 16) + lane;
-        uint4 data[8];
+    const long long stride = (long long)gridDim.x * kScanWarps;
+    long long tl = (long long)blockIdx.x * kScanWarps + warp;
+    float acc[16];
+    auto load = [&](uint4 (&d)[8], long long t) {
+        const uint4* tp = tiles + t * (MESSI_TILE_BYTES / 16) + lane;
 #pragma unroll
-        for (int t = 0; t < 8; ++t) data[t] = __ldcs(tp + t * 32);
-        float acc[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) acc[k] = 0.0f;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            const unsigned base = (unsigned)((8 * cpy + ((t + lane) & 7)) * 4);
-            const unsigned wv[4] = {data[t].x, data[t].y, data[t].z, data[t].w};
-#pragma unroll
-            for (int wi = 0; wi < 4; ++wi) {
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const unsigned addr = __byte_perm(wv[wi], base, 0x5504 | (b << 4));
-                    acc[wi * 4 + b] = __fadd_rd(acc[wi * 4 + b], *reinterpret_cast<const float*>(lbase + addr));
-                }
-            }
-        }
-        const long long id0 = tl * MESSI_TILE_ROWS + lane * 16;
-        if (MODE == SCAN_ALL) {
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-                if (id0 + k < N) lb_all[id0 + k] = acc[k];
-            continue;
-        }
-        unsigned mask = 0;
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if (acc[k] <= thr && id0 + k < N) mask |= 1u << k;
-        if (!__any_sync(0xffffffffu, mask)) continue;
-        const int cnt = __popc(mask);
-        int incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(&st->coarse_count, (unsigned)total);
-        unsigned pos = __shfl_sync(0xffffffffu, base, 0) + incl - cnt;
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if (mask & (1u << k)) out[pos++] = make_uint2((unsigned)(id0 + k), __float_as_uint(acc[k]));
+        for (int i = 0; i < 8; ++i) d[i] = __ldcs(tp + i * 32);
+    };
+#if !MESSI_SCAN_PREFETCH
+    for (; tl < ntiles; tl += stride) {
+        uint4 a[8];
+        load(a, tl);
+        coarse_tile(a, lbase, lane, acc);
+        coarse_emit<MODE>(acc, tl, N, thr, lane, st, out, lb_all);
+    }
+    return;
+#endif
+    uint4 a[8], b[8];
+    if (tl < ntiles) load(a, tl);
+    while (tl < ntiles) {
+        const long long t1 = tl + stride;
+        if (t1 < ntiles) load(b, t1);
+        coarse_tile(a, lbase, lane, acc);
+        coarse_emit<MODE>(acc, tl, N, thr, lane, st, out, lb_all);
+        if (t1 >= ntiles) break;
+        const long long t2 = t1 + stride;
+        if (t2 < ntiles) load(a, t2);
+        coarse_tile(b, lbase, lane, acc);
+        coarse_emit<MODE>(acc, t1, N, thr, lane, st, out, lb_all);
+        tl = t2;
     }
 }
 

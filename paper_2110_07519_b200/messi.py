@@ -16,7 +16,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmessi.so")
+# MESSI_LIB selects an alternative build of the same sources (kernel-tuning experiments)
+LIB_PATH = os.environ.get("MESSI_LIB") or os.path.join(_HERE, "libmessi.so")
 
 MESSI_OK, MESSI_EINVAL, MESSI_EEMPTY, MESSI_ENOMEM, MESSI_ECUDA = range(5)
 _STATUS = {1: "EINVAL", 2: "EEMPTY", 3: "ENOMEM", 4: "ECUDA"}
