@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
     ap.add_argument("--cpu-rows", type=int, default=4_000_000, help="row sample of the oracle timing")
     ap.add_argument("--cpu-queries", type=int, default=32, help="queries of the oracle timing sample")
+    ap.add_argument("--window", type=int, default=0, help="approximate-search window (0: library default 2000)")
     return ap.parse_args()
 
 
@@ -176,7 +177,7 @@ def run_arm(cfg, args, world, rank, dev, stream, time_steps, warmup):
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        idx = M.Index(X, row_begin=row_begin, stream=stream)
+        idx = M.Index(X, row_begin=row_begin, stream=stream, window=args.window)
         t1.record(stream)
         torch.cuda.synchronize()
         build_ms = t0.elapsed_time(t1)
@@ -298,7 +299,13 @@ def ours(args):
     # (DESIGN.md "Roofline"); achieved = those bytes over the kernel's own event time
     st = main["stats"]
     mean = lambda k: sum(s[k] for s in st) / len(st)  # noqa: E731
-    scan_bytes = 8 * main["N_local"] + 8 * mean("coarse_pass")
+    # tiles that survive the box filter are streamed (4 KB each); ED also gathers one 32 B
+    # sector of 8-bit word per coarse survivor inside the scan; DTW writes (pos, LB) per
+    # coarse survivor
+    if cfg["reach"] is None:
+        scan_bytes = 4096 * mean("tiles_scanned") + 32 * mean("coarse_pass") + 8 * mean("candidates")
+    else:
+        scan_bytes = 4096 * mean("tiles_scanned") + 8 * mean("coarse_pass")
     achieved = scan_bytes * scan_n / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
     peak = pk.get("hbm_gbs", 6650.0)
     traffic = None
@@ -309,8 +316,9 @@ def ours(args):
         pass
     # whole-query algorithmic bytes per GPU: coarse stream + one 32 B sector of 8-bit word per
     # coarse survivor + the rows refined + the approximate-search window rows
-    per_query_bytes = (8 * main["N_local"] + 32 * mean("coarse_pass") + 4 * main["n"] * mean("refined")
-                       + 4 * main["n"] * min(2000, main["N_local"]))
+    ntiles = (main["N_local"] + 511) // 512
+    per_query_bytes = (32 * ntiles + 4096 * mean("tiles_scanned") + 32 * mean("coarse_pass")
+                       + 4 * main["n"] * mean("refined") + 4 * main["n"] * min(2000, main["N_local"]))
     steps_total = {k: max_over_ranks(v[0], world) for k, v in main["prof"].items()}
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
@@ -319,9 +327,9 @@ def ours(args):
         "dtype": "f32", "data": "synthetic (seeded device Philox random walks, z-normalised)",
         "config": {"workload": cfg["name"], "mode": args.mode, "rows": cfg["N"], "length": cfg["n"],
                    "queries_per_step": nq, "reach": cfg["reach"], "parallelism": f"row-shard x{world}",
-                   "l2": "inputs larger than L2: every query streams %.2f GB of coarse summaries per GPU" % (8 * main["N_local"] / 1e9),
+                   "l2": "inputs larger than L2: %.2f GB of coarse summaries per GPU, every query streams the tiles its box filter keeps" % (8 * main["N_local"] / 1e9),
                    "query_model": "sequential queries (P:2024-2026), batch call per step"},
-        "roofline": {"bound": "hbm", "kernel": "k_scan (coarse iSAX LB scan + compaction)", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": "k_scan (coarse iSAX LB scan of the box-filtered tiles)", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in pk else "fallback",
                      "algorithmic_bytes_per_launch": scan_bytes, "launches": scan_n,
@@ -336,8 +344,8 @@ def ours(args):
         "clocks": main["clocks"],
         "build": {"ms": main["build_ms"], "rows_per_s": main["N_local"] / (main["build_ms"] / 1e3),
                   "what": "summarise (PAA + iSAX + key) + CUB key sort, per GPU"},
-        "stats_mean": {k: mean(k) for k in ("coarse_pass", "candidates", "lbk_pass", "refined", "abandoned",
-                                             "near_best", "seed_d2", "bsf_d2")},
+        "stats_mean": {k: mean(k) for k in ("tiles_scanned", "coarse_pass", "candidates", "lbk_pass", "refined",
+                                             "abandoned", "near_best", "seed_d2", "bsf_d2")},
     }
     if args.mode == "ed" and not args.no_dtw:
         c4 = dict(CONFIGS["c4"])
@@ -349,8 +357,8 @@ def ours(args):
         line["dtw"] = {"value": k4 * d["nq"] / (dms / 1e3), "unit": "queries/s", "workload": c4["name"],
                        "steps": k4, "ms_per_step": dms / k4,
                        "kernel_ms_per_step": {k: v[0] / k4 for k, v in d["prof"].items()},
-                       "stats_mean": {k: dm(k) for k in ("coarse_pass", "candidates", "lbk_pass", "refined",
-                                                         "abandoned", "near_best", "seed_d2", "bsf_d2")},
+                       "stats_mean": {k: dm(k) for k in ("tiles_scanned", "coarse_pass", "candidates", "lbk_pass",
+                                                         "refined", "abandoned", "near_best", "seed_d2", "bsf_d2")},
                        "gpu_launches": d["launches"]}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, args, dev, "ED" if cfg["reach"] is None else "DTW")

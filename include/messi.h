@@ -61,7 +61,8 @@ typedef struct {
 } messi_result;
 
 typedef struct {
-    int64_t lb_computed;  /* rows whose iSAX lower bound was evaluated (= count: flat scan) */
+    int64_t lb_computed;  /* rows of the shard (every row is covered by a tile or a series bound) */
+    int64_t tiles_scanned; /* 512-series tiles whose box bound <= BSF0 * (1 + eps) (scanned) */
     int64_t coarse_pass;  /* rows whose cardinality-16 (4-bit prefix) bound <= BSF0 * (1 + eps) */
     int64_t candidates;   /* of those, rows whose exact 8-bit bound <= BSF * (1 + eps) */
     int64_t lbk_pass;     /* DTW: candidates whose raw LB_Keogh <= BSF * (1 + eps) */
@@ -113,6 +114,12 @@ int64_t messi_launch_count(const messi_index* idx);
 messi_status messi_profile_enable(messi_index* idx, int32_t enable);
 messi_status messi_profile_read(messi_index* idx, int32_t kind, double* total_ms, int64_t* launches);
 
+/* Scan throughput in isolation: one query's prologue and tile filter, then `reps` scans back
+ * to back, each timed with CUDA events; *ms_out = summed kernel milliseconds, *coarse_out
+ * (nullable) = coarse survivors of the last repetition | (tiles scanned << 32). */
+messi_status messi_debug_scan_repeat(messi_index* idx, const float* query_dev, int32_t reps, double* ms_out,
+                                     int64_t* coarse_out);
+
 /* ---- inspection entry points (tests / bench; same kernels as the query path) ---------- */
 
 /* The 255 fp32 N(0,1) breakpoints the device derived (O3 reading), into host memory. */
@@ -134,6 +141,10 @@ messi_status messi_debug_coarse_summaries(messi_index* idx, uint8_t* pairs_dev);
  * _coarse_bounds: the same bound at cardinality 16 (top nibbles), what the scan streams. */
 messi_status messi_debug_lower_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
 messi_status messi_debug_coarse_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
+
+/* Box bound of every tile (512 consecutive series in approximate-search order; members are
+ * rows perm[512*t .. 512*t+511]), written to lb_dev[ntiles] (fp32 of the fp64 bound). */
+messi_status messi_debug_tile_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
 
 /* For `k` local row ids: fp32 squared distance as computed by the refine kernels (no
  * abandoning), the exact fp64 squared distance of the re-rank kernel, and (reach >= 0)

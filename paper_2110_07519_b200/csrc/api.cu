@@ -14,6 +14,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -32,6 +33,7 @@ struct Slot {
     float *lut = nullptr, *lut2 = nullptr, *U = nullptr, *L = nullptr;
     uint2* coarse = nullptr;  // coarse-scan survivors (id, coarse LB)
     uint2* list2 = nullptr;   // DTW: LB_Keogh survivors (id, LBK)  [lazy]
+    unsigned* tlist = nullptr;  // tiles surviving the box filter
     NearEntry* near = nullptr;
     cudaEvent_t ev_seed = nullptr, ev_scan = nullptr, ev_done = nullptr;
 };
@@ -48,7 +50,8 @@ struct messi_index {
     int sms = 148;
     // summaries
     uint4* tiles = nullptr;    // coarse tiles (4 KB per 512 series)
-    uint4* symrows = nullptr;  // [ntiles*512][16] u8
+    uint4* symrows = nullptr;  // [ntiles*512][16] u8, sorted positions
+    unsigned char* boxes = nullptr;  // [ntiles][32]: per-segment min / max symbol
     float* paa = nullptr;
     unsigned long long* skey = nullptr;
     unsigned* perm = nullptr;
@@ -68,7 +71,7 @@ struct messi_index {
 };
 
 static_assert(sizeof(messi_result) == 32, "messi_result layout");
-static_assert(sizeof(messi_stats) == 72, "messi_stats layout");
+static_assert(sizeof(messi_stats) == 80, "messi_stats layout");
 
 enum { K_SEED = 0, K_SCAN = 1, K_REFINE = 2, K_LBK = 3, K_RESOLVE = 4, K_KINDS = 5 };
 
@@ -151,7 +154,7 @@ struct ProfScope {
 // Reaches with a register-band DTW instantiation (DtwThread<R>); others use the warp path.
 #define MESSI_DTW_REACHES(X) X(2) X(5) X(12) X(25)
 
-static size_t scan_smem() { return kScanLutBytes; }
+static size_t scan_smem(int mode) { return kScanLutBytes + (mode == SCAN_FINE ? kFineLutBytes : 0); }
 static size_t lbk_smem(int n)
 {
     return (size_t)MESSI_W * MESSI_CARD * sizeof(float) + 2 * (size_t)((n + 3) & ~3) * sizeof(float);
@@ -162,9 +165,10 @@ static messi_status setup_kernels()
     static bool done = false;
     if (done) return MESSI_OK;
     const int big = 200 * 1024;
-    CK(cudaFuncSetAttribute(k_scan<SCAN_COMPACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
-    CK(cudaFuncSetAttribute(k_scan<SCAN_ALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
-    CK(cudaFuncSetAttribute(k_fine_ed, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_scan<SCAN_COMPACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem(SCAN_COMPACT)));
+    CK(cudaFuncSetAttribute(k_scan<SCAN_ALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem(SCAN_ALL)));
+    CK(cudaFuncSetAttribute(k_scan<SCAN_FINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem(SCAN_FINE)));
+    CK(cudaFuncSetAttribute(k_refine_ed, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_lbk_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_refine_dtw_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -230,7 +234,8 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     const long long N = count;
     const size_t npadrows = (size_t)idx->ntiles * MESSI_TILE_ROWS;
     messi_status s;
-    if ((s = dalloc(&idx->tiles, (size_t)idx->ntiles * (MESSI_TILE_BYTES / 16))) || (s = dalloc(&idx->symrows, npadrows)))
+    if ((s = dalloc(&idx->tiles, (size_t)idx->ntiles * (MESSI_TILE_BYTES / 16))) || (s = dalloc(&idx->symrows, npadrows)) ||
+        (s = dalloc(&idx->boxes, (size_t)idx->ntiles * 32)))
         return bail(s);
     if (idx->keep_paa && (s = dalloc(&idx->paa, (size_t)N * MESSI_W))) return bail(s);
     if ((s = dalloc(&idx->skey, (size_t)N)) || (s = dalloc(&idx->perm, (size_t)N))) return bail(s);
@@ -238,7 +243,8 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     for (Slot& sl : idx->slot) {
         if ((s = dalloc(&sl.st, 1)) || (s = dalloc(&sl.lut, MESSI_W * MESSI_CARD)) ||
             (s = dalloc(&sl.lut2, MESSI_PAIRS * MESSI_CARD)) || (s = dalloc(&sl.U, n)) || (s = dalloc(&sl.L, n)) ||
-            (s = dalloc(&sl.coarse, (size_t)N)) || (s = dalloc(&sl.near, (size_t)N)))
+            (s = dalloc(&sl.coarse, (size_t)N)) || (s = dalloc(&sl.near, (size_t)N)) ||
+            (s = dalloc(&sl.tlist, (size_t)idx->ntiles)))
             return bail(s);
         if (cudaEventCreateWithFlags(&sl.ev_seed, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&sl.ev_scan, cudaEventDisableTiming) != cudaSuccess ||
@@ -248,6 +254,7 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     if ((s = dalloc(&idx->qbuf, n)) || (s = dalloc(&idx->res1, 1)) || (s = dalloc(&idx->stats1, 1))) return bail(s);
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (getenv("MESSI_PRIO_EQUAL")) prio_hi = 0;
     if (cudaStreamCreateWithPriority(&idx->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&idx->rstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&idx->ev_fork, cudaEventDisableTiming) != cudaSuccess)
@@ -256,21 +263,23 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     cudaStream_t st = idx->stream;
     unsigned long long* keys_in = nullptr;
     unsigned* ids_in = nullptr;
+    uint4* sym_tmp = nullptr;
     void* temp = nullptr;
     size_t temp_bytes = 0;
     auto cleanup = [&]() {
         cudaFree(keys_in);
         cudaFree(ids_in);
+        cudaFree(sym_tmp);
         cudaFree(temp);
     };
     do {
-        if ((s = dalloc(&keys_in, (size_t)N)) || (s = dalloc(&ids_in, (size_t)N))) break;
+        if ((s = dalloc(&keys_in, (size_t)N)) || (s = dalloc(&ids_in, (size_t)N)) || (s = dalloc(&sym_tmp, npadrows))) break;
         k_breakpoints<<<1, 256, 0, st>>>(idx->beta32, idx->lo_w, idx->hi_w);
         ++idx->launches;
         if (cudaGetLastError() != cudaSuccess) { s = fail(MESSI_ECUDA, "k_breakpoints launch"); break; }
         long long grid = idx->ntiles < (long long)idx->sms * 8 ? idx->ntiles : (long long)idx->sms * 8;
-        k_summarise<<<(unsigned)grid, 256, 0, st>>>(rows_dev, N, n, idx->beta32, idx->tiles, idx->symrows, idx->ntiles,
-                                                    keys_in, ids_in, idx->paa);
+        k_summarise<<<(unsigned)grid, 256, 0, st>>>(rows_dev, N, n, idx->beta32, sym_tmp, idx->ntiles, keys_in, ids_in,
+                                                    idx->paa);
         ++idx->launches;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "k_summarise: %s", cudaGetErrorString(e)); break; }
@@ -281,6 +290,11 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
         e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, idx->skey, ids_in, idx->perm, (int)N, 0, 64, st);
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "cub sort: %s", cudaGetErrorString(e)); break; }
         idx->launches += 4;
+        k_layout<<<(unsigned)idx->ntiles, MESSI_TILE_ROWS, 0, st>>>(sym_tmp, idx->perm, N, idx->symrows, idx->tiles,
+                                                                   idx->boxes);
+        ++idx->launches;
+        e = cudaGetLastError();
+        if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "k_layout: %s", cudaGetErrorString(e)); break; }
         for (Slot& sl : idx->slot) {
             k_arm<<<1, 1, 0, st>>>(sl.st);
             ++idx->launches;
@@ -303,12 +317,12 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->rstr) cudaStreamSynchronize(idx->rstr);
     if (idx->stream) cudaStreamSynchronize(idx->stream);
     else cudaDeviceSynchronize();
-    void* ptrs[] = {idx->tiles, idx->symrows, idx->paa,  idx->skey, idx->perm,  idx->beta32,
-                    idx->lo_w,  idx->hi_w,    idx->qbuf, idx->res1, idx->stats1};
+    void* ptrs[] = {idx->tiles, idx->symrows, idx->boxes, idx->paa,  idx->skey,   idx->perm,
+                    idx->beta32, idx->lo_w,   idx->hi_w,  idx->qbuf, idx->res1, idx->stats1};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (Slot& sl : idx->slot) {
-        void* sp[] = {sl.st, sl.lut, sl.lut2, sl.U, sl.L, sl.coarse, sl.list2, sl.near};
+        void* sp[] = {sl.st, sl.lut, sl.lut2, sl.U, sl.L, sl.coarse, sl.list2, sl.near, sl.tlist};
         for (void* p : sp)
             if (p) cudaFree(p);
         cudaEvent_t es[] = {sl.ev_seed, sl.ev_scan, sl.ev_done};
@@ -316,8 +330,8 @@ extern "C" void messi_free(messi_index* idx)
             if (e) cudaEventDestroy(e);
     }
     if (idx->ev_fork) cudaEventDestroy(idx->ev_fork);
-    if (idx->side) cudaStreamDestroy(idx->side);
-    if (idx->rstr) cudaStreamDestroy(idx->rstr);
+    if (idx->side && idx->side != idx->stream) cudaStreamDestroy(idx->side);
+    if (idx->rstr && idx->rstr != idx->stream) cudaStreamDestroy(idx->rstr);
     for (auto& e : idx->evs) {
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
@@ -386,10 +400,28 @@ static int refine_grid(const messi_index* idx, int per_block_rows)
     return (int)(need < cap ? (need < 1 ? 1 : need) : cap);
 }
 
+// MESSI_SERIAL=1 (experiments): every stage on the caller's stream, no overlap.
+static bool serial_mode()
+{
+    static int v = -1;
+    if (v < 0) v = getenv("MESSI_SERIAL") ? 1 : 0;
+    return v == 1;
+}
+
 // Orders the side and refine streams after everything already enqueued on the main stream
 // (query buffers written by the caller) -- once per API call, not between batch queries.
 static messi_status fork_streams(messi_index* idx)
 {
+    if (serial_mode()) {
+        if (idx->side != idx->stream) {
+            cudaStreamSynchronize(idx->side);
+            cudaStreamSynchronize(idx->rstr);
+            cudaStreamDestroy(idx->side);
+            cudaStreamDestroy(idx->rstr);
+            idx->side = idx->rstr = idx->stream;
+        }
+        return MESSI_OK;
+    }
     CK(cudaEventRecord(idx->ev_fork, idx->stream));
     CK(cudaStreamWaitEvent(idx->side, idx->ev_fork, 0));
     CK(cudaStreamWaitEvent(idx->rstr, idx->ev_fork, 0));
@@ -410,13 +442,35 @@ static messi_status ensure_dtw_buffers(messi_index* idx)
     return MESSI_OK;
 }
 
-static messi_status launch_scan(messi_index* idx, Slot& sl)
+static int filter_grid(const messi_index* idx)
+{
+    long long need = (idx->ntiles + 255) / 256;
+    long long cap = (long long)idx->sms * 4;
+    return (int)(need < cap ? (need < 1 ? 1 : need) : cap);
+}
+
+// Box filter of every tile (side stream, right after the seed: needs BSF0 and the query PAA).
+static messi_status launch_tile_filter(messi_index* idx, Slot& sl, cudaStream_t st)
+{
+    k_tile_filter<<<filter_grid(idx), 256, 0, st>>>(idx->boxes, idx->ntiles, idx->n / MESSI_W, idx->lo_w, idx->hi_w,
+                                                   sl.st, sl.tlist, nullptr);
+    LAUNCHED(idx);
+    return MESSI_OK;
+}
+
+static messi_status launch_scan(messi_index* idx, Slot& sl, bool fine)
 {
     CK(cudaStreamWaitEvent(idx->stream, sl.ev_seed, 0));
     {
         ProfScope ps(idx, K_SCAN, idx->stream);
-        k_scan<SCAN_COMPACT><<<scan_grid(idx), 32 * kScanWarps, scan_smem(), idx->stream>>>(
-            idx->tiles, idx->ntiles, idx->N, sl.lut2, sl.st, sl.coarse, nullptr);
+        if (fine)
+            k_scan<SCAN_FINE><<<scan_grid(idx), 32 * kScanWarps, scan_smem(SCAN_FINE), idx->stream>>>(
+                idx->tiles, idx->ntiles, idx->N, sl.lut2, sl.lut, idx->symrows, sl.st, sl.coarse, nullptr, sl.tlist,
+                idx->perm);
+        else
+            k_scan<SCAN_COMPACT><<<scan_grid(idx), 32 * kScanWarps, scan_smem(SCAN_COMPACT), idx->stream>>>(
+                idx->tiles, idx->ntiles, idx->N, sl.lut2, sl.lut, idx->symrows, sl.st, sl.coarse, nullptr, sl.tlist,
+                idx->perm);
         LAUNCHED(idx);
     }
     CK(cudaEventRecord(sl.ev_scan, idx->stream));
@@ -438,13 +492,14 @@ static messi_status run_ed(messi_index* idx, const float* q_dev, messi_result* r
         k_seed_ed<<<seed_grid, 256, qsm, idx->side>>>(q_dev, n, idx->rows, idx->skey, idx->perm, idx->N, idx->window,
                                                       idx->beta32, idx->lo_w, idx->hi_w, sl.lut, sl.lut2, sl.st);
         LAUNCHED(idx);
+        TRY(launch_tile_filter(idx, sl, idx->side));
     }
     CK(cudaEventRecord(sl.ev_seed, idx->side));
-    TRY(launch_scan(idx, sl));
+    TRY(launch_scan(idx, sl, true));
     {
         ProfScope ps(idx, K_REFINE, idx->rstr);
-        k_fine_ed<<<refine_grid(idx, 4096), 256, fine_ed_smem(n), idx->rstr>>>(
-            sl.coarse, idx->symrows, sl.lut, idx->rows, n, q_dev, sl.st, sl.near, idx->N, idx->row_begin, res, stats);
+        k_refine_ed<<<refine_grid(idx, 32768), 256, refine_ed_smem(n), idx->rstr>>>(
+            sl.coarse, idx->perm, idx->rows, n, q_dev, sl.st, sl.near, idx->N, idx->row_begin, res, stats);
         LAUNCHED(idx);
     }
     CK(cudaEventRecord(sl.ev_done, idx->rstr));
@@ -470,13 +525,14 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
             q_dev, n, reach, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32, idx->lo_w, idx->hi_w,
             sl.lut, sl.U, sl.L, sl.lut2, sl.st);
         LAUNCHED(idx);
+        TRY(launch_tile_filter(idx, sl, idx->side));
     }
     CK(cudaEventRecord(sl.ev_seed, idx->side));
-    TRY(launch_scan(idx, sl));
+    TRY(launch_scan(idx, sl, false));
     {
         ProfScope ps(idx, K_LBK, rs);
-        k_lbk_filter<<<refine_grid(idx, 2048), 256, lbk_smem(n), rs>>>(sl.coarse, idx->symrows, sl.lut, idx->rows, n,
-                                                                       sl.U, sl.L, sl.st, sl.list2);
+        k_lbk_filter<<<refine_grid(idx, 2048), 256, lbk_smem(n), rs>>>(sl.coarse, idx->symrows, idx->perm, sl.lut,
+                                                                       idx->rows, n, sl.U, sl.L, sl.st, sl.list2);
         LAUNCHED(idx);
     }
     {
@@ -615,7 +671,9 @@ extern "C" messi_status messi_debug_summaries(messi_index* idx, uint8_t* sym_dev
     if (paa_dev && !idx->paa) return fail(MESSI_EINVAL, "index built without keep_paa");
     CK(cudaSetDevice(idx->device));
     TRY(sync_all(idx));
-    CK(cudaMemcpyAsync(sym_dev, idx->symrows, (size_t)idx->N * MESSI_W, cudaMemcpyDeviceToDevice, idx->stream));
+    k_unsort_sym<<<(unsigned)((idx->N + 255) / 256), 256, 0, idx->stream>>>(idx->symrows, idx->perm, idx->N,
+                                                                             reinterpret_cast<uint4*>(sym_dev));
+    LAUNCHED(idx);
     if (paa_dev)
         CK(cudaMemcpyAsync(paa_dev, idx->paa, (size_t)idx->N * MESSI_W * sizeof(float), cudaMemcpyDeviceToDevice,
                            idx->stream));
@@ -630,8 +688,8 @@ extern "C" messi_status messi_debug_coarse_summaries(messi_index* idx, uint8_t* 
     CK(cudaSetDevice(idx->device));
     TRY(sync_all(idx));
     long long total = idx->N * MESSI_PAIRS;
-    k_detile_coarse<<<(unsigned)((total + 255) / 256), 256, 0, idx->stream>>>((const unsigned char*)idx->tiles, idx->N,
-                                                                              pairs_dev);
+    k_detile_coarse<<<(unsigned)((total + 255) / 256), 256, 0, idx->stream>>>((const unsigned char*)idx->tiles, idx->perm,
+                                                                              idx->N, pairs_dev);
     LAUNCHED(idx);
     CK(cudaStreamSynchronize(idx->stream));
     return MESSI_OK;
@@ -674,7 +732,7 @@ extern "C" messi_status messi_debug_lower_bounds(messi_index* idx, const float* 
     CK(cudaSetDevice(idx->device));
     TRY(sync_all(idx));
     TRY(debug_prologue(idx, query_dev, reach));
-    k_fine_all<<<idx->sms * 4, 256, 0, idx->stream>>>(idx->symrows, idx->N, idx->slot[0].lut, lb_dev);
+    k_fine_all<<<idx->sms * 4, 256, 0, idx->stream>>>(idx->symrows, idx->perm, idx->N, idx->slot[0].lut, lb_dev);
     LAUNCHED(idx);
     CK(cudaStreamSynchronize(idx->stream));
     return MESSI_OK;
@@ -689,8 +747,8 @@ extern "C" messi_status messi_debug_coarse_bounds(messi_index* idx, const float*
     TRY(sync_all(idx));
     TRY(debug_prologue(idx, query_dev, reach));
     Slot& sl = idx->slot[0];
-    k_scan<SCAN_ALL><<<scan_grid(idx), 32 * kScanWarps, scan_smem(), idx->stream>>>(idx->tiles, idx->ntiles, idx->N,
-                                                                                    sl.lut2, sl.st, nullptr, lb_dev);
+    k_scan<SCAN_ALL><<<scan_grid(idx), 32 * kScanWarps, scan_smem(SCAN_ALL), idx->stream>>>(
+        idx->tiles, idx->ntiles, idx->N, sl.lut2, sl.lut, idx->symrows, sl.st, nullptr, lb_dev, nullptr, idx->perm);
     LAUNCHED(idx);
     CK(cudaStreamSynchronize(idx->stream));
     return MESSI_OK;
@@ -730,5 +788,80 @@ extern "C" messi_status messi_debug_distances(messi_index* idx, const float* que
                                                       d64_dev, lbk_dev);
     LAUNCHED(idx);
     CK(cudaStreamSynchronize(st));
+    return MESSI_OK;
+}
+
+// Scan throughput in isolation (tuning / roofline evidence): prologue for one query, then
+// `reps` coarse scans back to back on the main stream, each bracketed by CUDA events; the
+// survivor counter is reset between repetitions.  Returns the summed kernel milliseconds.
+__global__ void k_reset_coarse(QState* st)
+{
+    st->coarse_count = 0;
+    st->cand_count = 0;
+}
+
+extern "C" messi_status messi_debug_scan_repeat(messi_index* idx, const float* query_dev, int32_t reps, double* ms_out,
+                                                int64_t* coarse_out)
+{
+    g_err[0] = 0;
+    if (!idx || !query_dev || reps <= 0 || !ms_out) return fail(MESSI_EINVAL, "bad argument");
+    CK(cudaSetDevice(idx->device));
+    TRY(sync_all(idx));
+    Slot& sl = idx->slot[0];
+    cudaStream_t st = idx->stream;
+    const int n = idx->n;
+    const size_t qsm = (size_t)((n + 3) & ~3) * sizeof(float);
+    int len = (int)(idx->window < idx->N ? idx->window : idx->N);
+    int seed_grid = (len + 7) / 8;
+    if (seed_grid > 256) seed_grid = 256;
+    k_seed_ed<<<seed_grid, 256, qsm, st>>>(query_dev, n, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32,
+                                           idx->lo_w, idx->hi_w, sl.lut, sl.lut2, sl.st);
+    LAUNCHED(idx);
+    TRY(launch_tile_filter(idx, sl, st));
+    std::vector<cudaEvent_t> ev(2 * (size_t)reps);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    for (int r = 0; r < reps; ++r) {
+        k_reset_coarse<<<1, 1, 0, st>>>(sl.st);
+        CK(cudaEventRecord(ev[2 * r], st));
+        k_scan<SCAN_FINE><<<scan_grid(idx), 32 * kScanWarps, scan_smem(SCAN_FINE), st>>>(
+            idx->tiles, idx->ntiles, idx->N, sl.lut2, sl.lut, idx->symrows, sl.st, sl.coarse, nullptr, sl.tlist, idx->perm);
+        CK(cudaEventRecord(ev[2 * r + 1], st));
+    }
+    idx->launches += 2 * reps;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    double ms = 0.0;
+    for (int r = 0; r < reps; ++r) {
+        float t = 0.0f;
+        CK(cudaEventElapsedTime(&t, ev[2 * r], ev[2 * r + 1]));
+        ms += t;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (coarse_out) {
+        unsigned c[2] = {0, 0};
+        CK(cudaMemcpy(&c[0], &sl.st->coarse_count, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&c[1], &sl.st->tile_count, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        *coarse_out = (int64_t)c[0] | ((int64_t)c[1] << 32);
+    }
+    k_arm<<<1, 1, 0, st>>>(sl.st);
+    LAUNCHED(idx);
+    CK(cudaStreamSynchronize(st));
+    *ms_out = ms;
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_debug_tile_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev)
+{
+    g_err[0] = 0;
+    if (!idx || !query_dev || !lb_dev) return fail(MESSI_EINVAL, "NULL argument");
+    if (reach > idx->n) return fail(MESSI_EINVAL, "reach %d > n", reach);
+    CK(cudaSetDevice(idx->device));
+    TRY(sync_all(idx));
+    TRY(debug_prologue(idx, query_dev, reach));
+    Slot& sl = idx->slot[0];
+    k_tile_filter<<<filter_grid(idx), 256, 0, idx->stream>>>(idx->boxes, idx->ntiles, idx->n / MESSI_W, idx->lo_w,
+                                                            idx->hi_w, sl.st, nullptr, lb_dev);
+    LAUNCHED(idx);
+    CK(cudaStreamSynchronize(idx->stream));
     return MESSI_OK;
 }

@@ -29,10 +29,12 @@ struct QState {
     unsigned refined;       // real distances started
     unsigned abandoned;     // real distances abandoned early
     unsigned coarse_count;  // coarse-scan survivors appended
-    unsigned done;          // CTAs of the fused ED scan that finished (last one resolves)
+    unsigned done;          // CTAs of the refine stage that finished (last one resolves)
+    unsigned tile_count;    // tiles whose box bound <= BSF0 * (1 + eps) (scanned)
     unsigned long long qkey;  // query's approximate-search key
     int window_start;       // first sorted position of the approximate-search window
     int window_len;
+    double ubar[16], lbar[16];  // query PAA (ED: both) or envelope PAA (DTW), fp64
 };
 
 struct NearEntry { unsigned id; float d32; };
@@ -48,6 +50,7 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->abandoned = 0;
     st->coarse_count = 0;
     st->done = 0;
+    st->tile_count = 0;
 }
 
 __device__ __forceinline__ float warp_sum(float v)

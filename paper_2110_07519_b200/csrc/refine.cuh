@@ -70,51 +70,43 @@ __device__ void resolve_ed_block(const float* __restrict__ rows, int n, const fl
                                  const NearEntry* __restrict__ near, QState* st, long long N, long long row_begin,
                                  void* result, void* stats, double* sq, int wuse);
 
-// Dynamic shared memory of k_fine_ed: fine table + q, and room for >= 1 warp of the resolve.
-__host__ __device__ inline size_t fine_ed_smem(int n)
+// Dynamic shared memory of k_refine_ed: q, and room for up to 8 warps of the resolve.
+__host__ __device__ inline size_t refine_ed_smem(int n)
 {
-    size_t a = (size_t)MESSI_W * MESSI_CARD * sizeof(float) + (size_t)((n + 3) & ~3) * sizeof(float);
-    size_t b = (size_t)n * sizeof(double);
-    return a > b ? a : b;
+    const size_t a = (size_t)((n + 3) & ~3) * sizeof(float);
+    const size_t per = (size_t)n * sizeof(double);
+    size_t w = (96 * 1024) / per;
+    w = w < 1 ? 1 : (w > 8 ? 8 : w);
+    return a > per * w ? a : per * w;
 }
 
 // The ED refine stage of one query (runs on the refine stream, overlapping the next
-// query's scan).  Each warp takes 32 coarse survivors at a time: each lane loads its
-// series' 8-bit iSAX row (16 B) and evaluates the exact lower bound (fine_lb, Property 1
-// P:1766-1771) against the CURRENT BSF; the survivors' real distances follow
-// (refine_ed_pass).  The last CTA to finish re-ranks the near-best set exactly and writes
-// the query's result (A9).  Shared memory: fine table (16 KB) + q (n floats), reused by
-// the resolve.
-__global__ void __launch_bounds__(256) k_fine_ed(const uint2* __restrict__ coarse, const uint4* __restrict__ symrows,
-                                                 const float* __restrict__ lut_g, const float* __restrict__ rows, int n,
-                                                 const float* __restrict__ q_g, QState* st, NearEntry* near,
-                                                 long long N, long long row_begin, void* result, void* stats)
+// query's scan).  Input: the scan's candidates (id, exact 8-bit LB).  Each warp takes 32 at
+// a time, keeps those whose LB does not exceed the CURRENT BSF, and computes their real
+// distances (refine_ed_pass).  The last CTA to finish re-ranks the near-best set exactly
+// and writes the query's result (A9).  Shared memory: q (n floats), reused by the resolve.
+__global__ void __launch_bounds__(256) k_refine_ed(const uint2* __restrict__ cand, const unsigned* __restrict__ perm,
+                                                   const float* __restrict__ rows, int n, const float* __restrict__ q_g,
+                                                   QState* st, NearEntry* near, long long N, long long row_begin,
+                                                   void* result, void* stats)
 {
-    extern __shared__ __align__(16) float fsm[];
-    float* T = fsm;
-    float* q_s = fsm + MESSI_W * MESSI_CARD;
-    for (int i = threadIdx.x; i < MESSI_W * MESSI_CARD; i += blockDim.x) T[i] = lut_g[i];
+    extern __shared__ __align__(16) float q_s[];
     for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
     __syncthreads();
-    const unsigned total = *(volatile unsigned*)&st->coarse_count;
+    const unsigned total = *(volatile unsigned*)&st->cand_count;
     const int lane = threadIdx.x & 31;
     const unsigned wpb = blockDim.x >> 5;
-    unsigned n_fine = 0, n_ref = 0;
+    unsigned n_ref = 0;
     for (unsigned k0 = (blockIdx.x * wpb + (threadIdx.x >> 5)) * 32; k0 < total; k0 += gridDim.x * wpb * 32) {
         const bool valid = k0 + lane < total;
-        const uint2 e = valid ? coarse[k0 + lane] : make_uint2(0u, 0x7f800000u);
+        const uint2 e = valid ? cand[k0 + lane] : make_uint2(0u, 0x7f800000u);
         const float thr = slack_up(ld_bsf(st));
-        bool ok = valid && __uint_as_float(e.y) <= thr;
-        if (ok) ok = fine_lb(symrows[e.x], T) <= thr;
+        const bool ok = valid && __uint_as_float(e.y) <= thr;
         const unsigned pass = __ballot_sync(0xffffffffu, ok);
-        n_fine += __popc(pass);
         n_ref += __popc(pass);
-        refine_ed_pass(pass, e.x, rows, n, q_s, st, near, lane);
+        refine_ed_pass(pass, ok ? perm[e.x] : 0u, rows, n, q_s, st, near, lane);
     }
-    if (lane == 0 && n_fine) {
-        atomicAdd(&st->cand_count, n_fine);
-        atomicAdd(&st->refined, n_ref);
-    }
+    if (lane == 0 && n_ref) atomicAdd(&st->refined, n_ref);
     __shared__ bool last;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -125,7 +117,7 @@ __global__ void __launch_bounds__(256) k_fine_ed(const uint2* __restrict__ coars
     if (!last) return;
     __threadfence();
     extern __shared__ __align__(16) double dsq[];
-    int wuse = (int)(fine_ed_smem(n) / ((size_t)n * sizeof(double)));
+    int wuse = (int)(refine_ed_smem(n) / ((size_t)n * sizeof(double)));
     wuse = wuse < 1 ? 1 : (wuse > (int)wpb ? (int)wpb : wuse);
     resolve_ed_block(rows, n, q_g, near, st, N, row_begin, result, stats, dsq, wuse);
 }
@@ -135,6 +127,7 @@ __global__ void __launch_bounds__(256) k_fine_ed(const uint2* __restrict__ coars
 // LB <= BSF*(1+eps) (counted as candidates) get the raw LB_Keogh against the query
 // envelope, four rows in flight per warp; survivors go to list2 as (id, LBK).
 __global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ coarse, const uint4* __restrict__ symrows,
+                                                    const unsigned* __restrict__ perm,
                                                     const float* __restrict__ lut_g, const float* __restrict__ rows, int n,
                                                     const float* __restrict__ U_g, const float* __restrict__ L_g,
                                                     QState* st, uint2* __restrict__ list2)
@@ -156,6 +149,7 @@ __global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ co
         const uint2 e = valid ? coarse[k0 + lane] : make_uint2(0u, 0x7f800000u);
         bool ok = valid && __uint_as_float(e.y) <= thr;
         if (ok) ok = fine_lb(symrows[e.x], T) <= thr;
+        const unsigned rid = ok ? perm[e.x] : 0u;
         unsigned todo = __ballot_sync(0xffffffffu, ok);
         n_fine += __popc(todo);
         unsigned passmask = 0;
@@ -169,7 +163,7 @@ __global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ co
                 gok[g] = todo != 0;
                 src[g] = gok[g] ? __ffs(todo) - 1 : 0;
                 todo &= todo - 1;
-                id[g] = __shfl_sync(0xffffffffu, e.x, src[g]);
+                id[g] = __shfl_sync(0xffffffffu, rid, src[g]);
             }
             float acc[kRefineGroup];
 #pragma unroll
@@ -208,7 +202,7 @@ __global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ co
             if (lane == 0) base = atomicAdd(&st->list2_count, (unsigned)__popc(passmask));
             base = __shfl_sync(0xffffffffu, base, 0);
             if (passmask & (1u << lane))
-                list2[base + __popc(passmask & ((1u << lane) - 1))] = make_uint2(e.x, __float_as_uint(mylbk));
+                list2[base + __popc(passmask & ((1u << lane) - 1))] = make_uint2(rid, __float_as_uint(mylbk));
         }
     }
     if (lane == 0 && n_fine) atomicAdd(&st->cand_count, n_fine);
@@ -351,7 +345,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
                              void* result, void* stats)
 {
     struct R { double dist; long long id; double d2; long long reserved; };
-    struct S { long long lb, coarse, cand, lbk, refined, abandoned, near; double seed, bsf; };
+    struct S { long long lb, tiles, coarse, cand, lbk, refined, abandoned, near; double seed, bsf; };
     R* res = reinterpret_cast<R*>(result);
     res->dist = b.id >= 0 ? sqrt(b.d) : (double)INFINITY;
     res->id = b.id >= 0 ? row_begin + b.id : -1;
@@ -360,6 +354,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
     if (stats) {
         S* s = reinterpret_cast<S*>(stats);
         s->lb = N;
+        s->tiles = st->tile_count;
         s->coarse = st->coarse_count;
         s->cand = st->cand_count;
         s->lbk = st->list2_count;

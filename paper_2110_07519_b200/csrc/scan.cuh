@@ -17,7 +17,7 @@ namespace messi {
 __device__ void prologue_block(const float* __restrict__ q, int n, int reach, const float* __restrict__ beta_g,
                                const float* __restrict__ lo_w, const float* __restrict__ hi_w,
                                float* __restrict__ lut_g, float* __restrict__ U_g, float* __restrict__ L_g,
-                               unsigned long long* key_out, float* __restrict__ lut2_g)
+                               unsigned long long* key_out, float* __restrict__ lut2_g, QState* st)
 {
     __shared__ double ubar[MESSI_W], lbar[MESSI_W];
     __shared__ float beta[256];
@@ -48,6 +48,10 @@ __device__ void prologue_block(const float* __restrict__ q, int n, int reach, co
             double qbar = __ddiv_rn(sq, (double)m);
             ubar[s] = reach >= 0 ? __ddiv_rn(su, (double)m) : qbar;
             lbar[s] = reach >= 0 ? __ddiv_rn(sl, (double)m) : qbar;
+            if (lut_g) {  // for the tile filter
+                st->ubar[s] = ubar[s];
+                st->lbar[s] = lbar[s];
+            }
             sym = symbol_of(__double2float_rn(qbar), beta);
         }
         unsigned long long key = 0;
@@ -118,7 +122,8 @@ __global__ void __launch_bounds__(256) k_seed_ed(const float* __restrict__ q_g, 
     __shared__ unsigned long long qkey_s;
     for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
     __syncthreads();
-    prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, blockIdx.x == 0 ? lut_g : nullptr, nullptr, nullptr, &qkey_s, lut2_g);
+    prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, blockIdx.x == 0 ? lut_g : nullptr, nullptr, nullptr, &qkey_s, lut2_g,
+                   st);
     __syncthreads();
     const unsigned long long qkey = qkey_s;
     long long a = block_lower_bound(skey, N, qkey);
@@ -157,9 +162,9 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
     for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
     __syncthreads();
     if (blockIdx.x == 0)
-        prologue_block(q_s, n, reach, beta_g, lo_w, hi_w, lut_g, U_g, L_g, &qkey_s, lut2_g);
+        prologue_block(q_s, n, reach, beta_g, lo_w, hi_w, lut_g, U_g, L_g, &qkey_s, lut2_g, st);
     else
-        prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, nullptr, nullptr, nullptr, &qkey_s, nullptr);
+        prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, nullptr, nullptr, nullptr, &qkey_s, nullptr, st);
     __syncthreads();
     const unsigned long long qkey = qkey_s;
     long long a = block_lower_bound(skey, N, qkey);
@@ -188,36 +193,92 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
     }
 }
 
+// ---------------------------------------------------------------------- tile filter
+// MESSI's node pruning (Alg. 7 TraverseRootSubtree: "if FindDist(node) > BSF then prune",
+// P:1117-1143) on the flat tile array: the box of a tile (per segment the min and max
+// 8-bit symbol of its 512 sorted series) contains every member's symbol box, so
+// m * sum_s max(0, lo(min_s) - Ubar_s, Lbar_s - hi(max_s))^2 (fp64) lower-bounds every
+// member's bound and distance (Property 1/2).  Tiles whose bound exceeds
+// BSF0 * (1 + eps) are skipped; the others are listed (one thread per tile) for the scan.
+__global__ void k_tile_filter(const unsigned char* __restrict__ boxes, long long ntiles, int m,
+                              const float* __restrict__ lo_w, const float* __restrict__ hi_w, QState* st,
+                              unsigned* __restrict__ list, float* __restrict__ lb_all)
+{
+    __shared__ float lo[256], hi[256];
+    __shared__ double ub[16], lb[16];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) { lo[i] = lo_w[i]; hi[i] = hi_w[i]; }
+    if (threadIdx.x < 16) { ub[threadIdx.x] = st->ubar[threadIdx.x]; lb[threadIdx.x] = st->lbar[threadIdx.x]; }
+    __syncthreads();
+    const double thr = (double)slack_up(ld_bsf(st));
+    const int lane = threadIdx.x & 31;
+    for (long long t0 = (long long)blockIdx.x * blockDim.x; t0 < ntiles; t0 += (long long)gridDim.x * blockDim.x) {
+        const long long t = t0 + threadIdx.x;
+        bool keep = false;
+        double acc = 0.0;
+        if (t < ntiles) {
+            const uint4 mn = *reinterpret_cast<const uint4*>(boxes + t * 32);
+            const uint4 mx = *reinterpret_cast<const uint4*>(boxes + t * 32 + 16);
+            const unsigned a[4] = {mn.x, mn.y, mn.z, mn.w}, b[4] = {mx.x, mx.y, mx.z, mx.w};
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const unsigned vmin = (a[s >> 2] >> (8 * (s & 3))) & 255u, vmax = (b[s >> 2] >> (8 * (s & 3))) & 255u;
+                const double d = fmax(0.0, fmax((double)lo[vmin] - ub[s], lb[s] - (double)hi[vmax]));
+                acc += d * d;
+            }
+            acc *= (double)m;
+            keep = acc <= thr;
+            if (lb_all) lb_all[t] = (float)acc;
+        }
+        if (list) {
+            const unsigned msk = __ballot_sync(0xffffffffu, keep);
+            unsigned base = 0;
+            if (lane == 0 && msk) base = atomicAdd(&st->tile_count, (unsigned)__popc(msk));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (keep) list[base + __popc(msk & ((1u << lane) - 1))] = (unsigned)t;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------- lower-bound scan
 // The HBM-roofline step (A5): Alg. 9 line LowerBound_SIMD / Alg. 10 line
 // LowerBound_DTW_SIMD evaluated for EVERY series, like ParIS+'s SIMS scan
-// (P:432-443), in two resolutions of the same iSAX word.  This kernel streams the coarse
+// (P:432-443), in two resolutions of the same iSAX word.  The kernel streams the coarse
 // tiles (8 B per series: top nibbles, two segments per byte) and sums, per series, the 8
 // pair-table entries T2[p][byte] (round-down adds) -- the iSAX lower bound at cardinality
-// 16, which never exceeds the 8-bit one.  Series with coarse LB <= BSF*(1+eps) go to a
-// global list (warp ballot + prefix + one atomicAdd per warp-tile); the exact 8-bit bound
-// is applied to them by the refine stage (k_fine_ed / k_lbk_filter).
+// 16, which never exceeds the 8-bit one.
 // Shared-memory table: 64 KB, word v*64 + 8c + p holds T2[p][v] (4 copies c); the lane
 // owning block b reads pair p = (t + b) mod 8 at step t and uses copy c = b >> 3, so the 32
 // lanes hit 32 distinct banks for any byte values.  PRMT builds the byte address
 // (v << 8 | base) from the packed pair bytes in one instruction.
-//   SCAN_COMPACT: survivors -> global list;   SCAN_ALL: every coarse LB written (inspection).
-enum { SCAN_COMPACT = 0, SCAN_ALL = 1 };
-#ifndef MESSI_SCAN_WARPS
-#define MESSI_SCAN_WARPS 8
-#endif
-#ifndef MESSI_SCAN_MINB
-#define MESSI_SCAN_MINB 2
-#endif
-#ifndef MESSI_SCAN_PREFETCH
-#define MESSI_SCAN_PREFETCH 0
-#endif
-constexpr int kScanWarps = MESSI_SCAN_WARPS;
+//   SCAN_COMPACT: coarse survivors -> global list (warp ballot + prefix, one atomicAdd per
+//                 warp-tile); the exact 8-bit bound follows in k_lbk_filter (DTW).
+//   SCAN_ALL:     every coarse LB written out (inspection).
+//   SCAN_FINE:    coarse survivors' 8-bit words (16 B symbol rows) are loaded right after
+//                 the tile and consumed one tile later (the load latency hides behind the
+//                 next tile), their exact bound evaluated against the fine table (16 KB,
+//                 shared memory), and only those passing it are appended to the candidate
+//                 list -- the refine stage then touches ~0.1% of the rows only (ED).
+enum { SCAN_COMPACT = 0, SCAN_ALL = 1, SCAN_FINE = 2 };
+constexpr int kScanWarps = 8;
 constexpr size_t kScanLutBytes = (size_t)MESSI_CARD * 64 * sizeof(float);
+constexpr size_t kFineLutBytes = (size_t)MESSI_W * MESSI_CARD * sizeof(float);
+constexpr int kPend = 2;  // coarse survivors per lane carried to the next tile
+
+#ifndef MESSI_SCAN_NOCOMPUTE
+#define MESSI_SCAN_NOCOMPUTE 0
+#endif
 
 // Coarse bound of the 16 series of one lane for one tile already in registers.
 __device__ __forceinline__ void coarse_tile(const uint4 (&data)[8], const char* lbase, int lane, float (&acc)[16])
 {
+#if MESSI_SCAN_NOCOMPUTE  // bandwidth probe only: touch the data, no table lookups
+    unsigned x = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) x ^= data[t].x ^ data[t].y ^ data[t].z ^ data[t].w;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = x == 0x12345678u ? -1.0f : 1e30f;
+    return;
+#endif
     const int cpy = lane >> 3;
 #pragma unroll
     for (int k = 0; k < 16; ++k) acc[k] = 0.0f;
@@ -236,91 +297,8 @@ __device__ __forceinline__ void coarse_tile(const uint4 (&data)[8], const char* 
     }
 }
 
-template <int MODE>
-__device__ __forceinline__ void coarse_emit(const float (&acc)[16], long long tl, long long N, float thr, int lane,
-                                            QState* st, uint2* __restrict__ out, float* __restrict__ lb_all)
-{
-    const long long id0 = tl * MESSI_TILE_ROWS + lane * 16;
-    if (MODE == SCAN_ALL) {
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if (id0 + k < N) lb_all[id0 + k] = acc[k];
-        return;
-    }
-    unsigned mask = 0;
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-        if (acc[k] <= thr && id0 + k < N) mask |= 1u << k;
-    if (!__any_sync(0xffffffffu, mask)) return;
-    const int cnt = __popc(mask);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(&st->coarse_count, (unsigned)total);
-    unsigned pos = __shfl_sync(0xffffffffu, base, 0) + incl - cnt;
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-        if (mask & (1u << k)) out[pos++] = make_uint2((unsigned)(id0 + k), __float_as_uint(acc[k]));
-}
-
-// Each warp walks its tiles (grid-stride); with MESSI_SCAN_PREFETCH the NEXT tile's eight
-// 128-bit loads are issued before the current tile's lookups (8 KB per warp in flight).
-template <int MODE>
-__global__ void __launch_bounds__(32 * kScanWarps, MESSI_SCAN_MINB) k_scan(const uint4* __restrict__ tiles, long long ntiles, long long N,
-                                                 const float* __restrict__ lut2_g, QState* st,
-                                                 uint2* __restrict__ out, float* __restrict__ lb_all)
-{
-    extern __shared__ __align__(16) float lut_s[];  // 256 * 64 floats
-    for (int i = threadIdx.x; i < MESSI_PAIRS * MESSI_CARD; i += blockDim.x) {
-        const int pr = i >> 8, v = i & 255;
-        const float val = lut2_g[i];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) lut_s[v * 64 + 8 * c + pr] = val;
-    }
-    __syncthreads();
-    const float thr = MODE == SCAN_ALL ? INFINITY : slack_up(ld_bsf(st));
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const char* lbase = reinterpret_cast<const char*>(lut_s);
-    const long long stride = (long long)gridDim.x * kScanWarps;
-    long long tl = (long long)blockIdx.x * kScanWarps + warp;
-    float acc[16];
-    auto load = [&](uint4 (&d)[8], long long t) {
-        const uint4* tp = tiles + t * (MESSI_TILE_BYTES / 16) + lane;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) d[i] = __ldcs(tp + i * 32);
-    };
-#if !MESSI_SCAN_PREFETCH
-    for (; tl < ntiles; tl += stride) {
-        uint4 a[8];
-        load(a, tl);
-        coarse_tile(a, lbase, lane, acc);
-        coarse_emit<MODE>(acc, tl, N, thr, lane, st, out, lb_all);
-    }
-    return;
-#endif
-    uint4 a[8], b[8];
-    if (tl < ntiles) load(a, tl);
-    while (tl < ntiles) {
-        const long long t1 = tl + stride;
-        if (t1 < ntiles) load(b, t1);
-        coarse_tile(a, lbase, lane, acc);
-        coarse_emit<MODE>(acc, tl, N, thr, lane, st, out, lb_all);
-        if (t1 >= ntiles) break;
-        const long long t2 = t1 + stride;
-        if (t2 < ntiles) load(a, t2);
-        coarse_tile(b, lbase, lane, acc);
-        coarse_emit<MODE>(acc, t1, N, thr, lane, st, out, lb_all);
-        tl = t2;
-    }
-}
-
 // Exact (8-bit) lower bound of one series from its symbol row: sum_s T[s][sym_s], s in
-// order, round-down adds.  T: the fine table [16][256] in shared memory.
+// order, round-down adds.  T: the fine table [16][256].
 __device__ __forceinline__ float fine_lb(uint4 sr, const float* __restrict__ T)
 {
     const unsigned w[4] = {sr.x, sr.y, sr.z, sr.w};
@@ -330,15 +308,144 @@ __device__ __forceinline__ float fine_lb(uint4 sr, const float* __restrict__ T)
     return acc;
 }
 
-// Inspection: the fine bound of every row (one thread per row).
-__global__ void k_fine_all(const uint4* __restrict__ symrows, long long N, const float* __restrict__ lut_g,
-                           float* __restrict__ lb_all)
+// Warp-aggregated append of (id, value) pairs held by the lanes with `ok` set.
+__device__ __forceinline__ void warp_append(bool ok, unsigned id, float v, unsigned* counter, uint2* __restrict__ out,
+                                            int lane)
+{
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    if (!m) return;
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(counter, (unsigned)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (ok) out[base + __popc(m & ((1u << lane) - 1))] = make_uint2(id, __float_as_uint(v));
+}
+
+// Positions are SORTED positions p (row = perm[p]); the refine stages translate.  The scan
+// visits the tiles listed by k_tile_filter (SCAN_ALL: every tile, LBs scattered to rows).
+template <int MODE>
+__global__ void __launch_bounds__(32 * kScanWarps, 2) k_scan(const uint4* __restrict__ tiles, long long ntiles,
+                                                             long long N, const float* __restrict__ lut2_g,
+                                                             const float* __restrict__ lut_g,
+                                                             const uint4* __restrict__ symrows, QState* st,
+                                                             uint2* __restrict__ out, float* __restrict__ lb_all,
+                                                             const unsigned* __restrict__ tlist,
+                                                             const unsigned* __restrict__ perm)
+{
+    extern __shared__ __align__(16) float lut_s[];  // 256 * 64 floats (+ fine table in SCAN_FINE)
+    float* T = lut_s + MESSI_CARD * 64;
+    for (int i = threadIdx.x; i < MESSI_PAIRS * MESSI_CARD; i += blockDim.x) {
+        const int pr = i >> 8, v = i & 255;
+        const float val = lut2_g[i];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) lut_s[v * 64 + 8 * c + pr] = val;
+    }
+    if (MODE == SCAN_FINE)
+        for (int i = threadIdx.x; i < MESSI_W * MESSI_CARD; i += blockDim.x) T[i] = lut_g[i];
+    __syncthreads();
+    const float thr = MODE == SCAN_ALL ? INFINITY : slack_up(ld_bsf(st));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const char* lbase = reinterpret_cast<const char*>(lut_s);
+    const long long stride = (long long)gridDim.x * kScanWarps;
+    unsigned n_coarse = 0;
+    // SCAN_FINE: coarse survivors carried to the next tile (their symbol rows in flight)
+    unsigned pid[kPend];
+    uint4 psr[kPend];
+    int npend = 0;
+    const long long count = MODE == SCAN_ALL ? ntiles : (long long)*(volatile unsigned*)&st->tile_count;
+    for (long long it = (long long)blockIdx.x * kScanWarps + warp;; it += stride) {
+        const bool have = it < count;
+        const long long tl = MODE == SCAN_ALL ? it : (have ? (long long)tlist[it] : 0);
+        float acc[16];
+        if (have) {
+            const uint4* tp = tiles + tl * (MESSI_TILE_BYTES / 16) + lane;
+            uint4 data[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) data[i] = __ldcs(tp + i * 32);
+            coarse_tile(data, lbase, lane, acc);
+        }
+        if (MODE == SCAN_FINE) {  // the previous tile's survivors: exact bound, then append
+#pragma unroll
+            for (int j = 0; j < kPend; ++j) {
+                bool ok = j < npend;
+                float f = 0.0f;
+                if (ok) {
+                    f = fine_lb(psr[j], T);
+                    ok = f <= thr;
+                }
+                warp_append(ok, pid[j], f, &st->cand_count, out, lane);
+            }
+            npend = 0;
+        }
+        if (!__any_sync(0xffffffffu, have)) break;
+        if (!have) continue;
+        const long long id0 = tl * MESSI_TILE_ROWS + lane * 16;
+        if (MODE == SCAN_ALL) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (id0 + k < N) lb_all[perm[id0 + k]] = acc[k];
+            continue;
+        }
+        unsigned mask = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (acc[k] <= thr && id0 + k < N) mask |= 1u << k;
+        if (MODE == SCAN_FINE) {
+            n_coarse += __popc(mask);
+            // up to kPend survivors: issue their symbol-row loads now, consume next tile
+#pragma unroll
+            for (int j = 0; j < kPend; ++j) {
+                if (mask) {
+                    const int k = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    pid[j] = (unsigned)(id0 + k);
+                    psr[j] = __ldg(symrows + id0 + k);
+                    npend = j + 1;
+                }
+            }
+            // rare overflow: the rest synchronously
+            while (mask) {
+                const int k = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const float f = fine_lb(__ldg(symrows + id0 + k), T);
+                if (f <= thr) {
+                    const unsigned pos = atomicAdd(&st->cand_count, 1u);
+                    out[pos] = make_uint2((unsigned)(id0 + k), __float_as_uint(f));
+                }
+            }
+            continue;
+        }
+        // SCAN_COMPACT
+        if (!__any_sync(0xffffffffu, mask)) continue;
+        const int cnt = __popc(mask);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(&st->coarse_count, (unsigned)total);
+        unsigned pos = __shfl_sync(0xffffffffu, base, 0) + incl - cnt;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (mask & (1u << k)) out[pos++] = make_uint2((unsigned)(id0 + k), __float_as_uint(acc[k]));
+    }
+    if (MODE == SCAN_FINE) {
+        n_coarse = __reduce_add_sync(0xffffffffu, n_coarse);
+        if (lane == 0 && n_coarse) atomicAdd(&st->coarse_count, n_coarse);
+    }
+}
+
+// Inspection: the fine bound of every row (one thread per sorted position).
+__global__ void k_fine_all(const uint4* __restrict__ symrows, const unsigned* __restrict__ perm, long long N,
+                           const float* __restrict__ lut_g, float* __restrict__ lb_all)
 {
     __shared__ float T[MESSI_W * MESSI_CARD];
     for (int i = threadIdx.x; i < MESSI_W * MESSI_CARD; i += blockDim.x) T[i] = lut_g[i];
     __syncthreads();
-    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += (long long)gridDim.x * blockDim.x)
-        lb_all[r] = fine_lb(symrows[r], T);
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x)
+        lb_all[perm[p]] = fine_lb(symrows[p], T);
 }
 
 }  // namespace messi

@@ -27,17 +27,21 @@ __global__ void k_breakpoints(float* beta32, float* lo_w, float* hi_w)
     hi_w[v] = v == 255 ? INFINITY : nextafterf(b[v], INFINITY);
 }
 
-// Two resolutions of the same iSAX words (the bit-prefix property of variable-cardinality
-// iSAX, P:387-392 / P:408-417: the first b bits of an 8-bit symbol are the symbol at
-// cardinality 2^b):
-//  * symrows [Npad][16] u8: the full 8-bit word of every series, series-major (16 B).
-//  * coarse tiles (4 KB per 512 series): the top nibble of every symbol, two segments per
-//    byte -- byte = hi(sym_2p) << 4 | hi(sym_2p+1) for pair p -- 8 B per series, in a
-//    skewed tile layout.  Block b = 16 series (b < 32); tile row t (512 B) holds, at byte
-//    offset 16*b, the pair bytes of pair p = (t + b) mod 8 of block b's 16 series.  A warp
-//    reading tile row t (lane b loads 16 B) therefore gets 8 different pairs across each
-//    group of 8 lanes; with the coarse table replicated 4 times (copy b >> 3) the 32 lanes
-//    hit 32 distinct shared-memory banks whatever the symbol values.
+// Summaries in APPROXIMATE-SEARCH ORDER.  After the key sort every summary is stored at its
+// sorted position p (row = perm[p]); consecutive positions share the leading bit planes of
+// the interleaved key, i.e. they sit in the same subtree of the variable-cardinality iSAX
+// tree, and a tile of 512 consecutive positions is the analogue of a leaf node.
+//  * symrows [Npad][16] u8: the full 8-bit word, series-major (16 B), sorted.
+//  * coarse tiles (4 KB per 512 positions): the top nibble of every symbol (the symbol at
+//    cardinality 16 -- bit-prefix property), two segments per byte:
+//    byte = hi(sym_2p) << 4 | hi(sym_2p+1) for pair p, 8 B per series, in a skewed layout:
+//    block b = 16 series (b < 32); tile row t (512 B) holds, at byte offset 16*b, the pair
+//    bytes of pair p = (t + b) mod 8 of block b's 16 series.  A warp reading tile row t
+//    (lane b loads 16 B) gets 8 different pairs across each group of 8 lanes; with the
+//    coarse table replicated 4 times (copy b >> 3) the 32 lanes hit 32 distinct shared
+//    memory banks whatever the symbol values.
+//  * boxes [ntiles][32] u8: per segment, the min and max 8-bit symbol of the tile -- the
+//    tile's iSAX node summary (its "node" in Alg. 7's FindDist).
 __device__ __forceinline__ int coarse_offset(int rr, int pair)
 {
     int b = rr >> 4, k = rr & 15;
@@ -45,20 +49,18 @@ __device__ __forceinline__ int coarse_offset(int rr, int pair)
     return t * 512 + b * 16 + k;
 }
 
-// One CTA (256 threads) summarises one tile of 512 rows per iteration.  Lane (h2, s) of a
+// One CTA (256 threads) summarises 512 rows per iteration (row order).  Lane (h2, s) of a
 // warp takes segment s of row 2*pair + h2; the segment mean is an fp64 sequential sum
 // (reading R5: the same operation order as the oracle, so PAA and symbols are bit-exact),
 // divided by m and rounded once to fp32.  The approximate-search key interleaves the top
 // 4 bits of the 16 symbols, most significant bit plane first: bits 63..48 are the root
 // subtree of P:711 (one bit per segment), each further plane refines it like a split.
 __global__ void __launch_bounds__(256) k_summarise(const float* __restrict__ rows, int64_t N, int n,
-                                                   const float* __restrict__ beta_g, uint4* __restrict__ tiles,
-                                                   uint4* __restrict__ symrows, int64_t ntiles,
-                                                   unsigned long long* __restrict__ keys, unsigned* __restrict__ ids,
-                                                   float* __restrict__ paa)
+                                                   const float* __restrict__ beta_g, uint4* __restrict__ symrows_tmp,
+                                                   int64_t ntiles, unsigned long long* __restrict__ keys,
+                                                   unsigned* __restrict__ ids, float* __restrict__ paa)
 {
     __shared__ float beta[256];
-    __shared__ __align__(16) unsigned char tile[MESSI_TILE_BYTES];
     __shared__ __align__(16) unsigned char srow[MESSI_TILE_ROWS * MESSI_W];
     const int m = n / MESSI_W;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -92,9 +94,6 @@ __global__ void __launch_bounds__(256) k_summarise(const float* __restrict__ row
                 if (paa) paa[row * MESSI_W + s] = p32;
             }
             srow[rr * MESSI_W + s] = (unsigned char)sym;
-            // pair byte: even lane s takes its odd neighbour's top nibble
-            const int nb = __shfl_down_sync(0xffffffffu, sym, 1);
-            if ((s & 1) == 0) tile[coarse_offset(rr, s >> 1)] = (unsigned char)((sym & 0xf0) | (nb >> 4));
             unsigned long long key = 0;
 #pragma unroll
             for (int bit = 7; bit >= 4; --bit) {
@@ -107,23 +106,69 @@ __global__ void __launch_bounds__(256) k_summarise(const float* __restrict__ row
             }
         }
         __syncthreads();
-        uint4* dst = tiles + tl * (MESSI_TILE_BYTES / 16);
-        for (int i = threadIdx.x; i < MESSI_TILE_BYTES / 16; i += blockDim.x)
-            dst[i] = reinterpret_cast<const uint4*>(tile)[i];
-        uint4* sdst = symrows + tl * MESSI_TILE_ROWS;
+        uint4* sdst = symrows_tmp + tl * MESSI_TILE_ROWS;
         for (int i = threadIdx.x; i < MESSI_TILE_ROWS; i += blockDim.x)
             sdst[i] = reinterpret_cast<const uint4*>(srow)[i];
     }
 }
 
-// Inverse of the coarse layout (inspection): the pair bytes of every row, [N][8].
-__global__ void k_detile_coarse(const unsigned char* __restrict__ tiles, int64_t N, unsigned char* __restrict__ out)
+// Lays the summaries out in sorted order: one CTA (512 threads) per tile of 512 sorted
+// positions gathers its rows' 8-bit words, writes them, the coarse tile and the box.
+__global__ void __launch_bounds__(512) k_layout(const uint4* __restrict__ symrows_tmp, const unsigned* __restrict__ perm,
+                                                int64_t N, uint4* __restrict__ symrows, uint4* __restrict__ tiles,
+                                                unsigned char* __restrict__ boxes)
 {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ __align__(16) unsigned char tile[MESSI_TILE_BYTES];
+    __shared__ unsigned bmin[MESSI_W], bmax[MESSI_W];
+    const int i = threadIdx.x;
+    const int64_t tl = blockIdx.x;
+    const int64_t p = tl * MESSI_TILE_ROWS + i;
+    if (i < MESSI_W) { bmin[i] = 255; bmax[i] = 0; }
+    __syncthreads();
+    const bool valid = p < N;
+    const uint4 sr = valid ? symrows_tmp[perm[p]] : make_uint4(0, 0, 0, 0);
+    symrows[p] = sr;
+    const unsigned w[4] = {sr.x, sr.y, sr.z, sr.w};
+    unsigned sym[MESSI_W];
+#pragma unroll
+    for (int s = 0; s < MESSI_W; ++s) sym[s] = (w[s >> 2] >> (8 * (s & 3))) & 255u;
+#pragma unroll
+    for (int pr = 0; pr < MESSI_PAIRS; ++pr)
+        tile[coarse_offset(i, pr)] = (unsigned char)((sym[2 * pr] & 0xf0u) | (sym[2 * pr + 1] >> 4));
+    if (valid) {
+#pragma unroll
+        for (int s = 0; s < MESSI_W; ++s) {
+            atomicMin(&bmin[s], sym[s]);
+            atomicMax(&bmax[s], sym[s]);
+        }
+    }
+    __syncthreads();
+    uint4* dst = tiles + tl * (MESSI_TILE_BYTES / 16);
+    if (i < MESSI_TILE_BYTES / 16) dst[i] = reinterpret_cast<const uint4*>(tile)[i];
+    if (i < MESSI_W) {
+        boxes[tl * 32 + i] = (unsigned char)bmin[i];
+        boxes[tl * 32 + 16 + i] = (unsigned char)bmax[i];
+    }
+}
+
+// Inspection: the 8-bit words back in row order, out[row][16].
+__global__ void k_unsort_sym(const uint4* __restrict__ symrows, const unsigned* __restrict__ perm, int64_t N,
+                             uint4* __restrict__ out)
+{
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < N) out[perm[p]] = symrows[p];
+}
+
+// Inspection: the coarse pair bytes back in row order, out[row][8].
+__global__ void k_detile_coarse(const unsigned char* __restrict__ tiles, const unsigned* __restrict__ perm, int64_t N,
+                                unsigned char* __restrict__ out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N * MESSI_PAIRS) return;
-    int64_t row = i / MESSI_PAIRS;
-    int pair = (int)(i % MESSI_PAIRS);
-    out[i] = tiles[(row / MESSI_TILE_ROWS) * MESSI_TILE_BYTES + coarse_offset((int)(row % MESSI_TILE_ROWS), pair)];
+    const int64_t p = i / MESSI_PAIRS;
+    const int pair = (int)(i % MESSI_PAIRS);
+    out[(int64_t)perm[p] * MESSI_PAIRS + pair] =
+        tiles[(p / MESSI_TILE_ROWS) * MESSI_TILE_BYTES + coarse_offset((int)(p % MESSI_TILE_ROWS), pair)];
 }
 
 }  // namespace messi

@@ -135,6 +135,32 @@ def test_lower_bounds_ed(c1):
         assert np.all(np.abs(cl[rows] - ref16) <= _lb_tol(d16, 16) + 2.0 ** -20 * ref16)
 
 
+@pytest.mark.parametrize("reach", [-1, 25])
+def test_tile_box_bounds(c1, reach):
+    """The box of a tile (512 consecutive series in approximate-search order) bounds every
+    member from below: tile LB <= each member's 8-bit bound <= its true distance (the node
+    test of Alg. 7; Property 2)."""
+    X, Q, idx, Xh, Qh = c1
+    N = X.shape[0]
+    ntiles = (N + 511) // 512
+    _, perm = messi().messi_debug_order(idx.handle, N, X.device)
+    perm = perm.cpu().numpy().astype(np.int64)
+    tlb = messi().messi_debug_tile_bounds(idx.handle, Q[0].contiguous(), reach, ntiles).cpu().numpy()
+    flb = messi().messi_debug_lower_bounds(idx.handle, Q[0].contiguous(), reach, N).cpu().numpy()
+    member_min = np.full(ntiles, np.inf)
+    np.minimum.at(member_min, np.arange(N) // 512, flb[perm])
+    assert np.all(tlb <= member_min * (1 + 1e-6) + 1e-6)
+    if reach < 0:
+        ed = oracle.ed2_rows(Xh, Qh[0])
+        tmin = np.full(ntiles, np.inf)
+        np.minimum.at(tmin, np.arange(N) // 512, ed[perm])
+        assert np.all(tlb <= tmin)
+    # the filter keeps a minority of tiles at the NN distance (pruning is real)
+    d2, _ = oracle.nn("ed", Xh, Qh[:1])
+    if reach < 0:
+        assert np.mean(tlb <= d2[0]) < 0.8
+
+
 def test_lower_bounds_dtw(c1):
     X, Q, idx, Xh, Qh = c1
     _, S = oracle.isax_rows(Xh[:4000])
