@@ -299,13 +299,9 @@ def ours(args):
     # (DESIGN.md "Roofline"); achieved = those bytes over the kernel's own event time
     st = main["stats"]
     mean = lambda k: sum(s[k] for s in st) / len(st)  # noqa: E731
-    # tiles that survive the box filter are streamed (4 KB each); ED also gathers one 32 B
-    # sector of 8-bit word per coarse survivor inside the scan; DTW writes (pos, LB) per
-    # coarse survivor
-    if cfg["reach"] is None:
-        scan_bytes = 4096 * mean("tiles_scanned") + 32 * mean("coarse_pass") + 8 * mean("candidates")
-    else:
-        scan_bytes = 4096 * mean("tiles_scanned") + 8 * mean("coarse_pass")
+    # the tiles that survive the box filter are streamed (8 KB each: 16 B per series) and
+    # each candidate is written as (position, LB): 8 B
+    scan_bytes = 8192 * mean("tiles_scanned") + 8 * mean("candidates")
     achieved = scan_bytes * scan_n / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
     peak = pk.get("hbm_gbs", 6650.0)
     traffic = None
@@ -317,7 +313,9 @@ def ours(args):
     # whole-query algorithmic bytes per GPU: coarse stream + one 32 B sector of 8-bit word per
     # coarse survivor + the rows refined + the approximate-search window rows
     ntiles = (main["N_local"] + 511) // 512
-    per_query_bytes = (32 * ntiles + 4096 * mean("tiles_scanned") + 32 * mean("coarse_pass")
+    # whole-query algorithmic bytes per GPU: tile boxes + surviving tiles + candidate list
+    # (written, read) + the rows refined + the approximate-search window rows
+    per_query_bytes = (32 * ntiles + 8192 * mean("tiles_scanned") + 16 * mean("candidates")
                        + 4 * main["n"] * mean("refined") + 4 * main["n"] * min(2000, main["N_local"]))
     steps_total = {k: max_over_ranks(v[0], world) for k, v in main["prof"].items()}
     line = {
@@ -327,7 +325,7 @@ def ours(args):
         "dtype": "f32", "data": "synthetic (seeded device Philox random walks, z-normalised)",
         "config": {"workload": cfg["name"], "mode": args.mode, "rows": cfg["N"], "length": cfg["n"],
                    "queries_per_step": nq, "reach": cfg["reach"], "parallelism": f"row-shard x{world}",
-                   "l2": "inputs larger than L2: %.2f GB of coarse summaries per GPU, every query streams the tiles its box filter keeps" % (8 * main["N_local"] / 1e9),
+                   "l2": "inputs larger than L2: %.2f GB of iSAX tiles per GPU; each query streams the tiles its box filter keeps (distinct per query)" % (16 * main["N_local"] / 1e9),
                    "query_model": "sequential queries (P:2024-2026), batch call per step"},
         "roofline": {"bound": "hbm", "kernel": "k_scan (coarse iSAX LB scan of the box-filtered tiles)", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
@@ -344,7 +342,7 @@ def ours(args):
         "clocks": main["clocks"],
         "build": {"ms": main["build_ms"], "rows_per_s": main["N_local"] / (main["build_ms"] / 1e3),
                   "what": "summarise (PAA + iSAX + key) + CUB key sort, per GPU"},
-        "stats_mean": {k: mean(k) for k in ("tiles_scanned", "coarse_pass", "candidates", "lbk_pass", "refined",
+        "stats_mean": {k: mean(k) for k in ("lb_computed", "tiles_scanned", "candidates", "lbk_pass", "refined",
                                              "abandoned", "near_best", "seed_d2", "bsf_d2")},
     }
     if args.mode == "ed" and not args.no_dtw:
@@ -357,7 +355,7 @@ def ours(args):
         line["dtw"] = {"value": k4 * d["nq"] / (dms / 1e3), "unit": "queries/s", "workload": c4["name"],
                        "steps": k4, "ms_per_step": dms / k4,
                        "kernel_ms_per_step": {k: v[0] / k4 for k, v in d["prof"].items()},
-                       "stats_mean": {k: dm(k) for k in ("tiles_scanned", "coarse_pass", "candidates", "lbk_pass",
+                       "stats_mean": {k: dm(k) for k in ("lb_computed", "tiles_scanned", "candidates", "lbk_pass",
                                                          "refined", "abandoned", "near_best", "seed_d2", "bsf_d2")},
                        "gpu_launches": d["launches"]}
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -61,10 +61,9 @@ typedef struct {
 } messi_result;
 
 typedef struct {
-    int64_t lb_computed;  /* rows of the shard (every row is covered by a tile or a series bound) */
+    int64_t lb_computed;  /* series lower bounds evaluated (the members of the scanned tiles) */
     int64_t tiles_scanned; /* 512-series tiles whose box bound <= BSF0 * (1 + eps) (scanned) */
-    int64_t coarse_pass;  /* rows whose cardinality-16 (4-bit prefix) bound <= BSF0 * (1 + eps) */
-    int64_t candidates;   /* of those, rows whose exact 8-bit bound <= BSF * (1 + eps) */
+    int64_t candidates;   /* series whose iSAX bound <= BSF0 * (1 + eps) */
     int64_t lbk_pass;     /* DTW: candidates whose raw LB_Keogh <= BSF * (1 + eps) */
     int64_t refined;      /* real distances computed (fp32) in the refine step */
     int64_t abandoned;    /* real distance computations abandoned early */
@@ -116,7 +115,7 @@ messi_status messi_profile_read(messi_index* idx, int32_t kind, double* total_ms
 
 /* Scan throughput in isolation: one query's prologue and tile filter, then `reps` scans back
  * to back, each timed with CUDA events; *ms_out = summed kernel milliseconds, *coarse_out
- * (nullable) = coarse survivors of the last repetition | (tiles scanned << 32). */
+ * (nullable) = candidates of the last repetition | (tiles scanned << 32). */
 messi_status messi_debug_scan_repeat(messi_index* idx, const float* query_dev, int32_t reps, double* ms_out,
                                      int64_t* coarse_out);
 
@@ -132,15 +131,10 @@ messi_status messi_debug_summaries(messi_index* idx, uint8_t* sym_dev, float* pa
 /* Sorted approximate-search keys and the row permutation (device pointers owned by idx). */
 messi_status messi_debug_order(messi_index* idx, const uint64_t** skey_dev, const uint32_t** perm_dev);
 
-/* Pair bytes of the coarse summary, [count][8]: byte p = hi(sym_2p) << 4 | hi(sym_2p+1). */
-messi_status messi_debug_coarse_summaries(messi_index* idx, uint8_t* pairs_dev);
-
 /* Lower bound of every row against one query (device pointer): reach < 0 -> ED mindist
  * (Property 1); reach >= 0 -> DTW envelope-PAA bound.  Squared,
- * fp32 rounded down, written to lb_dev[count].  _lower_bounds: the exact 8-bit words;
- * _coarse_bounds: the same bound at cardinality 16 (top nibbles), what the scan streams. */
+ * fp32 rounded down, written to lb_dev[count] (the scan kernel's arithmetic). */
 messi_status messi_debug_lower_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
-messi_status messi_debug_coarse_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
 
 /* Box bound of every tile (512 consecutive series in approximate-search order; members are
  * rows perm[512*t .. 512*t+511]), written to lb_dev[ntiles] (fp32 of the fp64 bound). */

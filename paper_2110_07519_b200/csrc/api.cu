@@ -30,8 +30,8 @@ using namespace messi;
 
 struct Slot {
     QState* st = nullptr;
-    float *lut = nullptr, *lut2 = nullptr, *U = nullptr, *L = nullptr;
-    uint2* coarse = nullptr;  // coarse-scan survivors (id, coarse LB)
+    float *lut = nullptr, *U = nullptr, *L = nullptr;
+    uint2* cand = nullptr;    // scan survivors (sorted position, 8-bit LB)
     uint2* list2 = nullptr;   // DTW: LB_Keogh survivors (id, LBK)  [lazy]
     unsigned* tlist = nullptr;  // tiles surviving the box filter
     NearEntry* near = nullptr;
@@ -49,8 +49,7 @@ struct messi_index {
     const float* rows = nullptr;
     int sms = 148;
     // summaries
-    uint4* tiles = nullptr;    // coarse tiles (4 KB per 512 series)
-    uint4* symrows = nullptr;  // [ntiles*512][16] u8, sorted positions
+    uint4* tiles = nullptr;          // 8-bit iSAX words, 8 KB per 512 sorted positions
     unsigned char* boxes = nullptr;  // [ntiles][32]: per-segment min / max symbol
     float* paa = nullptr;
     unsigned long long* skey = nullptr;
@@ -71,7 +70,7 @@ struct messi_index {
 };
 
 static_assert(sizeof(messi_result) == 32, "messi_result layout");
-static_assert(sizeof(messi_stats) == 80, "messi_stats layout");
+static_assert(sizeof(messi_stats) == 72, "messi_stats layout");
 
 enum { K_SEED = 0, K_SCAN = 1, K_REFINE = 2, K_LBK = 3, K_RESOLVE = 4, K_KINDS = 5 };
 
@@ -154,20 +153,16 @@ struct ProfScope {
 // Reaches with a register-band DTW instantiation (DtwThread<R>); others use the warp path.
 #define MESSI_DTW_REACHES(X) X(2) X(5) X(12) X(25)
 
-static size_t scan_smem(int mode) { return kScanLutBytes + (mode == SCAN_FINE ? kFineLutBytes : 0); }
-static size_t lbk_smem(int n)
-{
-    return (size_t)MESSI_W * MESSI_CARD * sizeof(float) + 2 * (size_t)((n + 3) & ~3) * sizeof(float);
-}
+static size_t scan_smem() { return kScanLutBytes; }
+static size_t lbk_smem(int n) { return 2 * (size_t)((n + 3) & ~3) * sizeof(float); }
 
 static messi_status setup_kernels()
 {
     static bool done = false;
     if (done) return MESSI_OK;
     const int big = 200 * 1024;
-    CK(cudaFuncSetAttribute(k_scan<SCAN_COMPACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem(SCAN_COMPACT)));
-    CK(cudaFuncSetAttribute(k_scan<SCAN_ALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem(SCAN_ALL)));
-    CK(cudaFuncSetAttribute(k_scan<SCAN_FINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem(SCAN_FINE)));
+    CK(cudaFuncSetAttribute(k_scan<SCAN_COMPACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
+    CK(cudaFuncSetAttribute(k_scan<SCAN_ALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
     CK(cudaFuncSetAttribute(k_refine_ed, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_lbk_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -234,16 +229,15 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     const long long N = count;
     const size_t npadrows = (size_t)idx->ntiles * MESSI_TILE_ROWS;
     messi_status s;
-    if ((s = dalloc(&idx->tiles, (size_t)idx->ntiles * (MESSI_TILE_BYTES / 16))) || (s = dalloc(&idx->symrows, npadrows)) ||
+    if ((s = dalloc(&idx->tiles, (size_t)idx->ntiles * (MESSI_TILE_BYTES / 16))) ||
         (s = dalloc(&idx->boxes, (size_t)idx->ntiles * 32)))
         return bail(s);
     if (idx->keep_paa && (s = dalloc(&idx->paa, (size_t)N * MESSI_W))) return bail(s);
     if ((s = dalloc(&idx->skey, (size_t)N)) || (s = dalloc(&idx->perm, (size_t)N))) return bail(s);
     if ((s = dalloc(&idx->beta32, 256)) || (s = dalloc(&idx->lo_w, 256)) || (s = dalloc(&idx->hi_w, 256))) return bail(s);
     for (Slot& sl : idx->slot) {
-        if ((s = dalloc(&sl.st, 1)) || (s = dalloc(&sl.lut, MESSI_W * MESSI_CARD)) ||
-            (s = dalloc(&sl.lut2, MESSI_PAIRS * MESSI_CARD)) || (s = dalloc(&sl.U, n)) || (s = dalloc(&sl.L, n)) ||
-            (s = dalloc(&sl.coarse, (size_t)N)) || (s = dalloc(&sl.near, (size_t)N)) ||
+        if ((s = dalloc(&sl.st, 1)) || (s = dalloc(&sl.lut, MESSI_W * MESSI_CARD)) || (s = dalloc(&sl.U, n)) ||
+            (s = dalloc(&sl.L, n)) || (s = dalloc(&sl.cand, (size_t)N)) || (s = dalloc(&sl.near, (size_t)N)) ||
             (s = dalloc(&sl.tlist, (size_t)idx->ntiles)))
             return bail(s);
         if (cudaEventCreateWithFlags(&sl.ev_seed, cudaEventDisableTiming) != cudaSuccess ||
@@ -290,8 +284,7 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
         e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, idx->skey, ids_in, idx->perm, (int)N, 0, 64, st);
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "cub sort: %s", cudaGetErrorString(e)); break; }
         idx->launches += 4;
-        k_layout<<<(unsigned)idx->ntiles, MESSI_TILE_ROWS, 0, st>>>(sym_tmp, idx->perm, N, idx->symrows, idx->tiles,
-                                                                   idx->boxes);
+        k_layout<<<(unsigned)idx->ntiles, MESSI_TILE_ROWS, 0, st>>>(sym_tmp, idx->perm, N, idx->tiles, idx->boxes);
         ++idx->launches;
         e = cudaGetLastError();
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "k_layout: %s", cudaGetErrorString(e)); break; }
@@ -317,12 +310,12 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->rstr) cudaStreamSynchronize(idx->rstr);
     if (idx->stream) cudaStreamSynchronize(idx->stream);
     else cudaDeviceSynchronize();
-    void* ptrs[] = {idx->tiles, idx->symrows, idx->boxes, idx->paa,  idx->skey,   idx->perm,
-                    idx->beta32, idx->lo_w,   idx->hi_w,  idx->qbuf, idx->res1, idx->stats1};
+    void* ptrs[] = {idx->tiles, idx->boxes, idx->paa,  idx->skey, idx->perm,  idx->beta32,
+                    idx->lo_w,  idx->hi_w,  idx->qbuf, idx->res1, idx->stats1};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (Slot& sl : idx->slot) {
-        void* sp[] = {sl.st, sl.lut, sl.lut2, sl.U, sl.L, sl.coarse, sl.list2, sl.near, sl.tlist};
+        void* sp[] = {sl.st, sl.lut, sl.U, sl.L, sl.cand, sl.list2, sl.near, sl.tlist};
         for (void* p : sp)
             if (p) cudaFree(p);
         cudaEvent_t es[] = {sl.ev_seed, sl.ev_scan, sl.ev_done};
@@ -458,19 +451,13 @@ static messi_status launch_tile_filter(messi_index* idx, Slot& sl, cudaStream_t 
     return MESSI_OK;
 }
 
-static messi_status launch_scan(messi_index* idx, Slot& sl, bool fine)
+static messi_status launch_scan(messi_index* idx, Slot& sl)
 {
     CK(cudaStreamWaitEvent(idx->stream, sl.ev_seed, 0));
     {
         ProfScope ps(idx, K_SCAN, idx->stream);
-        if (fine)
-            k_scan<SCAN_FINE><<<scan_grid(idx), 32 * kScanWarps, scan_smem(SCAN_FINE), idx->stream>>>(
-                idx->tiles, idx->ntiles, idx->N, sl.lut2, sl.lut, idx->symrows, sl.st, sl.coarse, nullptr, sl.tlist,
-                idx->perm);
-        else
-            k_scan<SCAN_COMPACT><<<scan_grid(idx), 32 * kScanWarps, scan_smem(SCAN_COMPACT), idx->stream>>>(
-                idx->tiles, idx->ntiles, idx->N, sl.lut2, sl.lut, idx->symrows, sl.st, sl.coarse, nullptr, sl.tlist,
-                idx->perm);
+        k_scan<SCAN_COMPACT><<<scan_grid(idx), 32 * kScanWarps, scan_smem(), idx->stream>>>(
+            idx->tiles, idx->ntiles, idx->N, sl.lut, sl.st, sl.cand, nullptr, sl.tlist, idx->perm);
         LAUNCHED(idx);
     }
     CK(cudaEventRecord(sl.ev_scan, idx->stream));
@@ -490,16 +477,16 @@ static messi_status run_ed(messi_index* idx, const float* q_dev, messi_result* r
     {
         ProfScope ps(idx, K_SEED, idx->side);
         k_seed_ed<<<seed_grid, 256, qsm, idx->side>>>(q_dev, n, idx->rows, idx->skey, idx->perm, idx->N, idx->window,
-                                                      idx->beta32, idx->lo_w, idx->hi_w, sl.lut, sl.lut2, sl.st);
+                                                      idx->beta32, idx->lo_w, idx->hi_w, sl.lut, sl.st);
         LAUNCHED(idx);
         TRY(launch_tile_filter(idx, sl, idx->side));
     }
     CK(cudaEventRecord(sl.ev_seed, idx->side));
-    TRY(launch_scan(idx, sl, true));
+    TRY(launch_scan(idx, sl));
     {
         ProfScope ps(idx, K_REFINE, idx->rstr);
         k_refine_ed<<<refine_grid(idx, 32768), 256, refine_ed_smem(n), idx->rstr>>>(
-            sl.coarse, idx->perm, idx->rows, n, q_dev, sl.st, sl.near, idx->N, idx->row_begin, res, stats);
+            sl.cand, idx->perm, idx->rows, n, q_dev, sl.st, sl.near, idx->N, idx->row_begin, res, stats);
         LAUNCHED(idx);
     }
     CK(cudaEventRecord(sl.ev_done, idx->rstr));
@@ -523,16 +510,16 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
         ProfScope ps(idx, K_SEED, idx->side);
         k_seed_dtw<<<seed_grid, 32 * wf, qsm + wf * seed_warp, idx->side>>>(
             q_dev, n, reach, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32, idx->lo_w, idx->hi_w,
-            sl.lut, sl.U, sl.L, sl.lut2, sl.st);
+            sl.lut, sl.U, sl.L, sl.st);
         LAUNCHED(idx);
         TRY(launch_tile_filter(idx, sl, idx->side));
     }
     CK(cudaEventRecord(sl.ev_seed, idx->side));
-    TRY(launch_scan(idx, sl, false));
+    TRY(launch_scan(idx, sl));
     {
         ProfScope ps(idx, K_LBK, rs);
-        k_lbk_filter<<<refine_grid(idx, 2048), 256, lbk_smem(n), rs>>>(sl.coarse, idx->symrows, idx->perm, sl.lut,
-                                                                       idx->rows, n, sl.U, sl.L, sl.st, sl.list2);
+        k_lbk_filter<<<refine_grid(idx, 2048), 256, lbk_smem(n), rs>>>(sl.cand, idx->perm, idx->rows, n, sl.U, sl.L,
+                                                                       sl.st, sl.list2);
         LAUNCHED(idx);
     }
     {
@@ -671,26 +658,13 @@ extern "C" messi_status messi_debug_summaries(messi_index* idx, uint8_t* sym_dev
     if (paa_dev && !idx->paa) return fail(MESSI_EINVAL, "index built without keep_paa");
     CK(cudaSetDevice(idx->device));
     TRY(sync_all(idx));
-    k_unsort_sym<<<(unsigned)((idx->N + 255) / 256), 256, 0, idx->stream>>>(idx->symrows, idx->perm, idx->N,
-                                                                             reinterpret_cast<uint4*>(sym_dev));
+    const long long total = idx->N * MESSI_W;
+    k_detile<<<(unsigned)((total + 255) / 256), 256, 0, idx->stream>>>((const unsigned char*)idx->tiles, idx->perm, idx->N,
+                                                                       sym_dev);
     LAUNCHED(idx);
     if (paa_dev)
         CK(cudaMemcpyAsync(paa_dev, idx->paa, (size_t)idx->N * MESSI_W * sizeof(float), cudaMemcpyDeviceToDevice,
                            idx->stream));
-    CK(cudaStreamSynchronize(idx->stream));
-    return MESSI_OK;
-}
-
-extern "C" messi_status messi_debug_coarse_summaries(messi_index* idx, uint8_t* pairs_dev)
-{
-    g_err[0] = 0;
-    if (!idx || !pairs_dev) return fail(MESSI_EINVAL, "NULL argument");
-    CK(cudaSetDevice(idx->device));
-    TRY(sync_all(idx));
-    long long total = idx->N * MESSI_PAIRS;
-    k_detile_coarse<<<(unsigned)((total + 255) / 256), 256, 0, idx->stream>>>((const unsigned char*)idx->tiles, idx->perm,
-                                                                              idx->N, pairs_dev);
-    LAUNCHED(idx);
     CK(cudaStreamSynchronize(idx->stream));
     return MESSI_OK;
 }
@@ -712,11 +686,11 @@ static messi_status debug_prologue(messi_index* idx, const float* query_dev, int
     const size_t qsm = (size_t)((n + 3) & ~3) * sizeof(float);
     if (reach < 0) {
         k_seed_ed<<<1, 256, qsm, st>>>(query_dev, n, idx->rows, idx->skey, idx->perm, idx->N, 1, idx->beta32, idx->lo_w,
-                                       idx->hi_w, sl.lut, sl.lut2, sl.st);
+                                       idx->hi_w, sl.lut, sl.st);
     } else {
         k_seed_dtw<<<1, 32, 2 * qsm + 3 * (size_t)n * sizeof(float), st>>>(query_dev, n, reach, idx->rows, idx->skey,
                                                                           idx->perm, idx->N, 1, idx->beta32, idx->lo_w,
-                                                                          idx->hi_w, sl.lut, sl.U, sl.L, sl.lut2, sl.st);
+                                                                          idx->hi_w, sl.lut, sl.U, sl.L, sl.st);
     }
     LAUNCHED(idx);
     k_arm<<<1, 1, 0, st>>>(sl.st);
@@ -732,23 +706,9 @@ extern "C" messi_status messi_debug_lower_bounds(messi_index* idx, const float* 
     CK(cudaSetDevice(idx->device));
     TRY(sync_all(idx));
     TRY(debug_prologue(idx, query_dev, reach));
-    k_fine_all<<<idx->sms * 4, 256, 0, idx->stream>>>(idx->symrows, idx->perm, idx->N, idx->slot[0].lut, lb_dev);
-    LAUNCHED(idx);
-    CK(cudaStreamSynchronize(idx->stream));
-    return MESSI_OK;
-}
-
-extern "C" messi_status messi_debug_coarse_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev)
-{
-    g_err[0] = 0;
-    if (!idx || !query_dev || !lb_dev) return fail(MESSI_EINVAL, "NULL argument");
-    if (reach > idx->n) return fail(MESSI_EINVAL, "reach %d > n", reach);
-    CK(cudaSetDevice(idx->device));
-    TRY(sync_all(idx));
-    TRY(debug_prologue(idx, query_dev, reach));
     Slot& sl = idx->slot[0];
-    k_scan<SCAN_ALL><<<scan_grid(idx), 32 * kScanWarps, scan_smem(SCAN_ALL), idx->stream>>>(
-        idx->tiles, idx->ntiles, idx->N, sl.lut2, sl.lut, idx->symrows, sl.st, nullptr, lb_dev, nullptr, idx->perm);
+    k_scan<SCAN_ALL><<<scan_grid(idx), 32 * kScanWarps, scan_smem(), idx->stream>>>(
+        idx->tiles, idx->ntiles, idx->N, sl.lut, sl.st, nullptr, lb_dev, nullptr, idx->perm);
     LAUNCHED(idx);
     CK(cudaStreamSynchronize(idx->stream));
     return MESSI_OK;
@@ -794,11 +754,7 @@ extern "C" messi_status messi_debug_distances(messi_index* idx, const float* que
 // Scan throughput in isolation (tuning / roofline evidence): prologue for one query, then
 // `reps` coarse scans back to back on the main stream, each bracketed by CUDA events; the
 // survivor counter is reset between repetitions.  Returns the summed kernel milliseconds.
-__global__ void k_reset_coarse(QState* st)
-{
-    st->coarse_count = 0;
-    st->cand_count = 0;
-}
+__global__ void k_reset_cand(QState* st) { st->cand_count = 0; }
 
 extern "C" messi_status messi_debug_scan_repeat(messi_index* idx, const float* query_dev, int32_t reps, double* ms_out,
                                                 int64_t* coarse_out)
@@ -815,16 +771,16 @@ extern "C" messi_status messi_debug_scan_repeat(messi_index* idx, const float* q
     int seed_grid = (len + 7) / 8;
     if (seed_grid > 256) seed_grid = 256;
     k_seed_ed<<<seed_grid, 256, qsm, st>>>(query_dev, n, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32,
-                                           idx->lo_w, idx->hi_w, sl.lut, sl.lut2, sl.st);
+                                           idx->lo_w, idx->hi_w, sl.lut, sl.st);
     LAUNCHED(idx);
     TRY(launch_tile_filter(idx, sl, st));
     std::vector<cudaEvent_t> ev(2 * (size_t)reps);
     for (auto& e : ev) CK(cudaEventCreate(&e));
     for (int r = 0; r < reps; ++r) {
-        k_reset_coarse<<<1, 1, 0, st>>>(sl.st);
+        k_reset_cand<<<1, 1, 0, st>>>(sl.st);
         CK(cudaEventRecord(ev[2 * r], st));
-        k_scan<SCAN_FINE><<<scan_grid(idx), 32 * kScanWarps, scan_smem(SCAN_FINE), st>>>(
-            idx->tiles, idx->ntiles, idx->N, sl.lut2, sl.lut, idx->symrows, sl.st, sl.coarse, nullptr, sl.tlist, idx->perm);
+        k_scan<SCAN_COMPACT><<<scan_grid(idx), 32 * kScanWarps, scan_smem(), st>>>(
+            idx->tiles, idx->ntiles, idx->N, sl.lut, sl.st, sl.cand, nullptr, sl.tlist, idx->perm);
         CK(cudaEventRecord(ev[2 * r + 1], st));
     }
     idx->launches += 2 * reps;
@@ -839,7 +795,7 @@ extern "C" messi_status messi_debug_scan_repeat(messi_index* idx, const float* q
     for (auto& e : ev) cudaEventDestroy(e);
     if (coarse_out) {
         unsigned c[2] = {0, 0};
-        CK(cudaMemcpy(&c[0], &sl.st->coarse_count, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&c[0], &sl.st->cand_count, sizeof(unsigned), cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(&c[1], &sl.st->tile_count, sizeof(unsigned), cudaMemcpyDeviceToHost));
         *coarse_out = (int64_t)c[0] | ((int64_t)c[1] << 32);
     }

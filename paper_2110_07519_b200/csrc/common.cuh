@@ -6,9 +6,8 @@
 
 #define MESSI_W 16                 // PAA segments ("w is fixed to 16")
 #define MESSI_CARD 256             // 8-bit iSAX symbols
-#define MESSI_TILE_ROWS 512        // series per coarse tile (32 blocks x 16 series)
-#define MESSI_TILE_BYTES 4096      // coarse tile: 8 tile rows x 512 B (one nibble pair per byte)
-#define MESSI_PAIRS 8              // segment pairs (2p, 2p+1) of the coarse summary
+#define MESSI_TILE_ROWS 512        // series per tile (32 blocks x 16 series)
+#define MESSI_TILE_BYTES 8192      // tile: 16 tile rows x 512 B of 8-bit symbols
 #define MESSI_MAX_N 8192
 
 namespace messi {
@@ -23,12 +22,11 @@ __device__ __forceinline__ float slack_up(float bsf) { return __fmul_ru(bsf, 1.0
 struct QState {
     unsigned bsf_bits;      // current best-so-far (fp32 bits), +inf when armed
     unsigned seed_bits;     // BSF0 after the approximate search
-    unsigned cand_count;    // LB survivors appended by the scan
+    unsigned cand_count;    // series-bound survivors appended by the scan
     unsigned list2_count;   // DTW: LB_Keogh survivors
     unsigned near_count;    // near-best entries (d32 <= thr at refine time)
     unsigned refined;       // real distances started
     unsigned abandoned;     // real distances abandoned early
-    unsigned coarse_count;  // coarse-scan survivors appended
     unsigned done;          // CTAs of the refine stage that finished (last one resolves)
     unsigned tile_count;    // tiles whose box bound <= BSF0 * (1 + eps) (scanned)
     unsigned long long qkey;  // query's approximate-search key
@@ -48,7 +46,6 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->near_count = 0;
     st->refined = 0;
     st->abandoned = 0;
-    st->coarse_count = 0;
     st->done = 0;
     st->tile_count = 0;
 }

@@ -3,7 +3,6 @@
 #pragma once
 #include "common.cuh"
 #include "dtw.cuh"
-#include "scan.cuh"
 
 namespace messi {
 
@@ -81,7 +80,7 @@ __host__ __device__ inline size_t refine_ed_smem(int n)
 }
 
 // The ED refine stage of one query (runs on the refine stream, overlapping the next
-// query's scan).  Input: the scan's candidates (id, exact 8-bit LB).  Each warp takes 32 at
+// query's scan).  Input: the scan's candidates (sorted position, 8-bit LB).  Each warp takes 32 at
 // a time, keeps those whose LB does not exceed the CURRENT BSF, and computes their real
 // distances (refine_ed_pass).  The last CTA to finish re-ranks the near-best set exactly
 // and writes the query's result (A9).  Shared memory: q (n floats), reused by the resolve.
@@ -122,36 +121,29 @@ __global__ void __launch_bounds__(256) k_refine_ed(const uint2* __restrict__ can
     resolve_ed_block(rows, n, q_g, near, st, N, row_begin, result, stats, dsq, wuse);
 }
 
-// DTW step 1 (Alg. 10 lines LowerBound_DTW_SIMD and LB_Keogh): each coarse
-// survivor first gets the exact 8-bit envelope-PAA bound from its symbol row; those with
-// LB <= BSF*(1+eps) (counted as candidates) get the raw LB_Keogh against the query
-// envelope, four rows in flight per warp; survivors go to list2 as (id, LBK).
-__global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ coarse, const uint4* __restrict__ symrows,
-                                                    const unsigned* __restrict__ perm,
-                                                    const float* __restrict__ lut_g, const float* __restrict__ rows, int n,
-                                                    const float* __restrict__ U_g, const float* __restrict__ L_g,
-                                                    QState* st, uint2* __restrict__ list2)
+// DTW step 1 (Alg. 10 line LB_Keogh): the scan's candidates (sorted position,
+// envelope-PAA bound) whose bound still does not exceed the BSF get the raw LB_Keogh
+// against the query envelope, four rows in flight per warp; survivors go to list2 as
+// (row id, LBK).
+__global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ cand, const unsigned* __restrict__ perm,
+                                                    const float* __restrict__ rows, int n, const float* __restrict__ U_g,
+                                                    const float* __restrict__ L_g, QState* st, uint2* __restrict__ list2)
 {
     extern __shared__ __align__(16) float env[];
-    float* T = env;
-    float* U = env + MESSI_W * MESSI_CARD;
+    float* U = env;
     float* L = U + ((n + 3) & ~3);
-    for (int i = threadIdx.x; i < MESSI_W * MESSI_CARD; i += blockDim.x) T[i] = lut_g[i];
     for (int i = threadIdx.x; i < n; i += blockDim.x) { U[i] = U_g[i]; L[i] = L_g[i]; }
     __syncthreads();
-    const unsigned total = *(volatile unsigned*)&st->coarse_count;
+    const unsigned total = *(volatile unsigned*)&st->cand_count;
     const int lane = threadIdx.x & 31;
     const unsigned wpb = blockDim.x >> 5;
     const float thr = slack_up(ld_bsf(st));
-    unsigned n_fine = 0;
     for (unsigned k0 = (blockIdx.x * wpb + (threadIdx.x >> 5)) * 32; k0 < total; k0 += gridDim.x * wpb * 32) {
         const bool valid = k0 + lane < total;
-        const uint2 e = valid ? coarse[k0 + lane] : make_uint2(0u, 0x7f800000u);
-        bool ok = valid && __uint_as_float(e.y) <= thr;
-        if (ok) ok = fine_lb(symrows[e.x], T) <= thr;
+        const uint2 e = valid ? cand[k0 + lane] : make_uint2(0u, 0x7f800000u);
+        const bool ok = valid && __uint_as_float(e.y) <= thr;
         const unsigned rid = ok ? perm[e.x] : 0u;
         unsigned todo = __ballot_sync(0xffffffffu, ok);
-        n_fine += __popc(todo);
         unsigned passmask = 0;
         float mylbk = 0.0f;
         while (todo) {
@@ -205,7 +197,6 @@ __global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ co
                 list2[base + __popc(passmask & ((1u << lane) - 1))] = make_uint2(rid, __float_as_uint(mylbk));
         }
     }
-    if (lane == 0 && n_fine) atomicAdd(&st->cand_count, n_fine);
 }
 
 // DTW step 2 (Alg. 10 line RealDist, P:1425 / P:1453 "true DTW distance"): banded fp32
@@ -345,7 +336,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
                              void* result, void* stats)
 {
     struct R { double dist; long long id; double d2; long long reserved; };
-    struct S { long long lb, tiles, coarse, cand, lbk, refined, abandoned, near; double seed, bsf; };
+    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near; double seed, bsf; };
     R* res = reinterpret_cast<R*>(result);
     res->dist = b.id >= 0 ? sqrt(b.d) : (double)INFINITY;
     res->id = b.id >= 0 ? row_begin + b.id : -1;
@@ -353,9 +344,8 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
     res->reserved = 0;
     if (stats) {
         S* s = reinterpret_cast<S*>(stats);
-        s->lb = N;
+        s->lb = (long long)st->tile_count * MESSI_TILE_ROWS < N ? (long long)st->tile_count * MESSI_TILE_ROWS : N;
         s->tiles = st->tile_count;
-        s->coarse = st->coarse_count;
         s->cand = st->cand_count;
         s->lbk = st->list2_count;
         s->refined = st->refined;

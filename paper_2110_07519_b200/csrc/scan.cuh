@@ -10,14 +10,14 @@ namespace messi {
 // One CTA.  Query PAA (fp64 means; the fp32-rounded copy gives the query's iSAX word and
 // key, same rule as the data, "calculate iSAX summary for QDS"), and the per-query
 // lower-bound table T[s][v] = m * max(0, lo_w(v) - Ubar_s, Lbar_s - hi_w(v))^2 evaluated in
-// fp64 and rounded DOWN to fp32.  ED: Ubar = Lbar = query PAA, so T is mindist's per-segment
+// fp64 and rounded DOWN to fp32.  Ubar / Lbar also go to the query state (tile filter).  ED: Ubar = Lbar = query PAA, so T is mindist's per-segment
 // term (Property 1).  DTW (reach >= 0): U, L = the LB_Keogh envelope
 // (clamped windows) and Ubar, Lbar their PAA, T = the ABOVE / BELOW /
 // IN cases of Fig. fig:dtwsimd as one branch-free max.
 __device__ void prologue_block(const float* __restrict__ q, int n, int reach, const float* __restrict__ beta_g,
                                const float* __restrict__ lo_w, const float* __restrict__ hi_w,
                                float* __restrict__ lut_g, float* __restrict__ U_g, float* __restrict__ L_g,
-                               unsigned long long* key_out, float* __restrict__ lut2_g, QState* st)
+                               unsigned long long* key_out, QState* st)
 {
     __shared__ double ubar[MESSI_W], lbar[MESSI_W];
     __shared__ float beta[256];
@@ -71,16 +71,6 @@ __device__ void prologue_block(const float* __restrict__ q, int n, int reach, co
             double d = fmax(0.0, fmax(lo - ubar[s], lbar[s] - hi));
             lut_g[i] = __double2float_rd(md * d * d);
         }
-        // coarse table over nibble pairs: T2[p][h1 << 4 | h2] = the same bound at cardinality
-        // 16 (box of top nibble h = union of the 16 fine boxes 16h .. 16h+15) for segments
-        // 2p and 2p+1, summed in fp64 and rounded down: T2 <= T[2p][v1] + T[2p+1][v2].
-        for (int i = tid; i < MESSI_PAIRS * MESSI_CARD; i += blockDim.x) {
-            int pr = i >> 8, h1 = (i >> 4) & 15, hh = i & 15;
-            int s1 = 2 * pr, s2 = 2 * pr + 1;
-            double d1 = fmax(0.0, fmax((double)lo_w[16 * h1] - ubar[s1], lbar[s1] - (double)hi_w[16 * h1 + 15]));
-            double d2 = fmax(0.0, fmax((double)lo_w[16 * hh] - ubar[s2], lbar[s2] - (double)hi_w[16 * hh + 15]));
-            lut2_g[i] = __double2float_rd(md * d1 * d1 + md * d2 * d2);
-        }
     }
 }
 
@@ -116,14 +106,13 @@ __global__ void __launch_bounds__(256) k_seed_ed(const float* __restrict__ q_g, 
                                                  const unsigned* __restrict__ perm, long long N, int window,
                                                  const float* __restrict__ beta_g, const float* __restrict__ lo_w,
                                                  const float* __restrict__ hi_w, float* __restrict__ lut_g,
-                                                 float* __restrict__ lut2_g, QState* st)
+                                                 QState* st)
 {
     extern __shared__ __align__(16) float q_s[];
     __shared__ unsigned long long qkey_s;
     for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
     __syncthreads();
-    prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, blockIdx.x == 0 ? lut_g : nullptr, nullptr, nullptr, &qkey_s, lut2_g,
-                   st);
+    prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, blockIdx.x == 0 ? lut_g : nullptr, nullptr, nullptr, &qkey_s, st);
     __syncthreads();
     const unsigned long long qkey = qkey_s;
     long long a = block_lower_bound(skey, N, qkey);
@@ -153,8 +142,7 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
                            const unsigned long long* __restrict__ skey, const unsigned* __restrict__ perm,
                            long long N, int window, const float* __restrict__ beta_g,
                            const float* __restrict__ lo_w, const float* __restrict__ hi_w,
-                           float* __restrict__ lut_g, float* __restrict__ U_g, float* __restrict__ L_g,
-                           float* __restrict__ lut2_g, QState* st)
+                           float* __restrict__ lut_g, float* __restrict__ U_g, float* __restrict__ L_g, QState* st)
 {
     extern __shared__ __align__(16) float dsm[];
     float* q_s = dsm;
@@ -162,9 +150,9 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
     for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
     __syncthreads();
     if (blockIdx.x == 0)
-        prologue_block(q_s, n, reach, beta_g, lo_w, hi_w, lut_g, U_g, L_g, &qkey_s, lut2_g, st);
+        prologue_block(q_s, n, reach, beta_g, lo_w, hi_w, lut_g, U_g, L_g, &qkey_s, st);
     else
-        prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, nullptr, nullptr, nullptr, &qkey_s, nullptr, st);
+        prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, nullptr, nullptr, nullptr, &qkey_s, st);
     __syncthreads();
     const unsigned long long qkey = qkey_s;
     long long a = block_lower_bound(skey, N, qkey);
@@ -241,143 +229,73 @@ __global__ void k_tile_filter(const unsigned char* __restrict__ boxes, long long
 
 // ---------------------------------------------------------------------- lower-bound scan
 // The HBM-roofline step (A5): Alg. 9 line LowerBound_SIMD / Alg. 10 line
-// LowerBound_DTW_SIMD evaluated for EVERY series, like ParIS+'s SIMS scan
-// (P:432-443), in two resolutions of the same iSAX word.  The kernel streams the coarse
-// tiles (8 B per series: top nibbles, two segments per byte) and sums, per series, the 8
-// pair-table entries T2[p][byte] (round-down adds) -- the iSAX lower bound at cardinality
-// 16, which never exceeds the 8-bit one.
-// Shared-memory table: 64 KB, word v*64 + 8c + p holds T2[p][v] (4 copies c); the lane
-// owning block b reads pair p = (t + b) mod 8 at step t and uses copy c = b >> 3, so the 32
-// lanes hit 32 distinct banks for any byte values.  PRMT builds the byte address
-// (v << 8 | base) from the packed pair bytes in one instruction.
-//   SCAN_COMPACT: coarse survivors -> global list (warp ballot + prefix, one atomicAdd per
-//                 warp-tile); the exact 8-bit bound follows in k_lbk_filter (DTW).
-//   SCAN_ALL:     every coarse LB written out (inspection).
-//   SCAN_FINE:    coarse survivors' 8-bit words (16 B symbol rows) are loaded right after
-//                 the tile and consumed one tile later (the load latency hides behind the
-//                 next tile), their exact bound evaluated against the fine table (16 KB,
-//                 shared memory), and only those passing it are appended to the candidate
-//                 list -- the refine stage then touches ~0.1% of the rows only (ED).
-enum { SCAN_COMPACT = 0, SCAN_ALL = 1, SCAN_FINE = 2 };
+// LowerBound_DTW_SIMD for every series of every tile the box filter kept: LB =
+// sum_s T[s][sym_s] (round-down adds) from the 8-bit words.  Shared-memory table, 64 KB:
+// word v*64 + 16h + s holds T[s][v]; the lane owning block b = 2p + h reads segment
+// s = (t + p) mod 16 at step t, so the 32 lanes hit 32 distinct banks for any symbols.
+// PRMT builds the byte address (v << 8 | base) from the packed symbols in one instruction.
+// Survivors (LB <= BSF0 * (1 + eps)) are appended as (sorted position, LB) with a warp
+// ballot + prefix and one atomicAdd per warp-tile.
+//   SCAN_COMPACT: survivors -> candidate list;   SCAN_ALL: every LB written (inspection,
+//   all tiles, scattered back to row order).
+enum { SCAN_COMPACT = 0, SCAN_ALL = 1 };
 constexpr int kScanWarps = 8;
 constexpr size_t kScanLutBytes = (size_t)MESSI_CARD * 64 * sizeof(float);
-constexpr size_t kFineLutBytes = (size_t)MESSI_W * MESSI_CARD * sizeof(float);
-constexpr int kPend = 2;  // coarse survivors per lane carried to the next tile
 
 #ifndef MESSI_SCAN_NOCOMPUTE
 #define MESSI_SCAN_NOCOMPUTE 0
 #endif
 
-// Coarse bound of the 16 series of one lane for one tile already in registers.
-__device__ __forceinline__ void coarse_tile(const uint4 (&data)[8], const char* lbase, int lane, float (&acc)[16])
-{
-#if MESSI_SCAN_NOCOMPUTE  // bandwidth probe only: touch the data, no table lookups
-    unsigned x = 0;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) x ^= data[t].x ^ data[t].y ^ data[t].z ^ data[t].w;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) acc[k] = x == 0x12345678u ? -1.0f : 1e30f;
-    return;
-#endif
-    const int cpy = lane >> 3;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) acc[k] = 0.0f;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-        const unsigned base = (unsigned)((8 * cpy + ((t + lane) & 7)) * 4);
-        const unsigned wv[4] = {data[t].x, data[t].y, data[t].z, data[t].w};
-#pragma unroll
-        for (int wi = 0; wi < 4; ++wi) {
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const unsigned addr = __byte_perm(wv[wi], base, 0x5504 | (b << 4));
-                acc[wi * 4 + b] = __fadd_rd(acc[wi * 4 + b], *reinterpret_cast<const float*>(lbase + addr));
-            }
-        }
-    }
-}
-
-// Exact (8-bit) lower bound of one series from its symbol row: sum_s T[s][sym_s], s in
-// order, round-down adds.  T: the fine table [16][256].
-__device__ __forceinline__ float fine_lb(uint4 sr, const float* __restrict__ T)
-{
-    const unsigned w[4] = {sr.x, sr.y, sr.z, sr.w};
-    float acc = 0.0f;
-#pragma unroll
-    for (int s = 0; s < 16; ++s) acc = __fadd_rd(acc, T[s * 256 + ((w[s >> 2] >> (8 * (s & 3))) & 255u)]);
-    return acc;
-}
-
-// Warp-aggregated append of (id, value) pairs held by the lanes with `ok` set.
-__device__ __forceinline__ void warp_append(bool ok, unsigned id, float v, unsigned* counter, uint2* __restrict__ out,
-                                            int lane)
-{
-    const unsigned m = __ballot_sync(0xffffffffu, ok);
-    if (!m) return;
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(counter, (unsigned)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (ok) out[base + __popc(m & ((1u << lane) - 1))] = make_uint2(id, __float_as_uint(v));
-}
-
-// Positions are SORTED positions p (row = perm[p]); the refine stages translate.  The scan
-// visits the tiles listed by k_tile_filter (SCAN_ALL: every tile, LBs scattered to rows).
 template <int MODE>
 __global__ void __launch_bounds__(32 * kScanWarps, 2) k_scan(const uint4* __restrict__ tiles, long long ntiles,
-                                                             long long N, const float* __restrict__ lut2_g,
-                                                             const float* __restrict__ lut_g,
-                                                             const uint4* __restrict__ symrows, QState* st,
+                                                             long long N, const float* __restrict__ lut_g, QState* st,
                                                              uint2* __restrict__ out, float* __restrict__ lb_all,
                                                              const unsigned* __restrict__ tlist,
                                                              const unsigned* __restrict__ perm)
 {
-    extern __shared__ __align__(16) float lut_s[];  // 256 * 64 floats (+ fine table in SCAN_FINE)
-    float* T = lut_s + MESSI_CARD * 64;
-    for (int i = threadIdx.x; i < MESSI_PAIRS * MESSI_CARD; i += blockDim.x) {
-        const int pr = i >> 8, v = i & 255;
-        const float val = lut2_g[i];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) lut_s[v * 64 + 8 * c + pr] = val;
+    extern __shared__ __align__(16) float lut_s[];  // 256 * 64 floats
+    for (int i = threadIdx.x; i < MESSI_W * MESSI_CARD; i += blockDim.x) {
+        const int sg = i >> 8, v = i & 255;
+        const float val = lut_g[i];
+        lut_s[v * 64 + sg] = val;
+        lut_s[v * 64 + 16 + sg] = val;
     }
-    if (MODE == SCAN_FINE)
-        for (int i = threadIdx.x; i < MESSI_W * MESSI_CARD; i += blockDim.x) T[i] = lut_g[i];
     __syncthreads();
     const float thr = MODE == SCAN_ALL ? INFINITY : slack_up(ld_bsf(st));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int p = lane >> 1, h = lane & 1;
     const char* lbase = reinterpret_cast<const char*>(lut_s);
-    const long long stride = (long long)gridDim.x * kScanWarps;
-    unsigned n_coarse = 0;
-    // SCAN_FINE: coarse survivors carried to the next tile (their symbol rows in flight)
-    unsigned pid[kPend];
-    uint4 psr[kPend];
-    int npend = 0;
     const long long count = MODE == SCAN_ALL ? ntiles : (long long)*(volatile unsigned*)&st->tile_count;
-    for (long long it = (long long)blockIdx.x * kScanWarps + warp;; it += stride) {
-        const bool have = it < count;
-        const long long tl = MODE == SCAN_ALL ? it : (have ? (long long)tlist[it] : 0);
+    for (long long it = (long long)blockIdx.x * kScanWarps + warp; it < count; it += (long long)gridDim.x * kScanWarps) {
+        const long long tl = MODE == SCAN_ALL ? it : (long long)tlist[it];
+        const uint4* tp = tiles + tl * (MESSI_TILE_BYTES / 16) + lane;
+        uint4 data[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) data[t] = __ldcs(tp + t * 32);
         float acc[16];
-        if (have) {
-            const uint4* tp = tiles + tl * (MESSI_TILE_BYTES / 16) + lane;
-            uint4 data[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) data[i] = __ldcs(tp + i * 32);
-            coarse_tile(data, lbase, lane, acc);
-        }
-        if (MODE == SCAN_FINE) {  // the previous tile's survivors: exact bound, then append
+        for (int k = 0; k < 16; ++k) acc[k] = 0.0f;
+#if MESSI_SCAN_NOCOMPUTE  // bandwidth probe only
+        unsigned x = 0;
 #pragma unroll
-            for (int j = 0; j < kPend; ++j) {
-                bool ok = j < npend;
-                float f = 0.0f;
-                if (ok) {
-                    f = fine_lb(psr[j], T);
-                    ok = f <= thr;
+        for (int t = 0; t < 16; ++t) x ^= data[t].x ^ data[t].y ^ data[t].z ^ data[t].w;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] = x == 0x12345678u ? -1.0f : 1e30f;
+#else
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            const unsigned base = (unsigned)((16 * h + ((t + p) & 15)) * 4);
+            const unsigned wv[4] = {data[t].x, data[t].y, data[t].z, data[t].w};
+#pragma unroll
+            for (int wi = 0; wi < 4; ++wi) {
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const unsigned addr = __byte_perm(wv[wi], base, 0x5504 | (b << 4));
+                    acc[wi * 4 + b] = __fadd_rd(acc[wi * 4 + b], *reinterpret_cast<const float*>(lbase + addr));
                 }
-                warp_append(ok, pid[j], f, &st->cand_count, out, lane);
             }
-            npend = 0;
         }
-        if (!__any_sync(0xffffffffu, have)) break;
-        if (!have) continue;
+#endif
         const long long id0 = tl * MESSI_TILE_ROWS + lane * 16;
         if (MODE == SCAN_ALL) {
 #pragma unroll
@@ -389,32 +307,6 @@ __global__ void __launch_bounds__(32 * kScanWarps, 2) k_scan(const uint4* __rest
 #pragma unroll
         for (int k = 0; k < 16; ++k)
             if (acc[k] <= thr && id0 + k < N) mask |= 1u << k;
-        if (MODE == SCAN_FINE) {
-            n_coarse += __popc(mask);
-            // up to kPend survivors: issue their symbol-row loads now, consume next tile
-#pragma unroll
-            for (int j = 0; j < kPend; ++j) {
-                if (mask) {
-                    const int k = __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    pid[j] = (unsigned)(id0 + k);
-                    psr[j] = __ldg(symrows + id0 + k);
-                    npend = j + 1;
-                }
-            }
-            // rare overflow: the rest synchronously
-            while (mask) {
-                const int k = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const float f = fine_lb(__ldg(symrows + id0 + k), T);
-                if (f <= thr) {
-                    const unsigned pos = atomicAdd(&st->cand_count, 1u);
-                    out[pos] = make_uint2((unsigned)(id0 + k), __float_as_uint(f));
-                }
-            }
-            continue;
-        }
-        // SCAN_COMPACT
         if (!__any_sync(0xffffffffu, mask)) continue;
         const int cnt = __popc(mask);
         int incl = cnt;
@@ -425,27 +317,12 @@ __global__ void __launch_bounds__(32 * kScanWarps, 2) k_scan(const uint4* __rest
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         unsigned base = 0;
-        if (lane == 0) base = atomicAdd(&st->coarse_count, (unsigned)total);
+        if (lane == 0) base = atomicAdd(&st->cand_count, (unsigned)total);
         unsigned pos = __shfl_sync(0xffffffffu, base, 0) + incl - cnt;
 #pragma unroll
         for (int k = 0; k < 16; ++k)
             if (mask & (1u << k)) out[pos++] = make_uint2((unsigned)(id0 + k), __float_as_uint(acc[k]));
     }
-    if (MODE == SCAN_FINE) {
-        n_coarse = __reduce_add_sync(0xffffffffu, n_coarse);
-        if (lane == 0 && n_coarse) atomicAdd(&st->coarse_count, n_coarse);
-    }
-}
-
-// Inspection: the fine bound of every row (one thread per sorted position).
-__global__ void k_fine_all(const uint4* __restrict__ symrows, const unsigned* __restrict__ perm, long long N,
-                           const float* __restrict__ lut_g, float* __restrict__ lb_all)
-{
-    __shared__ float T[MESSI_W * MESSI_CARD];
-    for (int i = threadIdx.x; i < MESSI_W * MESSI_CARD; i += blockDim.x) T[i] = lut_g[i];
-    __syncthreads();
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x)
-        lb_all[perm[p]] = fine_lb(symrows[p], T);
 }
 
 }  // namespace messi

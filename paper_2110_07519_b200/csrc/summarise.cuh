@@ -27,25 +27,22 @@ __global__ void k_breakpoints(float* beta32, float* lo_w, float* hi_w)
     hi_w[v] = v == 255 ? INFINITY : nextafterf(b[v], INFINITY);
 }
 
-// Summaries in APPROXIMATE-SEARCH ORDER.  After the key sort every summary is stored at its
-// sorted position p (row = perm[p]); consecutive positions share the leading bit planes of
-// the interleaved key, i.e. they sit in the same subtree of the variable-cardinality iSAX
-// tree, and a tile of 512 consecutive positions is the analogue of a leaf node.
-//  * symrows [Npad][16] u8: the full 8-bit word, series-major (16 B), sorted.
-//  * coarse tiles (4 KB per 512 positions): the top nibble of every symbol (the symbol at
-//    cardinality 16 -- bit-prefix property), two segments per byte:
-//    byte = hi(sym_2p) << 4 | hi(sym_2p+1) for pair p, 8 B per series, in a skewed layout:
-//    block b = 16 series (b < 32); tile row t (512 B) holds, at byte offset 16*b, the pair
-//    bytes of pair p = (t + b) mod 8 of block b's 16 series.  A warp reading tile row t
-//    (lane b loads 16 B) gets 8 different pairs across each group of 8 lanes; with the
-//    coarse table replicated 4 times (copy b >> 3) the 32 lanes hit 32 distinct shared
-//    memory banks whatever the symbol values.
-//  * boxes [ntiles][32] u8: per segment, the min and max 8-bit symbol of the tile -- the
-//    tile's iSAX node summary (its "node" in Alg. 7's FindDist).
-__device__ __forceinline__ int coarse_offset(int rr, int pair)
+// Summaries in APPROXIMATE-SEARCH ORDER.  After the key sort every 8-bit iSAX word is
+// stored at its sorted position p (row = perm[p]).  Consecutive positions share the leading
+// bit planes of the interleaved key, i.e. they sit in the same subtree of the variable-
+// cardinality iSAX tree; a tile of 512 consecutive positions plays the role of a
+// leaf node, and its box -- per segment the min and max symbol of its members -- is the
+// node's iSAX summary used to prune it (Alg. 7's FindDist).
+//  * tiles (8 KB per 512 positions), skewed layout: block b = 16 series (b < 32), pair
+//    p = b >> 1, half h = b & 1; tile row t (512 B) holds, at byte offset 16*b, segment
+//    s = (t + p) mod 16 of block b's 16 series.  A warp reading tile row t (lane b loads
+//    16 B) therefore holds 16 different segments across the pairs; with the table stored
+//    twice (copy h) the 32 lanes hit 32 distinct shared-memory banks whatever the symbols.
+//  * boxes [ntiles][32] u8: per segment min (bytes 0..15) and max (16..31) symbol.
+__device__ __forceinline__ int tile_offset(int rr, int s)
 {
-    int b = rr >> 4, k = rr & 15;
-    int t = (pair - b) & 7;
+    int b = rr >> 4, k = rr & 15, p = b >> 1;
+    int t = (s - p) & 15;
     return t * 512 + b * 16 + k;
 }
 
@@ -113,10 +110,9 @@ __global__ void __launch_bounds__(256) k_summarise(const float* __restrict__ row
 }
 
 // Lays the summaries out in sorted order: one CTA (512 threads) per tile of 512 sorted
-// positions gathers its rows' 8-bit words, writes them, the coarse tile and the box.
+// positions gathers its rows' 8-bit words and writes the skewed tile and the box.
 __global__ void __launch_bounds__(512) k_layout(const uint4* __restrict__ symrows_tmp, const unsigned* __restrict__ perm,
-                                                int64_t N, uint4* __restrict__ symrows, uint4* __restrict__ tiles,
-                                                unsigned char* __restrict__ boxes)
+                                                int64_t N, uint4* __restrict__ tiles, unsigned char* __restrict__ boxes)
 {
     __shared__ __align__(16) unsigned char tile[MESSI_TILE_BYTES];
     __shared__ unsigned bmin[MESSI_W], bmax[MESSI_W];
@@ -127,24 +123,19 @@ __global__ void __launch_bounds__(512) k_layout(const uint4* __restrict__ symrow
     __syncthreads();
     const bool valid = p < N;
     const uint4 sr = valid ? symrows_tmp[perm[p]] : make_uint4(0, 0, 0, 0);
-    symrows[p] = sr;
     const unsigned w[4] = {sr.x, sr.y, sr.z, sr.w};
-    unsigned sym[MESSI_W];
 #pragma unroll
-    for (int s = 0; s < MESSI_W; ++s) sym[s] = (w[s >> 2] >> (8 * (s & 3))) & 255u;
-#pragma unroll
-    for (int pr = 0; pr < MESSI_PAIRS; ++pr)
-        tile[coarse_offset(i, pr)] = (unsigned char)((sym[2 * pr] & 0xf0u) | (sym[2 * pr + 1] >> 4));
-    if (valid) {
-#pragma unroll
-        for (int s = 0; s < MESSI_W; ++s) {
-            atomicMin(&bmin[s], sym[s]);
-            atomicMax(&bmax[s], sym[s]);
+    for (int s = 0; s < MESSI_W; ++s) {
+        const unsigned sym = (w[s >> 2] >> (8 * (s & 3))) & 255u;
+        tile[tile_offset(i, s)] = (unsigned char)sym;
+        if (valid) {
+            atomicMin(&bmin[s], sym);
+            atomicMax(&bmax[s], sym);
         }
     }
     __syncthreads();
     uint4* dst = tiles + tl * (MESSI_TILE_BYTES / 16);
-    if (i < MESSI_TILE_BYTES / 16) dst[i] = reinterpret_cast<const uint4*>(tile)[i];
+    dst[i] = reinterpret_cast<const uint4*>(tile)[i];
     if (i < MESSI_W) {
         boxes[tl * 32 + i] = (unsigned char)bmin[i];
         boxes[tl * 32 + 16 + i] = (unsigned char)bmax[i];
@@ -152,23 +143,15 @@ __global__ void __launch_bounds__(512) k_layout(const uint4* __restrict__ symrow
 }
 
 // Inspection: the 8-bit words back in row order, out[row][16].
-__global__ void k_unsort_sym(const uint4* __restrict__ symrows, const unsigned* __restrict__ perm, int64_t N,
-                             uint4* __restrict__ out)
-{
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < N) out[perm[p]] = symrows[p];
-}
-
-// Inspection: the coarse pair bytes back in row order, out[row][8].
-__global__ void k_detile_coarse(const unsigned char* __restrict__ tiles, const unsigned* __restrict__ perm, int64_t N,
-                                unsigned char* __restrict__ out)
+__global__ void k_detile(const unsigned char* __restrict__ tiles, const unsigned* __restrict__ perm, int64_t N,
+                         unsigned char* __restrict__ out)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= N * MESSI_PAIRS) return;
-    const int64_t p = i / MESSI_PAIRS;
-    const int pair = (int)(i % MESSI_PAIRS);
-    out[(int64_t)perm[p] * MESSI_PAIRS + pair] =
-        tiles[(p / MESSI_TILE_ROWS) * MESSI_TILE_BYTES + coarse_offset((int)(p % MESSI_TILE_ROWS), pair)];
+    if (i >= N * MESSI_W) return;
+    const int64_t p = i / MESSI_W;
+    const int s = (int)(i % MESSI_W);
+    out[(int64_t)perm[p] * MESSI_W + s] =
+        tiles[(p / MESSI_TILE_ROWS) * MESSI_TILE_BYTES + tile_offset((int)(p % MESSI_TILE_ROWS), s)];
 }
 
 }  // namespace messi

@@ -41,8 +41,7 @@ class Result(ctypes.Structure):
 
 
 class Stats(ctypes.Structure):
-    _fields_ = [("lb_computed", ctypes.c_int64), ("tiles_scanned", ctypes.c_int64), ("coarse_pass", ctypes.c_int64),
-                ("candidates", ctypes.c_int64),
+    _fields_ = [("lb_computed", ctypes.c_int64), ("tiles_scanned", ctypes.c_int64), ("candidates", ctypes.c_int64),
                 ("lbk_pass", ctypes.c_int64),
                 ("refined", ctypes.c_int64), ("abandoned", ctypes.c_int64), ("near_best", ctypes.c_int64),
                 ("seed_d2", ctypes.c_double), ("bsf_d2", ctypes.c_double)]
@@ -81,14 +80,12 @@ def lib():
         L.messi_debug_summaries.argtypes = [vp, vp, vp]
         L.messi_debug_order.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]
         L.messi_debug_lower_bounds.argtypes = [vp, vp, i32, vp]
-        L.messi_debug_coarse_bounds.argtypes = [vp, vp, i32, vp]
         L.messi_debug_tile_bounds.argtypes = [vp, vp, i32, vp]
-        L.messi_debug_coarse_summaries.argtypes = [vp, vp]
         L.messi_debug_distances.argtypes = [vp, vp, i32, vp, i32, vp, vp, vp]
         for f in ("messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_batch",
                   "messi_query_dtw_batch", "messi_profile_enable", "messi_profile_read", "messi_debug_breakpoints", "messi_debug_summaries",
                   "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances",
-                  "messi_debug_coarse_bounds", "messi_debug_coarse_summaries", "messi_debug_scan_repeat", "messi_debug_tile_bounds"):
+                  "messi_debug_scan_repeat", "messi_debug_tile_bounds"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -98,8 +95,7 @@ EXPORTED = ["messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_
             "messi_free", "messi_last_error", "messi_launch_count", "messi_profile_enable", "messi_profile_read",
             "messi_debug_breakpoints",
             "messi_debug_summaries", "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances",
-            "messi_debug_coarse_bounds", "messi_debug_coarse_summaries", "messi_debug_scan_repeat",
-            "messi_debug_tile_bounds"]
+            "messi_debug_scan_repeat", "messi_debug_tile_bounds"]
 
 
 def _check(status: int):
@@ -184,7 +180,7 @@ def messi_profile_read(handle, kind):
 
 
 def messi_debug_scan_repeat(handle, query_dev: torch.Tensor, reps: int):
-    """(summed ms of `reps` isolated scans, coarse survivors, tiles scanned)."""
+    """(summed ms of `reps` isolated scans, candidates, tiles scanned)."""
     ms, c = ctypes.c_double(), ctypes.c_int64()
     _check(lib().messi_debug_scan_repeat(handle, _ptr(query_dev), int(reps), ctypes.byref(ms), ctypes.byref(c)))
     return ms.value, c.value & 0xFFFFFFFF, c.value >> 32
@@ -222,22 +218,10 @@ def messi_debug_lower_bounds(handle, query_dev: torch.Tensor, reach: int, count:
     return lb
 
 
-def messi_debug_coarse_bounds(handle, query_dev: torch.Tensor, reach: int, count: int):
-    lb = torch.empty(count, dtype=torch.float32, device=query_dev.device)
-    _check(lib().messi_debug_coarse_bounds(handle, _ptr(query_dev), int(reach), _ptr(lb)))
-    return lb
-
-
 def messi_debug_tile_bounds(handle, query_dev: torch.Tensor, reach: int, ntiles: int):
     lb = torch.empty(ntiles, dtype=torch.float32, device=query_dev.device)
     _check(lib().messi_debug_tile_bounds(handle, _ptr(query_dev), int(reach), _ptr(lb)))
     return lb
-
-
-def messi_debug_coarse_summaries(handle, count: int, device):
-    pairs = torch.empty((count, 8), dtype=torch.uint8, device=device)
-    _check(lib().messi_debug_coarse_summaries(handle, _ptr(pairs)))
-    return pairs
 
 
 def messi_debug_distances(handle, query_dev: torch.Tensor, reach: int, ids_dev: torch.Tensor):
@@ -272,7 +256,7 @@ def _wrap_dev(ptr: int, nbytes: int, device):
     return torch.as_tensor(_Arr(), device=device)
 
 
-RESULT_BYTES, STATS_BYTES = 32, 80
+RESULT_BYTES, STATS_BYTES = 32, 72
 
 
 def result_buffer(nq: int, device) -> torch.Tensor:
@@ -299,8 +283,8 @@ def decode_results_device(buf: torch.Tensor):
 
 def decode_stats(buf: torch.Tensor):
     raw = buf.view(-1, STATS_BYTES).cpu()
-    ints = raw[:, :64].contiguous().view(torch.int64)
-    dbl = raw[:, 64:].contiguous().view(torch.float64)
+    ints = raw[:, :56].contiguous().view(torch.int64)
+    dbl = raw[:, 56:].contiguous().view(torch.float64)
     return [dict(zip(STATS_FIELDS, list(map(int, i.tolist())) + list(map(float, d.tolist()))))
             for i, d in zip(ints, dbl)]
 

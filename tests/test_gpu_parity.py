@@ -60,21 +60,6 @@ def test_summaries_bit_exact(c1):
     assert np.array_equal(sym.cpu().numpy(), S)
 
 
-def test_coarse_summary_is_the_4bit_prefix(c1):
-    """The coarse tiles hold the cardinality-16 iSAX word (bit-prefix property):
-    pair byte p = hi(sym_2p) << 4 | hi(sym_2p+1), bit-exact."""
-    X, Q, idx, Xh, Qh = c1
-    pairs = messi().messi_debug_coarse_summaries(idx.handle, X.shape[0], X.device).cpu().numpy()
-    _, S = oracle.isax_rows(Xh)
-    ref = ((S[:, 0::2] >> 4) << 4) | (S[:, 1::2] >> 4)
-    assert np.array_equal(pairs, ref.astype(np.uint8))
-    # and the 4-bit prefix IS the cardinality-16 symbol of the oracle's own card-16 table
-    b16 = oracle.breakpoints(16)[1]
-    P, _ = oracle.isax_rows(Xh[:2000])
-    for r in range(0, 2000, 97):
-        assert [oracle.symbol(v, b16, 16) for v in P[r]] == list(S[r] >> 4)
-
-
 def _interleave_key(S):
     key = np.zeros(S.shape[0], np.uint64)
     for bit in range(7, 3, -1):
@@ -123,16 +108,6 @@ def test_lower_bounds_ed(c1):
         # Property 1: LB <= true ED^2, for every row of the collection
         ed = oracle.ed2_rows(Xh, Qh[qi])
         assert np.all(lb.astype(np.float64) <= ed)
-        # the scan's cardinality-16 bound: <= the 8-bit bound, and = the oracle's mindist of
-        # the 4-bit words against the card-16 breakpoints (within the same tolerance)
-        cl = messi().messi_debug_coarse_bounds(idx.handle, Q[qi].contiguous(), -1, X.shape[0]).cpu().numpy()
-        assert np.all(cl <= lb)
-        b16 = oracle.breakpoints(16)[1]
-        ref16 = np.array([oracle.mindist2(qp, S[r] >> 4, 256, card=16, beta32=b16) for r in rows])
-        lo16 = np.concatenate([[-np.inf], b16]).astype(np.float64)
-        hi16 = np.concatenate([b16, [np.inf]]).astype(np.float64)
-        d16 = np.maximum(0, np.maximum(lo16[S[rows] >> 4] - qp, qp - hi16[S[rows] >> 4]))
-        assert np.all(np.abs(cl[rows] - ref16) <= _lb_tol(d16, 16) + 2.0 ** -20 * ref16)
 
 
 @pytest.mark.parametrize("reach", [-1, 25])

@@ -22,7 +22,7 @@ idx = M.Index(X)
 M.messi_debug_scan_repeat(idx.handle, Q[0], 3)
 ms, c, tiles = M.messi_debug_scan_repeat(idx.handle, Q[0], reps)
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
-gbs = (4096 * tiles + 32 * c) * reps / (ms / 1e3) / 1e9
+gbs = (8192 * tiles + 8 * c) * reps / (ms / 1e3) / 1e9
 print(json.dumps({"lib": os.environ.get("MESSI_LIB", "default"), "rows": rows, "us_per_scan": 1e3 * ms / reps,
-                  "GBps": gbs, "frac": gbs / peak, "coarse": c, "tiles": tiles,
+                  "GBps": gbs, "frac": gbs / peak, "candidates": c, "tiles": tiles,
                   "tile_frac": tiles / ((rows + 511) // 512)}))
