@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=4_000_000, help="row sample of the oracle timing")
     ap.add_argument("--cpu-queries", type=int, default=32, help="queries of the oracle timing sample")
     ap.add_argument("--window", type=int, default=0, help="approximate-search window (0: library default 2000)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: host-side merge; lets several ranks share one GPU)")
     return ap.parse_args()
 
 
@@ -70,8 +72,12 @@ def dist_init(args):
     if world > 1:
         import torch
         import torch.distributed as dist
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group("gloo")
     return world, rank, local
 
 
@@ -86,7 +92,8 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -325,6 +332,8 @@ def ours(args):
         "dtype": "f32", "data": "synthetic (seeded device Philox random walks, z-normalised)",
         "config": {"workload": cfg["name"], "mode": args.mode, "rows": cfg["N"], "length": cfg["n"],
                    "queries_per_step": nq, "reach": cfg["reach"], "parallelism": f"row-shard x{world}",
+                   "merge": "per step: one all_gather of (d2, gid) x queries per rank, lexicographic min" if world > 1
+                   else "single shard",
                    "l2": "inputs larger than L2: %.2f GB of iSAX tiles per GPU; each query streams the tiles its box filter keeps (distinct per query)" % (16 * main["N_local"] / 1e9),
                    "query_model": "sequential queries (P:2024-2026), batch call per step"},
         "roofline": {"bound": "hbm", "kernel": "k_scan (coarse iSAX LB scan of the box-filtered tiles)", "achieved": achieved, "peak": peak,
@@ -343,7 +352,7 @@ def ours(args):
         "build": {"ms": main["build_ms"], "rows_per_s": main["N_local"] / (main["build_ms"] / 1e3),
                   "what": "summarise (PAA + iSAX + key) + CUB key sort, per GPU"},
         "stats_mean": {k: mean(k) for k in ("lb_computed", "tiles_scanned", "candidates", "lbk_pass", "refined",
-                                             "abandoned", "near_best", "seed_d2", "bsf_d2")},
+                                             "abandoned", "near_best", "dtw_cells", "seed_d2", "bsf_d2")},
     }
     if args.mode == "ed" and not args.no_dtw:
         c4 = dict(CONFIGS["c4"])
@@ -356,7 +365,8 @@ def ours(args):
                        "steps": k4, "ms_per_step": dms / k4,
                        "kernel_ms_per_step": {k: v[0] / k4 for k, v in d["prof"].items()},
                        "stats_mean": {k: dm(k) for k in ("lb_computed", "tiles_scanned", "candidates", "lbk_pass",
-                                                         "refined", "abandoned", "near_best", "seed_d2", "bsf_d2")},
+                                                         "refined", "abandoned", "near_best", "dtw_cells",
+                                                         "seed_d2", "bsf_d2")},
                        "gpu_launches": d["launches"]}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, args, dev, "ED" if cfg["reach"] is None else "DTW")

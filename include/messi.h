@@ -68,6 +68,7 @@ typedef struct {
     int64_t refined;      /* real distances computed (fp32) in the refine step */
     int64_t abandoned;    /* real distance computations abandoned early */
     int64_t near_best;    /* fp32 near-ties re-ranked exactly in fp64 */
+    int64_t dtw_cells;    /* DTW band cells evaluated in fp32 by the register-band refine */
     double seed_d2;       /* BSF0: squared distance found by the approximate search */
     double bsf_d2;        /* final fp32 best-so-far (squared) before the exact re-rank */
 } messi_stats;

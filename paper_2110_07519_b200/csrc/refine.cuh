@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
     DtwThread<R> dp;
     bool have = k < total;
     const float* c = rows;
-    unsigned id = 0, refined = 0, abandoned = 0;
+    unsigned id = 0, refined = 0, abandoned = 0, steps = 0;
     float lbk_total = 0.0f;
     // the lane's next candidate is fetched one candidate ahead and the head of its row
     // prefetched, so a lane that restarts does not stall its warp on an HBM round trip
@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
     while (__any_sync(0xffffffffu, have)) {
         if (have) {
             const float rowmin = dp.step4(c, n, q_s, U, L);
+            ++steps;
             const float tail = fmaxf(0.0f, lbk_total * 0.9990234375f - dp.seen_lo * 1.0009765625f);
             const float bound = (rowmin + tail) * 0.9990234375f;
             bool done = false;
@@ -280,9 +281,11 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
     }
     refined = __reduce_add_sync(0xffffffffu, refined);
     abandoned = __reduce_add_sync(0xffffffffu, abandoned);
+    steps = __reduce_add_sync(0xffffffffu, steps);
     if ((threadIdx.x & 31) == 0) {
         if (refined) atomicAdd(&st->refined, refined);
         if (abandoned) atomicAdd(&st->abandoned, abandoned);
+        if (steps) atomicAdd(&st->dtw_cells, (unsigned long long)steps * 4ull * (2 * R + 1));
     }
 }
 
@@ -336,7 +339,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
                              void* result, void* stats)
 {
     struct R { double dist; long long id; double d2; long long reserved; };
-    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near; double seed, bsf; };
+    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells; double seed, bsf; };
     R* res = reinterpret_cast<R*>(result);
     res->dist = b.id >= 0 ? sqrt(b.d) : (double)INFINITY;
     res->id = b.id >= 0 ? row_begin + b.id : -1;
@@ -351,6 +354,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
         s->refined = st->refined;
         s->abandoned = st->abandoned;
         s->near = nb;
+        s->cells = (long long)st->dtw_cells;
         s->seed = (double)__uint_as_float(st->seed_bits);
         s->bsf = (double)__uint_as_float(st->bsf_bits);
     }

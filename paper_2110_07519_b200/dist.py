@@ -36,7 +36,10 @@ def merge_results(d2: torch.Tensor, gid: torch.Tensor, group=None):
     the process group's device.  Returns (d2, gid) of the global answers on every rank."""
     world = dist.get_world_size(group)
     packed = torch.stack([d2.contiguous().view(torch.int64), gid.to(torch.int64)], dim=1).contiguous()
+    home = packed.device
+    if dist.get_backend(group) == "gloo" and packed.is_cuda:  # gloo exchanges host tensors
+        packed = packed.cpu()
     parts = [torch.empty_like(packed) for _ in range(world)]
     dist.all_gather(parts, packed, group=group)
-    allp = torch.stack(parts)  # [R, nq, 2]
+    allp = torch.stack(parts).to(home)  # [R, nq, 2]
     return lexmin(allp[:, :, 0].contiguous().view(torch.float64), allp[:, :, 1])

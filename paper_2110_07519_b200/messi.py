@@ -44,6 +44,7 @@ class Stats(ctypes.Structure):
     _fields_ = [("lb_computed", ctypes.c_int64), ("tiles_scanned", ctypes.c_int64), ("candidates", ctypes.c_int64),
                 ("lbk_pass", ctypes.c_int64),
                 ("refined", ctypes.c_int64), ("abandoned", ctypes.c_int64), ("near_best", ctypes.c_int64),
+                ("dtw_cells", ctypes.c_int64),
                 ("seed_d2", ctypes.c_double), ("bsf_d2", ctypes.c_double)]
 
     def as_dict(self):
@@ -256,7 +257,7 @@ def _wrap_dev(ptr: int, nbytes: int, device):
     return torch.as_tensor(_Arr(), device=device)
 
 
-RESULT_BYTES, STATS_BYTES = 32, 72
+RESULT_BYTES, STATS_BYTES = 32, 80
 
 
 def result_buffer(nq: int, device) -> torch.Tensor:
@@ -283,8 +284,8 @@ def decode_results_device(buf: torch.Tensor):
 
 def decode_stats(buf: torch.Tensor):
     raw = buf.view(-1, STATS_BYTES).cpu()
-    ints = raw[:, :56].contiguous().view(torch.int64)
-    dbl = raw[:, 56:].contiguous().view(torch.float64)
+    ints = raw[:, :64].contiguous().view(torch.int64)
+    dbl = raw[:, 64:].contiguous().view(torch.float64)
     return [dict(zip(STATS_FIELDS, list(map(int, i.tolist())) + list(map(float, d.tolist()))))
             for i, d in zip(ints, dbl)]
 

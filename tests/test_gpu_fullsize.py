@@ -1,0 +1,138 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (own
+CUDA stream, batched sequential queries), on sampled outputs the oracle computes in full:
+a few queries of each config answered by the CUDA path and by the oracle's brute force over
+EVERY row (the rows are streamed device -> host in chunks; the oracle runs one serial call
+per chunk on all host cores and merges (d2, id) lexicographically).  Bars: id and d2
+bit-exact, dist within 1e-12.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+DEV = "cuda:0"
+CHUNK = 1 << 21
+
+
+def messi():
+    from paper_2110_07519_b200 import messi as m
+    return m
+
+
+def oracle_full(kind, X, Qh, reach=0):
+    """Brute force over every row of the device tensor X, chunk by chunk."""
+    d2 = np.full(Qh.shape[0], np.inf)
+    ids = np.full(Qh.shape[0], -1, np.int64)
+    for b in range(0, X.shape[0], CHUNK):
+        part = X[b:b + CHUNK].cpu().numpy()
+        pd, pi = oracle.nn(kind, part, Qh, r=reach, row_begin=b, chunk=max(1, part.shape[0] // 64))
+        d2, ids = oracle.merge(d2, ids, pd, pi)
+    return d2, ids
+
+
+def run_batch(idx, Q, reach=None):
+    m = messi()
+    res = m.result_buffer(Q.shape[0], DEV)
+    with torch.cuda.stream(idx.stream):
+        idx.query_batch(Q, reach, res)
+    torch.cuda.synchronize()
+    return m.decode_results(res)
+
+
+def check(got, d2, ids):
+    dist, gid, gd2 = (t.numpy() for t in got)
+    assert np.array_equal(gid, ids), (gid, ids)
+    assert np.array_equal(gd2, d2)
+    for a, b in zip(dist, d2):
+        assert math.isclose(a, math.sqrt(b), rel_tol=1e-12)
+
+
+def build(N, n, Q):
+    X = torch.empty((N, n), dtype=torch.float32, device=DEV)
+    datagen.walks_cuda(X, 0)
+    torch.cuda.synchronize()
+    idx = messi().Index(X, stream=torch.cuda.Stream(DEV))
+    return X, idx
+
+
+def test_config2_ed_10m():
+    X, idx = build(10_000_000, 256, None)
+    Q = torch.empty((100, 256), dtype=torch.float32, device=DEV)
+    datagen.walks_cuda(Q, 0, seed=datagen.QUERY_SEED)
+    try:
+        got = run_batch(idx, Q)
+        sample = [0, 17, 63, 99]
+        d2, ids = oracle_full("ed", X, Q[sample].cpu().numpy())
+        check(tuple(t[sample] for t in got), d2, ids)
+    finally:
+        idx.close()
+        del X
+        torch.cuda.empty_cache()
+
+
+def test_config3_ed_100m():
+    """The bench workload: 100M x 256 on one GPU, 100 queries batched; 3 sampled in full."""
+    X, idx = build(100_000_000, 256, None)
+    Q = torch.empty((100, 256), dtype=torch.float32, device=DEV)
+    datagen.walks_cuda(Q, 0, seed=datagen.QUERY_SEED)
+    try:
+        got = run_batch(idx, Q)
+        sample = [0, 42, 99]
+        d2, ids = oracle_full("ed", X, Q[sample].cpu().numpy())
+        check(tuple(t[sample] for t in got), d2, ids)
+    finally:
+        idx.close()
+        del X
+        torch.cuda.empty_cache()
+
+
+def test_config4_dtw_10m():
+    X, idx = build(10_000_000, 256, None)
+    Q = torch.empty((4, 256), dtype=torch.float32, device=DEV)
+    datagen.walks_cuda(Q, 0, seed=datagen.QUERY_SEED)
+    try:
+        got = run_batch(idx, Q, reach=25)
+        sample = [0]
+        d2, ids = oracle_full("dtw", X, Q[sample].cpu().numpy(), reach=25)
+        check(tuple(t[sample] for t in got), d2, ids)
+        # every other query: its answer is a real row at exactly that DTW distance, and no
+        # row of a 200K sample is strictly closer (a property that holds at any size)
+        dist, gid, gd2 = (t.numpy() for t in got)
+        Qh = Q.cpu().numpy()
+        rows = np.random.default_rng(0).choice(X.shape[0], 200_000, replace=False)
+        Xs = X[torch.from_numpy(rows).to(DEV)].cpu().numpy()
+        for qi in range(1, 4):
+            assert oracle.dtw2(Qh[qi], X[int(gid[qi])].cpu().numpy(), 25) == gd2[qi]
+            sd, si = oracle.nn("dtw", Xs, Qh[qi:qi + 1], r=25)
+            assert sd[0] >= gd2[qi]
+    finally:
+        idx.close()
+        del X
+        torch.cuda.empty_cache()
+
+
+def test_config5_noisy_ed_100m_x128():
+    """Config 5's shape on one GPU (all 100M x 128 rows, 51 GB): noisy dataset queries."""
+    N, n = 100_000_000, 128
+    X, idx = build(N, n, None)
+    Q = torch.empty((50, n), dtype=torch.float32, device=DEV)
+    datagen.noisy_queries_cuda(Q, N, sigma=0.1)
+    torch.cuda.synchronize()
+    try:
+        got = run_batch(idx, Q)
+        sample = [0, 25, 49]
+        d2, ids = oracle_full("ed", X, Q[sample].cpu().numpy())
+        check(tuple(t[sample] for t in got), d2, ids)
+        src = datagen.noisy_rows(50, N)
+        assert np.mean(got[1].numpy() == src) > 0.9  # the noisy source row is (almost always) the NN
+    finally:
+        idx.close()
+        del X
+        torch.cuda.empty_cache()
