@@ -69,6 +69,8 @@ typedef struct {
     int64_t abandoned;    /* real distance computations abandoned early */
     int64_t near_best;    /* fp32 near-ties re-ranked exactly in fp64 */
     int64_t dtw_cells;    /* DTW band cells evaluated in fp32 by the register-band refine */
+    int64_t exact;        /* real distances over the raw fp32 rows: ED = candidates whose
+                             quantised-row bound did not prune them; DTW = refined */
     double seed_d2;       /* BSF0: squared distance found by the approximate search */
     double bsf_d2;        /* final fp32 best-so-far (squared) before the exact re-rank */
 } messi_stats;
@@ -128,6 +130,11 @@ messi_status messi_debug_breakpoints(int32_t device, float* beta32_host);
 /* iSAX symbols [count][16] (u8) and, if cfg.keep_paa, PAA [count][16] (fp32) of every row,
  * de-tiled into caller device buffers (paa_dev may be NULL). */
 messi_status messi_debug_summaries(messi_index* idx, uint8_t* sym_dev, float* paa_dev);
+
+/* The quantised copy of the rows used by the ED refine's distance bound (DESIGN.md §5/§7),
+ * back in row order: q8_dev[count][n] bytes b = c + 128 (c = rint(x / s) in [-127, 127]) and
+ * meta_dev[count][2] fp32 {s, e}: s a power of two, e >= ||x - s c||_2.  Device buffers. */
+messi_status messi_debug_quantised(messi_index* idx, uint8_t* q8_dev, float* meta_dev);
 
 /* Sorted approximate-search keys and the row permutation (device pointers owned by idx). */
 messi_status messi_debug_order(messi_index* idx, const uint64_t** skey_dev, const uint32_t** perm_dev);

@@ -52,6 +52,9 @@ struct messi_index {
     uint4* tiles = nullptr;          // 8-bit iSAX words, 8 KB per 512 sorted positions
     unsigned char* boxes = nullptr;  // [ntiles][32]: per-segment min / max symbol
     float* paa = nullptr;
+    unsigned char* rows8 = nullptr;  // quantised rows in sorted order [npad][n] (biased int8)
+    float2* meta8 = nullptr;         // per sorted position {scale (power of 2), error norm bound}
+    float q8_omd = 1.0f;             // 1 - delta of the quantised bound (rounded down)
     unsigned long long* skey = nullptr;
     unsigned* perm = nullptr;
     float *beta32 = nullptr, *lo_w = nullptr, *hi_w = nullptr;
@@ -70,7 +73,7 @@ struct messi_index {
 };
 
 static_assert(sizeof(messi_result) == 32, "messi_result layout");
-static_assert(sizeof(messi_stats) == 80, "messi_stats layout");
+static_assert(sizeof(messi_stats) == 88, "messi_stats layout");
 
 enum { K_SEED = 0, K_SCAN = 1, K_REFINE = 2, K_LBK = 3, K_RESOLVE = 4, K_KINDS = 5 };
 
@@ -233,6 +236,16 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
         (s = dalloc(&idx->boxes, (size_t)idx->ntiles * 32)))
         return bail(s);
     if (idx->keep_paa && (s = dalloc(&idx->paa, (size_t)N * MESSI_W))) return bail(s);
+    if ((s = dalloc(&idx->rows8, npadrows * (size_t)n)) || (s = dalloc(&idx->meta8, npadrows))) return bail(s);
+    {
+        // relative error of the fp32 sqrt of the quantised distance: the sum of
+        // n non-negative fma terms plus the 3-level group reduction is within (n + 8) u of the
+        // exact value; delta = max(2^-12, (n + 16) 2^-23) covers it twice over
+        double delta = (double)(n + 16) * 0x1p-23;
+        if (delta < 0x1p-12) delta = 0x1p-12;
+        idx->q8_omd = (float)(1.0 - delta);  // 1 - delta is exact in fp32 up to rounding down below
+        if ((double)idx->q8_omd > 1.0 - delta) idx->q8_omd = nextafterf(idx->q8_omd, 0.0f);
+    }
     if ((s = dalloc(&idx->skey, (size_t)N)) || (s = dalloc(&idx->perm, (size_t)N))) return bail(s);
     if ((s = dalloc(&idx->beta32, 256)) || (s = dalloc(&idx->lo_w, 256)) || (s = dalloc(&idx->hi_w, 256))) return bail(s);
     for (Slot& sl : idx->slot) {
@@ -288,6 +301,11 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
         ++idx->launches;
         e = cudaGetLastError();
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "k_layout: %s", cudaGetErrorString(e)); break; }
+        k_quantise<<<(unsigned)(idx->sms * 8), 256, 0, st>>>(rows_dev, idx->perm, N, (int64_t)npadrows, n, idx->rows8,
+                                                            idx->meta8);
+        ++idx->launches;
+        e = cudaGetLastError();
+        if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "k_quantise: %s", cudaGetErrorString(e)); break; }
         for (Slot& sl : idx->slot) {
             k_arm<<<1, 1, 0, st>>>(sl.st);
             ++idx->launches;
@@ -310,8 +328,8 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->rstr) cudaStreamSynchronize(idx->rstr);
     if (idx->stream) cudaStreamSynchronize(idx->stream);
     else cudaDeviceSynchronize();
-    void* ptrs[] = {idx->tiles, idx->boxes, idx->paa,  idx->skey, idx->perm,  idx->beta32,
-                    idx->lo_w,  idx->hi_w,  idx->qbuf, idx->res1, idx->stats1};
+    void* ptrs[] = {idx->tiles, idx->boxes, idx->paa,  idx->skey, idx->perm,  idx->beta32, idx->lo_w,
+                    idx->hi_w,  idx->qbuf,  idx->res1, idx->stats1, idx->rows8, idx->meta8};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (Slot& sl : idx->slot) {
@@ -486,7 +504,8 @@ static messi_status run_ed(messi_index* idx, const float* q_dev, messi_result* r
     {
         ProfScope ps(idx, K_REFINE, idx->rstr);
         k_refine_ed<<<refine_grid(idx, 32768), 256, refine_ed_smem(n), idx->rstr>>>(
-            sl.cand, idx->perm, idx->rows, n, q_dev, sl.st, sl.near, idx->N, idx->row_begin, res, stats);
+            sl.cand, idx->perm, idx->rows, n, q_dev, idx->rows8, idx->meta8, idx->q8_omd, sl.st, sl.near, idx->N,
+            idx->row_begin, res, stats);
         LAUNCHED(idx);
     }
     CK(cudaEventRecord(sl.ev_done, idx->rstr));
@@ -665,6 +684,19 @@ extern "C" messi_status messi_debug_summaries(messi_index* idx, uint8_t* sym_dev
     if (paa_dev)
         CK(cudaMemcpyAsync(paa_dev, idx->paa, (size_t)idx->N * MESSI_W * sizeof(float), cudaMemcpyDeviceToDevice,
                            idx->stream));
+    CK(cudaStreamSynchronize(idx->stream));
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_debug_quantised(messi_index* idx, uint8_t* q8_dev, float* meta_dev)
+{
+    g_err[0] = 0;
+    if (!idx || !q8_dev || !meta_dev) return fail(MESSI_EINVAL, "NULL argument");
+    CK(cudaSetDevice(idx->device));
+    TRY(sync_all(idx));
+    k_unsort_q8<<<(unsigned)(idx->sms * 8), 256, 0, idx->stream>>>(idx->rows8, idx->meta8, idx->perm, idx->N, idx->n,
+                                                                   q8_dev, reinterpret_cast<float2*>(meta_dev));
+    LAUNCHED(idx);
     CK(cudaStreamSynchronize(idx->stream));
     return MESSI_OK;
 }

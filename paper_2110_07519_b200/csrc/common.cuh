@@ -29,6 +29,7 @@ struct QState {
     unsigned abandoned;     // real distances abandoned early
     unsigned done;          // CTAs of the refine stage that finished (last one resolves)
     unsigned tile_count;    // tiles whose box bound <= BSF0 * (1 + eps) (scanned)
+    unsigned exact;         // ED: fp32 distances over the raw rows (quantised bound passed)
     unsigned long long dtw_cells;  // DTW band cells evaluated in fp32 (refine)
     unsigned long long qkey;  // query's approximate-search key
     int window_start;       // first sorted position of the approximate-search window
@@ -49,6 +50,7 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->abandoned = 0;
     st->done = 0;
     st->tile_count = 0;
+    st->exact = 0;
     st->dtw_cells = 0;
 }
 

@@ -64,6 +64,87 @@ __device__ void refine_ed_pass(unsigned pass, unsigned my_id, const float* __res
     }
 }
 
+// Quantised-row bound (DESIGN.md §5/§7): for the candidates of `pass` (lane bit = candidate
+// held by that lane at sorted position my_pos), the fp32 squared distance dh2 between the
+// query and the dequantised row s*c (n bytes from rows8, biased by 128) gives
+//     ||q - x|| >= ||q - s c|| - e >= sqrt_rd(dh2) * (1 - delta) - e   (= L),
+// delta bounding the relative fp32 error of sqrt(dh2) (s*c exact: s is a power of two).  A
+// candidate with L > 0 and L^2 > thr cannot be the nearest neighbour; the others are
+// returned (bit set) for the exact fp32 refine.  Groups of 8 lanes take one row each, two
+// rows per group in flight (8 rows = 8n bytes per warp); lane gl of a group reads the 16 B
+// chunks gl, gl+8, ... of its rows.  Bytes convert exactly with the 2^23 trick:
+// float(0x4B000000 | b) = 2^23 + b.
+__device__ __forceinline__ unsigned q8_bound_pass(unsigned pass, unsigned my_pos, const unsigned char* __restrict__ rows8,
+                                                  const float2* __restrict__ meta8, int n, const float* __restrict__ q_s,
+                                                  float one_minus_delta, QState* st, int lane)
+{
+    const int g = lane >> 3, gl = lane & 7;
+    unsigned keep = 0;
+    while (pass) {
+        int src[8];
+        bool ok[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            ok[j] = pass != 0;
+            src[j] = ok[j] ? __ffs(pass) - 1 : 0;
+            pass &= pass - 1;
+        }
+        // this group's two rows: slots g and g + 4
+        const int sa = g == 0 ? src[0] : g == 1 ? src[1] : g == 2 ? src[2] : src[3];
+        const int sb = g == 0 ? src[4] : g == 1 ? src[5] : g == 2 ? src[6] : src[7];
+        const bool oa = g == 0 ? ok[0] : g == 1 ? ok[1] : g == 2 ? ok[2] : ok[3];
+        const bool ob = g == 0 ? ok[4] : g == 1 ? ok[5] : g == 2 ? ok[6] : ok[7];
+        const unsigned pa = __shfl_sync(0xffffffffu, my_pos, sa);
+        const unsigned pb = __shfl_sync(0xffffffffu, my_pos, sb);
+        const float2 ma = oa ? meta8[pa] : make_float2(0.0f, 0.0f);
+        const float2 mb = ob ? meta8[pb] : make_float2(0.0f, 0.0f);
+        const unsigned char* ra = rows8 + (long long)pa * n;
+        const unsigned char* rb = rows8 + (long long)pb * n;
+        float acc_a = 0.0f, acc_b = 0.0f;
+        for (int c = gl * 16; c < n; c += 128) {
+            const uint4 wa = oa ? __ldg(reinterpret_cast<const uint4*>(ra + c)) : make_uint4(0, 0, 0, 0);
+            const uint4 wb = ob ? __ldg(reinterpret_cast<const uint4*>(rb + c)) : make_uint4(0, 0, 0, 0);
+            const unsigned xa[4] = {wa.x, wa.y, wa.z, wa.w}, xb[4] = {wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const float4 qv = *reinterpret_cast<const float4*>(q_s + c + 4 * w);
+                const float qq[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const unsigned sel = 0x7650u | (unsigned)b;  // byte b of x, then 0x4B000000's bytes
+                    const float ca = __uint_as_float(__byte_perm(xa[w], 0x4B000000u, sel)) - 8388736.0f;  // - (2^23 + 128)
+                    const float cb = __uint_as_float(__byte_perm(xb[w], 0x4B000000u, sel)) - 8388736.0f;
+                    const float da = fmaf(-ma.x, ca, qq[b]);
+                    const float db = fmaf(-mb.x, cb, qq[b]);
+                    acc_a = fmaf(da, da, acc_a);
+                    acc_b = fmaf(db, db, acc_b);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 4; o; o >>= 1) {
+            acc_a += __shfl_xor_sync(0xffffffffu, acc_a, o);
+            acc_b += __shfl_xor_sync(0xffffffffu, acc_b, o);
+        }
+        const float thr = slack_up(ld_bsf(st));
+        auto survives = [&](float acc, float e) {
+            const float L = __fsub_rd(__fmul_rd(__fsqrt_rd(acc), one_minus_delta), e);
+            return !(L > 0.0f && __fmul_rd(L, L) > thr);
+        };
+        const bool ka = oa && survives(acc_a, ma.y);
+        const bool kb = ob && survives(acc_b, mb.y);
+        // lane gl == 0 of each group reports; collect the source-lane bits
+        const unsigned ba = __ballot_sync(0xffffffffu, gl == 0 && ka);
+        const unsigned bb = __ballot_sync(0xffffffffu, gl == 0 && kb);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (ba & (1u << (8 * j))) keep |= 1u << src[j];
+            if (bb & (1u << (8 * j))) keep |= 1u << src[j + 4];
+        }
+    }
+    return keep;
+}
+
 struct Best { double d; long long id; };
 __device__ void resolve_ed_block(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
                                  const NearEntry* __restrict__ near, QState* st, long long N, long long row_begin,
@@ -86,6 +167,8 @@ __host__ __device__ inline size_t refine_ed_smem(int n)
 // and writes the query's result (A9).  Shared memory: q (n floats), reused by the resolve.
 __global__ void __launch_bounds__(256) k_refine_ed(const uint2* __restrict__ cand, const unsigned* __restrict__ perm,
                                                    const float* __restrict__ rows, int n, const float* __restrict__ q_g,
+                                                   const unsigned char* __restrict__ rows8,
+                                                   const float2* __restrict__ meta8, float one_minus_delta,
                                                    QState* st, NearEntry* near, long long N, long long row_begin,
                                                    void* result, void* stats)
 {
@@ -95,7 +178,7 @@ __global__ void __launch_bounds__(256) k_refine_ed(const uint2* __restrict__ can
     const unsigned total = *(volatile unsigned*)&st->cand_count;
     const int lane = threadIdx.x & 31;
     const unsigned wpb = blockDim.x >> 5;
-    unsigned n_ref = 0;
+    unsigned n_ref = 0, n_exact = 0;
     for (unsigned k0 = (blockIdx.x * wpb + (threadIdx.x >> 5)) * 32; k0 < total; k0 += gridDim.x * wpb * 32) {
         const bool valid = k0 + lane < total;
         const uint2 e = valid ? cand[k0 + lane] : make_uint2(0u, 0x7f800000u);
@@ -103,9 +186,12 @@ __global__ void __launch_bounds__(256) k_refine_ed(const uint2* __restrict__ can
         const bool ok = valid && __uint_as_float(e.y) <= thr;
         const unsigned pass = __ballot_sync(0xffffffffu, ok);
         n_ref += __popc(pass);
-        refine_ed_pass(pass, ok ? perm[e.x] : 0u, rows, n, q_s, st, near, lane);
+        const unsigned keep = q8_bound_pass(pass, e.x, rows8, meta8, n, q_s, one_minus_delta, st, lane);
+        n_exact += __popc(keep);
+        refine_ed_pass(keep, (keep >> lane) & 1u ? perm[e.x] : 0u, rows, n, q_s, st, near, lane);
     }
     if (lane == 0 && n_ref) atomicAdd(&st->refined, n_ref);
+    if (lane == 0 && n_exact) atomicAdd(&st->exact, n_exact);
     __shared__ bool last;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -339,7 +425,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
                              void* result, void* stats)
 {
     struct R { double dist; long long id; double d2; long long reserved; };
-    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells; double seed, bsf; };
+    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells, exact; double seed, bsf; };
     R* res = reinterpret_cast<R*>(result);
     res->dist = b.id >= 0 ? sqrt(b.d) : (double)INFINITY;
     res->id = b.id >= 0 ? row_begin + b.id : -1;
@@ -355,6 +441,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
         s->abandoned = st->abandoned;
         s->near = nb;
         s->cells = (long long)st->dtw_cells;
+        s->exact = st->exact ? st->exact : st->refined;
         s->seed = (double)__uint_as_float(st->seed_bits);
         s->bsf = (double)__uint_as_float(st->bsf_bits);
     }

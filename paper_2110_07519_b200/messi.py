@@ -44,7 +44,7 @@ class Stats(ctypes.Structure):
     _fields_ = [("lb_computed", ctypes.c_int64), ("tiles_scanned", ctypes.c_int64), ("candidates", ctypes.c_int64),
                 ("lbk_pass", ctypes.c_int64),
                 ("refined", ctypes.c_int64), ("abandoned", ctypes.c_int64), ("near_best", ctypes.c_int64),
-                ("dtw_cells", ctypes.c_int64),
+                ("dtw_cells", ctypes.c_int64), ("exact", ctypes.c_int64),
                 ("seed_d2", ctypes.c_double), ("bsf_d2", ctypes.c_double)]
 
     def as_dict(self):
@@ -79,6 +79,7 @@ def lib():
         L.messi_debug_scan_repeat.argtypes = [vp, vp, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
         L.messi_debug_breakpoints.argtypes = [i32, vp]
         L.messi_debug_summaries.argtypes = [vp, vp, vp]
+        L.messi_debug_quantised.argtypes = [vp, vp, vp]
         L.messi_debug_order.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]
         L.messi_debug_lower_bounds.argtypes = [vp, vp, i32, vp]
         L.messi_debug_tile_bounds.argtypes = [vp, vp, i32, vp]
@@ -96,7 +97,7 @@ EXPORTED = ["messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_
             "messi_free", "messi_last_error", "messi_launch_count", "messi_profile_enable", "messi_profile_read",
             "messi_debug_breakpoints",
             "messi_debug_summaries", "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances",
-            "messi_debug_scan_repeat", "messi_debug_tile_bounds"]
+            "messi_debug_scan_repeat", "messi_debug_tile_bounds", "messi_debug_quantised"]
 
 
 def _check(status: int):
@@ -146,7 +147,7 @@ def messi_query_dtw(handle, query, reach: int, with_stats: bool = False):
 
 def messi_query_ed_batch(handle, queries_dev: torch.Tensor, results_dev: torch.Tensor, stats_dev=None):
     """Asynchronous on the build stream.  results_dev: uint8 CUDA tensor of nq*32 bytes (see
-    ``result_buffer``); stats_dev: optional nq*72 bytes (``stats_buffer``)."""
+    ``result_buffer``); stats_dev: optional nq*88 bytes (``stats_buffer``)."""
     _check(lib().messi_query_ed_batch(handle, _ptr(queries_dev), queries_dev.shape[0], _ptr(results_dev),
                                       _ptr(stats_dev)))
 
@@ -199,6 +200,14 @@ def messi_debug_summaries(handle, count: int, device, with_paa: bool = False):
     paa = torch.empty((count, 16), dtype=torch.float32, device=device) if with_paa else None
     _check(lib().messi_debug_summaries(handle, _ptr(sym), _ptr(paa)))
     return sym, paa
+
+
+def messi_debug_quantised(handle, count: int, n: int, device):
+    """(q8 uint8 [count, n] biased by 128, meta float32 [count, 2] = {scale, error bound}), row order."""
+    q8 = torch.empty((count, n), dtype=torch.uint8, device=device)
+    meta = torch.empty((count, 2), dtype=torch.float32, device=device)
+    _check(lib().messi_debug_quantised(handle, _ptr(q8), _ptr(meta)))
+    return q8, meta
 
 
 def messi_debug_order(handle, count: int, device):
@@ -257,7 +266,7 @@ def _wrap_dev(ptr: int, nbytes: int, device):
     return torch.as_tensor(_Arr(), device=device)
 
 
-RESULT_BYTES, STATS_BYTES = 32, 80
+RESULT_BYTES, STATS_BYTES = 32, 88
 
 
 def result_buffer(nq: int, device) -> torch.Tensor:
@@ -284,8 +293,8 @@ def decode_results_device(buf: torch.Tensor):
 
 def decode_stats(buf: torch.Tensor):
     raw = buf.view(-1, STATS_BYTES).cpu()
-    ints = raw[:, :64].contiguous().view(torch.int64)
-    dbl = raw[:, 64:].contiguous().view(torch.float64)
+    ints = raw[:, :72].contiguous().view(torch.int64)
+    dbl = raw[:, 72:].contiguous().view(torch.float64)
     return [dict(zip(STATS_FIELDS, list(map(int, i.tolist())) + list(map(float, d.tolist()))))
             for i, d in zip(ints, dbl)]
 

@@ -171,6 +171,34 @@ def test_distances_elementwise(c1, reach):
     assert np.allclose(d32, ref, rtol=2.0 ** -16, atol=1e-6)
 
 
+# ------------------------------------------------------- quantised-row bound
+def test_quantised_rows_and_bound(c1):
+    """The refine's quantised copy: c = rint(x / s) with s the smallest power of two such
+    that max|x| <= 127 s; e >= ||x - s c|| (and tight); the bound ||q - s c|| - e never exceeds
+    the true distance ||q - x|| (triangle inequality) -- checked in fp64 on every row of C1
+    for every C1 query, and the kernel's own fp32 evaluation is covered by the 1-NN parity."""
+    X, Q, idx, Xh, Qh = c1
+    q8, meta = messi().messi_debug_quantised(idx.handle, X.shape[0], X.shape[1], X.device)
+    c = q8.cpu().numpy().astype(np.int64) - 128
+    s = meta[:, 0].cpu().numpy().astype(np.float64)
+    e = meta[:, 1].cpu().numpy().astype(np.float64)
+    x = Xh.astype(np.float64)
+    assert np.all(np.abs(c) <= 127)
+    m, ex = np.frexp(s)
+    assert np.all(m == 0.5)  # powers of two
+    mx = np.abs(x).max(axis=1)
+    assert np.all(mx <= 127 * s) and np.all((mx > 127 * s / 2) | (mx == 0))
+    assert np.array_equal(c, np.rint(x / s[:, None]).astype(np.int64))
+    r = np.sqrt(((x - s[:, None] * c) ** 2).sum(axis=1))
+    assert np.all(e >= r) and np.all(e <= r * (1 + 2.0 ** -20) + 1e-30)
+    deq = s[:, None] * c
+    for qi in range(Q.shape[0]):
+        q = Qh[qi].astype(np.float64)
+        true = np.sqrt(((x - q) ** 2).sum(axis=1))
+        lb = np.sqrt(((deq - q) ** 2).sum(axis=1)) - e
+        assert np.all(lb <= true * (1 + 1e-12))
+
+
 # --------------------------------------------------------------------- 1-NN end to end
 def check_nn(got, ref_d2, ref_id):
     dist, gid, d2 = got[:3]
@@ -190,7 +218,7 @@ def test_nn_ed_config1(c1):
         assert 1 <= st["tiles_scanned"] <= (X.shape[0] + 511) // 512
         assert st["lb_computed"] <= X.shape[0]
         assert st["seed_d2"] >= st["bsf_d2"] >= 0  # BSF only decreases (Obs. 1)
-        assert st["near_best"] >= 1 and st["candidates"] >= st["refined"] >= 1
+        assert st["near_best"] >= 1 and st["candidates"] >= st["refined"] >= st["exact"] >= 1
 
 
 def test_nn_ed_host_query_and_batch(c1):
