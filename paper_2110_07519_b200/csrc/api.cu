@@ -25,6 +25,7 @@
 #include "refine.cuh"
 #include "scan.cuh"
 #include "summarise.cuh"
+#include "fused.cuh"
 
 using namespace messi;
 
@@ -58,6 +59,12 @@ struct messi_index {
     unsigned long long* skey = nullptr;
     unsigned* perm = nullptr;
     float *beta32 = nullptr, *lo_w = nullptr, *hi_w = nullptr;
+    // batched ED path (fused.cuh): per-query state, tables and tile lists of one launch group
+    QState* bst = nullptr;
+    float *lutc = nullptr, *lutx = nullptr, *lutf = nullptr;
+    uint2* btlist = nullptr;
+    unsigned* work = nullptr;
+    int fused_grid = 0;
     // per-query scratch
     Slot slot[2];
     unsigned long long qcount = 0;
@@ -166,12 +173,12 @@ static messi_status setup_kernels()
     const int big = 200 * 1024;
     CK(cudaFuncSetAttribute(k_scan<SCAN_COMPACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
     CK(cudaFuncSetAttribute(k_scan<SCAN_ALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
-    CK(cudaFuncSetAttribute(k_refine_ed, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_scan_refine_ed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(MESSI_MAX_N)));
+    CK(cudaFuncSetAttribute(k_filter_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, kFilterQ * kLutF * 4));
     CK(cudaFuncSetAttribute(k_lbk_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_refine_dtw_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_resolve_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CK(cudaFuncSetAttribute(k_resolve_ed, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
 #define SET_ATTR_R(R) CK(cudaFuncSetAttribute(k_refine_dtw<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
     MESSI_DTW_REACHES(SET_ATTR_R)
 #undef SET_ATTR_R
@@ -332,6 +339,11 @@ extern "C" void messi_free(messi_index* idx)
                     idx->hi_w,  idx->qbuf,  idx->res1, idx->stats1, idx->rows8, idx->meta8};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    {
+        void* bp[] = {idx->bst, idx->lutc, idx->lutx, idx->lutf, idx->btlist, idx->work};
+        for (void* p : bp)
+            if (p) cudaFree(p);
+    }
     for (Slot& sl : idx->slot) {
         void* sp[] = {sl.st, sl.lut, sl.U, sl.L, sl.cand, sl.list2, sl.near, sl.tlist};
         for (void* p : sp)
@@ -483,32 +495,59 @@ static messi_status launch_scan(messi_index* idx, Slot& sl)
     return MESSI_OK;
 }
 
-static messi_status run_ed(messi_index* idx, const float* q_dev, messi_result* res, messi_stats* stats)
+static messi_status ensure_batch_buffers(messi_index* idx)
 {
-    Slot& sl = idx->slot[idx->qcount++ & 1];
+    if (idx->bst) return MESSI_OK;
+    TRY(dalloc(&idx->bst, kBatchMax));
+    TRY(dalloc(&idx->lutc, (size_t)kBatchMax * MESSI_W * MESSI_CARD));
+    TRY(dalloc(&idx->lutx, (size_t)kBatchMax * kLutX));
+    TRY(dalloc(&idx->lutf, (size_t)kBatchMax * kLutF));
+    TRY(dalloc(&idx->btlist, (size_t)kBatchMax * (size_t)idx->ntiles));
+    TRY(dalloc(&idx->work, 1));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan_refine_ed, 32 * kFusedWarps, fused_smem(idx->n)));
+    idx->fused_grid = idx->sms * (occ < 1 ? 1 : occ);
+    return MESSI_OK;
+}
+
+// The batched ED path (fused.cuh) for nq queries [nq][n] on the device: groups of up to
+// kBatchMax queries, four launches per group on the index stream.
+static messi_status run_ed_batch(messi_index* idx, const float* queries_dev, int nq, messi_result* results_dev,
+                                 messi_stats* stats_dev)
+{
+    TRY(ensure_batch_buffers(idx));
     const int n = idx->n;
     const size_t qsm = (size_t)((n + 3) & ~3) * sizeof(float);
-    int len = (int)(idx->window < idx->N ? idx->window : idx->N);
-    int seed_grid = (len + 7) / 8;
-    if (seed_grid > 256) seed_grid = 256;
-    CK(cudaStreamWaitEvent(idx->side, sl.ev_done, 0));  // the slot's previous query is finished
-    {
-        ProfScope ps(idx, K_SEED, idx->side);
-        k_seed_ed<<<seed_grid, 256, qsm, idx->side>>>(q_dev, n, idx->rows, idx->skey, idx->perm, idx->N, idx->window,
-                                                      idx->beta32, idx->lo_w, idx->hi_w, sl.lut, sl.st);
-        LAUNCHED(idx);
-        TRY(launch_tile_filter(idx, sl, idx->side));
+    cudaStream_t st = idx->stream;
+    const int len = (int)(idx->window < idx->N ? idx->window : idx->N);
+    for (int g0 = 0; g0 < nq; g0 += kBatchMax) {
+        const int B = nq - g0 < kBatchMax ? nq - g0 : kBatchMax;
+        const float* q = queries_dev + (size_t)g0 * n;
+        {
+            ProfScope ps(idx, K_SEED, st);
+            k_prologue_batch<<<B, 256, qsm, st>>>(q, n, idx->beta32, idx->lo_w, idx->hi_w, idx->skey, idx->N,
+                                                  idx->window, idx->lutc, idx->lutx, idx->lutf, idx->bst, idx->work);
+            LAUNCHED(idx);
+            dim3 sg((unsigned)((len + kSeedRowsPerCta - 1) / kSeedRowsPerCta), (unsigned)B);
+            k_seed_batch<<<sg, 256, qsm, st>>>(q, n, idx->rows, idx->perm, idx->bst);
+            LAUNCHED(idx);
+            long long fx = (idx->ntiles + 255) / 256;
+            const long long fcap = (long long)idx->sms * 3 * 2 / ((B + kFilterQ - 1) / kFilterQ) + 1;
+            if (fx > fcap) fx = fcap;
+            dim3 fg((unsigned)fx, (unsigned)((B + kFilterQ - 1) / kFilterQ));
+            k_filter_batch<<<fg, 256, kFilterQ * kLutF * 4, st>>>(idx->boxes, idx->ntiles, idx->lutf, idx->bst, B,
+                                                                  idx->btlist);
+            LAUNCHED(idx);
+        }
+        {
+            ProfScope ps(idx, K_SCAN, st);
+            k_scan_refine_ed<<<idx->fused_grid, 32 * kFusedWarps, fused_smem(n), st>>>(
+                idx->tiles, idx->ntiles, idx->N, n, q, idx->lutx, idx->btlist, idx->bst, B, idx->rows8, idx->meta8,
+                idx->q8_omd, idx->perm, idx->rows, idx->row_begin, idx->work, results_dev + g0,
+                stats_dev ? stats_dev + g0 : nullptr);
+            LAUNCHED(idx);
+        }
     }
-    CK(cudaEventRecord(sl.ev_seed, idx->side));
-    TRY(launch_scan(idx, sl));
-    {
-        ProfScope ps(idx, K_REFINE, idx->rstr);
-        k_refine_ed<<<refine_grid(idx, 32768), 256, refine_ed_smem(n), idx->rstr>>>(
-            sl.cand, idx->perm, idx->rows, n, q_dev, idx->rows8, idx->meta8, idx->q8_omd, sl.st, sl.near, idx->N,
-            idx->row_begin, res, stats);
-        LAUNCHED(idx);
-    }
-    CK(cudaEventRecord(sl.ev_done, idx->rstr));
     return MESSI_OK;
 }
 
@@ -608,8 +647,7 @@ extern "C" messi_status messi_query_ed(messi_index* idx, const float* query, mes
     CK(cudaSetDevice(idx->device));
     const float* q = nullptr;
     TRY(stage_query(idx, query, &q));
-    TRY(fork_streams(idx));
-    TRY(run_ed(idx, q, idx->res1, idx->stats1));
+    TRY(run_ed_batch(idx, q, 1, idx->res1, idx->stats1));
     return finish_single(idx, local_best, stats);
 }
 
@@ -634,10 +672,9 @@ extern "C" messi_status messi_query_ed_batch(messi_index* idx, const float* quer
     g_err[0] = 0;
     if (!idx || !queries_dev || !results_dev || nq < 0) return fail(MESSI_EINVAL, "bad argument");
     CK(cudaSetDevice(idx->device));
-    TRY(fork_streams(idx));
-    for (int i = 0; i < nq; ++i)
-        TRY(run_ed(idx, queries_dev + (size_t)i * idx->n, results_dev + i, stats_dev ? stats_dev + i : nullptr));
-    return join_streams(idx);
+    TRY(join_streams(idx));  // earlier DTW queries (other streams) before the ED batch reuses qbuf users
+    if (nq == 0) return MESSI_OK;
+    return run_ed_batch(idx, queries_dev, nq, results_dev, stats_dev);
 }
 
 extern "C" messi_status messi_query_dtw_batch(messi_index* idx, const float* queries_dev, int32_t nq, int32_t reach,

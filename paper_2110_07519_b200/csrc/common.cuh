@@ -30,11 +30,17 @@ struct QState {
     unsigned done;          // CTAs of the refine stage that finished (last one resolves)
     unsigned tile_count;    // tiles whose box bound <= BSF0 * (1 + eps) (scanned)
     unsigned exact;         // ED: fp32 distances over the raw rows (quantised bound passed)
+    unsigned tiles_scanned; // batch ED: tiles whose box bound still passed the CURRENT BSF
+    unsigned chunks_done;   // batch ED: work chunks of this query finished (last one finalises)
+    unsigned lock;          // batch ED: guards best_d / best_id
     unsigned long long dtw_cells;  // DTW band cells evaluated in fp32 (refine)
+    double best_d;          // batch ED: lexicographic min (d64, id) over the fp64 re-ranked rows
+    long long best_id;
     unsigned long long qkey;  // query's approximate-search key
     int window_start;       // first sorted position of the approximate-search window
     int window_len;
     double ubar[16], lbar[16];  // query PAA (ED: both) or envelope PAA (DTW), fp64
+    unsigned char zlo[16], zhi[16];  // batch ED: per segment, the symbols whose table entry is 0
 };
 
 struct NearEntry { unsigned id; float d32; };
@@ -51,6 +57,11 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->done = 0;
     st->tile_count = 0;
     st->exact = 0;
+    st->tiles_scanned = 0;
+    st->chunks_done = 0;
+    st->lock = 0;
+    st->best_d = (double)INFINITY;
+    st->best_id = -1;
     st->dtw_cells = 0;
 }
 

@@ -1,0 +1,501 @@
+// fused.cuh -- the batched ED query path: B queries per launch group, four kernels.
+//
+//   k_prologue_batch  (B CTAs)        query PAA, key, lower-bound tables (A3), and the
+//                                     approximate-search position of the key (A4 part 1)
+//   k_seed_batch      (S x B CTAs)    real distances of the window rows -> BSF0 (A4)
+//   k_filter_batch    (tiles x B/2)   box bound of every tile for every query (Alg. 7 node
+//                                     pruning on the flat tile array) -> per-query tile lists
+//   k_scan_refine_ed  (persistent)    work chunks of (query, 16 listed tiles) in query order:
+//                                     box re-check against the CURRENT BSF, series bounds
+//                                     (A5), quantised-row bound, fp32 distance (A7), fp64
+//                                     re-rank of near-best rows (A9) -- all in one pass, as
+//                                     Alg. 9's workers do; the CTA finishing a
+//                                     query's last chunk writes its result.
+//
+// The batch replaces MESSI's one-query-at-a-time loop by one persistent pass
+// over the work of all B queries (results per query are unchanged: every query is exact).
+#pragma once
+#include "common.cuh"
+#include "dtw.cuh"
+#include "refine.cuh"
+#include "scan.cuh"
+
+namespace messi {
+
+constexpr int kLutX = MESSI_CARD * 64;   // expanded scan table: word v*64 + 16h + s (64 KB)
+constexpr int kLutF = MESSI_CARD * 32;   // filter table: word v*32 + 16h + s (32 KB)
+constexpr int kChunkTiles = 16;          // tiles per work chunk (2 per warp)
+constexpr int kFusedWarps = 8;
+constexpr int kBatchMax = 128;           // queries per launch group
+constexpr int kFilterQ = 2;              // queries per filter CTA
+
+// ------------------------------------------------------------------------ prologue
+// One CTA per query: arms the query's state, runs the prologue (prologue_block: PAA in fp64,
+// key, T[s][v] rounded down) into the compact table, then lays the table out for the scan
+// (expanded, conflict-free) and the filter, finds the per-segment zero runs
+// [zlo_s, zhi_s] of T (T[s][.] is non-increasing, zero on one run, non-decreasing: the box
+// of a symbol moves monotonically past the query mean), and locates the query's key in the
+// sorted keys (the approximate-search window, reading R14).
+__global__ void __launch_bounds__(256) k_prologue_batch(const float* __restrict__ queries, int n,
+                                                        const float* __restrict__ beta_g, const float* __restrict__ lo_w,
+                                                        const float* __restrict__ hi_w,
+                                                        const unsigned long long* __restrict__ skey, long long N,
+                                                        int window, float* __restrict__ lutc_all,
+                                                        float* __restrict__ lutx_all, float* __restrict__ lutf_all,
+                                                        QState* st_all, unsigned* work)
+{
+    extern __shared__ __align__(16) float q_s[];
+    __shared__ unsigned long long qkey_s;
+    const int b = blockIdx.x;
+    QState* st = st_all + b;
+    const float* q = queries + (size_t)b * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q[i];
+    if (threadIdx.x == 0) {
+        arm_state(st);
+        if (b == 0) *work = 0u;
+    }
+    __syncthreads();
+    float* lutc = lutc_all + (size_t)b * (MESSI_W * MESSI_CARD);
+    prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, lutc, nullptr, nullptr, &qkey_s, st);
+    __syncthreads();
+    float* lutx = lutx_all + (size_t)b * kLutX;
+    float* lutf = lutf_all + (size_t)b * kLutF;
+    for (int i = threadIdx.x; i < MESSI_W * MESSI_CARD; i += blockDim.x) {
+        const int s = i >> 8, v = i & 255;
+        const float val = lutc[i];
+        lutx[v * 64 + s] = val;
+        lutx[v * 64 + 16 + s] = val;
+        lutf[v * 32 + s] = val;
+        lutf[v * 32 + 16 + s] = val;
+    }
+    if (threadIdx.x < MESSI_W) {
+        const int s = threadIdx.x;
+        int lo = 256, hi = -1;
+        for (int v = 0; v < 256; ++v)
+            if (lutc[s * 256 + v] == 0.0f) { lo = min(lo, v); hi = max(hi, v); }
+        if (hi < 0) { lo = 255; hi = 0; }  // cannot happen (boxes tile the line); empty run is still safe
+        st->zlo[s] = (unsigned char)lo;
+        st->zhi[s] = (unsigned char)hi;
+    }
+    const unsigned long long qkey = qkey_s;
+    const long long a = block_lower_bound(skey, N, qkey);
+    if (threadIdx.x == 0) {
+        const int len = (int)min((long long)window, N);
+        st->qkey = qkey;
+        st->window_start = (int)max(0LL, min(a - len / 2, N - len));
+        st->window_len = len;
+    }
+}
+
+// ------------------------------------------------------------------------------ seed
+// Real distances of the approximate-search window (Alg. 5 approxSearch): CTA
+// (j, b) takes rows [j*per, (j+1)*per) of query b's window, one warp per group of four rows
+// (four rows in flight), and lowers BSF0 with atomicMin (fp32 bits).
+constexpr int kSeedRowsPerCta = 64;
+__global__ void __launch_bounds__(256) k_seed_batch(const float* __restrict__ queries, int n,
+                                                    const float* __restrict__ rows, const unsigned* __restrict__ perm,
+                                                    QState* st_all)
+{
+    extern __shared__ __align__(16) float q_s[];
+    const int b = blockIdx.y;
+    QState* st = st_all + b;
+    const float* q = queries + (size_t)b * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q[i];
+    __syncthreads();
+    const int start = st->window_start, len = st->window_len;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int k0 = blockIdx.x * kSeedRowsPerCta;
+    float best = INFINITY;
+    for (int g = k0 + 4 * w; g < min(len, k0 + kSeedRowsPerCta); g += 4 * (blockDim.x >> 5)) {
+        unsigned id[4];
+        bool ok[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            ok[u] = g + u < min(len, k0 + kSeedRowsPerCta);
+            id[u] = ok[u] ? perm[start + g + u] : 0u;
+        }
+        float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (int j = lane * 4; j < n; j += 128) {
+            const float4 qv = *reinterpret_cast<const float4*>(q_s + j);
+            float4 cv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                cv[u] = ok[u] ? __ldg(reinterpret_cast<const float4*>(rows + (long long)id[u] * n + j))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                float d;
+                d = qv.x - cv[u].x; acc[u] = fmaf(d, d, acc[u]);
+                d = qv.y - cv[u].y; acc[u] = fmaf(d, d, acc[u]);
+                d = qv.z - cv[u].z; acc[u] = fmaf(d, d, acc[u]);
+                d = qv.w - cv[u].w; acc[u] = fmaf(d, d, acc[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float d = warp_sum(acc[u]);
+            if (ok[u]) best = fminf(best, d);
+        }
+    }
+    if (lane == 0 && best < INFINITY) {
+        bsf_update(st, best);
+        atomicMin(&st->seed_bits, __float_as_uint(best));
+    }
+}
+
+// --------------------------------------------------------------------------- filter
+// Box bound of tile t for query b (Alg. 7 line "FindDist(node) > BSF -> prune"):
+// per segment the tile's symbols lie in [vmin, vmax]; the smallest table entry over that
+// range is 0 if it meets the zero run [zlo, zhi], else T[vmax] (range below the run) or
+// T[vmin] (above it) -- so sum_s of it (round-down adds) lower-bounds every member's bound.
+// Each thread takes one tile and kFilterQ queries; the 16 box bytes are rotated by
+// (lane & 15) so that at step s lane l reads segment (s + l) mod 16 from table copy l >> 4:
+// 32 distinct banks.  Kept tiles are appended as (tile, bound) to the query's list.
+__device__ __forceinline__ uint4 rotate_bytes(uint4 x, int r)
+{
+    const int wq = r >> 2, rb = (r & 3) * 8;
+    unsigned w[4] = {x.x, x.y, x.z, x.w}, o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const unsigned a0 = w[i], a1 = w[(i + 1) & 3], a2 = w[(i + 2) & 3], a3 = w[(i + 3) & 3];
+        o[i] = wq == 0 ? a0 : wq == 1 ? a1 : wq == 2 ? a2 : a3;
+    }
+    uint4 y;
+    y.x = __funnelshift_r(o[0], o[1], rb);
+    y.y = __funnelshift_r(o[1], o[2], rb);
+    y.z = __funnelshift_r(o[2], o[3], rb);
+    y.w = __funnelshift_r(o[3], o[0], rb);
+    return y;
+}
+
+__global__ void __launch_bounds__(256) k_filter_batch(const unsigned char* __restrict__ boxes, long long ntiles,
+                                                      const float* __restrict__ lutf_all, QState* st_all, int B,
+                                                      uint2* __restrict__ tlist_all)
+{
+    extern __shared__ __align__(16) float lutf_s[];  // kFilterQ * kLutF
+    __shared__ unsigned char zlo[kFilterQ][16], zhi[kFilterQ][16];
+    __shared__ float thr_s[kFilterQ];
+    const int b0 = blockIdx.y * kFilterQ;
+    const int nq = min(kFilterQ, B - b0);
+    for (int i = threadIdx.x; i < nq * kLutF / 4; i += blockDim.x)
+        reinterpret_cast<float4*>(lutf_s)[i] = reinterpret_cast<const float4*>(lutf_all + (size_t)b0 * kLutF)[i];
+    if (threadIdx.x < nq * 16) {
+        const int qq = threadIdx.x >> 4, s = threadIdx.x & 15;
+        zlo[qq][s] = st_all[b0 + qq].zlo[s];
+        zhi[qq][s] = st_all[b0 + qq].zhi[s];
+    }
+    if (threadIdx.x < nq) thr_s[threadIdx.x] = slack_up(ld_bsf(st_all + b0 + threadIdx.x));
+    __syncthreads();
+    const int lane = threadIdx.x & 31, r = lane & 15, h = lane >> 4;
+    for (long long t0 = (long long)blockIdx.x * blockDim.x; t0 < ntiles; t0 += (long long)gridDim.x * blockDim.x) {
+        const long long t = t0 + threadIdx.x;
+        const bool valid = t < ntiles;
+        uint4 mn = make_uint4(0, 0, 0, 0), mx = make_uint4(0, 0, 0, 0);
+        if (valid) {
+            mn = rotate_bytes(*reinterpret_cast<const uint4*>(boxes + t * 32), r);
+            mx = rotate_bytes(*reinterpret_cast<const uint4*>(boxes + t * 32 + 16), r);
+        }
+        const unsigned a[4] = {mn.x, mn.y, mn.z, mn.w}, c[4] = {mx.x, mx.y, mx.z, mx.w};
+        for (int qq = 0; qq < nq; ++qq) {
+            const float* T = lutf_s + qq * kLutF + 16 * h;
+            float acc = 0.0f;
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const int sg = (s + r) & 15;
+                const unsigned vmin = (a[s >> 2] >> (8 * (s & 3))) & 255u, vmax = (c[s >> 2] >> (8 * (s & 3))) & 255u;
+                const unsigned zl = zlo[qq][sg], zh = zhi[qq][sg];
+                const unsigned v = vmax < zl ? vmax : vmin;
+                const float term = T[v * 32 + sg];
+                acc = __fadd_rd(acc, (vmin <= zh && vmax >= zl) ? 0.0f : term);
+            }
+            const bool keep = valid && acc <= thr_s[qq];
+            const unsigned msk = __ballot_sync(0xffffffffu, keep);
+            if (msk) {
+                QState* st = st_all + b0 + qq;
+                unsigned base = 0;
+                if (lane == 0) base = atomicAdd(&st->tile_count, (unsigned)__popc(msk));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (keep)
+                    tlist_all[(size_t)(b0 + qq) * ntiles + base + __popc(msk & ((1u << lane) - 1))] =
+                        make_uint2((unsigned)t, __float_as_uint(acc));
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------- fused scan + refine
+// fp64 canonical squared ED of one row (the oracle's operation sequence: sequential in i,
+// round-to-nearest, no FMA), by one thread.
+__device__ __forceinline__ double ed2_exact_g(const float* __restrict__ q_s, const float* __restrict__ c, int n)
+{
+    double sum = 0.0;
+    for (int i = 0; i < n; i += 4) {
+        const float4 cv = __ldg(reinterpret_cast<const float4*>(c + i));
+        const float4 qv = *reinterpret_cast<const float4*>(q_s + i);
+        double d;
+        d = __dsub_rn((double)qv.x, (double)cv.x); sum = __dadd_rn(sum, __dmul_rn(d, d));
+        d = __dsub_rn((double)qv.y, (double)cv.y); sum = __dadd_rn(sum, __dmul_rn(d, d));
+        d = __dsub_rn((double)qv.z, (double)cv.z); sum = __dadd_rn(sum, __dmul_rn(d, d));
+        d = __dsub_rn((double)qv.w, (double)cv.w); sum = __dadd_rn(sum, __dmul_rn(d, d));
+    }
+    return sum;
+}
+
+// Lexicographic (d, id) min under the query's lock (near-ties only: a handful per query).
+__device__ __forceinline__ void best_update(QState* st, double d, long long id)
+{
+    while (atomicCAS(&st->lock, 0u, 1u) != 0u) __nanosleep(64);
+    __threadfence();
+    const double bd = *(volatile double*)&st->best_d;
+    const long long bi = *(volatile long long*)&st->best_id;
+    if (d < bd || (d == bd && (bi < 0 || id < bi))) {
+        *(volatile double*)&st->best_d = d;
+        *(volatile long long*)&st->best_id = id;
+    }
+    __threadfence();
+    atomicExch(&st->lock, 0u);
+}
+
+// The candidates of `keep` (one per lane, sorted position my_pos): fp32 squared ED over the
+// raw rows, four rows in flight per warp (Alg. 9 RealDist); a distance <= BSF*(1+eps)
+// lowers the BSF (atomicMin, Alg. 8's BSF update P:1178-1186) and is re-ranked exactly in
+// fp64 at once (reading R11/R12): the lexicographic min over the re-ranked rows is the answer.
+__device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __restrict__ perm,
+                           const float* __restrict__ rows, int n, const float* __restrict__ q_s, QState* st, int lane)
+{
+    while (keep) {
+        unsigned id[kRefineGroup];
+        bool ok[kRefineGroup];
+#pragma unroll
+        for (int g = 0; g < kRefineGroup; ++g) {
+            ok[g] = keep != 0;
+            const int src = ok[g] ? __ffs(keep) - 1 : 0;
+            keep &= keep - 1;
+            const unsigned pos = __shfl_sync(0xffffffffu, my_pos, src);
+            id[g] = ok[g] ? perm[pos] : 0u;
+        }
+        float acc[kRefineGroup];
+#pragma unroll
+        for (int g = 0; g < kRefineGroup; ++g) acc[g] = 0.0f;
+        for (int j = lane * 4; j < n; j += 128) {
+            const float4 qv = *reinterpret_cast<const float4*>(q_s + j);
+            float4 cv[kRefineGroup];
+#pragma unroll
+            for (int g = 0; g < kRefineGroup; ++g)
+                cv[g] = ok[g] ? __ldg(reinterpret_cast<const float4*>(rows + (long long)id[g] * n + j))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int g = 0; g < kRefineGroup; ++g) {
+                float d;
+                d = qv.x - cv[g].x; acc[g] = fmaf(d, d, acc[g]);
+                d = qv.y - cv[g].y; acc[g] = fmaf(d, d, acc[g]);
+                d = qv.z - cv[g].z; acc[g] = fmaf(d, d, acc[g]);
+                d = qv.w - cv[g].w; acc[g] = fmaf(d, d, acc[g]);
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < kRefineGroup; ++g) acc[g] = warp_sum(acc[g]);
+        if (lane == 0) {
+#pragma unroll
+            for (int g = 0; g < kRefineGroup; ++g) {
+                if (!ok[g]) continue;
+                const float thr = slack_up(ld_bsf(st));
+                if (acc[g] <= thr) {
+                    bsf_update(st, acc[g]);
+                    const double d64 = ed2_exact_g(q_s, rows + (long long)id[g] * n, n);
+                    best_update(st, d64, (long long)id[g]);
+                    atomicAdd(&st->near_count, 1u);
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+struct FusedTotals { unsigned tiles, cand, refined, exact; };
+
+// Dynamic shared memory of k_scan_refine_ed: expanded table, query, per-warp survivor lists,
+// chunk prefix over the batch.
+__host__ __device__ inline size_t fused_smem(int n)
+{
+    return (size_t)kLutX * 4 + (size_t)((n + 3) & ~3) * 4 + (size_t)kFusedWarps * MESSI_TILE_ROWS * 2 +
+           (size_t)(kBatchMax + 1) * 4;
+}
+
+__global__ void __launch_bounds__(32 * kFusedWarps, 3) k_scan_refine_ed(
+    const uint4* __restrict__ tiles, long long ntiles, long long N, int n, const float* __restrict__ queries,
+    const float* __restrict__ lutx_all, const uint2* __restrict__ tlist_all, QState* st_all, int B,
+    const unsigned char* __restrict__ rows8, const float2* __restrict__ meta8, float one_minus_delta,
+    const unsigned* __restrict__ perm, const float* __restrict__ rows, long long row_begin, unsigned* work,
+    void* results, void* stats)
+{
+    extern __shared__ __align__(16) float smem[];
+    float* lut_s = smem;
+    const int npad = (n + 3) & ~3;
+    float* q_s = lut_s + kLutX;
+    unsigned short* surv_all = reinterpret_cast<unsigned short*>(q_s + npad);
+    int* cpre = reinterpret_cast<int*>(surv_all + kFusedWarps * MESSI_TILE_ROWS);
+    __shared__ unsigned s_chunk;
+    __shared__ unsigned s_tot[4];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned short* surv = surv_all + warp * MESSI_TILE_ROWS;
+    // chunk prefix: query b owns chunks [cpre[b], cpre[b+1]), at least one (its finaliser)
+    if (warp == 0) {
+        int run = 0;
+        for (int b0 = 0; b0 < B; b0 += 32) {
+            const int b = b0 + lane;
+            int c = 0;
+            if (b < B) {
+                const unsigned cnt = *(volatile unsigned*)&st_all[b].tile_count;
+                c = max(1, (int)((cnt + kChunkTiles - 1) / kChunkTiles));
+            }
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (b < B) cpre[b] = run + incl - c;
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) cpre[B] = run;
+    }
+    if (threadIdx.x < 4) s_tot[threadIdx.x] = 0;  // thread 0 re-zeroes them after each chunk
+    __syncthreads();
+    const int total = cpre[B];
+    int cur = -1;
+    const int p = lane >> 1, h = lane & 1;
+    const char* lbase = reinterpret_cast<const char*>(lut_s);
+    for (;;) {
+        if (threadIdx.x == 0) s_chunk = atomicAdd(work, 1u);
+        __syncthreads();
+        const int c = (int)s_chunk;
+        if (c >= total) break;
+        int lo = 0, hi = B;  // largest b with cpre[b] <= c
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (cpre[mid] <= c) lo = mid; else hi = mid;
+        }
+        const int b = lo;
+        if (b != cur) {
+            const float4* src = reinterpret_cast<const float4*>(lutx_all + (size_t)b * kLutX);
+            for (int i = threadIdx.x; i < kLutX / 4; i += blockDim.x) reinterpret_cast<float4*>(lut_s)[i] = src[i];
+            for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = queries[(size_t)b * n + i];
+            __syncthreads();
+            cur = b;
+        }
+        QState* st = st_all + b;
+        const uint2* tl = tlist_all + (size_t)b * ntiles;
+        const unsigned count = *(volatile unsigned*)&st->tile_count;
+        const unsigned t_first = (unsigned)(c - cpre[b]) * kChunkTiles;
+        FusedTotals tot{0, 0, 0, 0};
+        for (unsigned k = t_first + warp; k < min(count, t_first + kChunkTiles); k += kFusedWarps) {
+            const uint2 te = tl[k];
+            // warp-uniform decision: lane 0's reading of the BSF
+            float thr = __shfl_sync(0xffffffffu, slack_up(ld_bsf(st)), 0);
+            if (__uint_as_float(te.y) > thr) continue;  // box pruned by the current BSF
+            ++tot.tiles;
+            const long long tile = te.x;
+            const uint4* tp = tiles + tile * (MESSI_TILE_BYTES / 16) + lane;
+            uint4 data[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) data[t] = __ldcs(tp + t * 32);
+            float acc[16];
+#pragma unroll
+            for (int k2 = 0; k2 < 16; ++k2) acc[k2] = 0.0f;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                const unsigned base = (unsigned)((16 * h + ((t + p) & 15)) * 4);
+                const unsigned wv[4] = {data[t].x, data[t].y, data[t].z, data[t].w};
+#pragma unroll
+                for (int wi = 0; wi < 4; ++wi) {
+#pragma unroll
+                    for (int bb = 0; bb < 4; ++bb) {
+                        const unsigned addr = __byte_perm(wv[wi], base, 0x5504 | (bb << 4));
+                        acc[wi * 4 + bb] = __fadd_rd(acc[wi * 4 + bb], *reinterpret_cast<const float*>(lbase + addr));
+                    }
+                }
+            }
+            thr = slack_up(ld_bsf(st));
+            const long long id0 = tile * MESSI_TILE_ROWS + lane * 16;
+            unsigned mask = 0;
+#pragma unroll
+            for (int k2 = 0; k2 < 16; ++k2)
+                if (acc[k2] <= thr && id0 + k2 < N) mask |= 1u << k2;
+            const int cnt = __popc(mask);
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int m = __shfl_sync(0xffffffffu, incl, 31);
+            if (m == 0) continue;
+            int off = incl - cnt;
+            while (mask) {
+                const int k2 = __ffs(mask) - 1;
+                mask &= mask - 1;
+                surv[off++] = (unsigned short)(lane * 16 + k2);
+            }
+            __syncwarp();
+            tot.cand += m;
+            for (int i0 = 0; i0 < m; i0 += 32) {
+                const bool v = i0 + lane < m;
+                const unsigned pos = v ? (unsigned)(tile * MESSI_TILE_ROWS + surv[i0 + lane]) : 0u;
+                const unsigned pass = __ballot_sync(0xffffffffu, v);
+                tot.refined += __popc(pass);
+                const unsigned keep = q8_bound_pass(pass, pos, rows8, meta8, n, q_s, one_minus_delta, st, lane);
+                tot.exact += __popc(keep);
+                exact_pass(keep, pos, perm, rows, n, q_s, st, lane);
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            atomicAdd(&s_tot[0], tot.tiles);
+            atomicAdd(&s_tot[1], tot.cand);
+            atomicAdd(&s_tot[2], tot.refined);
+            atomicAdd(&s_tot[3], tot.exact);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (s_tot[0]) atomicAdd(&st->tiles_scanned, s_tot[0]);
+            if (s_tot[1]) atomicAdd(&st->cand_count, s_tot[1]);
+            if (s_tot[2]) atomicAdd(&st->refined, s_tot[2]);
+            if (s_tot[3]) atomicAdd(&st->exact, s_tot[3]);
+            s_tot[0] = s_tot[1] = s_tot[2] = s_tot[3] = 0;
+            __threadfence();
+            const unsigned done = atomicAdd(&st->chunks_done, 1u) + 1u;
+            if ((int)done == cpre[b + 1] - cpre[b]) {
+                // the query's last chunk: every other chunk's updates are visible (fence before
+                // their increment); write the result and stats (finish_query's layout)
+                __threadfence();
+                struct R { double dist; long long id; double d2; long long reserved; };
+                struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells, exact; double seed, bsf; };
+                const double bd = *(volatile double*)&st->best_d;
+                const long long bi = *(volatile long long*)&st->best_id;
+                R* res = reinterpret_cast<R*>(results) + b;
+                res->dist = bi >= 0 ? sqrt(bd) : (double)INFINITY;
+                res->id = bi >= 0 ? row_begin + bi : -1;
+                res->d2 = bd;
+                res->reserved = 0;
+                if (stats) {
+                    S* s = reinterpret_cast<S*>(stats) + b;
+                    const unsigned ts = *(volatile unsigned*)&st->tiles_scanned;
+                    s->lb = (long long)ts * MESSI_TILE_ROWS < N ? (long long)ts * MESSI_TILE_ROWS : N;
+                    s->tiles = ts;
+                    s->cand = *(volatile unsigned*)&st->cand_count;
+                    s->lbk = 0;
+                    s->refined = *(volatile unsigned*)&st->refined;
+                    s->abandoned = s->refined - (long long)*(volatile unsigned*)&st->exact;
+                    s->near = *(volatile unsigned*)&st->near_count;
+                    s->cells = 0;
+                    s->exact = *(volatile unsigned*)&st->exact;
+                    s->seed = (double)__uint_as_float(*(volatile unsigned*)&st->seed_bits);
+                    s->bsf = (double)__uint_as_float(*(volatile unsigned*)&st->bsf_bits);
+                }
+            }
+        }
+    }
+}
+
+}  // namespace messi

@@ -12,57 +12,8 @@ __device__ __forceinline__ void append_near(QState* st, NearEntry* near, unsigne
     near[pos] = NearEntry{id, d};
 }
 
-// ED refine (Alg. 9; Alg. 8 BSF update P:1178-1186), one warp: the lanes set
-// in `pass` hold a candidate id each; their rows' fp32 squared ED are computed four at a
-// time (4 KB per warp in flight).  A result <= BSF*(1+eps) lowers the BSF (atomicMin: the
-// lock-free form of the paper's BSF lock) and joins the near-best list.
+// Rows in flight per warp in the fp32 distance loops (four 1 KB rows at n = 256).
 constexpr int kRefineGroup = 4;
-
-__device__ void refine_ed_pass(unsigned pass, unsigned my_id, const float* __restrict__ rows, int n,
-                               const float* __restrict__ q_s, QState* st, NearEntry* near, int lane)
-{
-    while (pass) {
-        unsigned id[kRefineGroup];
-        bool ok[kRefineGroup];
-#pragma unroll
-        for (int g = 0; g < kRefineGroup; ++g) {
-            ok[g] = pass != 0;
-            const int src = ok[g] ? __ffs(pass) - 1 : 0;
-            pass &= pass - 1;
-            id[g] = __shfl_sync(0xffffffffu, my_id, src);
-        }
-        float acc[kRefineGroup];
-#pragma unroll
-        for (int g = 0; g < kRefineGroup; ++g) acc[g] = 0.0f;
-#pragma unroll 2
-        for (int j = lane * 4; j < n; j += 128) {
-            const float4 qv = *reinterpret_cast<const float4*>(q_s + j);
-            float4 cv[kRefineGroup];
-#pragma unroll
-            for (int g = 0; g < kRefineGroup; ++g)
-                cv[g] = ok[g] ? __ldg(reinterpret_cast<const float4*>(rows + (long long)id[g] * n + j))
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int g = 0; g < kRefineGroup; ++g) {
-                float d;
-                d = qv.x - cv[g].x; acc[g] = fmaf(d, d, acc[g]);
-                d = qv.y - cv[g].y; acc[g] = fmaf(d, d, acc[g]);
-                d = qv.z - cv[g].z; acc[g] = fmaf(d, d, acc[g]);
-                d = qv.w - cv[g].w; acc[g] = fmaf(d, d, acc[g]);
-            }
-        }
-#pragma unroll
-        for (int g = 0; g < kRefineGroup; ++g) acc[g] = warp_sum(acc[g]);
-        const float thr = slack_up(ld_bsf(st));
-#pragma unroll
-        for (int g = 0; g < kRefineGroup; ++g) {
-            if (ok[g] && lane == 0 && acc[g] <= thr) {
-                bsf_update(st, acc[g]);
-                append_near(st, near, id[g], acc[g]);
-            }
-        }
-    }
-}
 
 // Quantised-row bound (DESIGN.md §5/§7): for the candidates of `pass` (lane bit = candidate
 // held by that lane at sorted position my_pos), the fp32 squared distance dh2 between the
@@ -146,66 +97,6 @@ __device__ __forceinline__ unsigned q8_bound_pass(unsigned pass, unsigned my_pos
 }
 
 struct Best { double d; long long id; };
-__device__ void resolve_ed_block(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
-                                 const NearEntry* __restrict__ near, QState* st, long long N, long long row_begin,
-                                 void* result, void* stats, double* sq, int wuse);
-
-// Dynamic shared memory of k_refine_ed: q, and room for up to 8 warps of the resolve.
-__host__ __device__ inline size_t refine_ed_smem(int n)
-{
-    const size_t a = (size_t)((n + 3) & ~3) * sizeof(float);
-    const size_t per = (size_t)n * sizeof(double);
-    size_t w = (96 * 1024) / per;
-    w = w < 1 ? 1 : (w > 8 ? 8 : w);
-    return a > per * w ? a : per * w;
-}
-
-// The ED refine stage of one query (runs on the refine stream, overlapping the next
-// query's scan).  Input: the scan's candidates (sorted position, 8-bit LB).  Each warp takes 32 at
-// a time, keeps those whose LB does not exceed the CURRENT BSF, and computes their real
-// distances (refine_ed_pass).  The last CTA to finish re-ranks the near-best set exactly
-// and writes the query's result (A9).  Shared memory: q (n floats), reused by the resolve.
-__global__ void __launch_bounds__(256) k_refine_ed(const uint2* __restrict__ cand, const unsigned* __restrict__ perm,
-                                                   const float* __restrict__ rows, int n, const float* __restrict__ q_g,
-                                                   const unsigned char* __restrict__ rows8,
-                                                   const float2* __restrict__ meta8, float one_minus_delta,
-                                                   QState* st, NearEntry* near, long long N, long long row_begin,
-                                                   void* result, void* stats)
-{
-    extern __shared__ __align__(16) float q_s[];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
-    __syncthreads();
-    const unsigned total = *(volatile unsigned*)&st->cand_count;
-    const int lane = threadIdx.x & 31;
-    const unsigned wpb = blockDim.x >> 5;
-    unsigned n_ref = 0, n_exact = 0;
-    for (unsigned k0 = (blockIdx.x * wpb + (threadIdx.x >> 5)) * 32; k0 < total; k0 += gridDim.x * wpb * 32) {
-        const bool valid = k0 + lane < total;
-        const uint2 e = valid ? cand[k0 + lane] : make_uint2(0u, 0x7f800000u);
-        const float thr = slack_up(ld_bsf(st));
-        const bool ok = valid && __uint_as_float(e.y) <= thr;
-        const unsigned pass = __ballot_sync(0xffffffffu, ok);
-        n_ref += __popc(pass);
-        const unsigned keep = q8_bound_pass(pass, e.x, rows8, meta8, n, q_s, one_minus_delta, st, lane);
-        n_exact += __popc(keep);
-        refine_ed_pass(keep, (keep >> lane) & 1u ? perm[e.x] : 0u, rows, n, q_s, st, near, lane);
-    }
-    if (lane == 0 && n_ref) atomicAdd(&st->refined, n_ref);
-    if (lane == 0 && n_exact) atomicAdd(&st->exact, n_exact);
-    __shared__ bool last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        last = atomicAdd(&st->done, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    extern __shared__ __align__(16) double dsq[];
-    int wuse = (int)(refine_ed_smem(n) / ((size_t)n * sizeof(double)));
-    wuse = wuse < 1 ? 1 : (wuse > (int)wpb ? (int)wpb : wuse);
-    resolve_ed_block(rows, n, q_g, near, st, N, row_begin, result, stats, dsq, wuse);
-}
 
 // DTW step 1 (Alg. 10 line LB_Keogh): the scan's candidates (sorted position,
 // envelope-PAA bound) whose bound still does not exceed the BSF get the raw LB_Keogh
@@ -473,53 +364,8 @@ __device__ Best block_best(Best b, int* cnt_io)
     return b;
 }
 
-// ED: every near-best entry with d32 <= BSF_final*(1+eps) is recomputed canonically in
-// fp64; the lexicographic min over (d64, id) is the answer (reading R11/R12; Thm. 2
-// P:1881-1913 exactness).  One CTA, one warp per entry: the warp stages the fp64 squared
-// differences in shared memory (elementwise, order-free), lane 0 sums them in index order
-// -- the oracle's sequential operation sequence.  `sq` holds n doubles per used warp.
-__device__ void resolve_ed_block(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
-                                 const NearEntry* __restrict__ near, QState* st, long long N, long long row_begin,
-                                 void* result, void* stats, double* sq, int wuse)
-{
-    const float thr = slack_up(ld_bsf(st));
-    const unsigned total = *(volatile unsigned*)&st->near_count;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    Best b{(double)INFINITY, -1};
-    int cnt = 0;
-    if (w < wuse) {
-        double* mine = sq + (size_t)w * n;
-        for (unsigned k = w; k < total; k += wuse) {
-            const NearEntry e = near[k];
-            if (!(e.d32 <= thr)) continue;
-            const float* c = rows + (long long)e.id * n;
-            for (int i = lane; i < n; i += 32) {
-                double d = __dsub_rn((double)q_g[i], (double)c[i]);
-                mine[i] = __dmul_rn(d, d);
-            }
-            __syncwarp();
-            if (lane == 0) {
-                ++cnt;
-                double sum = 0.0;
-                for (int i = 0; i < n; ++i) sum = __dadd_rn(sum, mine[i]);
-                if (better(sum, e.id, b.d, b.id)) { b.d = sum; b.id = e.id; }
-            }
-            __syncwarp();
-        }
-    }
-    b = block_best(b, &cnt);
-    if (threadIdx.x == 0) finish_query(b, (unsigned)cnt, st, N, row_begin, result, stats);
-}
-
-__global__ void k_resolve_ed(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
-                             const NearEntry* __restrict__ near, QState* st, long long N, long long row_begin,
-                             void* result, void* stats)
-{
-    extern __shared__ __align__(16) double sq[];
-    resolve_ed_block(rows, n, q_g, near, st, N, row_begin, result, stats, sq, blockDim.x >> 5);
-}
-
-// DTW: same, with the fp64 warp wavefront (bit-identical to the row-by-row DP of the
+// DTW exact resolution (A9): every near-best entry with d32 <= BSF_final*(1+eps) is
+// recomputed in fp64 with the warp wavefront (bit-identical to the row-by-row DP of the
 // oracle: every cell is fl(fl(d*d) + min) whatever the order).  Per-warp shared memory:
 // q and the row (2n floats) + 3n doubles.
 __global__ void k_resolve_dtw(const float* __restrict__ rows, int n, int reach, const float* __restrict__ q_g,

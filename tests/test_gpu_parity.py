@@ -234,6 +234,32 @@ def test_nn_ed_host_query_and_batch(c1):
         check_nn(idx.query_ed(Qh[qi]), d2[qi], ids[qi])
 
 
+def test_nn_ed_batch_spans_launch_groups(c1):
+    """More queries than one launch group of the batched ED path (kBatchMax = 128): 130
+    queries (seed 1, rows 0..129 of the query stream) over the first 30,000 rows of C1, the
+    last group holding 2; mixed with DTW calls on the same index before and after."""
+    X, Q, idx, Xh, Qh = c1
+    sub = 30_000
+    X2 = X[:sub].contiguous()
+    Q2 = gen_rows(130, 256, seed=datagen.QUERY_SEED)
+    idx2 = messi().Index(X2)
+    try:
+        d2, ids = oracle.nn("ed", Xh[:sub], Q2.cpu().numpy())
+        dref, iref = oracle.nn("dtw", Xh[:sub], Qh[:1], r=5)
+        check_nn(idx2.query_dtw(Q[0], 5), dref[0], iref[0])
+        m = messi()
+        res, stats = m.result_buffer(130, DEV), m.stats_buffer(130, DEV)
+        idx2.query_batch(Q2, None, res, stats)
+        check_nn(idx2.query_dtw(Q[0], 5), dref[0], iref[0])
+        torch.cuda.synchronize()
+        _, id_b, d2_b = m.decode_results(res)
+        assert np.array_equal(id_b.numpy(), ids) and np.array_equal(d2_b.numpy(), d2)
+        for st in m.decode_stats(stats):
+            assert st["near_best"] >= 1 and st["exact"] >= 1 and st["seed_d2"] >= st["bsf_d2"]
+    finally:
+        idx2.close()
+
+
 @pytest.mark.parametrize("reach", [25, 7])
 def test_nn_dtw(c1, reach):
     X, Q, idx, Xh, Qh = c1
