@@ -311,32 +311,35 @@ def ours(args):
     scan_ms = max_over_ranks(scan_ms, world)
     K, nq = args.steps, main["nq"]
     value = K * nq / (ms / 1e3)
-    # roofline of the dominant kernel: the coarse LB scan, algorithmic bytes = 8 B of coarse
-    # summary (16 top nibbles) per local series + 8 B per compacted coarse survivor
-    # (DESIGN.md "Roofline"); achieved = those bytes over the kernel's own event time
+    # roofline of the dominant kernel, k_scan_refine_ed (one launch per step for ED: the whole
+    # batch).  Algorithmic bytes per launch = sum over the batch's queries of
+    # 8 KB per tile scanned + 8 B per listed tile (the list entry) + n + 8 B per refined
+    # candidate (quantised row + scale / bound) + 4n B per exact fp32 distance; achieved =
+    # those bytes over the kernel's own CUDA-event time.
     st = main["stats"]
     mean = lambda k: sum(s[k] for s in st) / len(st)  # noqa: E731
-    # the tiles that survive the box filter are streamed (8 KB each: 16 B per series) and
-    # each candidate is written as (position, LB): 8 B
-    scan_bytes = 8192 * mean("tiles_scanned") + 8 * mean("candidates")
-    achieved = scan_bytes * scan_n / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
+    tot = lambda k: sum(s[k] for s in st)  # noqa: E731
+    n_ = main["n"]
+    ntiles = (main["N_local"] + 511) // 512
+    if cfg["reach"] is None:
+        kern = "k_scan_refine_ed (fused box re-check + iSAX LB scan + quantised/fp32/fp64 refine, whole batch)"
+        launch_bytes = (8192 * tot("tiles_scanned") + 8 * tot("tiles_listed") + (n_ + 8) * tot("refined")
+                        + 4 * n_ * tot("exact"))
+    else:
+        kern = "k_scan (iSAX envelope LB scan of the box-filtered tiles, per query)"
+        launch_bytes = 8192 * mean("tiles_scanned") + 8 * mean("candidates")
+    achieved = launch_bytes * scan_n / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
     peak = pk.get("hbm_gbs", 6650.0)
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        traffic = tr.get(f"{cname}_{args.mode}_scan_bytes_per_launch")
+        traffic = tr.get(f"{cname}_{args.mode}_bytes_per_launch")
     except Exception:
         pass
-    # whole-query algorithmic bytes per GPU: coarse stream + one 32 B sector of 8-bit word per
-    # coarse survivor + the rows refined + the approximate-search window rows
-    ntiles = (main["N_local"] + 511) // 512
-    # whole-query algorithmic bytes per GPU: tile boxes + surviving tiles + candidate list
-    # (written, read) + the rows refined + the approximate-search window rows
-    # (ED: n quantised bytes + 8 B of scale / error bound per refined candidate, 4n B per
-    # exact fp32 distance)
-    per_query_bytes = (32 * ntiles + 8192 * mean("tiles_scanned") + 16 * mean("candidates")
-                       + (main["n"] + 8) * mean("refined") + 4 * main["n"] * mean("exact")
-                       + 4 * main["n"] * min(2000, main["N_local"]))
+    # whole-query algorithmic bytes per GPU: tile boxes (filter) + surviving tiles + list
+    # entries + refine bytes + the approximate-search window rows
+    per_query_bytes = (32 * ntiles + 8192 * mean("tiles_scanned") + 8 * mean("tiles_listed")
+                       + (n_ + 8) * mean("refined") + 4 * n_ * mean("exact") + 4 * n_ * min(2000, main["N_local"]))
     steps_total = {k: max_over_ranks(v[0], world) for k, v in main["prof"].items()}
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
@@ -349,13 +352,13 @@ def ours(args):
                    else "single shard",
                    "l2": "inputs larger than L2: %.2f GB of iSAX tiles per GPU; each query streams the tiles its box filter keeps (distinct per query)" % (16 * main["N_local"] / 1e9),
                    "query_model": "sequential queries (P:2024-2026), batch call per step"},
-        "roofline": {"bound": "hbm", "kernel": "k_scan (coarse iSAX LB scan of the box-filtered tiles)", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in pk else "fallback",
-                     "algorithmic_bytes_per_launch": scan_bytes, "launches": scan_n,
+                     "algorithmic_bytes_per_launch": launch_bytes, "launches": scan_n,
                      "share_of_step": scan_ms / main["prof_ms"] if main["prof_ms"] else None,
-                     "timing": "CUDA events around every k_scan launch on its stream, in a second pass of "
-                               "the same steps (profiling events kept out of the timed region)"},
+                     "timing": "CUDA events around every launch of the kernel on its stream, in a second "
+                               "pass of the same steps (profiling events kept out of the timed region)"},
         "query_roofline": {"bytes_per_query_per_gpu": per_query_bytes,
                            "qps_at_peak": peak * 1e9 / per_query_bytes,
                            "frac": value / (peak * 1e9 / per_query_bytes)},
@@ -367,7 +370,8 @@ def ours(args):
         "build": {"ms": main["build_ms"], "rows_per_s": main["N_local"] / (main["build_ms"] / 1e3),
                   "what": "summarise (PAA + iSAX + key) + CUB key sort, per GPU"},
         "stats_mean": {k: mean(k) for k in ("lb_computed", "tiles_scanned", "candidates", "lbk_pass", "refined",
-                                             "abandoned", "near_best", "dtw_cells", "exact", "seed_d2", "bsf_d2")},
+                                             "abandoned", "near_best", "dtw_cells", "exact", "tiles_listed", "seed_d2",
+                                             "bsf_d2")},
     }
     if args.mode == "ed" and not args.no_dtw:
         c4 = dict(CONFIGS["c4"])

@@ -71,6 +71,8 @@ typedef struct {
     int64_t dtw_cells;    /* DTW band cells evaluated in fp32 by the register-band refine */
     int64_t exact;        /* real distances over the raw fp32 rows: ED = candidates whose
                              quantised-row bound did not prune them; DTW = refined */
+    int64_t tiles_listed; /* tiles whose box bound <= BSF0 * (1 + eps) (the filter's list); ED scans
+                             those still within the CURRENT BSF when reached (tiles_scanned) */
     double seed_d2;       /* BSF0: squared distance found by the approximate search */
     double bsf_d2;        /* final fp32 best-so-far (squared) before the exact re-rank */
 } messi_stats;

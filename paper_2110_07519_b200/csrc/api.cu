@@ -80,7 +80,7 @@ struct messi_index {
 };
 
 static_assert(sizeof(messi_result) == 32, "messi_result layout");
-static_assert(sizeof(messi_stats) == 88, "messi_stats layout");
+static_assert(sizeof(messi_stats) == 96, "messi_stats layout");
 
 enum { K_SEED = 0, K_SCAN = 1, K_REFINE = 2, K_LBK = 3, K_RESOLVE = 4, K_KINDS = 5 };
 
@@ -543,8 +543,10 @@ static messi_status run_ed_batch(messi_index* idx, const float* queries_dev, int
             ProfScope ps(idx, K_SCAN, st);
             k_scan_refine_ed<<<idx->fused_grid, 32 * kFusedWarps, fused_smem(n), st>>>(
                 idx->tiles, idx->ntiles, idx->N, n, q, idx->lutx, idx->btlist, idx->bst, B, idx->rows8, idx->meta8,
-                idx->q8_omd, idx->perm, idx->rows, idx->row_begin, idx->work, results_dev + g0,
-                stats_dev ? stats_dev + g0 : nullptr);
+                idx->q8_omd, idx->perm, idx->rows);
+            LAUNCHED(idx);
+            k_finalise_batch<<<(B + 127) / 128, 128, 0, st>>>(idx->bst, B, idx->N, idx->row_begin, results_dev + g0,
+                                                              stats_dev ? stats_dev + g0 : nullptr);
             LAUNCHED(idx);
         }
     }

@@ -31,7 +31,8 @@ struct QState {
     unsigned tile_count;    // tiles whose box bound <= BSF0 * (1 + eps) (scanned)
     unsigned exact;         // ED: fp32 distances over the raw rows (quantised bound passed)
     unsigned tiles_scanned; // batch ED: tiles whose box bound still passed the CURRENT BSF
-    unsigned chunks_done;   // batch ED: work chunks of this query finished (last one finalises)
+    unsigned next_tile;     // batch ED: next pair of listed tiles to hand out
+    unsigned tiles_done;    // batch ED: listed tiles finished (the warp finishing the last finalises)
     unsigned lock;          // batch ED: guards best_d / best_id
     unsigned long long dtw_cells;  // DTW band cells evaluated in fp32 (refine)
     double best_d;          // batch ED: lexicographic min (d64, id) over the fp64 re-ranked rows
@@ -58,7 +59,8 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->tile_count = 0;
     st->exact = 0;
     st->tiles_scanned = 0;
-    st->chunks_done = 0;
+    st->next_tile = 0;
+    st->tiles_done = 0;
     st->lock = 0;
     st->best_d = (double)INFINITY;
     st->best_id = -1;

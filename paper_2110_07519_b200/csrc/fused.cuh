@@ -225,13 +225,13 @@ __global__ void __launch_bounds__(256) k_filter_batch(const unsigned char* __res
 
 // ------------------------------------------------------------- fused scan + refine
 // fp64 canonical squared ED of one row (the oracle's operation sequence: sequential in i,
-// round-to-nearest, no FMA), by one thread.
-__device__ __forceinline__ double ed2_exact_g(const float* __restrict__ q_s, const float* __restrict__ c, int n)
+// round-to-nearest, no FMA), by one thread.  q_p: the padded query (element i at i + 4 (i >> 5)).
+__device__ __forceinline__ double ed2_exact_g(const float* __restrict__ q_p, const float* __restrict__ c, int n)
 {
     double sum = 0.0;
     for (int i = 0; i < n; i += 4) {
         const float4 cv = __ldg(reinterpret_cast<const float4*>(c + i));
-        const float4 qv = *reinterpret_cast<const float4*>(q_s + i);
+        const float4 qv = *reinterpret_cast<const float4*>(q_p + i + 4 * (i >> 5));
         double d;
         d = __dsub_rn((double)qv.x, (double)cv.x); sum = __dadd_rn(sum, __dmul_rn(d, d));
         d = __dsub_rn((double)qv.y, (double)cv.y); sum = __dadd_rn(sum, __dmul_rn(d, d));
@@ -261,7 +261,7 @@ __device__ __forceinline__ void best_update(QState* st, double d, long long id)
 // lowers the BSF (atomicMin, Alg. 8's BSF update P:1178-1186) and is re-ranked exactly in
 // fp64 at once (reading R11/R12): the lexicographic min over the re-ranked rows is the answer.
 __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __restrict__ perm,
-                           const float* __restrict__ rows, int n, const float* __restrict__ q_s, QState* st, int lane)
+                           const float* __restrict__ rows, int n, const float* __restrict__ q_p, QState* st, int lane)
 {
     while (keep) {
         unsigned id[kRefineGroup];
@@ -278,7 +278,7 @@ __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __res
 #pragma unroll
         for (int g = 0; g < kRefineGroup; ++g) acc[g] = 0.0f;
         for (int j = lane * 4; j < n; j += 128) {
-            const float4 qv = *reinterpret_cast<const float4*>(q_s + j);
+            const float4 qv = *reinterpret_cast<const float4*>(q_p + j + 4 * (j >> 5));
             float4 cv[kRefineGroup];
 #pragma unroll
             for (int g = 0; g < kRefineGroup; ++g)
@@ -302,7 +302,7 @@ __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __res
                 const float thr = slack_up(ld_bsf(st));
                 if (acc[g] <= thr) {
                     bsf_update(st, acc[g]);
-                    const double d64 = ed2_exact_g(q_s, rows + (long long)id[g] * n, n);
+                    const double d64 = ed2_exact_g(q_p, rows + (long long)id[g] * n, n);
                     best_update(st, d64, (long long)id[g]);
                     atomicAdd(&st->near_count, 1u);
                 }
@@ -312,189 +312,192 @@ __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __res
     }
 }
 
-struct FusedTotals { unsigned tiles, cand, refined, exact; };
-
-// Dynamic shared memory of k_scan_refine_ed: expanded table, query, per-warp survivor lists,
-// chunk prefix over the batch.
+// Dynamic shared memory of k_scan_refine_ed: expanded table, padded query, per-warp
+// survivor lists (n = 256: 73.1 KB -> 3 CTAs per SM).
+__host__ __device__ inline size_t fused_qpad(int n) { return (size_t)(n + 4 * ((n + 31) / 32) + 4) & ~(size_t)3; }
 __host__ __device__ inline size_t fused_smem(int n)
 {
-    return (size_t)kLutX * 4 + (size_t)((n + 3) & ~3) * 4 + (size_t)kFusedWarps * MESSI_TILE_ROWS * 2 +
-           (size_t)(kBatchMax + 1) * 4;
+    return (size_t)kLutX * 4 + fused_qpad(n) * 4 + (size_t)kFusedWarps * MESSI_TILE_ROWS * 2;
 }
 
+// Writes query b's result and stats (finish_query's layout) from its state.
+__device__ void fused_finalise(const QState* st, long long N, long long row_begin, void* result, void* stats)
+{
+    struct R { double dist; long long id; double d2; long long reserved; };
+    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells, exact, listed; double seed, bsf; };
+    const double bd = st->best_d;
+    const long long bi = st->best_id;
+    R* res = reinterpret_cast<R*>(result);
+    res->dist = bi >= 0 ? sqrt(bd) : (double)INFINITY;
+    res->id = bi >= 0 ? row_begin + bi : -1;
+    res->d2 = bd;
+    res->reserved = 0;
+    if (stats) {
+        S* s = reinterpret_cast<S*>(stats);
+        const unsigned ts = st->tiles_scanned;
+        s->lb = (long long)ts * MESSI_TILE_ROWS < N ? (long long)ts * MESSI_TILE_ROWS : N;
+        s->tiles = ts;
+        s->cand = st->cand_count;
+        s->lbk = 0;
+        s->refined = st->refined;
+        s->exact = st->exact;
+        s->listed = st->tile_count;
+        s->abandoned = s->refined - s->exact;
+        s->near = st->near_count;
+        s->cells = 0;
+        s->seed = (double)__uint_as_float(st->seed_bits);
+        s->bsf = (double)__uint_as_float(st->bsf_bits);
+    }
+}
+
+// One thread per query of the batch, after k_scan_refine_ed (stream order makes every
+// update of the fused kernel visible): results and stats.
+__global__ void k_finalise_batch(const QState* __restrict__ st_all, int B, long long N, long long row_begin,
+                                 void* results, void* stats)
+{
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    fused_finalise(st_all + b, N, row_begin, reinterpret_cast<char*>(results) + (size_t)b * 32,
+                   stats ? reinterpret_cast<char*>(stats) + (size_t)b * 96 : nullptr);
+}
+
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Persistent.  CTA j starts at query j mod B and walks the batch's queries cyclically once;
+// at a query with listed tiles left it loads the query's expanded table and padded query
+// into shared memory, then its warps take pairs of tiles from the query's list with one
+// atomicAdd (claimed one pair ahead; the next tiles are bulk-prefetched into L2), re-check
+// each tile's box bound against the CURRENT BSF (Alg. 7's node pruning), scan the tile's
+// 512 series bounds (A5, k_scan's arithmetic) and refine the survivors at once (quantised
+// bound -> fp32 distance -> fp64 re-rank; Alg. 9's worker loop).  When a
+// query's list runs dry the CTA joins the next one: light queries finish early and their
+// CTAs help the heavy ones.  k_finalise_batch writes the results.
 __global__ void __launch_bounds__(32 * kFusedWarps, 3) k_scan_refine_ed(
     const uint4* __restrict__ tiles, long long ntiles, long long N, int n, const float* __restrict__ queries,
     const float* __restrict__ lutx_all, const uint2* __restrict__ tlist_all, QState* st_all, int B,
     const unsigned char* __restrict__ rows8, const float2* __restrict__ meta8, float one_minus_delta,
-    const unsigned* __restrict__ perm, const float* __restrict__ rows, long long row_begin, unsigned* work,
-    void* results, void* stats)
+    const unsigned* __restrict__ perm, const float* __restrict__ rows)
 {
     extern __shared__ __align__(16) float smem[];
     float* lut_s = smem;
-    const int npad = (n + 3) & ~3;
-    float* q_s = lut_s + kLutX;
-    unsigned short* surv_all = reinterpret_cast<unsigned short*>(q_s + npad);
-    int* cpre = reinterpret_cast<int*>(surv_all + kFusedWarps * MESSI_TILE_ROWS);
-    __shared__ unsigned s_chunk;
-    __shared__ unsigned s_tot[4];
+    float* q_p = lut_s + kLutX;
+    unsigned short* surv_all = reinterpret_cast<unsigned short*>(q_p + fused_qpad(n));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned short* surv = surv_all + warp * MESSI_TILE_ROWS;
-    // chunk prefix: query b owns chunks [cpre[b], cpre[b+1]), at least one (its finaliser)
-    if (warp == 0) {
-        int run = 0;
-        for (int b0 = 0; b0 < B; b0 += 32) {
-            const int b = b0 + lane;
-            int c = 0;
-            if (b < B) {
-                const unsigned cnt = *(volatile unsigned*)&st_all[b].tile_count;
-                c = max(1, (int)((cnt + kChunkTiles - 1) / kChunkTiles));
-            }
-            int incl = c;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            if (b < B) cpre[b] = run + incl - c;
-            run += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        if (lane == 0) cpre[B] = run;
-    }
-    if (threadIdx.x < 4) s_tot[threadIdx.x] = 0;  // thread 0 re-zeroes them after each chunk
-    __syncthreads();
-    const int total = cpre[B];
-    int cur = -1;
+    __shared__ int s_has;
     const int p = lane >> 1, h = lane & 1;
     const char* lbase = reinterpret_cast<const char*>(lut_s);
-    for (;;) {
-        if (threadIdx.x == 0) s_chunk = atomicAdd(work, 1u);
+    int b = (int)(blockIdx.x % (unsigned)B);
+    for (int visited = 0; visited < B; ++visited, b = (b + 1 == B ? 0 : b + 1)) {
+        QState* st = st_all + b;
+        const unsigned count = *(volatile unsigned*)&st->tile_count;
+        if (threadIdx.x == 0) s_has = *(volatile unsigned*)&st->next_tile * 2u < count;
         __syncthreads();
-        const int c = (int)s_chunk;
-        if (c >= total) break;
-        int lo = 0, hi = B;  // largest b with cpre[b] <= c
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (cpre[mid] <= c) lo = mid; else hi = mid;
-        }
-        const int b = lo;
-        if (b != cur) {
+        const bool has = s_has;
+        __syncthreads();  // s_has is rewritten by the next visit
+        if (!has) continue;
+        {
             const float4* src = reinterpret_cast<const float4*>(lutx_all + (size_t)b * kLutX);
             for (int i = threadIdx.x; i < kLutX / 4; i += blockDim.x) reinterpret_cast<float4*>(lut_s)[i] = src[i];
-            for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = queries[(size_t)b * n + i];
-            __syncthreads();
-            cur = b;
-        }
-        QState* st = st_all + b;
-        const uint2* tl = tlist_all + (size_t)b * ntiles;
-        const unsigned count = *(volatile unsigned*)&st->tile_count;
-        const unsigned t_first = (unsigned)(c - cpre[b]) * kChunkTiles;
-        FusedTotals tot{0, 0, 0, 0};
-        for (unsigned k = t_first + warp; k < min(count, t_first + kChunkTiles); k += kFusedWarps) {
-            const uint2 te = tl[k];
-            // warp-uniform decision: lane 0's reading of the BSF
-            float thr = __shfl_sync(0xffffffffu, slack_up(ld_bsf(st)), 0);
-            if (__uint_as_float(te.y) > thr) continue;  // box pruned by the current BSF
-            ++tot.tiles;
-            const long long tile = te.x;
-            const uint4* tp = tiles + tile * (MESSI_TILE_BYTES / 16) + lane;
-            uint4 data[16];
-#pragma unroll
-            for (int t = 0; t < 16; ++t) data[t] = __ldcs(tp + t * 32);
-            float acc[16];
-#pragma unroll
-            for (int k2 = 0; k2 < 16; ++k2) acc[k2] = 0.0f;
-#pragma unroll
-            for (int t = 0; t < 16; ++t) {
-                const unsigned base = (unsigned)((16 * h + ((t + p) & 15)) * 4);
-                const unsigned wv[4] = {data[t].x, data[t].y, data[t].z, data[t].w};
-#pragma unroll
-                for (int wi = 0; wi < 4; ++wi) {
-#pragma unroll
-                    for (int bb = 0; bb < 4; ++bb) {
-                        const unsigned addr = __byte_perm(wv[wi], base, 0x5504 | (bb << 4));
-                        acc[wi * 4 + bb] = __fadd_rd(acc[wi * 4 + bb], *reinterpret_cast<const float*>(lbase + addr));
-                    }
-                }
-            }
-            thr = slack_up(ld_bsf(st));
-            const long long id0 = tile * MESSI_TILE_ROWS + lane * 16;
-            unsigned mask = 0;
-#pragma unroll
-            for (int k2 = 0; k2 < 16; ++k2)
-                if (acc[k2] <= thr && id0 + k2 < N) mask |= 1u << k2;
-            const int cnt = __popc(mask);
-            int incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const int m = __shfl_sync(0xffffffffu, incl, 31);
-            if (m == 0) continue;
-            int off = incl - cnt;
-            while (mask) {
-                const int k2 = __ffs(mask) - 1;
-                mask &= mask - 1;
-                surv[off++] = (unsigned short)(lane * 16 + k2);
-            }
-            __syncwarp();
-            tot.cand += m;
-            for (int i0 = 0; i0 < m; i0 += 32) {
-                const bool v = i0 + lane < m;
-                const unsigned pos = v ? (unsigned)(tile * MESSI_TILE_ROWS + surv[i0 + lane]) : 0u;
-                const unsigned pass = __ballot_sync(0xffffffffu, v);
-                tot.refined += __popc(pass);
-                const unsigned keep = q8_bound_pass(pass, pos, rows8, meta8, n, q_s, one_minus_delta, st, lane);
-                tot.exact += __popc(keep);
-                exact_pass(keep, pos, perm, rows, n, q_s, st, lane);
-            }
-            __syncwarp();
-        }
-        if (lane == 0) {
-            atomicAdd(&s_tot[0], tot.tiles);
-            atomicAdd(&s_tot[1], tot.cand);
-            atomicAdd(&s_tot[2], tot.refined);
-            atomicAdd(&s_tot[3], tot.exact);
+            const float* q = queries + (size_t)b * n;
+            for (int i = threadIdx.x; i < n; i += blockDim.x) q_p[i + 4 * (i >> 5)] = q[i];
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            if (s_tot[0]) atomicAdd(&st->tiles_scanned, s_tot[0]);
-            if (s_tot[1]) atomicAdd(&st->cand_count, s_tot[1]);
-            if (s_tot[2]) atomicAdd(&st->refined, s_tot[2]);
-            if (s_tot[3]) atomicAdd(&st->exact, s_tot[3]);
-            s_tot[0] = s_tot[1] = s_tot[2] = s_tot[3] = 0;
-            __threadfence();
-            const unsigned done = atomicAdd(&st->chunks_done, 1u) + 1u;
-            if ((int)done == cpre[b + 1] - cpre[b]) {
-                // the query's last chunk: every other chunk's updates are visible (fence before
-                // their increment); write the result and stats (finish_query's layout)
-                __threadfence();
-                struct R { double dist; long long id; double d2; long long reserved; };
-                struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells, exact; double seed, bsf; };
-                const double bd = *(volatile double*)&st->best_d;
-                const long long bi = *(volatile long long*)&st->best_id;
-                R* res = reinterpret_cast<R*>(results) + b;
-                res->dist = bi >= 0 ? sqrt(bd) : (double)INFINITY;
-                res->id = bi >= 0 ? row_begin + bi : -1;
-                res->d2 = bd;
-                res->reserved = 0;
-                if (stats) {
-                    S* s = reinterpret_cast<S*>(stats) + b;
-                    const unsigned ts = *(volatile unsigned*)&st->tiles_scanned;
-                    s->lb = (long long)ts * MESSI_TILE_ROWS < N ? (long long)ts * MESSI_TILE_ROWS : N;
-                    s->tiles = ts;
-                    s->cand = *(volatile unsigned*)&st->cand_count;
-                    s->lbk = 0;
-                    s->refined = *(volatile unsigned*)&st->refined;
-                    s->abandoned = s->refined - (long long)*(volatile unsigned*)&st->exact;
-                    s->near = *(volatile unsigned*)&st->near_count;
-                    s->cells = 0;
-                    s->exact = *(volatile unsigned*)&st->exact;
-                    s->seed = (double)__uint_as_float(*(volatile unsigned*)&st->seed_bits);
-                    s->bsf = (double)__uint_as_float(*(volatile unsigned*)&st->bsf_bits);
+        const uint2* tl = tlist_all + (size_t)b * ntiles;
+        unsigned n_tiles = 0, n_cand = 0, n_ref = 0, n_exact = 0;
+        unsigned k_next = 0;
+        if (lane == 0) k_next = atomicAdd(&st->next_tile, 1u) * 2u;
+        k_next = __shfl_sync(0xffffffffu, k_next, 0);
+        while (k_next < count) {
+            const unsigned k0 = k_next;
+            const uint2 te0 = tl[k0];
+            const uint2 te1 = k0 + 1 < count ? tl[k0 + 1] : make_uint2(0u, 0u);
+            // claim the following pair now and prefetch its tiles into L2
+            if (lane == 0) {
+                k_next = atomicAdd(&st->next_tile, 1u) * 2u;
+                const float pthr = slack_up(ld_bsf(st));
+                for (unsigned kk = k_next; kk < min(k_next + 2u, count); ++kk) {
+                    const uint2 tn = tl[kk];
+                    if (__uint_as_float(tn.y) <= pthr)  // not already box-pruned
+                        prefetch_l2_bulk(tiles + (long long)tn.x * (MESSI_TILE_BYTES / 16), MESSI_TILE_BYTES);
                 }
             }
+            k_next = __shfl_sync(0xffffffffu, k_next, 0);
+#pragma unroll 1
+            for (int u = 0; u < 2; ++u) {
+                if (k0 + u >= count) break;
+                const uint2 te = u == 0 ? te0 : te1;
+                // warp-uniform decision: lane 0's reading of the BSF
+                float thr = __shfl_sync(0xffffffffu, slack_up(ld_bsf(st)), 0);
+                if (__uint_as_float(te.y) > thr) continue;  // box pruned by the current BSF
+                ++n_tiles;
+                const long long tile = te.x;
+                const uint4* tp = tiles + tile * (MESSI_TILE_BYTES / 16) + lane;
+                uint4 data[16];
+#pragma unroll
+                for (int t = 0; t < 16; ++t) data[t] = __ldcs(tp + t * 32);
+                float acc[16];
+#pragma unroll
+                for (int k2 = 0; k2 < 16; ++k2) acc[k2] = 0.0f;
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                    const unsigned base = (unsigned)((16 * h + ((t + p) & 15)) * 4);
+                    const unsigned wv[4] = {data[t].x, data[t].y, data[t].z, data[t].w};
+#pragma unroll
+                    for (int wi = 0; wi < 4; ++wi) {
+#pragma unroll
+                        for (int bb = 0; bb < 4; ++bb) {
+                            const unsigned addr = __byte_perm(wv[wi], base, 0x5504 | (bb << 4));
+                            acc[wi * 4 + bb] =
+                                __fadd_rd(acc[wi * 4 + bb], *reinterpret_cast<const float*>(lbase + addr));
+                        }
+                    }
+                }
+                thr = slack_up(ld_bsf(st));
+                const long long id0 = tile * MESSI_TILE_ROWS + lane * 16;
+                unsigned mask = 0;
+#pragma unroll
+                for (int k2 = 0; k2 < 16; ++k2)
+                    if (acc[k2] <= thr && id0 + k2 < N) mask |= 1u << k2;
+                const int cnt = __popc(mask);
+                int incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const int m = __shfl_sync(0xffffffffu, incl, 31);
+                if (m == 0) continue;
+                int off = incl - cnt;
+                while (mask) {
+                    const int k2 = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    surv[off++] = (unsigned short)(lane * 16 + k2);
+                }
+                __syncwarp();
+                n_cand += m;
+                for (int i0 = 0; i0 < m; i0 += 32) {
+                    const bool v = i0 + lane < m;
+                    const unsigned pos = v ? (unsigned)(tile * MESSI_TILE_ROWS + surv[i0 + lane]) : 0u;
+                    const unsigned pass = __ballot_sync(0xffffffffu, v);
+                    n_ref += __popc(pass);
+                    const unsigned keep = q8_bound_pass(pass, pos, rows8, meta8, n, q_p, one_minus_delta, st, lane);
+                    n_exact += __popc(keep);
+                    exact_pass(keep, pos, perm, rows, n, q_p, st, lane);
+                }
+                __syncwarp();
+            }
         }
+        if (lane == 0) {
+            if (n_tiles) atomicAdd(&st->tiles_scanned, n_tiles);
+            if (n_cand) atomicAdd(&st->cand_count, n_cand);
+            if (n_ref) atomicAdd(&st->refined, n_ref);
+            if (n_exact) atomicAdd(&st->exact, n_exact);
+        }
+        __syncthreads();  // every warp is done with b's table before it is overwritten
     }
 }
 

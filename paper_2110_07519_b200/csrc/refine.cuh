@@ -23,10 +23,11 @@ constexpr int kRefineGroup = 4;
 // candidate with L > 0 and L^2 > thr cannot be the nearest neighbour; the others are
 // returned (bit set) for the exact fp32 refine.  Groups of 8 lanes take one row each, two
 // rows per group in flight (8 rows = 8n bytes per warp); lane gl of a group reads the 16 B
-// chunks gl, gl+8, ... of its rows.  Bytes convert exactly with the 2^23 trick:
+// chunks gl, gl+8, ... of its rows; the query comes from q_p, a padded copy (element i at
+// i + 4 (i >> 5)).  Bytes convert exactly with the 2^23 trick:
 // float(0x4B000000 | b) = 2^23 + b.
 __device__ __forceinline__ unsigned q8_bound_pass(unsigned pass, unsigned my_pos, const unsigned char* __restrict__ rows8,
-                                                  const float2* __restrict__ meta8, int n, const float* __restrict__ q_s,
+                                                  const float2* __restrict__ meta8, int n, const float* __restrict__ q_p,
                                                   float one_minus_delta, QState* st, int lane)
 {
     const int g = lane >> 3, gl = lane & 7;
@@ -58,7 +59,9 @@ __device__ __forceinline__ unsigned q8_bound_pass(unsigned pass, unsigned my_pos
             const unsigned xa[4] = {wa.x, wa.y, wa.z, wa.w}, xb[4] = {wb.x, wb.y, wb.z, wb.w};
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
-                const float4 qv = *reinterpret_cast<const float4*>(q_s + c + 4 * w);
+                // q_p: element i at i + 4 (i >> 5) -- the eight lanes of a group then read
+                // 8 x 16 B from 32 distinct banks
+                const float4 qv = *reinterpret_cast<const float4*>(q_p + c + 4 * w + 4 * (c >> 5));
                 const float qq[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
@@ -316,7 +319,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
                              void* result, void* stats)
 {
     struct R { double dist; long long id; double d2; long long reserved; };
-    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells, exact; double seed, bsf; };
+    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells, exact, listed; double seed, bsf; };
     R* res = reinterpret_cast<R*>(result);
     res->dist = b.id >= 0 ? sqrt(b.d) : (double)INFINITY;
     res->id = b.id >= 0 ? row_begin + b.id : -1;
@@ -333,6 +336,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
         s->near = nb;
         s->cells = (long long)st->dtw_cells;
         s->exact = st->exact ? st->exact : st->refined;
+        s->listed = st->tile_count;
         s->seed = (double)__uint_as_float(st->seed_bits);
         s->bsf = (double)__uint_as_float(st->bsf_bits);
     }

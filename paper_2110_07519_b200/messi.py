@@ -44,7 +44,7 @@ class Stats(ctypes.Structure):
     _fields_ = [("lb_computed", ctypes.c_int64), ("tiles_scanned", ctypes.c_int64), ("candidates", ctypes.c_int64),
                 ("lbk_pass", ctypes.c_int64),
                 ("refined", ctypes.c_int64), ("abandoned", ctypes.c_int64), ("near_best", ctypes.c_int64),
-                ("dtw_cells", ctypes.c_int64), ("exact", ctypes.c_int64),
+                ("dtw_cells", ctypes.c_int64), ("exact", ctypes.c_int64), ("tiles_listed", ctypes.c_int64),
                 ("seed_d2", ctypes.c_double), ("bsf_d2", ctypes.c_double)]
 
     def as_dict(self):
@@ -147,7 +147,7 @@ def messi_query_dtw(handle, query, reach: int, with_stats: bool = False):
 
 def messi_query_ed_batch(handle, queries_dev: torch.Tensor, results_dev: torch.Tensor, stats_dev=None):
     """Asynchronous on the build stream.  results_dev: uint8 CUDA tensor of nq*32 bytes (see
-    ``result_buffer``); stats_dev: optional nq*88 bytes (``stats_buffer``)."""
+    ``result_buffer``); stats_dev: optional nq*96 bytes (``stats_buffer``)."""
     _check(lib().messi_query_ed_batch(handle, _ptr(queries_dev), queries_dev.shape[0], _ptr(results_dev),
                                       _ptr(stats_dev)))
 
@@ -266,7 +266,7 @@ def _wrap_dev(ptr: int, nbytes: int, device):
     return torch.as_tensor(_Arr(), device=device)
 
 
-RESULT_BYTES, STATS_BYTES = 32, 88
+RESULT_BYTES, STATS_BYTES = 32, 96
 
 
 def result_buffer(nq: int, device) -> torch.Tensor:
@@ -293,8 +293,8 @@ def decode_results_device(buf: torch.Tensor):
 
 def decode_stats(buf: torch.Tensor):
     raw = buf.view(-1, STATS_BYTES).cpu()
-    ints = raw[:, :72].contiguous().view(torch.int64)
-    dbl = raw[:, 72:].contiguous().view(torch.float64)
+    ints = raw[:, :80].contiguous().view(torch.int64)
+    dbl = raw[:, 80:].contiguous().view(torch.float64)
     return [dict(zip(STATS_FIELDS, list(map(int, i.tolist())) + list(map(float, d.tolist()))))
             for i, d in zip(ints, dbl)]
 
