@@ -323,11 +323,11 @@ def ours(args):
     ntiles = (main["N_local"] + 511) // 512
     if cfg["reach"] is None:
         kern = "k_scan_refine_ed (fused box re-check + iSAX LB scan + quantised/fp32/fp64 refine, whole batch)"
-        launch_bytes = (8192 * tot("tiles_scanned") + 8 * tot("tiles_listed") + (n_ + 8) * tot("refined")
-                        + 4 * n_ * tot("exact"))
+        launch_bytes = (4096 * tot("tiles_scanned") + 8 * tot("tiles_listed") + 16 * tot("coarse")
+                        + (n_ + 8) * tot("refined") + 4 * n_ * tot("exact"))
     else:
         kern = "k_scan (iSAX envelope LB scan of the box-filtered tiles, per query)"
-        launch_bytes = 8192 * mean("tiles_scanned") + 8 * mean("candidates")
+        launch_bytes = 4096 * mean("tiles_scanned") + 16 * mean("coarse") + 8 * mean("candidates")
     achieved = launch_bytes * scan_n / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
     peak = pk.get("hbm_gbs", 6650.0)
     traffic = None
@@ -338,7 +338,7 @@ def ours(args):
         pass
     # whole-query algorithmic bytes per GPU: tile boxes (filter) + surviving tiles + list
     # entries + refine bytes + the approximate-search window rows
-    per_query_bytes = (32 * ntiles + 8192 * mean("tiles_scanned") + 8 * mean("tiles_listed")
+    per_query_bytes = (32 * ntiles + 4096 * mean("tiles_scanned") + 8 * mean("tiles_listed") + 16 * mean("coarse")
                        + (n_ + 8) * mean("refined") + 4 * n_ * mean("exact") + 4 * n_ * min(2000, main["N_local"]))
     steps_total = {k: max_over_ranks(v[0], world) for k, v in main["prof"].items()}
     line = {
@@ -350,7 +350,7 @@ def ours(args):
                    "queries_per_step": nq, "reach": cfg["reach"], "parallelism": f"row-shard x{world}",
                    "merge": "per step: one all_gather of (d2, gid) x queries per rank, lexicographic min" if world > 1
                    else "single shard",
-                   "l2": "inputs larger than L2: %.2f GB of iSAX tiles per GPU; each query streams the tiles its box filter keeps (distinct per query)" % (16 * main["N_local"] / 1e9),
+                   "l2": "inputs larger than L2: %.2f GB of coarse iSAX tiles + %.2f GB of 8-bit words + %.2f GB of quantised rows per GPU; each query streams the tiles its box filter keeps (distinct per query)" % (8 * main["N_local"] / 1e9, 16 * main["N_local"] / 1e9, main["n"] * main["N_local"] / 1e9),
                    "query_model": "sequential queries (P:2024-2026), batch call per step"},
         "roofline": {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
@@ -370,8 +370,8 @@ def ours(args):
         "build": {"ms": main["build_ms"], "rows_per_s": main["N_local"] / (main["build_ms"] / 1e3),
                   "what": "summarise (PAA + iSAX + key) + CUB key sort, per GPU"},
         "stats_mean": {k: mean(k) for k in ("lb_computed", "tiles_scanned", "candidates", "lbk_pass", "refined",
-                                             "abandoned", "near_best", "dtw_cells", "exact", "tiles_listed", "seed_d2",
-                                             "bsf_d2")},
+                                             "abandoned", "near_best", "dtw_cells", "exact", "tiles_listed", "coarse",
+                                             "seed_d2", "bsf_d2")},
     }
     if args.mode == "ed" and not args.no_dtw:
         c4 = dict(CONFIGS["c4"])

@@ -73,6 +73,7 @@ typedef struct {
                              quantised-row bound did not prune them; DTW = refined */
     int64_t tiles_listed; /* tiles whose box bound <= BSF0 * (1 + eps) (the filter's list); ED scans
                              those still within the CURRENT BSF when reached (tiles_scanned) */
+    int64_t coarse;       /* series whose cardinality-16 bound passed (their 8-bit bound evaluated) */
     double seed_d2;       /* BSF0: squared distance found by the approximate search */
     double bsf_d2;        /* final fp32 best-so-far (squared) before the exact re-rank */
 } messi_stats;
@@ -145,6 +146,11 @@ messi_status messi_debug_order(messi_index* idx, const uint64_t** skey_dev, cons
  * (Property 1); reach >= 0 -> DTW envelope-PAA bound.  Squared,
  * fp32 rounded down, written to lb_dev[count] (the scan kernel's arithmetic). */
 messi_status messi_debug_lower_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
+
+/* Coarse (cardinality-16, the top 4 bits of every symbol) bound of every row against one
+ * query with the scan kernel's own arithmetic: squared, fp32, rounded down, <= the 8-bit bound
+ * of messi_debug_lower_bounds (the coarse boxes contain the fine ones).  lb_dev[count]. */
+messi_status messi_debug_coarse_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
 
 /* Box bound of every tile (512 consecutive series in approximate-search order; members are
  * rows perm[512*t .. 512*t+511]), written to lb_dev[ntiles] (fp32 of the fp64 bound). */

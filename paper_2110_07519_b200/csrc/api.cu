@@ -31,7 +31,7 @@ using namespace messi;
 
 struct Slot {
     QState* st = nullptr;
-    float *lut = nullptr, *U = nullptr, *L = nullptr;
+    float *lut = nullptr, *tab = nullptr, *U = nullptr, *L = nullptr;  // tab: 64 KB scan table
     uint2* cand = nullptr;    // scan survivors (sorted position, 8-bit LB)
     uint2* list2 = nullptr;   // DTW: LB_Keogh survivors (id, LBK)  [lazy]
     unsigned* tlist = nullptr;  // tiles surviving the box filter
@@ -50,7 +50,8 @@ struct messi_index {
     const float* rows = nullptr;
     int sms = 148;
     // summaries
-    uint4* tiles = nullptr;          // 8-bit iSAX words, 8 KB per 512 sorted positions
+    uint4* tiles = nullptr;          // cardinality-16 pair bytes, 4 KB per 512 sorted positions
+    uint4* sym8 = nullptr;           // 8-bit iSAX words in sorted order [npad][16]
     unsigned char* boxes = nullptr;  // [ntiles][32]: per-segment min / max symbol
     float* paa = nullptr;
     unsigned char* rows8 = nullptr;  // quantised rows in sorted order [npad][n] (biased int8)
@@ -80,7 +81,7 @@ struct messi_index {
 };
 
 static_assert(sizeof(messi_result) == 32, "messi_result layout");
-static_assert(sizeof(messi_stats) == 96, "messi_stats layout");
+static_assert(sizeof(messi_stats) == 104, "messi_stats layout");
 
 enum { K_SEED = 0, K_SCAN = 1, K_REFINE = 2, K_LBK = 3, K_RESOLVE = 4, K_KINDS = 5 };
 
@@ -171,8 +172,8 @@ static messi_status setup_kernels()
     static bool done = false;
     if (done) return MESSI_OK;
     const int big = 200 * 1024;
-    CK(cudaFuncSetAttribute(k_scan<SCAN_COMPACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
-    CK(cudaFuncSetAttribute(k_scan<SCAN_ALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
+    CK(cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
+    CK(cudaFuncSetAttribute(k_debug_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
     CK(cudaFuncSetAttribute(k_scan_refine_ed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(MESSI_MAX_N)));
     CK(cudaFuncSetAttribute(k_filter_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, kFilterQ * kLutF * 4));
     CK(cudaFuncSetAttribute(k_lbk_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -240,7 +241,7 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     const size_t npadrows = (size_t)idx->ntiles * MESSI_TILE_ROWS;
     messi_status s;
     if ((s = dalloc(&idx->tiles, (size_t)idx->ntiles * (MESSI_TILE_BYTES / 16))) ||
-        (s = dalloc(&idx->boxes, (size_t)idx->ntiles * 32)))
+        (s = dalloc(&idx->boxes, (size_t)idx->ntiles * 32)) || (s = dalloc(&idx->sym8, npadrows)))
         return bail(s);
     if (idx->keep_paa && (s = dalloc(&idx->paa, (size_t)N * MESSI_W))) return bail(s);
     if ((s = dalloc(&idx->rows8, npadrows * (size_t)n)) || (s = dalloc(&idx->meta8, npadrows))) return bail(s);
@@ -256,7 +257,8 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     if ((s = dalloc(&idx->skey, (size_t)N)) || (s = dalloc(&idx->perm, (size_t)N))) return bail(s);
     if ((s = dalloc(&idx->beta32, 256)) || (s = dalloc(&idx->lo_w, 256)) || (s = dalloc(&idx->hi_w, 256))) return bail(s);
     for (Slot& sl : idx->slot) {
-        if ((s = dalloc(&sl.st, 1)) || (s = dalloc(&sl.lut, MESSI_W * MESSI_CARD)) || (s = dalloc(&sl.U, n)) ||
+        if ((s = dalloc(&sl.st, 1)) || (s = dalloc(&sl.lut, MESSI_W * MESSI_CARD)) || (s = dalloc(&sl.tab, kScanTab)) ||
+            (s = dalloc(&sl.U, n)) ||
             (s = dalloc(&sl.L, n)) || (s = dalloc(&sl.cand, (size_t)N)) || (s = dalloc(&sl.near, (size_t)N)) ||
             (s = dalloc(&sl.tlist, (size_t)idx->ntiles)))
             return bail(s);
@@ -304,7 +306,8 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
         e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, idx->skey, ids_in, idx->perm, (int)N, 0, 64, st);
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "cub sort: %s", cudaGetErrorString(e)); break; }
         idx->launches += 4;
-        k_layout<<<(unsigned)idx->ntiles, MESSI_TILE_ROWS, 0, st>>>(sym_tmp, idx->perm, N, idx->tiles, idx->boxes);
+        k_layout<<<(unsigned)idx->ntiles, MESSI_TILE_ROWS, 0, st>>>(sym_tmp, idx->perm, N, idx->tiles, idx->sym8,
+                                                                    idx->boxes);
         ++idx->launches;
         e = cudaGetLastError();
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "k_layout: %s", cudaGetErrorString(e)); break; }
@@ -335,7 +338,7 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->rstr) cudaStreamSynchronize(idx->rstr);
     if (idx->stream) cudaStreamSynchronize(idx->stream);
     else cudaDeviceSynchronize();
-    void* ptrs[] = {idx->tiles, idx->boxes, idx->paa,  idx->skey, idx->perm,  idx->beta32, idx->lo_w,
+    void* ptrs[] = {idx->tiles, idx->sym8, idx->boxes, idx->paa, idx->skey, idx->perm, idx->beta32, idx->lo_w,
                     idx->hi_w,  idx->qbuf,  idx->res1, idx->stats1, idx->rows8, idx->meta8};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -345,7 +348,7 @@ extern "C" void messi_free(messi_index* idx)
             if (p) cudaFree(p);
     }
     for (Slot& sl : idx->slot) {
-        void* sp[] = {sl.st, sl.lut, sl.U, sl.L, sl.cand, sl.list2, sl.near, sl.tlist};
+        void* sp[] = {sl.st, sl.lut, sl.tab, sl.U, sl.L, sl.cand, sl.list2, sl.near, sl.tlist};
         for (void* p : sp)
             if (p) cudaFree(p);
         cudaEvent_t es[] = {sl.ev_seed, sl.ev_scan, sl.ev_done};
@@ -486,8 +489,8 @@ static messi_status launch_scan(messi_index* idx, Slot& sl)
     CK(cudaStreamWaitEvent(idx->stream, sl.ev_seed, 0));
     {
         ProfScope ps(idx, K_SCAN, idx->stream);
-        k_scan<SCAN_COMPACT><<<scan_grid(idx), 32 * kScanWarps, scan_smem(), idx->stream>>>(
-            idx->tiles, idx->ntiles, idx->N, sl.lut, sl.st, sl.cand, nullptr, sl.tlist, idx->perm);
+        k_scan<<<scan_grid(idx), 32 * kScanWarps, scan_smem(), idx->stream>>>(idx->tiles, idx->sym8, idx->N, sl.tab,
+                                                                              sl.st, sl.cand, sl.tlist);
         LAUNCHED(idx);
     }
     CK(cudaEventRecord(sl.ev_scan, idx->stream));
@@ -542,7 +545,7 @@ static messi_status run_ed_batch(messi_index* idx, const float* queries_dev, int
         {
             ProfScope ps(idx, K_SCAN, st);
             k_scan_refine_ed<<<idx->fused_grid, 32 * kFusedWarps, fused_smem(n), st>>>(
-                idx->tiles, idx->ntiles, idx->N, n, q, idx->lutx, idx->btlist, idx->bst, B, idx->rows8, idx->meta8,
+                idx->tiles, idx->sym8, idx->ntiles, idx->N, n, q, idx->lutx, idx->btlist, idx->bst, B, idx->rows8, idx->meta8,
                 idx->q8_omd, idx->perm, idx->rows);
             LAUNCHED(idx);
             k_finalise_batch<<<(B + 127) / 128, 128, 0, st>>>(idx->bst, B, idx->N, idx->row_begin, results_dev + g0,
@@ -570,7 +573,7 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
         ProfScope ps(idx, K_SEED, idx->side);
         k_seed_dtw<<<seed_grid, 32 * wf, qsm + wf * seed_warp, idx->side>>>(
             q_dev, n, reach, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32, idx->lo_w, idx->hi_w,
-            sl.lut, sl.U, sl.L, sl.st);
+            sl.lut, sl.tab, sl.U, sl.L, sl.st);
         LAUNCHED(idx);
         TRY(launch_tile_filter(idx, sl, idx->side));
     }
@@ -716,9 +719,8 @@ extern "C" messi_status messi_debug_summaries(messi_index* idx, uint8_t* sym_dev
     if (paa_dev && !idx->paa) return fail(MESSI_EINVAL, "index built without keep_paa");
     CK(cudaSetDevice(idx->device));
     TRY(sync_all(idx));
-    const long long total = idx->N * MESSI_W;
-    k_detile<<<(unsigned)((total + 255) / 256), 256, 0, idx->stream>>>((const unsigned char*)idx->tiles, idx->perm, idx->N,
-                                                                       sym_dev);
+    k_detile<<<(unsigned)((idx->N + 255) / 256), 256, 0, idx->stream>>>(idx->sym8, idx->perm, idx->N,
+                                                                        reinterpret_cast<uint4*>(sym_dev));
     LAUNCHED(idx);
     if (paa_dev)
         CK(cudaMemcpyAsync(paa_dev, idx->paa, (size_t)idx->N * MESSI_W * sizeof(float), cudaMemcpyDeviceToDevice,
@@ -757,11 +759,11 @@ static messi_status debug_prologue(messi_index* idx, const float* query_dev, int
     const size_t qsm = (size_t)((n + 3) & ~3) * sizeof(float);
     if (reach < 0) {
         k_seed_ed<<<1, 256, qsm, st>>>(query_dev, n, idx->rows, idx->skey, idx->perm, idx->N, 1, idx->beta32, idx->lo_w,
-                                       idx->hi_w, sl.lut, sl.st);
+                                       idx->hi_w, sl.lut, sl.tab, sl.st);
     } else {
         k_seed_dtw<<<1, 32, 2 * qsm + 3 * (size_t)n * sizeof(float), st>>>(query_dev, n, reach, idx->rows, idx->skey,
                                                                           idx->perm, idx->N, 1, idx->beta32, idx->lo_w,
-                                                                          idx->hi_w, sl.lut, sl.U, sl.L, sl.st);
+                                                                          idx->hi_w, sl.lut, sl.tab, sl.U, sl.L, sl.st);
     }
     LAUNCHED(idx);
     k_arm<<<1, 1, 0, st>>>(sl.st);
@@ -778,8 +780,7 @@ extern "C" messi_status messi_debug_lower_bounds(messi_index* idx, const float* 
     TRY(sync_all(idx));
     TRY(debug_prologue(idx, query_dev, reach));
     Slot& sl = idx->slot[0];
-    k_scan<SCAN_ALL><<<scan_grid(idx), 32 * kScanWarps, scan_smem(), idx->stream>>>(
-        idx->tiles, idx->ntiles, idx->N, sl.lut, sl.st, nullptr, lb_dev, nullptr, idx->perm);
+    k_debug_lb8<<<(unsigned)((idx->N + 255) / 256), 256, 0, idx->stream>>>(idx->sym8, idx->perm, idx->N, sl.lut, lb_dev);
     LAUNCHED(idx);
     CK(cudaStreamSynchronize(idx->stream));
     return MESSI_OK;
@@ -842,7 +843,7 @@ extern "C" messi_status messi_debug_scan_repeat(messi_index* idx, const float* q
     int seed_grid = (len + 7) / 8;
     if (seed_grid > 256) seed_grid = 256;
     k_seed_ed<<<seed_grid, 256, qsm, st>>>(query_dev, n, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32,
-                                           idx->lo_w, idx->hi_w, sl.lut, sl.st);
+                                           idx->lo_w, idx->hi_w, sl.lut, sl.tab, sl.st);
     LAUNCHED(idx);
     TRY(launch_tile_filter(idx, sl, st));
     std::vector<cudaEvent_t> ev(2 * (size_t)reps);
@@ -850,8 +851,8 @@ extern "C" messi_status messi_debug_scan_repeat(messi_index* idx, const float* q
     for (int r = 0; r < reps; ++r) {
         k_reset_cand<<<1, 1, 0, st>>>(sl.st);
         CK(cudaEventRecord(ev[2 * r], st));
-        k_scan<SCAN_COMPACT><<<scan_grid(idx), 32 * kScanWarps, scan_smem(), st>>>(
-            idx->tiles, idx->ntiles, idx->N, sl.lut, sl.st, sl.cand, nullptr, sl.tlist, idx->perm);
+        k_scan<<<scan_grid(idx), 32 * kScanWarps, scan_smem(), st>>>(idx->tiles, idx->sym8, idx->N, sl.tab, sl.st, sl.cand,
+                                                                     sl.tlist);
         CK(cudaEventRecord(ev[2 * r + 1], st));
     }
     idx->launches += 2 * reps;
@@ -874,6 +875,22 @@ extern "C" messi_status messi_debug_scan_repeat(messi_index* idx, const float* q
     LAUNCHED(idx);
     CK(cudaStreamSynchronize(st));
     *ms_out = ms;
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_debug_coarse_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev)
+{
+    g_err[0] = 0;
+    if (!idx || !query_dev || !lb_dev) return fail(MESSI_EINVAL, "NULL argument");
+    if (reach > idx->n) return fail(MESSI_EINVAL, "reach %d > n", reach);
+    CK(cudaSetDevice(idx->device));
+    TRY(sync_all(idx));
+    TRY(debug_prologue(idx, query_dev, reach));
+    Slot& sl = idx->slot[0];
+    k_debug_coarse<<<scan_grid(idx), 32 * kScanWarps, scan_smem(), idx->stream>>>(idx->tiles, idx->ntiles, idx->N, sl.tab,
+                                                                                 idx->perm, lb_dev);
+    LAUNCHED(idx);
+    CK(cudaStreamSynchronize(idx->stream));
     return MESSI_OK;
 }
 

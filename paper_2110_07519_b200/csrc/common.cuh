@@ -7,7 +7,7 @@
 #define MESSI_W 16                 // PAA segments ("w is fixed to 16")
 #define MESSI_CARD 256             // 8-bit iSAX symbols
 #define MESSI_TILE_ROWS 512        // series per tile (32 blocks x 16 series)
-#define MESSI_TILE_BYTES 8192      // tile: 16 tile rows x 512 B of 8-bit symbols
+#define MESSI_TILE_BYTES 4096      // tile: 8 tile rows x 512 B of cardinality-16 pair bytes
 #define MESSI_MAX_N 8192
 
 namespace messi {
@@ -31,6 +31,7 @@ struct QState {
     unsigned tile_count;    // tiles whose box bound <= BSF0 * (1 + eps) (scanned)
     unsigned exact;         // ED: fp32 distances over the raw rows (quantised bound passed)
     unsigned tiles_scanned; // batch ED: tiles whose box bound still passed the CURRENT BSF
+    unsigned coarse_count;  // series whose cardinality-16 bound passed (fine bound evaluated)
     unsigned next_tile;     // batch ED: next pair of listed tiles to hand out
     unsigned tiles_done;    // batch ED: listed tiles finished (the warp finishing the last finalises)
     unsigned lock;          // batch ED: guards best_d / best_id
@@ -60,6 +61,7 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->exact = 0;
     st->tiles_scanned = 0;
     st->next_tile = 0;
+    st->coarse_count = 0;
     st->tiles_done = 0;
     st->lock = 0;
     st->best_d = (double)INFINITY;

@@ -25,7 +25,8 @@ namespace messi {
 constexpr int kLutX = MESSI_CARD * 64;   // expanded scan table: word v*64 + 16h + s (64 KB)
 constexpr int kLutF = MESSI_CARD * 32;   // filter table: word v*32 + 16h + s (32 KB)
 constexpr int kChunkTiles = 16;          // tiles per work chunk (2 per warp)
-constexpr int kFusedWarps = 8;
+constexpr int kFusedWarps = 12;         // 2 CTAs of 12 warps per SM (64 KB table each)
+constexpr int kCandBuf = 64;            // per-warp buffer of fine survivors awaiting the refine
 constexpr int kBatchMax = 128;           // queries per launch group
 constexpr int kFilterQ = 2;              // queries per filter CTA
 
@@ -56,15 +57,12 @@ __global__ void __launch_bounds__(256) k_prologue_batch(const float* __restrict_
     }
     __syncthreads();
     float* lutc = lutc_all + (size_t)b * (MESSI_W * MESSI_CARD);
-    prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, lutc, nullptr, nullptr, &qkey_s, st);
+    prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, lutc, lutx_all + (size_t)b * kLutX, nullptr, nullptr, &qkey_s, st);
     __syncthreads();
-    float* lutx = lutx_all + (size_t)b * kLutX;
     float* lutf = lutf_all + (size_t)b * kLutF;
     for (int i = threadIdx.x; i < MESSI_W * MESSI_CARD; i += blockDim.x) {
         const int s = i >> 8, v = i & 255;
         const float val = lutc[i];
-        lutx[v * 64 + s] = val;
-        lutx[v * 64 + 16 + s] = val;
         lutf[v * 32 + s] = val;
         lutf[v * 32 + 16 + s] = val;
     }
@@ -151,23 +149,6 @@ __global__ void __launch_bounds__(256) k_seed_batch(const float* __restrict__ qu
 // Each thread takes one tile and kFilterQ queries; the 16 box bytes are rotated by
 // (lane & 15) so that at step s lane l reads segment (s + l) mod 16 from table copy l >> 4:
 // 32 distinct banks.  Kept tiles are appended as (tile, bound) to the query's list.
-__device__ __forceinline__ uint4 rotate_bytes(uint4 x, int r)
-{
-    const int wq = r >> 2, rb = (r & 3) * 8;
-    unsigned w[4] = {x.x, x.y, x.z, x.w}, o[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const unsigned a0 = w[i], a1 = w[(i + 1) & 3], a2 = w[(i + 2) & 3], a3 = w[(i + 3) & 3];
-        o[i] = wq == 0 ? a0 : wq == 1 ? a1 : wq == 2 ? a2 : a3;
-    }
-    uint4 y;
-    y.x = __funnelshift_r(o[0], o[1], rb);
-    y.y = __funnelshift_r(o[1], o[2], rb);
-    y.z = __funnelshift_r(o[2], o[3], rb);
-    y.w = __funnelshift_r(o[3], o[0], rb);
-    return y;
-}
-
 __global__ void __launch_bounds__(256) k_filter_batch(const unsigned char* __restrict__ boxes, long long ntiles,
                                                       const float* __restrict__ lutf_all, QState* st_all, int B,
                                                       uint2* __restrict__ tlist_all)
@@ -312,19 +293,20 @@ __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __res
     }
 }
 
-// Dynamic shared memory of k_scan_refine_ed: expanded table, padded query, per-warp
-// survivor lists (n = 256: 73.1 KB -> 3 CTAs per SM).
+// Dynamic shared memory of k_scan_refine_ed: scan table, padded query, per-warp coarse
+// survivor lists (current + previous tile) and fine-survivor buffer (n = 256: 92.2 KB ->
+// 2 CTAs of 12 warps per SM).
 __host__ __device__ inline size_t fused_qpad(int n) { return (size_t)(n + 4 * ((n + 31) / 32) + 4) & ~(size_t)3; }
 __host__ __device__ inline size_t fused_smem(int n)
 {
-    return (size_t)kLutX * 4 + fused_qpad(n) * 4 + (size_t)kFusedWarps * MESSI_TILE_ROWS * 2;
+    return (size_t)kLutX * 4 + fused_qpad(n) * 4 + (size_t)kFusedWarps * (2 * MESSI_TILE_ROWS * 2 + kCandBuf * 4);
 }
 
 // Writes query b's result and stats (finish_query's layout) from its state.
 __device__ void fused_finalise(const QState* st, long long N, long long row_begin, void* result, void* stats)
 {
     struct R { double dist; long long id; double d2; long long reserved; };
-    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells, exact, listed; double seed, bsf; };
+    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells, exact, listed, coarse; double seed, bsf; };
     const double bd = st->best_d;
     const long long bi = st->best_id;
     R* res = reinterpret_cast<R*>(result);
@@ -342,6 +324,7 @@ __device__ void fused_finalise(const QState* st, long long N, long long row_begi
         s->refined = st->refined;
         s->exact = st->exact;
         s->listed = st->tile_count;
+        s->coarse = st->coarse_count;
         s->abandoned = s->refined - s->exact;
         s->near = st->near_count;
         s->cells = 0;
@@ -358,7 +341,7 @@ __global__ void k_finalise_batch(const QState* __restrict__ st_all, int B, long 
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
     fused_finalise(st_all + b, N, row_begin, reinterpret_cast<char*>(results) + (size_t)b * 32,
-                   stats ? reinterpret_cast<char*>(stats) + (size_t)b * 96 : nullptr);
+                   stats ? reinterpret_cast<char*>(stats) + (size_t)b * 104 : nullptr);
 }
 
 __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes)
@@ -366,18 +349,68 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// Fine pass + refine of the coarse survivors of one tile (list surv, m entries, warp-
+// uniform).  Round 0 uses the 8-bit words the warp preloaded (w0 / pos0) one tile earlier,
+// later rounds load theirs.  Fine survivors (LB8 <= current thr) wait in the warp's buffer
+// cbuf (prefetched into L2); every full round of 32 goes through the quantised bound and
+// the exact passes.
+struct WarpCounts { unsigned tiles, coarse, cand, exact; };
+
+__device__ __forceinline__ void fine_and_refine(long long tile, int m, const unsigned short* surv, uint4 w0, unsigned pos0,
+                                                const uint4* __restrict__ sym8, const char* lbase, unsigned* cbuf,
+                                                unsigned& ncb, const unsigned char* __restrict__ rows8,
+                                                const float2* __restrict__ meta8, int n, const float* q_p,
+                                                float one_minus_delta, const unsigned* __restrict__ perm,
+                                                const float* __restrict__ rows, QState* st, WarpCounts& wc, int lane)
+{
+    for (int i0 = 0; i0 < m; i0 += 32) {
+        const bool v = i0 + lane < m;
+        unsigned pos = pos0;
+        uint4 w = w0;
+        if (i0 > 0) {
+            pos = v ? (unsigned)(tile * MESSI_TILE_ROWS + surv[i0 + lane]) : 0u;
+            if (v) w = sym8[pos];
+        }
+        float lb = INFINITY;
+        if (v) lb = fine_lb(w, lbase, lane);
+        const bool ok = v && lb <= slack_up(ld_bsf(st));
+        const unsigned pass = __ballot_sync(0xffffffffu, ok);
+        if (!pass) continue;
+        if (ok) {
+            cbuf[ncb + __popc(pass & ((1u << lane) - 1))] = pos;
+            prefetch_l2_bulk(rows8 + (long long)pos * n, (unsigned)n);
+        }
+        ncb += __popc(pass);
+        wc.cand += __popc(pass);
+        __syncwarp();
+        if (ncb >= 32) {
+            const unsigned cp = cbuf[lane];
+            const unsigned rest = ncb - 32 > (unsigned)lane ? cbuf[32 + lane] : 0u;
+            __syncwarp();
+            if (ncb - 32 > (unsigned)lane) cbuf[lane] = rest;
+            ncb -= 32;
+            __syncwarp();
+            const unsigned keep = q8_bound_pass(0xffffffffu, cp, rows8, meta8, n, q_p, one_minus_delta, st, lane);
+            wc.exact += __popc(keep);
+            exact_pass(keep, cp, perm, rows, n, q_p, st, lane);
+        }
+    }
+}
+
 // Persistent.  CTA j starts at query j mod B and walks the batch's queries cyclically once;
-// at a query with listed tiles left it loads the query's expanded table and padded query
-// into shared memory, then its warps take pairs of tiles from the query's list with one
+// at a query with listed tiles left it loads the query's scan table and padded query into
+// shared memory, then its warps take pairs of tiles from the query's list with one
 // atomicAdd (claimed one pair ahead; the next tiles are bulk-prefetched into L2), re-check
-// each tile's box bound against the CURRENT BSF (Alg. 7's node pruning), scan the tile's
-// 512 series bounds (A5, k_scan's arithmetic) and refine the survivors at once (quantised
-// bound -> fp32 distance -> fp64 re-rank; Alg. 9's worker loop).  When a
-// query's list runs dry the CTA joins the next one: light queries finish early and their
-// CTAs help the heavy ones.  k_finalise_batch writes the results.
-__global__ void __launch_bounds__(32 * kFusedWarps, 3) k_scan_refine_ed(
-    const uint4* __restrict__ tiles, long long ntiles, long long N, int n, const float* __restrict__ queries,
-    const float* __restrict__ lutx_all, const uint2* __restrict__ tlist_all, QState* st_all, int B,
+// each tile's box bound against the CURRENT BSF (Alg. 7's node pruning), run the coarse
+// pass of the tile (A5), and the fine pass + refine of the PREVIOUS tile's coarse survivors
+// (whose 8-bit words were loaded before this tile's coarse pass, hiding the gather), as
+// Alg. 9's workers do.  When a query's list runs dry the CTA joins the next
+// one: light queries finish early and their CTAs help the heavy ones.  k_finalise_batch
+// writes the results.
+__global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
+    const uint4* __restrict__ tiles, const uint4* __restrict__ sym8, long long ntiles, long long N, int n,
+    const float* __restrict__ queries, const float* __restrict__ lutx_all, const uint2* __restrict__ tlist_all,
+    QState* st_all, int B,
     const unsigned char* __restrict__ rows8, const float2* __restrict__ meta8, float one_minus_delta,
     const unsigned* __restrict__ perm, const float* __restrict__ rows)
 {
@@ -385,10 +418,11 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 3) k_scan_refine_ed(
     float* lut_s = smem;
     float* q_p = lut_s + kLutX;
     unsigned short* surv_all = reinterpret_cast<unsigned short*>(q_p + fused_qpad(n));
+    unsigned* cbuf_all = reinterpret_cast<unsigned*>(surv_all + kFusedWarps * 2 * MESSI_TILE_ROWS);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned short* surv = surv_all + warp * MESSI_TILE_ROWS;
+    unsigned short* survb = surv_all + warp * 2 * MESSI_TILE_ROWS;  // two lists: current / previous tile
+    unsigned* cbuf = cbuf_all + warp * kCandBuf;
     __shared__ int s_has;
-    const int p = lane >> 1, h = lane & 1;
     const char* lbase = reinterpret_cast<const char*>(lut_s);
     int b = (int)(blockIdx.x % (unsigned)B);
     for (int visited = 0; visited < B; ++visited, b = (b + 1 == B ? 0 : b + 1)) {
@@ -407,7 +441,12 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 3) k_scan_refine_ed(
         }
         __syncthreads();
         const uint2* tl = tlist_all + (size_t)b * ntiles;
-        unsigned n_tiles = 0, n_cand = 0, n_ref = 0, n_exact = 0;
+        WarpCounts wc{0, 0, 0, 0};
+        unsigned ncb = 0;        // fine survivors pending in cbuf (warp-uniform)
+        int pm = 0, cur = 0;     // previous tile's coarse survivors (list survb[cur ^ 1])
+        long long ptile = 0;
+        uint4 pw = make_uint4(0, 0, 0, 0);
+        unsigned ppos = 0;
         unsigned k_next = 0;
         if (lane == 0) k_next = atomicAdd(&st->next_tile, 1u) * 2u;
         k_next = __shfl_sync(0xffffffffu, k_next, 0);
@@ -431,71 +470,42 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 3) k_scan_refine_ed(
                 if (k0 + u >= count) break;
                 const uint2 te = u == 0 ? te0 : te1;
                 // warp-uniform decision: lane 0's reading of the BSF
-                float thr = __shfl_sync(0xffffffffu, slack_up(ld_bsf(st)), 0);
-                if (__uint_as_float(te.y) > thr) continue;  // box pruned by the current BSF
-                ++n_tiles;
+                const float bthr = __shfl_sync(0xffffffffu, slack_up(ld_bsf(st)), 0);
+                if (__uint_as_float(te.y) > bthr) continue;  // box pruned by the current BSF
+                ++wc.tiles;
                 const long long tile = te.x;
-                const uint4* tp = tiles + tile * (MESSI_TILE_BYTES / 16) + lane;
-                uint4 data[16];
-#pragma unroll
-                for (int t = 0; t < 16; ++t) data[t] = __ldcs(tp + t * 32);
-                float acc[16];
-#pragma unroll
-                for (int k2 = 0; k2 < 16; ++k2) acc[k2] = 0.0f;
-#pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                    const unsigned base = (unsigned)((16 * h + ((t + p) & 15)) * 4);
-                    const unsigned wv[4] = {data[t].x, data[t].y, data[t].z, data[t].w};
-#pragma unroll
-                    for (int wi = 0; wi < 4; ++wi) {
-#pragma unroll
-                        for (int bb = 0; bb < 4; ++bb) {
-                            const unsigned addr = __byte_perm(wv[wi], base, 0x5504 | (bb << 4));
-                            acc[wi * 4 + bb] =
-                                __fadd_rd(acc[wi * 4 + bb], *reinterpret_cast<const float*>(lbase + addr));
-                        }
-                    }
-                }
-                thr = slack_up(ld_bsf(st));
-                const long long id0 = tile * MESSI_TILE_ROWS + lane * 16;
-                unsigned mask = 0;
-#pragma unroll
-                for (int k2 = 0; k2 < 16; ++k2)
-                    if (acc[k2] <= thr && id0 + k2 < N) mask |= 1u << k2;
-                const int cnt = __popc(mask);
-                int incl = cnt;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                const int m = __shfl_sync(0xffffffffu, incl, 31);
-                if (m == 0) continue;
-                int off = incl - cnt;
-                while (mask) {
-                    const int k2 = __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    surv[off++] = (unsigned short)(lane * 16 + k2);
-                }
-                __syncwarp();
-                n_cand += m;
-                for (int i0 = 0; i0 < m; i0 += 32) {
-                    const bool v = i0 + lane < m;
-                    const unsigned pos = v ? (unsigned)(tile * MESSI_TILE_ROWS + surv[i0 + lane]) : 0u;
-                    const unsigned pass = __ballot_sync(0xffffffffu, v);
-                    n_ref += __popc(pass);
-                    const unsigned keep = q8_bound_pass(pass, pos, rows8, meta8, n, q_p, one_minus_delta, st, lane);
-                    n_exact += __popc(keep);
-                    exact_pass(keep, pos, perm, rows, n, q_p, st, lane);
-                }
-                __syncwarp();
+                unsigned short* surv = survb + cur * MESSI_TILE_ROWS;
+                const int m = scan_tile_coarse(tiles, tile, lbase, slack_up(ld_bsf(st)), N, surv, lane);
+                wc.coarse += m;
+                if (pm)
+                    fine_and_refine(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb,
+                                    rows8, meta8, n, q_p, one_minus_delta, perm, rows, st, wc, lane);
+                // preload the 8-bit words of this tile's first 32 coarse survivors
+                ppos = lane < m ? (unsigned)(tile * MESSI_TILE_ROWS + surv[lane]) : 0u;
+                pw = lane < m ? sym8[ppos] : make_uint4(0, 0, 0, 0);
+                pm = m;
+                ptile = tile;
+                cur ^= 1;
             }
         }
+        if (pm)
+            fine_and_refine(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb, rows8,
+                            meta8, n, q_p, one_minus_delta, perm, rows, st, wc, lane);
+        if (ncb) {  // the query's last fine survivors
+            const unsigned cp = (unsigned)lane < ncb ? cbuf[lane] : 0u;
+            const unsigned pass = ncb >= 32 ? 0xffffffffu : (1u << ncb) - 1u;
+            __syncwarp();
+            const unsigned keep = q8_bound_pass(pass, cp, rows8, meta8, n, q_p, one_minus_delta, st, lane);
+            wc.exact += __popc(keep);
+            exact_pass(keep, cp, perm, rows, n, q_p, st, lane);
+            ncb = 0;
+        }
         if (lane == 0) {
-            if (n_tiles) atomicAdd(&st->tiles_scanned, n_tiles);
-            if (n_cand) atomicAdd(&st->cand_count, n_cand);
-            if (n_ref) atomicAdd(&st->refined, n_ref);
-            if (n_exact) atomicAdd(&st->exact, n_exact);
+            if (wc.tiles) atomicAdd(&st->tiles_scanned, wc.tiles);
+            if (wc.cand) atomicAdd(&st->cand_count, wc.cand);
+            if (wc.cand) atomicAdd(&st->refined, wc.cand);
+            if (wc.coarse) atomicAdd(&st->coarse_count, wc.coarse);
+            if (wc.exact) atomicAdd(&st->exact, wc.exact);
         }
         __syncthreads();  // every warp is done with b's table before it is overwritten
     }

@@ -319,7 +319,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
                              void* result, void* stats)
 {
     struct R { double dist; long long id; double d2; long long reserved; };
-    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells, exact, listed; double seed, bsf; };
+    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells, exact, listed, coarse; double seed, bsf; };
     R* res = reinterpret_cast<R*>(result);
     res->dist = b.id >= 0 ? sqrt(b.d) : (double)INFINITY;
     res->id = b.id >= 0 ? row_begin + b.id : -1;
@@ -337,6 +337,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
         s->cells = (long long)st->dtw_cells;
         s->exact = st->exact ? st->exact : st->refined;
         s->listed = st->tile_count;
+        s->coarse = st->coarse_count;
         s->seed = (double)__uint_as_float(st->seed_bits);
         s->bsf = (double)__uint_as_float(st->bsf_bits);
     }

@@ -16,8 +16,8 @@ namespace messi {
 // IN cases of Fig. fig:dtwsimd as one branch-free max.
 __device__ void prologue_block(const float* __restrict__ q, int n, int reach, const float* __restrict__ beta_g,
                                const float* __restrict__ lo_w, const float* __restrict__ hi_w,
-                               float* __restrict__ lut_g, float* __restrict__ U_g, float* __restrict__ L_g,
-                               unsigned long long* key_out, QState* st)
+                               float* __restrict__ lut_g, float* __restrict__ tab, float* __restrict__ U_g,
+                               float* __restrict__ L_g, unsigned long long* key_out, QState* st)
 {
     __shared__ double ubar[MESSI_W], lbar[MESSI_W];
     __shared__ float beta[256];
@@ -69,7 +69,26 @@ __device__ void prologue_block(const float* __restrict__ q, int n, int reach, co
             int s = i >> 8, v = i & 255;
             double lo = (double)lo_w[v], hi = (double)hi_w[v];
             double d = fmax(0.0, fmax(lo - ubar[s], lbar[s] - hi));
-            lut_g[i] = __double2float_rd(md * d * d);
+            const float t8 = __double2float_rd(md * d * d);
+            lut_g[i] = t8;
+            if (tab) {
+                tab[v * 64 + 32 + s] = t8;
+                tab[v * 64 + 48 + s] = t8;
+            }
+        }
+        // scan table, coarse part: pair byte v = (a << 4 | c) of segments (2j, 2j+1) at
+        // cardinality 16 -- the box of 4-bit symbol a is the union of the 8-bit boxes
+        // 16a .. 16a+15, so T16 <= T8 of every refinement (Property 1 holds per level)
+        if (tab) {
+            for (int i = tid; i < MESSI_CARD * 8; i += blockDim.x) {
+                const int v = i >> 3, j = i & 7, a = v >> 4, c = v & 15;
+                const double da = fmax(0.0, fmax((double)lo_w[16 * a] - ubar[2 * j], lbar[2 * j] - (double)hi_w[16 * a + 15]));
+                const double dc = fmax(0.0, fmax((double)lo_w[16 * c] - ubar[2 * j + 1],
+                                                 lbar[2 * j + 1] - (double)hi_w[16 * c + 15]));
+                const float pt = __double2float_rd(md * da * da + md * dc * dc);
+#pragma unroll
+                for (int cp = 0; cp < 4; ++cp) tab[v * 64 + 4 * j + cp] = pt;
+            }
         }
     }
 }
@@ -106,13 +125,14 @@ __global__ void __launch_bounds__(256) k_seed_ed(const float* __restrict__ q_g, 
                                                  const unsigned* __restrict__ perm, long long N, int window,
                                                  const float* __restrict__ beta_g, const float* __restrict__ lo_w,
                                                  const float* __restrict__ hi_w, float* __restrict__ lut_g,
-                                                 QState* st)
+                                                 float* __restrict__ tab, QState* st)
 {
     extern __shared__ __align__(16) float q_s[];
     __shared__ unsigned long long qkey_s;
     for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
     __syncthreads();
-    prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, blockIdx.x == 0 ? lut_g : nullptr, nullptr, nullptr, &qkey_s, st);
+    prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, blockIdx.x == 0 ? lut_g : nullptr, blockIdx.x == 0 ? tab : nullptr,
+                   nullptr, nullptr, &qkey_s, st);
     __syncthreads();
     const unsigned long long qkey = qkey_s;
     long long a = block_lower_bound(skey, N, qkey);
@@ -142,7 +162,8 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
                            const unsigned long long* __restrict__ skey, const unsigned* __restrict__ perm,
                            long long N, int window, const float* __restrict__ beta_g,
                            const float* __restrict__ lo_w, const float* __restrict__ hi_w,
-                           float* __restrict__ lut_g, float* __restrict__ U_g, float* __restrict__ L_g, QState* st)
+                           float* __restrict__ lut_g, float* __restrict__ tab, float* __restrict__ U_g,
+                           float* __restrict__ L_g, QState* st)
 {
     extern __shared__ __align__(16) float dsm[];
     float* q_s = dsm;
@@ -150,9 +171,9 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
     for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
     __syncthreads();
     if (blockIdx.x == 0)
-        prologue_block(q_s, n, reach, beta_g, lo_w, hi_w, lut_g, U_g, L_g, &qkey_s, st);
+        prologue_block(q_s, n, reach, beta_g, lo_w, hi_w, lut_g, tab, U_g, L_g, &qkey_s, st);
     else
-        prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, nullptr, nullptr, nullptr, &qkey_s, st);
+        prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, nullptr, nullptr, nullptr, nullptr, &qkey_s, st);
     __syncthreads();
     const unsigned long long qkey = qkey_s;
     long long a = block_lower_bound(skey, N, qkey);
@@ -227,102 +248,187 @@ __global__ void k_tile_filter(const unsigned char* __restrict__ boxes, long long
     }
 }
 
+// Rotates the 16 bytes of x down by r (byte s of the result = byte (s + r) mod 16 of x).
+__device__ __forceinline__ uint4 rotate_bytes(uint4 x, int r)
+{
+    // branch-free (lane-dependent r): two predicated word rotations, then one funnel shift
+    const bool r1 = (r & 4) != 0, r2 = (r & 8) != 0;
+    unsigned a0 = r1 ? x.y : x.x, a1 = r1 ? x.z : x.y, a2 = r1 ? x.w : x.z, a3 = r1 ? x.x : x.w;
+    const unsigned b0 = r2 ? a2 : a0, b1 = r2 ? a3 : a1, b2 = r2 ? a0 : a2, b3 = r2 ? a1 : a3;
+    const int rb = (r & 3) * 8;
+    uint4 y;
+    y.x = __funnelshift_r(b0, b1, rb);
+    y.y = __funnelshift_r(b1, b2, rb);
+    y.z = __funnelshift_r(b2, b3, rb);
+    y.w = __funnelshift_r(b3, b0, rb);
+    return y;
+}
+
 // ---------------------------------------------------------------------- lower-bound scan
 // The HBM-roofline step (A5): Alg. 9 line LowerBound_SIMD / Alg. 10 line
-// LowerBound_DTW_SIMD for every series of every tile the box filter kept: LB =
-// sum_s T[s][sym_s] (round-down adds) from the 8-bit words.  Shared-memory table, 64 KB:
-// word v*64 + 16h + s holds T[s][v]; the lane owning block b = 2p + h reads segment
-// s = (t + p) mod 16 at step t, so the 32 lanes hit 32 distinct banks for any symbols.
-// PRMT builds the byte address (v << 8 | base) from the packed symbols in one instruction.
-// Survivors (LB <= BSF0 * (1 + eps)) are appended as (sorted position, LB) with a warp
-// ballot + prefix and one atomicAdd per warp-tile.
-//   SCAN_COMPACT: survivors -> candidate list;   SCAN_ALL: every LB written (inspection,
-//   all tiles, scattered back to row order).
-enum { SCAN_COMPACT = 0, SCAN_ALL = 1 };
+// LowerBound_DTW_SIMD, in two resolutions of the same iSAX word (variable
+// cardinality):
+//   coarse: every series of a tile, from its cardinality-16 pair bytes (4 KB per tile):
+//           LB16 = sum_j PT[j][H_j] (round-down adds), PT[j][.] = T16[2j] + T16[2j+1]
+//   fine:   the coarse survivors, from their 8-bit words (sym8, 16 B each):
+//           LB8 = sum_s T8[s][sym_s] >= LB16 (T16 = min of T8 over the 16 refinements)
+// Shared-memory scan table (64 KB, built by the prologue, copied per CTA), word v*64 + w:
+//   w = 4j + c (c < 4): PT[j][v]      -- lane b reads pair (t + b) mod 8 at tile row t from
+//                                        copy b >> 3: 32 distinct banks for any bytes
+//   w = 32 + 16x + s  : T8[s][v]      -- lane l reads segment (s + l) mod 16 at step s from
+//                                        copy l >> 4: 32 distinct banks for any symbols
+// PRMT builds every byte address (v << 8 | w * 4) in one instruction.
 constexpr int kScanWarps = 8;
-constexpr size_t kScanLutBytes = (size_t)MESSI_CARD * 64 * sizeof(float);
+constexpr int kScanTab = MESSI_CARD * 64;                 // floats per scan table
+constexpr size_t kScanLutBytes = (size_t)kScanTab * sizeof(float);
 
-#ifndef MESSI_SCAN_NOCOMPUTE
-#define MESSI_SCAN_NOCOMPUTE 0
-#endif
-
-template <int MODE>
-__global__ void __launch_bounds__(32 * kScanWarps, 2) k_scan(const uint4* __restrict__ tiles, long long ntiles,
-                                                             long long N, const float* __restrict__ lut_g, QState* st,
-                                                             uint2* __restrict__ out, float* __restrict__ lb_all,
-                                                             const unsigned* __restrict__ tlist,
-                                                             const unsigned* __restrict__ perm)
+// Coarse bounds of the 512 series of tile `tile`; the series with LB16 <= thr are written to
+// the warp's list surv (tile-local index) in ascending order; returns their number
+// (warp-uniform).
+// Coarse bounds acc[k] of the lane's 16 series 16*lane + k of tile `tile`.
+__device__ __forceinline__ void coarse_acc(const uint4* __restrict__ tiles, long long tile, const char* lbase, int lane,
+                                           float acc[16])
 {
-    extern __shared__ __align__(16) float lut_s[];  // 256 * 64 floats
-    for (int i = threadIdx.x; i < MESSI_W * MESSI_CARD; i += blockDim.x) {
-        const int sg = i >> 8, v = i & 255;
-        const float val = lut_g[i];
-        lut_s[v * 64 + sg] = val;
-        lut_s[v * 64 + 16 + sg] = val;
-    }
-    __syncthreads();
-    const float thr = MODE == SCAN_ALL ? INFINITY : slack_up(ld_bsf(st));
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int p = lane >> 1, h = lane & 1;
-    const char* lbase = reinterpret_cast<const char*>(lut_s);
-    const long long count = MODE == SCAN_ALL ? ntiles : (long long)*(volatile unsigned*)&st->tile_count;
-    for (long long it = (long long)blockIdx.x * kScanWarps + warp; it < count; it += (long long)gridDim.x * kScanWarps) {
-        const long long tl = MODE == SCAN_ALL ? it : (long long)tlist[it];
-        const uint4* tp = tiles + tl * (MESSI_TILE_BYTES / 16) + lane;
-        uint4 data[16];
+    const uint4* tp = tiles + tile * (MESSI_TILE_BYTES / 16) + lane;
+    uint4 data[8];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) data[t] = __ldcs(tp + t * 32);
-        float acc[16];
+    for (int t = 0; t < 8; ++t) data[t] = __ldcs(tp + t * 32);
 #pragma unroll
-        for (int k = 0; k < 16; ++k) acc[k] = 0.0f;
-#if MESSI_SCAN_NOCOMPUTE  // bandwidth probe only
-        unsigned x = 0;
+    for (int k = 0; k < 16; ++k) acc[k] = 0.0f;
+    const int bl = lane & 7, cp = lane >> 3;
 #pragma unroll
-        for (int t = 0; t < 16; ++t) x ^= data[t].x ^ data[t].y ^ data[t].z ^ data[t].w;
+    for (int t = 0; t < 8; ++t) {
+        const unsigned base = (unsigned)((4 * ((t + bl) & 7) + cp) * 4);
+        const unsigned wv[4] = {data[t].x, data[t].y, data[t].z, data[t].w};
 #pragma unroll
-        for (int k = 0; k < 16; ++k) acc[k] = x == 0x12345678u ? -1.0f : 1e30f;
-#else
+        for (int wi = 0; wi < 4; ++wi) {
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-            const unsigned base = (unsigned)((16 * h + ((t + p) & 15)) * 4);
-            const unsigned wv[4] = {data[t].x, data[t].y, data[t].z, data[t].w};
-#pragma unroll
-            for (int wi = 0; wi < 4; ++wi) {
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const unsigned addr = __byte_perm(wv[wi], base, 0x5504 | (b << 4));
-                    acc[wi * 4 + b] = __fadd_rd(acc[wi * 4 + b], *reinterpret_cast<const float*>(lbase + addr));
-                }
+            for (int bb = 0; bb < 4; ++bb) {
+                const unsigned addr = __byte_perm(wv[wi], base, 0x5504 | (bb << 4));
+                acc[wi * 4 + bb] = __fadd_rd(acc[wi * 4 + bb], *reinterpret_cast<const float*>(lbase + addr));
             }
         }
-#endif
-        const long long id0 = tl * MESSI_TILE_ROWS + lane * 16;
-        if (MODE == SCAN_ALL) {
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-                if (id0 + k < N) lb_all[perm[id0 + k]] = acc[k];
-            continue;
-        }
-        unsigned mask = 0;
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if (acc[k] <= thr && id0 + k < N) mask |= 1u << k;
-        if (!__any_sync(0xffffffffu, mask)) continue;
-        const int cnt = __popc(mask);
-        int incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(&st->cand_count, (unsigned)total);
-        unsigned pos = __shfl_sync(0xffffffffu, base, 0) + incl - cnt;
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if (mask & (1u << k)) out[pos++] = make_uint2((unsigned)(id0 + k), __float_as_uint(acc[k]));
     }
+}
+
+__device__ __forceinline__ int scan_tile_coarse(const uint4* __restrict__ tiles, long long tile, const char* lbase,
+                                                float thr, long long N, unsigned short* surv, int lane)
+{
+    float acc[16];
+    coarse_acc(tiles, tile, lbase, lane, acc);
+    const long long id0 = tile * MESSI_TILE_ROWS + lane * 16;
+    unsigned mask = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+        if (acc[k] <= thr && id0 + k < N) mask |= 1u << k;
+    const int cnt = __popc(mask);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int m = __shfl_sync(0xffffffffu, incl, 31);
+    int off = incl - cnt;
+    while (mask) {
+        const int k = __ffs(mask) - 1;
+        mask &= mask - 1;
+        surv[off++] = (unsigned short)(lane * 16 + k);
+    }
+    __syncwarp();
+    return m;
+}
+
+// Fine bound of one series from its 8-bit word (16 symbols, segment s in byte s); the lane
+// sums the segments in the order (s + lane) mod 16 (any order gives a valid bound).
+__device__ __forceinline__ float fine_lb(uint4 w, const char* lbase, int lane)
+{
+    const int r = lane & 15;
+    const uint4 x = rotate_bytes(w, r);  // byte s of x = symbol of segment (s + r) mod 16
+    const unsigned xv[4] = {x.x, x.y, x.z, x.w};
+    const unsigned cbase = 128u + 64u * (unsigned)(lane >> 4);
+    float acc = 0.0f;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const unsigned base = cbase + 4u * (unsigned)((s + r) & 15);
+        const unsigned addr = __byte_perm(xv[s >> 2], base, 0x5504 | ((s & 3) << 4));
+        acc = __fadd_rd(acc, *reinterpret_cast<const float*>(lbase + addr));
+    }
+    return acc;
+}
+
+// Per-query scan for the DTW path (and the scan-throughput probe): the tiles the box filter
+// listed, coarse + fine bounds, survivors (LB8 <= BSF0 * (1 + eps)) appended as (sorted
+// position, LB8) with one atomicAdd per warp-round.
+__global__ void __launch_bounds__(32 * kScanWarps, 3) k_scan(const uint4* __restrict__ tiles, const uint4* __restrict__ sym8,
+                                                             long long N, const float* __restrict__ tab_g, QState* st,
+                                                             uint2* __restrict__ out, const unsigned* __restrict__ tlist)
+{
+    extern __shared__ __align__(16) float tab_s[];
+    __shared__ unsigned short surv_all[kScanWarps][MESSI_TILE_ROWS];
+    for (int i = threadIdx.x; i < kScanTab / 4; i += blockDim.x)
+        reinterpret_cast<float4*>(tab_s)[i] = reinterpret_cast<const float4*>(tab_g)[i];
+    __syncthreads();
+    const float thr = slack_up(ld_bsf(st));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned short* surv = surv_all[warp];
+    const char* lbase = reinterpret_cast<const char*>(tab_s);
+    const long long count = (long long)*(volatile unsigned*)&st->tile_count;
+    for (long long it = (long long)blockIdx.x * kScanWarps + warp; it < count; it += (long long)gridDim.x * kScanWarps) {
+        const long long tl = (long long)tlist[it];
+        const int m = scan_tile_coarse(tiles, tl, lbase, thr, N, surv, lane);
+        if (lane == 0 && m) atomicAdd(&st->coarse_count, (unsigned)m);
+        for (int i0 = 0; i0 < m; i0 += 32) {
+            const bool v = i0 + lane < m;
+            const unsigned pos = v ? (unsigned)(tl * MESSI_TILE_ROWS + surv[i0 + lane]) : 0u;
+            float lb = INFINITY;
+            if (v) lb = fine_lb(sym8[pos], lbase, lane);
+            const bool ok = v && lb <= thr;
+            const unsigned msk = __ballot_sync(0xffffffffu, ok);
+            if (!msk) continue;
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(&st->cand_count, (unsigned)__popc(msk));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (ok) out[base + __popc(msk & ((1u << lane) - 1))] = make_uint2(pos, __float_as_uint(lb));
+        }
+        __syncwarp();
+    }
+}
+
+// Inspection: the coarse (cardinality-16) bound of every series with the scan's own
+// arithmetic (coarse_acc), scattered back to row order.
+__global__ void __launch_bounds__(32 * kScanWarps) k_debug_coarse(const uint4* __restrict__ tiles, long long ntiles,
+                                                                  long long N, const float* __restrict__ tab_g,
+                                                                  const unsigned* __restrict__ perm, float* __restrict__ lb_all)
+{
+    extern __shared__ __align__(16) float tab_s[];
+    for (int i = threadIdx.x; i < kScanTab / 4; i += blockDim.x)
+        reinterpret_cast<float4*>(tab_s)[i] = reinterpret_cast<const float4*>(tab_g)[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (long long tl = (long long)blockIdx.x * kScanWarps + warp; tl < ntiles; tl += (long long)gridDim.x * kScanWarps) {
+        float acc[16];
+        coarse_acc(tiles, tl, reinterpret_cast<const char*>(tab_s), lane, acc);
+        const long long id0 = tl * MESSI_TILE_ROWS + lane * 16;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (id0 + k < N) lb_all[perm[id0 + k]] = acc[k];
+    }
+}
+
+// Inspection: the fine bound of every series (segments in order 0..15), scattered back to
+// row order; table T8 from the compact prologue output lut_g[s][v].
+__global__ void k_debug_lb8(const uint4* __restrict__ sym8, const unsigned* __restrict__ perm, long long N,
+                            const float* __restrict__ lut_g, float* __restrict__ lb_all)
+{
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const uint4 w = sym8[p];
+    const unsigned wv[4] = {w.x, w.y, w.z, w.w};
+    float acc = 0.0f;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) acc = __fadd_rd(acc, lut_g[s * 256 + ((wv[s >> 2] >> (8 * (s & 3))) & 255u)]);
+    lb_all[perm[p]] = acc;
 }
 
 }  // namespace messi

@@ -33,16 +33,20 @@ __global__ void k_breakpoints(float* beta32, float* lo_w, float* hi_w)
 // cardinality iSAX tree; a tile of 512 consecutive positions plays the role of a
 // leaf node, and its box -- per segment the min and max symbol of its members -- is the
 // node's iSAX summary used to prune it (Alg. 7's FindDist).
-//  * tiles (8 KB per 512 positions), skewed layout: block b = 16 series (b < 32), pair
-//    p = b >> 1, half h = b & 1; tile row t (512 B) holds, at byte offset 16*b, segment
-//    s = (t + p) mod 16 of block b's 16 series.  A warp reading tile row t (lane b loads
-//    16 B) therefore holds 16 different segments across the pairs; with the table stored
-//    twice (copy h) the 32 lanes hit 32 distinct shared-memory banks whatever the symbols.
+//  * tiles (4 KB per 512 positions): the cardinality-16 word of each series (the top 4 bits
+//    of its 8-bit symbols: iSAX is variable-cardinality by construction), as 8
+//    pair bytes H_j = hi4(sym_2j) << 4 | hi4(sym_2j+1).  Skewed: block b = 16 series
+//    (b < 32); tile row t (512 B) holds at byte 16b + k the pair byte j = (t + b) mod 8 of
+//    series 16b + k.  A warp reading tile row t (lane b loads 16 B) holds all 8 pairs, each
+//    for 4 lanes; with the pair table stored 4 times (copy b >> 3) the 32 lanes hit 32
+//    distinct shared-memory banks whatever the bytes.
+//  * sym8 [npad][16] u8: the full 8-bit words, series-major (one 16 B load per series) --
+//    read only for the few series whose coarse bound survives.
 //  * boxes [ntiles][32] u8: per segment min (bytes 0..15) and max (16..31) symbol.
-__device__ __forceinline__ int tile_offset(int rr, int s)
+__device__ __forceinline__ int tile_offset(int rr, int j)
 {
-    int b = rr >> 4, k = rr & 15, p = b >> 1;
-    int t = (s - p) & 15;
+    const int b = rr >> 4, k = rr & 15;
+    const int t = (j - b) & 7;
     return t * 512 + b * 16 + k;
 }
 
@@ -110,9 +114,11 @@ __global__ void __launch_bounds__(256) k_summarise(const float* __restrict__ row
 }
 
 // Lays the summaries out in sorted order: one CTA (512 threads) per tile of 512 sorted
-// positions gathers its rows' 8-bit words and writes the skewed tile and the box.
+// positions gathers its rows' 8-bit words, writes them series-major (sym8), the skewed
+// coarse tile and the box.
 __global__ void __launch_bounds__(512) k_layout(const uint4* __restrict__ symrows_tmp, const unsigned* __restrict__ perm,
-                                                int64_t N, uint4* __restrict__ tiles, unsigned char* __restrict__ boxes)
+                                                int64_t N, uint4* __restrict__ tiles, uint4* __restrict__ sym8,
+                                                unsigned char* __restrict__ boxes)
 {
     __shared__ __align__(16) unsigned char tile[MESSI_TILE_BYTES];
     __shared__ unsigned bmin[MESSI_W], bmax[MESSI_W];
@@ -123,19 +129,27 @@ __global__ void __launch_bounds__(512) k_layout(const uint4* __restrict__ symrow
     __syncthreads();
     const bool valid = p < N;
     const uint4 sr = valid ? symrows_tmp[perm[p]] : make_uint4(0, 0, 0, 0);
+    sym8[p] = sr;
     const unsigned w[4] = {sr.x, sr.y, sr.z, sr.w};
 #pragma unroll
-    for (int s = 0; s < MESSI_W; ++s) {
-        const unsigned sym = (w[s >> 2] >> (8 * (s & 3))) & 255u;
-        tile[tile_offset(i, s)] = (unsigned char)sym;
+    for (int j = 0; j < MESSI_W / 2; ++j) {
+        const unsigned a = (w[(2 * j) >> 2] >> (8 * ((2 * j) & 3))) & 255u;
+        const unsigned c = (w[(2 * j + 1) >> 2] >> (8 * ((2 * j + 1) & 3))) & 255u;
+        tile[tile_offset(i, j)] = (unsigned char)((a & 0xF0u) | (c >> 4));
+    }
+#pragma unroll
+    for (int sg = 0; sg < MESSI_W; ++sg) {
+        const unsigned sym = (w[sg >> 2] >> (8 * (sg & 3))) & 255u;
         if (valid) {
-            atomicMin(&bmin[s], sym);
-            atomicMax(&bmax[s], sym);
+            atomicMin(&bmin[sg], sym);
+            atomicMax(&bmax[sg], sym);
         }
     }
     __syncthreads();
-    uint4* dst = tiles + tl * (MESSI_TILE_BYTES / 16);
-    dst[i] = reinterpret_cast<const uint4*>(tile)[i];
+    if (i < MESSI_TILE_BYTES / 16) {
+        uint4* dst = tiles + tl * (MESSI_TILE_BYTES / 16);
+        dst[i] = reinterpret_cast<const uint4*>(tile)[i];
+    }
     if (i < MESSI_W) {
         boxes[tl * 32 + i] = (unsigned char)bmin[i];
         boxes[tl * 32 + 16 + i] = (unsigned char)bmax[i];
@@ -224,15 +238,11 @@ __global__ void k_unsort_q8(const unsigned char* __restrict__ rows8, const float
 }
 
 // Inspection: the 8-bit words back in row order, out[row][16].
-__global__ void k_detile(const unsigned char* __restrict__ tiles, const unsigned* __restrict__ perm, int64_t N,
-                         unsigned char* __restrict__ out)
+__global__ void k_detile(const uint4* __restrict__ sym8, const unsigned* __restrict__ perm, int64_t N,
+                         uint4* __restrict__ out)
 {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= N * MESSI_W) return;
-    const int64_t p = i / MESSI_W;
-    const int s = (int)(i % MESSI_W);
-    out[(int64_t)perm[p] * MESSI_W + s] =
-        tiles[(p / MESSI_TILE_ROWS) * MESSI_TILE_BYTES + tile_offset((int)(p % MESSI_TILE_ROWS), s)];
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < N) out[perm[p]] = sym8[p];
 }
 
 }  // namespace messi

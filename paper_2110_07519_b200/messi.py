@@ -45,6 +45,7 @@ class Stats(ctypes.Structure):
                 ("lbk_pass", ctypes.c_int64),
                 ("refined", ctypes.c_int64), ("abandoned", ctypes.c_int64), ("near_best", ctypes.c_int64),
                 ("dtw_cells", ctypes.c_int64), ("exact", ctypes.c_int64), ("tiles_listed", ctypes.c_int64),
+                ("coarse", ctypes.c_int64),
                 ("seed_d2", ctypes.c_double), ("bsf_d2", ctypes.c_double)]
 
     def as_dict(self):
@@ -80,6 +81,7 @@ def lib():
         L.messi_debug_breakpoints.argtypes = [i32, vp]
         L.messi_debug_summaries.argtypes = [vp, vp, vp]
         L.messi_debug_quantised.argtypes = [vp, vp, vp]
+        L.messi_debug_coarse_bounds.argtypes = [vp, vp, i32, vp]
         L.messi_debug_order.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]
         L.messi_debug_lower_bounds.argtypes = [vp, vp, i32, vp]
         L.messi_debug_tile_bounds.argtypes = [vp, vp, i32, vp]
@@ -97,7 +99,8 @@ EXPORTED = ["messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_
             "messi_free", "messi_last_error", "messi_launch_count", "messi_profile_enable", "messi_profile_read",
             "messi_debug_breakpoints",
             "messi_debug_summaries", "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances",
-            "messi_debug_scan_repeat", "messi_debug_tile_bounds", "messi_debug_quantised"]
+            "messi_debug_scan_repeat", "messi_debug_tile_bounds", "messi_debug_quantised",
+            "messi_debug_coarse_bounds"]
 
 
 def _check(status: int):
@@ -147,7 +150,7 @@ def messi_query_dtw(handle, query, reach: int, with_stats: bool = False):
 
 def messi_query_ed_batch(handle, queries_dev: torch.Tensor, results_dev: torch.Tensor, stats_dev=None):
     """Asynchronous on the build stream.  results_dev: uint8 CUDA tensor of nq*32 bytes (see
-    ``result_buffer``); stats_dev: optional nq*96 bytes (``stats_buffer``)."""
+    ``result_buffer``); stats_dev: optional nq*104 bytes (``stats_buffer``)."""
     _check(lib().messi_query_ed_batch(handle, _ptr(queries_dev), queries_dev.shape[0], _ptr(results_dev),
                                       _ptr(stats_dev)))
 
@@ -228,6 +231,12 @@ def messi_debug_lower_bounds(handle, query_dev: torch.Tensor, reach: int, count:
     return lb
 
 
+def messi_debug_coarse_bounds(handle, query_dev: torch.Tensor, reach: int, count: int):
+    lb = torch.empty(count, dtype=torch.float32, device=query_dev.device)
+    _check(lib().messi_debug_coarse_bounds(handle, _ptr(query_dev), int(reach), _ptr(lb)))
+    return lb
+
+
 def messi_debug_tile_bounds(handle, query_dev: torch.Tensor, reach: int, ntiles: int):
     lb = torch.empty(ntiles, dtype=torch.float32, device=query_dev.device)
     _check(lib().messi_debug_tile_bounds(handle, _ptr(query_dev), int(reach), _ptr(lb)))
@@ -266,7 +275,7 @@ def _wrap_dev(ptr: int, nbytes: int, device):
     return torch.as_tensor(_Arr(), device=device)
 
 
-RESULT_BYTES, STATS_BYTES = 32, 96
+RESULT_BYTES, STATS_BYTES = 32, 104
 
 
 def result_buffer(nq: int, device) -> torch.Tensor:
@@ -293,8 +302,8 @@ def decode_results_device(buf: torch.Tensor):
 
 def decode_stats(buf: torch.Tensor):
     raw = buf.view(-1, STATS_BYTES).cpu()
-    ints = raw[:, :80].contiguous().view(torch.int64)
-    dbl = raw[:, 80:].contiguous().view(torch.float64)
+    ints = raw[:, :88].contiguous().view(torch.int64)
+    dbl = raw[:, 88:].contiguous().view(torch.float64)
     return [dict(zip(STATS_FIELDS, list(map(int, i.tolist())) + list(map(float, d.tolist()))))
             for i, d in zip(ints, dbl)]
 

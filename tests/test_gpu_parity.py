@@ -111,6 +111,37 @@ def test_lower_bounds_ed(c1):
 
 
 @pytest.mark.parametrize("reach", [-1, 25])
+def test_coarse_bounds(c1, reach):
+    """The scan's coarse pass (cardinality 16 = the top 4 bits of every symbol):
+    its bound equals the oracle's card-16 mindist (ED) within the widened-box / round-down
+    tolerance, never exceeds the 8-bit bound of the same row (the coarse box contains the
+    fine one), and never exceeds the true distance (ED) / the DTW bound chain."""
+    X, Q, idx, Xh, Qh = c1
+    N = X.shape[0]
+    _, S = oracle.isax_rows(Xh)
+    b16 = oracle.breakpoints(16)[1]
+    for qi in range(2):
+        q = Q[qi].contiguous()
+        cb = messi().messi_debug_coarse_bounds(idx.handle, q, reach, N).cpu().numpy().astype(np.float64)
+        fb = messi().messi_debug_lower_bounds(idx.handle, q, reach, N).cpu().numpy().astype(np.float64)
+        assert np.all(cb <= fb * (1 + 2.0 ** -20) + 1e-30)
+        if reach < 0:
+            qp = oracle.paa64(Qh[qi])
+            rows = np.random.default_rng(10 + qi).choice(N, 2000, replace=False)
+            ref = np.array([oracle.mindist2(qp, S[r] >> 4, 256, card=16) for r in rows])
+            lo = np.concatenate([[-np.inf], b16]).astype(np.float64)
+            hi = np.concatenate([b16, [np.inf]]).astype(np.float64)
+            d_seg = np.maximum(0, np.maximum(lo[S[rows] >> 4] - qp, qp - hi[S[rows] >> 4]))
+            tol = _lb_tol(d_seg, 16) + 2.0 ** -20 * ref
+            assert np.all(np.abs(cb[rows] - ref) <= tol)
+            assert np.all(cb <= oracle.ed2_rows(Xh, Qh[qi]))
+        # the coarse pass is a real filter: most rows fail it at the NN distance
+        d2, _ = oracle.nn("ed", Xh[:20000], Qh[qi:qi + 1]) if reach < 0 else (None, None)
+        if reach < 0:
+            assert np.mean(cb <= d2[0]) < 0.5
+
+
+@pytest.mark.parametrize("reach", [-1, 25])
 def test_tile_box_bounds(c1, reach):
     """The box of a tile (512 consecutive series in approximate-search order) bounds every
     member from below: tile LB <= each member's 8-bit bound <= its true distance (the node
