@@ -463,8 +463,9 @@ static messi_status join_streams(messi_index* idx)
 
 static messi_status ensure_dtw_buffers(messi_index* idx)
 {
-    for (Slot& sl : idx->slot)
+    for (Slot& sl : idx->slot) {
         if (!sl.list2) TRY(dalloc(&sl.list2, (size_t)idx->N));
+    }
     return MESSI_OK;
 }
 

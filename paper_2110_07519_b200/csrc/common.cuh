@@ -43,6 +43,7 @@ struct QState {
     int window_len;
     double ubar[16], lbar[16];  // query PAA (ED: both) or envelope PAA (DTW), fp64
     unsigned char zlo[16], zhi[16];  // batch ED: per segment, the symbols whose table entry is 0
+    unsigned lbk_thr_bits;  // DTW: the scan's threshold (BSF0), used by the LB_Keogh filter
 };
 
 struct NearEntry { unsigned id; float d32; };

@@ -39,6 +39,15 @@ template <typename T> __device__ __forceinline__ T inf_of();
 template <> __device__ __forceinline__ float inf_of<float>() { return INFINITY; }
 template <> __device__ __forceinline__ double inf_of<double>() { return (double)INFINITY; }
 
+// Three-input fp32 minimum: one FMNMX3 on sm_100a (min is exact, so the DP values are the
+// same as with two fminf).
+__device__ __forceinline__ float min3f(float a, float b, float c)
+{
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
 __device__ __forceinline__ float cell_cost_add(float q, float c, float m) { float d = q - c; return fmaf(d, d, m); }
 __device__ __forceinline__ double cell_cost_add(float q, float c, double m)
 {
@@ -240,7 +249,7 @@ struct DtwThread {
             float left = INFINITY;
 #pragma unroll
             for (int d = 0; d < W; ++d) {
-                float mn = fminf(fminf(D[d], D[d + 1]), left);
+                const float mn = min3f(D[d], D[d + 1], left);
                 float df = qq[u] - cw[d + u];
                 left = fmaf(df, df, mn);
                 D[d] = left;
@@ -248,7 +257,8 @@ struct DtwThread {
         }
         float mn = D[0];
 #pragma unroll
-        for (int d = 1; d < W; ++d) mn = fminf(mn, D[d]);
+        for (int d = 1; d + 1 < W; d += 2) mn = min3f(mn, D[d], D[d + 1]);
+        if ((W & 1) == 0) mn = fminf(mn, D[W - 1]);
         seen_lo = seen;
 #pragma unroll
         for (int e = 0; e < CW - 4; ++e) cw[e] = cw[e + 4];

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ ca
     const unsigned total = *(volatile unsigned*)&st->cand_count;
     const int lane = threadIdx.x & 31;
     const unsigned wpb = blockDim.x >> 5;
-    const float thr = slack_up(ld_bsf(st));
+    const float thr = __uint_as_float(st->lbk_thr_bits);  // the scan's threshold (BSF0, fixed)
     for (unsigned k0 = (blockIdx.x * wpb + (threadIdx.x >> 5)) * 32; k0 < total; k0 += gridDim.x * wpb * 32) {
         const bool valid = k0 + lane < total;
         const uint2 e = valid ? cand[k0 + lane] : make_uint2(0u, 0x7f800000u);
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
     DtwThread<R> dp;
     bool have = k < total;
     const float* c = rows;
-    unsigned id = 0, refined = 0, abandoned = 0, steps = 0;
+    unsigned id = 0, refined = 0, abandoned = 0, steps = 0, skipped = 0;
     float lbk_total = 0.0f;
     // the lane's next candidate is fetched one candidate ahead and the head of its row
     // prefetched, so a lane that restarts does not stall its warp on an HBM round trip
@@ -212,6 +212,9 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
         asm volatile("prefetch.global.L1 [%0];" ::"l"(pr + 128));
     };
     if (k + nthreads < total) prefetch_row(nxt.x);
+    float thr = slack_up(ld_bsf(st));
+    // a candidate whose LB_Keogh already exceeds the current threshold is skipped unstarted
+    auto admit = [&](float lbk) { return lbk * 0.9990234375f <= thr; };
     if (have) {
         const uint2 e = list2[k];
         id = e.x;
@@ -220,7 +223,6 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
         dp.start(c, n, U, L);
         ++refined;
     }
-    float thr = slack_up(ld_bsf(st));
     while (__any_sync(0xffffffffu, have)) {
         if (have) {
             const float rowmin = dp.step4(c, n, q_s, U, L);
@@ -242,25 +244,30 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
                 }
             }
             if (done) {
-                k += nthreads;
-                have = k < total;
-                if (have) {
+                thr = slack_up(ld_bsf(st));
+                for (;;) {
+                    k += nthreads;
+                    have = k < total;
+                    if (!have) break;
                     id = nxt.x;
                     lbk_total = __uint_as_float(nxt.y);
-                    c = rows + (long long)id * n;
                     if (k + nthreads < total) {
                         nxt = list2[k + nthreads];
-                        prefetch_row(nxt.x);
+                        if (admit(__uint_as_float(nxt.y))) prefetch_row(nxt.x);
                     }
+                    if (admit(lbk_total)) break;
+                    ++skipped;
+                }
+                if (have) {
+                    c = rows + (long long)id * n;
                     dp.start(c, n, U, L);
                     ++refined;
-                    thr = slack_up(ld_bsf(st));
                 }
             }
         }
     }
     refined = __reduce_add_sync(0xffffffffu, refined);
-    abandoned = __reduce_add_sync(0xffffffffu, abandoned);
+    abandoned = __reduce_add_sync(0xffffffffu, abandoned + skipped);
     steps = __reduce_add_sync(0xffffffffu, steps);
     if ((threadIdx.x & 31) == 0) {
         if (refined) atomicAdd(&st->refined, refined);

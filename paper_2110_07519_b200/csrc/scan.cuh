@@ -370,6 +370,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 3) k_scan(const uint4* __rest
         reinterpret_cast<float4*>(tab_s)[i] = reinterpret_cast<const float4*>(tab_g)[i];
     __syncthreads();
     const float thr = slack_up(ld_bsf(st));
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->lbk_thr_bits = __float_as_uint(thr);  // for the DTW filter
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned short* surv = surv_all[warp];
     const char* lbase = reinterpret_cast<const char*>(tab_s);
