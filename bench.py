@@ -260,6 +260,19 @@ def run_arm(cfg, args, world, rank, dev, stream, time_steps, warmup):
     return out
 
 
+def arm_config(cfg, args, world, nq):
+    """The workload description both arms print (same keys, same values)."""
+    nl = cfg["N"] // world
+    return {"workload": cfg["name"], "mode": args.mode, "rows": cfg["N"], "length": cfg["n"],
+            "queries_per_step": nq, "reach": cfg["reach"], "parallelism": f"row-shard x{world}",
+            "merge": "per step: one all_gather of (d2, gid) x queries per rank, lexicographic min" if world > 1
+            else "single shard",
+            "l2": "inputs larger than L2: %.2f GB of coarse iSAX tiles + %.2f GB of 8-bit words + %.2f GB of "
+                  "quantised rows per GPU; each query streams the tiles its box filter keeps (distinct per query)"
+                  % (8 * nl / 1e9, 16 * nl / 1e9, cfg["n"] * nl / 1e9),
+            "query_model": "sequential queries (P:2024-2026), batch call per step"}
+
+
 def cpu_baseline(cfg, args, dev, kind):
     """The oracle, as it stands, timed on this host's cores over a bounded row sample of the
     workload (rows copied back from the device generator), scaled to the full collection."""
@@ -346,12 +359,7 @@ def ours(args):
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": value / PAPER_QPS if args.mode == "ed" and cname == "c3" else None,
         "dtype": "f32", "data": "synthetic (seeded device Philox random walks, z-normalised)",
-        "config": {"workload": cfg["name"], "mode": args.mode, "rows": cfg["N"], "length": cfg["n"],
-                   "queries_per_step": nq, "reach": cfg["reach"], "parallelism": f"row-shard x{world}",
-                   "merge": "per step: one all_gather of (d2, gid) x queries per rank, lexicographic min" if world > 1
-                   else "single shard",
-                   "l2": "inputs larger than L2: %.2f GB of coarse iSAX tiles + %.2f GB of 8-bit words + %.2f GB of quantised rows per GPU; each query streams the tiles its box filter keeps (distinct per query)" % (8 * main["N_local"] / 1e9, 16 * main["N_local"] / 1e9, main["n"] * main["N_local"] / 1e9),
-                   "query_model": "sequential queries (P:2024-2026), batch call per step"},
+        "config": arm_config(cfg, args, world, nq),
         "roofline": {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in pk else "fallback",
@@ -442,7 +450,7 @@ def reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * scale * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded random walks, z-normalised)",
-            "config": {"workload": cfg["name"], "mode": args.mode, "rows": cfg["N"], "length": cfg["n"]},
+            "config": arm_config(cfg, args, world, args.queries or cfg["Q"]),
             "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "oracle",
                              "sample": f"each step: 1 query over the first {rows:,} of {cfg['N']:,} rows, "
                                        f"time scaled x{scale:g} to the full collection"},
