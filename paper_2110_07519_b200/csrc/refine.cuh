@@ -52,7 +52,10 @@ __device__ __forceinline__ unsigned q8_bound_pass(unsigned pass, unsigned my_pos
         const float2 mb = ob ? meta8[pb] : make_float2(0.0f, 0.0f);
         const unsigned char* ra = rows8 + (long long)pa * n;
         const unsigned char* rb = rows8 + (long long)pb * n;
-        float acc_a = 0.0f, acc_b = 0.0f;
+        // paired fp32 (FADD2 / FFMA2): bytes (0,1) and (2,3) of every word in one op each
+        float2 qsa = make_float2(0.0f, 0.0f), qsb = make_float2(0.0f, 0.0f);
+        const float2 nsa = make_float2(-ma.x, -ma.x), nsb = make_float2(-mb.x, -mb.x);
+        const float2 bias = make_float2(-8388736.0f, -8388736.0f);  // - (2^23 + 128)
         for (int c = gl * 16; c < n; c += 128) {
             const uint4 wa = oa ? __ldg(reinterpret_cast<const uint4*>(ra + c)) : make_uint4(0, 0, 0, 0);
             const uint4 wb = ob ? __ldg(reinterpret_cast<const uint4*>(rb + c)) : make_uint4(0, 0, 0, 0);
@@ -62,19 +65,23 @@ __device__ __forceinline__ unsigned q8_bound_pass(unsigned pass, unsigned my_pos
                 // q_p: element i at i + 4 (i >> 5) -- the eight lanes of a group then read
                 // 8 x 16 B from 32 distinct banks
                 const float4 qv = *reinterpret_cast<const float4*>(q_p + c + 4 * w + 4 * (c >> 5));
-                const float qq[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const unsigned sel = 0x7650u | (unsigned)b;  // byte b of x, then 0x4B000000's bytes
-                    const float ca = __uint_as_float(__byte_perm(xa[w], 0x4B000000u, sel)) - 8388736.0f;  // - (2^23 + 128)
-                    const float cb = __uint_as_float(__byte_perm(xb[w], 0x4B000000u, sel)) - 8388736.0f;
-                    const float da = fmaf(-ma.x, ca, qq[b]);
-                    const float db = fmaf(-mb.x, cb, qq[b]);
-                    acc_a = fmaf(da, da, acc_a);
-                    acc_b = fmaf(db, db, acc_b);
+                for (int b = 0; b < 4; b += 2) {
+                    // byte b of x, then 0x4B000000's bytes: float(2^23 + byte)
+                    const unsigned s0 = 0x7650u | (unsigned)b, s1 = 0x7650u | (unsigned)(b + 1);
+                    const float2 qq = b == 0 ? make_float2(qv.x, qv.y) : make_float2(qv.z, qv.w);
+                    const float2 ca = fadd2(make_float2(__uint_as_float(__byte_perm(xa[w], 0x4B000000u, s0)),
+                                                        __uint_as_float(__byte_perm(xa[w], 0x4B000000u, s1))), bias);
+                    const float2 cb = fadd2(make_float2(__uint_as_float(__byte_perm(xb[w], 0x4B000000u, s0)),
+                                                        __uint_as_float(__byte_perm(xb[w], 0x4B000000u, s1))), bias);
+                    const float2 da = ffma2(nsa, ca, qq);
+                    const float2 db = ffma2(nsb, cb, qq);
+                    qsa = ffma2(da, da, qsa);
+                    qsb = ffma2(db, db, qsb);
                 }
             }
         }
+        float acc_a = qsa.x + qsa.y, acc_b = qsb.x + qsb.y;
 #pragma unroll
         for (int o = 4; o; o >>= 1) {
             acc_a += __shfl_xor_sync(0xffffffffu, acc_a, o);

@@ -303,9 +303,14 @@ __device__ __forceinline__ void coarse_acc(const uint4* __restrict__ tiles, long
 #pragma unroll
         for (int wi = 0; wi < 4; ++wi) {
 #pragma unroll
-            for (int bb = 0; bb < 4; ++bb) {
-                const unsigned addr = __byte_perm(wv[wi], base, 0x5504 | (bb << 4));
-                acc[wi * 4 + bb] = __fadd_rd(acc[wi * 4 + bb], *reinterpret_cast<const float*>(lbase + addr));
+            for (int bb = 0; bb < 4; bb += 2) {
+                const unsigned a0 = __byte_perm(wv[wi], base, 0x5504 | (bb << 4));
+                const unsigned a1 = __byte_perm(wv[wi], base, 0x5504 | ((bb + 1) << 4));
+                const float2 t = make_float2(*reinterpret_cast<const float*>(lbase + a0),
+                                             *reinterpret_cast<const float*>(lbase + a1));
+                const float2 r = fadd2_rd(make_float2(acc[wi * 4 + bb], acc[wi * 4 + bb + 1]), t);
+                acc[wi * 4 + bb] = r.x;
+                acc[wi * 4 + bb + 1] = r.y;
             }
         }
     }
@@ -347,14 +352,16 @@ __device__ __forceinline__ float fine_lb(uint4 w, const char* lbase, int lane)
     const uint4 x = rotate_bytes(w, r);  // byte s of x = symbol of segment (s + r) mod 16
     const unsigned xv[4] = {x.x, x.y, x.z, x.w};
     const unsigned cbase = 128u + 64u * (unsigned)(lane >> 4);
-    float acc = 0.0f;
+    float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
-    for (int s = 0; s < 16; ++s) {
-        const unsigned base = cbase + 4u * (unsigned)((s + r) & 15);
-        const unsigned addr = __byte_perm(xv[s >> 2], base, 0x5504 | ((s & 3) << 4));
-        acc = __fadd_rd(acc, *reinterpret_cast<const float*>(lbase + addr));
+    for (int s = 0; s < 16; s += 2) {
+        const unsigned b0 = cbase + 4u * (unsigned)((s + r) & 15), b1 = cbase + 4u * (unsigned)((s + 1 + r) & 15);
+        const unsigned a0 = __byte_perm(xv[s >> 2], b0, 0x5504 | ((s & 3) << 4));
+        const unsigned a1 = __byte_perm(xv[s >> 2], b1, 0x5504 | (((s + 1) & 3) << 4));
+        acc = fadd2_rd(acc, make_float2(*reinterpret_cast<const float*>(lbase + a0),
+                                        *reinterpret_cast<const float*>(lbase + a1)));
     }
-    return acc;
+    return __fadd_rd(acc.x, acc.y);
 }
 
 // Per-query scan for the DTW path (and the scan-throughput probe): the tiles the box filter
