@@ -60,11 +60,13 @@ struct messi_index {
     unsigned long long* skey = nullptr;
     unsigned* perm = nullptr;
     float *beta32 = nullptr, *lo_w = nullptr, *hi_w = nullptr;
-    // batched ED path (fused.cuh): per-query state, tables and tile lists of one launch group
-    QState* bst = nullptr;
-    float *lutc = nullptr, *lutx = nullptr, *lutf = nullptr;
-    uint2* btlist = nullptr;
-    unsigned* work = nullptr;
+    // batched ED path (fused.cuh): per-query state, tables and tile lists of a launch group
+    // (two sets, alternating between consecutive groups of one call)
+    struct BatchSet {
+        QState* bst = nullptr;
+        float *lutc = nullptr, *lutx = nullptr, *lutf = nullptr;
+        uint2* btlist = nullptr;
+    } bset[2];
     int fused_grid = 0;
     // per-query scratch
     Slot slot[2];
@@ -342,8 +344,8 @@ extern "C" void messi_free(messi_index* idx)
                     idx->hi_w,  idx->qbuf,  idx->res1, idx->stats1, idx->rows8, idx->meta8};
     for (void* p : ptrs)
         if (p) cudaFree(p);
-    {
-        void* bp[] = {idx->bst, idx->lutc, idx->lutx, idx->lutf, idx->btlist, idx->work};
+    for (auto& bs : idx->bset) {
+        void* bp[] = {bs.bst, bs.lutc, bs.lutx, bs.lutf, bs.btlist};
         for (void* p : bp)
             if (p) cudaFree(p);
     }
@@ -501,58 +503,69 @@ static messi_status launch_scan(messi_index* idx, Slot& sl)
 
 static messi_status ensure_batch_buffers(messi_index* idx)
 {
-    if (idx->bst) return MESSI_OK;
-    TRY(dalloc(&idx->bst, kBatchMax));
-    TRY(dalloc(&idx->lutc, (size_t)kBatchMax * MESSI_W * MESSI_CARD));
-    TRY(dalloc(&idx->lutx, (size_t)kBatchMax * kLutX));
-    TRY(dalloc(&idx->lutf, (size_t)kBatchMax * kLutF));
-    TRY(dalloc(&idx->btlist, (size_t)kBatchMax * (size_t)idx->ntiles));
-    TRY(dalloc(&idx->work, 1));
+    if (idx->bset[0].bst) return MESSI_OK;
+    for (auto& bs : idx->bset) {
+        TRY(dalloc(&bs.bst, kBatchMax));
+        TRY(dalloc(&bs.lutc, (size_t)kBatchMax * MESSI_W * MESSI_CARD));
+        TRY(dalloc(&bs.lutx, (size_t)kBatchMax * kLutX));
+        TRY(dalloc(&bs.lutf, (size_t)kBatchMax * kLutF));
+        TRY(dalloc(&bs.btlist, (size_t)kBatchMax * (size_t)idx->ntiles));
+    }
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan_refine_ed, 32 * kFusedWarps, fused_smem(idx->n)));
-    idx->fused_grid = idx->sms * (occ < 1 ? 1 : occ);
+    if (occ < 1) return fail(MESSI_ECUDA, "fused kernel does not fit an SM (n = %d)", idx->n);
+    idx->fused_grid = idx->sms * occ;
     return MESSI_OK;
 }
 
-// The batched ED path (fused.cuh) for nq queries [nq][n] on the device: groups of up to
-// kBatchMax queries, four launches per group on the index stream.
+// One group of B <= kBatchMax queries of the batched ED path (fused.cuh) on stream st with
+// state set bs: prologue, seed, tile filter, the fused scan + refine kernel, finalise.
+static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSet& bs, cudaStream_t st, const float* q, int B,
+                                    messi_result* res, messi_stats* stats)
+{
+    const int n = idx->n;
+    const size_t qsm = (size_t)((n + 3) & ~3) * sizeof(float);
+    const int len = (int)(idx->window < idx->N ? idx->window : idx->N);
+    {
+        ProfScope ps(idx, K_SEED, st);
+        k_prologue_batch<<<B, 256, qsm, st>>>(q, n, idx->beta32, idx->lo_w, idx->hi_w, idx->skey, idx->N, idx->window,
+                                              bs.lutc, bs.lutx, bs.lutf, bs.bst);
+        LAUNCHED(idx);
+        dim3 sg((unsigned)((len + kSeedRowsPerCta - 1) / kSeedRowsPerCta), (unsigned)B);
+        k_seed_batch<<<sg, 256, qsm, st>>>(q, n, idx->rows, idx->perm, bs.bst);
+        LAUNCHED(idx);
+        long long fx = (idx->ntiles + 255) / 256;
+        const long long fcap = (long long)idx->sms * 3 * 2 / ((B + kFilterQ - 1) / kFilterQ) + 1;
+        if (fx > fcap) fx = fcap;
+        dim3 fg((unsigned)fx, (unsigned)((B + kFilterQ - 1) / kFilterQ));
+        k_filter_batch<<<fg, 256, kFilterQ * kLutF * 4, st>>>(idx->boxes, idx->ntiles, bs.lutf, bs.bst, B, bs.btlist);
+        LAUNCHED(idx);
+    }
+    {
+        ProfScope ps(idx, K_SCAN, st);
+        k_scan_refine_ed<<<idx->fused_grid, 32 * kFusedWarps, fused_smem(n), st>>>(
+            idx->tiles, idx->sym8, idx->ntiles, idx->N, n, q, bs.lutx, bs.btlist, bs.bst, B, idx->rows8,
+            idx->meta8, idx->q8_omd, idx->perm, idx->rows);
+        LAUNCHED(idx);
+        k_finalise_batch<<<(B + 127) / 128, 128, 0, st>>>(bs.bst, B, idx->N, idx->row_begin, res, stats);
+        LAUNCHED(idx);
+    }
+    return MESSI_OK;
+}
+
+// The batched ED path for nq queries [nq][n] on the device: one group per kBatchMax queries
+// on the caller's stream.  (Splitting a batch over the two library streams, to overlap one
+// group's prologue / filter with the other's fused kernel, was measured slower: each
+// persistent kernel then balances fewer queries.)
 static messi_status run_ed_batch(messi_index* idx, const float* queries_dev, int nq, messi_result* results_dev,
                                  messi_stats* stats_dev)
 {
     TRY(ensure_batch_buffers(idx));
     const int n = idx->n;
-    const size_t qsm = (size_t)((n + 3) & ~3) * sizeof(float);
-    cudaStream_t st = idx->stream;
-    const int len = (int)(idx->window < idx->N ? idx->window : idx->N);
     for (int g0 = 0; g0 < nq; g0 += kBatchMax) {
         const int B = nq - g0 < kBatchMax ? nq - g0 : kBatchMax;
-        const float* q = queries_dev + (size_t)g0 * n;
-        {
-            ProfScope ps(idx, K_SEED, st);
-            k_prologue_batch<<<B, 256, qsm, st>>>(q, n, idx->beta32, idx->lo_w, idx->hi_w, idx->skey, idx->N,
-                                                  idx->window, idx->lutc, idx->lutx, idx->lutf, idx->bst, idx->work);
-            LAUNCHED(idx);
-            dim3 sg((unsigned)((len + kSeedRowsPerCta - 1) / kSeedRowsPerCta), (unsigned)B);
-            k_seed_batch<<<sg, 256, qsm, st>>>(q, n, idx->rows, idx->perm, idx->bst);
-            LAUNCHED(idx);
-            long long fx = (idx->ntiles + 255) / 256;
-            const long long fcap = (long long)idx->sms * 3 * 2 / ((B + kFilterQ - 1) / kFilterQ) + 1;
-            if (fx > fcap) fx = fcap;
-            dim3 fg((unsigned)fx, (unsigned)((B + kFilterQ - 1) / kFilterQ));
-            k_filter_batch<<<fg, 256, kFilterQ * kLutF * 4, st>>>(idx->boxes, idx->ntiles, idx->lutf, idx->bst, B,
-                                                                  idx->btlist);
-            LAUNCHED(idx);
-        }
-        {
-            ProfScope ps(idx, K_SCAN, st);
-            k_scan_refine_ed<<<idx->fused_grid, 32 * kFusedWarps, fused_smem(n), st>>>(
-                idx->tiles, idx->sym8, idx->ntiles, idx->N, n, q, idx->lutx, idx->btlist, idx->bst, B, idx->rows8, idx->meta8,
-                idx->q8_omd, idx->perm, idx->rows);
-            LAUNCHED(idx);
-            k_finalise_batch<<<(B + 127) / 128, 128, 0, st>>>(idx->bst, B, idx->N, idx->row_begin, results_dev + g0,
-                                                              stats_dev ? stats_dev + g0 : nullptr);
-            LAUNCHED(idx);
-        }
+        TRY(launch_ed_group(idx, idx->bset[(g0 / kBatchMax) & 1], idx->stream, queries_dev + (size_t)g0 * n, B,
+                            results_dev + g0, stats_dev ? stats_dev + g0 : nullptr));
     }
     return MESSI_OK;
 }

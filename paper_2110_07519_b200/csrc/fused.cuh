@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(256) k_prologue_batch(const float* __restrict_
                                                         const unsigned long long* __restrict__ skey, long long N,
                                                         int window, float* __restrict__ lutc_all,
                                                         float* __restrict__ lutx_all, float* __restrict__ lutf_all,
-                                                        QState* st_all, unsigned* work)
+                                                        QState* st_all)
 {
     extern __shared__ __align__(16) float q_s[];
     __shared__ unsigned long long qkey_s;
@@ -51,10 +51,7 @@ __global__ void __launch_bounds__(256) k_prologue_batch(const float* __restrict_
     QState* st = st_all + b;
     const float* q = queries + (size_t)b * n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q[i];
-    if (threadIdx.x == 0) {
-        arm_state(st);
-        if (b == 0) *work = 0u;
-    }
+    if (threadIdx.x == 0) arm_state(st);
     __syncthreads();
     float* lutc = lutc_all + (size_t)b * (MESSI_W * MESSI_CARD);
     prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, lutc, lutx_all + (size_t)b * kLutX, nullptr, nullptr, &qkey_s, st);
