@@ -53,6 +53,7 @@ struct messi_index {
     uint4* tiles = nullptr;          // cardinality-16 pair bytes, 4 KB per 512 sorted positions
     uint4* sym8 = nullptr;           // 8-bit iSAX words in sorted order [npad][16]
     unsigned char* boxes = nullptr;  // [ntiles][32]: per-segment min / max symbol
+    uint4* sboxes = nullptr;         // [nsuper][2]: union boxes of kSuperTiles consecutive tiles
     float* paa = nullptr;
     unsigned char* rows8 = nullptr;  // quantised rows in sorted order [npad][n] (biased int8)
     float2* meta8 = nullptr;         // per sorted position {scale (power of 2), error norm bound}
@@ -243,7 +244,8 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     const size_t npadrows = (size_t)idx->ntiles * MESSI_TILE_ROWS;
     messi_status s;
     if ((s = dalloc(&idx->tiles, (size_t)idx->ntiles * (MESSI_TILE_BYTES / 16))) ||
-        (s = dalloc(&idx->boxes, (size_t)idx->ntiles * 32)) || (s = dalloc(&idx->sym8, npadrows)))
+        (s = dalloc(&idx->boxes, (size_t)idx->ntiles * 32)) || (s = dalloc(&idx->sym8, npadrows)) ||
+        (s = dalloc(&idx->sboxes, (size_t)2 * ((idx->ntiles + kSuperTiles - 1) / kSuperTiles))))
         return bail(s);
     if (idx->keep_paa && (s = dalloc(&idx->paa, (size_t)N * MESSI_W))) return bail(s);
     if ((s = dalloc(&idx->rows8, npadrows * (size_t)n)) || (s = dalloc(&idx->meta8, npadrows))) return bail(s);
@@ -313,6 +315,12 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
         ++idx->launches;
         e = cudaGetLastError();
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "k_layout: %s", cudaGetErrorString(e)); break; }
+        {
+            const long long nsuper = (idx->ntiles + kSuperTiles - 1) / kSuperTiles;
+            k_superbox<<<(unsigned)((nsuper + 255) / 256), 256, 0, st>>>(reinterpret_cast<const uint4*>(idx->boxes),
+                                                                       idx->ntiles, idx->sboxes);
+            ++idx->launches;
+        }
         k_quantise<<<(unsigned)(idx->sms * 8), 256, 0, st>>>(rows_dev, idx->perm, N, (int64_t)npadrows, n, idx->rows8,
                                                             idx->meta8);
         ++idx->launches;
@@ -340,7 +348,7 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->rstr) cudaStreamSynchronize(idx->rstr);
     if (idx->stream) cudaStreamSynchronize(idx->stream);
     else cudaDeviceSynchronize();
-    void* ptrs[] = {idx->tiles, idx->sym8, idx->boxes, idx->paa, idx->skey, idx->perm, idx->beta32, idx->lo_w,
+    void* ptrs[] = {idx->tiles, idx->sym8, idx->boxes, idx->sboxes, idx->paa, idx->skey, idx->perm, idx->beta32, idx->lo_w,
                     idx->hi_w,  idx->qbuf,  idx->res1, idx->stats1, idx->rows8, idx->meta8};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -534,11 +542,14 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
         dim3 sg((unsigned)((len + kSeedRowsPerCta - 1) / kSeedRowsPerCta), (unsigned)B);
         k_seed_batch<<<sg, 256, qsm, st>>>(q, n, idx->rows, idx->perm, bs.bst);
         LAUNCHED(idx);
-        long long fx = (idx->ntiles + 255) / 256;
-        const long long fcap = (long long)idx->sms * 3 * 2 / ((B + kFilterQ - 1) / kFilterQ) + 1;
+        const long long nsuper = (idx->ntiles + kSuperTiles - 1) / kSuperTiles;
+        const int npairs = (B + kFilterQ - 1) / kFilterQ;
+        long long fx = (nsuper + 255) / 256;
+        const long long fcap = (long long)idx->sms * 8 / npairs + 1;
         if (fx > fcap) fx = fcap;
-        dim3 fg((unsigned)fx, (unsigned)((B + kFilterQ - 1) / kFilterQ));
-        k_filter_batch<<<fg, 256, kFilterQ * kLutF * 4, st>>>(idx->boxes, idx->ntiles, bs.lutf, bs.bst, B, bs.btlist);
+        dim3 fg((unsigned)fx, (unsigned)npairs);
+        k_filter_batch<<<fg, 256, kFilterQ * kLutF * 4, st>>>(reinterpret_cast<const uint4*>(idx->boxes), idx->sboxes,
+                                                              idx->ntiles, nsuper, bs.lutf, bs.bst, B, bs.btlist);
         LAUNCHED(idx);
     }
     {

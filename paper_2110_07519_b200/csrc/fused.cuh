@@ -139,14 +139,52 @@ __global__ void __launch_bounds__(256) k_seed_batch(const float* __restrict__ qu
 }
 
 // --------------------------------------------------------------------------- filter
-// Box bound of tile t for query b (Alg. 7 line "FindDist(node) > BSF -> prune"):
+// Box bound of a tile for one query (Alg. 7 line "FindDist(node) > BSF -> prune"):
 // per segment the tile's symbols lie in [vmin, vmax]; the smallest table entry over that
 // range is 0 if it meets the zero run [zlo, zhi], else T[vmax] (range below the run) or
 // T[vmin] (above it) -- so sum_s of it (round-down adds) lower-bounds every member's bound.
-// Each thread takes one tile and kFilterQ queries; the 16 box bytes are rotated by
-// (lane & 15) so that at step s lane l reads segment (s + l) mod 16 from table copy l >> 4:
-// 32 distinct banks.  Kept tiles are appended as (tile, bound) to the query's list.
-__global__ void __launch_bounds__(256) k_filter_batch(const unsigned char* __restrict__ boxes, long long ntiles,
+// mn / mx are the box bytes rotated by r = lane & 15, so that at step s lane l reads
+// segment (s + l) mod 16 from table copy l >> 4 (T = table + 16 (l >> 4)): 32 distinct banks.
+__device__ __forceinline__ float box_lb(uint4 mn, uint4 mx, const float* T, const unsigned char* zlo,
+                                        const unsigned char* zhi, int r)
+{
+    const unsigned a[4] = {mn.x, mn.y, mn.z, mn.w}, c[4] = {mx.x, mx.y, mx.z, mx.w};
+    float acc = 0.0f;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const int sg = (s + r) & 15;
+        const unsigned vmin = (a[s >> 2] >> (8 * (s & 3))) & 255u, vmax = (c[s >> 2] >> (8 * (s & 3))) & 255u;
+        const unsigned zl = zlo[sg], zh = zhi[sg];
+        const unsigned v = vmax < zl ? vmax : vmin;
+        const float term = T[v * 32 + sg];
+        acc = __fadd_rd(acc, (vmin <= zh && vmax >= zl) ? 0.0f : term);
+    }
+    return acc;
+}
+
+// Super-tile boxes: the union box of kSuperTiles consecutive tiles (a node one level up the
+// key-sorted "tree"), bytewise min of the mins / max of the maxes.
+constexpr int kSuperTiles = 16;
+__global__ void k_superbox(const uint4* __restrict__ boxes, long long ntiles, uint4* __restrict__ sboxes)
+{
+    const long long S = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long t0 = S * kSuperTiles;
+    if (t0 >= ntiles) return;
+    uint4 mn = boxes[2 * t0], mx = boxes[2 * t0 + 1];
+    for (long long t = t0 + 1; t < min(ntiles, t0 + kSuperTiles); ++t) {
+        const uint4 a = boxes[2 * t], c = boxes[2 * t + 1];
+        mn = make_uint4(__vminu4(mn.x, a.x), __vminu4(mn.y, a.y), __vminu4(mn.z, a.z), __vminu4(mn.w, a.w));
+        mx = make_uint4(__vmaxu4(mx.x, c.x), __vmaxu4(mx.y, c.y), __vmaxu4(mx.z, c.z), __vmaxu4(mx.w, c.w));
+    }
+    sboxes[2 * S] = mn;
+    sboxes[2 * S + 1] = mx;
+}
+
+// Two-level filter, kFilterQ queries per CTA: a warp tests 32 super-tiles (one per lane);
+// the tiles of every super-tile that passes are tested 16 at a time (half-warps), and the
+// kept tiles are appended as (tile, bound) to the query's list.
+__global__ void __launch_bounds__(256) k_filter_batch(const uint4* __restrict__ boxes, const uint4* __restrict__ sboxes,
+                                                      long long ntiles, long long nsuper,
                                                       const float* __restrict__ lutf_all, QState* st_all, int B,
                                                       uint2* __restrict__ tlist_all)
 {
@@ -165,37 +203,46 @@ __global__ void __launch_bounds__(256) k_filter_batch(const unsigned char* __res
     if (threadIdx.x < nq) thr_s[threadIdx.x] = slack_up(ld_bsf(st_all + b0 + threadIdx.x));
     __syncthreads();
     const int lane = threadIdx.x & 31, r = lane & 15, h = lane >> 4;
-    for (long long t0 = (long long)blockIdx.x * blockDim.x; t0 < ntiles; t0 += (long long)gridDim.x * blockDim.x) {
-        const long long t = t0 + threadIdx.x;
-        const bool valid = t < ntiles;
-        uint4 mn = make_uint4(0, 0, 0, 0), mx = make_uint4(0, 0, 0, 0);
-        if (valid) {
-            mn = rotate_bytes(*reinterpret_cast<const uint4*>(boxes + t * 32), r);
-            mx = rotate_bytes(*reinterpret_cast<const uint4*>(boxes + t * 32 + 16), r);
+    const int wpb = blockDim.x >> 5;
+    for (long long s0 = ((long long)blockIdx.x * wpb + (threadIdx.x >> 5)) * 32; s0 < nsuper;
+         s0 += (long long)gridDim.x * wpb * 32) {
+        const long long S = s0 + lane;
+        const bool sval = S < nsuper;
+        uint4 smn = make_uint4(0, 0, 0, 0), smx = make_uint4(0, 0, 0, 0);
+        if (sval) {
+            smn = rotate_bytes(sboxes[2 * S], r);
+            smx = rotate_bytes(sboxes[2 * S + 1], r);
         }
-        const unsigned a[4] = {mn.x, mn.y, mn.z, mn.w}, c[4] = {mx.x, mx.y, mx.z, mx.w};
         for (int qq = 0; qq < nq; ++qq) {
             const float* T = lutf_s + qq * kLutF + 16 * h;
-            float acc = 0.0f;
-#pragma unroll
-            for (int s = 0; s < 16; ++s) {
-                const int sg = (s + r) & 15;
-                const unsigned vmin = (a[s >> 2] >> (8 * (s & 3))) & 255u, vmax = (c[s >> 2] >> (8 * (s & 3))) & 255u;
-                const unsigned zl = zlo[qq][sg], zh = zhi[qq][sg];
-                const unsigned v = vmax < zl ? vmax : vmin;
-                const float term = T[v * 32 + sg];
-                acc = __fadd_rd(acc, (vmin <= zh && vmax >= zl) ? 0.0f : term);
-            }
-            const bool keep = valid && acc <= thr_s[qq];
-            const unsigned msk = __ballot_sync(0xffffffffu, keep);
-            if (msk) {
-                QState* st = st_all + b0 + qq;
-                unsigned base = 0;
-                if (lane == 0) base = atomicAdd(&st->tile_count, (unsigned)__popc(msk));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (keep)
-                    tlist_all[(size_t)(b0 + qq) * ntiles + base + __popc(msk & ((1u << lane) - 1))] =
-                        make_uint2((unsigned)t, __float_as_uint(acc));
+            const float thr = thr_s[qq];
+            const bool skeep = sval && box_lb(smn, smx, T, zlo[qq], zhi[qq], r) <= thr;
+            unsigned m = __ballot_sync(0xffffffffu, skeep);
+            QState* st = st_all + b0 + qq;
+            while (m) {
+                const int S1 = __ffs(m) - 1;
+                m &= m - 1;
+                const int S2 = m ? __ffs(m) - 1 : -1;
+                if (m) m &= m - 1;
+                const int mine = h == 0 ? S1 : S2;
+                const long long t = mine >= 0 ? (s0 + mine) * kSuperTiles + r : ntiles;
+                const bool tval = t < ntiles;
+                bool keep = false;
+                float lb = 0.0f;
+                if (tval) {
+                    const uint4 mn = rotate_bytes(boxes[2 * t], r), mx = rotate_bytes(boxes[2 * t + 1], r);
+                    lb = box_lb(mn, mx, T, zlo[qq], zhi[qq], r);
+                    keep = lb <= thr;
+                }
+                const unsigned msk = __ballot_sync(0xffffffffu, keep);
+                if (msk) {
+                    unsigned base = 0;
+                    if (lane == 0) base = atomicAdd(&st->tile_count, (unsigned)__popc(msk));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (keep)
+                        tlist_all[(size_t)(b0 + qq) * ntiles + base + __popc(msk & ((1u << lane) - 1))] =
+                            make_uint2((unsigned)t, __float_as_uint(lb));
+                }
             }
         }
     }
