@@ -28,7 +28,8 @@ struct QState {
     unsigned refined;       // real distances started
     unsigned abandoned;     // real distances abandoned early
     unsigned done;          // CTAs of the refine stage that finished (last one resolves)
-    unsigned tile_count;    // tiles whose box bound <= BSF0 * (1 + eps) (scanned)
+    unsigned tile_count;    // tiles whose box bound <= BSF0 * (1 + eps) (batch ED: those <= BSF0 / 2)
+    unsigned tile_back;     // batch ED: the listed tiles with box bound > BSF0 / 2 (list back end)
     unsigned exact;         // ED: fp32 distances over the raw rows (quantised bound passed)
     unsigned tiles_scanned; // batch ED: tiles whose box bound still passed the CURRENT BSF
     unsigned coarse_count;  // series whose cardinality-16 bound passed (fine bound evaluated)
@@ -59,6 +60,7 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->abandoned = 0;
     st->done = 0;
     st->tile_count = 0;
+    st->tile_back = 0;
     st->exact = 0;
     st->tiles_scanned = 0;
     st->next_tile = 0;

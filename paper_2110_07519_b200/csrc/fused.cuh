@@ -234,13 +234,24 @@ __global__ void __launch_bounds__(256) k_filter_batch(const uint4* __restrict__ 
                     lb = box_lb(mn, mx, T, zlo[qq], zhi[qq], r);
                     keep = lb <= thr;
                 }
-                const unsigned msk = __ballot_sync(0xffffffffu, keep);
-                if (msk) {
-                    unsigned base = 0;
-                    if (lane == 0) base = atomicAdd(&st->tile_count, (unsigned)__popc(msk));
-                    base = __shfl_sync(0xffffffffu, base, 0);
-                    if (keep)
-                        tlist_all[(size_t)(b0 + qq) * ntiles + base + __popc(msk & ((1u << lane) - 1))] =
+                // best-first in two bins: tiles with bound <= thr / 2 fill the list from the
+                // front, the others from the back; the fused kernel hands out the front first
+                const bool near = lb <= 0.5f * thr;
+                const unsigned mf = __ballot_sync(0xffffffffu, keep && near);
+                const unsigned mb = __ballot_sync(0xffffffffu, keep && !near);
+                if (mf | mb) {
+                    unsigned basef = 0, baseb = 0;
+                    if (lane == 0) {
+                        if (mf) basef = atomicAdd(&st->tile_count, (unsigned)__popc(mf));
+                        if (mb) baseb = atomicAdd(&st->tile_back, (unsigned)__popc(mb));
+                    }
+                    basef = __shfl_sync(0xffffffffu, basef, 0);
+                    baseb = __shfl_sync(0xffffffffu, baseb, 0);
+                    uint2* tl = tlist_all + (size_t)(b0 + qq) * ntiles;
+                    if (keep && near)
+                        tl[basef + __popc(mf & ((1u << lane) - 1))] = make_uint2((unsigned)t, __float_as_uint(lb));
+                    if (keep && !near)
+                        tl[ntiles - 1 - (baseb + __popc(mb & ((1u << lane) - 1)))] =
                             make_uint2((unsigned)t, __float_as_uint(lb));
                 }
             }
@@ -367,7 +378,7 @@ __device__ void fused_finalise(const QState* st, long long N, long long row_begi
         s->lbk = 0;
         s->refined = st->refined;
         s->exact = st->exact;
-        s->listed = st->tile_count;
+        s->listed = st->tile_count + st->tile_back;
         s->coarse = st->coarse_count;
         s->abandoned = s->refined - s->exact;
         s->near = st->near_count;
@@ -471,7 +482,8 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
     int b = (int)(blockIdx.x % (unsigned)B);
     for (int visited = 0; visited < B; ++visited, b = (b + 1 == B ? 0 : b + 1)) {
         QState* st = st_all + b;
-        const unsigned count = *(volatile unsigned*)&st->tile_count;
+        const unsigned c0 = *(volatile unsigned*)&st->tile_count;   // front bin
+        const unsigned count = c0 + *(volatile unsigned*)&st->tile_back;
         if (threadIdx.x == 0) s_has = *(volatile unsigned*)&st->next_tile * 2u < count;
         __syncthreads();
         const bool has = s_has;
@@ -496,14 +508,16 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
         k_next = __shfl_sync(0xffffffffu, k_next, 0);
         while (k_next < count) {
             const unsigned k0 = k_next;
-            const uint2 te0 = tl[k0];
-            const uint2 te1 = k0 + 1 < count ? tl[k0 + 1] : make_uint2(0u, 0u);
+            // list position of claim k: the front bin, then the back bin from its far end
+            auto at = [&](unsigned k) { return tl[k < c0 ? k : (unsigned)ntiles - 1u - (k - c0)]; };
+            const uint2 te0 = at(k0);
+            const uint2 te1 = k0 + 1 < count ? at(k0 + 1) : make_uint2(0u, 0u);
             // claim the following pair now and prefetch its tiles into L2
             if (lane == 0) {
                 k_next = atomicAdd(&st->next_tile, 1u) * 2u;
                 const float pthr = slack_up(ld_bsf(st));
                 for (unsigned kk = k_next; kk < min(k_next + 2u, count); ++kk) {
-                    const uint2 tn = tl[kk];
+                    const uint2 tn = at(kk);
                     if (__uint_as_float(tn.y) <= pthr)  // not already box-pruned
                         prefetch_l2_bulk(tiles + (long long)tn.x * (MESSI_TILE_BYTES / 16), MESSI_TILE_BYTES);
                 }
