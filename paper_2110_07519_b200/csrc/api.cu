@@ -33,7 +33,7 @@ struct Slot {
     QState* st = nullptr;
     float *lut = nullptr, *tab = nullptr, *U = nullptr, *L = nullptr;  // tab: 64 KB scan table
     uint2* cand = nullptr;    // scan survivors (sorted position, 8-bit LB)
-    uint2* list2 = nullptr;   // DTW: LB_Keogh survivors (id, LBK)  [lazy]
+    uint4* list2 = nullptr;   // DTW: LB_Keogh survivors (id, LBK, LBK of the first window, 0)  [lazy]
     unsigned* tlist = nullptr;  // tiles surviving the box filter
     NearEntry* near = nullptr;
     cudaEvent_t ev_seed = nullptr, ev_scan = nullptr, ev_done = nullptr;
@@ -607,7 +607,7 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     {
         ProfScope ps(idx, K_LBK, rs);
         k_lbk_filter<<<refine_grid(idx, 2048), 256, lbk_smem(n), rs>>>(sl.cand, idx->perm, idx->rows, n, sl.U, sl.L,
-                                                                       sl.st, sl.list2);
+                                                                       reach, sl.st, sl.list2);
         LAUNCHED(idx);
     }
     {

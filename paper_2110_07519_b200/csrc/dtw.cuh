@@ -206,8 +206,9 @@ struct DtwThread {
         return d * d;
     }
 
-    __device__ __forceinline__ void start(const float* __restrict__ c, int n, const float* __restrict__ U,
-                                          const float* __restrict__ L)
+    // head_lbk: the LB_Keogh terms of columns 0 .. R+3 (the first window), summed by the
+    // filter kernel (any summation order: the tail bound carries 2^-10 margins)
+    __device__ __forceinline__ void start(const float* __restrict__ c, int n, float head_lbk)
     {
 #pragma unroll
         for (int d = 0; d <= W; ++d) D[d] = INFINITY;
@@ -219,13 +220,12 @@ struct DtwThread {
             float4 v = block(c, n, b);
             f[4 * b] = v.x; f[4 * b + 1] = v.y; f[4 * b + 2] = v.z; f[4 * b + 3] = v.w;
         }
-        seen = 0.0f;
+        seen = head_lbk;
         seen_lo = 0.0f;
 #pragma unroll
         for (int e = 0; e < CW; ++e) {
             const int j = e - R;
             cw[e] = j < 0 ? INFINITY : f[j];
-            if (j >= 0 && j < n) seen += lbk_term(f[j], U[j], L[j]);
         }
         hold = block(c, n, (R + 4) >> 2);
         h2 = block(c, n, ((R + 4) >> 2) + 1);

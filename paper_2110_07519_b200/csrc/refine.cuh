@@ -111,10 +111,11 @@ struct Best { double d; long long id; };
 // DTW step 1 (Alg. 10 line LB_Keogh): the scan's candidates (sorted position,
 // envelope-PAA bound) whose bound still does not exceed the BSF get the raw LB_Keogh
 // against the query envelope, four rows in flight per warp; survivors go to list2 as
-// (row id, LBK).
+// (row id, LBK, LBK of columns 0 .. reach+3 -- the columns the DP's first window holds).
 __global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ cand, const unsigned* __restrict__ perm,
                                                     const float* __restrict__ rows, int n, const float* __restrict__ U_g,
-                                                    const float* __restrict__ L_g, QState* st, uint2* __restrict__ list2)
+                                                    const float* __restrict__ L_g, int reach, QState* st,
+                                                    uint4* __restrict__ list2)
 {
     extern __shared__ __align__(16) float env[];
     float* U = env;
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ ca
         const unsigned rid = ok ? perm[e.x] : 0u;
         unsigned todo = __ballot_sync(0xffffffffu, ok);
         unsigned passmask = 0;
-        float mylbk = 0.0f;
+        float mylbk = 0.0f, myhead = 0.0f;
         while (todo) {
             int src[kRefineGroup];
             unsigned id[kRefineGroup];
@@ -144,9 +145,9 @@ __global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ ca
                 todo &= todo - 1;
                 id[g] = __shfl_sync(0xffffffffu, rid, src[g]);
             }
-            float acc[kRefineGroup];
+            float acc[kRefineGroup], head[kRefineGroup];
 #pragma unroll
-            for (int g = 0; g < kRefineGroup; ++g) acc[g] = 0.0f;
+            for (int g = 0; g < kRefineGroup; ++g) acc[g] = head[g] = 0.0f;
 #pragma unroll 2
             for (int j = lane * 4; j < n; j += 128) {
                 const float4 uv = *reinterpret_cast<const float4*>(U + j);
@@ -164,15 +165,17 @@ __global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ ca
                     for (int k = 0; k < 4; ++k) {
                         float d = c[k] > u[k] ? c[k] - u[k] : (c[k] < l[k] ? c[k] - l[k] : 0.0f);
                         acc[g] = fmaf(d, d, acc[g]);
+                        if (j + k <= reach + 3) head[g] = fmaf(d, d, head[g]);
                     }
                 }
             }
 #pragma unroll
             for (int g = 0; g < kRefineGroup; ++g) {
                 acc[g] = warp_sum(acc[g]);
+                head[g] = warp_sum(head[g]);
                 if (gok[g] && acc[g] <= thr) {
                     passmask |= 1u << src[g];
-                    if (lane == src[g]) mylbk = acc[g];
+                    if (lane == src[g]) { mylbk = acc[g]; myhead = head[g]; }
                 }
             }
         }
@@ -181,7 +184,8 @@ __global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ ca
             if (lane == 0) base = atomicAdd(&st->list2_count, (unsigned)__popc(passmask));
             base = __shfl_sync(0xffffffffu, base, 0);
             if (passmask & (1u << lane))
-                list2[base + __popc(passmask & ((1u << lane) - 1))] = make_uint2(rid, __float_as_uint(mylbk));
+                list2[base + __popc(passmask & ((1u << lane) - 1))] =
+                    make_uint4(rid, __float_as_uint(mylbk), __float_as_uint(myhead), 0u);
         }
     }
 }
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ ca
 template <int R>
 __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
                                                     const float* __restrict__ U_g, const float* __restrict__ L_g,
-                                                    const uint2* __restrict__ list2, QState* st, NearEntry* near)
+                                                    const uint4* __restrict__ list2, QState* st, NearEntry* near)
 {
     extern __shared__ __align__(16) float dsm[];
     const int npad = (n + 3) & ~3;
@@ -209,10 +213,15 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
     bool have = k < total;
     const float* c = rows;
     unsigned id = 0, refined = 0, abandoned = 0, steps = 0, skipped = 0;
-    float lbk_total = 0.0f;
-    // the lane's next candidate is fetched one candidate ahead and the head of its row
-    // prefetched, so a lane that restarts does not stall its warp on an HBM round trip
-    uint2 nxt = k + nthreads < total ? list2[k + nthreads] : make_uint2(0u, 0u);
+    float lbk_total = 0.0f, head0 = 0.0f;
+    // The lane's next two candidates are fetched ahead (nxt = k + nthreads, nxt2 = k +
+    // 2 nthreads) and the head of the next row prefetched into L1, so a lane that restarts
+    // does not stall its warp on memory round trips.  The BSF is re-read every step, its
+    // load issued before the step's band work and used after it (a stale value is a larger
+    // threshold: safe).
+    const uint4 none = make_uint4(0u, 0u, 0u, 0u);
+    uint4 nxt = k + nthreads < total ? list2[k + nthreads] : none;
+    uint4 nxt2 = k + 2 * nthreads < total ? list2[k + 2 * nthreads] : none;
     auto prefetch_row = [&](unsigned rid) {
         const char* pr = reinterpret_cast<const char*>(rows + (long long)rid * n);
         asm volatile("prefetch.global.L1 [%0];" ::"l"(pr));
@@ -223,51 +232,49 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
     // a candidate whose LB_Keogh already exceeds the current threshold is skipped unstarted
     auto admit = [&](float lbk) { return lbk * 0.9990234375f <= thr; };
     if (have) {
-        const uint2 e = list2[k];
+        const uint4 e = list2[k];
         id = e.x;
         lbk_total = __uint_as_float(e.y);
         c = rows + (long long)id * n;
-        dp.start(c, n, U, L);
+        dp.start(c, n, __uint_as_float(e.z));
         ++refined;
     }
     while (__any_sync(0xffffffffu, have)) {
         if (have) {
+            const unsigned bsf_bits = *(volatile const unsigned*)&st->bsf_bits;  // consumed after the step
             const float rowmin = dp.step4(c, n, q_s, U, L);
             ++steps;
+            thr = fminf(thr, slack_up(__uint_as_float(bsf_bits)));
             const float tail = fmaxf(0.0f, lbk_total * 0.9990234375f - dp.seen_lo * 1.0009765625f);
             const float bound = (rowmin + tail) * 0.9990234375f;
             bool done = false;
-            if (bound > thr) {
-                thr = slack_up(ld_bsf(st));
-                if (bound > thr) { done = true; ++abandoned; }
-            }
+            if (bound > thr) { done = true; ++abandoned; }
             if (!done && dp.i >= n) {
                 done = true;
                 const float d = dp.result();
-                thr = slack_up(ld_bsf(st));
                 if (d <= thr) {
                     bsf_update(st, d);
                     append_near(st, near, id, d);
+                    thr = fminf(thr, slack_up(d));
                 }
             }
             if (done) {
-                thr = slack_up(ld_bsf(st));
                 for (;;) {
                     k += nthreads;
                     have = k < total;
                     if (!have) break;
                     id = nxt.x;
                     lbk_total = __uint_as_float(nxt.y);
-                    if (k + nthreads < total) {
-                        nxt = list2[k + nthreads];
-                        if (admit(__uint_as_float(nxt.y))) prefetch_row(nxt.x);
-                    }
+                    head0 = __uint_as_float(nxt.z);
+                    nxt = nxt2;
+                    if (k + 2 * nthreads < total) nxt2 = list2[k + 2 * nthreads];
+                    if (k + nthreads < total && admit(__uint_as_float(nxt.y))) prefetch_row(nxt.x);
                     if (admit(lbk_total)) break;
                     ++skipped;
                 }
                 if (have) {
                     c = rows + (long long)id * n;
-                    dp.start(c, n, U, L);
+                    dp.start(c, n, head0);
                     ++refined;
                 }
             }
@@ -295,7 +302,7 @@ __device__ __forceinline__ void stage_row(float* dst, const float* __restrict__ 
 // fp32 anti-diagonal wavefront (dtw_warp<float>) over the row staged in shared memory.
 // Per-warp shared memory: n floats of row + 3n floats of anti-diagonals.
 __global__ void k_refine_dtw_warp(const float* __restrict__ rows, int n, int reach, const float* __restrict__ q_g,
-                                  const uint2* __restrict__ list2, QState* st, NearEntry* near)
+                                  const uint4* __restrict__ list2, QState* st, NearEntry* near)
 {
     extern __shared__ __align__(16) float dsm[];
     const int npad = (n + 3) & ~3;
@@ -461,7 +468,7 @@ __global__ void k_debug_dist(const float* __restrict__ rows, int n, int reach, c
                     v = INFINITY;
                     if (lane == 0) {
                         DtwThread<(R >= 0 ? R : 0)> dp;
-                        dp.start(c, n, U, L);
+                        dp.start(c, n, 0.0f);
                         while (dp.i < n) dp.step4(c, n, q_s, U, L);
                         v = dp.result();
                     }
