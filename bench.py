@@ -260,6 +260,30 @@ def run_arm(cfg, args, world, rank, dev, stream, time_steps, warmup):
     return out
 
 
+# DTW band DP roofline: a cell costs one FADD + one FFMA on the FMA pipe (plus
+# an FMNMX3 on the ALU pipe); the FMA pipe retires one warp instruction per 2 cycles per SM
+# sub-partition, so the fp32 cell peak is 148 SMs x 4 SMSPs x 32 lanes / (2 x 2 cycles) x clock.
+def dtw_cell_peak(sm_mhz=1965.0, sms=148):
+    return sms * 4 * 32 / 4.0 * sm_mhz * 1e6
+
+
+def dtw_roofline(run, steps):
+    st = run["stats"]
+    cells = sum(s["dtw_cells"] for s in st) * steps
+    ms, nl = run["prof"]["refine"]
+    if ms <= 0:
+        return None
+    achieved = cells / (ms / 1e3)
+    peak = dtw_cell_peak(run["clocks"].get("sm_max_mhz", 1965.0) or 1965.0)
+    lbk_ms, _ = run["prof"]["lbk"]
+    lbk_bytes = sum(4 * run["n"] * s["candidates"] + 16 * s["lbk_pass"] for s in st) * steps
+    return {"bound": "alu", "kernel": "k_refine_dtw<R> (fp32 banded DTW, one thread per candidate)",
+            "achieved": achieved, "peak": peak, "unit": "cells/s", "frac": achieved / peak,
+            "peak_source": "derived: FMA pipe 1 warp-instr / 2 cycles / SMSP, 2 FMA-pipe instr per cell",
+            "lbk_filter": {"bound": "hbm", "achieved_gbs": lbk_bytes / (lbk_ms / 1e3) / 1e9 if lbk_ms > 0 else None,
+                           "bytes_per_query": lbk_bytes / steps / len(st)}}
+
+
 def arm_config(cfg, args, world, nq):
     """The workload description both arms print (same keys, same values)."""
     nl = cfg["N"] // world
@@ -381,6 +405,8 @@ def ours(args):
                                              "abandoned", "near_best", "dtw_cells", "exact", "tiles_listed", "coarse",
                                              "seed_d2", "bsf_d2")},
     }
+    if args.mode == "dtw":
+        line["roofline"] = dtw_roofline(main, K)
     if args.mode == "ed" and not args.no_dtw:
         c4 = dict(CONFIGS["c4"])
         k4 = max(1, min(2, K))
@@ -393,8 +419,8 @@ def ours(args):
                        "kernel_ms_per_step": {k: v[0] / k4 for k, v in d["prof"].items()},
                        "stats_mean": {k: dm(k) for k in ("lb_computed", "tiles_scanned", "candidates", "lbk_pass",
                                                          "refined", "abandoned", "near_best", "dtw_cells",
-                                                         "seed_d2", "bsf_d2")},
-                       "gpu_launches": d["launches"]}
+                                                         "coarse", "seed_d2", "bsf_d2")},
+                       "gpu_launches": d["launches"], "roofline": dtw_roofline(d, k4)}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, args, dev, "ED" if cfg["reach"] is None else "DTW")
     if rank == 0:

@@ -36,14 +36,15 @@ struct Slot {
     uint4* list2 = nullptr;   // DTW: LB_Keogh survivors (id, LBK, LBK of the first window, 0)  [lazy]
     unsigned* tlist = nullptr;  // tiles surviving the box filter
     NearEntry* near = nullptr;
-    cudaEvent_t ev_seed = nullptr, ev_scan = nullptr, ev_done = nullptr;
+    cudaEvent_t ev_seed = nullptr, ev_scan = nullptr, ev_lbk = nullptr, ev_done = nullptr;
 };
 
 struct messi_index {
     int device = 0;
     cudaStream_t stream = nullptr;  // the caller's stream ("main": scans)
     cudaStream_t side = nullptr;    // library-owned: seeds
-    cudaStream_t rstr = nullptr;    // library-owned: refine / resolve
+    cudaStream_t rstr = nullptr;    // library-owned: ED sub-batches; DTW LB_Keogh filter
+    cudaStream_t dstr = nullptr;    // library-owned: DTW refine / resolve (overlaps the next query's filter)
     cudaEvent_t ev_fork = nullptr;
     int n = 0, window = 2000, keep_paa = 0;
     long long N = 0, ntiles = 0, row_begin = 0;
@@ -268,6 +269,7 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
             return bail(s);
         if (cudaEventCreateWithFlags(&sl.ev_seed, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&sl.ev_scan, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sl.ev_lbk, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&sl.ev_done, cudaEventDisableTiming) != cudaSuccess)
             return bail(fail(MESSI_ECUDA, "event creation failed"));
     }
@@ -277,6 +279,7 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     if (getenv("MESSI_PRIO_EQUAL")) prio_hi = 0;
     if (cudaStreamCreateWithPriority(&idx->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&idx->rstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&idx->dstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&idx->ev_fork, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(MESSI_ECUDA, "stream creation failed"));
 
@@ -346,6 +349,7 @@ extern "C" void messi_free(messi_index* idx)
     cudaSetDevice(idx->device);
     if (idx->side) cudaStreamSynchronize(idx->side);
     if (idx->rstr) cudaStreamSynchronize(idx->rstr);
+    if (idx->dstr) cudaStreamSynchronize(idx->dstr);
     if (idx->stream) cudaStreamSynchronize(idx->stream);
     else cudaDeviceSynchronize();
     void* ptrs[] = {idx->tiles, idx->sym8, idx->boxes, idx->sboxes, idx->paa, idx->skey, idx->perm, idx->beta32, idx->lo_w,
@@ -361,13 +365,14 @@ extern "C" void messi_free(messi_index* idx)
         void* sp[] = {sl.st, sl.lut, sl.tab, sl.U, sl.L, sl.cand, sl.list2, sl.near, sl.tlist};
         for (void* p : sp)
             if (p) cudaFree(p);
-        cudaEvent_t es[] = {sl.ev_seed, sl.ev_scan, sl.ev_done};
+        cudaEvent_t es[] = {sl.ev_seed, sl.ev_scan, sl.ev_lbk, sl.ev_done};
         for (cudaEvent_t e : es)
             if (e) cudaEventDestroy(e);
     }
     if (idx->ev_fork) cudaEventDestroy(idx->ev_fork);
     if (idx->side && idx->side != idx->stream) cudaStreamDestroy(idx->side);
     if (idx->rstr && idx->rstr != idx->stream) cudaStreamDestroy(idx->rstr);
+    if (idx->dstr && idx->dstr != idx->stream) cudaStreamDestroy(idx->dstr);
     for (auto& e : idx->evs) {
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
@@ -385,6 +390,7 @@ static messi_status sync_all(messi_index* idx)
     CK(cudaStreamSynchronize(idx->stream));
     CK(cudaStreamSynchronize(idx->side));
     CK(cudaStreamSynchronize(idx->rstr));
+    CK(cudaStreamSynchronize(idx->dstr));
     return MESSI_OK;
 }
 
@@ -452,15 +458,18 @@ static messi_status fork_streams(messi_index* idx)
         if (idx->side != idx->stream) {
             cudaStreamSynchronize(idx->side);
             cudaStreamSynchronize(idx->rstr);
+            cudaStreamSynchronize(idx->dstr);
             cudaStreamDestroy(idx->side);
             cudaStreamDestroy(idx->rstr);
-            idx->side = idx->rstr = idx->stream;
+            cudaStreamDestroy(idx->dstr);
+            idx->side = idx->rstr = idx->dstr = idx->stream;
         }
         return MESSI_OK;
     }
     CK(cudaEventRecord(idx->ev_fork, idx->stream));
     CK(cudaStreamWaitEvent(idx->side, idx->ev_fork, 0));
     CK(cudaStreamWaitEvent(idx->rstr, idx->ev_fork, 0));
+    CK(cudaStreamWaitEvent(idx->dstr, idx->ev_fork, 0));
     return MESSI_OK;
 }
 
@@ -610,6 +619,11 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
                                                                        reach, sl.st, sl.list2);
         LAUNCHED(idx);
     }
+    // the refine and the resolve run on their own stream: the LB_Keogh filter of the next
+    // query (bandwidth-bound) overlaps this query's band DP (latency / ALU-bound)
+    CK(cudaEventRecord(sl.ev_lbk, rs));
+    rs = idx->dstr;
+    CK(cudaStreamWaitEvent(rs, sl.ev_lbk, 0));
     {
         ProfScope ps(idx, K_REFINE, rs);
         bool launched = false;
