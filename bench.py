@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=4_000_000, help="row sample of the oracle timing")
     ap.add_argument("--cpu-queries", type=int, default=32, help="queries of the oracle timing sample")
     ap.add_argument("--window", type=int, default=0, help="approximate-search window (0: library default 2000)")
+    ap.add_argument("--no-share-bsf", action="store_true",
+                    help="N > 1: do not link the shards (no best-so-far sharing over peer memory)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: host-side merge; lets several ranks share one GPU)")
     return ap.parse_args()
@@ -186,6 +188,9 @@ def run_arm(cfg, args, world, rank, dev, stream, time_steps, warmup):
         t0.record(stream)
         idx = M.Index(X, row_begin=row_begin, stream=stream, window=args.window)
         t1.record(stream)
+        if world > 1 and not args.no_share_bsf:
+            from paper_2110_07519_b200.dist import link_shards
+            link_shards(idx)  # shards share each query's best-so-far over peer memory (NVLink)
         torch.cuda.synchronize()
         build_ms = t0.elapsed_time(t1)
         nq = Q.shape[0]

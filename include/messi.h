@@ -102,6 +102,26 @@ messi_status messi_query_ed_batch(messi_index* idx, const float* queries_dev, in
 messi_status messi_query_dtw_batch(messi_index* idx, const float* queries_dev, int32_t nq, int32_t reach,
                                    messi_result* results_dev, messi_stats* stats_dev);
 
+/* ---- shards of one row-sharded collection (north_star: "each GPU returns a local (dist,
+ * id) minimum") -------------------------------------------------------------------------
+ * Linked indexes share each query's best-so-far while the batched ED kernels run: every new
+ * local best is also raised into the peers' per-query states (atomicMax of an epoch-tagged
+ * key, over NVLink peer memory between GPUs), and every shard prunes with the smallest of
+ * them.  Exactness is unchanged: a shard may then prune its own rows down to "no row within
+ * the global BSF" (its local answer is then (inf, -1)), and the cross-shard lexicographic
+ * min of the local answers (dist.py) is the global one.  Linked shards must make the same
+ * sequence of ED batch calls (the epoch counts launch groups); the DTW path ignores links.
+ *
+ * messi_batch_state_ipc: the CUDA IPC handle (64 bytes into handle_out) of this index's
+ *   per-query state array `set` (0 or 1).
+ * messi_link_peers_ipc: open the handles of npeers (<= 8) peers, handles = npeers x 2 x 64
+ *   bytes (peer-major, set 0 then set 1), replacing earlier links; npeers = 0 unlinks.
+ * messi_link_peers_local: the same for indexes of this process (same or peer-accessible
+ *   GPUs; used by the tests to emulate shards on one GPU). */
+messi_status messi_batch_state_ipc(messi_index* idx, int32_t set, void* handle_out);
+messi_status messi_link_peers_ipc(messi_index* idx, const void* handles, int32_t npeers);
+messi_status messi_link_peers_local(messi_index* idx, messi_index* const* peers, int32_t npeers);
+
 /* Release everything the library allocated for idx.  NULL-safe. */
 void messi_free(messi_index* idx);
 

@@ -69,6 +69,13 @@ struct messi_index {
         float *lutc = nullptr, *lutx = nullptr, *lutf = nullptr;
         uint2* btlist = nullptr;
     } bset[2];
+    // shards sharing each query's best-so-far (PeerSet): their per-set state arrays, the
+    // IPC mappings to close, and the launch epoch (identical on every shard for the same
+    // sequence of calls)
+    QState* peer_st[2][MESSI_MAX_PEERS] = {};
+    void* peer_ipc[2][MESSI_MAX_PEERS] = {};
+    int npeers = 0;
+    unsigned epoch = 0;
     int fused_grid = 0;
     // per-query scratch
     Slot slot[2];
@@ -356,6 +363,9 @@ extern "C" void messi_free(messi_index* idx)
                     idx->hi_w,  idx->qbuf,  idx->res1, idx->stats1, idx->rows8, idx->meta8};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (auto& row : idx->peer_ipc)
+        for (void* p : row)
+            if (p) cudaIpcCloseMemHandle(p);
     for (auto& bs : idx->bset) {
         void* bp[] = {bs.bst, bs.lutc, bs.lutx, bs.lutf, bs.btlist};
         for (void* p : bp)
@@ -523,6 +533,7 @@ static messi_status ensure_batch_buffers(messi_index* idx)
     if (idx->bset[0].bst) return MESSI_OK;
     for (auto& bs : idx->bset) {
         TRY(dalloc(&bs.bst, kBatchMax));
+        CK(cudaMemset(bs.bst, 0, sizeof(QState) * kBatchMax));  // gbsf = 0: no epoch
         TRY(dalloc(&bs.lutc, (size_t)kBatchMax * MESSI_W * MESSI_CARD));
         TRY(dalloc(&bs.lutx, (size_t)kBatchMax * kLutX));
         TRY(dalloc(&bs.lutf, (size_t)kBatchMax * kLutF));
@@ -540,6 +551,12 @@ static messi_status ensure_batch_buffers(messi_index* idx)
 static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSet& bs, cudaStream_t st, const float* q, int B,
                                     messi_result* res, messi_stats* stats)
 {
+    const int set = (int)(&bs - idx->bset);
+    PeerSet peers;
+    for (int i = 0; i < MESSI_MAX_PEERS; ++i) peers.st[i] = idx->peer_st[set][i];
+    peers.n = idx->npeers;
+    peers.epoch = ++idx->epoch;
+    if (peers.epoch == 0) peers.epoch = ++idx->epoch;  // epoch 0 means unlinked
     const int n = idx->n;
     const size_t qsm = (size_t)((n + 3) & ~3) * sizeof(float);
     const int len = (int)(idx->window < idx->N ? idx->window : idx->N);
@@ -549,7 +566,7 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
                                               bs.lutc, bs.lutx, bs.lutf, bs.bst);
         LAUNCHED(idx);
         dim3 sg((unsigned)((len + kSeedRowsPerCta - 1) / kSeedRowsPerCta), (unsigned)B);
-        k_seed_batch<<<sg, 256, qsm, st>>>(q, n, idx->rows, idx->perm, bs.bst);
+        k_seed_batch<<<sg, 256, qsm, st>>>(q, n, idx->rows, idx->perm, bs.bst, peers);
         LAUNCHED(idx);
         const long long nsuper = (idx->ntiles + kSuperTiles - 1) / kSuperTiles;
         const int npairs = (B + kFilterQ - 1) / kFilterQ;
@@ -558,14 +575,15 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
         if (fx > fcap) fx = fcap;
         dim3 fg((unsigned)fx, (unsigned)npairs);
         k_filter_batch<<<fg, 256, kFilterQ * kLutF * 4, st>>>(reinterpret_cast<const uint4*>(idx->boxes), idx->sboxes,
-                                                              idx->ntiles, nsuper, bs.lutf, bs.bst, B, bs.btlist);
+                                                              idx->ntiles, nsuper, bs.lutf, bs.bst, B, bs.btlist,
+                                                              peers.epoch);
         LAUNCHED(idx);
     }
     {
         ProfScope ps(idx, K_SCAN, st);
         k_scan_refine_ed<<<idx->fused_grid, 32 * kFusedWarps, fused_smem(n), st>>>(
             idx->tiles, idx->sym8, idx->ntiles, idx->N, n, q, bs.lutx, bs.btlist, bs.bst, B, idx->rows8,
-            idx->meta8, idx->q8_omd, idx->perm, idx->rows);
+            idx->meta8, idx->q8_omd, idx->perm, idx->rows, peers);
         LAUNCHED(idx);
         k_finalise_batch<<<(B + 127) / 128, 128, 0, st>>>(bs.bst, B, idx->N, idx->row_begin, res, stats);
         LAUNCHED(idx);
@@ -733,6 +751,84 @@ extern "C" messi_status messi_query_dtw_batch(messi_index* idx, const float* que
     for (int i = 0; i < nq; ++i)
         TRY(run_dtw(idx, queries_dev + (size_t)i * idx->n, reach, results_dev + i, stats_dev ? stats_dev + i : nullptr));
     return join_streams(idx);
+}
+
+// ------------------------------------------------------------ shared best-so-far (shards)
+extern "C" messi_status messi_batch_state_ipc(messi_index* idx, int32_t set, void* handle_out)
+{
+    g_err[0] = 0;
+    if (!idx || !handle_out || set < 0 || set > 1) return fail(MESSI_EINVAL, "bad argument");
+    CK(cudaSetDevice(idx->device));
+    TRY(ensure_batch_buffers(idx));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, idx->bset[set].bst));
+    memcpy(handle_out, &h, sizeof h);
+    return MESSI_OK;
+}
+
+static messi_status unlink_peers(messi_index* idx)
+{
+    for (auto& row : idx->peer_ipc)
+        for (void*& p : row)
+            if (p) {
+                CK(cudaIpcCloseMemHandle(p));
+                p = nullptr;
+            }
+    for (auto& row : idx->peer_st)
+        for (QState*& p : row) p = nullptr;
+    idx->npeers = 0;
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_link_peers_ipc(messi_index* idx, const void* handles, int32_t npeers)
+{
+    g_err[0] = 0;
+    if (!idx || npeers < 0 || npeers > MESSI_MAX_PEERS || (npeers && !handles)) return fail(MESSI_EINVAL, "bad argument");
+    CK(cudaSetDevice(idx->device));
+    TRY(sync_all(idx));
+    TRY(ensure_batch_buffers(idx));
+    TRY(unlink_peers(idx));
+    const unsigned char* h = static_cast<const unsigned char*>(handles);
+    for (int i = 0; i < npeers; ++i)
+        for (int set = 0; set < 2; ++set) {
+            cudaIpcMemHandle_t mh;
+            memcpy(&mh, h + ((size_t)i * 2 + set) * sizeof(cudaIpcMemHandle_t), sizeof mh);
+            void* p = nullptr;
+            cudaError_t e = cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
+                unlink_peers(idx);
+                return fail(MESSI_ECUDA, "cudaIpcOpenMemHandle(peer %d, set %d): %s", i, set, cudaGetErrorString(e));
+            }
+            idx->peer_ipc[set][i] = p;
+            idx->peer_st[set][i] = static_cast<QState*>(p);
+        }
+    idx->npeers = npeers;
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_link_peers_local(messi_index* idx, messi_index* const* peers, int32_t npeers)
+{
+    g_err[0] = 0;
+    if (!idx || npeers < 0 || npeers > MESSI_MAX_PEERS || (npeers && !peers)) return fail(MESSI_EINVAL, "bad argument");
+    CK(cudaSetDevice(idx->device));
+    TRY(sync_all(idx));
+    TRY(ensure_batch_buffers(idx));
+    TRY(unlink_peers(idx));
+    for (int i = 0; i < npeers; ++i) {
+        if (!peers[i] || peers[i] == idx) return fail(MESSI_EINVAL, "peer %d is NULL or the index itself", i);
+        if (peers[i]->device != idx->device) {
+            cudaError_t e = cudaDeviceEnablePeerAccess(peers[i]->device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                return fail(MESSI_ECUDA, "peer access %d -> %d: %s", idx->device, peers[i]->device, cudaGetErrorString(e));
+            cudaGetLastError();
+        }
+        CK(cudaSetDevice(peers[i]->device));
+        TRY(ensure_batch_buffers(peers[i]));
+        CK(cudaSetDevice(idx->device));
+        for (int set = 0; set < 2; ++set) idx->peer_st[set][i] = peers[i]->bset[set].bst;
+    }
+    idx->npeers = npeers;
+    return MESSI_OK;
 }
 
 // ------------------------------------------------------------------------ inspection

@@ -9,6 +9,7 @@
 #define MESSI_TILE_ROWS 512        // series per tile (32 blocks x 16 series)
 #define MESSI_TILE_BYTES 4096      // tile: 8 tile rows x 512 B of cardinality-16 pair bytes
 #define MESSI_MAX_N 8192
+#define MESSI_MAX_PEERS 8          // shards that share each query's best-so-far (batched ED)
 
 namespace messi {
 
@@ -37,6 +38,7 @@ struct QState {
     unsigned tiles_done;    // batch ED: listed tiles finished (the warp finishing the last finalises)
     unsigned lock;          // batch ED: guards best_d / best_id
     unsigned long long dtw_cells;  // DTW band cells evaluated in fp32 (refine)
+    unsigned long long gbsf; // batch ED: the epoch-tagged best-so-far of all shards (PeerSet)
     double best_d;          // batch ED: lexicographic min (d64, id) over the fp64 re-ranked rows
     long long best_id;
     unsigned long long qkey;  // query's approximate-search key
@@ -48,6 +50,18 @@ struct QState {
 };
 
 struct NearEntry { unsigned id; float d32; };
+
+// Best-so-far shared with the other shards of a row-sharded collection (batched ED path):
+// the per-query states of up to MESSI_MAX_PEERS peer indexes (peer GPUs' memory reached over
+// NVLink, or other indexes of this process) and the launch epoch every shard tags its
+// updates with.  gbsf = epoch << 32 | (0xffffffff - fp32 bits) is raised with atomicMax: a
+// newer epoch wins, within an epoch the smaller distance wins, and a reader ignores other
+// epochs -- so a peer running a batch ahead can never lower this batch's threshold.
+struct PeerSet {
+    QState* st[MESSI_MAX_PEERS];
+    int n;
+    unsigned epoch;
+};
 
 __device__ __forceinline__ void arm_state(QState* st)
 {
@@ -124,6 +138,28 @@ __device__ __forceinline__ float ld_bsf(const QState* st)
 __device__ __forceinline__ void bsf_update(QState* st, float d)
 {
     if (d >= 0.0f) atomicMin(&st->bsf_bits, __float_as_uint(d));
+}
+
+// The threshold source of the batched ED path: the local BSF, lowered by the shards' shared
+// one when it carries this launch's epoch (epoch 0 = unlinked: gbsf is never written with it).
+__device__ __forceinline__ float ld_bsf_eff(const QState* st, unsigned epoch)
+{
+    const float loc = __uint_as_float(*(volatile const unsigned*)&st->bsf_bits);
+    const unsigned long long g = *(volatile const unsigned long long*)&st->gbsf;
+    if (epoch != 0u && (unsigned)(g >> 32) == epoch) return fminf(loc, __uint_as_float(0xffffffffu - (unsigned)g));
+    return loc;
+}
+
+// A new local best d of query b: the local BSF, and (linked) every peer's shared one.
+__device__ __forceinline__ void bsf_publish(QState* st, const PeerSet& ps, int b, float d)
+{
+    bsf_update(st, d);
+    if (ps.n > 0 && d >= 0.0f) {
+        const unsigned long long key = ((unsigned long long)ps.epoch << 32) | (0xffffffffu - __float_as_uint(d));
+#pragma unroll
+        for (int i = 0; i < MESSI_MAX_PEERS; ++i)
+            if (i < ps.n) atomicMax(&ps.st[i][b].gbsf, key);
+    }
 }
 
 // Symbol of a fp32 PAA value: #{k : beta32_k <= x} over the 255 ascending breakpoints

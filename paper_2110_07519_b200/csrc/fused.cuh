@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) k_prologue_batch(const float* __restrict_
 constexpr int kSeedRowsPerCta = 64;
 __global__ void __launch_bounds__(256) k_seed_batch(const float* __restrict__ queries, int n,
                                                     const float* __restrict__ rows, const unsigned* __restrict__ perm,
-                                                    QState* st_all)
+                                                    QState* st_all, PeerSet ps)
 {
     extern __shared__ __align__(16) float q_s[];
     const int b = blockIdx.y;
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(256) k_seed_batch(const float* __restrict__ qu
         }
     }
     if (lane == 0 && best < INFINITY) {
-        bsf_update(st, best);
+        bsf_publish(st, ps, b, best);
         atomicMin(&st->seed_bits, __float_as_uint(best));
     }
 }
@@ -186,7 +186,7 @@ __global__ void k_superbox(const uint4* __restrict__ boxes, long long ntiles, ui
 __global__ void __launch_bounds__(256) k_filter_batch(const uint4* __restrict__ boxes, const uint4* __restrict__ sboxes,
                                                       long long ntiles, long long nsuper,
                                                       const float* __restrict__ lutf_all, QState* st_all, int B,
-                                                      uint2* __restrict__ tlist_all)
+                                                      uint2* __restrict__ tlist_all, unsigned epoch)
 {
     extern __shared__ __align__(16) float lutf_s[];  // kFilterQ * kLutF
     __shared__ unsigned char zlo[kFilterQ][16], zhi[kFilterQ][16];
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(256) k_filter_batch(const uint4* __restrict__ 
         zlo[qq][s] = st_all[b0 + qq].zlo[s];
         zhi[qq][s] = st_all[b0 + qq].zhi[s];
     }
-    if (threadIdx.x < nq) thr_s[threadIdx.x] = slack_up(ld_bsf(st_all + b0 + threadIdx.x));
+    if (threadIdx.x < nq) thr_s[threadIdx.x] = slack_up(ld_bsf_eff(st_all + b0 + threadIdx.x, epoch));
     __syncthreads();
     const int lane = threadIdx.x & 31, r = lane & 15, h = lane >> 4;
     const int wpb = blockDim.x >> 5;
@@ -297,7 +297,8 @@ __device__ __forceinline__ void best_update(QState* st, double d, long long id)
 // lowers the BSF (atomicMin, Alg. 8's BSF update P:1178-1186) and is re-ranked exactly in
 // fp64 at once (reading R11/R12): the lexicographic min over the re-ranked rows is the answer.
 __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __restrict__ perm,
-                           const float* __restrict__ rows, int n, const float* __restrict__ q_p, QState* st, int lane)
+                           const float* __restrict__ rows, int n, const float* __restrict__ q_p, QState* st,
+                           const PeerSet& ps, int b, int lane)
 {
     while (keep) {
         unsigned id[kRefineGroup];
@@ -335,9 +336,9 @@ __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __res
 #pragma unroll
             for (int g = 0; g < kRefineGroup; ++g) {
                 if (!ok[g]) continue;
-                const float thr = slack_up(ld_bsf(st));
+                const float thr = slack_up(ld_bsf_eff(st, ps.epoch));
                 if (acc[g] <= thr) {
-                    bsf_update(st, acc[g]);
+                    bsf_publish(st, ps, b, acc[g]);
                     const double d64 = ed2_exact_g(q_p, rows + (long long)id[g] * n, n);
                     best_update(st, d64, (long long)id[g]);
                     atomicAdd(&st->near_count, 1u);
@@ -416,7 +417,8 @@ __device__ __forceinline__ void fine_and_refine(long long tile, int m, const uns
                                                 unsigned& ncb, const unsigned char* __restrict__ rows8,
                                                 const float2* __restrict__ meta8, int n, const float* q_p,
                                                 float one_minus_delta, const unsigned* __restrict__ perm,
-                                                const float* __restrict__ rows, QState* st, WarpCounts& wc, int lane)
+                                                const float* __restrict__ rows, QState* st, const PeerSet& ps, int b,
+                                                WarpCounts& wc, int lane)
 {
     for (int i0 = 0; i0 < m; i0 += 32) {
         const bool v = i0 + lane < m;
@@ -428,7 +430,7 @@ __device__ __forceinline__ void fine_and_refine(long long tile, int m, const uns
         }
         float lb = INFINITY;
         if (v) lb = fine_lb(w, lbase, lane);
-        const bool ok = v && lb <= slack_up(ld_bsf(st));
+        const bool ok = v && lb <= slack_up(ld_bsf_eff(st, ps.epoch));
         const unsigned pass = __ballot_sync(0xffffffffu, ok);
         if (!pass) continue;
         if (ok) {
@@ -445,9 +447,10 @@ __device__ __forceinline__ void fine_and_refine(long long tile, int m, const uns
             if (ncb - 32 > (unsigned)lane) cbuf[lane] = rest;
             ncb -= 32;
             __syncwarp();
-            const unsigned keep = q8_bound_pass(0xffffffffu, cp, rows8, meta8, n, q_p, one_minus_delta, st, lane);
+            const unsigned keep =
+                q8_bound_pass(0xffffffffu, cp, rows8, meta8, n, q_p, one_minus_delta, st, ps.epoch, lane);
             wc.exact += __popc(keep);
-            exact_pass(keep, cp, perm, rows, n, q_p, st, lane);
+            exact_pass(keep, cp, perm, rows, n, q_p, st, ps, b, lane);
         }
     }
 }
@@ -467,7 +470,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
     const float* __restrict__ queries, const float* __restrict__ lutx_all, const uint2* __restrict__ tlist_all,
     QState* st_all, int B,
     const unsigned char* __restrict__ rows8, const float2* __restrict__ meta8, float one_minus_delta,
-    const unsigned* __restrict__ perm, const float* __restrict__ rows)
+    const unsigned* __restrict__ perm, const float* __restrict__ rows, PeerSet ps)
 {
     extern __shared__ __align__(16) float smem[];
     float* lut_s = smem;
@@ -515,7 +518,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
             // claim the following pair now and prefetch its tiles into L2
             if (lane == 0) {
                 k_next = atomicAdd(&st->next_tile, 1u) * 2u;
-                const float pthr = slack_up(ld_bsf(st));
+                const float pthr = slack_up(ld_bsf_eff(st, ps.epoch));
                 for (unsigned kk = k_next; kk < min(k_next + 2u, count); ++kk) {
                     const uint2 tn = at(kk);
                     if (__uint_as_float(tn.y) <= pthr)  // not already box-pruned
@@ -528,16 +531,16 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
                 if (k0 + u >= count) break;
                 const uint2 te = u == 0 ? te0 : te1;
                 // warp-uniform decision: lane 0's reading of the BSF
-                const float bthr = __shfl_sync(0xffffffffu, slack_up(ld_bsf(st)), 0);
+                const float bthr = __shfl_sync(0xffffffffu, slack_up(ld_bsf_eff(st, ps.epoch)), 0);
                 if (__uint_as_float(te.y) > bthr) continue;  // box pruned by the current BSF
                 ++wc.tiles;
                 const long long tile = te.x;
                 unsigned short* surv = survb + cur * MESSI_TILE_ROWS;
-                const int m = scan_tile_coarse(tiles, tile, lbase, slack_up(ld_bsf(st)), N, surv, lane);
+                const int m = scan_tile_coarse(tiles, tile, lbase, slack_up(ld_bsf_eff(st, ps.epoch)), N, surv, lane);
                 wc.coarse += m;
                 if (pm)
                     fine_and_refine(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb,
-                                    rows8, meta8, n, q_p, one_minus_delta, perm, rows, st, wc, lane);
+                                    rows8, meta8, n, q_p, one_minus_delta, perm, rows, st, ps, b, wc, lane);
                 // preload the 8-bit words of this tile's first 32 coarse survivors
                 ppos = lane < m ? (unsigned)(tile * MESSI_TILE_ROWS + surv[lane]) : 0u;
                 pw = lane < m ? sym8[ppos] : make_uint4(0, 0, 0, 0);
@@ -548,14 +551,14 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
         }
         if (pm)
             fine_and_refine(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb, rows8,
-                            meta8, n, q_p, one_minus_delta, perm, rows, st, wc, lane);
+                            meta8, n, q_p, one_minus_delta, perm, rows, st, ps, b, wc, lane);
         if (ncb) {  // the query's last fine survivors
             const unsigned cp = (unsigned)lane < ncb ? cbuf[lane] : 0u;
             const unsigned pass = ncb >= 32 ? 0xffffffffu : (1u << ncb) - 1u;
             __syncwarp();
-            const unsigned keep = q8_bound_pass(pass, cp, rows8, meta8, n, q_p, one_minus_delta, st, lane);
+            const unsigned keep = q8_bound_pass(pass, cp, rows8, meta8, n, q_p, one_minus_delta, st, ps.epoch, lane);
             wc.exact += __popc(keep);
-            exact_pass(keep, cp, perm, rows, n, q_p, st, lane);
+            exact_pass(keep, cp, perm, rows, n, q_p, st, ps, b, lane);
             ncb = 0;
         }
         if (lane == 0) {

@@ -28,7 +28,7 @@ constexpr int kRefineGroup = 4;
 // float(0x4B000000 | b) = 2^23 + b.
 __device__ __forceinline__ unsigned q8_bound_pass(unsigned pass, unsigned my_pos, const unsigned char* __restrict__ rows8,
                                                   const float2* __restrict__ meta8, int n, const float* __restrict__ q_p,
-                                                  float one_minus_delta, QState* st, int lane)
+                                                  float one_minus_delta, QState* st, unsigned epoch, int lane)
 {
     const int g = lane >> 3, gl = lane & 7;
     unsigned keep = 0;
@@ -87,7 +87,7 @@ __device__ __forceinline__ unsigned q8_bound_pass(unsigned pass, unsigned my_pos
             acc_a += __shfl_xor_sync(0xffffffffu, acc_a, o);
             acc_b += __shfl_xor_sync(0xffffffffu, acc_b, o);
         }
-        const float thr = slack_up(ld_bsf(st));
+        const float thr = slack_up(ld_bsf_eff(st, epoch));
         auto survives = [&](float acc, float e) {
             const float L = __fsub_rd(__fmul_rd(__fsqrt_rd(acc), one_minus_delta), e);
             return !(L > 0.0f && __fmul_rd(L, L) > thr);

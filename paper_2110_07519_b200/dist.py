@@ -43,3 +43,19 @@ def merge_results(d2: torch.Tensor, gid: torch.Tensor, group=None):
     dist.all_gather(parts, packed, group=group)
     allp = torch.stack(parts).to(home)  # [R, nq, 2]
     return lexmin(allp[:, :, 0].contiguous().view(torch.float64), allp[:, :, 1])
+
+
+def link_shards(index, group=None):
+    """Let the shards of this process group share each query's best-so-far during the
+    batched ED kernels (include/messi.h, messi_link_peers_ipc): every rank publishes the CUDA
+    IPC handles of its per-query state arrays, and opens those of all other ranks (their
+    GPUs' memory, reached over NVLink).  Collective: every rank calls it, once per index."""
+    from . import messi as M
+    world = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    mine = (M.messi_batch_state_ipc(index.handle, 0), M.messi_batch_state_ipc(index.handle, 1))
+    allh = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    peers = [allh[r] for r in range(world) if r != me]
+    M.messi_link_peers_ipc(index.handle, peers)
+    return len(peers)

@@ -82,6 +82,9 @@ def lib():
         L.messi_debug_summaries.argtypes = [vp, vp, vp]
         L.messi_debug_quantised.argtypes = [vp, vp, vp]
         L.messi_debug_coarse_bounds.argtypes = [vp, vp, i32, vp]
+        L.messi_batch_state_ipc.argtypes = [vp, i32, vp]
+        L.messi_link_peers_ipc.argtypes = [vp, vp, i32]
+        L.messi_link_peers_local.argtypes = [vp, ctypes.POINTER(vp), i32]
         L.messi_debug_order.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]
         L.messi_debug_lower_bounds.argtypes = [vp, vp, i32, vp]
         L.messi_debug_tile_bounds.argtypes = [vp, vp, i32, vp]
@@ -100,7 +103,8 @@ EXPORTED = ["messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_
             "messi_debug_breakpoints",
             "messi_debug_summaries", "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances",
             "messi_debug_scan_repeat", "messi_debug_tile_bounds", "messi_debug_quantised",
-            "messi_debug_coarse_bounds"]
+            "messi_debug_coarse_bounds", "messi_batch_state_ipc", "messi_link_peers_ipc",
+            "messi_link_peers_local"]
 
 
 def _check(status: int):
@@ -158,6 +162,25 @@ def messi_query_ed_batch(handle, queries_dev: torch.Tensor, results_dev: torch.T
 def messi_query_dtw_batch(handle, queries_dev: torch.Tensor, reach: int, results_dev: torch.Tensor, stats_dev=None):
     _check(lib().messi_query_dtw_batch(handle, _ptr(queries_dev), queries_dev.shape[0], int(reach),
                                        _ptr(results_dev), _ptr(stats_dev)))
+
+
+def messi_batch_state_ipc(handle, set_index: int) -> bytes:
+    """The 64-byte CUDA IPC handle of the index's per-query state array `set_index` (0/1)."""
+    buf = ctypes.create_string_buffer(64)
+    _check(lib().messi_batch_state_ipc(handle, int(set_index), buf))
+    return buf.raw
+
+
+def messi_link_peers_ipc(handle, peer_handles):
+    """peer_handles: list over peers of (set-0 handle, set-1 handle) byte strings."""
+    blob = b"".join(h0 + h1 for h0, h1 in peer_handles)
+    buf = ctypes.create_string_buffer(blob, len(blob)) if blob else None
+    _check(lib().messi_link_peers_ipc(handle, buf, len(peer_handles)))
+
+
+def messi_link_peers_local(handle, peer_handles_list):
+    arr = (ctypes.c_void_p * max(1, len(peer_handles_list)))(*[h.value for h in peer_handles_list])
+    _check(lib().messi_link_peers_local(handle, arr, len(peer_handles_list)))
 
 
 def messi_free(handle):
