@@ -74,6 +74,7 @@ struct messi_index {
     // sequence of calls)
     QState* peer_st[2][MESSI_MAX_PEERS] = {};
     void* peer_ipc[2][MESSI_MAX_PEERS] = {};
+    QState** d_peers = nullptr;  // device copy of peer_st
     int npeers = 0;
     unsigned epoch = 0;
     int fused_grid = 0;
@@ -185,7 +186,8 @@ static messi_status setup_kernels()
     const int big = 200 * 1024;
     CK(cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
     CK(cudaFuncSetAttribute(k_debug_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
-    CK(cudaFuncSetAttribute(k_scan_refine_ed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(MESSI_MAX_N)));
+    CK(cudaFuncSetAttribute(k_scan_refine_ed<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(MESSI_MAX_N)));
+    CK(cudaFuncSetAttribute(k_scan_refine_ed<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(MESSI_MAX_N)));
     CK(cudaFuncSetAttribute(k_filter_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, kFilterQ * kLutF * 4));
     CK(cudaFuncSetAttribute(k_lbk_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -366,6 +368,7 @@ extern "C" void messi_free(messi_index* idx)
     for (auto& row : idx->peer_ipc)
         for (void* p : row)
             if (p) cudaIpcCloseMemHandle(p);
+    if (idx->d_peers) cudaFree(idx->d_peers);
     for (auto& bs : idx->bset) {
         void* bp[] = {bs.bst, bs.lutc, bs.lutx, bs.lutf, bs.btlist};
         for (void* p : bp)
@@ -531,6 +534,8 @@ static messi_status launch_scan(messi_index* idx, Slot& sl)
 static messi_status ensure_batch_buffers(messi_index* idx)
 {
     if (idx->bset[0].bst) return MESSI_OK;
+    TRY(dalloc(&idx->d_peers, 2 * MESSI_MAX_PEERS));
+    CK(cudaMemset(idx->d_peers, 0, sizeof(QState*) * 2 * MESSI_MAX_PEERS));
     for (auto& bs : idx->bset) {
         TRY(dalloc(&bs.bst, kBatchMax));
         CK(cudaMemset(bs.bst, 0, sizeof(QState) * kBatchMax));  // gbsf = 0: no epoch
@@ -540,7 +545,7 @@ static messi_status ensure_batch_buffers(messi_index* idx)
         TRY(dalloc(&bs.btlist, (size_t)kBatchMax * (size_t)idx->ntiles));
     }
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan_refine_ed, 32 * kFusedWarps, fused_smem(idx->n)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan_refine_ed<false>, 32 * kFusedWarps, fused_smem(idx->n)));
     if (occ < 1) return fail(MESSI_ECUDA, "fused kernel does not fit an SM (n = %d)", idx->n);
     idx->fused_grid = idx->sms * occ;
     return MESSI_OK;
@@ -553,10 +558,11 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
 {
     const int set = (int)(&bs - idx->bset);
     PeerSet peers;
-    for (int i = 0; i < MESSI_MAX_PEERS; ++i) peers.st[i] = idx->peer_st[set][i];
+    peers.st = idx->d_peers + set * MESSI_MAX_PEERS;
     peers.n = idx->npeers;
     peers.epoch = ++idx->epoch;
-    if (peers.epoch == 0) peers.epoch = ++idx->epoch;  // epoch 0 means unlinked
+    if (peers.epoch == 0) peers.epoch = ++idx->epoch;
+    if (peers.n == 0) peers.epoch = 0;  // unlinked: kernels read the local BSF only
     const int n = idx->n;
     const size_t qsm = (size_t)((n + 3) & ~3) * sizeof(float);
     const int len = (int)(idx->window < idx->N ? idx->window : idx->N);
@@ -581,7 +587,12 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
     }
     {
         ProfScope ps(idx, K_SCAN, st);
-        k_scan_refine_ed<<<idx->fused_grid, 32 * kFusedWarps, fused_smem(n), st>>>(
+        if (peers.n > 0)
+            k_scan_refine_ed<true><<<idx->fused_grid, 32 * kFusedWarps, fused_smem(n), st>>>(
+            idx->tiles, idx->sym8, idx->ntiles, idx->N, n, q, bs.lutx, bs.btlist, bs.bst, B, idx->rows8,
+            idx->meta8, idx->q8_omd, idx->perm, idx->rows, peers);
+        else
+            k_scan_refine_ed<false><<<idx->fused_grid, 32 * kFusedWarps, fused_smem(n), st>>>(
             idx->tiles, idx->sym8, idx->ntiles, idx->N, n, q, bs.lutx, bs.btlist, bs.bst, B, idx->rows8,
             idx->meta8, idx->q8_omd, idx->perm, idx->rows, peers);
         LAUNCHED(idx);
@@ -780,6 +791,12 @@ static messi_status unlink_peers(messi_index* idx)
     return MESSI_OK;
 }
 
+static messi_status upload_peers(messi_index* idx)
+{
+    CK(cudaMemcpy(idx->d_peers, &idx->peer_st[0][0], sizeof(QState*) * 2 * MESSI_MAX_PEERS, cudaMemcpyHostToDevice));
+    return MESSI_OK;
+}
+
 extern "C" messi_status messi_link_peers_ipc(messi_index* idx, const void* handles, int32_t npeers)
 {
     g_err[0] = 0;
@@ -803,7 +820,7 @@ extern "C" messi_status messi_link_peers_ipc(messi_index* idx, const void* handl
             idx->peer_st[set][i] = static_cast<QState*>(p);
         }
     idx->npeers = npeers;
-    return MESSI_OK;
+    return upload_peers(idx);
 }
 
 extern "C" messi_status messi_link_peers_local(messi_index* idx, messi_index* const* peers, int32_t npeers)
@@ -828,7 +845,7 @@ extern "C" messi_status messi_link_peers_local(messi_index* idx, messi_index* co
         for (int set = 0; set < 2; ++set) idx->peer_st[set][i] = peers[i]->bset[set].bst;
     }
     idx->npeers = npeers;
-    return MESSI_OK;
+    return upload_peers(idx);
 }
 
 // ------------------------------------------------------------------------ inspection

@@ -58,7 +58,7 @@ struct NearEntry { unsigned id; float d32; };
 // newer epoch wins, within an epoch the smaller distance wins, and a reader ignores other
 // epochs -- so a peer running a batch ahead can never lower this batch's threshold.
 struct PeerSet {
-    QState* st[MESSI_MAX_PEERS];
+    QState* const* st;  // device array of the n peers' per-query state arrays
     int n;
     unsigned epoch;
 };
@@ -141,25 +141,42 @@ __device__ __forceinline__ void bsf_update(QState* st, float d)
 }
 
 // The threshold source of the batched ED path: the local BSF, lowered by the shards' shared
-// one when it carries this launch's epoch (epoch 0 = unlinked: gbsf is never written with it).
+// one when it carries this launch's epoch (epoch 0 = unlinked: gbsf is not read).
+template <bool LINKED>
+__device__ __forceinline__ float ld_bsf_l(const QState* st, unsigned epoch)
+{
+    if (!LINKED) return __uint_as_float(*(volatile const unsigned*)&st->bsf_bits);
+    const float loc = __uint_as_float(*(volatile const unsigned*)&st->bsf_bits);
+    const unsigned long long g = *(volatile const unsigned long long*)&st->gbsf;
+    if ((unsigned)(g >> 32) == epoch) return fminf(loc, __uint_as_float(0xffffffffu - (unsigned)g));
+    return loc;
+}
+
 __device__ __forceinline__ float ld_bsf_eff(const QState* st, unsigned epoch)
 {
     const float loc = __uint_as_float(*(volatile const unsigned*)&st->bsf_bits);
+    if (epoch == 0u) return loc;  // unlinked: the local BSF only (one load)
     const unsigned long long g = *(volatile const unsigned long long*)&st->gbsf;
-    if (epoch != 0u && (unsigned)(g >> 32) == epoch) return fminf(loc, __uint_as_float(0xffffffffu - (unsigned)g));
+    if ((unsigned)(g >> 32) == epoch) return fminf(loc, __uint_as_float(0xffffffffu - (unsigned)g));
     return loc;
 }
 
 // A new local best d of query b: the local BSF, and (linked) every peer's shared one.
-__device__ __forceinline__ void bsf_publish(QState* st, const PeerSet& ps, int b, float d)
+// The peer fan-out is out of line (rare: a few BSF improvements per query) and uses global-
+// space atomics explicitly, so the hot kernels do not carry generic-address atomic code.
+__device__ __noinline__ void bsf_publish_peers(PeerSet ps, int b, float d)
+{
+    const unsigned long long key = ((unsigned long long)ps.epoch << 32) | (0xffffffffu - __float_as_uint(d));
+    for (int i = 0; i < ps.n; ++i) {
+        unsigned long long* a = &ps.st[i][b].gbsf;
+        asm volatile("red.relaxed.sys.global.max.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(a)), "l"(key) : "memory");
+    }
+}
+
+__device__ __forceinline__ void bsf_publish(QState* st, PeerSet ps, int b, float d)
 {
     bsf_update(st, d);
-    if (ps.n > 0 && d >= 0.0f) {
-        const unsigned long long key = ((unsigned long long)ps.epoch << 32) | (0xffffffffu - __float_as_uint(d));
-#pragma unroll
-        for (int i = 0; i < MESSI_MAX_PEERS; ++i)
-            if (i < ps.n) atomicMax(&ps.st[i][b].gbsf, key);
-    }
+    if (ps.n > 0 && d >= 0.0f) bsf_publish_peers(ps, b, d);
 }
 
 // Symbol of a fp32 PAA value: #{k : beta32_k <= x} over the 255 ascending breakpoints

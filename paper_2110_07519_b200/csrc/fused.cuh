@@ -296,9 +296,10 @@ __device__ __forceinline__ void best_update(QState* st, double d, long long id)
 // raw rows, four rows in flight per warp (Alg. 9 RealDist); a distance <= BSF*(1+eps)
 // lowers the BSF (atomicMin, Alg. 8's BSF update P:1178-1186) and is re-ranked exactly in
 // fp64 at once (reading R11/R12): the lexicographic min over the re-ranked rows is the answer.
+template <bool LINKED>
 __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __restrict__ perm,
                            const float* __restrict__ rows, int n, const float* __restrict__ q_p, QState* st,
-                           const PeerSet& ps, int b, int lane)
+                           PeerSet ps, int b, int lane)
 {
     while (keep) {
         unsigned id[kRefineGroup];
@@ -336,9 +337,10 @@ __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __res
 #pragma unroll
             for (int g = 0; g < kRefineGroup; ++g) {
                 if (!ok[g]) continue;
-                const float thr = slack_up(ld_bsf_eff(st, ps.epoch));
+                const float thr = slack_up(ld_bsf_l<LINKED>(st, ps.epoch));
                 if (acc[g] <= thr) {
-                    bsf_publish(st, ps, b, acc[g]);
+                    if (LINKED) bsf_publish(st, ps, b, acc[g]);
+                    else bsf_update(st, acc[g]);
                     const double d64 = ed2_exact_g(q_p, rows + (long long)id[g] * n, n);
                     best_update(st, d64, (long long)id[g]);
                     atomicAdd(&st->near_count, 1u);
@@ -412,12 +414,13 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes)
 // the exact passes.
 struct WarpCounts { unsigned tiles, coarse, cand, exact; };
 
+template <bool LINKED>
 __device__ __forceinline__ void fine_and_refine(long long tile, int m, const unsigned short* surv, uint4 w0, unsigned pos0,
                                                 const uint4* __restrict__ sym8, const char* lbase, unsigned* cbuf,
                                                 unsigned& ncb, const unsigned char* __restrict__ rows8,
                                                 const float2* __restrict__ meta8, int n, const float* q_p,
                                                 float one_minus_delta, const unsigned* __restrict__ perm,
-                                                const float* __restrict__ rows, QState* st, const PeerSet& ps, int b,
+                                                const float* __restrict__ rows, QState* st, PeerSet ps, int b,
                                                 WarpCounts& wc, int lane)
 {
     for (int i0 = 0; i0 < m; i0 += 32) {
@@ -430,7 +433,7 @@ __device__ __forceinline__ void fine_and_refine(long long tile, int m, const uns
         }
         float lb = INFINITY;
         if (v) lb = fine_lb(w, lbase, lane);
-        const bool ok = v && lb <= slack_up(ld_bsf_eff(st, ps.epoch));
+        const bool ok = v && lb <= slack_up(ld_bsf_l<LINKED>(st, ps.epoch));
         const unsigned pass = __ballot_sync(0xffffffffu, ok);
         if (!pass) continue;
         if (ok) {
@@ -448,9 +451,9 @@ __device__ __forceinline__ void fine_and_refine(long long tile, int m, const uns
             ncb -= 32;
             __syncwarp();
             const unsigned keep =
-                q8_bound_pass(0xffffffffu, cp, rows8, meta8, n, q_p, one_minus_delta, st, ps.epoch, lane);
+                q8_bound_pass<LINKED>(0xffffffffu, cp, rows8, meta8, n, q_p, one_minus_delta, st, ps.epoch, lane);
             wc.exact += __popc(keep);
-            exact_pass(keep, cp, perm, rows, n, q_p, st, ps, b, lane);
+            exact_pass<LINKED>(keep, cp, perm, rows, n, q_p, st, ps, b, lane);
         }
     }
 }
@@ -465,6 +468,7 @@ __device__ __forceinline__ void fine_and_refine(long long tile, int m, const uns
 // Alg. 9's workers do.  When a query's list runs dry the CTA joins the next
 // one: light queries finish early and their CTAs help the heavy ones.  k_finalise_batch
 // writes the results.
+template <bool LINKED>
 __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
     const uint4* __restrict__ tiles, const uint4* __restrict__ sym8, long long ntiles, long long N, int n,
     const float* __restrict__ queries, const float* __restrict__ lutx_all, const uint2* __restrict__ tlist_all,
@@ -518,7 +522,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
             // claim the following pair now and prefetch its tiles into L2
             if (lane == 0) {
                 k_next = atomicAdd(&st->next_tile, 1u) * 2u;
-                const float pthr = slack_up(ld_bsf_eff(st, ps.epoch));
+                const float pthr = slack_up(ld_bsf_l<LINKED>(st, ps.epoch));
                 for (unsigned kk = k_next; kk < min(k_next + 2u, count); ++kk) {
                     const uint2 tn = at(kk);
                     if (__uint_as_float(tn.y) <= pthr)  // not already box-pruned
@@ -531,15 +535,15 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
                 if (k0 + u >= count) break;
                 const uint2 te = u == 0 ? te0 : te1;
                 // warp-uniform decision: lane 0's reading of the BSF
-                const float bthr = __shfl_sync(0xffffffffu, slack_up(ld_bsf_eff(st, ps.epoch)), 0);
+                const float bthr = __shfl_sync(0xffffffffu, slack_up(ld_bsf_l<LINKED>(st, ps.epoch)), 0);
                 if (__uint_as_float(te.y) > bthr) continue;  // box pruned by the current BSF
                 ++wc.tiles;
                 const long long tile = te.x;
                 unsigned short* surv = survb + cur * MESSI_TILE_ROWS;
-                const int m = scan_tile_coarse(tiles, tile, lbase, slack_up(ld_bsf_eff(st, ps.epoch)), N, surv, lane);
+                const int m = scan_tile_coarse(tiles, tile, lbase, slack_up(ld_bsf_l<LINKED>(st, ps.epoch)), N, surv, lane);
                 wc.coarse += m;
                 if (pm)
-                    fine_and_refine(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb,
+                    fine_and_refine<LINKED>(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb,
                                     rows8, meta8, n, q_p, one_minus_delta, perm, rows, st, ps, b, wc, lane);
                 // preload the 8-bit words of this tile's first 32 coarse survivors
                 ppos = lane < m ? (unsigned)(tile * MESSI_TILE_ROWS + surv[lane]) : 0u;
@@ -550,15 +554,16 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
             }
         }
         if (pm)
-            fine_and_refine(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb, rows8,
+            fine_and_refine<LINKED>(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb, rows8,
                             meta8, n, q_p, one_minus_delta, perm, rows, st, ps, b, wc, lane);
         if (ncb) {  // the query's last fine survivors
             const unsigned cp = (unsigned)lane < ncb ? cbuf[lane] : 0u;
             const unsigned pass = ncb >= 32 ? 0xffffffffu : (1u << ncb) - 1u;
             __syncwarp();
-            const unsigned keep = q8_bound_pass(pass, cp, rows8, meta8, n, q_p, one_minus_delta, st, ps.epoch, lane);
+            const unsigned keep =
+                q8_bound_pass<LINKED>(pass, cp, rows8, meta8, n, q_p, one_minus_delta, st, ps.epoch, lane);
             wc.exact += __popc(keep);
-            exact_pass(keep, cp, perm, rows, n, q_p, st, ps, b, lane);
+            exact_pass<LINKED>(keep, cp, perm, rows, n, q_p, st, ps, b, lane);
             ncb = 0;
         }
         if (lane == 0) {

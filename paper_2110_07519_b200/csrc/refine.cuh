@@ -26,6 +26,7 @@ constexpr int kRefineGroup = 4;
 // chunks gl, gl+8, ... of its rows; the query comes from q_p, a padded copy (element i at
 // i + 4 (i >> 5)).  Bytes convert exactly with the 2^23 trick:
 // float(0x4B000000 | b) = 2^23 + b.
+template <bool LINKED>
 __device__ __forceinline__ unsigned q8_bound_pass(unsigned pass, unsigned my_pos, const unsigned char* __restrict__ rows8,
                                                   const float2* __restrict__ meta8, int n, const float* __restrict__ q_p,
                                                   float one_minus_delta, QState* st, unsigned epoch, int lane)
@@ -87,7 +88,7 @@ __device__ __forceinline__ unsigned q8_bound_pass(unsigned pass, unsigned my_pos
             acc_a += __shfl_xor_sync(0xffffffffu, acc_a, o);
             acc_b += __shfl_xor_sync(0xffffffffu, acc_b, o);
         }
-        const float thr = slack_up(ld_bsf_eff(st, epoch));
+        const float thr = slack_up(ld_bsf_l<LINKED>(st, epoch));
         auto survives = [&](float acc, float e) {
             const float L = __fsub_rd(__fmul_rd(__fsqrt_rd(acc), one_minus_delta), e);
             return !(L > 0.0f && __fmul_rd(L, L) > thr);

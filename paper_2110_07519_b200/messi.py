@@ -82,9 +82,10 @@ def lib():
         L.messi_debug_summaries.argtypes = [vp, vp, vp]
         L.messi_debug_quantised.argtypes = [vp, vp, vp]
         L.messi_debug_coarse_bounds.argtypes = [vp, vp, i32, vp]
-        L.messi_batch_state_ipc.argtypes = [vp, i32, vp]
-        L.messi_link_peers_ipc.argtypes = [vp, vp, i32]
-        L.messi_link_peers_local.argtypes = [vp, ctypes.POINTER(vp), i32]
+        if hasattr(L, "messi_batch_state_ipc"):  # (MESSI_LIB may name an older build in A/B runs)
+            L.messi_batch_state_ipc.argtypes = [vp, i32, vp]
+            L.messi_link_peers_ipc.argtypes = [vp, vp, i32]
+            L.messi_link_peers_local.argtypes = [vp, ctypes.POINTER(vp), i32]
         L.messi_debug_order.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]
         L.messi_debug_lower_bounds.argtypes = [vp, vp, i32, vp]
         L.messi_debug_tile_bounds.argtypes = [vp, vp, i32, vp]
