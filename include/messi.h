@@ -122,6 +122,21 @@ messi_status messi_batch_state_ipc(messi_index* idx, int32_t set, void* handle_o
 messi_status messi_link_peers_ipc(messi_index* idx, const void* handles, int32_t npeers);
 messi_status messi_link_peers_local(messi_index* idx, messi_index* const* peers, int32_t npeers);
 
+/* Exact k-NN under ED (the paper's k-NN variant: the BSF becomes
+ * the k-th best distance), 1 <= k <= 64 (k > 1 needs cfg.window <= 4096).  The pruning
+ * threshold is the k-th smallest fp32 distance of the rows refined so far (seeded with the
+ * k-th smallest of the approximate-search window); every row within it is re-ranked in fp64,
+ * and the answer is the k lexicographically smallest (d2, id): ascending, ties to the lowest
+ * id; fewer than k rows -> the remaining entries are (inf, -1).
+ * messi_query_ed_knn: one query (host or device pointer), results = k messi_result in host
+ *   memory, stats (host, nullable).  Synchronous.
+ * messi_query_ed_knn_batch: nq queries [nq][n] on the device, results_dev[nq][k] and
+ *   stats_dev[nq] (nullable) device arrays; asynchronous on cfg.stream like the 1-NN batch. */
+messi_status messi_query_ed_knn(messi_index* idx, const float* query, int32_t k, messi_result* results,
+                                messi_stats* stats);
+messi_status messi_query_ed_knn_batch(messi_index* idx, const float* queries_dev, int32_t nq, int32_t k,
+                                      messi_result* results_dev, messi_stats* stats_dev);
+
 /* Release everything the library allocated for idx.  NULL-safe. */
 void messi_free(messi_index* idx);
 

@@ -245,3 +245,20 @@ def nn(kind: str, data, queries, r: int = 0, row_begin: int = 0, threads: int | 
     for pd, pi in parts:
         d2, ids = merge(d2, ids, pd, pi)
     return d2, ids
+
+
+def knn(kind: str, data, queries, k: int, r: int = 0, row_begin: int = 0):
+    """Exact k-NN by the plain definition: every row's distance by the C
+    oracle (ed2_rows / dtw2_rows: fp64, sequential), then the k lexicographically smallest
+    (d2, id) per query (ties -> lowest id).  Returns d2 [nq, k], ids [nq, k] (-1 past N)."""
+    data = np.ascontiguousarray(data, dtype=np.float32)
+    queries = np.atleast_2d(np.ascontiguousarray(queries, dtype=np.float32))
+    nq, N = queries.shape[0], data.shape[0]
+    out_d = np.full((nq, k), np.inf)
+    out_i = np.full((nq, k), -1, np.int64)
+    for qi in range(nq):
+        d = ed2_rows(data, queries[qi]) if kind == "ed" else dtw2_rows(data, queries[qi], r)
+        order = np.lexsort((np.arange(N), d))[:k]
+        out_d[qi, :len(order)] = d[order]
+        out_i[qi, :len(order)] = order + row_begin
+    return out_d, out_i

@@ -68,6 +68,8 @@ struct messi_index {
         QState* bst = nullptr;
         float *lutc = nullptr, *lutx = nullptr, *lutf = nullptr;
         uint2* btlist = nullptr;
+        KnnState* knn = nullptr;  // k-NN state (lazy)
+        float* seedd = nullptr;   // k-NN: the window distances of every query (lazy)
     } bset[2];
     // shards sharing each query's best-so-far (PeerSet): their per-set state arrays, the
     // IPC mappings to close, and the launch epoch (identical on every shard for the same
@@ -83,6 +85,7 @@ struct messi_index {
     unsigned long long qcount = 0;
     float* qbuf = nullptr;
     messi_result* res1 = nullptr;
+    messi_result* resk = nullptr;    // k-NN single-query results (device)
     messi_stats* stats1 = nullptr;
     long long launches = 0;
     // optional per-kernel event timing
@@ -362,7 +365,7 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->stream) cudaStreamSynchronize(idx->stream);
     else cudaDeviceSynchronize();
     void* ptrs[] = {idx->tiles, idx->sym8, idx->boxes, idx->sboxes, idx->paa, idx->skey, idx->perm, idx->beta32, idx->lo_w,
-                    idx->hi_w,  idx->qbuf,  idx->res1, idx->stats1, idx->rows8, idx->meta8};
+                    idx->hi_w,  idx->qbuf,  idx->res1, idx->resk, idx->stats1, idx->rows8, idx->meta8};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& row : idx->peer_ipc)
@@ -370,7 +373,7 @@ extern "C" void messi_free(messi_index* idx)
             if (p) cudaIpcCloseMemHandle(p);
     if (idx->d_peers) cudaFree(idx->d_peers);
     for (auto& bs : idx->bset) {
-        void* bp[] = {bs.bst, bs.lutc, bs.lutx, bs.lutf, bs.btlist};
+        void* bp[] = {bs.bst, bs.lutc, bs.lutx, bs.lutf, bs.btlist, bs.knn, bs.seedd};
         for (void* p : bp)
             if (p) cudaFree(p);
     }
@@ -554,8 +557,10 @@ static messi_status ensure_batch_buffers(messi_index* idx)
 // One group of B <= kBatchMax queries of the batched ED path (fused.cuh) on stream st with
 // state set bs: prologue, seed, tile filter, the fused scan + refine kernel, finalise.
 static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSet& bs, cudaStream_t st, const float* q, int B,
-                                    messi_result* res, messi_stats* stats)
+                                    messi_result* res, messi_stats* stats, int k)
 {
+    KnnState* knn = k > 1 ? bs.knn : nullptr;
+    float* seed_d = k > 1 ? bs.seedd : nullptr;
     const int set = (int)(&bs - idx->bset);
     PeerSet peers;
     peers.st = idx->d_peers + set * MESSI_MAX_PEERS;
@@ -569,11 +574,17 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
     {
         ProfScope ps(idx, K_SEED, st);
         k_prologue_batch<<<B, 256, qsm, st>>>(q, n, idx->beta32, idx->lo_w, idx->hi_w, idx->skey, idx->N, idx->window,
-                                              bs.lutc, bs.lutx, bs.lutf, bs.bst);
+                                              bs.lutc, bs.lutx, bs.lutf, bs.bst, knn);
         LAUNCHED(idx);
         dim3 sg((unsigned)((len + kSeedRowsPerCta - 1) / kSeedRowsPerCta), (unsigned)B);
-        k_seed_batch<<<sg, 256, qsm, st>>>(q, n, idx->rows, idx->perm, bs.bst, peers);
+        k_seed_batch<<<sg, 256, qsm, st>>>(q, n, idx->rows, idx->perm, bs.bst, peers, seed_d, idx->window);
         LAUNCHED(idx);
+        if (knn) {
+            int np = 1;
+            while (np < len) np <<= 1;
+            k_seed_select<<<B, 1024, (size_t)np * sizeof(float), st>>>(seed_d, idx->window, k, bs.bst, peers);
+            LAUNCHED(idx);
+        }
         const long long nsuper = (idx->ntiles + kSuperTiles - 1) / kSuperTiles;
         const int npairs = (B + kFilterQ - 1) / kFilterQ;
         long long fx = (nsuper + 255) / 256;
@@ -590,13 +601,13 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
         if (peers.n > 0)
             k_scan_refine_ed<true><<<idx->fused_grid, 32 * kFusedWarps, fused_smem(n), st>>>(
             idx->tiles, idx->sym8, idx->ntiles, idx->N, n, q, bs.lutx, bs.btlist, bs.bst, B, idx->rows8,
-            idx->meta8, idx->q8_omd, idx->perm, idx->rows, peers);
+            idx->meta8, idx->q8_omd, idx->perm, idx->rows, peers, knn, k);
         else
             k_scan_refine_ed<false><<<idx->fused_grid, 32 * kFusedWarps, fused_smem(n), st>>>(
             idx->tiles, idx->sym8, idx->ntiles, idx->N, n, q, bs.lutx, bs.btlist, bs.bst, B, idx->rows8,
-            idx->meta8, idx->q8_omd, idx->perm, idx->rows, peers);
+            idx->meta8, idx->q8_omd, idx->perm, idx->rows, peers, knn, k);
         LAUNCHED(idx);
-        k_finalise_batch<<<(B + 127) / 128, 128, 0, st>>>(bs.bst, B, idx->N, idx->row_begin, res, stats);
+        k_finalise_batch<<<(B + 127) / 128, 128, 0, st>>>(bs.bst, B, idx->N, idx->row_begin, res, stats, knn, k);
         LAUNCHED(idx);
     }
     return MESSI_OK;
@@ -607,14 +618,19 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
 // group's prologue / filter with the other's fused kernel, was measured slower: each
 // persistent kernel then balances fewer queries.)
 static messi_status run_ed_batch(messi_index* idx, const float* queries_dev, int nq, messi_result* results_dev,
-                                 messi_stats* stats_dev)
+                                 messi_stats* stats_dev, int k = 1)
 {
     TRY(ensure_batch_buffers(idx));
+    if (k > 1)
+        for (auto& bs : idx->bset) {
+            if (!bs.knn) TRY(dalloc(&bs.knn, kBatchMax));
+            if (!bs.seedd) TRY(dalloc(&bs.seedd, (size_t)kBatchMax * idx->window));
+        }
     const int n = idx->n;
     for (int g0 = 0; g0 < nq; g0 += kBatchMax) {
         const int B = nq - g0 < kBatchMax ? nq - g0 : kBatchMax;
         TRY(launch_ed_group(idx, idx->bset[(g0 / kBatchMax) & 1], idx->stream, queries_dev + (size_t)g0 * n, B,
-                            results_dev + g0, stats_dev ? stats_dev + g0 : nullptr));
+                            results_dev + (size_t)g0 * k, stats_dev ? stats_dev + g0 : nullptr, k));
     }
     return MESSI_OK;
 }
@@ -748,6 +764,44 @@ extern "C" messi_status messi_query_ed_batch(messi_index* idx, const float* quer
     TRY(join_streams(idx));  // earlier DTW queries (other streams) before the ED batch reuses qbuf users
     if (nq == 0) return MESSI_OK;
     return run_ed_batch(idx, queries_dev, nq, results_dev, stats_dev);
+}
+
+static messi_status check_k(const messi_index* idx, int32_t k)
+{
+    if (k < 1 || k > MESSI_MAX_K) return fail(MESSI_EINVAL, "k = %d outside [1, %d]", k, MESSI_MAX_K);
+    if (k > 1 && idx->window > 4096) return fail(MESSI_EINVAL, "k-NN needs an approximate-search window <= 4096");
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_query_ed_knn(messi_index* idx, const float* query, int32_t k, messi_result* results,
+                                           messi_stats* stats)
+{
+    g_err[0] = 0;
+    if (!idx || !query || !results) return fail(MESSI_EINVAL, "NULL argument");
+    TRY(check_k(idx, k));
+    CK(cudaSetDevice(idx->device));
+    if (k == 1) return messi_query_ed(idx, query, results, stats);
+    const float* q = nullptr;
+    TRY(stage_query(idx, query, &q));
+    if (!idx->resk) TRY(dalloc(&idx->resk, MESSI_MAX_K));
+    TRY(run_ed_batch(idx, q, 1, idx->resk, idx->stats1, k));
+    TRY(join_streams(idx));
+    CK(cudaMemcpyAsync(results, idx->resk, sizeof(messi_result) * k, cudaMemcpyDeviceToHost, idx->stream));
+    if (stats) CK(cudaMemcpyAsync(stats, idx->stats1, sizeof(messi_stats), cudaMemcpyDeviceToHost, idx->stream));
+    CK(cudaStreamSynchronize(idx->stream));
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_query_ed_knn_batch(messi_index* idx, const float* queries_dev, int32_t nq, int32_t k,
+                                                 messi_result* results_dev, messi_stats* stats_dev)
+{
+    g_err[0] = 0;
+    if (!idx || !queries_dev || !results_dev || nq < 0) return fail(MESSI_EINVAL, "bad argument");
+    TRY(check_k(idx, k));
+    CK(cudaSetDevice(idx->device));
+    TRY(join_streams(idx));
+    if (nq == 0) return MESSI_OK;
+    return run_ed_batch(idx, queries_dev, nq, results_dev, stats_dev, k);
 }
 
 extern "C" messi_status messi_query_dtw_batch(messi_index* idx, const float* queries_dev, int32_t nq, int32_t reach,

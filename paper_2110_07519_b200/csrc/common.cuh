@@ -51,6 +51,17 @@ struct QState {
 
 struct NearEntry { unsigned id; float d32; };
 
+// k-NN (k > 1) state of one query of the batched ED path, under QState::lock: the k smallest
+// fp32 distances of the rows refined so far (their k-th is the pruning threshold, held in
+// bsf_bits) and the k lexicographically smallest (fp64 d2, id) of the rows re-ranked.
+#define MESSI_MAX_K 64
+struct KnnState {
+    float d32[MESSI_MAX_K];
+    double d64[MESSI_MAX_K];
+    long long id[MESSI_MAX_K];
+    int n32, n64;
+};
+
 // Best-so-far shared with the other shards of a row-sharded collection (batched ED path):
 // the per-query states of up to MESSI_MAX_PEERS peer indexes (peer GPUs' memory reached over
 // NVLink, or other indexes of this process) and the launch epoch every shard tags its

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(256) k_prologue_batch(const float* __restrict_
                                                         const unsigned long long* __restrict__ skey, long long N,
                                                         int window, float* __restrict__ lutc_all,
                                                         float* __restrict__ lutx_all, float* __restrict__ lutf_all,
-                                                        QState* st_all)
+                                                        QState* st_all, KnnState* knn)
 {
     extern __shared__ __align__(16) float q_s[];
     __shared__ unsigned long long qkey_s;
@@ -51,7 +51,10 @@ __global__ void __launch_bounds__(256) k_prologue_batch(const float* __restrict_
     QState* st = st_all + b;
     const float* q = queries + (size_t)b * n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q[i];
-    if (threadIdx.x == 0) arm_state(st);
+    if (threadIdx.x == 0) {
+        arm_state(st);
+        if (knn) knn[b].n32 = knn[b].n64 = 0;
+    }
     __syncthreads();
     float* lutc = lutc_all + (size_t)b * (MESSI_W * MESSI_CARD);
     prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, lutc, lutx_all + (size_t)b * kLutX, nullptr, nullptr, &qkey_s, st);
@@ -89,7 +92,7 @@ __global__ void __launch_bounds__(256) k_prologue_batch(const float* __restrict_
 constexpr int kSeedRowsPerCta = 64;
 __global__ void __launch_bounds__(256) k_seed_batch(const float* __restrict__ queries, int n,
                                                     const float* __restrict__ rows, const unsigned* __restrict__ perm,
-                                                    QState* st_all, PeerSet ps)
+                                                    QState* st_all, PeerSet ps, float* __restrict__ seed_d, int seed_cap)
 {
     extern __shared__ __align__(16) float q_s[];
     const int b = blockIdx.y;
@@ -129,12 +132,46 @@ __global__ void __launch_bounds__(256) k_seed_batch(const float* __restrict__ qu
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const float d = warp_sum(acc[u]);
-            if (ok[u]) best = fminf(best, d);
+            if (ok[u]) {
+                best = fminf(best, d);
+                if (seed_d && lane == 0) seed_d[(size_t)b * seed_cap + g + u] = d;  // k-NN: every window distance
+            }
         }
     }
-    if (lane == 0 && best < INFINITY) {
+    if (!seed_d && lane == 0 && best < INFINITY) {  // 1-NN: the window's best is BSF0
         bsf_publish(st, ps, b, best);
         atomicMin(&st->seed_bits, __float_as_uint(best));
+    }
+}
+
+// k-NN seed: the k-th smallest fp32 distance of the window (a distance k rows achieve) is
+// BSF0; one CTA per query sorts the window's distances in shared memory (bitonic).
+__global__ void __launch_bounds__(1024) k_seed_select(const float* __restrict__ seed_d, int seed_cap, int k,
+                                                      QState* st_all, PeerSet ps)
+{
+    extern __shared__ float sv[];
+    const int b = blockIdx.x;
+    QState* st = st_all + b;
+    const int len = st->window_len;
+    int np = 1;
+    while (np < len) np <<= 1;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) sv[i] = i < len ? seed_d[(size_t)b * seed_cap + i] : INFINITY;
+    __syncthreads();
+    for (int size = 2; size <= np; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < np; i += blockDim.x) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const float a = sv[i], c = sv[j];
+                    if ((a > c) == up) { sv[i] = c; sv[j] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    if (threadIdx.x == 0 && len >= k && sv[k - 1] < INFINITY) {
+        bsf_publish(st, ps, b, sv[k - 1]);
+        atomicMin(&st->seed_bits, __float_as_uint(sv[k - 1]));
     }
 }
 
@@ -292,6 +329,45 @@ __device__ __forceinline__ void best_update(QState* st, double d, long long id)
     atomicExch(&st->lock, 0u);
 }
 
+// k-NN: a refined row (fp32 d32, fp64 d64, id) under the query's lock.  The fp32 list keeps
+// the k smallest d32 (distinct rows: each row is refined once); once it holds k, its k-th is
+// a distance k rows achieve, i.e. a valid threshold for the k-th neighbour, and lowers the
+// BSF.  The fp64 list keeps the k lexicographically smallest (d64, id) -- the answer.
+__device__ void knn_insert(QState* st, KnnState* kn, int k, float d32, double d64, long long id, PeerSet ps, int b,
+                           bool linked)
+{
+    while (atomicCAS(&st->lock, 0u, 1u) != 0u) __nanosleep(64);
+    __threadfence();
+    volatile KnnState* v = kn;
+    int n = v->n32;
+    if (n < k || d32 < v->d32[k - 1]) {
+        int i = n < k ? n : k - 1;
+        while (i > 0 && v->d32[i - 1] > d32) { v->d32[i] = v->d32[i - 1]; --i; }
+        v->d32[i] = d32;
+        if (n < k) v->n32 = ++n;
+    }
+    float kth = n == k ? v->d32[k - 1] : -1.0f;
+    n = v->n64;
+    auto less = [&](double a, long long ia, double c, long long ic) { return a < c || (a == c && ia < ic); };
+    if (n < k || less(d64, id, v->d64[k - 1], v->id[k - 1])) {
+        int i = n < k ? n : k - 1;
+        while (i > 0 && less(d64, id, v->d64[i - 1], v->id[i - 1])) {
+            v->d64[i] = v->d64[i - 1];
+            v->id[i] = v->id[i - 1];
+            --i;
+        }
+        v->d64[i] = d64;
+        v->id[i] = id;
+        if (n < k) v->n64 = n + 1;
+    }
+    __threadfence();
+    atomicExch(&st->lock, 0u);
+    if (kth >= 0.0f) {
+        if (linked) bsf_publish(st, ps, b, kth);
+        else bsf_update(st, kth);
+    }
+}
+
 // The candidates of `keep` (one per lane, sorted position my_pos): fp32 squared ED over the
 // raw rows, four rows in flight per warp (Alg. 9 RealDist); a distance <= BSF*(1+eps)
 // lowers the BSF (atomicMin, Alg. 8's BSF update P:1178-1186) and is re-ranked exactly in
@@ -299,7 +375,7 @@ __device__ __forceinline__ void best_update(QState* st, double d, long long id)
 template <bool LINKED>
 __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __restrict__ perm,
                            const float* __restrict__ rows, int n, const float* __restrict__ q_p, QState* st,
-                           PeerSet ps, int b, int lane)
+                           PeerSet ps, int b, KnnState* knn, int k, int lane)
 {
     while (keep) {
         unsigned id[kRefineGroup];
@@ -339,10 +415,14 @@ __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __res
                 if (!ok[g]) continue;
                 const float thr = slack_up(ld_bsf_l<LINKED>(st, ps.epoch));
                 if (acc[g] <= thr) {
-                    if (LINKED) bsf_publish(st, ps, b, acc[g]);
-                    else bsf_update(st, acc[g]);
                     const double d64 = ed2_exact_g(q_p, rows + (long long)id[g] * n, n);
-                    best_update(st, d64, (long long)id[g]);
+                    if (knn) {
+                        knn_insert(st, knn + b, k, acc[g], d64, (long long)id[g], ps, b, LINKED);
+                    } else {
+                        if (LINKED) bsf_publish(st, ps, b, acc[g]);
+                        else bsf_update(st, acc[g]);
+                        best_update(st, d64, (long long)id[g]);
+                    }
                     atomicAdd(&st->near_count, 1u);
                 }
             }
@@ -392,14 +472,30 @@ __device__ void fused_finalise(const QState* st, long long N, long long row_begi
 }
 
 // One thread per query of the batch, after k_scan_refine_ed (stream order makes every
-// update of the fused kernel visible): results and stats.
+// update of the fused kernel visible): results and stats.  k-NN: k results per query,
+// ascending (d2, id); fewer than k rows -> the rest (inf, -1).
 __global__ void k_finalise_batch(const QState* __restrict__ st_all, int B, long long N, long long row_begin,
-                                 void* results, void* stats)
+                                 void* results, void* stats, const KnnState* __restrict__ knn, int k)
 {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
-    fused_finalise(st_all + b, N, row_begin, reinterpret_cast<char*>(results) + (size_t)b * 32,
+    if (!knn) {
+        fused_finalise(st_all + b, N, row_begin, reinterpret_cast<char*>(results) + (size_t)b * 32,
+                       stats ? reinterpret_cast<char*>(stats) + (size_t)b * 104 : nullptr);
+        return;
+    }
+    fused_finalise(st_all + b, N, row_begin, reinterpret_cast<char*>(results) + (size_t)b * k * 32,
                    stats ? reinterpret_cast<char*>(stats) + (size_t)b * 104 : nullptr);
+    struct R { double dist; long long id; double d2; long long reserved; };
+    R* res = reinterpret_cast<R*>(results) + (size_t)b * k;
+    const KnnState* kn = knn + b;
+    for (int i = 0; i < k; ++i) {
+        const bool have = i < kn->n64;
+        res[i].dist = have ? sqrt(kn->d64[i]) : (double)INFINITY;
+        res[i].id = have ? row_begin + kn->id[i] : -1;
+        res[i].d2 = have ? kn->d64[i] : (double)INFINITY;
+        res[i].reserved = 0;
+    }
 }
 
 __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes)
@@ -421,7 +517,7 @@ __device__ __forceinline__ void fine_and_refine(long long tile, int m, const uns
                                                 const float2* __restrict__ meta8, int n, const float* q_p,
                                                 float one_minus_delta, const unsigned* __restrict__ perm,
                                                 const float* __restrict__ rows, QState* st, PeerSet ps, int b,
-                                                WarpCounts& wc, int lane)
+                                                KnnState* knn, int k, WarpCounts& wc, int lane)
 {
     for (int i0 = 0; i0 < m; i0 += 32) {
         const bool v = i0 + lane < m;
@@ -453,7 +549,7 @@ __device__ __forceinline__ void fine_and_refine(long long tile, int m, const uns
             const unsigned keep =
                 q8_bound_pass<LINKED>(0xffffffffu, cp, rows8, meta8, n, q_p, one_minus_delta, st, ps.epoch, lane);
             wc.exact += __popc(keep);
-            exact_pass<LINKED>(keep, cp, perm, rows, n, q_p, st, ps, b, lane);
+            exact_pass<LINKED>(keep, cp, perm, rows, n, q_p, st, ps, b, knn, k, lane);
         }
     }
 }
@@ -474,7 +570,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
     const float* __restrict__ queries, const float* __restrict__ lutx_all, const uint2* __restrict__ tlist_all,
     QState* st_all, int B,
     const unsigned char* __restrict__ rows8, const float2* __restrict__ meta8, float one_minus_delta,
-    const unsigned* __restrict__ perm, const float* __restrict__ rows, PeerSet ps)
+    const unsigned* __restrict__ perm, const float* __restrict__ rows, PeerSet ps, KnnState* knn, int k)
 {
     extern __shared__ __align__(16) float smem[];
     float* lut_s = smem;
@@ -544,7 +640,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
                 wc.coarse += m;
                 if (pm)
                     fine_and_refine<LINKED>(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb,
-                                    rows8, meta8, n, q_p, one_minus_delta, perm, rows, st, ps, b, wc, lane);
+                                    rows8, meta8, n, q_p, one_minus_delta, perm, rows, st, ps, b, knn, k, wc, lane);
                 // preload the 8-bit words of this tile's first 32 coarse survivors
                 ppos = lane < m ? (unsigned)(tile * MESSI_TILE_ROWS + surv[lane]) : 0u;
                 pw = lane < m ? sym8[ppos] : make_uint4(0, 0, 0, 0);
@@ -555,7 +651,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
         }
         if (pm)
             fine_and_refine<LINKED>(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb, rows8,
-                            meta8, n, q_p, one_minus_delta, perm, rows, st, ps, b, wc, lane);
+                            meta8, n, q_p, one_minus_delta, perm, rows, st, ps, b, knn, k, wc, lane);
         if (ncb) {  // the query's last fine survivors
             const unsigned cp = (unsigned)lane < ncb ? cbuf[lane] : 0u;
             const unsigned pass = ncb >= 32 ? 0xffffffffu : (1u << ncb) - 1u;
@@ -563,7 +659,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
             const unsigned keep =
                 q8_bound_pass<LINKED>(pass, cp, rows8, meta8, n, q_p, one_minus_delta, st, ps.epoch, lane);
             wc.exact += __popc(keep);
-            exact_pass<LINKED>(keep, cp, perm, rows, n, q_p, st, ps, b, lane);
+            exact_pass<LINKED>(keep, cp, perm, rows, n, q_p, st, ps, b, knn, k, lane);
             ncb = 0;
         }
         if (lane == 0) {

@@ -59,3 +59,29 @@ def link_shards(index, group=None):
     peers = [allh[r] for r in range(world) if r != me]
     M.messi_link_peers_ipc(index.handle, peers)
     return len(peers)
+
+
+def merge_knn(d2: torch.Tensor, gid: torch.Tensor, group=None):
+    """Exact cross-rank k-NN merge: d2 float64 [nq, k], gid int64 [nq, k] (local answers, -1 =
+    none) -> the k lexicographically smallest (d2, gid) of all ranks, per query."""
+    world = dist.get_world_size(group)
+    nq, k = d2.shape
+    packed = torch.stack([d2.contiguous().view(torch.int64), gid.to(torch.int64)], dim=2).contiguous()
+    home = packed.device
+    if dist.get_backend(group) == "gloo" and packed.is_cuda:
+        packed = packed.cpu()
+    parts = [torch.empty_like(packed) for _ in range(world)]
+    dist.all_gather(parts, packed, group=group)
+    allp = torch.cat(parts, dim=1).to(home)  # [nq, R k, 2]
+    ad = allp[:, :, 0].contiguous().view(torch.float64)
+    ag = allp[:, :, 1]
+    ad = torch.where(ag < 0, torch.full_like(ad, float("inf")), ad)
+    big = torch.iinfo(torch.int64).max
+    ag2 = torch.where(ag < 0, torch.full_like(ag, big), ag)
+    # lexicographic: sort by id, then stable sort by distance
+    o1 = torch.argsort(ag2, dim=1, stable=True)
+    ad1, ag1 = torch.gather(ad, 1, o1), torch.gather(ag2, 1, o1)
+    o2 = torch.argsort(ad1, dim=1, stable=True)
+    bd, bi = torch.gather(ad1, 1, o2)[:, :k], torch.gather(ag1, 1, o2)[:, :k]
+    bi = torch.where(bi == big, torch.full_like(bi, -1), bi)
+    return bd, bi

@@ -70,6 +70,9 @@ def lib():
         L.messi_query_dtw.argtypes = [vp, vp, i32, ctypes.POINTER(Result), vp]
         L.messi_query_ed_batch.argtypes = [vp, vp, i32, vp, vp]
         L.messi_query_dtw_batch.argtypes = [vp, vp, i32, i32, vp, vp]
+        if hasattr(L, "messi_query_ed_knn"):
+            L.messi_query_ed_knn.argtypes = [vp, vp, i32, vp, vp]
+            L.messi_query_ed_knn_batch.argtypes = [vp, vp, i32, i32, vp, vp]
         L.messi_free.argtypes = [vp]
         L.messi_free.restype = None
         L.messi_last_error.restype = ctypes.c_char_p
@@ -105,7 +108,7 @@ EXPORTED = ["messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_
             "messi_debug_summaries", "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances",
             "messi_debug_scan_repeat", "messi_debug_tile_bounds", "messi_debug_quantised",
             "messi_debug_coarse_bounds", "messi_batch_state_ipc", "messi_link_peers_ipc",
-            "messi_link_peers_local"]
+            "messi_link_peers_local", "messi_query_ed_knn", "messi_query_ed_knn_batch"]
 
 
 def _check(status: int):
@@ -182,6 +185,24 @@ def messi_link_peers_ipc(handle, peer_handles):
 def messi_link_peers_local(handle, peer_handles_list):
     arr = (ctypes.c_void_p * max(1, len(peer_handles_list)))(*[h.value for h in peer_handles_list])
     _check(lib().messi_link_peers_local(handle, arr, len(peer_handles_list)))
+
+
+def messi_query_ed_knn(handle, query, k: int, with_stats: bool = False):
+    """Exact k-NN (ED) of one query: (dist float64[k], id int64[k], d2 float64[k][, stats])."""
+    import numpy as np
+    q, keep = _query_ptr(query)
+    res = (Result * k)()
+    st = Stats()
+    _check(lib().messi_query_ed_knn(handle, q, int(k), res, ctypes.byref(st) if with_stats else None))
+    dist = np.array([r.dist for r in res]); ids = np.array([r.id for r in res], dtype=np.int64)
+    d2 = np.array([r.d2 for r in res])
+    return (dist, ids, d2, st.as_dict()) if with_stats else (dist, ids, d2)
+
+
+def messi_query_ed_knn_batch(handle, queries_dev: torch.Tensor, k: int, results_dev: torch.Tensor, stats_dev=None):
+    """results_dev: uint8 CUDA tensor of nq*k*32 bytes (result_buffer(nq * k))."""
+    _check(lib().messi_query_ed_knn_batch(handle, _ptr(queries_dev), queries_dev.shape[0], int(k), _ptr(results_dev),
+                                          _ptr(stats_dev)))
 
 
 def messi_free(handle):
@@ -358,6 +379,16 @@ class Index:
             messi_query_ed_batch(self.handle, queries_dev, results, stats)
         else:
             messi_query_dtw_batch(self.handle, queries_dev, reach, results, stats)
+        return results, stats
+
+    def query_knn(self, q, k: int, with_stats=False):
+        return messi_query_ed_knn(self.handle, q, k, with_stats)
+
+    def query_batch_knn(self, queries_dev: torch.Tensor, k: int, results=None, stats=None):
+        """Enqueue nq exact k-NN (ED) queries; results: nq*k entries (decode_results -> [nq*k])."""
+        nq = queries_dev.shape[0]
+        results = results if results is not None else result_buffer(nq * k, self.device)
+        messi_query_ed_knn_batch(self.handle, queries_dev, k, results, stats)
         return results, stats
 
     def launches(self) -> int:

@@ -71,3 +71,39 @@ def test_sharded_answers_equal_single_scan(world):
     d2, ids = oracle.nn("ed", X, Q)
     assert np.array_equal(gid, ids) and np.array_equal(gd2, d2)
     assert gid[0] == 5
+
+
+def _knn_worker(rank, world, port, X, Q, k, out):
+    from paper_2110_07519_b200.dist import merge_knn
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b, e = shard_range(X.shape[0], world, rank)
+    d2, ids = oracle.knn("ed", X[b:e], Q, k, row_begin=b)
+    gd2, gid = merge_knn(torch.from_numpy(d2), torch.from_numpy(ids))
+    if rank == 0:
+        out.put((gd2.numpy(), gid.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("k", [1, 7])
+def test_sharded_knn_merge_equals_single_scan(k):
+    """k-NN across 2 ranks (gloo): the merge of the local k lists is the global k list,
+    including cross-shard exact ties (lowest id first) and a shard with fewer than k rows."""
+    rng = np.random.default_rng(1)
+    X = rng.standard_normal((13, 16)).astype(np.float32)
+    X[10] = X[2]  # cross-shard duplicate
+    Q = np.concatenate([X[[10]], rng.standard_normal((3, 16)).astype(np.float32)])
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_knn_worker, args=(r, 2, port, X, Q, k, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    gd2, gid = out.get(timeout=120)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    d2, ids = oracle.knn("ed", X, Q, k)
+    assert np.array_equal(gid, ids) and np.array_equal(gd2, d2)
+    assert gid[0, 0] == 2

@@ -301,3 +301,24 @@ def test_nn_dtw_vs_brute_paths_tiny():
             ref = [brute_dtw(q, x, r) for x in X]
             assert ids[qi] == int(np.argmin(ref))
             assert math.isclose(d2[qi], min(ref), rel_tol=1e-12, abs_tol=1e-12)
+
+
+def test_knn_oracle_definition():
+    """oracle.knn against an independent numpy fp64 brute force (k smallest of the sum of
+    squares, ties to the lowest id), k = 1 against oracle.nn, and k > N padding."""
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((300, 24)).astype(np.float32)
+    X[250] = X[17]
+    Q = np.concatenate([X[[17]], rng.standard_normal((4, 24)).astype(np.float32)])
+    d2, ids = oracle.knn("ed", X, Q, 9)
+    for qi in range(Q.shape[0]):
+        ref = ((X.astype(np.float64) - Q[qi].astype(np.float64)) ** 2).sum(axis=1)
+        order = sorted(range(X.shape[0]), key=lambda i: (ref[i], i))[:9]
+        assert list(ids[qi]) == order
+        assert np.allclose(d2[qi], ref[order], rtol=1e-12, atol=0)
+    assert list(ids[0, :2]) == [17, 250] and d2[0, 0] == 0.0 and d2[0, 1] == 0.0
+    n1d, n1i = oracle.nn("ed", X, Q)
+    k1d, k1i = oracle.knn("ed", X, Q, 1)
+    assert np.array_equal(k1i[:, 0], n1i) and np.array_equal(k1d[:, 0], n1d)
+    pd, pi = oracle.knn("ed", X[:3], Q[:1], 5)
+    assert list(pi[0, 3:]) == [-1, -1] and np.all(np.isinf(pd[0, 3:]))
