@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=4_000_000, help="row sample of the oracle timing")
     ap.add_argument("--cpu-queries", type=int, default=32, help="queries of the oracle timing sample")
     ap.add_argument("--window", type=int, default=0, help="approximate-search window (0: library default 2000)")
+    ap.add_argument("--knn", type=int, default=10, help="ED: also time exact k-NN with this k (<= 1: skip)")
     ap.add_argument("--no-share-bsf", action="store_true",
                     help="N > 1: do not link the shards (no best-so-far sharing over peer memory)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -257,8 +258,33 @@ def run_arm(cfg, args, world, rank, dev, stream, time_steps, warmup):
         torch.cuda.synchronize()
         barrier(world)
         e2e_ms = e0.elapsed_time(e1)
+        # exact k-NN (f2) on the same index and queries: k = args.knn results per query
+        knn = None
+        if reach is None and args.knn > 1:
+            from paper_2110_07519_b200.dist import merge_knn
+            kres = M.result_buffer(nq * args.knn, dev)
+
+            def kstep():
+                idx.query_batch_knn(Q, args.knn, kres)
+                if world > 1:
+                    _, kid, kd2 = M.decode_results_device(kres)
+                    merge_knn(kd2.view(nq, args.knn), kid.view(nq, args.knn))
+
+            for _ in range(max(1, warmup)):
+                kstep()
+            torch.cuda.synchronize()
+            barrier(world)
+            k0 = torch.cuda.Event(enable_timing=True)
+            k1 = torch.cuda.Event(enable_timing=True)
+            k0.record(stream)
+            for _ in range(time_steps):
+                kstep()
+            k1.record(stream)
+            torch.cuda.synchronize()
+            barrier(world)
+            knn = k0.elapsed_time(k1)
     out = dict(ms=ms, build_ms=build_ms, launches=launches, prof=prof, prof_ms=prof_ms, stats=st, clocks=clk.summary(),
-               e2e_ms=e2e_ms, nq=nq, N_local=X.shape[0], n=cfg["n"], h2d=qh.numel() * 4, d2h=rh.numel())
+               e2e_ms=e2e_ms, knn_ms=knn, nq=nq, N_local=X.shape[0], n=cfg["n"], h2d=qh.numel() * 4, d2h=rh.numel())
     idx.close()
     del X, Q
     torch.cuda.empty_cache()
@@ -410,6 +436,10 @@ def ours(args):
                                              "abandoned", "near_best", "dtw_cells", "exact", "tiles_listed", "coarse",
                                              "seed_d2", "bsf_d2")},
     }
+    if main.get("knn_ms"):
+        kms = max_over_ranks(main["knn_ms"], world)
+        line["knn"] = {"k": args.knn, "value": K * nq / (kms / 1e3), "unit": "queries/s", "ms_per_step": kms / K,
+                       "what": "exact k-NN (ED) of the same queries on the same index, k results per query"}
     if args.mode == "dtw":
         line["roofline"] = dtw_roofline(main, K)
     if args.mode == "ed" and not args.no_dtw:
