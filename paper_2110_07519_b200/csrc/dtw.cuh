@@ -244,15 +244,37 @@ struct DtwThread {
         for (int u = 0; u < 4; ++u) nx[u] = hv[T + u];
         const float4 qv = *reinterpret_cast<const float4*>(q_s + i);
         const float qq[4] = {qv.x, qv.y, qv.z, qv.w};
+        // rows (0, 1) then (2, 3), each pair as a skewed wavefront: row u+1 runs two cells
+        // behind row u (its cell c needs row u's cells c and c+1), so one paired FFMA2
+        // finishes a cell of each row (Blackwell f32x2: half the FMA-pipe issue).  In-place:
+        // row u+1 overwrites D[c] only after row u has read it.
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            float left = INFINITY;
+        for (int u = 0; u < 4; u += 2) {
+            float lu = INFINITY, lv = INFINITY;
 #pragma unroll
-            for (int d = 0; d < W; ++d) {
-                const float mn = min3f(D[d], D[d + 1], left);
-                float df = qq[u] - cw[d + u];
-                left = fmaf(df, df, mn);
-                D[d] = left;
+            for (int dd = 0; dd < W + 2; ++dd) {
+                const int a = dd, c2 = dd - 2;
+                if (a < W && c2 >= 0) {
+                    const float mna = min3f(D[a], D[a + 1], lu);
+                    const float mnc = min3f(D[c2], D[c2 + 1], lv);
+                    const float dfa = qq[u] - cw[a + u];
+                    const float dfc = qq[u + 1] - cw[c2 + u + 1];
+                    const float2 r = ffma2(make_float2(dfa, dfc), make_float2(dfa, dfc), make_float2(mna, mnc));
+                    lu = r.x;
+                    lv = r.y;
+                    D[a] = lu;
+                    D[c2] = lv;
+                } else if (a < W) {
+                    const float mna = min3f(D[a], D[a + 1], lu);
+                    const float dfa = qq[u] - cw[a + u];
+                    lu = fmaf(dfa, dfa, mna);
+                    D[a] = lu;
+                } else {
+                    const float mnc = min3f(D[c2], D[c2 + 1], lv);
+                    const float dfc = qq[u + 1] - cw[c2 + u + 1];
+                    lv = fmaf(dfc, dfc, mnc);
+                    D[c2] = lv;
+                }
             }
         }
         float mn = D[0];
