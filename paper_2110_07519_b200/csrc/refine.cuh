@@ -135,48 +135,60 @@ __global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ ca
         unsigned todo = __ballot_sync(0xffffffffu, ok);
         unsigned passmask = 0;
         float mylbk = 0.0f, myhead = 0.0f;
+        // eight rows in flight per warp; per element d = c - clamp(c, L, U) (the LB_Keogh term
+        // c - U above the envelope, c - L below it, 0 inside: P:1392-1405), squares summed
+        // in element pairs with FFMA2
+        constexpr int G = 8;
         while (todo) {
-            int src[kRefineGroup];
-            unsigned id[kRefineGroup];
-            bool gok[kRefineGroup];
+            int src[G];
+            unsigned id[G];
+            bool gok[G];
 #pragma unroll
-            for (int g = 0; g < kRefineGroup; ++g) {
+            for (int g = 0; g < G; ++g) {
                 gok[g] = todo != 0;
                 src[g] = gok[g] ? __ffs(todo) - 1 : 0;
                 todo &= todo - 1;
                 id[g] = __shfl_sync(0xffffffffu, rid, src[g]);
             }
-            float acc[kRefineGroup], head[kRefineGroup];
+            float2 acc[G];
+            float head[G];
 #pragma unroll
-            for (int g = 0; g < kRefineGroup; ++g) acc[g] = head[g] = 0.0f;
-#pragma unroll 2
+            for (int g = 0; g < G; ++g) {
+                acc[g] = make_float2(0.0f, 0.0f);
+                head[g] = 0.0f;
+            }
             for (int j = lane * 4; j < n; j += 128) {
                 const float4 uv = *reinterpret_cast<const float4*>(U + j);
                 const float4 lv = *reinterpret_cast<const float4*>(L + j);
-                const float u[4] = {uv.x, uv.y, uv.z, uv.w}, l[4] = {lv.x, lv.y, lv.z, lv.w};
-                float4 cv[kRefineGroup];
+                float4 cv[G];
 #pragma unroll
-                for (int g = 0; g < kRefineGroup; ++g)
+                for (int g = 0; g < G; ++g)
                     cv[g] = gok[g] ? __ldg(reinterpret_cast<const float4*>(rows + (long long)id[g] * n + j))
                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                const bool in_head = j <= reach + 3;  // the columns of the DP's first window
 #pragma unroll
-                for (int g = 0; g < kRefineGroup; ++g) {
-                    const float c[4] = {cv[g].x, cv[g].y, cv[g].z, cv[g].w};
+                for (int g = 0; g < G; ++g) {
+                    const float d0 = cv[g].x - fminf(fmaxf(cv[g].x, lv.x), uv.x);
+                    const float d1 = cv[g].y - fminf(fmaxf(cv[g].y, lv.y), uv.y);
+                    const float d2 = cv[g].z - fminf(fmaxf(cv[g].z, lv.z), uv.z);
+                    const float d3 = cv[g].w - fminf(fmaxf(cv[g].w, lv.w), uv.w);
+                    acc[g] = ffma2(make_float2(d0, d1), make_float2(d0, d1), acc[g]);
+                    acc[g] = ffma2(make_float2(d2, d3), make_float2(d2, d3), acc[g]);
+                    if (in_head) {
+                        const float dd[4] = {d0, d1, d2, d3};
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        float d = c[k] > u[k] ? c[k] - u[k] : (c[k] < l[k] ? c[k] - l[k] : 0.0f);
-                        acc[g] = fmaf(d, d, acc[g]);
-                        if (j + k <= reach + 3) head[g] = fmaf(d, d, head[g]);
+                        for (int k = 0; k < 4; ++k)
+                            if (j + k <= reach + 3) head[g] = fmaf(dd[k], dd[k], head[g]);
                     }
                 }
             }
 #pragma unroll
-            for (int g = 0; g < kRefineGroup; ++g) {
-                acc[g] = warp_sum(acc[g]);
-                head[g] = warp_sum(head[g]);
-                if (gok[g] && acc[g] <= thr) {
+            for (int g = 0; g < G; ++g) {
+                const float a = warp_sum(acc[g].x + acc[g].y);
+                const float h = warp_sum(head[g]);
+                if (gok[g] && a <= thr) {
                     passmask |= 1u << src[g];
-                    if (lane == src[g]) { mylbk = acc[g]; myhead = head[g]; }
+                    if (lane == src[g]) { mylbk = a; myhead = h; }
                 }
             }
         }
