@@ -36,7 +36,7 @@ struct Slot {
     uint4* list2 = nullptr;   // DTW: LB_Keogh survivors (id, LBK, LBK of the first window, 0)  [lazy]
     unsigned* tlist = nullptr;  // tiles surviving the box filter
     NearEntry* near = nullptr;
-    cudaEvent_t ev_seed = nullptr, ev_scan = nullptr, ev_lbk = nullptr, ev_done = nullptr;
+    cudaEvent_t ev_seed = nullptr, ev_scan = nullptr, ev_lbk = nullptr, ev_refined = nullptr, ev_done = nullptr;
 };
 
 struct messi_index {
@@ -44,7 +44,8 @@ struct messi_index {
     cudaStream_t stream = nullptr;  // the caller's stream ("main": scans)
     cudaStream_t side = nullptr;    // library-owned: seeds
     cudaStream_t rstr = nullptr;    // library-owned: ED sub-batches; DTW LB_Keogh filter
-    cudaStream_t dstr = nullptr;    // library-owned: DTW refine / resolve (overlaps the next query's filter)
+    cudaStream_t dstr = nullptr;    // library-owned: DTW refine (overlaps the next query's filter)
+    cudaStream_t xstr = nullptr;    // library-owned: DTW exact resolve (overlaps the next query's refine)
     cudaEvent_t ev_fork = nullptr;
     int n = 0, window = 2000, keep_paa = 0;
     long long N = 0, ntiles = 0, row_begin = 0;
@@ -282,6 +283,7 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
         if (cudaEventCreateWithFlags(&sl.ev_seed, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&sl.ev_scan, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&sl.ev_lbk, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sl.ev_refined, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&sl.ev_done, cudaEventDisableTiming) != cudaSuccess)
             return bail(fail(MESSI_ECUDA, "event creation failed"));
     }
@@ -292,6 +294,7 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     if (cudaStreamCreateWithPriority(&idx->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&idx->rstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&idx->dstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&idx->xstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&idx->ev_fork, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(MESSI_ECUDA, "stream creation failed"));
 
@@ -362,6 +365,7 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->side) cudaStreamSynchronize(idx->side);
     if (idx->rstr) cudaStreamSynchronize(idx->rstr);
     if (idx->dstr) cudaStreamSynchronize(idx->dstr);
+    if (idx->xstr) cudaStreamSynchronize(idx->xstr);
     if (idx->stream) cudaStreamSynchronize(idx->stream);
     else cudaDeviceSynchronize();
     void* ptrs[] = {idx->tiles, idx->sym8, idx->boxes, idx->sboxes, idx->paa, idx->skey, idx->perm, idx->beta32, idx->lo_w,
@@ -381,7 +385,7 @@ extern "C" void messi_free(messi_index* idx)
         void* sp[] = {sl.st, sl.lut, sl.tab, sl.U, sl.L, sl.cand, sl.list2, sl.near, sl.tlist};
         for (void* p : sp)
             if (p) cudaFree(p);
-        cudaEvent_t es[] = {sl.ev_seed, sl.ev_scan, sl.ev_lbk, sl.ev_done};
+        cudaEvent_t es[] = {sl.ev_seed, sl.ev_scan, sl.ev_lbk, sl.ev_refined, sl.ev_done};
         for (cudaEvent_t e : es)
             if (e) cudaEventDestroy(e);
     }
@@ -389,6 +393,7 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->side && idx->side != idx->stream) cudaStreamDestroy(idx->side);
     if (idx->rstr && idx->rstr != idx->stream) cudaStreamDestroy(idx->rstr);
     if (idx->dstr && idx->dstr != idx->stream) cudaStreamDestroy(idx->dstr);
+    if (idx->xstr && idx->xstr != idx->stream) cudaStreamDestroy(idx->xstr);
     for (auto& e : idx->evs) {
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
@@ -407,6 +412,7 @@ static messi_status sync_all(messi_index* idx)
     CK(cudaStreamSynchronize(idx->side));
     CK(cudaStreamSynchronize(idx->rstr));
     CK(cudaStreamSynchronize(idx->dstr));
+    CK(cudaStreamSynchronize(idx->xstr));
     return MESSI_OK;
 }
 
@@ -475,10 +481,12 @@ static messi_status fork_streams(messi_index* idx)
             cudaStreamSynchronize(idx->side);
             cudaStreamSynchronize(idx->rstr);
             cudaStreamSynchronize(idx->dstr);
+            cudaStreamSynchronize(idx->xstr);
             cudaStreamDestroy(idx->side);
             cudaStreamDestroy(idx->rstr);
             cudaStreamDestroy(idx->dstr);
-            idx->side = idx->rstr = idx->dstr = idx->stream;
+            cudaStreamDestroy(idx->xstr);
+            idx->side = idx->rstr = idx->dstr = idx->xstr = idx->stream;
         }
         return MESSI_OK;
     }
@@ -486,6 +494,7 @@ static messi_status fork_streams(messi_index* idx)
     CK(cudaStreamWaitEvent(idx->side, idx->ev_fork, 0));
     CK(cudaStreamWaitEvent(idx->rstr, idx->ev_fork, 0));
     CK(cudaStreamWaitEvent(idx->dstr, idx->ev_fork, 0));
+    CK(cudaStreamWaitEvent(idx->xstr, idx->ev_fork, 0));
     return MESSI_OK;
 }
 
@@ -687,6 +696,10 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
         }
         LAUNCHED(idx);
     }
+    // the exact resolve of this query overlaps the next query's refine (another slot)
+    CK(cudaEventRecord(sl.ev_refined, rs));
+    rs = idx->xstr;
+    CK(cudaStreamWaitEvent(rs, sl.ev_refined, 0));
     {
         const size_t rw = (size_t)(3 * n + npad) * sizeof(double);
         const int wr = warps_for(rw, 8);
