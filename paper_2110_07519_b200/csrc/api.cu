@@ -193,7 +193,8 @@ static messi_status setup_kernels()
     CK(cudaFuncSetAttribute(k_scan_refine_ed<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(MESSI_MAX_N)));
     CK(cudaFuncSetAttribute(k_scan_refine_ed<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(MESSI_MAX_N)));
     CK(cudaFuncSetAttribute(k_filter_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, kFilterQ * kLutF * 4));
-    CK(cudaFuncSetAttribute(k_lbk_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_lbk_filter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_lbk_filter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_refine_dtw_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_resolve_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -669,7 +670,7 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     TRY(launch_scan(idx, sl));
     {
         ProfScope ps(idx, K_LBK, rs);
-        k_lbk_filter<<<refine_grid(idx, 2048), 256, lbk_smem(n), rs>>>(sl.cand, idx->perm, idx->rows, n, sl.U, sl.L,
+        k_lbk_filter<4><<<refine_grid(idx, 1024) * 2, 128, lbk_smem(n), rs>>>(sl.cand, idx->perm, idx->rows, n, sl.U, sl.L,
                                                                        reach, sl.st, sl.list2);
         LAUNCHED(idx);
     }

@@ -113,7 +113,8 @@ struct Best { double d; long long id; };
 // envelope-PAA bound) whose bound still does not exceed the BSF get the raw LB_Keogh
 // against the query envelope, four rows in flight per warp; survivors go to list2 as
 // (row id, LBK, LBK of columns 0 .. reach+3 -- the columns the DP's first window holds).
-__global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ cand, const unsigned* __restrict__ perm,
+template <int G>
+__global__ void __launch_bounds__(G == 8 ? 256 : 128, G == 8 ? 1 : 8) k_lbk_filter(const uint2* __restrict__ cand, const unsigned* __restrict__ perm,
                                                     const float* __restrict__ rows, int n, const float* __restrict__ U_g,
                                                     const float* __restrict__ L_g, int reach, QState* st,
                                                     uint4* __restrict__ list2)
@@ -135,10 +136,11 @@ __global__ void __launch_bounds__(256) k_lbk_filter(const uint2* __restrict__ ca
         unsigned todo = __ballot_sync(0xffffffffu, ok);
         unsigned passmask = 0;
         float mylbk = 0.0f, myhead = 0.0f;
-        // eight rows in flight per warp; per element d = c - clamp(c, L, U) (the LB_Keogh term
+        // G rows in flight per warp; per element d = c - clamp(c, L, U) (the LB_Keogh term
         // c - U above the envelope, c - L below it, 0 inside: P:1392-1405), squares summed
-        // in element pairs with FFMA2
-        constexpr int G = 8;
+        // in element pairs with FFMA2.  G = 4: 128-thread CTAs of <= 64 registers, which fit
+        // beside the resident refine kernel of the previous query (its 2 CTAs per SM leave
+        // 8.7K registers).
         while (todo) {
             int src[G];
             unsigned id[G];
