@@ -77,8 +77,26 @@ def test_config2_ed_10m():
         torch.cuda.empty_cache()
 
 
+def oracle_full_knn(X, Qh, k):
+    """k-NN brute force over every row of X, chunk by chunk (oracle.knn per chunk, then the
+    k lexicographically smallest (d2, id) of the chunk lists)."""
+    alld, alli = [], []
+    for b in range(0, X.shape[0], CHUNK):
+        part = X[b:b + CHUNK].cpu().numpy()
+        d, i = oracle.knn("ed", part, Qh, k, row_begin=b)
+        alld.append(d)
+        alli.append(i)
+    D, I = np.concatenate(alld, axis=1), np.concatenate(alli, axis=1)
+    out_d, out_i = np.empty((Qh.shape[0], k)), np.empty((Qh.shape[0], k), np.int64)
+    for qi in range(Qh.shape[0]):
+        o = np.lexsort((I[qi], D[qi]))[:k]
+        out_d[qi], out_i[qi] = D[qi, o], I[qi, o]
+    return out_d, out_i
+
+
 def test_config3_ed_100m():
-    """The bench workload: 100M x 256 on one GPU, 100 queries batched; 3 sampled in full."""
+    """The bench workload: 100M x 256 on one GPU, 100 queries batched; 3 sampled in full;
+    and exact 10-NN of one query against the oracle's brute force."""
     X, idx = build(100_000_000, 256, None)
     Q = torch.empty((100, 256), dtype=torch.float32, device=DEV)
     datagen.walks_cuda(Q, 0, seed=datagen.QUERY_SEED)
@@ -87,6 +105,15 @@ def test_config3_ed_100m():
         sample = [0, 42, 99]
         d2, ids = oracle_full("ed", X, Q[sample].cpu().numpy())
         check(tuple(t[sample] for t in got), d2, ids)
+        m = messi()
+        res = m.result_buffer(Q.shape[0] * 10, DEV)
+        with torch.cuda.stream(idx.stream):
+            idx.query_batch_knn(Q, 10, res)
+        torch.cuda.synchronize()
+        _, kid, kd2 = m.decode_results(res)
+        kd, ki = oracle_full_knn(X, Q[[7]].cpu().numpy(), 10)
+        assert np.array_equal(kid.numpy().reshape(-1, 10)[7], ki[0])
+        assert np.array_equal(kd2.numpy().reshape(-1, 10)[7], kd[0])
     finally:
         idx.close()
         del X
