@@ -684,8 +684,10 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
         bool launched = false;
 #define LAUNCH_R(R)                                                                                           \
     if (!launched && reach == R) {                                                                            \
-        k_refine_dtw<R><<<idx->sms * 8, 128, 3 * qsm, rs>>>(idx->rows, n, q_dev, sl.U, sl.L, sl.list2, sl.st, \
-                                                            sl.near);                                         \
+        int occ = 0;                                                                                          \
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_dtw<R>, 128, 3 * qsm));               \
+        k_refine_dtw<R><<<idx->sms * (occ > 0 ? occ : 1), 128, 3 * qsm, rs>>>(idx->rows, n, q_dev, sl.U, sl.L, \
+                                                                            sl.list2, sl.st, sl.near);        \
         launched = true;                                                                                      \
     }
         MESSI_DTW_REACHES(LAUNCH_R)

@@ -205,10 +205,50 @@ __global__ void __launch_bounds__(G == 8 ? 256 : 128, G == 8 ? 1 : 8) k_lbk_filt
     }
 }
 
+// Work distribution of the per-thread refine kernels: a lane that finishes (or skips) a
+// candidate takes the next one from its warp's chunk of list2 entries; chunks of kClaimChunk
+// consecutive entries are claimed with one atomicAdd on QState::next_tile, the next chunk one
+// chunk ahead so the warp never waits on the atomic.  Lanes thus stay busy until the list is
+// exhausted, whatever the spread of candidate lifetimes (early abandon after a few rows vs
+// the full n), where a static lane stride left most lanes of a warp idle behind its slowest.
+constexpr unsigned kClaimChunk = 64;
+
+struct WarpClaim {
+    unsigned cbase, cused, nbase;  // warp-uniform: current chunk, entries used, next chunk
+
+    __device__ __forceinline__ void init(unsigned* ctr, int lane)
+    {
+        unsigned a = 0, b = 0;
+        if (lane == 0) { a = atomicAdd(ctr, kClaimChunk); b = atomicAdd(ctr, kClaimChunk); }
+        cbase = __shfl_sync(0xffffffffu, a, 0);
+        nbase = __shfl_sync(0xffffffffu, b, 0);
+        cused = 0;
+    }
+
+    // Lanes of `m` (ballot of the lanes asking) get distinct entry indices.
+    __device__ __forceinline__ unsigned take(unsigned* ctr, unsigned m, int lane)
+    {
+        const unsigned cnt = __popc(m);
+        const unsigned pos = cused + __popc(m & ((1u << lane) - 1u));
+        unsigned k = cbase + pos;
+        if (cused + cnt > kClaimChunk) {  // warp-uniform: the chunk runs out
+            if (pos >= kClaimChunk) k = nbase + (pos - kClaimChunk);
+            cbase = nbase;
+            cused = cused + cnt - kClaimChunk;
+            unsigned b = 0;
+            if (lane == 0) b = atomicAdd(ctr, kClaimChunk);
+            nbase = __shfl_sync(0xffffffffu, b, 0);
+        } else {
+            cused += cnt;
+        }
+        return k;
+    }
+};
+
 // DTW step 2 (Alg. 10 line RealDist, P:1425 / P:1453 "true DTW distance"): banded fp32
-// DTW, one thread per LB_Keogh survivor (band in registers, DtwThread<R>), lanes striding
-// over list2.  Each lane keeps its own candidate; the loop runs while any lane has one, so
-// a lane that abandons early simply starts its next candidate.
+// DTW, one thread per LB_Keogh survivor (band in registers, DtwThread<R>), entries handed
+// out by WarpClaim.  Each lane holds its current candidate and the next two list2 entries
+// (nxt loaded, nxt2 in flight); the row of nxt is prefetched into L1.
 template <int R>
 __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
                                                     const float* __restrict__ U_g, const float* __restrict__ L_g,
@@ -221,76 +261,69 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
     float* L = dsm + 2 * npad;
     for (int i = threadIdx.x; i < n; i += blockDim.x) { q_s[i] = q_g[i]; U[i] = U_g[i]; L[i] = L_g[i]; }
     __syncthreads();
+    const int lane = threadIdx.x & 31;
     const unsigned total = *(volatile unsigned*)&st->list2_count;
-    const unsigned nthreads = gridDim.x * blockDim.x;
-    unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
-    DtwThread<R> dp;
-    bool have = k < total;
-    const float* c = rows;
-    unsigned id = 0, refined = 0, abandoned = 0, steps = 0, skipped = 0;
-    float lbk_total = 0.0f, head0 = 0.0f;
-    // The lane's next two candidates are fetched ahead (nxt = k + nthreads, nxt2 = k +
-    // 2 nthreads) and the head of the next row prefetched into L1, so a lane that restarts
-    // does not stall its warp on memory round trips.  The BSF is re-read every step, its
-    // load issued before the step's band work and used after it (a stale value is a larger
-    // threshold: safe).
-    const uint4 none = make_uint4(0u, 0u, 0u, 0u);
-    uint4 nxt = k + nthreads < total ? list2[k + nthreads] : none;
-    uint4 nxt2 = k + 2 * nthreads < total ? list2[k + 2 * nthreads] : none;
+    unsigned* ctr = &st->next_tile;
+    WarpClaim wc;
+    wc.init(ctr, lane);
+    const uint4 none = make_uint4(0xffffffffu, 0u, 0u, 0u);  // .x = ~0: no entry
+    auto fetch = [&](unsigned k) { return k < total ? list2[k] : none; };
+    uint4 nxt = fetch(wc.take(ctr, 0xffffffffu, lane));
+    uint4 nxt2 = fetch(wc.take(ctr, 0xffffffffu, lane));
     auto prefetch_row = [&](unsigned rid) {
         const char* pr = reinterpret_cast<const char*>(rows + (long long)rid * n);
         asm volatile("prefetch.global.L1 [%0];" ::"l"(pr));
         asm volatile("prefetch.global.L1 [%0];" ::"l"(pr + 128));
     };
-    if (k + nthreads < total) prefetch_row(nxt.x);
+    if (nxt.x != 0xffffffffu) prefetch_row(nxt.x);
+    DtwThread<R> dp;
+    const float* c = rows;
+    unsigned id = 0, refined = 0, abandoned = 0, steps = 0, skipped = 0;
+    float lbk_total = 0.0f;
     float thr = slack_up(ld_bsf(st));
-    // a candidate whose LB_Keogh already exceeds the current threshold is skipped unstarted
-    auto admit = [&](float lbk) { return lbk * 0.9990234375f <= thr; };
-    if (have) {
-        const uint4 e = list2[k];
-        id = e.x;
-        lbk_total = __uint_as_float(e.y);
-        c = rows + (long long)id * n;
-        dp.start(c, n, __uint_as_float(e.z));
-        ++refined;
-    }
-    while (__any_sync(0xffffffffu, have)) {
-        if (have) {
+    bool running = false;
+    for (;;) {
+        // lanes without a candidate take their next entry (a candidate whose LB_Keogh
+        // already exceeds the threshold is skipped unstarted)
+        const bool need = !running && nxt.x != 0xffffffffu;
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        if (m) {
+            const unsigned k = wc.take(ctr, m, lane);
+            if (need) {
+                id = nxt.x;
+                lbk_total = __uint_as_float(nxt.y);
+                const float head = __uint_as_float(nxt.z);
+                nxt = nxt2;
+                nxt2 = fetch(k);
+                if (nxt.x != 0xffffffffu) prefetch_row(nxt.x);
+                if (lbk_total * 0.9990234375f <= thr) {
+                    c = rows + (long long)id * n;
+                    dp.start(c, n, head);
+                    ++refined;
+                    running = true;
+                } else {
+                    ++skipped;
+                }
+            }
+        }
+        if (!__any_sync(0xffffffffu, running || nxt.x != 0xffffffffu)) break;
+        if (running) {
             const unsigned bsf_bits = *(volatile const unsigned*)&st->bsf_bits;  // consumed after the step
             const float rowmin = dp.step4(c, n, q_s, U, L);
             ++steps;
             thr = fminf(thr, slack_up(__uint_as_float(bsf_bits)));
             const float tail = fmaxf(0.0f, lbk_total * 0.9990234375f - dp.seen_lo * 1.0009765625f);
             const float bound = (rowmin + tail) * 0.9990234375f;
-            bool done = false;
-            if (bound > thr) { done = true; ++abandoned; }
-            if (!done && dp.i >= n) {
-                done = true;
+            if (bound > thr) {
+                running = false;
+                ++abandoned;
+            } else if (dp.i >= n) {
+                running = false;
                 const float d = dp.result();
                 if (d <= thr) {
                     bsf_update(st, d);
                     append_near(st, near, id, d);
                     thr = fminf(thr, slack_up(d));
-                }
-            }
-            if (done) {
-                for (;;) {
-                    k += nthreads;
-                    have = k < total;
-                    if (!have) break;
-                    id = nxt.x;
-                    lbk_total = __uint_as_float(nxt.y);
-                    head0 = __uint_as_float(nxt.z);
-                    nxt = nxt2;
-                    if (k + 2 * nthreads < total) nxt2 = list2[k + 2 * nthreads];
-                    if (k + nthreads < total && admit(__uint_as_float(nxt.y))) prefetch_row(nxt.x);
-                    if (admit(lbk_total)) break;
-                    ++skipped;
-                }
-                if (have) {
-                    c = rows + (long long)id * n;
-                    dp.start(c, n, head0);
-                    ++refined;
                 }
             }
         }
