@@ -45,6 +45,8 @@ struct messi_index {
     cudaStream_t side = nullptr;    // library-owned: seeds
     cudaStream_t rstr = nullptr;    // library-owned: ED sub-batches; DTW LB_Keogh filter
     cudaStream_t dstr = nullptr;    // library-owned: DTW refine (overlaps the next query's filter)
+    cudaStream_t dstr2 = nullptr;   // library-owned: DTW refine of the other slot (its start overlaps
+                                    // the tail of the previous query's refine)
     cudaStream_t xstr = nullptr;    // library-owned: DTW exact resolve (overlaps the next query's refine)
     cudaEvent_t ev_fork = nullptr;
     int n = 0, window = 2000, keep_paa = 0;
@@ -180,6 +182,55 @@ struct ProfScope {
 // Reaches with a register-band DTW instantiation (DtwThread<R>); others use the warp path.
 #define MESSI_DTW_REACHES(X) X(2) X(5) X(12) X(25)
 
+// Strip DTW instantiations (rows per strip H, REM = (2R - 2H + 3) mod H): H = 8 for R >= 7,
+// 4 for R in [3, 6], 2 for R in [1, 2].
+#define MESSI_STRIP_VARIANTS(X) \
+    X(8, 0) X(8, 1) X(8, 2) X(8, 3) X(8, 4) X(8, 5) X(8, 6) X(8, 7) X(4, 0) X(4, 1) X(4, 2) X(4, 3) X(2, 0) X(2, 1)
+static const int kStripSmemMax = 227 * 1024;
+
+static int strip_rows(int R)
+{
+    const char* e = getenv("MESSI_DTW_STRIP_H");  // experiments: rows per strip (8, 4, 2)
+    const int h = e ? atoi(e) : 0;
+    if ((h == 8 || h == 4 || h == 2) && R >= h - 1) return h;
+    return R >= 7 ? 8 : (R >= 3 ? 4 : 2);
+}
+
+// Which refine kernel serves reach R: the register band (DtwThread<R>) where instantiated,
+// else the strip kernel when its shared memory fits (R >= 1), else the warp wavefront.
+// MESSI_DTW_STRIP=1 / 0 forces the strip kernel on / off (experiments).
+static bool use_strip(int n, int R, bool have_band)
+{
+    const char* e = getenv("MESSI_DTW_STRIP");  // read per launch: tests switch it
+    const int force = e ? atoi(e) : -1;
+    const bool fits = R >= 1 && strip_smem(n, R) <= (size_t)kStripSmemMax;
+    if (force == 0) return false;
+    if (force == 1) return fits;
+    return fits && !have_band;
+}
+
+static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R, const float* q_dev, cudaStream_t rs)
+{
+    const int H = strip_rows(R);
+    const int rem = (2 * R - 2 * H + 3) % H;
+    const size_t smem = strip_smem(n, R);
+    bool launched = false;
+#define LAUNCH_S(HH, REM)                                                                                        \
+    if (!launched && H == HH && rem == REM) {                                                                   \
+        int occ = 0;                                                                                             \
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_dtw_strip<HH, REM>, kStripThreads, smem)); \
+        const char* oe = getenv("MESSI_DTW_REFINE_OCC"); /* experiments: CTAs per SM */                          \
+        if (oe && atoi(oe) > 0 && atoi(oe) < occ) occ = atoi(oe);                                                \
+        k_refine_dtw_strip<HH, REM><<<idx->sms * (occ > 0 ? occ : 1), kStripThreads, smem, rs>>>(                \
+            idx->rows, n, R, q_dev, sl.U, sl.L, sl.list2, (unsigned)idx->N, sl.st, sl.near);                     \
+        launched = true;                                                                                         \
+    }
+    MESSI_STRIP_VARIANTS(LAUNCH_S)
+#undef LAUNCH_S
+    if (!launched) return fail(MESSI_EINVAL, "no strip DTW variant for reach %d", R);
+    return MESSI_OK;
+}
+
 static size_t scan_smem() { return kScanLutBytes; }
 static size_t lbk_smem(int n) { return 2 * (size_t)((n + 3) & ~3) * sizeof(float); }
 
@@ -198,6 +249,9 @@ static messi_status setup_kernels()
     CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_refine_dtw_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_resolve_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+#define SET_ATTR_S(H, REM) CK(cudaFuncSetAttribute(k_refine_dtw_strip<H, REM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStripSmemMax));
+    MESSI_STRIP_VARIANTS(SET_ATTR_S)
+#undef SET_ATTR_S
 #define SET_ATTR_R(R) CK(cudaFuncSetAttribute(k_refine_dtw<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
     MESSI_DTW_REACHES(SET_ATTR_R)
 #undef SET_ATTR_R
@@ -295,6 +349,7 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     if (cudaStreamCreateWithPriority(&idx->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&idx->rstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&idx->dstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&idx->dstr2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&idx->xstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&idx->ev_fork, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(MESSI_ECUDA, "stream creation failed"));
@@ -366,6 +421,7 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->side) cudaStreamSynchronize(idx->side);
     if (idx->rstr) cudaStreamSynchronize(idx->rstr);
     if (idx->dstr) cudaStreamSynchronize(idx->dstr);
+    if (idx->dstr2) cudaStreamSynchronize(idx->dstr2);
     if (idx->xstr) cudaStreamSynchronize(idx->xstr);
     if (idx->stream) cudaStreamSynchronize(idx->stream);
     else cudaDeviceSynchronize();
@@ -394,6 +450,7 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->side && idx->side != idx->stream) cudaStreamDestroy(idx->side);
     if (idx->rstr && idx->rstr != idx->stream) cudaStreamDestroy(idx->rstr);
     if (idx->dstr && idx->dstr != idx->stream) cudaStreamDestroy(idx->dstr);
+    if (idx->dstr2 && idx->dstr2 != idx->stream) cudaStreamDestroy(idx->dstr2);
     if (idx->xstr && idx->xstr != idx->stream) cudaStreamDestroy(idx->xstr);
     for (auto& e : idx->evs) {
         cudaEventDestroy(e.a);
@@ -413,6 +470,7 @@ static messi_status sync_all(messi_index* idx)
     CK(cudaStreamSynchronize(idx->side));
     CK(cudaStreamSynchronize(idx->rstr));
     CK(cudaStreamSynchronize(idx->dstr));
+    CK(cudaStreamSynchronize(idx->dstr2));
     CK(cudaStreamSynchronize(idx->xstr));
     return MESSI_OK;
 }
@@ -465,6 +523,18 @@ static int refine_grid(const messi_index* idx, int per_block_rows)
     return (int)(need < cap ? (need < 1 ? 1 : need) : cap);
 }
 
+// The LB_Keogh filter's front bin: survivors with LBK <= front * BSF0 are refined first
+// (MESSI_DTW_FRONT overrides, for experiments; 0 = one bin in filter order).
+static float dtw_front()
+{
+    static float v = -1.0f;
+    if (v < 0.0f) {
+        const char* e = getenv("MESSI_DTW_FRONT");
+        v = e ? (float)atof(e) : 0.5f;
+    }
+    return v;
+}
+
 // MESSI_SERIAL=1 (experiments): every stage on the caller's stream, no overlap.
 static bool serial_mode()
 {
@@ -482,12 +552,14 @@ static messi_status fork_streams(messi_index* idx)
             cudaStreamSynchronize(idx->side);
             cudaStreamSynchronize(idx->rstr);
             cudaStreamSynchronize(idx->dstr);
+            cudaStreamSynchronize(idx->dstr2);
             cudaStreamSynchronize(idx->xstr);
             cudaStreamDestroy(idx->side);
             cudaStreamDestroy(idx->rstr);
             cudaStreamDestroy(idx->dstr);
+            cudaStreamDestroy(idx->dstr2);
             cudaStreamDestroy(idx->xstr);
-            idx->side = idx->rstr = idx->dstr = idx->xstr = idx->stream;
+            idx->side = idx->rstr = idx->dstr = idx->dstr2 = idx->xstr = idx->stream;
         }
         return MESSI_OK;
     }
@@ -495,6 +567,7 @@ static messi_status fork_streams(messi_index* idx)
     CK(cudaStreamWaitEvent(idx->side, idx->ev_fork, 0));
     CK(cudaStreamWaitEvent(idx->rstr, idx->ev_fork, 0));
     CK(cudaStreamWaitEvent(idx->dstr, idx->ev_fork, 0));
+    CK(cudaStreamWaitEvent(idx->dstr2, idx->ev_fork, 0));
     CK(cudaStreamWaitEvent(idx->xstr, idx->ev_fork, 0));
     return MESSI_OK;
 }
@@ -671,23 +744,32 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     {
         ProfScope ps(idx, K_LBK, rs);
         k_lbk_filter<4><<<refine_grid(idx, 1024) * 2, 128, lbk_smem(n), rs>>>(sl.cand, idx->perm, idx->rows, n, sl.U, sl.L,
-                                                                       reach, sl.st, sl.list2);
+                                                                       reach, sl.st, sl.list2,
+                                                                       (unsigned)idx->N, dtw_front());
         LAUNCHED(idx);
     }
     // the refine and the resolve run on their own stream: the LB_Keogh filter of the next
     // query (bandwidth-bound) overlaps this query's band DP (latency / ALU-bound)
     CK(cudaEventRecord(sl.ev_lbk, rs));
-    rs = idx->dstr;
+    rs = (idx->qcount & 1) ? idx->dstr : idx->dstr2;  // qcount was advanced for this query
     CK(cudaStreamWaitEvent(rs, sl.ev_lbk, 0));
     {
         ProfScope ps(idx, K_REFINE, rs);
-        bool launched = false;
+        bool launched = false, band = false;
+#define HAVE_R(R) band = band || reach == R;
+        MESSI_DTW_REACHES(HAVE_R)
+#undef HAVE_R
+        if (use_strip(n, reach, band)) {
+            TRY(launch_strip(idx, sl, n, reach, q_dev, rs));
+            launched = true;
+        }
 #define LAUNCH_R(R)                                                                                           \
     if (!launched && reach == R) {                                                                            \
         int occ = 0;                                                                                          \
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_dtw<R>, 128, 3 * qsm));               \
         k_refine_dtw<R><<<idx->sms * (occ > 0 ? occ : 1), 128, 3 * qsm, rs>>>(idx->rows, n, q_dev, sl.U, sl.L, \
-                                                                            sl.list2, sl.st, sl.near);        \
+                                                                            sl.list2, (unsigned)idx->N, sl.st, \
+                                                                            sl.near);                         \
         launched = true;                                                                                      \
     }
         MESSI_DTW_REACHES(LAUNCH_R)
@@ -695,7 +777,7 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
         if (!launched) {
             const int wr = warps_for((size_t)4 * npad * sizeof(float), 8);
             k_refine_dtw_warp<<<idx->sms * 4, 32 * wr, qsm + (size_t)wr * 4 * npad * sizeof(float), rs>>>(
-                idx->rows, n, reach, q_dev, sl.list2, sl.st, sl.near);
+                idx->rows, n, reach, q_dev, sl.list2, (unsigned)idx->N, sl.st, sl.near);
         }
         LAUNCHED(idx);
     }

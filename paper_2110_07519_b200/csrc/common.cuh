@@ -47,6 +47,7 @@ struct QState {
     double ubar[16], lbar[16];  // query PAA (ED: both) or envelope PAA (DTW), fp64
     unsigned char zlo[16], zhi[16];  // batch ED: per segment, the symbols whose table entry is 0
     unsigned lbk_thr_bits;  // DTW: the scan's threshold (BSF0), used by the LB_Keogh filter
+    unsigned list2_back;    // DTW: LB_Keogh survivors appended from the back of list2 (larger LBK)
 };
 
 struct NearEntry { unsigned id; float d32; };
@@ -80,6 +81,7 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->seed_bits = 0x7f800000u;
     st->cand_count = 0;
     st->list2_count = 0;
+    st->list2_back = 0;
     st->near_count = 0;
     st->refined = 0;
     st->abandoned = 0;

@@ -4,6 +4,8 @@
 #pragma once
 #include "common.cuh"
 
+#include <utility>
+
 namespace messi {
 
 // Squared ED in fp32, one warp: lane handles float4 chunks lane*4 + 128k, then a butterfly
@@ -297,6 +299,130 @@ struct DtwThread {
     }
 
     __device__ __forceinline__ float result() const { return D[R]; }
+};
+
+
+// ------------------------------------------------------------------ strip DTW (any reach)
+// Banded DTW in fp32, one thread per candidate, for ANY reach R >= H - 1, with O(H)
+// registers.  DTW is symmetric in its two series, so the thread walks the CANDIDATE's points
+// as rows j (read from global memory, H at a time) and the query's as columns i:
+//     D(j, i) = (q_i - c_j)^2 + min(D(j-1, i-1), D(j-1, i), D(j, i-1)),  |i - j| <= R,
+// the same cell arithmetic as DtwThread (fl(d*d + min) with d = fl(q_i - c_j)), so the fp32
+// value of every cell -- and the distance -- is the same as there.
+// Rows go in strips of H.  Inside a strip row u runs one column behind row u-1 (at step t
+// row u is at column j0 - R + t - u), so the H cells of a step are independent (paired
+// FFMA2) and each needs only values of the previous two steps, held in registers:
+//     left = row u at t-1, up = row u-1 at t-1, diag = row u-1 at t-2.
+// Row 0 reads the previous strip's last row, and row H-1 writes this strip's, from/to a
+// per-thread boundary array B of 2R+2 slots in shared memory (slot x of strip j0 = column
+// j0 - R - 1 + x; thread-interleaved, so conflict-free); slot 2R+1 stays +inf (the cell
+// right of the band).  The query comes from shared memory padded with +inf outside
+// [0, n) (so cells outside the matrix are +inf), in 8 lane-interleaved copies.  Row u is
+// active at steps [2u, 2u + 2R]: the first 2H-2 steps (prologue) and the last 2H-2
+// (epilogue) are unrolled with their active rows fixed at compile time, the 2R - 2H + 3
+// steps between them run in H-step chunks (the query window rotates through H registers)
+// plus REM = (2R - 2H + 3) mod H single steps (a template parameter).
+constexpr int kStripThreads = 128;
+constexpr int kStripQCopies = 8;
+
+template <int... Is, class F>
+__device__ __forceinline__ void static_for_impl(std::integer_sequence<int, Is...>, F&& f)
+{
+    (f(std::integral_constant<int, Is>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f)
+{
+    static_for_impl(std::make_integer_sequence<int, N>{}, f);
+}
+
+template <int H>
+struct DtwStrip {
+    float S[2][H];  // row values at steps of parity 0 / 1
+    float Qw[H];    // query window: Qw[t % H] = q at row 0's column of step t
+    float cv[H];    // candidate points of the strip's rows
+    float bprev;    // row 0's diagonal input (boundary slot of the previous step)
+    float rmin;     // min over row H-1 (the strip's last row)
+
+    // One step t (compile-time facts: PH = t % H, PAR = t & 1, active rows [LO, HI],
+    // whether row H-1 writes the boundary).  bsrc: boundary slot t+1 (read when row 0 is
+    // active), qsrc: query column j0 - R + t, bdst: boundary slot t - 2H + 2.
+    template <int PH, int PAR, int LO, int HI>
+    __device__ __forceinline__ void step(const float* bsrc, const float* qsrc, float* bdst)
+    {
+        float up0 = 0.0f, dg0 = 0.0f;
+        if constexpr (LO == 0) {
+            up0 = *bsrc;
+            dg0 = bprev;
+            bprev = up0;
+        }
+        Qw[PH] = *qsrc;
+        float nv[H];
+        static_for<(HI - LO + 2) / 2>([&](auto P) {
+            constexpr int u = LO + 2 * decltype(P)::value;
+            constexpr int v = u + 1;
+            const float upu = u == 0 ? up0 : S[PAR ^ 1][u == 0 ? 0 : u - 1];
+            const float dgu = u == 0 ? dg0 : S[PAR][u == 0 ? 0 : u - 1];
+            const float mnu = min3f(dgu, upu, S[PAR ^ 1][u]);
+            const float dfu = Qw[(PH - u + 2 * H) % H] - cv[u];
+            if constexpr (v <= HI) {
+                const float mnv = min3f(S[PAR][u], S[PAR ^ 1][u], S[PAR ^ 1][v]);
+                const float dfv = Qw[(PH - v + 2 * H) % H] - cv[v];
+                const float2 r = ffma2(make_float2(dfu, dfv), make_float2(dfu, dfv), make_float2(mnu, mnv));
+                nv[u] = r.x;
+                nv[v] = r.y;
+            } else {
+                nv[u] = fmaf(dfu, dfu, mnu);
+            }
+        });
+#pragma unroll
+        for (int u = 0; u < H; ++u) {
+            if (u >= LO && u <= HI) S[PAR][u] = nv[u];
+            else if (u < LO) S[PAR][u] = INFINITY;  // finished rows read as out of band
+        }
+        if constexpr (HI == H - 1) {
+            *bdst = nv[H - 1];
+            rmin = fminf(rmin, nv[H - 1]);
+        }
+    }
+
+    // All steps of the strip of rows j0 .. j0+H-1 (cv loaded).  Bt: this thread's boundary
+    // slot 0; qt: the query copy at column j0 - R; nfull = (2R - 2H + 3) / H.
+    template <int REM>
+    __device__ __forceinline__ void run(float* Bt, const float* qt, int R, int nfull)
+    {
+        constexpr int T = kStripThreads, K = kStripQCopies;
+#pragma unroll
+        for (int u = 0; u < H; ++u) S[0][u] = S[1][u] = INFINITY;
+        bprev = Bt[0];
+        rmin = INFINITY;
+        static_for<2 * H - 2>([&](auto I) {  // prologue: rows 0 .. t/2
+            constexpr int t = decltype(I)::value;
+            step<t % H, t & 1, 0, t / 2>(Bt + (t + 1) * T, qt + t * K, nullptr);
+        });
+        float* bp = Bt + (2 * H - 1) * T;
+        const float* qp = qt + (2 * H - 2) * K;
+        float* wp = Bt;
+        for (int c = 0; c < nfull; ++c) {
+            static_for<H>([&](auto I) {
+                constexpr int k = decltype(I)::value;
+                step<(2 * H - 2 + k) % H, k & 1, 0, H - 1>(bp + k * T, qp + k * K, wp + k * T);
+            });
+            bp += H * T;
+            qp += H * K;
+            wp += H * T;
+        }
+        static_for<REM>([&](auto I) {
+            constexpr int k = decltype(I)::value;
+            step<(2 * H - 2 + k) % H, k & 1, 0, H - 1>(bp + k * T, qp + k * K, wp + k * T);
+        });
+        float* we = wp + REM * T;                 // boundary slot of step 2R+1
+        const float* qe = qt + 2 * R * K;         // query column of step 2R
+        static_for<2 * H - 2>([&](auto I) {  // epilogue: rows (t+1)/2 .. H-1 at step 2R + t
+            constexpr int t = decltype(I)::value + 1;
+            step<(REM + 3 * H - 3 + t) % H, t & 1, (t + 1) / 2, H - 1>(nullptr, qe + t * K, we + (t - 1) * T);
+        });
+    }
 };
 
 }  // namespace messi

@@ -113,11 +113,20 @@ struct Best { double d; long long id; };
 // envelope-PAA bound) whose bound still does not exceed the BSF get the raw LB_Keogh
 // against the query envelope, four rows in flight per warp; survivors go to list2 as
 // (row id, LBK, LBK of columns 0 .. reach+3 -- the columns the DP's first window holds).
+// Best-first in two bins (the priority-queue order of MESSI, coarsened):
+// survivors with LBK <= front * BSF0 are appended at the front of list2, the others from
+// its back end (capacity cap), so the refine -- which hands entries out in list order --
+// starts the candidates most likely to be near (and to run longest) first.
+__device__ __forceinline__ uint4 list2_at(const uint4* __restrict__ list2, unsigned k, unsigned nfront, unsigned cap)
+{
+    return k < nfront ? list2[k] : list2[cap - 1u - (k - nfront)];
+}
+
 template <int G>
 __global__ void __launch_bounds__(G == 8 ? 256 : 128, G == 8 ? 1 : 8) k_lbk_filter(const uint2* __restrict__ cand, const unsigned* __restrict__ perm,
                                                     const float* __restrict__ rows, int n, const float* __restrict__ U_g,
                                                     const float* __restrict__ L_g, int reach, QState* st,
-                                                    uint4* __restrict__ list2)
+                                                    uint4* __restrict__ list2, unsigned cap, float front)
 {
     extern __shared__ __align__(16) float env[];
     float* U = env;
@@ -134,7 +143,7 @@ __global__ void __launch_bounds__(G == 8 ? 256 : 128, G == 8 ? 1 : 8) k_lbk_filt
         const bool ok = valid && __uint_as_float(e.y) <= thr;
         const unsigned rid = ok ? perm[e.x] : 0u;
         unsigned todo = __ballot_sync(0xffffffffu, ok);
-        unsigned passmask = 0;
+        unsigned passmask = 0, frontmask = 0;
         float mylbk = 0.0f, myhead = 0.0f;
         // G rows in flight per warp; per element d = c - clamp(c, L, U) (the LB_Keogh term
         // c - U above the envelope, c - L below it, 0 inside: P:1392-1405), squares summed
@@ -190,17 +199,24 @@ __global__ void __launch_bounds__(G == 8 ? 256 : 128, G == 8 ? 1 : 8) k_lbk_filt
                 const float h = warp_sum(head[g]);
                 if (gok[g] && a <= thr) {
                     passmask |= 1u << src[g];
+                    if (a <= thr * front) frontmask |= 1u << src[g];
                     if (lane == src[g]) { mylbk = a; myhead = h; }
                 }
             }
         }
         if (passmask) {
-            unsigned base = 0;
-            if (lane == 0) base = atomicAdd(&st->list2_count, (unsigned)__popc(passmask));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (passmask & (1u << lane))
-                list2[base + __popc(passmask & ((1u << lane) - 1))] =
-                    make_uint4(rid, __float_as_uint(mylbk), __float_as_uint(myhead), 0u);
+            const unsigned backmask = passmask & ~frontmask;
+            unsigned fb = 0, bb = 0;
+            if (lane == 0) {
+                if (frontmask) fb = atomicAdd(&st->list2_count, (unsigned)__popc(frontmask));
+                if (backmask) bb = atomicAdd(&st->list2_back, (unsigned)__popc(backmask));
+            }
+            fb = __shfl_sync(0xffffffffu, fb, 0);
+            bb = __shfl_sync(0xffffffffu, bb, 0);
+            const unsigned lt = (1u << lane) - 1u;
+            const uint4 e = make_uint4(rid, __float_as_uint(mylbk), __float_as_uint(myhead), 0u);
+            if (frontmask & (1u << lane)) list2[fb + __popc(frontmask & lt)] = e;
+            if (backmask & (1u << lane)) list2[cap - 1u - (bb + __popc(backmask & lt))] = e;
         }
     }
 }
@@ -214,14 +230,15 @@ __global__ void __launch_bounds__(G == 8 ? 256 : 128, G == 8 ? 1 : 8) k_lbk_filt
 constexpr unsigned kClaimChunk = 64;
 
 struct WarpClaim {
-    unsigned cbase, cused, nbase;  // warp-uniform: current chunk, entries used, next chunk
+    unsigned cbase, cused;  // warp-uniform: current chunk, entries used
+    unsigned nraw;          // lane 0: the next chunk (its atomic's result, read one chunk later)
 
     __device__ __forceinline__ void init(unsigned* ctr, int lane)
     {
-        unsigned a = 0, b = 0;
-        if (lane == 0) { a = atomicAdd(ctr, kClaimChunk); b = atomicAdd(ctr, kClaimChunk); }
+        unsigned a = 0;
+        nraw = 0;
+        if (lane == 0) { a = atomicAdd(ctr, kClaimChunk); nraw = atomicAdd(ctr, kClaimChunk); }
         cbase = __shfl_sync(0xffffffffu, a, 0);
-        nbase = __shfl_sync(0xffffffffu, b, 0);
         cused = 0;
     }
 
@@ -232,12 +249,11 @@ struct WarpClaim {
         const unsigned pos = cused + __popc(m & ((1u << lane) - 1u));
         unsigned k = cbase + pos;
         if (cused + cnt > kClaimChunk) {  // warp-uniform: the chunk runs out
+            const unsigned nbase = __shfl_sync(0xffffffffu, nraw, 0);
             if (pos >= kClaimChunk) k = nbase + (pos - kClaimChunk);
             cbase = nbase;
             cused = cused + cnt - kClaimChunk;
-            unsigned b = 0;
-            if (lane == 0) b = atomicAdd(ctr, kClaimChunk);
-            nbase = __shfl_sync(0xffffffffu, b, 0);
+            if (lane == 0) nraw = atomicAdd(ctr, kClaimChunk);  // consumed at the next overflow
         } else {
             cused += cnt;
         }
@@ -252,7 +268,8 @@ struct WarpClaim {
 template <int R>
 __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
                                                     const float* __restrict__ U_g, const float* __restrict__ L_g,
-                                                    const uint4* __restrict__ list2, QState* st, NearEntry* near)
+                                                    const uint4* __restrict__ list2, unsigned cap, QState* st,
+                                                    NearEntry* near)
 {
     extern __shared__ __align__(16) float dsm[];
     const int npad = (n + 3) & ~3;
@@ -262,12 +279,13 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
     for (int i = threadIdx.x; i < n; i += blockDim.x) { q_s[i] = q_g[i]; U[i] = U_g[i]; L[i] = L_g[i]; }
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const unsigned total = *(volatile unsigned*)&st->list2_count;
+    const unsigned nfront = *(volatile unsigned*)&st->list2_count;
+    const unsigned total = nfront + *(volatile unsigned*)&st->list2_back;
     unsigned* ctr = &st->next_tile;
     WarpClaim wc;
     wc.init(ctr, lane);
     const uint4 none = make_uint4(0xffffffffu, 0u, 0u, 0u);  // .x = ~0: no entry
-    auto fetch = [&](unsigned k) { return k < total ? list2[k] : none; };
+    auto fetch = [&](unsigned k) { return k < total ? list2_at(list2, k, nfront, cap) : none; };
     uint4 nxt = fetch(wc.take(ctr, 0xffffffffu, lane));
     uint4 nxt2 = fetch(wc.take(ctr, 0xffffffffu, lane));
     auto prefetch_row = [&](unsigned rid) {
@@ -338,6 +356,145 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
     }
 }
 
+// Shared memory of k_refine_dtw_strip: the boundary arrays (2R+2 slots x kStripThreads),
+// the query padded by R points of +inf on each side in kStripQCopies lane copies, U, L.
+__host__ __device__ inline size_t strip_smem(int n, int R)
+{
+    const size_t npad = (size_t)((n + 3) & ~3);
+    return ((size_t)(2 * R + 2) * kStripThreads + (size_t)(n + 2 * R) * kStripQCopies + 2 * npad) * sizeof(float);
+}
+
+// DTW step 2 for any reach (DtwStrip<H>, one thread per LB_Keogh survivor), the same
+// candidate hand-out, BSF sharing and early abandon as k_refine_dtw: after each strip of
+// H rows every warping path still has to cross its last row (>= rmin) and visit every
+// later candidate point j at least once, at a cost >= that point's LB_Keogh term against
+// the query envelope, so the candidate is dropped when rmin + (LBK_total -
+// LBK of the rows done) exceeds the threshold (2^-10 margins for the fp32 sums).
+template <int H, int REM>
+__global__ void __launch_bounds__(kStripThreads) k_refine_dtw_strip(const float* __restrict__ rows, int n, int R,
+                                                                   const float* __restrict__ q_g,
+                                                                   const float* __restrict__ U_g,
+                                                                   const float* __restrict__ L_g,
+                                                                   const uint4* __restrict__ list2, unsigned cap,
+                                                                   QState* st, NearEntry* near)
+{
+    extern __shared__ __align__(16) float dsm[];
+    constexpr int T = kStripThreads, K = kStripQCopies;
+    const int npad = (n + 3) & ~3;
+    float* qrep = dsm + (size_t)(2 * R + 2) * T;
+    float* U = qrep + (size_t)(n + 2 * R) * K;
+    float* L = U + npad;
+    for (int x = threadIdx.x; x < (n + 2 * R) * K; x += T) {
+        const int i = x / K - R;
+        qrep[x] = (i >= 0 && i < n) ? q_g[i] : INFINITY;
+    }
+    for (int i = threadIdx.x; i < n; i += T) { U[i] = U_g[i]; L[i] = L_g[i]; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    float* Bt = dsm + threadIdx.x;
+    const float* qlane = qrep + (lane & (K - 1));
+    const int nfull = (2 * R - 2 * H + 3) / H;
+    const unsigned nfront = *(volatile unsigned*)&st->list2_count;
+    const unsigned total = nfront + *(volatile unsigned*)&st->list2_back;
+    unsigned* ctr = &st->next_tile;
+    WarpClaim wc;
+    wc.init(ctr, lane);
+    const uint4 none = make_uint4(0xffffffffu, 0u, 0u, 0u);
+    auto fetch = [&](unsigned k) { return k < total ? list2_at(list2, k, nfront, cap) : none; };
+    uint4 nxt = fetch(wc.take(ctr, 0xffffffffu, lane));
+    uint4 nxt2 = fetch(wc.take(ctr, 0xffffffffu, lane));
+    auto prefetch_row = [&](unsigned rid) {
+        const char* pr = reinterpret_cast<const char*>(rows + (long long)rid * n);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(pr));
+    };
+    if (nxt.x != 0xffffffffu) prefetch_row(nxt.x);
+    auto load_h = [&](const float* c, int j, float (&dst)[H]) {
+        if constexpr (H % 4 == 0) {
+#pragma unroll
+            for (int b = 0; b < H / 4; ++b) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(c + j) + b);
+                dst[4 * b] = v.x; dst[4 * b + 1] = v.y; dst[4 * b + 2] = v.z; dst[4 * b + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < H; ++u) dst[u] = __ldg(c + j + u);
+        }
+    };
+    DtwStrip<H> dp;
+    float cnext[H];
+    const float* c = rows;
+    int j0 = 0;
+    unsigned id = 0, refined = 0, abandoned = 0, strips = 0, skipped = 0;
+    float lbk_total = 0.0f, seen = 0.0f;
+    float thr = slack_up(ld_bsf(st));
+    bool running = false;
+    for (;;) {
+        const bool need = !running && nxt.x != 0xffffffffu;
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        if (m) {
+            const unsigned k = wc.take(ctr, m, lane);
+            if (need) {
+                id = nxt.x;
+                lbk_total = __uint_as_float(nxt.y);
+                nxt = nxt2;
+                nxt2 = fetch(k);
+                if (nxt.x != 0xffffffffu) prefetch_row(nxt.x);
+                if (lbk_total * 0.9990234375f <= thr) {
+                    c = rows + (long long)id * n;
+                    load_h(c, 0, cnext);
+                    // virtual row -1: D(-1, -1) = 0 (slot R), +inf elsewhere
+                    for (int x = 0; x < 2 * R + 2; ++x) Bt[x * T] = x == R ? 0.0f : INFINITY;
+                    j0 = 0;
+                    seen = 0.0f;
+                    ++refined;
+                    running = true;
+                } else {
+                    ++skipped;
+                }
+            }
+        }
+        if (!__any_sync(0xffffffffu, running || nxt.x != 0xffffffffu)) break;
+        if (running) {
+            const unsigned bsf_bits = *(volatile const unsigned*)&st->bsf_bits;  // consumed after the strip
+#pragma unroll
+            for (int u = 0; u < H; ++u) dp.cv[u] = cnext[u];
+            if (j0 + H < n) load_h(c, j0 + H, cnext);  // the next strip's points, one strip ahead
+            dp.template run<REM>(Bt, qlane + (size_t)j0 * K, R, nfull);
+            ++strips;
+#pragma unroll
+            for (int u = 0; u < H; ++u) {
+                const float v = dp.cv[u], uu = U[j0 + u], ll = L[j0 + u];
+                const float d = v > uu ? v - uu : (v < ll ? v - ll : 0.0f);
+                seen = fmaf(d, d, seen);
+            }
+            j0 += H;
+            thr = fminf(thr, slack_up(__uint_as_float(bsf_bits)));
+            const float tail = fmaxf(0.0f, lbk_total * 0.9990234375f - seen * 1.0009765625f);
+            const float bound = (dp.rmin + tail) * 0.9990234375f;
+            if (bound > thr) {
+                running = false;
+                ++abandoned;
+            } else if (j0 >= n) {
+                running = false;
+                const float d = Bt[R * T];  // D(n-1, n-1): column n-1 of the last row
+                if (d <= thr) {
+                    bsf_update(st, d);
+                    append_near(st, near, id, d);
+                    thr = fminf(thr, slack_up(d));
+                }
+            }
+        }
+    }
+    refined = __reduce_add_sync(0xffffffffu, refined);
+    abandoned = __reduce_add_sync(0xffffffffu, abandoned + skipped);
+    strips = __reduce_add_sync(0xffffffffu, strips);
+    if (lane == 0) {
+        if (refined) atomicAdd(&st->refined, refined);
+        if (abandoned) atomicAdd(&st->abandoned, abandoned);
+        if (strips) atomicAdd(&st->dtw_cells, (unsigned long long)strips * H * (2 * R + 1));
+    }
+}
+
 // Stage one row into a warp's shared buffer (float4, n % 4 == 0).
 __device__ __forceinline__ void stage_row(float* dst, const float* __restrict__ src, int n, int lane)
 {
@@ -350,7 +507,7 @@ __device__ __forceinline__ void stage_row(float* dst, const float* __restrict__ 
 // fp32 anti-diagonal wavefront (dtw_warp<float>) over the row staged in shared memory.
 // Per-warp shared memory: n floats of row + 3n floats of anti-diagonals.
 __global__ void k_refine_dtw_warp(const float* __restrict__ rows, int n, int reach, const float* __restrict__ q_g,
-                                  const uint4* __restrict__ list2, QState* st, NearEntry* near)
+                                  const uint4* __restrict__ list2, unsigned cap, QState* st, NearEntry* near)
 {
     extern __shared__ __align__(16) float dsm[];
     const int npad = (n + 3) & ~3;
@@ -360,10 +517,11 @@ __global__ void k_refine_dtw_warp(const float* __restrict__ rows, int n, int rea
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     float* c_s = dsm + npad + (size_t)w * 4 * npad;
     float* buf = c_s + npad;
-    const unsigned total = *(volatile unsigned*)&st->list2_count;
+    const unsigned nfront = *(volatile unsigned*)&st->list2_count;
+    const unsigned total = nfront + *(volatile unsigned*)&st->list2_back;
     unsigned refined = 0;
     for (unsigned k = blockIdx.x * wpb + w; k < total; k += gridDim.x * wpb) {
-        const unsigned id = list2[k].x;
+        const unsigned id = list2_at(list2, k, nfront, cap).x;
         stage_row(c_s, rows + (long long)id * n, n, lane);
         const float d = dtw_warp_any<float>(q_s, c_s, n, reach, buf, lane);
         ++refined;
@@ -399,7 +557,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
         s->lb = (long long)st->tile_count * MESSI_TILE_ROWS < N ? (long long)st->tile_count * MESSI_TILE_ROWS : N;
         s->tiles = st->tile_count;
         s->cand = st->cand_count;
-        s->lbk = st->list2_count;
+        s->lbk = st->list2_count + st->list2_back;
         s->refined = st->refined;
         s->abandoned = st->abandoned;
         s->near = nb;

@@ -291,8 +291,14 @@ def test_nn_ed_batch_spans_launch_groups(c1):
         idx2.close()
 
 
-@pytest.mark.parametrize("reach", [25, 7])
-def test_nn_dtw(c1, reach):
+@pytest.mark.parametrize("reach,strip", [(25, None), (7, None), (1, None), (3, None), (9, None), (51, None),
+                                         (2, "1"), (5, "1"), (12, "1"), (25, "1")])
+def test_nn_dtw(c1, reach, strip, monkeypatch):
+    """Exact DTW 1-NN against the oracle.  Reaches 1/3/7/9/51 take the strip kernel
+    (k_refine_dtw_strip, any reach); MESSI_DTW_STRIP=1 forces it where a register-band
+    instantiation exists too."""
+    if strip is not None:
+        monkeypatch.setenv("MESSI_DTW_STRIP", strip)
     X, Q, idx, Xh, Qh = c1
     sub = 20_000
     X2 = X[:sub].contiguous()
