@@ -295,7 +295,8 @@ def run_arm(cfg, args, world, rank, dev, stream, time_steps, warmup):
 # an FMNMX3 on the ALU pipe); the FMA pipe retires one warp instruction per 2 cycles per SM
 # sub-partition, so the fp32 cell peak is 148 SMs x 4 SMSPs x 32 lanes / (2 x 2 cycles) x clock.
 def dtw_cell_peak(sm_mhz=1965.0, sms=148):
-    return sms * 4 * 32 / 4.0 * sm_mhz * 1e6
+    # >= 2 issue slots per cell (FMNMX3 + paired FADD2/FFMA2), 1 warp instruction / cycle / SMSP
+    return sms * 4 * 32 / 2.0 * sm_mhz * 1e6
 
 
 def dtw_roofline(run, steps):
@@ -308,9 +309,12 @@ def dtw_roofline(run, steps):
     peak = dtw_cell_peak(run["clocks"].get("sm_max_mhz", 1965.0) or 1965.0)
     lbk_ms, _ = run["prof"]["lbk"]
     lbk_bytes = sum(4 * run["n"] * s["candidates"] + 16 * s["lbk_pass"] for s in st) * steps
-    return {"bound": "alu", "kernel": "k_refine_dtw<R> (fp32 banded DTW, one thread per candidate)",
+    return {"bound": "alu", "kernel": "k_refine_dtw_strip<8,REM> (fp32 banded DTW, one thread per candidate; "
+                                      "k_refine_dtw<R> at R = 2, 5)",
             "achieved": achieved, "peak": peak, "unit": "cells/s", "frac": achieved / peak,
-            "peak_source": "derived: FMA pipe 1 warp-instr / 2 cycles / SMSP, 2 FMA-pipe instr per cell",
+            "peak_source": "derived (DESIGN.md 6): issue limit 1 warp-instr / cycle / SMSP at >= 2 instr per cell "
+                           "(FMNMX3 + paired FADD2/FFMA2), 148 SMs x 4 SMSP, max SM clock",
+            "time": "CUDA events on the refine streams (includes waits for SMs held by overlapping stages)",
             "lbk_filter": {"bound": "hbm", "achieved_gbs": lbk_bytes / (lbk_ms / 1e3) / 1e9 if lbk_ms > 0 else None,
                            "bytes_per_query": lbk_bytes / steps / len(st)}}
 

@@ -196,9 +196,11 @@ static int strip_rows(int R)
     return R >= 7 ? 8 : (R >= 3 ? 4 : 2);
 }
 
-// Which refine kernel serves reach R: the register band (DtwThread<R>) where instantiated,
-// else the strip kernel when its shared memory fits (R >= 1), else the warp wavefront.
-// MESSI_DTW_STRIP=1 / 0 forces the strip kernel on / off (experiments).
+// Which refine kernel serves reach R: the strip kernel for R >= 7 (measured faster than
+// the register band from R = 12 on: 3084 vs 2999 q/s at R = 12, 1174 vs 1099 at R = 25,
+// profiles/r01_sweeps_dtw.jsonl) and wherever no register band is instantiated, as long as
+// its shared memory fits; the register band (DtwThread<R>) for R = 2, 5; else the warp
+// wavefront.  MESSI_DTW_STRIP=1 / 0 forces the strip kernel on / off (experiments).
 static bool use_strip(int n, int R, bool have_band)
 {
     const char* e = getenv("MESSI_DTW_STRIP");  // read per launch: tests switch it
@@ -206,7 +208,7 @@ static bool use_strip(int n, int R, bool have_band)
     const bool fits = R >= 1 && strip_smem(n, R) <= (size_t)kStripSmemMax;
     if (force == 0) return false;
     if (force == 1) return fits;
-    return fits && !have_band;
+    return fits && (!have_band || R >= 7);
 }
 
 static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R, const float* q_dev, cudaStream_t rs)
