@@ -58,8 +58,10 @@ def test_knn_single_and_k1_equals_nn(coll):
         assert k_id[0] == n_id and k_d2[0] == n_d2
 
 
-def test_knn_duplicates_and_small_collection():
-    """Exact duplicate rows (ties broken by id) and a collection smaller than k."""
+@pytest.mark.parametrize("k", [8, 24])
+def test_knn_duplicates_and_small_collection(k):
+    """Exact duplicate rows (ties broken by id) and a collection smaller than k; k = 24 takes
+    the warp-cooperative insert (k > 16), k = 8 the single-lane one."""
     from paper_2110_07519_b200 import messi as M
     X = _gen(3000, 64, datagen.DATA_SEED)
     X[2000:2005] = X[10]
@@ -67,33 +69,33 @@ def test_knn_duplicates_and_small_collection():
     torch.cuda.synchronize()
     idx = M.Index(X)
     try:
-        d2, ids = oracle.knn("ed", X.cpu().numpy(), Q.cpu().numpy(), 8)
-        res = M.result_buffer(2 * 8, DEV)
-        idx.query_batch_knn(Q, 8, res)
+        d2, ids = oracle.knn("ed", X.cpu().numpy(), Q.cpu().numpy(), k)
+        res = M.result_buffer(2 * k, DEV)
+        idx.query_batch_knn(Q, k, res)
         torch.cuda.synchronize()
         _, gid, gd2 = M.decode_results(res)
-        assert np.array_equal(gid.numpy().reshape(-1, 8), ids) and np.array_equal(gd2.numpy().reshape(-1, 8), d2)
+        assert np.array_equal(gid.numpy().reshape(-1, k), ids) and np.array_equal(gd2.numpy().reshape(-1, k), d2)
         assert list(ids[0, :6]) == [10, 2000, 2001, 2002, 2003, 2004]
     finally:
         idx.close()
     Xs = X[:5].contiguous()
     idx2 = M.Index(Xs)
     try:
-        dist, gid, gd2 = idx2.query_knn(Q[0], 8)
-        d2, ids = oracle.knn("ed", Xs.cpu().numpy(), Q[:1].cpu().numpy(), 8)
-        assert list(gid) == list(ids[0]) and list(gid[5:]) == [-1, -1, -1] and np.all(np.isinf(gd2[5:]))
+        dist, gid, gd2 = idx2.query_knn(Q[0], k)
+        d2, ids = oracle.knn("ed", Xs.cpu().numpy(), Q[:1].cpu().numpy(), k)
+        assert list(gid) == list(ids[0]) and list(gid[5:]) == [-1] * (k - 5) and np.all(np.isinf(gd2[5:]))
     finally:
         idx2.close()
 
 
-def test_knn_linked_shards():
+@pytest.mark.parametrize("k", [9, 33])
+def test_knn_linked_shards(k):
     """Shards sharing their k-th best (valid: one shard alone has k rows within it) still
     merge to the exact global k-NN."""
     from paper_2110_07519_b200 import messi as M
     from paper_2110_07519_b200.dist import shard_range
     X = _gen(45_000, 128, datagen.DATA_SEED)
     Q = _gen(6, 128, datagen.QUERY_SEED)
-    k = 9
     idxs, parts = [], []
     streams = [torch.cuda.Stream() for _ in range(3)]
     for g in range(3):
