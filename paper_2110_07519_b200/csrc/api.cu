@@ -29,6 +29,12 @@
 
 using namespace messi;
 
+// Per-query state sets of the DTW path: queries in flight at once (the stages of
+// consecutive queries overlap across the library's streams).
+#ifndef MESSI_DTW_SLOTS
+#define MESSI_DTW_SLOTS 4  // C4: 2 -> 1136, 3 -> 1232, 4 -> 1281, 6 -> 1303, 8 -> 1307 q/s
+#endif
+
 struct Slot {
     QState* st = nullptr;
     float *lut = nullptr, *tab = nullptr, *U = nullptr, *L = nullptr;  // tab: 64 KB scan table
@@ -84,7 +90,7 @@ struct messi_index {
     unsigned epoch = 0;
     int fused_grid = 0;
     // per-query scratch
-    Slot slot[2];
+    Slot slot[MESSI_DTW_SLOTS];
     unsigned long long qcount = 0;
     float* qbuf = nullptr;
     messi_result* res1 = nullptr;
@@ -722,7 +728,7 @@ static messi_status run_ed_batch(messi_index* idx, const float* queries_dev, int
 
 static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, messi_result* res, messi_stats* stats)
 {
-    Slot& sl = idx->slot[idx->qcount++ & 1];
+    Slot& sl = idx->slot[idx->qcount++ % MESSI_DTW_SLOTS];
     cudaStream_t rs = idx->rstr;
     const int n = idx->n;
     const int npad = (n + 3) & ~3;
