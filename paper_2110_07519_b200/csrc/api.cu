@@ -249,8 +249,10 @@ static messi_status setup_kernels()
     const int big = 200 * 1024;
     CK(cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
     CK(cudaFuncSetAttribute(k_debug_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
-    CK(cudaFuncSetAttribute(k_scan_refine_ed<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(MESSI_MAX_N)));
-    CK(cudaFuncSetAttribute(k_scan_refine_ed<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(MESSI_MAX_N)));
+    CK(cudaFuncSetAttribute(k_scan_refine_ed<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(MESSI_MAX_N)));
+    CK(cudaFuncSetAttribute(k_scan_refine_ed<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(MESSI_MAX_N)));
+    CK(cudaFuncSetAttribute(k_scan_refine_ed<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(MESSI_MAX_N)));
+    CK(cudaFuncSetAttribute(k_scan_refine_ed<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(MESSI_MAX_N)));
     CK(cudaFuncSetAttribute(k_filter_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, kFilterQ * kLutF * 4));
     CK(cudaFuncSetAttribute(k_lbk_filter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_lbk_filter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -639,7 +641,7 @@ static messi_status ensure_batch_buffers(messi_index* idx)
         TRY(dalloc(&bs.btlist, (size_t)kBatchMax * (size_t)idx->ntiles));
     }
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan_refine_ed<false>, 32 * kFusedWarps, fused_smem(idx->n)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan_refine_ed<false, false>, 32 * kFusedWarps, fused_smem(idx->n)));
     if (occ < 1) return fail(MESSI_ECUDA, "fused kernel does not fit an SM (n = %d)", idx->n);
     idx->fused_grid = idx->sms * occ;
     return MESSI_OK;
@@ -689,14 +691,16 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
     }
     {
         ProfScope ps(idx, K_SCAN, st);
-        if (peers.n > 0)
-            k_scan_refine_ed<true><<<idx->fused_grid, 32 * kFusedWarps, fused_smem(n), st>>>(
-            idx->tiles, idx->sym8, idx->ntiles, idx->N, n, q, bs.lutx, bs.btlist, bs.bst, B, idx->rows8,
-            idx->meta8, idx->q8_omd, idx->perm, idx->rows, peers, knn, k);
-        else
-            k_scan_refine_ed<false><<<idx->fused_grid, 32 * kFusedWarps, fused_smem(n), st>>>(
-            idx->tiles, idx->sym8, idx->ntiles, idx->N, n, q, bs.lutx, bs.btlist, bs.bst, B, idx->rows8,
-            idx->meta8, idx->q8_omd, idx->perm, idx->rows, peers, knn, k);
+#define FUSED_ARGS                                                                                        \
+    idx->tiles, idx->sym8, idx->ntiles, idx->N, n, q, bs.lutx, bs.btlist, bs.bst, B, idx->rows8, idx->meta8, \
+        idx->q8_omd, idx->perm, idx->rows, peers, knn, k
+        const dim3 fg(idx->fused_grid), fb(32 * kFusedWarps);
+        const size_t fs = fused_smem(n);
+        if (peers.n > 0 && k > 1) k_scan_refine_ed<true, true><<<fg, fb, fs, st>>>(FUSED_ARGS);
+        else if (peers.n > 0) k_scan_refine_ed<true, false><<<fg, fb, fs, st>>>(FUSED_ARGS);
+        else if (k > 1) k_scan_refine_ed<false, true><<<fg, fb, fs, st>>>(FUSED_ARGS);
+        else k_scan_refine_ed<false, false><<<fg, fb, fs, st>>>(FUSED_ARGS);
+#undef FUSED_ARGS
         LAUNCHED(idx);
         k_finalise_batch<<<(B + 127) / 128, 128, 0, st>>>(bs.bst, B, idx->N, idx->row_begin, res, stats, knn, k);
         LAUNCHED(idx);

