@@ -190,8 +190,11 @@ struct ProfScope {
 
 // Strip DTW instantiations (rows per strip H, REM = (2R - 2H + 3) mod H): H = 8 for R >= 7,
 // 4 for R in [3, 6], 2 for R in [1, 2].
-#define MESSI_STRIP_VARIANTS(X) \
-    X(8, 0) X(8, 1) X(8, 2) X(8, 3) X(8, 4) X(8, 5) X(8, 6) X(8, 7) X(4, 0) X(4, 1) X(4, 2) X(4, 3) X(2, 0) X(2, 1)
+// K: query copies (32, or 8 when 32 would not fit three CTAs per SM -- large R, H = 8).
+#define MESSI_STRIP_VARIANTS(X)                                                                               \
+    X(8, 0, 32) X(8, 1, 32) X(8, 2, 32) X(8, 3, 32) X(8, 4, 32) X(8, 5, 32) X(8, 6, 32) X(8, 7, 32) X(4, 0, 32) \
+    X(4, 1, 32) X(4, 2, 32) X(4, 3, 32) X(2, 0, 32) X(2, 1, 32) X(8, 0, 8) X(8, 1, 8) X(8, 2, 8) X(8, 3, 8)        \
+    X(8, 4, 8) X(8, 5, 8) X(8, 6, 8) X(8, 7, 8)
 static const int kStripSmemMax = 227 * 1024;
 
 static int strip_rows(int R)
@@ -211,7 +214,7 @@ static bool use_strip(int n, int R, bool have_band)
 {
     const char* e = getenv("MESSI_DTW_STRIP");  // read per launch: tests switch it
     const int force = e ? atoi(e) : -1;
-    const bool fits = R >= 1 && strip_smem(n, R) <= (size_t)kStripSmemMax;
+    const bool fits = R >= 1 && strip_smem(n, R, strip_qcopies(n, R)) <= (size_t)kStripSmemMax;
     if (force == 0) return false;
     if (force == 1) return fits;
     return fits && (!have_band || R >= 7);
@@ -221,15 +224,16 @@ static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R,
 {
     const int H = strip_rows(R);
     const int rem = (2 * R - 2 * H + 3) % H;
-    const size_t smem = strip_smem(n, R);
+    const int K = strip_qcopies(n, R);
+    const size_t smem = strip_smem(n, R, K);
     bool launched = false;
-#define LAUNCH_S(HH, REM)                                                                                        \
-    if (!launched && H == HH && rem == REM) {                                                                   \
+#define LAUNCH_S(HH, REM, KK)                                                                                    \
+    if (!launched && H == HH && rem == REM && K == KK) {                                                        \
         int occ = 0;                                                                                             \
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_dtw_strip<HH, REM>, kStripThreads, smem)); \
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_dtw_strip<HH, REM, KK>, kStripThreads, smem)); \
         const char* oe = getenv("MESSI_DTW_REFINE_OCC"); /* experiments: CTAs per SM */                          \
         if (oe && atoi(oe) > 0 && atoi(oe) < occ) occ = atoi(oe);                                                \
-        k_refine_dtw_strip<HH, REM><<<idx->sms * (occ > 0 ? occ : 1), kStripThreads, smem, rs>>>(                \
+        k_refine_dtw_strip<HH, REM, KK><<<idx->sms * (occ > 0 ? occ : 1), kStripThreads, smem, rs>>>(            \
             idx->rows, n, R, q_dev, sl.U, sl.L, sl.list2, (unsigned)idx->N, sl.st, sl.near);                     \
         launched = true;                                                                                         \
     }
@@ -259,7 +263,7 @@ static messi_status setup_kernels()
     CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_refine_dtw_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_resolve_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-#define SET_ATTR_S(H, REM) CK(cudaFuncSetAttribute(k_refine_dtw_strip<H, REM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStripSmemMax));
+#define SET_ATTR_S(H, REM, K) CK(cudaFuncSetAttribute(k_refine_dtw_strip<H, REM, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStripSmemMax));
     MESSI_STRIP_VARIANTS(SET_ATTR_S)
 #undef SET_ATTR_S
 #define SET_ATTR_R(R) CK(cudaFuncSetAttribute(k_refine_dtw<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));

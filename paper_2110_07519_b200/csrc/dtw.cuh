@@ -365,7 +365,8 @@ struct DtwThread {
 // steps between them run in H-step chunks (the query window rotates through H registers)
 // plus REM = (2R - 2H + 3) mod H single steps (a template parameter).
 constexpr int kStripThreads = 128;
-constexpr int kStripQCopies = 8;
+// Lane copies of the padded query: 32 (one per lane: conflict-free loads) when the copies fit
+// beside the boundary arrays, else 8 (chosen per launch; strip_qcopies in refine.cuh).
 
 template <int... Is, class F>
 __device__ __forceinline__ void static_for_impl(std::integer_sequence<int, Is...>, F&& f)
@@ -388,9 +389,9 @@ struct DtwStrip {
 
     // One step t (compile-time facts: PH = t % H, PAR = t & 1, active rows [LO, HI],
     // whether row H-1 writes the boundary).  bsrc: boundary slot t+1 (read when row 0 is
-    // active), qsrc: query column j0 - R + t, bdst: boundary slot t - 2H + 2.
-    template <int PH, int PAR, int LO, int HI>
-    __device__ __forceinline__ void step(const float* bsrc, const float* qsrc, float* bdst)
+    // active), q: query column j0 - R + t (advanced by K copies), bdst: boundary slot t - 2H + 2.
+    template <int PH, int PAR, int LO, int HI, int K>
+    __device__ __forceinline__ void step(const float* bsrc, const float* q, float* bdst)
     {
         float up0 = 0.0f, dg0 = 0.0f;
         if constexpr (LO == 0) {
@@ -398,7 +399,7 @@ struct DtwStrip {
             dg0 = bprev;
             bprev = up0;
         }
-        Qw[PH] = *qsrc;
+        Qw[PH] = *q;
         float nv[H];
         static_for<(HI - LO + 2) / 2>([&](auto P) {
             constexpr int u = LO + 2 * decltype(P)::value;
@@ -429,26 +430,26 @@ struct DtwStrip {
     }
 
     // All steps of the strip of rows j0 .. j0+H-1 (cv loaded).  Bt: this thread's boundary
-    // slot 0; qt: the query copy at column j0 - R; nfull = (2R - 2H + 3) / H.
-    template <int REM>
+    // slot 0; qt: the query copy at column j0 - R (K copies per column); nfull = (2R - 2H + 3) / H.
+    template <int REM, int K>
     __device__ __forceinline__ void run(float* Bt, const float* qt, int R, int nfull)
     {
-        constexpr int T = kStripThreads, K = kStripQCopies;
+        constexpr int T = kStripThreads;
 #pragma unroll
         for (int u = 0; u < H; ++u) S[0][u] = S[1][u] = INFINITY;
         bprev = Bt[0];
         rmin = INFINITY;
         static_for<2 * H - 2>([&](auto I) {  // prologue: rows 0 .. t/2
             constexpr int t = decltype(I)::value;
-            step<t % H, t & 1, 0, t / 2>(Bt + (t + 1) * T, qt + t * K, nullptr);
+            step<t % H, t & 1, 0, t / 2, K>(Bt + (t + 1) * T, qt + t * K, nullptr);
         });
         float* bp = Bt + (2 * H - 1) * T;
-        const float* qp = qt + (2 * H - 2) * K;
         float* wp = Bt;
+        const float* qp = qt + (2 * H - 2) * K;
         for (int c = 0; c < nfull; ++c) {
             static_for<H>([&](auto I) {
                 constexpr int k = decltype(I)::value;
-                step<(2 * H - 2 + k) % H, k & 1, 0, H - 1>(bp + k * T, qp + k * K, wp + k * T);
+                step<(2 * H - 2 + k) % H, k & 1, 0, H - 1, K>(bp + k * T, qp + k * K, wp + k * T);
             });
             bp += H * T;
             qp += H * K;
@@ -456,13 +457,13 @@ struct DtwStrip {
         }
         static_for<REM>([&](auto I) {
             constexpr int k = decltype(I)::value;
-            step<(2 * H - 2 + k) % H, k & 1, 0, H - 1>(bp + k * T, qp + k * K, wp + k * T);
+            step<(2 * H - 2 + k) % H, k & 1, 0, H - 1, K>(bp + k * T, qp + k * K, wp + k * T);
         });
         float* we = wp + REM * T;                 // boundary slot of step 2R+1
         const float* qe = qt + 2 * R * K;         // query column of step 2R
         static_for<2 * H - 2>([&](auto I) {  // epilogue: rows (t+1)/2 .. H-1 at step 2R + t
             constexpr int t = decltype(I)::value + 1;
-            step<(REM + 3 * H - 3 + t) % H, t & 1, (t + 1) / 2, H - 1>(nullptr, qe + t * K, we + (t - 1) * T);
+            step<(REM + 3 * H - 3 + t) % H, t & 1, (t + 1) / 2, H - 1, K>(nullptr, qe + t * K, we + (t - 1) * T);
         });
     }
 };
