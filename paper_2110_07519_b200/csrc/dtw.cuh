@@ -144,48 +144,6 @@ __device__ T dtw_warp_shfl(const float* __restrict__ q, const float* __restrict_
     return __shfl_sync(0xffffffffu, cur, 0);  // t = 2n-2: ilo = n-1, lane 0 holds D(n-1, n-1)
 }
 
-// fp32 register wavefront with early abandon against the query's running BSF (the
-// approximate search, Alg. 5): a warping path moves by (1,0), (0,1) or (1,1), so it has a
-// cell on anti-diagonal t or t+1, and D never decreases along it (costs >= 0; fp32 adds of
-// non-negative values are monotone): D(n-1, n-1) >= the min over two consecutive
-// anti-diagonals.  Checked every 8 anti-diagonals; returns +inf when that min exceeds
-// slack_up(BSF) (such a row cannot lower the BSF).
-__device__ float dtw_warp_shfl_abandon(const float* __restrict__ q, const float* __restrict__ c, int n, int r,
-                                       int lane, const QState* st)
-{
-    const float INF = INFINITY;
-    float cur = INF, prev = INF;
-    int ilo1 = 0, ilo2 = 0;
-    for (int t = 0; t <= 2 * n - 2; ++t) {
-        const int ilo = max(max(0, t - (n - 1)), (t - r + 1) >> 1);
-        const int ihi = min(min(n - 1, t), (t + r) >> 1);
-        const int i = ilo + lane, j = t - i;
-        const int su = lane + (ilo - ilo1) - 1;
-        const int sl = lane + (ilo - ilo1);
-        const int sd = lane + (ilo - ilo2) - 1;
-        float up = __shfl_sync(0xffffffffu, cur, su & 31);
-        float left = __shfl_sync(0xffffffffu, cur, sl & 31);
-        float diag = __shfl_sync(0xffffffffu, prev, sd & 31);
-        up = su >= 0 && su < 32 ? up : INF;
-        left = sl < 32 ? left : INF;
-        diag = sd >= 0 && sd < 32 ? diag : INF;
-        float mn = min3f(diag, up, left);
-        if (t == 0) mn = 0.0f;
-        const bool valid = i <= ihi;
-        const float val = valid ? cell_cost_add(q[valid ? i : 0], c[valid ? j : 0], mn) : INF;
-        prev = cur;
-        cur = val;
-        ilo2 = ilo1;
-        ilo1 = ilo;
-        if ((t & 7) == 7) {
-            float m = fminf(cur, prev);
-            for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
-            if (m > slack_up(ld_bsf(st))) return INF;
-        }
-    }
-    return __shfl_sync(0xffffffffu, cur, 0);
-}
-
 // Dispatch: register wavefront when the band fits a warp, shared-memory wavefront otherwise.
 template <typename T>
 __device__ __forceinline__ T dtw_warp_any(const float* __restrict__ q, const float* __restrict__ c, int n, int r,

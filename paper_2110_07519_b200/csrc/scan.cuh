@@ -194,12 +194,7 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
             *reinterpret_cast<float4*>(c_s + j) =
                 __ldg(reinterpret_cast<const float4*>(rows + (long long)perm[start + k] * n + j));
         __syncwarp();
-        const float d = reach <= kShflMaxReach ? dtw_warp_shfl_abandon(q_s, c_s, n, reach, lane, st)
-                                               : dtw_warp_any<float>(q_s, c_s, n, reach, buf, lane);
-        if (d < best) {
-            best = d;
-            if (lane == 0) bsf_update(st, d);  // lets the other warps abandon against it
-        }
+        best = fminf(best, dtw_warp_any<float>(q_s, c_s, n, reach, buf, lane));
     }
     if (lane == 0 && best < INFINITY) {
         bsf_update(st, best);
