@@ -284,7 +284,8 @@ def run_arm(cfg, args, world, rank, dev, stream, time_steps, warmup):
             barrier(world)
             knn = k0.elapsed_time(k1)
     out = dict(ms=ms, build_ms=build_ms, launches=launches, prof=prof, prof_ms=prof_ms, stats=st, clocks=clk.summary(),
-               e2e_ms=e2e_ms, knn_ms=knn, nq=nq, N_local=X.shape[0], n=cfg["n"], h2d=qh.numel() * 4, d2h=rh.numel())
+               e2e_ms=e2e_ms, knn_ms=knn, nq=nq, N_local=X.shape[0], n=cfg["n"], reach=reach, h2d=qh.numel() * 4,
+               d2h=rh.numel())
     idx.close()
     del X, Q
     torch.cuda.empty_cache()
@@ -308,7 +309,10 @@ def dtw_roofline(run, steps):
     achieved = cells / (ms / 1e3)
     peak = dtw_cell_peak(run["clocks"].get("sm_max_mhz", 1965.0) or 1965.0)
     lbk_ms, _ = run["prof"]["lbk"]
-    lbk_bytes = sum(4 * run["n"] * s["candidates"] + 16 * s["lbk_pass"] for s in st) * steps
+    # strip refine reaches (r >= 7): the filter reads the quantised rows (n bytes + 8 B of
+    # scale / error per candidate); register-band reaches: the raw rows (4n bytes)
+    per_cand = run["n"] + 8 if (run.get("reach") or 0) >= 7 else 4 * run["n"]
+    lbk_bytes = sum(per_cand * s["candidates"] + 16 * s["lbk_pass"] for s in st) * steps
     return {"bound": "alu", "kernel": "k_refine_dtw_strip<8,REM> (fp32 banded DTW, one thread per candidate; "
                                       "k_refine_dtw<R> at R = 2, 5)",
             "achieved": achieved, "peak": peak, "unit": "cells/s", "frac": achieved / peak,

@@ -757,11 +757,20 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     }
     CK(cudaEventRecord(sl.ev_seed, idx->side));
     TRY(launch_scan(idx, sl));
+    bool band = false;
+#define HAVE_R(R) band = band || reach == R;
+    MESSI_DTW_REACHES(HAVE_R)
+#undef HAVE_R
+    const bool strip = use_strip(n, reach, band);
     {
         ProfScope ps(idx, K_LBK, rs);
-        k_lbk_filter<4><<<refine_grid(idx, 1024) * 2, 128, lbk_smem(n), rs>>>(sl.cand, idx->perm, idx->rows, n, sl.U, sl.L,
-                                                                       reach, sl.st, sl.list2,
-                                                                       (unsigned)idx->N, dtw_front());
+        if (strip)  // LB_Keogh of the quantised rows (the strip refine's tail bound uses the same terms)
+            k_lbk_filter_q8<<<idx->sms * 8, 128, 2 * (size_t)((n + 15) & ~15) * sizeof(float), rs>>>(
+                sl.cand, idx->perm, idx->rows8, idx->meta8, n, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N,
+                dtw_front());
+        else
+            k_lbk_filter<4><<<refine_grid(idx, 1024) * 2, 128, lbk_smem(n), rs>>>(
+                sl.cand, idx->perm, idx->rows, n, sl.U, sl.L, reach, sl.st, sl.list2, (unsigned)idx->N, dtw_front());
         LAUNCHED(idx);
     }
     // the refine and the resolve run on their own stream: the LB_Keogh filter of the next
@@ -771,11 +780,8 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     CK(cudaStreamWaitEvent(rs, sl.ev_lbk, 0));
     {
         ProfScope ps(idx, K_REFINE, rs);
-        bool launched = false, band = false;
-#define HAVE_R(R) band = band || reach == R;
-        MESSI_DTW_REACHES(HAVE_R)
-#undef HAVE_R
-        if (use_strip(n, reach, band)) {
+        bool launched = false;
+        if (strip) {
             TRY(launch_strip(idx, sl, n, reach, q_dev, rs));
             launched = true;
         }

@@ -221,6 +221,103 @@ __global__ void __launch_bounds__(G == 8 ? 256 : 128, G == 8 ? 1 : 8) k_lbk_filt
     }
 }
 
+// Lower bound of sqrt(LB_Keogh(x)) from the quantised row x^ = s c: the
+// per-point term x -> dist(x, [L_i, U_i]) is 1-Lipschitz, so for any set S of points
+//     sqrt(sum_S lbk(x_i)) >= sqrt(sum_S lbk(x^_i)) - ||x - x^||_2 >= sqrt(tq) - e
+// for tq <= sum_S lbk(x^_i) and e >= ||x - x^||_2 (meta8).  Returns the squared bound,
+// rounded down (tq is reduced by 2^-10 for the fp32 summation order).
+__device__ __forceinline__ float q8_lbk_bound(float tq, float e)
+{
+    const float r = __fsub_rd(__fsqrt_rd(fmaxf(0.0f, tq * 0.9990234375f)), e);
+    return r > 0.0f ? __fmul_rd(r, r) : 0.0f;
+}
+
+// DTW step 1 over the QUANTISED rows (strip refine reaches): the scan's candidates whose
+// bound does not exceed BSF0 get the LB_Keogh of their quantised row x^ (n bytes + s, e
+// instead of 4n bytes), kept when q8_lbk_bound(LBK(x^), e) <= BSF0 -- a lower bound of
+// the raw LB_Keogh, hence of DTW.  list2 entries: (row id, LBK(x^), s, e);
+// the strip refine computes its tail bound from the same quantised terms.  One lane per
+// candidate: a lane streams its row's bytes 16 at a time (all lanes read the same U, L
+// words: shared-memory broadcasts); two best-first bins as k_lbk_filter.
+__global__ void __launch_bounds__(128) k_lbk_filter_q8(const uint2* __restrict__ cand, const unsigned* __restrict__ perm,
+                                                       const unsigned char* __restrict__ rows8,
+                                                       const float2* __restrict__ meta8, int n,
+                                                       const float* __restrict__ U_g, const float* __restrict__ L_g,
+                                                       QState* st, uint4* __restrict__ list2, unsigned cap, float front)
+{
+    extern __shared__ __align__(16) float env[];
+    float* U = env;
+    float* L = U + ((n + 15) & ~15);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) { U[i] = U_g[i]; L[i] = L_g[i]; }
+    __syncthreads();
+    const unsigned total = *(volatile unsigned*)&st->cand_count;
+    const int lane = threadIdx.x & 31;
+    const float thr = __uint_as_float(st->lbk_thr_bits);
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k - lane < total; k += gridDim.x * blockDim.x) {
+        const bool valid = k < total;
+        const uint2 ce = valid ? cand[k] : make_uint2(0u, 0x7f800000u);
+        const bool ok = valid && __uint_as_float(ce.y) <= thr;
+        float a = 0.0f;
+        float2 meta = make_float2(1.0f, INFINITY);
+        if (ok) {
+            meta = __ldg(meta8 + ce.x);
+            const float qoff = -8388736.0f * meta.x;  // -(2^23 + 128) s, exact (s a power of two)
+            const uint4* src = reinterpret_cast<const uint4*>(rows8 + (long long)ce.x * n);
+            float2 acc = make_float2(0.0f, 0.0f);
+            for (int j0 = 0; j0 < n; j0 += 64) {  // 64 bytes in flight per lane
+                uint4 raw4[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h)
+                    raw4[h] = j0 + 16 * h < n ? __ldg(src + (j0 >> 4) + h) : make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                const int j = j0 + 16 * h;
+                if (j >= n) break;
+                const uint4 raw = raw4[h];
+                const unsigned wd[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const float4 uu = *reinterpret_cast<const float4*>(U + j + 4 * g);
+                    const float4 ll = *reinterpret_cast<const float4*>(L + j + 4 * g);
+                    const float us[4] = {uu.x, uu.y, uu.z, uu.w}, ls[4] = {ll.x, ll.y, ll.z, ll.w};
+                    float d[4];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        // 2^23 + byte via PRMT, then (2^23 + byte - 2^23 - 128) * s in one exact FFMA
+                        const float fm = __uint_as_float(__byte_perm(wd[g], 0x4B000000u, 0x7650u | b));
+                        const float xq = fmaf(fm, meta.x, qoff);
+                        d[b] = xq - fminf(fmaxf(xq, ls[b]), us[b]);
+                    }
+                    acc = ffma2(make_float2(d[0], d[1]), make_float2(d[0], d[1]), acc);
+                    acc = ffma2(make_float2(d[2], d[3]), make_float2(d[2], d[3]), acc);
+                }
+                }
+            }
+            a = acc.x + acc.y;
+        }
+        const float bnd = q8_lbk_bound(a, meta.y);
+        const bool pass = ok && bnd <= thr;
+        const bool fr = pass && bnd <= thr * front;
+        const unsigned passmask = __ballot_sync(0xffffffffu, pass), frontmask = __ballot_sync(0xffffffffu, fr);
+        if (passmask) {
+            const unsigned backmask = passmask & ~frontmask;
+            unsigned fb = 0, bb = 0;
+            if (lane == 0) {
+                if (frontmask) fb = atomicAdd(&st->list2_count, (unsigned)__popc(frontmask));
+                if (backmask) bb = atomicAdd(&st->list2_back, (unsigned)__popc(backmask));
+            }
+            fb = __shfl_sync(0xffffffffu, fb, 0);
+            bb = __shfl_sync(0xffffffffu, bb, 0);
+            const unsigned lt = (1u << lane) - 1u;
+            if (pass) {
+                const uint4 e = make_uint4(perm[ce.x], __float_as_uint(a), __float_as_uint(meta.x), __float_as_uint(meta.y));
+                if (fr) list2[fb + __popc(frontmask & lt)] = e;
+                else list2[cap - 1u - (bb + __popc(backmask & lt))] = e;
+            }
+        }
+    }
+}
+
 // Work distribution of the per-thread refine kernels: a lane that finishes (or skips) a
 // candidate takes the next one from its warp's chunk of list2 entries; chunks of kClaimChunk
 // consecutive entries are claimed with one atomicAdd on QState::next_tile, the next chunk one
@@ -432,7 +529,10 @@ __global__ void __launch_bounds__(kStripThreads) k_refine_dtw_strip(const float*
     const float* c = rows;
     int j0 = 0;
     unsigned id = 0, refined = 0, abandoned = 0, strips = 0, skipped = 0;
-    float lbk_total = 0.0f, seen = 0.0f;
+    // list2 entries of k_lbk_filter_q8: (id, LB_Keogh of the quantised row x^, s, e); the
+    // tail bound uses the quantised terms of the rows not done yet (q8_lbk_bound), with
+    // x^_j = s rint(x_j / s) recomputed from the raw point (bit-identical to k_quantise)
+    float lbk_total = 0.0f, seen = 0.0f, qs = 1.0f, qinv = 1.0f, qe = INFINITY;
     float thr = slack_up(ld_bsf(st));
     bool running = false;
     for (;;) {
@@ -443,10 +543,13 @@ __global__ void __launch_bounds__(kStripThreads) k_refine_dtw_strip(const float*
             if (need) {
                 id = nxt.x;
                 lbk_total = __uint_as_float(nxt.y);
+                qs = __uint_as_float(nxt.z);
+                qe = __uint_as_float(nxt.w);
+                qinv = __frcp_rn(qs);  // exact: s is a power of two
                 nxt = nxt2;
                 nxt2 = fetch(k);
                 if (nxt.x != 0xffffffffu) prefetch_row(nxt.x);
-                if (lbk_total * 0.9990234375f <= thr) {
+                if (q8_lbk_bound(lbk_total, qe) <= thr) {
                     c = rows + (long long)id * n;
                     load_h(c, 0, cnext);
                     // virtual row -1: D(-1, -1) = 0 (slot R), +inf elsewhere
@@ -470,13 +573,13 @@ __global__ void __launch_bounds__(kStripThreads) k_refine_dtw_strip(const float*
             ++strips;
 #pragma unroll
             for (int u = 0; u < H; ++u) {
-                const float v = dp.cv[u], uu = U[j0 + u], ll = L[j0 + u];
-                const float d = v > uu ? v - uu : (v < ll ? v - ll : 0.0f);
+                const float v = rintf(dp.cv[u] * qinv) * qs, uu = U[j0 + u], ll = L[j0 + u];
+                const float d = v - fminf(fmaxf(v, ll), uu);
                 seen = fmaf(d, d, seen);
             }
             j0 += H;
             thr = fminf(thr, slack_up(__uint_as_float(bsf_bits)));
-            const float tail = fmaxf(0.0f, lbk_total * 0.9990234375f - seen * 1.0009765625f);
+            const float tail = q8_lbk_bound(fmaxf(0.0f, lbk_total - seen * 1.0009765625f), qe);
             const float bound = (dp.rmin + tail) * 0.9990234375f;
             if (bound > thr) {
                 running = false;
