@@ -190,10 +190,10 @@ struct ProfScope {
 
 // Strip DTW instantiations (rows per strip H, REM = (2R - 2H + 3) mod H): H = 8 for R >= 7,
 // 4 for R in [3, 6], 2 for R in [1, 2].
-// K: query copies (32, or 8 when 32 would not fit three CTAs per SM -- large R, H = 8).
+// K: query-pair copies (16, or 8 when 16 would not fit three CTAs per SM -- large R, H = 8).
 #define MESSI_STRIP_VARIANTS(X)                                                                               \
-    X(8, 0, 32) X(8, 1, 32) X(8, 2, 32) X(8, 3, 32) X(8, 4, 32) X(8, 5, 32) X(8, 6, 32) X(8, 7, 32) X(4, 0, 32) \
-    X(4, 1, 32) X(4, 2, 32) X(4, 3, 32) X(2, 0, 32) X(2, 1, 32) X(8, 0, 8) X(8, 1, 8) X(8, 2, 8) X(8, 3, 8)        \
+    X(8, 0, 16) X(8, 1, 16) X(8, 2, 16) X(8, 3, 16) X(8, 4, 16) X(8, 5, 16) X(8, 6, 16) X(8, 7, 16) X(4, 0, 16) \
+    X(4, 1, 16) X(4, 2, 16) X(4, 3, 16) X(2, 0, 16) X(2, 1, 16) X(8, 0, 8) X(8, 1, 8) X(8, 2, 8) X(8, 3, 8)        \
     X(8, 4, 8) X(8, 5, 8) X(8, 6, 8) X(8, 7, 8)
 static const int kStripSmemMax = 227 * 1024;
 

@@ -323,8 +323,9 @@ struct DtwThread {
 // steps between them run in H-step chunks (the query window rotates through H registers)
 // plus REM = (2R - 2H + 3) mod H single steps (a template parameter).
 constexpr int kStripThreads = 128;
-// Lane copies of the padded query: 32 (one per lane: conflict-free loads) when the copies fit
-// beside the boundary arrays, else 8 (chosen per launch; strip_qcopies in refine.cuh).
+// Lane copies of the padded query pairs (q[c], q[c-1]): 16 (a 64-bit load serves a half-warp
+// per wavefront: conflict-free) when they fit beside the boundary arrays, else 8 (chosen
+// per launch; strip_qcopies in refine.cuh).
 
 template <int... Is, class F>
 __device__ __forceinline__ void static_for_impl(std::integer_sequence<int, Is...>, F&& f)
@@ -340,16 +341,20 @@ __device__ __forceinline__ void static_for(F&& f)
 template <int H>
 struct DtwStrip {
     float S[2][H];  // row values at steps of parity 0 / 1
-    float Qw[H];    // query window: Qw[t % H] = q at row 0's column of step t
+    float2 Qp[H];   // query window: Qp[t % H] = (q[c], q[c-1]), c = row 0's column at step t
     float cv[H];    // candidate points of the strip's rows
+    float2 ncv[H / 2];  // (-cv[2p], -cv[2p+1]): row pairs subtract with one FADD2
     float bprev;    // row 0's diagonal input (boundary slot of the previous step)
     float rmin;     // min over row H-1 (the strip's last row)
 
     // One step t (compile-time facts: PH = t % H, PAR = t & 1, active rows [LO, HI],
     // whether row H-1 writes the boundary).  bsrc: boundary slot t+1 (read when row 0 is
-    // active), q: query column j0 - R + t (advanced by K copies), bdst: boundary slot t - 2H + 2.
-    template <int PH, int PAR, int LO, int HI, int K>
-    __device__ __forceinline__ void step(const float* bsrc, const float* q, float* bdst)
+    // active), q: the pair (q[c], q[c-1]) at column c = j0 - R + t, bdst: boundary slot t - 2H + 2.
+    // Rows go in aligned pairs (2p, 2p+1): the pair loaded u steps ago holds exactly the two
+    // query points rows u and u+1 need now, so both differences are one FADD2 and both cells
+    // one FFMA2.
+    template <int PH, int PAR, int LO, int HI>
+    __device__ __forceinline__ void step(const float* bsrc, const float2* q, float* bdst)
     {
         float up0 = 0.0f, dg0 = 0.0f;
         if constexpr (LO == 0) {
@@ -357,23 +362,32 @@ struct DtwStrip {
             dg0 = bprev;
             bprev = up0;
         }
-        Qw[PH] = *q;
+        Qp[PH] = *q;
         float nv[H];
-        static_for<(HI - LO + 2) / 2>([&](auto P) {
-            constexpr int u = LO + 2 * decltype(P)::value;
+        static_for<HI / 2 - LO / 2 + 1>([&](auto P) {
+            constexpr int u = 2 * (LO / 2 + decltype(P)::value);
             constexpr int v = u + 1;
-            const float upu = u == 0 ? up0 : S[PAR ^ 1][u == 0 ? 0 : u - 1];
-            const float dgu = u == 0 ? dg0 : S[PAR][u == 0 ? 0 : u - 1];
-            const float mnu = min3f(dgu, upu, S[PAR ^ 1][u]);
-            const float dfu = Qw[(PH - u + 2 * H) % H] - cv[u];
-            if constexpr (v <= HI) {
+            constexpr bool au = u >= LO && u <= HI, av = v >= LO && v <= HI;
+            const float2 qq = Qp[(PH - u + 2 * H) % H];  // (q[c-u], q[c-u-1])
+            float mnu = 0.0f;
+            if constexpr (au) {
+                const float upu = u == 0 ? up0 : S[PAR ^ 1][u == 0 ? 0 : u - 1];
+                const float dgu = u == 0 ? dg0 : S[PAR][u == 0 ? 0 : u - 1];
+                mnu = min3f(dgu, upu, S[PAR ^ 1][u]);
+            }
+            if constexpr (au && av) {
                 const float mnv = min3f(S[PAR][u], S[PAR ^ 1][u], S[PAR ^ 1][v]);
-                const float dfv = Qw[(PH - v + 2 * H) % H] - cv[v];
-                const float2 r = ffma2(make_float2(dfu, dfv), make_float2(dfu, dfv), make_float2(mnu, mnv));
+                const float2 df = fadd2(qq, ncv[u / 2]);
+                const float2 r = ffma2(df, df, make_float2(mnu, mnv));
                 nv[u] = r.x;
                 nv[v] = r.y;
-            } else {
+            } else if constexpr (au) {
+                const float dfu = qq.x - cv[u];
                 nv[u] = fmaf(dfu, dfu, mnu);
+            } else if constexpr (av) {
+                const float mnv = min3f(S[PAR][u], S[PAR ^ 1][u], S[PAR ^ 1][v]);
+                const float dfv = qq.y - cv[v];
+                nv[v] = fmaf(dfv, dfv, mnv);
             }
         });
 #pragma unroll
@@ -388,26 +402,29 @@ struct DtwStrip {
     }
 
     // All steps of the strip of rows j0 .. j0+H-1 (cv loaded).  Bt: this thread's boundary
-    // slot 0; qt: the query copy at column j0 - R (K copies per column); nfull = (2R - 2H + 3) / H.
+    // slot 0; qt: the query pairs' copy at column j0 - R (K copies per column); nfull =
+    // (2R - 2H + 3) / H.
     template <int REM, int K>
-    __device__ __forceinline__ void run(float* Bt, const float* qt, int R, int nfull)
+    __device__ __forceinline__ void run(float* Bt, const float2* qt, int R, int nfull)
     {
         constexpr int T = kStripThreads;
 #pragma unroll
         for (int u = 0; u < H; ++u) S[0][u] = S[1][u] = INFINITY;
+#pragma unroll
+        for (int p = 0; p < H / 2; ++p) ncv[p] = make_float2(-cv[2 * p], -cv[2 * p + 1]);
         bprev = Bt[0];
         rmin = INFINITY;
         static_for<2 * H - 2>([&](auto I) {  // prologue: rows 0 .. t/2
             constexpr int t = decltype(I)::value;
-            step<t % H, t & 1, 0, t / 2, K>(Bt + (t + 1) * T, qt + t * K, nullptr);
+            step<t % H, t & 1, 0, t / 2>(Bt + (t + 1) * T, qt + t * K, nullptr);
         });
         float* bp = Bt + (2 * H - 1) * T;
         float* wp = Bt;
-        const float* qp = qt + (2 * H - 2) * K;
+        const float2* qp = qt + (2 * H - 2) * K;
         for (int c = 0; c < nfull; ++c) {
             static_for<H>([&](auto I) {
                 constexpr int k = decltype(I)::value;
-                step<(2 * H - 2 + k) % H, k & 1, 0, H - 1, K>(bp + k * T, qp + k * K, wp + k * T);
+                step<(2 * H - 2 + k) % H, k & 1, 0, H - 1>(bp + k * T, qp + k * K, wp + k * T);
             });
             bp += H * T;
             qp += H * K;
@@ -415,13 +432,13 @@ struct DtwStrip {
         }
         static_for<REM>([&](auto I) {
             constexpr int k = decltype(I)::value;
-            step<(2 * H - 2 + k) % H, k & 1, 0, H - 1, K>(bp + k * T, qp + k * K, wp + k * T);
+            step<(2 * H - 2 + k) % H, k & 1, 0, H - 1>(bp + k * T, qp + k * K, wp + k * T);
         });
         float* we = wp + REM * T;                 // boundary slot of step 2R+1
-        const float* qe = qt + 2 * R * K;         // query column of step 2R
+        const float2* qe = qt + 2 * R * K;        // query column of step 2R
         static_for<2 * H - 2>([&](auto I) {  // epilogue: rows (t+1)/2 .. H-1 at step 2R + t
             constexpr int t = decltype(I)::value + 1;
-            step<(REM + 3 * H - 3 + t) % H, t & 1, (t + 1) / 2, H - 1, K>(nullptr, qe + t * K, we + (t - 1) * T);
+            step<(REM + 3 * H - 3 + t) % H, t & 1, (t + 1) / 2, H - 1>(nullptr, qe + t * K, we + (t - 1) * T);
         });
     }
 };

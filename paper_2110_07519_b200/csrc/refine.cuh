@@ -454,18 +454,19 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
 }
 
 // Shared memory of k_refine_dtw_strip: the boundary arrays (2R+2 slots x kStripThreads),
-// the query padded by R points of +inf on each side in K lane copies, U, L.
+// the query pairs padded by R points of +inf on each side in K lane copies, U, L.
 __host__ __device__ inline size_t strip_smem(int n, int R, int K)
 {
     const size_t npad = (size_t)((n + 3) & ~3);
-    return ((size_t)(2 * R + 2) * kStripThreads + (size_t)(n + 2 * R) * K + 2 * npad) * sizeof(float);
+    return ((size_t)(2 * R + 2) * kStripThreads + (size_t)(n + 2 * R) * K * 2 + 2 * npad) * sizeof(float);
 }
 
-// Query copies: 32 while the CTA's shared memory stays <= 76 KB (three CTAs per SM; C4: 68 KB,
-// 1305 vs 1277 q/s with 8 copies -- the 8-copy loads conflicted on 46% of wavefronts), else 8.
+// Query copies: 16 while the CTA's shared memory stays <= 76 KB (three CTAs per SM; C4: 68 KB;
+// with 8 copies of single points the loads conflicted on 46% of wavefronts: 1277 vs 1305
+// q/s), else 8.
 __host__ __device__ inline int strip_qcopies(int n, int R)
 {
-    return (strip_smem(n, R, 32) <= 76 * 1024 || R < 7) ? 32 : 8;  // K = 8 variants exist for H = 8
+    return (strip_smem(n, R, 16) <= 76 * 1024 || R < 7) ? 16 : 8;  // K = 8 variants exist for H = 8
 }
 
 // DTW step 2 for any reach (DtwStrip<H>, one thread per LB_Keogh survivor), the same
@@ -485,18 +486,18 @@ __global__ void __launch_bounds__(kStripThreads) k_refine_dtw_strip(const float*
     extern __shared__ __align__(16) float dsm[];
     constexpr int T = kStripThreads;
     const int npad = (n + 3) & ~3;
-    float* qrep = dsm + (size_t)(2 * R + 2) * T;
-    float* U = qrep + (size_t)(n + 2 * R) * K;
+    float2* qrep = reinterpret_cast<float2*>(dsm + (size_t)(2 * R + 2) * T);  // 8-byte aligned: 2R+2 even
+    float* U = reinterpret_cast<float*>(qrep + (size_t)(n + 2 * R) * K);
     float* L = U + npad;
     for (int x = threadIdx.x; x < (n + 2 * R) * K; x += T) {
         const int i = x / K - R;
-        qrep[x] = (i >= 0 && i < n) ? q_g[i] : INFINITY;
+        qrep[x] = make_float2((i >= 0 && i < n) ? q_g[i] : INFINITY, (i >= 1 && i <= n) ? q_g[i - 1] : INFINITY);
     }
     for (int i = threadIdx.x; i < n; i += T) { U[i] = U_g[i]; L[i] = L_g[i]; }
     __syncthreads();
     const int lane = threadIdx.x & 31;
     float* Bt = dsm + threadIdx.x;
-    const float* qlane = qrep + (lane & (K - 1));
+    const float2* qlane = qrep + (lane & (K - 1));
     const int nfull = (2 * R - 2 * H + 3) / H;
     const unsigned nfront = *(volatile unsigned*)&st->list2_count;
     const unsigned total = nfront + *(volatile unsigned*)&st->list2_back;
