@@ -190,11 +190,16 @@ struct ProfScope {
 
 // Strip DTW instantiations (rows per strip H, REM = (2R - 2H + 3) mod H): H = 8 for R >= 7,
 // 4 for R in [3, 6], 2 for R in [1, 2].
-// K: query-pair copies (16, or 8 when 16 would not fit three CTAs per SM -- large R, H = 8).
-#define MESSI_STRIP_VARIANTS(X)                                                                               \
-    X(8, 0, 16) X(8, 1, 16) X(8, 2, 16) X(8, 3, 16) X(8, 4, 16) X(8, 5, 16) X(8, 6, 16) X(8, 7, 16) X(4, 0, 16) \
-    X(4, 1, 16) X(4, 2, 16) X(4, 3, 16) X(2, 0, 16) X(2, 1, 16) X(8, 0, 8) X(8, 1, 8) X(8, 2, 8) X(8, 3, 8)        \
-    X(8, 4, 8) X(8, 5, 8) X(8, 6, 8) X(8, 7, 8)
+// K: query-pair copies (16, or 8 when 16 would not fit three CTAs per SM -- large R, H = 8);
+// T: threads per CTA (128; 64 with one query copy when even 8 copies and 128 threads would not
+// fit: e.g. n = 2048 at a 10% window).
+#define MESSI_STRIP_VARIANTS(X)                                                                  \
+    X(8, 0, 16, 128) X(8, 1, 16, 128) X(8, 2, 16, 128) X(8, 3, 16, 128) X(8, 4, 16, 128)          \
+    X(8, 5, 16, 128) X(8, 6, 16, 128) X(8, 7, 16, 128) X(4, 0, 16, 128) X(4, 1, 16, 128)          \
+    X(4, 2, 16, 128) X(4, 3, 16, 128) X(2, 0, 16, 128) X(2, 1, 16, 128) X(8, 0, 8, 128)           \
+    X(8, 1, 8, 128) X(8, 2, 8, 128) X(8, 3, 8, 128) X(8, 4, 8, 128) X(8, 5, 8, 128) X(8, 6, 8, 128) \
+    X(8, 7, 8, 128) X(8, 0, 1, 64) X(8, 1, 1, 64) X(8, 2, 1, 64) X(8, 3, 1, 64) X(8, 4, 1, 64)      \
+    X(8, 5, 1, 64) X(8, 6, 1, 64) X(8, 7, 1, 64)
 static const int kStripSmemMax = 227 * 1024;
 
 static int strip_rows(int R)
@@ -210,11 +215,16 @@ static int strip_rows(int R)
 // profiles/r01_sweeps_dtw.jsonl) and wherever no register band is instantiated, as long as
 // its shared memory fits; the register band (DtwThread<R>) for R = 2, 5; else the warp
 // wavefront.  MESSI_DTW_STRIP=1 / 0 forces the strip kernel on / off (experiments).
+// Threads per strip CTA: 128 when the CTA's shared memory fits, else 64 (large reaches).
+static int strip_threads(int n, int R) { return strip_qcopies(n, R) == 1 ? 64 : 128; }
+
 static bool use_strip(int n, int R, bool have_band)
 {
     const char* e = getenv("MESSI_DTW_STRIP");  // read per launch: tests switch it
     const int force = e ? atoi(e) : -1;
-    const bool fits = R >= 1 && strip_smem(n, R, strip_qcopies(n, R)) <= (size_t)kStripSmemMax;
+    const int T = strip_threads(n, R);
+    const bool fits = R >= 1 && (T == 128 || R >= 7) &&
+                      strip_smem(n, R, strip_qcopies(n, R), T) <= (size_t)kStripSmemMax;
     if (force == 0) return false;
     if (force == 1) return fits;
     return fits && (!have_band || R >= 7);
@@ -225,15 +235,16 @@ static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R,
     const int H = strip_rows(R);
     const int rem = (2 * R - 2 * H + 3) % H;
     const int K = strip_qcopies(n, R);
-    const size_t smem = strip_smem(n, R, K);
+    const int T = strip_threads(n, R);
+    const size_t smem = strip_smem(n, R, K, T);
     bool launched = false;
-#define LAUNCH_S(HH, REM, KK)                                                                                    \
-    if (!launched && H == HH && rem == REM && K == KK) {                                                        \
+#define LAUNCH_S(HH, REM, KK, TT)                                                                                \
+    if (!launched && H == HH && rem == REM && K == KK && T == TT) {                                             \
         int occ = 0;                                                                                             \
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_dtw_strip<HH, REM, KK>, kStripThreads, smem)); \
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_dtw_strip<HH, REM, KK, TT>, TT, smem));  \
         const char* oe = getenv("MESSI_DTW_REFINE_OCC"); /* experiments: CTAs per SM */                          \
         if (oe && atoi(oe) > 0 && atoi(oe) < occ) occ = atoi(oe);                                                \
-        k_refine_dtw_strip<HH, REM, KK><<<idx->sms * (occ > 0 ? occ : 1), kStripThreads, smem, rs>>>(            \
+        k_refine_dtw_strip<HH, REM, KK, TT><<<idx->sms * (occ > 0 ? occ : 1), TT, smem, rs>>>(                   \
             idx->rows, n, R, q_dev, sl.U, sl.L, sl.list2, (unsigned)idx->N, sl.st, sl.near);                     \
         launched = true;                                                                                         \
     }
@@ -263,7 +274,7 @@ static messi_status setup_kernels()
     CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_refine_dtw_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_resolve_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-#define SET_ATTR_S(H, REM, K) CK(cudaFuncSetAttribute(k_refine_dtw_strip<H, REM, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStripSmemMax));
+#define SET_ATTR_S(H, REM, K, T) CK(cudaFuncSetAttribute(k_refine_dtw_strip<H, REM, K, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStripSmemMax));
     MESSI_STRIP_VARIANTS(SET_ATTR_S)
 #undef SET_ATTR_S
 #define SET_ATTR_R(R) CK(cudaFuncSetAttribute(k_refine_dtw<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));

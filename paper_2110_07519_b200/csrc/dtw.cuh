@@ -322,7 +322,7 @@ struct DtwThread {
 // (epilogue) are unrolled with their active rows fixed at compile time, the 2R - 2H + 3
 // steps between them run in H-step chunks (the query window rotates through H registers)
 // plus REM = (2R - 2H + 3) mod H single steps (a template parameter).
-constexpr int kStripThreads = 128;
+constexpr int kStripThreads = 128;  // threads per CTA (64 for reaches whose boundary arrays need it)
 // Lane copies of the padded query pairs (q[c], q[c-1]): 16 (a 64-bit load serves a half-warp
 // per wavefront: conflict-free) when they fit beside the boundary arrays, else 8 (chosen
 // per launch; strip_qcopies in refine.cuh).
@@ -404,10 +404,9 @@ struct DtwStrip {
     // All steps of the strip of rows j0 .. j0+H-1 (cv loaded).  Bt: this thread's boundary
     // slot 0; qt: the query pairs' copy at column j0 - R (K copies per column); nfull =
     // (2R - 2H + 3) / H.
-    template <int REM, int K>
+    template <int REM, int K, int T>
     __device__ __forceinline__ void run(float* Bt, const float2* qt, int R, int nfull)
     {
-        constexpr int T = kStripThreads;
 #pragma unroll
         for (int u = 0; u < H; ++u) S[0][u] = S[1][u] = INFINITY;
 #pragma unroll

@@ -453,12 +453,12 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
     }
 }
 
-// Shared memory of k_refine_dtw_strip: the boundary arrays (2R+2 slots x kStripThreads),
-// the query pairs padded by R points of +inf on each side in K lane copies, U, L.
-__host__ __device__ inline size_t strip_smem(int n, int R, int K)
+// Shared memory of k_refine_dtw_strip: the boundary arrays (2R+2 slots x T threads), the
+// query pairs padded by R points of +inf on each side in K lane copies, U, L.
+__host__ __device__ inline size_t strip_smem(int n, int R, int K, int T = kStripThreads)
 {
     const size_t npad = (size_t)((n + 3) & ~3);
-    return ((size_t)(2 * R + 2) * kStripThreads + (size_t)(n + 2 * R) * K * 2 + 2 * npad) * sizeof(float);
+    return ((size_t)(2 * R + 2) * T + (size_t)(n + 2 * R) * K * 2 + 2 * npad) * sizeof(float);
 }
 
 // Query copies: 16 while the CTA's shared memory stays <= 76 KB (three CTAs per SM; C4: 68 KB;
@@ -466,7 +466,9 @@ __host__ __device__ inline size_t strip_smem(int n, int R, int K)
 // q/s), else 8.
 __host__ __device__ inline int strip_qcopies(int n, int R)
 {
-    return (strip_smem(n, R, 16) <= 76 * 1024 || R < 7) ? 16 : 8;  // K = 8 variants exist for H = 8
+    if (strip_smem(n, R, 16) <= 76 * 1024 || R < 7) return 16;
+    if (strip_smem(n, R, 8) <= 227 * 1024) return 8;  // K = 8 variants exist for H = 8
+    return 1;  // large n and R: one copy, 64-thread CTAs (strip_threads)
 }
 
 // DTW step 2 for any reach (DtwStrip<H>, one thread per LB_Keogh survivor), the same
@@ -475,8 +477,8 @@ __host__ __device__ inline int strip_qcopies(int n, int R)
 // later candidate point j at least once, at a cost >= that point's LB_Keogh term against
 // the query envelope, so the candidate is dropped when rmin + (LBK_total -
 // LBK of the rows done) exceeds the threshold (2^-10 margins for the fp32 sums).
-template <int H, int REM, int K>
-__global__ void __launch_bounds__(kStripThreads) k_refine_dtw_strip(const float* __restrict__ rows, int n, int R,
+template <int H, int REM, int K, int T>
+__global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict__ rows, int n, int R,
                                                                    const float* __restrict__ q_g,
                                                                    const float* __restrict__ U_g,
                                                                    const float* __restrict__ L_g,
@@ -484,7 +486,6 @@ __global__ void __launch_bounds__(kStripThreads) k_refine_dtw_strip(const float*
                                                                    QState* st, NearEntry* near)
 {
     extern __shared__ __align__(16) float dsm[];
-    constexpr int T = kStripThreads;
     const int npad = (n + 3) & ~3;
     float2* qrep = reinterpret_cast<float2*>(dsm + (size_t)(2 * R + 2) * T);  // 8-byte aligned: 2R+2 even
     float* U = reinterpret_cast<float*>(qrep + (size_t)(n + 2 * R) * K);
@@ -570,7 +571,7 @@ __global__ void __launch_bounds__(kStripThreads) k_refine_dtw_strip(const float*
 #pragma unroll
             for (int u = 0; u < H; ++u) dp.cv[u] = cnext[u];
             if (j0 + H < n) load_h(c, j0 + H, cnext);  // the next strip's points, one strip ahead
-            dp.template run<REM, K>(Bt, qlane + (size_t)j0 * K, R, nfull);
+            dp.template run<REM, K, T>(Bt, qlane + (size_t)j0 * K, R, nfull);
             ++strips;
 #pragma unroll
             for (int u = 0; u < H; ++u) {
