@@ -64,11 +64,13 @@ typedef struct {
     int64_t lb_computed;  /* series lower bounds evaluated (the members of the scanned tiles) */
     int64_t tiles_scanned; /* 512-series tiles whose box bound <= BSF0 * (1 + eps) (scanned) */
     int64_t candidates;   /* series whose iSAX bound <= BSF0 * (1 + eps) */
-    int64_t lbk_pass;     /* DTW: candidates whose raw LB_Keogh <= BSF * (1 + eps) */
+    int64_t lbk_pass;     /* DTW: candidates passing the LB_Keogh filter against BSF0: the bound
+                             from the quantised row, (sqrt(LBK(x^)) - e)^2, at reaches served by
+                             the strip refine (r >= 7), the raw LB_Keogh otherwise */
     int64_t refined;      /* real distances computed (fp32) in the refine step */
     int64_t abandoned;    /* real distance computations abandoned early */
     int64_t near_best;    /* fp32 near-ties re-ranked exactly in fp64 */
-    int64_t dtw_cells;    /* DTW band cells evaluated in fp32 by the register-band refine */
+    int64_t dtw_cells;    /* DTW band cells evaluated in fp32 by the refine (strip or register band) */
     int64_t exact;        /* real distances over the raw fp32 rows: ED = candidates whose
                              quantised-row bound did not prune them; DTW = refined */
     int64_t tiles_listed; /* tiles whose box bound <= BSF0 * (1 + eps) (the filter's list); ED scans
