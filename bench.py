@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--cpu-queries", type=int, default=32, help="queries of the oracle timing sample")
     ap.add_argument("--window", type=int, default=0, help="approximate-search window (0: library default 2000)")
     ap.add_argument("--knn", type=int, default=10, help="ED: also time exact k-NN with this k (<= 1: skip)")
+    ap.add_argument("--latency", type=int, default=20,
+                    help="1 GPU: also time this many single-query calls (latency mode, p50/p99; 0: skip)")
     ap.add_argument("--no-share-bsf", action="store_true",
                     help="N > 1: do not link the shards (no best-so-far sharing over peer memory)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -283,9 +285,25 @@ def run_arm(cfg, args, world, rank, dev, stream, time_steps, warmup):
             torch.cuda.synchronize()
             barrier(world)
             knn = k0.elapsed_time(k1)
+        # latency mode (SURVEY 8(d) protocol, the paper's one-query-at-a-time model P:2024-2026):
+        # the synchronous single-query call, query from pinned host memory to result in host
+        # memory, CUDA events on the index stream around each call
+        lat = []
+        if world == 1 and args.latency > 0:
+            qh1 = Q[: min(nq, args.latency)].cpu().pin_memory()
+            for i in range(min(3, qh1.shape[0])):  # warm-up
+                idx.query_ed(qh1[i]) if reach is None else idx.query_dtw(qh1[i], reach)
+            for i in range(qh1.shape[0]):
+                l0 = torch.cuda.Event(enable_timing=True)
+                l1 = torch.cuda.Event(enable_timing=True)
+                l0.record(stream)
+                idx.query_ed(qh1[i]) if reach is None else idx.query_dtw(qh1[i], reach)
+                l1.record(stream)
+                torch.cuda.synchronize()
+                lat.append(l0.elapsed_time(l1))
     out = dict(ms=ms, build_ms=build_ms, launches=launches, prof=prof, prof_ms=prof_ms, stats=st, clocks=clk.summary(),
                e2e_ms=e2e_ms, knn_ms=knn, nq=nq, N_local=X.shape[0], n=cfg["n"], reach=reach, h2d=qh.numel() * 4,
-               d2h=rh.numel())
+               d2h=rh.numel(), latency_ms=lat)
     idx.close()
     del X, Q
     torch.cuda.empty_cache()
@@ -444,6 +462,26 @@ def ours(args):
                                              "abandoned", "near_best", "dtw_cells", "exact", "tiles_listed", "coarse",
                                              "seed_d2", "bsf_d2")},
     }
+    def dist_of(stl):
+        import statistics
+        def q(vals, p):
+            v = sorted(vals)
+            return v[min(len(v) - 1, int(p * len(v)))]
+        c = [x["candidates"] for x in stl]
+        r = [x["refined"] for x in stl]
+        ratio = [x["seed_d2"] / x["bsf_d2"] for x in stl if x["bsf_d2"] > 0]
+        return {"candidates": {"mean": statistics.fmean(c), "median": statistics.median(c), "p90": q(c, 0.9)},
+                "refined": {"mean": statistics.fmean(r), "median": statistics.median(r), "p90": q(r, 0.9)},
+                "bsf0_over_final": {"median": statistics.median(ratio) if ratio else None,
+                                    "p90": q(ratio, 0.9) if ratio else None},
+                "near_best_mean": statistics.fmean(x["near_best"] for x in stl)}
+
+    line["stats_dist"] = dist_of(main["stats"])
+    if main.get("latency_ms"):
+        lt = sorted(main["latency_ms"])
+        line["latency"] = {"queries": len(lt), "p50_ms": lt[len(lt) // 2], "p99_ms": lt[min(len(lt) - 1, int(0.99 * len(lt)))],
+                           "mean_ms": sum(lt) / len(lt),
+                           "what": "synchronous single-query calls (host query in, host result out), CUDA events"}
     if main.get("knn_ms"):
         kms = max_over_ranks(main["knn_ms"], world)
         line["knn"] = {"k": args.knn, "value": K * nq / (kms / 1e3), "unit": "queries/s", "ms_per_step": kms / K,
@@ -463,7 +501,12 @@ def ours(args):
                        "stats_mean": {k: dm(k) for k in ("lb_computed", "tiles_scanned", "candidates", "lbk_pass",
                                                          "refined", "abandoned", "near_best", "dtw_cells",
                                                          "coarse", "seed_d2", "bsf_d2")},
-                       "gpu_launches": d["launches"], "roofline": dtw_roofline(d, k4)}
+                       "gpu_launches": d["launches"], "roofline": dtw_roofline(d, k4),
+                       "stats_dist": dist_of(dst)}
+        if d.get("latency_ms"):
+            lt = sorted(d["latency_ms"])
+            line["dtw"]["latency"] = {"queries": len(lt), "p50_ms": lt[len(lt) // 2],
+                                      "p99_ms": lt[min(len(lt) - 1, int(0.99 * len(lt)))]}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, args, dev, "ED" if cfg["reach"] is None else "DTW")
     if rank == 0:
