@@ -447,5 +447,15 @@ def test_errors():
         with pytest.raises(m.MessiError) as e:
             idx.query_dtw(X[0], 65)
         assert e.value.status == m.MESSI_EINVAL
+        with pytest.raises(m.MessiError) as e:
+            idx.query_dtw(X[0], -1)
+        assert e.value.status == m.MESSI_EINVAL
+        for bad_k in (0, 65):  # k-NN: 1 <= k <= 64
+            with pytest.raises(m.MessiError) as e:
+                idx.query_knn(X[0], bad_k)
+            assert e.value.status == m.MESSI_EINVAL
+        # the index stays usable after rejected calls
+        _, gid, d2 = idx.query_ed(X[3])
+        assert gid == 3 and d2 == 0.0
     finally:
         idx.close()
