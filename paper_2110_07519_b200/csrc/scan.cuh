@@ -386,11 +386,21 @@ __global__ void __launch_bounds__(32 * kScanWarps, 3) k_scan(const uint4* __rest
         const long long tl = (long long)tlist[it];
         const int m = scan_tile_coarse(tiles, tl, lbase, thr, N, surv, lane);
         if (lane == 0 && m) atomicAdd(&st->coarse_count, (unsigned)m);
+        // rounds of 32 coarse survivors; the next round's 8-bit words are loaded before this
+        // round's bounds are evaluated (DTW: ~40% of a tile survives the coarse bound)
+        unsigned pos_n = lane < m ? (unsigned)(tl * MESSI_TILE_ROWS + surv[lane]) : 0u;
+        uint4 w_n = lane < m ? sym8[pos_n] : make_uint4(0u, 0u, 0u, 0u);
         for (int i0 = 0; i0 < m; i0 += 32) {
             const bool v = i0 + lane < m;
-            const unsigned pos = v ? (unsigned)(tl * MESSI_TILE_ROWS + surv[i0 + lane]) : 0u;
+            const unsigned pos = pos_n;
+            const uint4 w = w_n;
+            if (i0 + 32 < m) {
+                const bool vn = i0 + 32 + lane < m;
+                pos_n = vn ? (unsigned)(tl * MESSI_TILE_ROWS + surv[i0 + 32 + lane]) : 0u;
+                if (vn) w_n = sym8[pos_n];
+            }
             float lb = INFINITY;
-            if (v) lb = fine_lb(sym8[pos], lbase, lane);
+            if (v) lb = fine_lb(w, lbase, lane);
             const bool ok = v && lb <= thr;
             const unsigned msk = __ballot_sync(0xffffffffu, ok);
             if (!msk) continue;
