@@ -230,6 +230,36 @@ def test_quantised_rows_and_bound(c1):
         assert np.all(lb <= true * (1 + 1e-12))
 
 
+def test_quantised_lb_keogh_bound(c1):
+    """The quantised LB_Keogh bound of the strip DTW path (k_lbk_filter_q8 and the strip
+    refine's tail): for every row x of C1 and every suffix of its points,
+    (sqrt(LBK_S(x^)) - e)^2 <= LBK_S(x) (the raw LB_Keogh of the suffix, oracle.lb_keogh2
+    terms) <= DTW^2 when S is the whole row -- checked in fp64 with the GPU's own quantised
+    rows, for two C1 queries and reaches 7 / 25."""
+    X, Q, idx, Xh, Qh = c1
+    rows = 3000
+    q8, meta = messi().messi_debug_quantised(idx.handle, X.shape[0], X.shape[1], X.device)
+    c = q8[:rows].cpu().numpy().astype(np.float64) - 128.0
+    s = meta[:rows, 0].cpu().numpy().astype(np.float64)
+    e = meta[:rows, 1].cpu().numpy().astype(np.float64)
+    x = Xh[:rows].astype(np.float64)
+    xq = s[:, None] * c
+    for r in (7, 25):
+        for qi in range(2):
+            U, L = oracle.envelope(Qh[qi], r)
+            U, L = np.asarray(U, dtype=np.float64), np.asarray(L, dtype=np.float64)
+            term = lambda v: np.where(v > U, v - U, np.where(v < L, v - L, 0.0)) ** 2  # noqa: E731
+            tx, tq = term(x), term(xq)
+            for j in (0, 8, 64, 200):  # suffixes S = points j .. n-1
+                raw = tx[:, j:].sum(axis=1)
+                bnd = np.maximum(0.0, np.sqrt(tq[:, j:].sum(axis=1)) - e) ** 2
+                assert np.all(bnd <= raw * (1 + 1e-12) + 1e-300)
+            full = np.array([oracle.lb_keogh2(U, L, x[i]) for i in range(50)])
+            assert np.allclose(full, tx[:50].sum(axis=1), rtol=1e-12, atol=0)
+            d = oracle.dtw2_rows(Xh[:50], Qh[qi], r)
+            assert np.all(tx[:50].sum(axis=1) <= np.asarray(d) * (1 + 1e-12))
+
+
 # --------------------------------------------------------------------- 1-NN end to end
 def check_nn(got, ref_d2, ref_id):
     dist, gid, d2 = got[:3]
