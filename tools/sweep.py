@@ -55,7 +55,7 @@ def time_batch(idx, Q, reach, steps=2, warmup=1, knn=1):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--what", default="dtw,length,noise,knn")
+    ap.add_argument("--what", default="dtw,length,noise,knn,dtw_length")
     a = ap.parse_args()
     what = a.what.split(",")
     if "dtw" in what:  # DTW window sweep, 10M x 256 (C4 collection), 20 queries
@@ -70,6 +70,20 @@ def main():
         idx.close()
         del X, Q
         torch.cuda.empty_cache()
+    if "dtw_length" in what:  # DTW at a 10% window, series length 128..2048 at 2.56 GB of rows, 10 queries
+        for n in (128, 256, 512, 1024, 2048):
+            N = 2_560_000_000 // (4 * n)
+            X = gen(N, n, datagen.DATA_SEED)
+            Q = gen(10, n, datagen.QUERY_SEED)
+            torch.cuda.synchronize()
+            idx = M.Index(X)
+            r = n // 10
+            qps, ms, mean = time_batch(idx, Q, r)
+            print(json.dumps({"sweep": "dtw_length", "rows": N, "n": n, "reach": r, "queries": 10, "qps": qps,
+                              "ms_per_batch": ms, **mean}), flush=True)
+            idx.close()
+            del X, Q
+            torch.cuda.empty_cache()
     if "length" in what:  # ED, series length at 25.6 GB of rows, 100 queries
         for n in (128, 256, 512, 1024, 2048):
             N = 25_600_000_000 // (4 * n)
