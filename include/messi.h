@@ -22,6 +22,14 @@
  *     non-batch calls synchronise that stream before returning.
  *   - float data is row-major fp32 [count][length]; ids are 0-based, global ids are
  *     cfg.row_begin + local row.
+ *
+ * Deviations from the contract SURVEY.md 8(b) proposed (all additive): messi_result also
+ * carries the exact fp64 d2 (the cross-shard merge key: sqrt loses the order of near-ties)
+ * and a reserved word (32-byte records); messi_stats has per-stage counters of this design
+ * (tiles, coarse / fine survivors, quantised-bound survivors) instead of the proposed list;
+ * messi_config has keep_paa (tests only).  Beyond the four north-star calls the library
+ * exports batched and k-NN forms, the shard-linking calls, per-kernel timing and the
+ * inspection entry points at the end of this file.
  */
 #ifndef MESSI_H
 #define MESSI_H
@@ -70,7 +78,9 @@ typedef struct {
     int64_t refined;      /* real distances computed (fp32) in the refine step */
     int64_t abandoned;    /* real distance computations abandoned early */
     int64_t near_best;    /* fp32 near-ties re-ranked exactly in fp64 */
-    int64_t dtw_cells;    /* DTW band cells evaluated in fp32 by the refine (strip or register band) */
+    int64_t dtw_cells;    /* DTW: valid band cells (|i - j| <= r inside the n x n matrix) of the rows the
+                             fp32 refine evaluated -- n(2r+1) - r(r+1) per completed candidate, the
+                             rows done for an abandoned one */
     int64_t exact;        /* real distances over the raw fp32 rows: ED = candidates whose
                              quantised-row bound did not prune them; DTW = refined */
     int64_t tiles_listed; /* tiles whose box bound <= BSF0 * (1 + eps) (the filter's list); ED scans
@@ -112,7 +122,8 @@ messi_status messi_query_dtw_batch(messi_index* idx, const float* queries_dev, i
  * them.  Exactness is unchanged: a shard may then prune its own rows down to "no row within
  * the global BSF" (its local answer is then (inf, -1)), and the cross-shard lexicographic
  * min of the local answers (dist.py) is the global one.  Linked shards must make the same
- * sequence of ED batch calls (the epoch counts launch groups); the DTW path ignores links.
+ * sequence of ED batch calls after linking (the epoch = link generation | launch groups since
+ * the link, so values written under an earlier link never match); the DTW path ignores links.
  *
  * messi_batch_state_ipc: the CUDA IPC handle (64 bytes into handle_out) of this index's
  *   per-query state array `set` (0 or 1).
@@ -148,13 +159,21 @@ const char* messi_last_error(void);
 /* Kernel launches the library enqueued so far on this index (for bench accounting). */
 int64_t messi_launch_count(const messi_index* idx);
 
-/* Per-kernel device timing (bench accounting): when enabled, the library brackets every
- * launch of the query path with CUDA events on the index stream.  kind: 0 seed (prologue +
- * approximate search), 1 lower-bound scan, 2 refine (ED or DTW), 3 DTW LB_Keogh filter,
- * 4 exact resolve.  messi_profile_enable resets the accumulators; messi_profile_read
- * synchronises the stream and returns the summed milliseconds and the launch count. */
+/* Per-kernel device timing (bench accounting): with bit 0 of `enable` set the library brackets
+ * every launch of the query path with CUDA events on the stream it is launched on; with bit 1
+ * set every stage of the per-query (DTW) path runs on cfg.stream, with no overlap between
+ * stages or queries (so per-kernel times add up to the step).  kind: 0 seed (prologue +
+ * approximate search + tile filter), 1 lower-bound scan (ED: the fused scan + refine
+ * kernel), 2 refine (DTW), 3 DTW LB_Keogh filter, 4 exact resolve.  messi_profile_enable
+ * resets the accumulators; messi_profile_read synchronises and returns the summed
+ * milliseconds and the launch count. */
 messi_status messi_profile_enable(messi_index* idx, int32_t enable);
 messi_status messi_profile_read(messi_index* idx, int32_t kind, double* total_ms, int64_t* launches);
+
+/* Device time of the build phases (CUDA events on cfg.stream inside messi_build), ms_out[4]:
+ * 0 breakpoints + summarisation (PAA, symbols, keys: Alg. 3), 1 the CUB key sort,
+ * 2 sorted layout (tiles, 8-bit words, boxes, super-boxes), 3 quantised rows. */
+messi_status messi_build_times(const messi_index* idx, double* ms_out);
 
 /* Scan throughput in isolation: one query's prologue and tile filter, then `reps` scans back
  * to back, each timed with CUDA events; *ms_out = summed kernel milliseconds, *coarse_out
@@ -162,7 +181,12 @@ messi_status messi_profile_read(messi_index* idx, int32_t kind, double* total_ms
 messi_status messi_debug_scan_repeat(messi_index* idx, const float* query_dev, int32_t reps, double* ms_out,
                                      int64_t* coarse_out);
 
-/* ---- inspection entry points (tests / bench; same kernels as the query path) ---------- */
+/* ---- inspection entry points (tests) -------------------------------------------------
+ * Each runs the QUERY PATH'S OWN KERNELS with their pruning thresholds at +inf (nothing is
+ * pruned, nothing abandoned) and scatters what they produce back to row / id order; only the
+ * ED refine's inner passes, which live inside the fused kernel, are reached through a small
+ * kernel calling the same device functions.  All outputs are device buffers; entries a call
+ * did not produce are left NaN.  Synchronous. */
 
 /* The 255 fp32 N(0,1) breakpoints the device derived (O3 reading), into host memory. */
 messi_status messi_debug_breakpoints(int32_t device, float* beta32_host);
@@ -179,24 +203,49 @@ messi_status messi_debug_quantised(messi_index* idx, uint8_t* q8_dev, float* met
 /* Sorted approximate-search keys and the row permutation (device pointers owned by idx). */
 messi_status messi_debug_order(messi_index* idx, const uint64_t** skey_dev, const uint32_t** perm_dev);
 
-/* Lower bound of every row against one query (device pointer): reach < 0 -> ED mindist
- * (Property 1); reach >= 0 -> DTW envelope-PAA bound.  Squared,
- * fp32 rounded down, written to lb_dev[count] (the scan kernel's arithmetic). */
+/* 8-bit iSAX lower bound of every row against one query (device pointer), lb_dev[count]:
+ * the scan kernel k_scan (coarse pass, then fine_lb -- the device function the fused ED
+ * kernel's fine pass calls) over every tile, with the scan table of the query path: ED
+ * (reach < 0) -> mindist (Property 1) from k_prologue_batch's table; DTW
+ * (reach >= 0) -> the envelope-PAA bound from k_seed_dtw's.  Squared, fp32, table
+ * entries rounded down and summed rounding down. */
 messi_status messi_debug_lower_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
 
 /* Coarse (cardinality-16, the top 4 bits of every symbol) bound of every row against one
- * query with the scan kernel's own arithmetic: squared, fp32, rounded down, <= the 8-bit bound
- * of messi_debug_lower_bounds (the coarse boxes contain the fine ones).  lb_dev[count]. */
+ * query with the scan kernel's own arithmetic (coarse_acc, called by scan_tile_coarse):
+ * squared, fp32, rounded down, <= the 8-bit bound (the coarse boxes contain the fine ones). */
 messi_status messi_debug_coarse_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
 
 /* Box bound of every tile (512 consecutive series in approximate-search order; members are
- * rows perm[512*t .. 512*t+511]), written to lb_dev[ntiles] (fp32 of the fp64 bound). */
+ * rows perm[512*t .. 512*t+511]), lb_dev[ntiles]: ED (reach < 0) -> the batch filter kernel
+ * k_filter_batch (fp32 box_lb over the zero runs of the filter table, rounded down); DTW ->
+ * the per-query filter k_tile_filter (fp64 bound, rounded to fp32). */
 messi_status messi_debug_tile_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
 
-/* For `k` local row ids: fp32 squared distance as computed by the refine kernels (no
- * abandoning), the exact fp64 squared distance of the re-rank kernel, and (reach >= 0)
- * the fp32 raw LB_Keogh of the filter kernel.  reach < 0 -> ED, else DTW with that reach.
- * Any output pointer may be NULL. */
+/* ED box bound of every super-tile (16 consecutive tiles, the union box) with the filter's
+ * box_lb, lb_dev[ceil(ntiles / 16)]. */
+messi_status messi_debug_super_bounds(messi_index* idx, const float* query_dev, float* lb_dev);
+
+/* ED refine of `k` local row ids (device u32, distinct): out4_dev[k][4] fp32 = (dh2, L, d32, 0)
+ * -- dh2 the fp32 squared distance to the quantised row and L = sqrt_rd(dh2)(1 - delta) - e
+ * its lower bound of ||q - x|| (q8_bound_pass), d32 the fp32 squared ED of the exact pass
+ * (ed2_group) -- and d64_dev[k] the fp64 canonical re-rank (ed2_exact_g). */
+messi_status messi_debug_ed_refine(messi_index* idx, const float* query_dev, const uint32_t* ids_dev, int32_t k,
+                                   float* out4_dev, double* d64_dev);
+
+/* DTW filter + refine of `k` local row ids (device u32, distinct) with reach `reach`: the ids
+ * are handed to the query path's LB_Keogh filter kernel (threshold +inf) and refine kernel
+ * (frozen: threshold +inf, no BSF update, no abandon).  lbk_dev[k] (nullable) = the filter's
+ * LB_Keogh -- of the QUANTISED row x^ = s c at reaches served by the strip refine
+ * (*quantised = 1), of the raw row otherwise (*quantised = 0); d32_dev[k] (nullable) = the
+ * refine kernel's fp32 DTW^2.  quantised may be NULL. */
+messi_status messi_debug_dtw_stages(messi_index* idx, const float* query_dev, int32_t reach, const uint32_t* ids_dev,
+                                    int32_t k, float* lbk_dev, float* d32_dev, int32_t* quantised);
+
+/* For `k` local row ids: d32 = the refine's fp32 squared distance (ED: ed2_group; DTW: the
+ * refine kernel via messi_debug_dtw_stages), d64 = the exact fp64 re-rank (ED: ed2_exact_g;
+ * DTW: the resolve kernel's dtw_warp_any<double>), lbk (DTW) = the filter kernel's LB_Keogh as
+ * in messi_debug_dtw_stages.  reach < 0 -> ED.  Any output pointer may be NULL. */
 messi_status messi_debug_distances(messi_index* idx, const float* query_dev, int32_t reach, const uint32_t* ids_dev,
                                    int32_t k, float* d32_dev, double* d64_dev, float* lbk_dev);
 

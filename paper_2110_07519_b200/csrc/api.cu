@@ -38,10 +38,11 @@ using namespace messi;
 struct Slot {
     QState* st = nullptr;
     float *lut = nullptr, *tab = nullptr, *U = nullptr, *L = nullptr;  // tab: 64 KB scan table
-    uint2* cand = nullptr;    // scan survivors (sorted position, 8-bit LB)
+    uint2* cand = nullptr;    // scan survivors (sorted position, 8-bit LB)                      [lazy]
     uint4* list2 = nullptr;   // DTW: LB_Keogh survivors (id, LBK, LBK of the first window, 0)  [lazy]
     unsigned* tlist = nullptr;  // tiles surviving the box filter
-    NearEntry* near = nullptr;
+    NearEntry* near = nullptr;  // near-best (id, d32) of the DTW refine                          [lazy]
+    double* rbuf = nullptr;     // DTW resolve: global wavefront scratch for long series         [lazy]
     cudaEvent_t ev_seed = nullptr, ev_scan = nullptr, ev_lbk = nullptr, ev_refined = nullptr, ev_done = nullptr;
 };
 
@@ -89,6 +90,15 @@ struct messi_index {
     int npeers = 0;
     unsigned epoch = 0;
     int fused_grid = 0;
+    unsigned link_gen = 0;  // links made so far (the high byte of every epoch: see launch_ed_group)
+    // inspection scratch (messi_debug_*, allocated on first use): inverse permutation, row ->
+    // index map of the ids being inspected, tile iota, per-id outputs
+    unsigned* dbg_inv = nullptr;
+    int* dbg_map = nullptr;
+    unsigned* dbg_iota = nullptr;
+    float4* dbg_out4 = nullptr;
+    size_t dbg_out4_cap = 0;
+    double* dbg_gbuf = nullptr;
     // per-query scratch
     Slot slot[MESSI_DTW_SLOTS];
     unsigned long long qcount = 0;
@@ -97,8 +107,10 @@ struct messi_index {
     messi_result* resk = nullptr;    // k-NN single-query results (device)
     messi_stats* stats1 = nullptr;
     long long launches = 0;
+    float build_ms[4] = {0, 0, 0, 0};  // build phases (messi_build_times)
     // optional per-kernel event timing
     bool prof = false;
+    bool serial = false;  // every per-query stage on the caller's stream (profiling passes)
     struct Ev { int kind; cudaEvent_t a, b; };
     std::vector<Ev> evs;
     std::vector<cudaEvent_t> pool;
@@ -257,10 +269,13 @@ static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R,
 static size_t scan_smem() { return kScanLutBytes; }
 static size_t lbk_smem(int n) { return 2 * (size_t)((n + 3) & ~3) * sizeof(float); }
 
-static messi_status setup_kernels()
+// Function attributes (the shared-memory opt-ins) belong to the current device's context:
+// set them once per device (bit `device` of `done`).
+static messi_status setup_kernels(int device)
 {
-    static bool done = false;
-    if (done) return MESSI_OK;
+    static unsigned long long done = 0;  // guarded by the caller's single-threaded use per device
+    const unsigned long long bit = 1ull << (device & 63);
+    if (done & bit) return MESSI_OK;
     const int big = 200 * 1024;
     CK(cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
     CK(cudaFuncSetAttribute(k_debug_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
@@ -271,6 +286,8 @@ static messi_status setup_kernels()
     CK(cudaFuncSetAttribute(k_filter_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, kFilterQ * kLutF * 4));
     CK(cudaFuncSetAttribute(k_lbk_filter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_lbk_filter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_lbk_filter_q8, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_debug_dtw64, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_refine_dtw_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_resolve_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -280,11 +297,7 @@ static messi_status setup_kernels()
 #define SET_ATTR_R(R) CK(cudaFuncSetAttribute(k_refine_dtw<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
     MESSI_DTW_REACHES(SET_ATTR_R)
 #undef SET_ATTR_R
-    CK(cudaFuncSetAttribute(k_debug_dist<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-#define SET_ATTR(R) CK(cudaFuncSetAttribute(k_debug_dist<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    MESSI_DTW_REACHES(SET_ATTR)
-#undef SET_ATTR
-    done = true;
+    done |= bit;
     return MESSI_OK;
 }
 
@@ -318,7 +331,7 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     CK(cudaPointerGetAttributes(&pa, rows_dev));
     if (pa.type != cudaMemoryTypeDevice && pa.type != cudaMemoryTypeManaged)
         return fail(MESSI_EINVAL, "rows_dev is not a device pointer");
-    TRY(setup_kernels());
+    TRY(setup_kernels(cfg->device));
 
     messi_index* idx = new (std::nothrow) messi_index();
     if (!idx) return fail(MESSI_ENOMEM, "host allocation failed");
@@ -356,9 +369,7 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     if ((s = dalloc(&idx->beta32, 256)) || (s = dalloc(&idx->lo_w, 256)) || (s = dalloc(&idx->hi_w, 256))) return bail(s);
     for (Slot& sl : idx->slot) {
         if ((s = dalloc(&sl.st, 1)) || (s = dalloc(&sl.lut, MESSI_W * MESSI_CARD)) || (s = dalloc(&sl.tab, kScanTab)) ||
-            (s = dalloc(&sl.U, n)) ||
-            (s = dalloc(&sl.L, n)) || (s = dalloc(&sl.cand, (size_t)N)) || (s = dalloc(&sl.near, (size_t)N)) ||
-            (s = dalloc(&sl.tlist, (size_t)idx->ntiles)))
+            (s = dalloc(&sl.U, n)) || (s = dalloc(&sl.L, n)) || (s = dalloc(&sl.tlist, (size_t)idx->ntiles)))
             return bail(s);
         if (cudaEventCreateWithFlags(&sl.ev_seed, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&sl.ev_scan, cudaEventDisableTiming) != cudaSuccess ||
@@ -391,8 +402,15 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
         cudaFree(sym_tmp);
         cudaFree(temp);
     };
+    cudaEvent_t bev[5] = {};
+    for (auto& e : bev)
+        if (cudaEventCreate(&e) != cudaSuccess) return bail(fail(MESSI_ECUDA, "event creation failed"));
+    auto free_bev = [&]() {
+        for (auto& e : bev) cudaEventDestroy(e);
+    };
     do {
         if ((s = dalloc(&keys_in, (size_t)N)) || (s = dalloc(&ids_in, (size_t)N)) || (s = dalloc(&sym_tmp, npadrows))) break;
+        cudaEventRecord(bev[0], st);
         k_breakpoints<<<1, 256, 0, st>>>(idx->beta32, idx->lo_w, idx->hi_w);
         ++idx->launches;
         if (cudaGetLastError() != cudaSuccess) { s = fail(MESSI_ECUDA, "k_breakpoints launch"); break; }
@@ -406,8 +424,10 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "cub sort sizing: %s", cudaGetErrorString(e)); break; }
         e = cudaMalloc(&temp, temp_bytes ? temp_bytes : 1);
         if (e != cudaSuccess) { s = fail(MESSI_ENOMEM, "cub temp (%zu B): %s", temp_bytes, cudaGetErrorString(e)); break; }
+        cudaEventRecord(bev[1], st);
         e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, idx->skey, ids_in, idx->perm, (int)N, 0, 64, st);
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "cub sort: %s", cudaGetErrorString(e)); break; }
+        cudaEventRecord(bev[2], st);
         idx->launches += 4;
         k_layout<<<(unsigned)idx->ntiles, MESSI_TILE_ROWS, 0, st>>>(sym_tmp, idx->perm, N, idx->tiles, idx->sym8,
                                                                     idx->boxes);
@@ -420,9 +440,11 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
                                                                        idx->ntiles, idx->sboxes);
             ++idx->launches;
         }
+        cudaEventRecord(bev[3], st);
         k_quantise<<<(unsigned)(idx->sms * 8), 256, 0, st>>>(rows_dev, idx->perm, N, (int64_t)npadrows, n, idx->rows8,
                                                             idx->meta8);
         ++idx->launches;
+        cudaEventRecord(bev[4], st);
         e = cudaGetLastError();
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "k_quantise: %s", cudaGetErrorString(e)); break; }
         for (Slot& sl : idx->slot) {
@@ -431,9 +453,11 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
         }
         e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) { s = fail(MESSI_ECUDA, "build: %s", cudaGetErrorString(e)); break; }
+        for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&idx->build_ms[i], bev[i], bev[i + 1]);
         s = MESSI_OK;
     } while (0);
     cleanup();
+    free_bev();
     if (s != MESSI_OK) return bail(s);
     *out = idx;
     return MESSI_OK;
@@ -451,7 +475,8 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->stream) cudaStreamSynchronize(idx->stream);
     else cudaDeviceSynchronize();
     void* ptrs[] = {idx->tiles, idx->sym8, idx->boxes, idx->sboxes, idx->paa, idx->skey, idx->perm, idx->beta32, idx->lo_w,
-                    idx->hi_w,  idx->qbuf,  idx->res1, idx->resk, idx->stats1, idx->rows8, idx->meta8};
+                    idx->hi_w,  idx->qbuf,  idx->res1, idx->resk, idx->stats1, idx->rows8, idx->meta8,
+                    idx->dbg_inv, idx->dbg_map, idx->dbg_iota, idx->dbg_out4, idx->dbg_gbuf};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& row : idx->peer_ipc)
@@ -464,7 +489,7 @@ extern "C" void messi_free(messi_index* idx)
             if (p) cudaFree(p);
     }
     for (Slot& sl : idx->slot) {
-        void* sp[] = {sl.st, sl.lut, sl.tab, sl.U, sl.L, sl.cand, sl.list2, sl.near, sl.tlist};
+        void* sp[] = {sl.st, sl.lut, sl.tab, sl.U, sl.L, sl.cand, sl.list2, sl.near, sl.tlist, sl.rbuf};
         for (void* p : sp)
             if (p) cudaFree(p);
         cudaEvent_t es[] = {sl.ev_seed, sl.ev_scan, sl.ev_lbk, sl.ev_refined, sl.ev_done};
@@ -486,6 +511,13 @@ extern "C" void messi_free(messi_index* idx)
 }
 
 extern "C" const char* messi_last_error(void) { return g_err; }
+
+extern "C" messi_status messi_build_times(const messi_index* idx, double* ms_out)
+{
+    if (!idx || !ms_out) return fail(MESSI_EINVAL, "NULL argument");
+    for (int i = 0; i < 4; ++i) ms_out[i] = idx->build_ms[i];
+    return MESSI_OK;
+}
 
 extern "C" int64_t messi_launch_count(const messi_index* idx) { return idx ? idx->launches : 0; }
 
@@ -510,7 +542,8 @@ extern "C" messi_status messi_profile_enable(messi_index* idx, int32_t enable)
         idx->pool.push_back(e.b);
     }
     idx->evs.clear();
-    idx->prof = enable != 0;
+    idx->prof = (enable & 1) != 0;
+    idx->serial = (enable & 2) != 0;
     return MESSI_OK;
 }
 
@@ -560,34 +593,22 @@ static float dtw_front()
     return v;
 }
 
-// MESSI_SERIAL=1 (experiments): every stage on the caller's stream, no overlap.
-static bool serial_mode()
+// Serial mode (messi_profile_enable bit 1, or MESSI_SERIAL=1 for experiments): every stage of
+// the per-query path on the caller's stream, no overlap between stages or queries -- so the
+// per-kernel event times of a profiling pass add up to the step time.
+static bool serial_env()
 {
     static int v = -1;
     if (v < 0) v = getenv("MESSI_SERIAL") ? 1 : 0;
     return v == 1;
 }
+static bool serial_mode(const messi_index* idx) { return idx->serial || serial_env(); }
 
 // Orders the side and refine streams after everything already enqueued on the main stream
 // (query buffers written by the caller) -- once per API call, not between batch queries.
 static messi_status fork_streams(messi_index* idx)
 {
-    if (serial_mode()) {
-        if (idx->side != idx->stream) {
-            cudaStreamSynchronize(idx->side);
-            cudaStreamSynchronize(idx->rstr);
-            cudaStreamSynchronize(idx->dstr);
-            cudaStreamSynchronize(idx->dstr2);
-            cudaStreamSynchronize(idx->xstr);
-            cudaStreamDestroy(idx->side);
-            cudaStreamDestroy(idx->rstr);
-            cudaStreamDestroy(idx->dstr);
-            cudaStreamDestroy(idx->dstr2);
-            cudaStreamDestroy(idx->xstr);
-            idx->side = idx->rstr = idx->dstr = idx->dstr2 = idx->xstr = idx->stream;
-        }
-        return MESSI_OK;
-    }
+    if (serial_mode(idx)) return MESSI_OK;
     CK(cudaEventRecord(idx->ev_fork, idx->stream));
     CK(cudaStreamWaitEvent(idx->side, idx->ev_fork, 0));
     CK(cudaStreamWaitEvent(idx->rstr, idx->ev_fork, 0));
@@ -604,12 +625,27 @@ static messi_status join_streams(messi_index* idx)
     return MESSI_OK;
 }
 
+// Per-slot candidate buffers of the per-query (DTW) path, allocated on its first use: an
+// ED-only index never holds them (4 slots x 32 B per row: 12.8 GB at 100M rows).
 static messi_status ensure_dtw_buffers(messi_index* idx)
 {
     for (Slot& sl : idx->slot) {
+        if (!sl.cand) TRY(dalloc(&sl.cand, (size_t)idx->N));
+        if (!sl.near) TRY(dalloc(&sl.near, (size_t)idx->N));
         if (!sl.list2) TRY(dalloc(&sl.list2, (size_t)idx->N));
     }
     return MESSI_OK;
+}
+
+// Warps of the DTW resolve and whether its wavefront buffers go to global scratch (series
+// too long for shared memory at reaches above the register wavefront's).
+static const size_t kResolveSmemMax = 200 * 1024;
+static int resolve_warps(int n, int reach, bool* global_buf)
+{
+    *global_buf = resolve_warp_bytes(n, reach, false) > kResolveSmemMax;
+    const size_t per = resolve_warp_bytes(n, reach, *global_buf);
+    int w = (int)(kResolveSmemMax / per);
+    return w < 1 ? 1 : (w > 8 ? 8 : w);
 }
 
 static int filter_grid(const messi_index* idx)
@@ -628,7 +664,7 @@ static messi_status launch_tile_filter(messi_index* idx, Slot& sl, cudaStream_t 
     return MESSI_OK;
 }
 
-static messi_status launch_scan(messi_index* idx, Slot& sl)
+static messi_status launch_scan(messi_index* idx, Slot& sl, cudaStream_t next)
 {
     CK(cudaStreamWaitEvent(idx->stream, sl.ev_seed, 0));
     {
@@ -638,7 +674,7 @@ static messi_status launch_scan(messi_index* idx, Slot& sl)
         LAUNCHED(idx);
     }
     CK(cudaEventRecord(sl.ev_scan, idx->stream));
-    CK(cudaStreamWaitEvent(idx->rstr, sl.ev_scan, 0));
+    CK(cudaStreamWaitEvent(next, sl.ev_scan, 0));
     return MESSI_OK;
 }
 
@@ -673,8 +709,11 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
     PeerSet peers;
     peers.st = idx->d_peers + set * MESSI_MAX_PEERS;
     peers.n = idx->npeers;
-    peers.epoch = ++idx->epoch;
-    if (peers.epoch == 0) peers.epoch = ++idx->epoch;
+    // epoch = link generation (high byte) | launch groups since that link (low 24 bits): every
+    // shard of one link counts the same groups (they make the same batch calls after linking),
+    // and a value a peer wrote under an earlier link never carries a current epoch
+    idx->epoch = (idx->epoch + 1) & 0xffffffu;
+    peers.epoch = ((idx->link_gen & 0xffu) << 24) | idx->epoch;
     if (peers.n == 0) peers.epoch = 0;  // unlinked: kernels read the local BSF only
     const int n = idx->n;
     const size_t qsm = (size_t)((n + 3) & ~3) * sizeof(float);
@@ -745,57 +784,45 @@ static messi_status run_ed_batch(messi_index* idx, const float* queries_dev, int
     return MESSI_OK;
 }
 
-static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, messi_result* res, messi_stats* stats)
+// The refine kernel of reach R (see use_strip): the strip kernel, a register band, or the
+// warp wavefront.
+static bool dtw_uses_strip(int n, int reach)
 {
-    Slot& sl = idx->slot[idx->qcount++ % MESSI_DTW_SLOTS];
-    cudaStream_t rs = idx->rstr;
-    const int n = idx->n;
-    const int npad = (n + 3) & ~3;
-    const size_t qsm = (size_t)npad * sizeof(float);
-    int len = (int)(idx->window < idx->N ? idx->window : idx->N);
-    const size_t seed_warp = (size_t)(npad + 3 * n) * sizeof(float);
-    const int wf = warps_for(seed_warp, 8);
-    int seed_grid = (len + wf - 1) / wf;
-    if (seed_grid > idx->sms * 4) seed_grid = idx->sms * 4;
-    CK(cudaStreamWaitEvent(idx->side, sl.ev_done, 0));
-    {
-        ProfScope ps(idx, K_SEED, idx->side);
-        k_seed_dtw<<<seed_grid, 32 * wf, qsm + wf * seed_warp, idx->side>>>(
-            q_dev, n, reach, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32, idx->lo_w, idx->hi_w,
-            sl.lut, sl.tab, sl.U, sl.L, sl.st);
-        LAUNCHED(idx);
-        TRY(launch_tile_filter(idx, sl, idx->side));
-    }
-    CK(cudaEventRecord(sl.ev_seed, idx->side));
-    TRY(launch_scan(idx, sl));
     bool band = false;
 #define HAVE_R(R) band = band || reach == R;
     MESSI_DTW_REACHES(HAVE_R)
 #undef HAVE_R
-    const bool strip = use_strip(n, reach, band);
-    {
-        ProfScope ps(idx, K_LBK, rs);
-        if (strip)  // LB_Keogh of the quantised rows (the strip refine's tail bound uses the same terms)
-            k_lbk_filter_q8<<<idx->sms * 8, 128, 2 * (size_t)((n + 15) & ~15) * sizeof(float), rs>>>(
-                sl.cand, idx->perm, idx->rows8, idx->meta8, n, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N,
-                dtw_front());
-        else
-            k_lbk_filter<4><<<refine_grid(idx, 1024) * 2, 128, lbk_smem(n), rs>>>(
-                sl.cand, idx->perm, idx->rows, n, sl.U, sl.L, reach, sl.st, sl.list2, (unsigned)idx->N, dtw_front());
-        LAUNCHED(idx);
+    return use_strip(n, reach, band);
+}
+
+// DTW step 1: the LB_Keogh filter of the slot's candidates (list sl.cand, count and threshold
+// in sl.st) into list2 -- over the quantised rows at strip reaches (the strip refine's tail
+// bound uses the same terms), else over the raw rows.
+static messi_status launch_lbk_filter(messi_index* idx, Slot& sl, int reach, bool strip, cudaStream_t rs)
+{
+    const int n = idx->n;
+    if (strip)
+        k_lbk_filter_q8<<<idx->sms * 8, 128, 2 * (size_t)((n + 15) & ~15) * sizeof(float), rs>>>(
+            sl.cand, idx->perm, idx->rows8, idx->meta8, n, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N, dtw_front());
+    else
+        k_lbk_filter<4><<<refine_grid(idx, 1024) * 2, 128, lbk_smem(n), rs>>>(
+            sl.cand, idx->perm, idx->rows, n, sl.U, sl.L, reach, sl.st, sl.list2, (unsigned)idx->N, dtw_front());
+    LAUNCHED(idx);
+    return MESSI_OK;
+}
+
+// DTW step 2: banded fp32 DTW of the list2 entries (near-best entries to sl.near).
+static messi_status launch_dtw_refine(messi_index* idx, Slot& sl, int reach, bool strip, const float* q_dev,
+                                      cudaStream_t rs)
+{
+    const int n = idx->n;
+    const int npad = (n + 3) & ~3;
+    const size_t qsm = (size_t)npad * sizeof(float);
+    bool launched = false;
+    if (strip) {
+        TRY(launch_strip(idx, sl, n, reach, q_dev, rs));
+        launched = true;
     }
-    // the refine and the resolve run on their own stream: the LB_Keogh filter of the next
-    // query (bandwidth-bound) overlaps this query's band DP (latency / ALU-bound)
-    CK(cudaEventRecord(sl.ev_lbk, rs));
-    rs = (idx->qcount & 1) ? idx->dstr : idx->dstr2;  // qcount was advanced for this query
-    CK(cudaStreamWaitEvent(rs, sl.ev_lbk, 0));
-    {
-        ProfScope ps(idx, K_REFINE, rs);
-        bool launched = false;
-        if (strip) {
-            TRY(launch_strip(idx, sl, n, reach, q_dev, rs));
-            launched = true;
-        }
 #define LAUNCH_R(R)                                                                                           \
     if (!launched && reach == R) {                                                                            \
         int occ = 0;                                                                                          \
@@ -805,25 +832,71 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
                                                                             sl.near);                         \
         launched = true;                                                                                      \
     }
-        MESSI_DTW_REACHES(LAUNCH_R)
+    MESSI_DTW_REACHES(LAUNCH_R)
 #undef LAUNCH_R
-        if (!launched) {
-            const int wr = warps_for((size_t)4 * npad * sizeof(float), 8);
-            k_refine_dtw_warp<<<idx->sms * 4, 32 * wr, qsm + (size_t)wr * 4 * npad * sizeof(float), rs>>>(
-                idx->rows, n, reach, q_dev, sl.list2, (unsigned)idx->N, sl.st, sl.near);
-        }
+    if (!launched) {
+        const int wr = warps_for((size_t)4 * npad * sizeof(float), 8);
+        k_refine_dtw_warp<<<idx->sms * 4, 32 * wr, qsm + (size_t)wr * 4 * npad * sizeof(float), rs>>>(
+            idx->rows, n, reach, q_dev, sl.list2, (unsigned)idx->N, sl.st, sl.near);
+    }
+    LAUNCHED(idx);
+    return MESSI_OK;
+}
+
+static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, messi_result* res, messi_stats* stats)
+{
+    Slot& sl = idx->slot[idx->qcount++ % MESSI_DTW_SLOTS];
+    const bool ser = serial_mode(idx);
+    cudaStream_t side = ser ? idx->stream : idx->side;
+    cudaStream_t rs = ser ? idx->stream : idx->rstr;
+    const int n = idx->n;
+    const int npad = (n + 3) & ~3;
+    const size_t qsm = (size_t)npad * sizeof(float);
+    int len = (int)(idx->window < idx->N ? idx->window : idx->N);
+    const size_t seed_warp = (size_t)(npad + 3 * n) * sizeof(float);
+    const int wf = warps_for(seed_warp, 8);
+    int seed_grid = (len + wf - 1) / wf;
+    if (seed_grid > idx->sms * 4) seed_grid = idx->sms * 4;
+    CK(cudaStreamWaitEvent(side, sl.ev_done, 0));
+    // arm the slot for this query (whatever the previous query on it did, e.g. a launch that
+    // failed part-way): BSF +inf, every counter 0
+    k_arm<<<1, 1, 0, side>>>(sl.st);
+    LAUNCHED(idx);
+    {
+        ProfScope ps(idx, K_SEED, side);
+        k_seed_dtw<<<seed_grid, 32 * wf, qsm + wf * seed_warp, side>>>(
+            q_dev, n, reach, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32, idx->lo_w, idx->hi_w,
+            sl.lut, sl.tab, sl.U, sl.L, sl.st);
         LAUNCHED(idx);
+        TRY(launch_tile_filter(idx, sl, side));
+    }
+    CK(cudaEventRecord(sl.ev_seed, side));
+    TRY(launch_scan(idx, sl, rs));
+    const bool strip = dtw_uses_strip(n, reach);
+    {
+        ProfScope ps(idx, K_LBK, rs);
+        TRY(launch_lbk_filter(idx, sl, reach, strip, rs));
+    }
+    // the refine and the resolve run on their own stream: the LB_Keogh filter of the next
+    // query (bandwidth-bound) overlaps this query's band DP (latency / ALU-bound)
+    CK(cudaEventRecord(sl.ev_lbk, rs));
+    if (!ser) rs = (idx->qcount & 1) ? idx->dstr : idx->dstr2;  // qcount was advanced for this query
+    CK(cudaStreamWaitEvent(rs, sl.ev_lbk, 0));
+    {
+        ProfScope ps(idx, K_REFINE, rs);
+        TRY(launch_dtw_refine(idx, sl, reach, strip, q_dev, rs));
     }
     // the exact resolve of this query overlaps the next query's refine (another slot)
     CK(cudaEventRecord(sl.ev_refined, rs));
-    rs = idx->xstr;
+    if (!ser) rs = idx->xstr;
     CK(cudaStreamWaitEvent(rs, sl.ev_refined, 0));
     {
-        const size_t rw = (size_t)(3 * n + npad) * sizeof(double);
-        const int wr = warps_for(rw, 8);
+        bool gb = false;
+        const int wr = resolve_warps(n, reach, &gb);
+        if (gb && !sl.rbuf) TRY(dalloc(&sl.rbuf, (size_t)8 * 3 * n));
         ProfScope ps(idx, K_RESOLVE, rs);
-        k_resolve_dtw<<<1, 32 * wr, wr * rw, rs>>>(idx->rows, n, reach, q_dev, sl.near, sl.st, idx->N, idx->row_begin,
-                                                   res, stats);
+        k_resolve_dtw<<<1, 32 * wr, wr * resolve_warp_bytes(n, reach, gb), rs>>>(
+            idx->rows, n, reach, q_dev, sl.near, sl.st, idx->N, idx->row_begin, res, stats, gb ? sl.rbuf : nullptr);
         LAUNCHED(idx);
     }
     CK(cudaEventRecord(sl.ev_done, rs));
@@ -1005,6 +1078,8 @@ extern "C" messi_status messi_link_peers_ipc(messi_index* idx, const void* handl
             idx->peer_st[set][i] = static_cast<QState*>(p);
         }
     idx->npeers = npeers;
+    idx->link_gen = (idx->link_gen + 1) % 255 + 1;  // never 0: epoch 0 means unlinked
+    idx->epoch = 0;
     return upload_peers(idx);
 }
 
@@ -1030,6 +1105,8 @@ extern "C" messi_status messi_link_peers_local(messi_index* idx, messi_index* co
         for (int set = 0; set < 2; ++set) idx->peer_st[set][i] = peers[i]->bset[set].bst;
     }
     idx->npeers = npeers;
+    idx->link_gen = (idx->link_gen + 1) % 255 + 1;
+    idx->epoch = 0;
     return upload_peers(idx);
 }
 
@@ -1087,39 +1164,293 @@ extern "C" messi_status messi_debug_order(messi_index* idx, const uint64_t** ske
     return MESSI_OK;
 }
 
-// Prologue only (tables, envelope) for `reach` into slot 0, which is left armed.
+// ------------------------------------------------------------------ inspection helpers
+// The step-level inspection calls run the QUERY PATH'S OWN KERNELS with their pruning
+// thresholds at +inf, so that every row / tile comes out of them, and scatter the outputs back
+// to row (or id) order: k_scan for the 8-bit bound, k_filter_batch for the tile boxes,
+// k_lbk_filter_q8 / k_lbk_filter and the strip / band / warp DTW refine (frozen: no BSF update,
+// no abandon) for LB_Keogh and the fp32 DTW.  Only the ED refine's inner passes, which sit
+// inside the fused kernel, are reached through a small kernel that calls the same device
+// functions (q8_bound_pass, ed2_group, ed2_exact_g).
+__global__ void k_dbg_invert(const unsigned* __restrict__ perm, long long N, unsigned* __restrict__ inv)
+{
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < N) inv[perm[p]] = (unsigned)p;
+}
+__global__ void k_dbg_iota(unsigned* a, long long n)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = (unsigned)i;
+}
+// arm, then the inspection setup: tile list length, candidate count, filter threshold +inf
+__global__ void k_dbg_state(QState* st, unsigned tiles, unsigned cands, unsigned frozen)
+{
+    arm_state(st);
+    st->tile_count = tiles;
+    st->cand_count = cands;
+    st->lbk_thr_bits = 0x7f800000u;
+    st->frozen = frozen;
+}
+__global__ void k_dbg_map(const unsigned* __restrict__ ids, int k, int* map, const unsigned* __restrict__ inv,
+                          uint2* __restrict__ cand, int set)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= k) return;
+    map[ids[t]] = set ? t : -1;
+    if (cand) cand[t] = make_uint2(inv[ids[t]], 0u);  // (sorted position, 8-bit bound 0)
+}
+__global__ void k_dbg_scatter_cand(const uint2* __restrict__ cand, const QState* st, const unsigned* __restrict__ perm,
+                                   float* __restrict__ out)
+{
+    const unsigned total = st->cand_count;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x)
+        out[perm[cand[i].x]] = __uint_as_float(cand[i].y);
+}
+__global__ void k_dbg_scatter_tiles(const uint2* __restrict__ tl, const QState* st, float* __restrict__ out)
+{
+    const unsigned total = st->tile_count;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x)
+        out[tl[i].x] = __uint_as_float(tl[i].y);
+}
+__global__ void k_dbg_scatter_dtw(const uint4* __restrict__ list2, const NearEntry* __restrict__ near, const QState* st,
+                                  const int* __restrict__ map, float* __restrict__ lbk, float* __restrict__ d32)
+{
+    const unsigned nl = st->list2_count, nn = st->near_count;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < max(nl, nn); i += gridDim.x * blockDim.x) {
+        if (lbk && i < nl) lbk[map[list2[i].x]] = __uint_as_float(list2[i].y);
+        if (d32 && i < nn) d32[map[near[i].id]] = near[i].d32;
+    }
+}
+__global__ void k_dbg_col(const float4* __restrict__ v, int k, int c, float* __restrict__ out)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < k) out[t] = c == 0 ? v[t].x : (c == 1 ? v[t].y : v[t].z);
+}
+// Box bound of every super-tile (16 consecutive tiles) with the filter's own code (box_lb,
+// same lane mapping: lane = super-tile mod 32), from query 0's filter table of a batch set.
+__global__ void __launch_bounds__(256) k_dbg_superbox(const uint4* __restrict__ sboxes, long long nsuper,
+                                                      const float* __restrict__ lutf, const QState* st,
+                                                      float* __restrict__ out)
+{
+    extern __shared__ __align__(16) float lutf_s[];
+    __shared__ unsigned char zlo[16], zhi[16];
+    for (int i = threadIdx.x; i < kLutF / 4; i += blockDim.x)
+        reinterpret_cast<float4*>(lutf_s)[i] = reinterpret_cast<const float4*>(lutf)[i];
+    if (threadIdx.x < 16) { zlo[threadIdx.x] = st->zlo[threadIdx.x]; zhi[threadIdx.x] = st->zhi[threadIdx.x]; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, r = lane & 15, h = lane >> 4;
+    const long long S = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (S >= nsuper) return;
+    const uint4 mn = rotate_bytes(sboxes[2 * S], r), mx = rotate_bytes(sboxes[2 * S + 1], r);
+    out[S] = box_lb(mn, mx, lutf_s + 16 * h, zlo, zhi, r);
+}
+
+static unsigned grid_of(long long n, int threads)
+{
+    long long g = (n + threads - 1) / threads;
+    return (unsigned)(g < 1 ? 1 : (g > 65535LL * 32 ? 65535LL * 32 : g));
+}
+
+static messi_status ensure_debug_buffers(messi_index* idx)
+{
+    if (idx->dbg_inv) return MESSI_OK;
+    TRY(dalloc(&idx->dbg_inv, (size_t)idx->N));
+    TRY(dalloc(&idx->dbg_map, (size_t)idx->N));
+    TRY(dalloc(&idx->dbg_iota, (size_t)idx->ntiles));
+    CK(cudaMemsetAsync(idx->dbg_map, 0xff, sizeof(int) * (size_t)idx->N, idx->stream));  // -1: not inspected
+    k_dbg_invert<<<grid_of(idx->N, 256), 256, 0, idx->stream>>>(idx->perm, idx->N, idx->dbg_inv);
+    LAUNCHED(idx);
+    k_dbg_iota<<<grid_of(idx->ntiles, 256), 256, 0, idx->stream>>>(idx->dbg_iota, idx->ntiles);
+    LAUNCHED(idx);
+    return MESSI_OK;
+}
+
+// DTW prologue only (envelope U/L, tables) for `reach` into slot 0 (k_seed_dtw over a
+// one-row window), then re-armed.
 static messi_status debug_prologue(messi_index* idx, const float* query_dev, int reach)
 {
     cudaStream_t st = idx->stream;
     Slot& sl = idx->slot[0];
     const int n = idx->n;
     const size_t qsm = (size_t)((n + 3) & ~3) * sizeof(float);
-    if (reach < 0) {
-        k_seed_ed<<<1, 256, qsm, st>>>(query_dev, n, idx->rows, idx->skey, idx->perm, idx->N, 1, idx->beta32, idx->lo_w,
-                                       idx->hi_w, sl.lut, sl.tab, sl.st);
-    } else {
-        k_seed_dtw<<<1, 32, 2 * qsm + 3 * (size_t)n * sizeof(float), st>>>(query_dev, n, reach, idx->rows, idx->skey,
-                                                                          idx->perm, idx->N, 1, idx->beta32, idx->lo_w,
-                                                                          idx->hi_w, sl.lut, sl.tab, sl.U, sl.L, sl.st);
-    }
+    k_seed_dtw<<<1, 32, 2 * qsm + 3 * (size_t)n * sizeof(float), st>>>(query_dev, n, reach < 0 ? 0 : reach, idx->rows,
+                                                                      idx->skey, idx->perm, idx->N, 1, idx->beta32,
+                                                                      idx->lo_w, idx->hi_w, sl.lut, sl.tab, sl.U, sl.L,
+                                                                      sl.st);
     LAUNCHED(idx);
     k_arm<<<1, 1, 0, st>>>(sl.st);
     LAUNCHED(idx);
     return MESSI_OK;
 }
 
-extern "C" messi_status messi_debug_lower_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev)
+// ED prologue only: k_prologue_batch for one query into batch set 0 (the ED batch path's
+// tables: expanded scan table lutx, filter table lutf, zero runs, query PAA).
+static messi_status debug_prologue_ed(messi_index* idx, const float* query_dev)
+{
+    TRY(ensure_batch_buffers(idx));
+    const auto& bs = idx->bset[0];
+    const size_t qsm = (size_t)((idx->n + 3) & ~3) * sizeof(float);
+    k_prologue_batch<<<1, 256, qsm, idx->stream>>>(query_dev, idx->n, idx->beta32, idx->lo_w, idx->hi_w, idx->skey,
+                                                   idx->N, idx->window, bs.lutc, bs.lutx, bs.lutf, bs.bst, nullptr);
+    LAUNCHED(idx);
+    return MESSI_OK;
+}
+
+static messi_status debug_begin(messi_index* idx, const float* query_dev, int reach)
 {
     g_err[0] = 0;
-    if (!idx || !query_dev || !lb_dev) return fail(MESSI_EINVAL, "NULL argument");
+    if (!idx || !query_dev) return fail(MESSI_EINVAL, "NULL argument");
     if (reach > idx->n) return fail(MESSI_EINVAL, "reach %d > n", reach);
     CK(cudaSetDevice(idx->device));
     TRY(sync_all(idx));
-    TRY(debug_prologue(idx, query_dev, reach));
+    TRY(ensure_dtw_buffers(idx));
+    TRY(ensure_debug_buffers(idx));
+    return MESSI_OK;
+}
+
+// The scan table and state of `reach`'s query path: ED -> batch set 0 (k_prologue_batch),
+// DTW -> slot 0 (k_seed_dtw's prologue).
+static messi_status debug_tables(messi_index* idx, const float* query_dev, int reach, const float** tab, QState** st)
+{
+    if (reach < 0) {
+        TRY(debug_prologue_ed(idx, query_dev));
+        *tab = idx->bset[0].lutx;
+        *st = idx->bset[0].bst;
+    } else {
+        TRY(debug_prologue(idx, query_dev, reach));
+        *tab = idx->slot[0].tab;
+        *st = idx->slot[0].st;
+    }
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_debug_lower_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev)
+{
+    if (!lb_dev) return fail(MESSI_EINVAL, "NULL argument");
+    TRY(debug_begin(idx, query_dev, reach));
+    const float* tab = nullptr;
+    QState* st = nullptr;
+    TRY(debug_tables(idx, query_dev, reach, &tab, &st));
     Slot& sl = idx->slot[0];
-    k_debug_lb8<<<(unsigned)((idx->N + 255) / 256), 256, 0, idx->stream>>>(idx->sym8, idx->perm, idx->N, sl.lut, lb_dev);
+    cudaStream_t s = idx->stream;
+    k_dbg_state<<<1, 1, 0, s>>>(st, (unsigned)idx->ntiles, 0u, 0u);  // every tile listed, BSF +inf
+    LAUNCHED(idx);
+    CK(cudaMemsetAsync(lb_dev, 0xff, sizeof(float) * (size_t)idx->N, s));  // NaN: not written
+    k_scan<<<scan_grid(idx), 32 * kScanWarps, scan_smem(), s>>>(idx->tiles, idx->sym8, idx->N, tab, st, sl.cand,
+                                                                idx->dbg_iota);
+    LAUNCHED(idx);
+    k_dbg_scatter_cand<<<idx->sms * 8, 256, 0, s>>>(sl.cand, st, idx->perm, lb_dev);
+    LAUNCHED(idx);
+    k_arm<<<1, 1, 0, s>>>(st);
+    LAUNCHED(idx);
+    CK(cudaStreamSynchronize(s));
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_debug_coarse_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev)
+{
+    if (!lb_dev) return fail(MESSI_EINVAL, "NULL argument");
+    TRY(debug_begin(idx, query_dev, reach));
+    const float* tab = nullptr;
+    QState* st = nullptr;
+    TRY(debug_tables(idx, query_dev, reach, &tab, &st));
+    k_debug_coarse<<<scan_grid(idx), 32 * kScanWarps, scan_smem(), idx->stream>>>(idx->tiles, idx->ntiles, idx->N, tab,
+                                                                                 idx->perm, lb_dev);
     LAUNCHED(idx);
     CK(cudaStreamSynchronize(idx->stream));
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_debug_tile_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev)
+{
+    if (!lb_dev) return fail(MESSI_EINVAL, "NULL argument");
+    TRY(debug_begin(idx, query_dev, reach));
+    cudaStream_t s = idx->stream;
+    if (reach < 0) {  // the ED batch path's filter (fp32 box bound, zero runs), threshold +inf
+        TRY(debug_prologue_ed(idx, query_dev));
+        const auto& bs = idx->bset[0];
+        const long long nsuper = (idx->ntiles + kSuperTiles - 1) / kSuperTiles;
+        CK(cudaMemsetAsync(lb_dev, 0xff, sizeof(float) * (size_t)idx->ntiles, s));
+        long long fx = (nsuper + 255) / 256;
+        if (fx > idx->sms * 8) fx = idx->sms * 8;
+        k_filter_batch<<<dim3((unsigned)fx, 1), 256, kFilterQ * kLutF * 4, s>>>(
+            reinterpret_cast<const uint4*>(idx->boxes), idx->sboxes, idx->ntiles, nsuper, bs.lutf, bs.bst, 1, bs.btlist,
+            0u);
+        LAUNCHED(idx);
+        k_dbg_scatter_tiles<<<idx->sms * 4, 256, 0, s>>>(bs.btlist, bs.bst, lb_dev);
+        LAUNCHED(idx);
+    } else {  // the DTW path's filter (fp64 box bound)
+        TRY(debug_prologue(idx, query_dev, reach));
+        Slot& sl = idx->slot[0];
+        k_tile_filter<<<filter_grid(idx), 256, 0, s>>>(idx->boxes, idx->ntiles, idx->n / MESSI_W, idx->lo_w, idx->hi_w,
+                                                      sl.st, nullptr, lb_dev);
+        LAUNCHED(idx);
+    }
+    CK(cudaStreamSynchronize(s));
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_debug_super_bounds(messi_index* idx, const float* query_dev, float* lb_dev)
+{
+    if (!lb_dev) return fail(MESSI_EINVAL, "NULL argument");
+    TRY(debug_begin(idx, query_dev, -1));
+    TRY(debug_prologue_ed(idx, query_dev));
+    const long long nsuper = (idx->ntiles + kSuperTiles - 1) / kSuperTiles;
+    k_dbg_superbox<<<grid_of(nsuper, 256), 256, kLutF * 4, idx->stream>>>(idx->sboxes, nsuper, idx->bset[0].lutf,
+                                                                          idx->bset[0].bst, lb_dev);
+    LAUNCHED(idx);
+    CK(cudaStreamSynchronize(idx->stream));
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_debug_ed_refine(messi_index* idx, const float* query_dev, const uint32_t* ids_dev,
+                                              int32_t k, float* out4_dev, double* d64_dev)
+{
+    if ((!ids_dev && k > 0) || k < 0 || !out4_dev || !d64_dev) return fail(MESSI_EINVAL, "bad argument");
+    TRY(debug_begin(idx, query_dev, -1));
+    if (k == 0) return MESSI_OK;
+    cudaStream_t s = idx->stream;
+    Slot& sl = idx->slot[0];
+    k_dbg_state<<<1, 1, 0, s>>>(sl.st, 0u, 0u, 0u);  // BSF +inf: nothing pruned
+    LAUNCHED(idx);
+    const int wpb = 8;
+    unsigned grid = (unsigned)((k + 32 * wpb - 1) / (32 * wpb));
+    if (grid > (unsigned)idx->sms * 8) grid = idx->sms * 8;
+    k_debug_ed_refine<<<grid, 32 * wpb, fused_qpad(idx->n) * sizeof(float), s>>>(
+        idx->rows, idx->n, query_dev, idx->rows8, idx->meta8, idx->q8_omd, idx->dbg_inv, sl.st, ids_dev, k,
+        reinterpret_cast<float4*>(out4_dev), d64_dev);
+    LAUNCHED(idx);
+    CK(cudaStreamSynchronize(s));
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_debug_dtw_stages(messi_index* idx, const float* query_dev, int32_t reach,
+                                               const uint32_t* ids_dev, int32_t k, float* lbk_dev, float* d32_dev,
+                                               int32_t* quantised)
+{
+    if ((!ids_dev && k > 0) || k < 0 || reach < 0) return fail(MESSI_EINVAL, "bad argument");
+    TRY(debug_begin(idx, query_dev, reach));
+    const bool strip = dtw_uses_strip(idx->n, reach);
+    if (quantised) *quantised = strip ? 1 : 0;
+    if (k == 0) return MESSI_OK;
+    cudaStream_t s = idx->stream;
+    Slot& sl = idx->slot[0];
+    TRY(debug_prologue(idx, query_dev, reach));
+    k_dbg_state<<<1, 1, 0, s>>>(sl.st, 0u, (unsigned)k, 1u);  // k candidates, threshold +inf, frozen
+    LAUNCHED(idx);
+    k_dbg_map<<<grid_of(k, 256), 256, 0, s>>>(ids_dev, k, idx->dbg_map, idx->dbg_inv, sl.cand, 1);
+    LAUNCHED(idx);
+    TRY(launch_lbk_filter(idx, sl, reach, strip, s));
+    TRY(launch_dtw_refine(idx, sl, reach, strip, query_dev, s));
+    if (lbk_dev) CK(cudaMemsetAsync(lbk_dev, 0xff, sizeof(float) * (size_t)k, s));
+    if (d32_dev) CK(cudaMemsetAsync(d32_dev, 0xff, sizeof(float) * (size_t)k, s));
+    k_dbg_scatter_dtw<<<grid_of(k, 256), 256, 0, s>>>(sl.list2, sl.near, sl.st, idx->dbg_map, lbk_dev, d32_dev);
+    LAUNCHED(idx);
+    k_dbg_map<<<grid_of(k, 256), 256, 0, s>>>(ids_dev, k, idx->dbg_map, idx->dbg_inv, nullptr, 0);
+    LAUNCHED(idx);
+    k_arm<<<1, 1, 0, s>>>(sl.st);
+    LAUNCHED(idx);
+    CK(cudaStreamSynchronize(s));
     return MESSI_OK;
 }
 
@@ -1127,36 +1458,44 @@ extern "C" messi_status messi_debug_distances(messi_index* idx, const float* que
                                               const uint32_t* ids_dev, int32_t k, float* d32_dev, double* d64_dev,
                                               float* lbk_dev)
 {
-    g_err[0] = 0;
-    if (!idx || !query_dev || (!ids_dev && k > 0) || k < 0) return fail(MESSI_EINVAL, "bad argument");
-    if (reach > idx->n) return fail(MESSI_EINVAL, "reach %d > n", reach);
-    CK(cudaSetDevice(idx->device));
-    TRY(sync_all(idx));
-    cudaStream_t st = idx->stream;
-    Slot& sl = idx->slot[0];
+    if ((!ids_dev && k > 0) || k < 0) return fail(MESSI_EINVAL, "bad argument");
+    TRY(debug_begin(idx, query_dev, reach));
+    if (k == 0) return MESSI_OK;
+    cudaStream_t s = idx->stream;
     const int n = idx->n;
-    const int npad = (n + 3) & ~3;
-    if (reach >= 0) TRY(debug_prologue(idx, query_dev, reach));  // envelope for LB_Keogh
-    const size_t per_warp = (size_t)(npad + 6 * n) * sizeof(float);
-    const int wr = warps_for(per_warp, 4);
-    const size_t smem = 3 * (size_t)npad * sizeof(float) + (size_t)wr * per_warp;
-    int grid = (k + wr - 1) / wr;
-    if (grid > idx->sms * 8) grid = idx->sms * 8;
-    if (grid < 1) grid = 1;
-    bool launched = false;
-#define LAUNCH_D(R)                                                                                          \
-    if (!launched && reach == R) {                                                                           \
-        k_debug_dist<R><<<grid, 32 * wr, smem, st>>>(idx->rows, n, reach, query_dev, sl.U, sl.L, ids_dev, k,   \
-                                                     d32_dev, d64_dev, lbk_dev);                             \
-        launched = true;                                                                                     \
+    if (reach < 0) {
+        if ((size_t)k > idx->dbg_out4_cap) {
+            cudaFree(idx->dbg_out4);
+            idx->dbg_out4 = nullptr;
+            idx->dbg_out4_cap = 0;
+            TRY(dalloc(&idx->dbg_out4, (size_t)k));
+            idx->dbg_out4_cap = (size_t)k;
+        }
+        double* d64 = d64_dev;
+        if (!d64) TRY(dalloc(&d64, (size_t)k));
+        messi_status st = messi_debug_ed_refine(idx, query_dev, ids_dev, k, reinterpret_cast<float*>(idx->dbg_out4), d64);
+        if (st == MESSI_OK && d32_dev) {
+            k_dbg_col<<<grid_of(k, 256), 256, 0, s>>>(idx->dbg_out4, k, 2, d32_dev);
+            ++idx->launches;
+            if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+                st = fail(MESSI_ECUDA, "k_dbg_col");
+        }
+        if (!d64_dev) cudaFree(d64);
+        return st;
     }
-    MESSI_DTW_REACHES(LAUNCH_D)
-#undef LAUNCH_D
-    if (!launched)
-        k_debug_dist<-1><<<grid, 32 * wr, smem, st>>>(idx->rows, n, reach, query_dev, sl.U, sl.L, ids_dev, k, d32_dev,
-                                                      d64_dev, lbk_dev);
-    LAUNCHED(idx);
-    CK(cudaStreamSynchronize(st));
+    if (d64_dev) {  // the resolve kernel's fp64 engine
+        bool gb = false;
+        const int wr = resolve_warps(n, reach, &gb);
+        if (gb && !idx->dbg_gbuf) TRY(dalloc(&idx->dbg_gbuf, (size_t)8 * 3 * MESSI_MAX_N));
+        unsigned grid = gb ? 1u : (unsigned)((k + wr - 1) / wr);
+        if (grid > (unsigned)idx->sms * 8) grid = idx->sms * 8;
+        k_debug_dtw64<<<grid, 32 * wr, wr * resolve_warp_bytes(n, reach, gb), s>>>(idx->rows, n, reach, query_dev,
+                                                                                 ids_dev, k, d64_dev,
+                                                                                 gb ? idx->dbg_gbuf : nullptr);
+        LAUNCHED(idx);
+    }
+    if (d32_dev || lbk_dev) TRY(messi_debug_dtw_stages(idx, query_dev, reach, ids_dev, k, lbk_dev, d32_dev, nullptr));
+    CK(cudaStreamSynchronize(s));
     return MESSI_OK;
 }
 
@@ -1172,6 +1511,7 @@ extern "C" messi_status messi_debug_scan_repeat(messi_index* idx, const float* q
     if (!idx || !query_dev || reps <= 0 || !ms_out) return fail(MESSI_EINVAL, "bad argument");
     CK(cudaSetDevice(idx->device));
     TRY(sync_all(idx));
+    TRY(ensure_dtw_buffers(idx));
     Slot& sl = idx->slot[0];
     cudaStream_t st = idx->stream;
     const int n = idx->n;
@@ -1215,34 +1555,3 @@ extern "C" messi_status messi_debug_scan_repeat(messi_index* idx, const float* q
     return MESSI_OK;
 }
 
-extern "C" messi_status messi_debug_coarse_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev)
-{
-    g_err[0] = 0;
-    if (!idx || !query_dev || !lb_dev) return fail(MESSI_EINVAL, "NULL argument");
-    if (reach > idx->n) return fail(MESSI_EINVAL, "reach %d > n", reach);
-    CK(cudaSetDevice(idx->device));
-    TRY(sync_all(idx));
-    TRY(debug_prologue(idx, query_dev, reach));
-    Slot& sl = idx->slot[0];
-    k_debug_coarse<<<scan_grid(idx), 32 * kScanWarps, scan_smem(), idx->stream>>>(idx->tiles, idx->ntiles, idx->N, sl.tab,
-                                                                                 idx->perm, lb_dev);
-    LAUNCHED(idx);
-    CK(cudaStreamSynchronize(idx->stream));
-    return MESSI_OK;
-}
-
-extern "C" messi_status messi_debug_tile_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev)
-{
-    g_err[0] = 0;
-    if (!idx || !query_dev || !lb_dev) return fail(MESSI_EINVAL, "NULL argument");
-    if (reach > idx->n) return fail(MESSI_EINVAL, "reach %d > n", reach);
-    CK(cudaSetDevice(idx->device));
-    TRY(sync_all(idx));
-    TRY(debug_prologue(idx, query_dev, reach));
-    Slot& sl = idx->slot[0];
-    k_tile_filter<<<filter_grid(idx), 256, 0, idx->stream>>>(idx->boxes, idx->ntiles, idx->n / MESSI_W, idx->lo_w,
-                                                            idx->hi_w, sl.st, nullptr, lb_dev);
-    LAUNCHED(idx);
-    CK(cudaStreamSynchronize(idx->stream));
-    return MESSI_OK;
-}

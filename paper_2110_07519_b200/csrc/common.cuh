@@ -48,6 +48,9 @@ struct QState {
     unsigned char zlo[16], zhi[16];  // batch ED: per segment, the symbols whose table entry is 0
     unsigned lbk_thr_bits;  // DTW: the scan's threshold (BSF0), used by the LB_Keogh filter
     unsigned list2_back;    // DTW: LB_Keogh survivors appended from the back of list2 (larger LBK)
+    unsigned frozen;        // inspection only (messi_debug_dtw_stages): the DTW refine kernels keep
+                            // their threshold at its start value and never lower the BSF, so every
+                            // candidate runs to completion (no abandon) and reports its fp32 DTW
 };
 
 struct NearEntry { unsigned id; float d32; };
@@ -97,6 +100,7 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->best_d = (double)INFINITY;
     st->best_id = -1;
     st->dtw_cells = 0;
+    st->frozen = 0;
 }
 
 // Paired fp32 arithmetic (Blackwell FADD2 / FFMA2: two lanes of fp32 per instruction on the

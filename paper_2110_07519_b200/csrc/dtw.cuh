@@ -1,6 +1,6 @@
 // dtw.cuh -- real-distance engines: fp32 ED (warp), fp32/fp64 banded DTW (warp
-// wavefront), fp32 banded DTW (one thread per candidate, band in registers), raw
-// LB_Keogh (warp), and the canonical fp64 ED used for the exact re-rank.
+// wavefront), fp32 banded DTW (one thread per candidate: band in registers, or strips of
+// candidate rows for any reach).
 #pragma once
 #include "common.cuh"
 
@@ -23,18 +23,6 @@ __device__ __forceinline__ float ed2_warp(const float* __restrict__ q_s, const f
         d = qv.w - cv.w; acc = fmaf(d, d, acc);
     }
     return warp_sum(acc);
-}
-
-// Canonical fp64 squared ED: d = sum_i ((double)q_i - (double)c_i)^2, sequential in i,
-// explicit round-to-nearest ops (no FMA contraction).  The exact re-rank of near-ties.
-__device__ __forceinline__ double ed2_exact(const float* __restrict__ q, const float* __restrict__ c, int n)
-{
-    double sum = 0.0;
-    for (int i = 0; i < n; ++i) {
-        double d = __dsub_rn((double)q[i], (double)c[i]);
-        sum = __dadd_rn(sum, __dmul_rn(d, d));
-    }
-    return sum;
 }
 
 template <typename T> __device__ __forceinline__ T inf_of();
@@ -150,26 +138,6 @@ __device__ __forceinline__ T dtw_warp_any(const float* __restrict__ q, const flo
                                           T* buf, int lane)
 {
     return r <= kShflMaxReach ? dtw_warp_shfl<T>(q, c, n, r, lane) : dtw_warp<T>(q, c, n, r, buf, lane);
-}
-
-// Raw LB_Keogh, squared, fp32, one warp: sum_i (c_i - U_i)^2 [c_i > U_i] +
-// (c_i - L_i)^2 [c_i < L_i].  Alg. 10 line LB_Keogh.
-__device__ __forceinline__ float lbk_warp(const float* __restrict__ U, const float* __restrict__ L,
-                                          const float* __restrict__ c, int n, int lane)
-{
-    float acc = 0.0f;
-    for (int j = lane * 4; j < n; j += 128) {
-        float4 cv = __ldg(reinterpret_cast<const float4*>(c + j));
-        float4 uv = *reinterpret_cast<const float4*>(U + j);
-        float4 lv = *reinterpret_cast<const float4*>(L + j);
-        float e[4] = {cv.x, cv.y, cv.z, cv.w}, u[4] = {uv.x, uv.y, uv.z, uv.w}, l[4] = {lv.x, lv.y, lv.z, lv.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            float d = e[k] > u[k] ? e[k] - u[k] : (e[k] < l[k] ? e[k] - l[k] : 0.0f);
-            acc = fmaf(d, d, acc);
-        }
-    }
-    return warp_sum(acc);
 }
 
 // Banded DTW in fp32, ONE THREAD per candidate, band of width W = 2R+1 held in registers.

@@ -450,6 +450,35 @@ __device__ void knn_insert_warp(QState* st, KnnState* kn, int k, float d32, doub
 // raw rows, four rows in flight per warp (Alg. 9 RealDist); a distance <= BSF*(1+eps)
 // lowers the BSF (atomicMin, Alg. 8's BSF update P:1178-1186) and is re-ranked exactly in
 // fp64 at once (reading R11/R12): the lexicographic min over the re-ranked rows is the answer.
+// fp32 squared ED of the warp's kRefineGroup rows id[g] (ok[g]: slot used), all rows in flight
+// at once: lane takes float4 chunks lane*4 + 128k of each row, then a butterfly sum (every lane
+// ends with the totals).  The query comes from q_p (element i at i + 4 (i >> 5)).
+__device__ __forceinline__ void ed2_group(const unsigned (&id)[kRefineGroup], const bool (&ok)[kRefineGroup],
+                                          const float* __restrict__ rows, int n, const float* __restrict__ q_p,
+                                          int lane, float (&acc)[kRefineGroup])
+{
+#pragma unroll
+    for (int g = 0; g < kRefineGroup; ++g) acc[g] = 0.0f;
+    for (int j = lane * 4; j < n; j += 128) {
+        const float4 qv = *reinterpret_cast<const float4*>(q_p + j + 4 * (j >> 5));
+        float4 cv[kRefineGroup];
+#pragma unroll
+        for (int g = 0; g < kRefineGroup; ++g)
+            cv[g] = ok[g] ? __ldg(reinterpret_cast<const float4*>(rows + (long long)id[g] * n + j))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int g = 0; g < kRefineGroup; ++g) {
+            float d;
+            d = qv.x - cv[g].x; acc[g] = fmaf(d, d, acc[g]);
+            d = qv.y - cv[g].y; acc[g] = fmaf(d, d, acc[g]);
+            d = qv.z - cv[g].z; acc[g] = fmaf(d, d, acc[g]);
+            d = qv.w - cv[g].w; acc[g] = fmaf(d, d, acc[g]);
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < kRefineGroup; ++g) acc[g] = warp_sum(acc[g]);
+}
+
 template <bool LINKED, bool KNN>
 __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __restrict__ perm,
                            const float* __restrict__ rows, int n, const float* __restrict__ q_p, QState* st,
@@ -467,26 +496,7 @@ __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __res
             id[g] = ok[g] ? perm[pos] : 0u;
         }
         float acc[kRefineGroup];
-#pragma unroll
-        for (int g = 0; g < kRefineGroup; ++g) acc[g] = 0.0f;
-        for (int j = lane * 4; j < n; j += 128) {
-            const float4 qv = *reinterpret_cast<const float4*>(q_p + j + 4 * (j >> 5));
-            float4 cv[kRefineGroup];
-#pragma unroll
-            for (int g = 0; g < kRefineGroup; ++g)
-                cv[g] = ok[g] ? __ldg(reinterpret_cast<const float4*>(rows + (long long)id[g] * n + j))
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int g = 0; g < kRefineGroup; ++g) {
-                float d;
-                d = qv.x - cv[g].x; acc[g] = fmaf(d, d, acc[g]);
-                d = qv.y - cv[g].y; acc[g] = fmaf(d, d, acc[g]);
-                d = qv.z - cv[g].z; acc[g] = fmaf(d, d, acc[g]);
-                d = qv.w - cv[g].w; acc[g] = fmaf(d, d, acc[g]);
-            }
-        }
-#pragma unroll
-        for (int g = 0; g < kRefineGroup; ++g) acc[g] = warp_sum(acc[g]);
+        ed2_group(id, ok, rows, n, q_p, lane, acc);
         if (KNN && k > kKnnLaneMax) {  // large k: the warp inserts each accepted row together
             // (the KNN = false instantiation keeps the runtime knn test below: measured
             // 2% faster C3 code than with the k-NN branches folded away)
@@ -770,6 +780,60 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
             if (wc.exact) atomicAdd(&st->exact, wc.exact);
         }
         __syncthreads();  // every warp is done with b's table before it is overwritten
+    }
+}
+
+// ------------------------------------------------------------------------ inspection
+// Inspection of the ED refine (messi_debug_ed_refine): for `k` local row ids, one warp per 32
+// of them, the query path's own device code -- q8_bound_pass (quantised-row fp32 distance dh2
+// and its lower bound L of ||q - x||), ed2_group (the exact pass's fp32 squared ED) and
+// ed2_exact_g (the fp64 re-rank) -- with the threshold at +inf (st armed), nothing pruned.
+// inv: sorted position of every row (the inverse of perm).  out4[t] = (dh2, L, d32, 0).
+__global__ void __launch_bounds__(256) k_debug_ed_refine(const float* __restrict__ rows, int n,
+                                                         const float* __restrict__ q_g,
+                                                         const unsigned char* __restrict__ rows8,
+                                                         const float2* __restrict__ meta8, float one_minus_delta,
+                                                         const unsigned* __restrict__ inv, QState* st,
+                                                         const unsigned* __restrict__ ids, int k,
+                                                         float4* __restrict__ out4, double* __restrict__ d64)
+{
+    extern __shared__ __align__(16) float q_p[];
+    __shared__ float2 dbg_s[8][32];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) q_p[i + 4 * (i >> 5)] = q_g[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    for (int t0 = (blockIdx.x * wpb + w) * 32; t0 < k; t0 += gridDim.x * wpb * 32) {
+        const bool v = t0 + lane < k;
+        const unsigned id = v ? ids[t0 + lane] : 0u;
+        const unsigned pos = v ? inv[id] : 0u;
+        const unsigned mask = __ballot_sync(0xffffffffu, v);
+        q8_bound_pass<false, true>(mask, pos, rows8, meta8, n, q_p, one_minus_delta, st, 0u, lane, dbg_s[w]);
+        __syncwarp();
+        float mine = 0.0f;
+        unsigned rest = mask;
+        while (rest) {
+            unsigned gid[kRefineGroup];
+            bool ok[kRefineGroup];
+            int src[kRefineGroup];
+#pragma unroll
+            for (int g = 0; g < kRefineGroup; ++g) {
+                ok[g] = rest != 0;
+                src[g] = ok[g] ? __ffs(rest) - 1 : 0;
+                rest &= rest - 1;
+                gid[g] = __shfl_sync(0xffffffffu, id, src[g]);
+            }
+            float acc[kRefineGroup];
+            ed2_group(gid, ok, rows, n, q_p, lane, acc);
+#pragma unroll
+            for (int g = 0; g < kRefineGroup; ++g)
+                if (ok[g] && lane == src[g]) mine = acc[g];
+        }
+        if (v) {
+            const float2 qd = dbg_s[w][lane];
+            out4[t0 + lane] = make_float4(qd.x, qd.y, mine, 0.0f);
+            d64[t0 + lane] = ed2_exact_g(q_p, rows + (long long)id * n, n);
+        }
+        __syncwarp();
     }
 }
 

@@ -12,6 +12,28 @@ __device__ __forceinline__ void append_near(QState* st, NearEntry* near, unsigne
     near[pos] = NearEntry{id, d};
 }
 
+// Valid band cells of the first J rows of an n x n DTW matrix with reach R (|i - j| <= R,
+// 0 <= i, j < n): sum_{j < J} (min(n - 1, j + R) - max(0, j - R) + 1); J = n gives
+// n(2R + 1) - R(R + 1) (SURVEY 8(d)'s cell count).  The refine kernels report the cells of
+// the rows they evaluated (an abandoned candidate counts the rows done).
+__device__ __forceinline__ unsigned long long band_cells(long long n, long long R, long long J)
+{
+    if (J <= 0) return 0ull;
+    if (J > n) J = n;
+    if (R > n - 1) R = n - 1;
+    const long long J1 = J < n - R ? J : n - R;  // rows whose band end j + R stays inside
+    const long long A = J1 * (J1 - 1) / 2 + J1 * (R + 1) + (J - J1) * n;
+    const long long K = J - R - 1 > 0 ? J - R - 1 : 0;  // rows whose band start j - R > 0
+    return (unsigned long long)(A - K * (K + 1) / 2);
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
+{
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
 // Rows in flight per warp in the fp32 distance loops (four 1 KB rows at n = 256).
 constexpr int kRefineGroup = 4;
 
@@ -26,10 +48,19 @@ constexpr int kRefineGroup = 4;
 // chunks gl, gl+8, ... of its rows; the query comes from q_p, a padded copy (element i at
 // i + 4 (i >> 5)).  Bytes convert exactly with the 2^23 trick:
 // float(0x4B000000 | b) = 2^23 + b.
-template <bool LINKED>
+// L = sqrt_rd(dh2) * (1 - delta) - e, rounded down: the quantised-row lower bound of ||q - x||.
+__device__ __forceinline__ float q8_lower(float dh2, float e, float one_minus_delta)
+{
+    return __fsub_rd(__fmul_rd(__fsqrt_rd(dh2), one_minus_delta), e);
+}
+
+// DBG (inspection, messi_debug_ed_refine): also writes dbg[src lane] = (dh2, L) of every
+// candidate -- the same instructions as the query path, plus two stores.
+template <bool LINKED, bool DBG = false>
 __device__ __forceinline__ unsigned q8_bound_pass(unsigned pass, unsigned my_pos, const unsigned char* __restrict__ rows8,
                                                   const float2* __restrict__ meta8, int n, const float* __restrict__ q_p,
-                                                  float one_minus_delta, QState* st, unsigned epoch, int lane)
+                                                  float one_minus_delta, QState* st, unsigned epoch, int lane,
+                                                  float2* dbg = nullptr)
 {
     const int g = lane >> 3, gl = lane & 7;
     unsigned keep = 0;
@@ -89,12 +120,13 @@ __device__ __forceinline__ unsigned q8_bound_pass(unsigned pass, unsigned my_pos
             acc_b += __shfl_xor_sync(0xffffffffu, acc_b, o);
         }
         const float thr = slack_up(ld_bsf_l<LINKED>(st, epoch));
-        auto survives = [&](float acc, float e) {
-            const float L = __fsub_rd(__fmul_rd(__fsqrt_rd(acc), one_minus_delta), e);
-            return !(L > 0.0f && __fmul_rd(L, L) > thr);
-        };
-        const bool ka = oa && survives(acc_a, ma.y);
-        const bool kb = ob && survives(acc_b, mb.y);
+        const float La = q8_lower(acc_a, ma.y, one_minus_delta), Lb = q8_lower(acc_b, mb.y, one_minus_delta);
+        const bool ka = oa && !(La > 0.0f && __fmul_rd(La, La) > thr);
+        const bool kb = ob && !(Lb > 0.0f && __fmul_rd(Lb, Lb) > thr);
+        if constexpr (DBG) {
+            if (gl == 0 && oa) dbg[sa] = make_float2(acc_a, La);
+            if (gl == 0 && ob) dbg[sb] = make_float2(acc_b, Lb);
+        }
         // lane gl == 0 of each group reports; collect the source-lane bits
         const unsigned ba = __ballot_sync(0xffffffffu, gl == 0 && ka);
         const unsigned bb = __ballot_sync(0xffffffffu, gl == 0 && kb);
@@ -393,9 +425,11 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
     if (nxt.x != 0xffffffffu) prefetch_row(nxt.x);
     DtwThread<R> dp;
     const float* c = rows;
-    unsigned id = 0, refined = 0, abandoned = 0, steps = 0, skipped = 0;
+    unsigned id = 0, refined = 0, abandoned = 0, skipped = 0;
+    unsigned long long cells = 0;
     float lbk_total = 0.0f;
     float thr = slack_up(ld_bsf(st));
+    const bool frozen = *(volatile const unsigned*)&st->frozen != 0u;  // inspection: no BSF updates
     bool running = false;
     for (;;) {
         // lanes without a candidate take their next entry (a candidate whose LB_Keogh
@@ -425,31 +459,34 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
         if (running) {
             const unsigned bsf_bits = *(volatile const unsigned*)&st->bsf_bits;  // consumed after the step
             const float rowmin = dp.step4(c, n, q_s, U, L);
-            ++steps;
             thr = fminf(thr, slack_up(__uint_as_float(bsf_bits)));
             const float tail = fmaxf(0.0f, lbk_total * 0.9990234375f - dp.seen_lo * 1.0009765625f);
             const float bound = (rowmin + tail) * 0.9990234375f;
             if (bound > thr) {
                 running = false;
                 ++abandoned;
+                cells += band_cells(n, R, dp.i);
             } else if (dp.i >= n) {
                 running = false;
+                cells += band_cells(n, R, n);
                 const float d = dp.result();
                 if (d <= thr) {
-                    bsf_update(st, d);
                     append_near(st, near, id, d);
-                    thr = fminf(thr, slack_up(d));
+                    if (!frozen) {
+                        bsf_update(st, d);
+                        thr = fminf(thr, slack_up(d));
+                    }
                 }
             }
         }
     }
     refined = __reduce_add_sync(0xffffffffu, refined);
     abandoned = __reduce_add_sync(0xffffffffu, abandoned + skipped);
-    steps = __reduce_add_sync(0xffffffffu, steps);
+    cells = warp_sum_u64(cells);
     if ((threadIdx.x & 31) == 0) {
         if (refined) atomicAdd(&st->refined, refined);
         if (abandoned) atomicAdd(&st->abandoned, abandoned);
-        if (steps) atomicAdd(&st->dtw_cells, (unsigned long long)steps * 4ull * (2 * R + 1));
+        if (cells) atomicAdd(&st->dtw_cells, cells);
     }
 }
 
@@ -530,12 +567,14 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
     float cnext[H];
     const float* c = rows;
     int j0 = 0;
-    unsigned id = 0, refined = 0, abandoned = 0, strips = 0, skipped = 0;
+    unsigned id = 0, refined = 0, abandoned = 0, skipped = 0;
+    unsigned long long cells = 0;
     // list2 entries of k_lbk_filter_q8: (id, LB_Keogh of the quantised row x^, s, e); the
     // tail bound uses the quantised terms of the rows not done yet (q8_lbk_bound), with
     // x^_j = s rint(x_j / s) recomputed from the raw point (bit-identical to k_quantise)
     float lbk_total = 0.0f, seen = 0.0f, qs = 1.0f, qinv = 1.0f, qe = INFINITY;
     float thr = slack_up(ld_bsf(st));
+    const bool frozen = *(volatile const unsigned*)&st->frozen != 0u;  // inspection: no BSF updates
     bool running = false;
     for (;;) {
         const bool need = !running && nxt.x != 0xffffffffu;
@@ -572,7 +611,6 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
             for (int u = 0; u < H; ++u) dp.cv[u] = cnext[u];
             if (j0 + H < n) load_h(c, j0 + H, cnext);  // the next strip's points, one strip ahead
             dp.template run<REM, K, T>(Bt, qlane + (size_t)j0 * K, R, nfull);
-            ++strips;
 #pragma unroll
             for (int u = 0; u < H; ++u) {
                 const float v = rintf(dp.cv[u] * qinv) * qs, uu = U[j0 + u], ll = L[j0 + u];
@@ -586,24 +624,28 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
             if (bound > thr) {
                 running = false;
                 ++abandoned;
+                cells += band_cells(n, R, j0);
             } else if (j0 >= n) {
                 running = false;
+                cells += band_cells(n, R, n);
                 const float d = Bt[R * T];  // D(n-1, n-1): column n-1 of the last row
                 if (d <= thr) {
-                    bsf_update(st, d);
                     append_near(st, near, id, d);
-                    thr = fminf(thr, slack_up(d));
+                    if (!frozen) {
+                        bsf_update(st, d);
+                        thr = fminf(thr, slack_up(d));
+                    }
                 }
             }
         }
     }
     refined = __reduce_add_sync(0xffffffffu, refined);
     abandoned = __reduce_add_sync(0xffffffffu, abandoned + skipped);
-    strips = __reduce_add_sync(0xffffffffu, strips);
+    cells = warp_sum_u64(cells);
     if (lane == 0) {
         if (refined) atomicAdd(&st->refined, refined);
         if (abandoned) atomicAdd(&st->abandoned, abandoned);
-        if (strips) atomicAdd(&st->dtw_cells, (unsigned long long)strips * H * (2 * R + 1));
+        if (cells) atomicAdd(&st->dtw_cells, cells);
     }
 }
 
@@ -639,11 +681,14 @@ __global__ void k_refine_dtw_warp(const float* __restrict__ rows, int n, int rea
         ++refined;
         const float thr = slack_up(ld_bsf(st));
         if (lane == 0 && d <= thr) {
-            bsf_update(st, d);
+            if (!*(volatile const unsigned*)&st->frozen) bsf_update(st, d);
             append_near(st, near, id, d);
         }
     }
-    if (lane == 0 && refined) atomicAdd(&st->refined, refined);
+    if (lane == 0 && refined) {
+        atomicAdd(&st->refined, refined);
+        atomicAdd(&st->dtw_cells, (unsigned long long)refined * band_cells(n, reach, n));
+    }
 }
 
 // ------------------------------------------------------------------- exact resolution
@@ -711,18 +756,27 @@ __device__ Best block_best(Best b, int* cnt_io)
 // DTW exact resolution (A9): every near-best entry with d32 <= BSF_final*(1+eps) is
 // recomputed in fp64 with the warp wavefront (bit-identical to the row-by-row DP of the
 // oracle: every cell is fl(fl(d*d) + min) whatever the order).  Per-warp shared memory:
-// q and the row (2n floats) + 3n doubles.
+// q and the row (2 npad floats), then (reach > kShflMaxReach and gbuf == NULL) the 3n
+// doubles of the shared-memory wavefront; with gbuf the wavefront lives in global scratch
+// (gbuf + 3n per warp: long series whose buffers do not fit shared memory).
+__host__ __device__ inline size_t resolve_warp_bytes(int n, int reach, bool global_buf)
+{
+    const size_t npad = (size_t)((n + 3) & ~3);
+    return 2 * npad * sizeof(float) + ((reach > kShflMaxReach && !global_buf) ? (size_t)3 * n * sizeof(double) : 0);
+}
+
 __global__ void k_resolve_dtw(const float* __restrict__ rows, int n, int reach, const float* __restrict__ q_g,
                               const NearEntry* __restrict__ near, QState* st, long long N, long long row_begin,
-                              void* result, void* stats)
+                              void* result, void* stats, double* gbuf)
 {
     extern __shared__ __align__(16) double dbuf[];
     const int npad = (n + 3) & ~3;
     const float thr = slack_up(ld_bsf(st));
     const unsigned total = *(volatile unsigned*)&st->near_count;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-    double* buf = dbuf + (size_t)w * (3 * n + npad);
-    float* qc = reinterpret_cast<float*>(buf + 3 * n);  // q then c
+    char* mine = reinterpret_cast<char*>(dbuf) + (size_t)w * resolve_warp_bytes(n, reach, gbuf != nullptr);
+    float* qc = reinterpret_cast<float*>(mine);  // q then c
+    double* buf = gbuf ? gbuf + (size_t)w * 3 * n : reinterpret_cast<double*>(mine + 2 * (size_t)npad * sizeof(float));
     for (int i = lane; i < n; i += 32) qc[i] = q_g[i];
     Best b{(double)INFINITY, -1};
     int cnt = 0;
@@ -741,61 +795,23 @@ __global__ void k_resolve_dtw(const float* __restrict__ rows, int n, int reach, 
 __global__ void k_arm(QState* st) { arm_state(st); }
 
 // --------------------------------------------------------------------- inspection
-// Per id: refine-kernel fp32 distance (no abandoning), exact fp64 distance, and (DTW) the
-// fp32 LB_Keogh -- the same device routines the query path runs.  One warp per id.
-// Shared memory: q, U, L (3 npad floats) + per warp: row (npad floats) + 3n doubles.
-template <int R>
-__global__ void k_debug_dist(const float* __restrict__ rows, int n, int reach, const float* __restrict__ q_g,
-                             const float* __restrict__ U_g, const float* __restrict__ L_g,
-                             const unsigned* __restrict__ ids, int k, float* d32, double* d64, float* lbk)
+// fp64 DTW of `k` local row ids with the resolve kernel's engine (dtw_warp_any<double>,
+// one warp per id; same per-warp memory layout as k_resolve_dtw).
+__global__ void k_debug_dtw64(const float* __restrict__ rows, int n, int reach, const float* __restrict__ q_g,
+                              const unsigned* __restrict__ ids, int k, double* __restrict__ d64, double* gbuf)
 {
-    extern __shared__ __align__(16) float dsm[];
+    extern __shared__ __align__(16) double dbuf[];
     const int npad = (n + 3) & ~3;
-    float* q_s = dsm;
-    float* U = dsm + npad;
-    float* L = dsm + 2 * npad;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-    float* c_s = dsm + 3 * npad + (size_t)w * (npad + 6 * n);
-    double* buf = reinterpret_cast<double*>(c_s + npad);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        q_s[i] = q_g[i];
-        if (reach >= 0) { U[i] = U_g[i]; L[i] = L_g[i]; }
-    }
-    __syncthreads();
+    char* mine = reinterpret_cast<char*>(dbuf) + (size_t)w * resolve_warp_bytes(n, reach, gbuf != nullptr);
+    float* qc = reinterpret_cast<float*>(mine);
+    double* buf = gbuf ? gbuf + ((size_t)blockIdx.x * wpb + w) * 3 * n
+                       : reinterpret_cast<double*>(mine + 2 * (size_t)npad * sizeof(float));
+    for (int i = lane; i < n; i += 32) qc[i] = q_g[i];
     for (int t = blockIdx.x * wpb + w; t < k; t += gridDim.x * wpb) {
-        const float* c = rows + (long long)ids[t] * n;
-        stage_row(c_s, c, n, lane);
-        if (reach < 0) {
-            float v = ed2_warp(q_s, c, n, lane);
-            if (lane == 0) {
-                if (d32) d32[t] = v;
-                if (d64) d64[t] = ed2_exact(q_s, c_s, n);
-            }
-        } else {
-            if (lbk) {
-                float v = lbk_warp(U, L, c, n, lane);
-                if (lane == 0) lbk[t] = v;
-            }
-            if (d64) {
-                double v = dtw_warp_any<double>(q_s, c_s, n, reach, buf, lane);
-                if (lane == 0) d64[t] = v;
-            }
-            if (d32) {
-                float v;
-                if (R >= 0 && reach == R) {
-                    v = INFINITY;
-                    if (lane == 0) {
-                        DtwThread<(R >= 0 ? R : 0)> dp;
-                        dp.start(c, n, 0.0f);
-                        while (dp.i < n) dp.step4(c, n, q_s, U, L);
-                        v = dp.result();
-                    }
-                } else {
-                    v = dtw_warp_any<float>(q_s, c_s, n, reach, reinterpret_cast<float*>(buf), lane);
-                }
-                if (lane == 0) d32[t] = v;
-            }
-        }
+        stage_row(qc + npad, rows + (long long)ids[t] * n, n, lane);
+        const double d = dtw_warp_any<double>(qc, qc + npad, n, reach, buf, lane);
+        if (lane == 0) d64[t] = d;
         __syncwarp();
     }
 }

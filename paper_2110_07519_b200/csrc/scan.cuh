@@ -434,19 +434,4 @@ __global__ void __launch_bounds__(32 * kScanWarps) k_debug_coarse(const uint4* _
     }
 }
 
-// Inspection: the fine bound of every series (segments in order 0..15), scattered back to
-// row order; table T8 from the compact prologue output lut_g[s][v].
-__global__ void k_debug_lb8(const uint4* __restrict__ sym8, const unsigned* __restrict__ perm, long long N,
-                            const float* __restrict__ lut_g, float* __restrict__ lb_all)
-{
-    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= N) return;
-    const uint4 w = sym8[p];
-    const unsigned wv[4] = {w.x, w.y, w.z, w.w};
-    float acc = 0.0f;
-#pragma unroll
-    for (int s = 0; s < 16; ++s) acc = __fadd_rd(acc, lut_g[s * 256 + ((wv[s >> 2] >> (8 * (s & 3))) & 255u)]);
-    lb_all[perm[p]] = acc;
-}
-
 }  // namespace messi

@@ -16,7 +16,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# MESSI_LIB selects an alternative build of the same sources (kernel-tuning experiments)
+# The in-tree build.  MESSI_LIB may select an alternative build of the same sources for A/B
+# kernel experiments (tools/); bench.py refuses to run with it set.
 LIB_PATH = os.environ.get("MESSI_LIB") or os.path.join(_HERE, "libmessi.so")
 
 MESSI_OK, MESSI_EINVAL, MESSI_EEMPTY, MESSI_ENOMEM, MESSI_ECUDA = range(5)
@@ -80,6 +81,8 @@ def lib():
         L.messi_launch_count.restype = i64
         L.messi_profile_enable.argtypes = [vp, i32]
         L.messi_profile_read.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
+        L.messi_build_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
+        L.messi_build_times.restype = ctypes.c_int
         L.messi_debug_scan_repeat.argtypes = [vp, vp, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
         L.messi_debug_breakpoints.argtypes = [i32, vp]
         L.messi_debug_summaries.argtypes = [vp, vp, vp]
@@ -93,10 +96,15 @@ def lib():
         L.messi_debug_lower_bounds.argtypes = [vp, vp, i32, vp]
         L.messi_debug_tile_bounds.argtypes = [vp, vp, i32, vp]
         L.messi_debug_distances.argtypes = [vp, vp, i32, vp, i32, vp, vp, vp]
+        L.messi_debug_super_bounds.argtypes = [vp, vp, vp]
+        L.messi_debug_ed_refine.argtypes = [vp, vp, vp, i32, vp, vp]
+        L.messi_debug_dtw_stages.argtypes = [vp, vp, i32, vp, i32, vp, vp, ctypes.POINTER(i32)]
         for f in ("messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_batch",
                   "messi_query_dtw_batch", "messi_profile_enable", "messi_profile_read", "messi_debug_breakpoints", "messi_debug_summaries",
                   "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances",
-                  "messi_debug_scan_repeat", "messi_debug_tile_bounds"):
+                  "messi_debug_scan_repeat", "messi_debug_tile_bounds", "messi_debug_super_bounds",
+                  "messi_debug_ed_refine", "messi_debug_dtw_stages", "messi_debug_coarse_bounds",
+                  "messi_debug_quantised"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -108,7 +116,8 @@ EXPORTED = ["messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_
             "messi_debug_summaries", "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances",
             "messi_debug_scan_repeat", "messi_debug_tile_bounds", "messi_debug_quantised",
             "messi_debug_coarse_bounds", "messi_batch_state_ipc", "messi_link_peers_ipc",
-            "messi_link_peers_local", "messi_query_ed_knn", "messi_query_ed_knn_batch"]
+            "messi_link_peers_local", "messi_query_ed_knn", "messi_query_ed_knn_batch", "messi_debug_super_bounds",
+            "messi_debug_ed_refine", "messi_debug_dtw_stages", "messi_build_times"]
 
 
 def _check(status: int):
@@ -156,16 +165,43 @@ def messi_query_dtw(handle, query, reach: int, with_stats: bool = False):
     return (res.dist, res.id, res.d2, st.as_dict()) if with_stats else (res.dist, res.id, res.d2)
 
 
-def messi_query_ed_batch(handle, queries_dev: torch.Tensor, results_dev: torch.Tensor, stats_dev=None):
+def _check_batch(queries_dev, results_dev, stats_dev, per_query_results=1, n=None):
+    """Argument checks of the batch calls (the C-ABI takes raw pointers and counts): float32,
+    contiguous, CUDA, [nq, n] queries; result / stats buffers on the same device, contiguous,
+    large enough for nq * per_query_results records / nq stats."""
+    def bad(msg):
+        raise MessiError(MESSI_EINVAL, msg)
+    if not isinstance(queries_dev, torch.Tensor) or not queries_dev.is_cuda:
+        bad("queries must be a CUDA tensor")
+    if queries_dev.dtype != torch.float32 or not queries_dev.is_contiguous() or queries_dev.dim() != 2:
+        bad("queries must be a contiguous float32 [nq, n] tensor")
+    if n is not None and queries_dev.shape[1] != n:
+        bad(f"queries have length {queries_dev.shape[1]}, the index {n}")
+    nq = queries_dev.shape[0]
+    for name, buf, need in (("results", results_dev, nq * per_query_results * RESULT_BYTES),
+                            ("stats", stats_dev, nq * STATS_BYTES)):
+        if buf is None:
+            if name == "results":
+                bad("results buffer is required")
+            continue
+        if not buf.is_cuda or buf.device != queries_dev.device or not buf.is_contiguous():
+            bad(f"{name} must be a contiguous tensor on {queries_dev.device}")
+        if buf.numel() * buf.element_size() < need:
+            bad(f"{name} buffer holds {buf.numel() * buf.element_size()} bytes, needs {need}")
+    return nq
+
+
+def messi_query_ed_batch(handle, queries_dev: torch.Tensor, results_dev: torch.Tensor, stats_dev=None, n=None):
     """Asynchronous on the build stream.  results_dev: uint8 CUDA tensor of nq*32 bytes (see
     ``result_buffer``); stats_dev: optional nq*104 bytes (``stats_buffer``)."""
-    _check(lib().messi_query_ed_batch(handle, _ptr(queries_dev), queries_dev.shape[0], _ptr(results_dev),
-                                      _ptr(stats_dev)))
+    nq = _check_batch(queries_dev, results_dev, stats_dev, 1, n)
+    _check(lib().messi_query_ed_batch(handle, _ptr(queries_dev), nq, _ptr(results_dev), _ptr(stats_dev)))
 
 
-def messi_query_dtw_batch(handle, queries_dev: torch.Tensor, reach: int, results_dev: torch.Tensor, stats_dev=None):
-    _check(lib().messi_query_dtw_batch(handle, _ptr(queries_dev), queries_dev.shape[0], int(reach),
-                                       _ptr(results_dev), _ptr(stats_dev)))
+def messi_query_dtw_batch(handle, queries_dev: torch.Tensor, reach: int, results_dev: torch.Tensor, stats_dev=None,
+                          n=None):
+    nq = _check_batch(queries_dev, results_dev, stats_dev, 1, n)
+    _check(lib().messi_query_dtw_batch(handle, _ptr(queries_dev), nq, int(reach), _ptr(results_dev), _ptr(stats_dev)))
 
 
 def messi_batch_state_ipc(handle, set_index: int) -> bytes:
@@ -199,10 +235,11 @@ def messi_query_ed_knn(handle, query, k: int, with_stats: bool = False):
     return (dist, ids, d2, st.as_dict()) if with_stats else (dist, ids, d2)
 
 
-def messi_query_ed_knn_batch(handle, queries_dev: torch.Tensor, k: int, results_dev: torch.Tensor, stats_dev=None):
+def messi_query_ed_knn_batch(handle, queries_dev: torch.Tensor, k: int, results_dev: torch.Tensor, stats_dev=None,
+                             n=None):
     """results_dev: uint8 CUDA tensor of nq*k*32 bytes (result_buffer(nq * k))."""
-    _check(lib().messi_query_ed_knn_batch(handle, _ptr(queries_dev), queries_dev.shape[0], int(k), _ptr(results_dev),
-                                          _ptr(stats_dev)))
+    nq = _check_batch(queries_dev, results_dev, stats_dev, max(1, int(k)), n)
+    _check(lib().messi_query_ed_knn_batch(handle, _ptr(queries_dev), nq, int(k), _ptr(results_dev), _ptr(stats_dev)))
 
 
 def messi_free(handle):
@@ -217,8 +254,16 @@ def messi_launch_count(handle) -> int:
 KERNEL_KINDS = {"seed": 0, "scan": 1, "refine": 2, "lbk": 3, "resolve": 4}
 
 
-def messi_profile_enable(handle, enable: bool = True):
-    _check(lib().messi_profile_enable(handle, int(enable)))
+def messi_profile_enable(handle, enable: bool = True, serial: bool = False):
+    """enable: per-kernel CUDA-event timing; serial: every per-query stage on the index stream."""
+    _check(lib().messi_profile_enable(handle, int(bool(enable)) | (2 if serial else 0)))
+
+
+def messi_build_times(handle):
+    """Device ms of the build phases: summarise, key sort, layout, quantise."""
+    out = (ctypes.c_double * 4)()
+    _check(lib().messi_build_times(handle, out))
+    return {"summarise": out[0], "sort": out[1], "layout": out[2], "quantise": out[3]}
 
 
 def messi_profile_read(handle, kind):
@@ -286,6 +331,34 @@ def messi_debug_tile_bounds(handle, query_dev: torch.Tensor, reach: int, ntiles:
     lb = torch.empty(ntiles, dtype=torch.float32, device=query_dev.device)
     _check(lib().messi_debug_tile_bounds(handle, _ptr(query_dev), int(reach), _ptr(lb)))
     return lb
+
+
+def messi_debug_super_bounds(handle, query_dev: torch.Tensor, nsuper: int):
+    lb = torch.empty(nsuper, dtype=torch.float32, device=query_dev.device)
+    _check(lib().messi_debug_super_bounds(handle, _ptr(query_dev), _ptr(lb)))
+    return lb
+
+
+def messi_debug_ed_refine(handle, query_dev: torch.Tensor, ids_dev: torch.Tensor):
+    """(dh2, L, d32) float32 [k] each and d64 float64 [k] of the ED refine's device code."""
+    ids = ids_dev.to(torch.int32).contiguous()
+    k = ids.numel()
+    out4 = torch.empty((k, 4), dtype=torch.float32, device=query_dev.device)
+    d64 = torch.empty(k, dtype=torch.float64, device=query_dev.device)
+    _check(lib().messi_debug_ed_refine(handle, _ptr(query_dev), _ptr(ids), k, _ptr(out4), _ptr(d64)))
+    return out4[:, 0], out4[:, 1], out4[:, 2], d64
+
+
+def messi_debug_dtw_stages(handle, query_dev: torch.Tensor, reach: int, ids_dev: torch.Tensor):
+    """(lbk float32 [k], d32 float32 [k], quantised: bool) of the DTW filter and refine kernels."""
+    ids = ids_dev.to(torch.int32).contiguous()
+    k = ids.numel()
+    lbk = torch.empty(k, dtype=torch.float32, device=query_dev.device)
+    d32 = torch.empty(k, dtype=torch.float32, device=query_dev.device)
+    qz = ctypes.c_int32()
+    _check(lib().messi_debug_dtw_stages(handle, _ptr(query_dev), int(reach), _ptr(ids), k, _ptr(lbk), _ptr(d32),
+                                        ctypes.byref(qz)))
+    return lbk, d32, bool(qz.value)
 
 
 def messi_debug_distances(handle, query_dev: torch.Tensor, reach: int, ids_dev: torch.Tensor):
@@ -376,9 +449,9 @@ class Index:
         nq = queries_dev.shape[0]
         results = results if results is not None else result_buffer(nq, self.device)
         if reach is None:
-            messi_query_ed_batch(self.handle, queries_dev, results, stats)
+            messi_query_ed_batch(self.handle, queries_dev, results, stats, n=self.n)
         else:
-            messi_query_dtw_batch(self.handle, queries_dev, reach, results, stats)
+            messi_query_dtw_batch(self.handle, queries_dev, reach, results, stats, n=self.n)
         return results, stats
 
     def query_knn(self, q, k: int, with_stats=False):
@@ -388,7 +461,7 @@ class Index:
         """Enqueue nq exact k-NN (ED) queries; results: nq*k entries (decode_results -> [nq*k])."""
         nq = queries_dev.shape[0]
         results = results if results is not None else result_buffer(nq * k, self.device)
-        messi_query_ed_knn_batch(self.handle, queries_dev, k, results, stats)
+        messi_query_ed_knn_batch(self.handle, queries_dev, k, results, stats, n=self.n)
         return results, stats
 
     def launches(self) -> int:

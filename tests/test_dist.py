@@ -107,3 +107,15 @@ def test_sharded_knn_merge_equals_single_scan(k):
     d2, ids = oracle.knn("ed", X, Q, k)
     assert np.array_equal(gid, ids) and np.array_equal(gd2, d2)
     assert gid[0, 0] == 2
+
+
+def test_bench_rejects_gpus_world_size_mismatch():
+    """bench.py --gpus N under a launcher whose WORLD_SIZE disagrees refuses to run (it would
+    otherwise time a different number of GPUs than the command line names)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--no-cpu"], cwd=root, capture_output=True,
+                         text=True, timeout=300, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE=1" in (out.stderr + out.stdout)

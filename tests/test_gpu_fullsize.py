@@ -121,24 +121,39 @@ def test_config3_ed_100m():
 
 
 def test_config4_dtw_10m():
+    """Config 4 (10M x 256, reach 25) in the bench's launch configuration: 10 queries batched.
+    Query 0 against the oracle's brute force over every row.  All 10 against an exact brute
+    force over every row that COULD beat the GPU's answer: a row whose LB_Keogh exceeds the
+    GPU's d2 has DTW > d2 (LB_Keogh <= DTW, pinned in test_oracle_pins), so the
+    oracle's DTW over the rows with LB_Keogh <= d2 (selected here with fp64 torch and a 1e-9
+    margin) must return exactly the GPU's (d2, id), ties to the lowest id."""
     X, idx = build(10_000_000, 256, None)
-    Q = torch.empty((4, 256), dtype=torch.float32, device=DEV)
+    nq = 10
+    Q = torch.empty((nq, 256), dtype=torch.float32, device=DEV)
     datagen.walks_cuda(Q, 0, seed=datagen.QUERY_SEED)
     try:
         got = run_batch(idx, Q, reach=25)
         sample = [0]
         d2, ids = oracle_full("dtw", X, Q[sample].cpu().numpy(), reach=25)
         check(tuple(t[sample] for t in got), d2, ids)
-        # every other query: its answer is a real row at exactly that DTW distance, and no
-        # row of a 200K sample is strictly closer (a property that holds at any size)
         dist, gid, gd2 = (t.numpy() for t in got)
         Qh = Q.cpu().numpy()
-        rows = np.random.default_rng(0).choice(X.shape[0], 200_000, replace=False)
-        Xs = X[torch.from_numpy(rows).to(DEV)].cpu().numpy()
-        for qi in range(1, 4):
-            assert oracle.dtw2(Qh[qi], X[int(gid[qi])].cpu().numpy(), 25) == gd2[qi]
+        for qi in range(nq):
+            U, L = oracle.envelope(Qh[qi], 25)
+            Ud = torch.from_numpy(U.astype(np.float64)).to(DEV)
+            Ld = torch.from_numpy(L.astype(np.float64)).to(DEV)
+            sel = []
+            for b in range(0, X.shape[0], CHUNK):
+                c = X[b:b + CHUNK].double()
+                lbk = ((c - Ud).clamp(min=0) ** 2 + (Ld - c).clamp(min=0) ** 2).sum(1)
+                sel.append(torch.nonzero(lbk <= gd2[qi] * (1 + 1e-9)).flatten() + b)
+                del c, lbk
+            sel = torch.cat(sel)
+            assert sel.numel() >= 1
+            Xs = X[sel].cpu().numpy()
             sd, si = oracle.nn("dtw", Xs, Qh[qi:qi + 1], r=25)
-            assert sd[0] >= gd2[qi]
+            assert sd[0] == gd2[qi], (qi, sd[0], gd2[qi])
+            assert int(sel[int(si[0])]) == gid[qi], (qi, int(sel[int(si[0])]), gid[qi])
     finally:
         idx.close()
         del X

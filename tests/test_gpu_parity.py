@@ -84,38 +84,55 @@ def test_approximate_search_order_is_valid(c1):
 
 
 # ------------------------------------------------------------------ lower bounds (A3/A5)
+# Every step-level check below reads the QUERY PATH'S OWN KERNELS (include/messi.h, inspection
+# entry points): k_scan / fine_lb for the 8-bit bound, coarse_acc for the cardinality-16 one,
+# k_filter_batch / box_lb for the ED tile boxes, k_tile_filter for the DTW ones, q8_bound_pass /
+# ed2_group / ed2_exact_g for the ED refine, and the LB_Keogh filter + strip / band / warp
+# refine kernels (frozen) for DTW.
+U32 = 2.0 ** -24  # fp32 unit roundoff
+
+
 def _lb_tol(d_seg, m):
-    # GPU boxes are widened by one fp32 ulp (<= 4.8e-7 for |beta| < 4) and summed rounding
-    # down: |GPU - oracle| <= m * sum_s (2 d_s u + u^2) + 2^-20 * LB
+    # GPU boxes are widened by one fp32 ulp (<= 4.8e-7 for |beta| < 4), table entries rounded
+    # down to fp32 and summed rounding down: GPU <= oracle, and oracle - GPU <= m * sum_s
+    # (2 d_s u + u^2) + 18 u * LB (16 roundings of the terms, 16 of the sum, the fp64 products)
     u = 4.8e-7
     return m * (2 * d_seg.sum(1) * u + 16 * u * u)
 
 
+def _mindist_rows(qp, S, card=256):
+    b32 = oracle.breakpoints(card)[1]
+    return np.array([oracle.mindist2(qp, S[r], 256, card=card, beta32=b32) for r in range(S.shape[0])])
+
+
 def test_lower_bounds_ed(c1):
+    """The scan's 8-bit bound (k_scan: fine_lb over the fused ED kernel's own table) of EVERY C1
+    row: GPU <= oracle mindist <= true ED^2 (Property 1), and oracle - GPU within
+    the widened-box / round-down tolerance."""
     X, Q, idx, Xh, Qh = c1
     _, S = oracle.isax_rows(Xh)
     b32 = oracle.breakpoints()[1]
     lo = np.concatenate([[-np.inf], b32]).astype(np.float64)
     hi = np.concatenate([b32, [np.inf]]).astype(np.float64)
-    for qi in range(3):
+    for qi in range(2):
         lb = messi().messi_debug_lower_bounds(idx.handle, Q[qi].contiguous(), -1, X.shape[0]).cpu().numpy()
+        assert not np.isnan(lb).any()  # every row came out of the scan kernel
+        lb = lb.astype(np.float64)
         qp = oracle.paa64(Qh[qi])
-        rows = np.random.default_rng(qi).choice(X.shape[0], 3000, replace=False)
-        ref = np.array([oracle.mindist2(qp, S[r], 256) for r in rows])
-        d_seg = np.maximum(0, np.maximum(lo[S[rows]] - qp, qp - hi[S[rows]]))
-        tol = _lb_tol(d_seg, 16) + 2.0 ** -20 * ref
-        assert np.all(np.abs(lb[rows] - ref) <= tol)
-        # Property 1: LB <= true ED^2, for every row of the collection
-        ed = oracle.ed2_rows(Xh, Qh[qi])
-        assert np.all(lb.astype(np.float64) <= ed)
+        ref = _mindist_rows(qp, S)
+        d_seg = np.maximum(0, np.maximum(lo[S] - qp, qp - hi[S]))
+        tol = _lb_tol(d_seg, 16) + 18 * U32 * ref
+        assert np.all(lb <= ref * (1 + 1e-12))
+        assert np.all(ref - lb <= tol)
+        assert np.all(ref <= oracle.ed2_rows(Xh, Qh[qi]))
 
 
 @pytest.mark.parametrize("reach", [-1, 25])
 def test_coarse_bounds(c1, reach):
     """The scan's coarse pass (cardinality 16 = the top 4 bits of every symbol):
-    its bound equals the oracle's card-16 mindist (ED) within the widened-box / round-down
-    tolerance, never exceeds the 8-bit bound of the same row (the coarse box contains the
-    fine one), and never exceeds the true distance (ED) / the DTW bound chain."""
+    on every C1 row its bound never exceeds the 8-bit bound of the same row (the coarse box
+    contains the fine one); ED: GPU <= the oracle's card-16 mindist <= true ED^2, within the
+    widened-box / round-down tolerance."""
     X, Q, idx, Xh, Qh = c1
     N = X.shape[0]
     _, S = oracle.isax_rows(Xh)
@@ -124,20 +141,20 @@ def test_coarse_bounds(c1, reach):
         q = Q[qi].contiguous()
         cb = messi().messi_debug_coarse_bounds(idx.handle, q, reach, N).cpu().numpy().astype(np.float64)
         fb = messi().messi_debug_lower_bounds(idx.handle, q, reach, N).cpu().numpy().astype(np.float64)
+        assert not np.isnan(cb).any() and not np.isnan(fb).any()
         assert np.all(cb <= fb * (1 + 2.0 ** -20) + 1e-30)
         if reach < 0:
             qp = oracle.paa64(Qh[qi])
-            rows = np.random.default_rng(10 + qi).choice(N, 2000, replace=False)
-            ref = np.array([oracle.mindist2(qp, S[r] >> 4, 256, card=16) for r in rows])
+            ref = _mindist_rows(qp, S >> 4, card=16)
             lo = np.concatenate([[-np.inf], b16]).astype(np.float64)
             hi = np.concatenate([b16, [np.inf]]).astype(np.float64)
-            d_seg = np.maximum(0, np.maximum(lo[S[rows] >> 4] - qp, qp - hi[S[rows] >> 4]))
-            tol = _lb_tol(d_seg, 16) + 2.0 ** -20 * ref
-            assert np.all(np.abs(cb[rows] - ref) <= tol)
-            assert np.all(cb <= oracle.ed2_rows(Xh, Qh[qi]))
-        # the coarse pass is a real filter: most rows fail it at the NN distance
-        d2, _ = oracle.nn("ed", Xh[:20000], Qh[qi:qi + 1]) if reach < 0 else (None, None)
-        if reach < 0:
+            d_seg = np.maximum(0, np.maximum(lo[S >> 4] - qp, qp - hi[S >> 4]))
+            tol = _lb_tol(d_seg, 16) + 18 * U32 * ref
+            assert np.all(cb <= ref * (1 + 1e-12))
+            assert np.all(ref - cb <= tol)
+            assert np.all(ref <= oracle.ed2_rows(Xh, Qh[qi]))
+            # the coarse pass is a real filter: most rows fail it at the NN distance
+            d2, _ = oracle.nn("ed", Xh[:20000], Qh[qi:qi + 1])
             assert np.mean(cb <= d2[0]) < 0.5
 
 
@@ -145,48 +162,157 @@ def test_coarse_bounds(c1, reach):
 def test_tile_box_bounds(c1, reach):
     """The box of a tile (512 consecutive series in approximate-search order) bounds every
     member from below: tile LB <= each member's 8-bit bound <= its true distance (the node
-    test of Alg. 7; Property 2)."""
+    test of Alg. 7; Property 2).  ED: the batch filter kernel's
+    fp32 zero-run bound (k_filter_batch), and every super-tile's bound <= its 16 tiles'; DTW:
+    k_tile_filter."""
     X, Q, idx, Xh, Qh = c1
     N = X.shape[0]
     ntiles = (N + 511) // 512
     _, perm = messi().messi_debug_order(idx.handle, N, X.device)
     perm = perm.cpu().numpy().astype(np.int64)
-    tlb = messi().messi_debug_tile_bounds(idx.handle, Q[0].contiguous(), reach, ntiles).cpu().numpy()
-    flb = messi().messi_debug_lower_bounds(idx.handle, Q[0].contiguous(), reach, N).cpu().numpy()
-    member_min = np.full(ntiles, np.inf)
-    np.minimum.at(member_min, np.arange(N) // 512, flb[perm])
-    assert np.all(tlb <= member_min * (1 + 1e-6) + 1e-6)
-    if reach < 0:
-        ed = oracle.ed2_rows(Xh, Qh[0])
-        tmin = np.full(ntiles, np.inf)
-        np.minimum.at(tmin, np.arange(N) // 512, ed[perm])
-        assert np.all(tlb <= tmin)
-    # the filter keeps a minority of tiles at the NN distance (pruning is real)
-    d2, _ = oracle.nn("ed", Xh, Qh[:1])
-    if reach < 0:
-        assert np.mean(tlb <= d2[0]) < 0.8
+    for qi in range(3):
+        q = Q[qi].contiguous()
+        tlb = messi().messi_debug_tile_bounds(idx.handle, q, reach, ntiles).cpu().numpy()
+        assert not np.isnan(tlb).any()  # every tile listed by the filter kernel at threshold +inf
+        flb = messi().messi_debug_lower_bounds(idx.handle, q, reach, N).cpu().numpy()
+        member_min = np.full(ntiles, np.inf)
+        np.minimum.at(member_min, np.arange(N) // 512, flb[perm])
+        if reach < 0:
+            assert np.all(tlb <= member_min * (1 + 16 * U32))  # fp32 sums rounded down, own orders
+            ed = oracle.ed2_rows(Xh, Qh[qi])
+            tmin = np.full(ntiles, np.inf)
+            np.minimum.at(tmin, np.arange(N) // 512, ed[perm])
+            assert np.all(tlb <= tmin)
+            nsuper = (ntiles + 15) // 16
+            slb = messi().messi_debug_super_bounds(idx.handle, q, nsuper).cpu().numpy()
+            tpad = np.full(nsuper * 16, np.inf, np.float32)
+            tpad[:ntiles] = tlb
+            # the union box's exact bound is <= each tile's; both fp32 sums round down in their
+            # own (lane-rotated) order, so compare within the 16 roundings of a sum
+            assert np.all(slb <= tpad.reshape(nsuper, 16).min(axis=1) * (1 + 16 * U32))
+            # the filter keeps a minority of tiles at the NN distance (pruning is real)
+            d2, _ = oracle.nn("ed", Xh, Qh[qi:qi + 1])
+            assert np.mean(tlb <= d2[0]) < 0.8
+        else:
+            assert np.all(tlb <= member_min * (1 + 1e-6) + 1e-6)  # fp64 bound rounded to nearest
 
 
 def test_lower_bounds_dtw(c1):
+    """The scan's envelope-PAA bound (k_scan over k_seed_dtw's table) of every C1 row:
+    GPU <= the oracle's lb_env_paa2 (within rounding), and the chain LB <= LB_Keogh <= DTW."""
     X, Q, idx, Xh, Qh = c1
-    _, S = oracle.isax_rows(Xh[:4000])
+    _, S = oracle.isax_rows(Xh)
     r = 25
     for qi in range(2):
         lb = messi().messi_debug_lower_bounds(idx.handle, Q[qi].contiguous(), r, X.shape[0]).cpu().numpy()
+        assert not np.isnan(lb).any()
         U, L = oracle.envelope(Qh[qi], r)
         Up, Lp = oracle.paa64(U), oracle.paa64(L)
-        rows = np.arange(0, 4000, 7)
-        ref = np.array([oracle.lb_env_paa2(Up, Lp, S[k], 256) for k in rows])
-        assert np.all(lb[rows] <= ref * (1 + 1e-6) + 1e-9)
-        assert np.all(lb[rows] >= ref * (1 - 1e-4) - 1e-3)
-        for k in rows[:200]:  # the chain LB_envPAA <= LB_Keogh <= DTW holds on the GPU bound
-            assert lb[k] <= oracle.lb_keogh2(U, L, Xh[k]) <= oracle.dtw2(Qh[qi], Xh[k], r)
+        b32 = oracle.breakpoints(256)[1]
+        ref = np.array([oracle.lb_env_paa2(Up, Lp, S[k], 256, beta32=b32) for k in range(S.shape[0])])
+        assert np.all(lb <= ref * (1 + 1e-6) + 1e-9)
+        assert np.all(lb >= ref * (1 - 1e-4) - 1e-3)
+        lbk = np.array([oracle.lb_keogh2(U, L, Xh[k]) for k in range(0, S.shape[0], 50)])
+        assert np.all(lb[::50] <= lbk)
+        assert np.all(lbk <= oracle.dtw2_rows(Xh[::50], Qh[qi], r))
 
 
 # -------------------------------------------------------------- real distances (A7-A9)
+def test_ed_refine_stages_every_row(c1):
+    """The ED refine's own device code on EVERY C1 row (messi_debug_ed_refine):
+      * q8_bound_pass: dh2 = fp32 ||q - s c||^2 over the GPU's quantised row within its fp32
+        error ((n + 16) u relative) of the fp64 value, and its bound L never exceeds the true
+        distance ||q - x|| (oracle ED, triangle inequality; DESIGN.md 5): the prune is safe;
+      * ed2_group (the exact pass): fp32 squared ED within (n/32 + 5 + 2) u relative of the
+        oracle's (8 sequential fma per lane, a 5-level butterfly);
+      * ed2_exact_g (the re-rank): bit-identical to the oracle's fp64 ED^2."""
+    X, Q, idx, Xh, Qh = c1
+    N, n = X.shape
+    q8, meta = messi().messi_debug_quantised(idx.handle, N, n, X.device)
+    c = q8.cpu().numpy().astype(np.float64) - 128.0
+    s = meta[:, 0].cpu().numpy().astype(np.float64)
+    e = meta[:, 1].cpu().numpy().astype(np.float64)
+    xq = s[:, None] * c
+    ids = torch.arange(N, dtype=torch.int32, device=DEV)
+    for qi in range(2):
+        dh2, L, d32, d64 = messi().messi_debug_ed_refine(idx.handle, Q[qi].contiguous(), ids)
+        dh2, L, d32, d64 = (t.cpu().numpy() for t in (dh2, L, d32, d64))
+        q = Qh[qi].astype(np.float64)
+        ref_dh2 = ((xq - q) ** 2).sum(axis=1)
+        assert np.all(np.abs(dh2 - ref_dh2) <= (n + 16) * U32 * ref_dh2 + 1e-30)
+        ed = oracle.ed2_rows(Xh, Qh[qi])
+        assert np.all(L.astype(np.float64) <= np.sqrt(ed))
+        assert np.all(L >= np.sqrt(ref_dh2) * (1 - 2.0 ** -11) - e - 1e-6)  # and it is tight
+        assert np.all(np.abs(d32 - ed) <= (n // 32 + 9) * U32 * ed + 1e-30)
+        assert np.array_equal(d64, ed)
+
+
+@pytest.mark.parametrize("reach", [0, 2, 5, 7, 12, 25, 51])
+def test_dtw_stages_elementwise(c1, reach):
+    """The DTW filter and refine KERNELS of the query path on 1,500 C1 rows (the ids handed
+    to them as candidates, threshold +inf, refine frozen: no abandon):
+      * LB_Keogh: at strip reaches (r >= 7) the filter's LB_Keogh of the quantised row x^
+        within fp32 summation error of its fp64 value, and (sqrt(LBK(x^)(1 - 2^-10)) - e)^2
+        <= the oracle's raw LB_Keogh <= DTW; at other reaches the raw LB_Keogh within fp32
+        error of the oracle's;
+      * refine (strip kernel r >= 7, register band r = 2, 5, warp wavefront r = 0): fp32 DTW^2
+        within (2n + 2) u relative of the oracle's fp64 DTW^2 (the error of a sum along one
+        warping path of <= 2n - 1 cells)."""
+    X, Q, idx, Xh, Qh = c1
+    N, n = X.shape
+    rng = np.random.default_rng(100 + reach)
+    ids_np = rng.choice(20_000, 1500, replace=False).astype(np.int32)
+    ids = torch.from_numpy(ids_np).to(DEV)
+    q = Q[2].contiguous()
+    lbk, d32, quantised = messi().messi_debug_dtw_stages(idx.handle, q, reach, ids)
+    lbk, d32 = lbk.cpu().numpy().astype(np.float64), d32.cpu().numpy().astype(np.float64)
+    assert not np.isnan(lbk).any() and not np.isnan(d32).any()
+    assert quantised == (reach >= 7)
+    ref = oracle.dtw2_rows(Xh[ids_np], Qh[2], reach)
+    assert np.all(np.abs(d32 - ref) <= (2 * n + 2) * U32 * ref + 1e-30)
+    U, L = oracle.envelope(Qh[2], reach)
+    raw = np.array([oracle.lb_keogh2(U, L, Xh[i]) for i in ids_np])
+    assert np.all(raw <= ref * (1 + 1e-12))
+    if quantised:
+        q8, meta = messi().messi_debug_quantised(idx.handle, N, n, X.device)
+        cq = q8[ids].cpu().numpy().astype(np.float64) - 128.0
+        sc = meta[ids, 0].cpu().numpy().astype(np.float64)
+        e = meta[ids, 1].cpu().numpy().astype(np.float64)
+        xq = sc[:, None] * cq
+        Ud, Ld = U.astype(np.float64), L.astype(np.float64)
+        tq = (np.where(xq > Ud, xq - Ud, np.where(xq < Ld, xq - Ld, 0.0)) ** 2).sum(axis=1)
+        assert np.all(np.abs(lbk - tq) <= (n + 4) * U32 * tq + 1e-30)
+        bnd = np.maximum(0.0, np.sqrt(lbk * (1 - 2.0 ** -10)) - e) ** 2
+        assert np.all(bnd <= raw * (1 + 1e-12))
+    else:
+        assert np.all(np.abs(lbk - raw) <= (n // 32 + 8) * U32 * raw + 1e-30)
+
+
+def test_dtw_stages_long_series():
+    """The strip refine at n = 2048 with r = 204 (10%) and r = 100 (64-thread CTAs, one query
+    copy: the boundary rows fill shared memory), against the oracle's DTW on 160 rows each."""
+    n = 2048
+    X = gen_rows(3000, n, seed=5)
+    Q = gen_rows(1, n, seed=6)
+    Xh, Qh = X.cpu().numpy(), Q.cpu().numpy()
+    idx = messi().Index(X)
+    try:
+        ids_np = np.random.default_rng(3).choice(3000, 160, replace=False).astype(np.int32)
+        ids = torch.from_numpy(ids_np).to(DEV)
+        for r in (204, 100):
+            _, d32, quantised = messi().messi_debug_dtw_stages(idx.handle, Q[0].contiguous(), r, ids)
+            d32 = d32.cpu().numpy().astype(np.float64)
+            assert quantised
+            ref = oracle.dtw2_rows(Xh[ids_np], Qh[0], r)
+            assert np.all(np.abs(d32 - ref) <= (2 * n + 2) * U32 * ref + 1e-30)
+    finally:
+        idx.close()
+
+
 @pytest.mark.parametrize("reach", [-1, 0, 3, 12, 25, 40])
 def test_distances_elementwise(c1, reach):
     X, Q, idx, Xh, Qh = c1
+    n = X.shape[1]
     ids = np.random.default_rng(7 + reach).choice(X.shape[0], 300, replace=False).astype(np.int32)
     d32, d64, lbk = messi().messi_debug_distances(idx.handle, Q[1].contiguous(), reach,
                                                   torch.from_numpy(ids).to(DEV))
@@ -195,11 +321,9 @@ def test_distances_elementwise(c1, reach):
         ref = np.array([oracle.ed2(Qh[1], Xh[i]) for i in ids])
     else:
         ref = np.array([oracle.dtw2(Qh[1], Xh[i], reach) for i in ids])
-        U, L = oracle.envelope(Qh[1], reach)
-        lref = np.array([oracle.lb_keogh2(U, L, Xh[i]) for i in ids])
-        assert np.allclose(lbk.cpu().numpy(), lref, rtol=2.0 ** -16, atol=1e-6)
+        assert not np.isnan(lbk.cpu().numpy()).any()
     assert np.array_equal(d64, ref)  # canonical fp64: bit-exact
-    assert np.allclose(d32, ref, rtol=2.0 ** -16, atol=1e-6)
+    assert np.all(np.abs(d32 - ref) <= (2 * n + 2) * U32 * ref + 1e-30)
 
 
 # ------------------------------------------------------- quantised-row bound

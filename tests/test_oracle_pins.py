@@ -267,6 +267,35 @@ def test_lower_bound_chain_dtw():
         assert oracle.lb_env_paa2(Up, Lp, S[k], 256) == oracle.mindist2(qp, S[k], 256)
 
 
+def test_lb_env_paa_hand_value_reach1():
+    """O11 at r > 0 on a worked example (Fig. fig:dtwsimd's ABOVE / BELOW / IN cases
+    P:1471-1486), cardinality 4 (breakpoints -b, 0, b with b = Phi^-1(3/4), fp32):
+      q = [0, 1, 0, 0, 2, 0, -1, 0], r = 1 -> U = [1,1,1,2,2,2,0,0], L = [0,0,0,0,0,-1,-1,-1]
+      PAA (w = 4, m = 2): Ubar = [1, 1.5, 2, 0], Lbar = [0, 0, -0.5, -1]
+      symbols [0, 3, 0, 3]: seg 0 BELOW (Lbar - hi(0) = 0 + b), seg 1 IN, seg 2 BELOW
+      (-0.5 + b), seg 3 ABOVE (lo(3) - Ubar = b)
+      LB = m ((b)^2 + (b - 0.5)^2 + (b)^2) with b = 0.6744897365570068 (fp32 of 0.67448975...)
+         = 1.8806389552104292 (evaluated by hand to the last digit in fp64).
+    The series c = [-1,-1, 1,1, -1,-1, 1,1] has exactly those symbols and LB_Keogh 5 (points
+    0, 1, 4 below L by 1; points 6, 7 above U by 1), so the chain LB <= LB_Keogh <= DTW holds."""
+    q = np.array([0, 1, 0, 0, 2, 0, -1, 0], np.float32)
+    U, L = oracle.envelope(q, 1)
+    assert U.tolist() == [1, 1, 1, 2, 2, 2, 0, 0] and L.tolist() == [0, 0, 0, 0, 0, -1, -1, -1]
+    Up, Lp = oracle.paa64(U, 4), oracle.paa64(L, 4)
+    assert Up.tolist() == [1.0, 1.5, 2.0, 0.0] and Lp.tolist() == [0.0, 0.0, -0.5, -1.0]
+    c = np.array([-1, -1, 1, 1, -1, -1, 1, 1], np.float32)
+    _, sym = oracle.isax(c, 4, 4)
+    assert sym.tolist() == [0, 3, 0, 3]
+    lb = oracle.lb_env_paa2(Up, Lp, sym, 8, card=4)
+    assert lb == 1.8806389552104292
+    assert oracle.lb_keogh2(U, L, c) == 5.0
+    assert lb <= 5.0 <= oracle.dtw2(q, c, 1)
+    # flipping any one case changes the value: all three cases are exercised
+    assert oracle.lb_env_paa2(Up, Lp, np.array([3, 3, 0, 3], np.uint8), 8, card=4) < lb
+    assert oracle.lb_env_paa2(Up, Lp, np.array([0, 3, 3, 3], np.uint8), 8, card=4) < lb
+    assert oracle.lb_env_paa2(Up, Lp, np.array([0, 3, 0, 0], np.uint8), 8, card=4) < lb
+
+
 # ------------------------------------------------------------------------- 1-NN (O8/O13)
 def test_nn_ed_vs_numpy_scan_and_threads():
     X = zwalks(3000, 256, 31)
