@@ -150,6 +150,17 @@ messi_status messi_query_ed_knn(messi_index* idx, const float* query, int32_t k,
 messi_status messi_query_ed_knn_batch(messi_index* idx, const float* queries_dev, int32_t nq, int32_t k,
                                       messi_result* results_dev, messi_stats* stats_dev);
 
+/* Exact k-NN under DTW with reach `reach` (the paper's k-NN for both measures, P:2604-2611,
+ * DTW priced at P:2718-2719), 1 <= k <= 64 (k > 1 needs cfg.window <= 4096): BSF0 = the k-th
+ * smallest window distance; the refine keeps the k smallest fp32 distances (their k-th is the
+ * pruning threshold); every completed candidate within it is re-ranked in fp64 and the answer
+ * is the k lexicographically smallest (d2, id), ascending, ties to the lowest id; fewer than k
+ * rows -> the remaining entries are (inf, -1).  Same forms as the ED k-NN calls. */
+messi_status messi_query_dtw_knn(messi_index* idx, const float* query, int32_t reach, int32_t k, messi_result* results,
+                                 messi_stats* stats);
+messi_status messi_query_dtw_knn_batch(messi_index* idx, const float* queries_dev, int32_t nq, int32_t reach, int32_t k,
+                                       messi_result* results_dev, messi_stats* stats_dev);
+
 /* Release everything the library allocated for idx.  NULL-safe. */
 void messi_free(messi_index* idx);
 
@@ -226,12 +237,14 @@ messi_status messi_debug_tile_bounds(messi_index* idx, const float* query_dev, i
  * box_lb, lb_dev[ceil(ntiles / 16)]. */
 messi_status messi_debug_super_bounds(messi_index* idx, const float* query_dev, float* lb_dev);
 
-/* ED refine of `k` local row ids (device u32, distinct): out4_dev[k][4] fp32 = (dh2, L, d32, 0)
- * -- dh2 the fp32 squared distance to the quantised row and L = sqrt_rd(dh2)(1 - delta) - e
- * its lower bound of ||q - x|| (q8_bound_pass), d32 the fp32 squared ED of the exact pass
- * (ed2_group) -- and d64_dev[k] the fp64 canonical re-rank (ed2_exact_g). */
+/* ED refine of `k` local row ids (device u32, distinct), with the query path's device code and
+ * nothing pruned: q8_dev[k][2] fp64 = (dh2, L) -- dh2 a lower bound (fp64, error margin
+ * subtracted) of ||q^ - x^||^2 between the quantised query and the quantised row, L =
+ * sqrt(dh2) - e_q - e_x its lower bound of ||q - x|| (q8i_bound_pass);
+ * d32_dev[k] the fp32 squared ED of the exact pass (ed2_group); d64_dev[k] the fp64 canonical
+ * re-rank (ed2_exact_g).  The quantised query is the batch path's (k_prologue_batch). */
 messi_status messi_debug_ed_refine(messi_index* idx, const float* query_dev, const uint32_t* ids_dev, int32_t k,
-                                   float* out4_dev, double* d64_dev);
+                                   double* q8_dev, float* d32_dev, double* d64_dev);
 
 /* DTW filter + refine of `k` local row ids (device u32, distinct) with reach `reach`: the ids
  * are handed to the query path's LB_Keogh filter kernel (threshold +inf) and refine kernel

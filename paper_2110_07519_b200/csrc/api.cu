@@ -43,6 +43,8 @@ struct Slot {
     unsigned* tlist = nullptr;  // tiles surviving the box filter
     NearEntry* near = nullptr;  // near-best (id, d32) of the DTW refine                          [lazy]
     double* rbuf = nullptr;     // DTW resolve: global wavefront scratch for long series         [lazy]
+    KnnState* knn = nullptr;    // DTW k-NN: the k smallest fp32 distances of the query          [lazy]
+    float* seedd = nullptr;     // DTW k-NN: every approximate-search window distance            [lazy]
     cudaEvent_t ev_seed = nullptr, ev_scan = nullptr, ev_lbk = nullptr, ev_refined = nullptr, ev_done = nullptr;
 };
 
@@ -68,7 +70,6 @@ struct messi_index {
     float* paa = nullptr;
     unsigned char* rows8 = nullptr;  // quantised rows in sorted order [npad][n] (biased int8)
     float2* meta8 = nullptr;         // per sorted position {scale (power of 2), error norm bound}
-    float q8_omd = 1.0f;             // 1 - delta of the quantised bound (rounded down)
     unsigned long long* skey = nullptr;
     unsigned* perm = nullptr;
     float *beta32 = nullptr, *lo_w = nullptr, *hi_w = nullptr;
@@ -77,6 +78,7 @@ struct messi_index {
     struct BatchSet {
         QState* bst = nullptr;
         float *lutc = nullptr, *lutx = nullptr, *lutf = nullptr;
+        unsigned* qc = nullptr;   // quantised queries [kBatchMax][n / 4] (4 x s8 per word)
         uint2* btlist = nullptr;
         KnnState* knn = nullptr;  // k-NN state (lazy)
         float* seedd = nullptr;   // k-NN: the window distances of every query (lazy)
@@ -96,8 +98,6 @@ struct messi_index {
     unsigned* dbg_inv = nullptr;
     int* dbg_map = nullptr;
     unsigned* dbg_iota = nullptr;
-    float4* dbg_out4 = nullptr;
-    size_t dbg_out4_cap = 0;
     double* dbg_gbuf = nullptr;
     // per-query scratch
     Slot slot[MESSI_DTW_SLOTS];
@@ -242,7 +242,8 @@ static bool use_strip(int n, int R, bool have_band)
     return fits && (!have_band || R >= 7);
 }
 
-static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R, const float* q_dev, cudaStream_t rs)
+static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R, const float* q_dev, cudaStream_t rs,
+                                 KnnState* knn, int kk)
 {
     const int H = strip_rows(R);
     const int rem = (2 * R - 2 * H + 3) % H;
@@ -257,7 +258,7 @@ static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R,
         const char* oe = getenv("MESSI_DTW_REFINE_OCC"); /* experiments: CTAs per SM */                          \
         if (oe && atoi(oe) > 0 && atoi(oe) < occ) occ = atoi(oe);                                                \
         k_refine_dtw_strip<HH, REM, KK, TT><<<idx->sms * (occ > 0 ? occ : 1), TT, smem, rs>>>(                   \
-            idx->rows, n, R, q_dev, sl.U, sl.L, sl.list2, (unsigned)idx->N, sl.st, sl.near);                     \
+            idx->rows, n, R, q_dev, sl.U, sl.L, sl.list2, (unsigned)idx->N, sl.st, sl.near, knn, kk);            \
         launched = true;                                                                                         \
     }
     MESSI_STRIP_VARIANTS(LAUNCH_S)
@@ -291,6 +292,7 @@ static messi_status setup_kernels(int device)
     CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_refine_dtw_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_resolve_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_resolve_dtw_knn, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
 #define SET_ATTR_S(H, REM, K, T) CK(cudaFuncSetAttribute(k_refine_dtw_strip<H, REM, K, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStripSmemMax));
     MESSI_STRIP_VARIANTS(SET_ATTR_S)
 #undef SET_ATTR_S
@@ -356,15 +358,6 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
         return bail(s);
     if (idx->keep_paa && (s = dalloc(&idx->paa, (size_t)N * MESSI_W))) return bail(s);
     if ((s = dalloc(&idx->rows8, npadrows * (size_t)n)) || (s = dalloc(&idx->meta8, npadrows))) return bail(s);
-    {
-        // relative error of the fp32 sqrt of the quantised distance: the sum of
-        // n non-negative fma terms plus the 3-level group reduction is within (n + 8) u of the
-        // exact value; delta = max(2^-12, (n + 16) 2^-23) covers it twice over
-        double delta = (double)(n + 16) * 0x1p-23;
-        if (delta < 0x1p-12) delta = 0x1p-12;
-        idx->q8_omd = (float)(1.0 - delta);  // 1 - delta is exact in fp32 up to rounding down below
-        if ((double)idx->q8_omd > 1.0 - delta) idx->q8_omd = nextafterf(idx->q8_omd, 0.0f);
-    }
     if ((s = dalloc(&idx->skey, (size_t)N)) || (s = dalloc(&idx->perm, (size_t)N))) return bail(s);
     if ((s = dalloc(&idx->beta32, 256)) || (s = dalloc(&idx->lo_w, 256)) || (s = dalloc(&idx->hi_w, 256))) return bail(s);
     for (Slot& sl : idx->slot) {
@@ -476,7 +469,7 @@ extern "C" void messi_free(messi_index* idx)
     else cudaDeviceSynchronize();
     void* ptrs[] = {idx->tiles, idx->sym8, idx->boxes, idx->sboxes, idx->paa, idx->skey, idx->perm, idx->beta32, idx->lo_w,
                     idx->hi_w,  idx->qbuf,  idx->res1, idx->resk, idx->stats1, idx->rows8, idx->meta8,
-                    idx->dbg_inv, idx->dbg_map, idx->dbg_iota, idx->dbg_out4, idx->dbg_gbuf};
+                    idx->dbg_inv, idx->dbg_map, idx->dbg_iota, idx->dbg_gbuf};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& row : idx->peer_ipc)
@@ -484,12 +477,12 @@ extern "C" void messi_free(messi_index* idx)
             if (p) cudaIpcCloseMemHandle(p);
     if (idx->d_peers) cudaFree(idx->d_peers);
     for (auto& bs : idx->bset) {
-        void* bp[] = {bs.bst, bs.lutc, bs.lutx, bs.lutf, bs.btlist, bs.knn, bs.seedd};
+        void* bp[] = {bs.bst, bs.lutc, bs.lutx, bs.lutf, bs.qc, bs.btlist, bs.knn, bs.seedd};
         for (void* p : bp)
             if (p) cudaFree(p);
     }
     for (Slot& sl : idx->slot) {
-        void* sp[] = {sl.st, sl.lut, sl.tab, sl.U, sl.L, sl.cand, sl.list2, sl.near, sl.tlist, sl.rbuf};
+        void* sp[] = {sl.st, sl.lut, sl.tab, sl.U, sl.L, sl.cand, sl.list2, sl.near, sl.tlist, sl.rbuf, sl.knn, sl.seedd};
         for (void* p : sp)
             if (p) cudaFree(p);
         cudaEvent_t es[] = {sl.ev_seed, sl.ev_scan, sl.ev_lbk, sl.ev_refined, sl.ev_done};
@@ -689,6 +682,7 @@ static messi_status ensure_batch_buffers(messi_index* idx)
         TRY(dalloc(&bs.lutc, (size_t)kBatchMax * MESSI_W * MESSI_CARD));
         TRY(dalloc(&bs.lutx, (size_t)kBatchMax * kLutX));
         TRY(dalloc(&bs.lutf, (size_t)kBatchMax * kLutF));
+        TRY(dalloc(&bs.qc, (size_t)kBatchMax * (idx->n / 4)));
         TRY(dalloc(&bs.btlist, (size_t)kBatchMax * (size_t)idx->ntiles));
     }
     int occ = 0;
@@ -721,7 +715,7 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
     {
         ProfScope ps(idx, K_SEED, st);
         k_prologue_batch<<<B, 256, qsm, st>>>(q, n, idx->beta32, idx->lo_w, idx->hi_w, idx->skey, idx->N, idx->window,
-                                              bs.lutc, bs.lutx, bs.lutf, bs.bst, knn);
+                                              bs.lutc, bs.lutx, bs.lutf, bs.bst, knn, bs.qc);
         LAUNCHED(idx);
         dim3 sg((unsigned)((len + kSeedRowsPerCta - 1) / kSeedRowsPerCta), (unsigned)B);
         k_seed_batch<<<sg, 256, qsm, st>>>(q, n, idx->rows, idx->perm, bs.bst, peers, seed_d, idx->window);
@@ -747,7 +741,7 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
         ProfScope ps(idx, K_SCAN, st);
 #define FUSED_ARGS                                                                                        \
     idx->tiles, idx->sym8, idx->ntiles, idx->N, n, q, bs.lutx, bs.btlist, bs.bst, B, idx->rows8, idx->meta8, \
-        idx->q8_omd, idx->perm, idx->rows, peers, knn, k
+        bs.qc, idx->perm, idx->rows, peers, knn, k
         const dim3 fg(idx->fused_grid), fb(32 * kFusedWarps);
         const size_t fs = fused_smem(n);
         if (peers.n > 0 && k > 1) k_scan_refine_ed<true, true><<<fg, fb, fs, st>>>(FUSED_ARGS);
@@ -813,14 +807,15 @@ static messi_status launch_lbk_filter(messi_index* idx, Slot& sl, int reach, boo
 
 // DTW step 2: banded fp32 DTW of the list2 entries (near-best entries to sl.near).
 static messi_status launch_dtw_refine(messi_index* idx, Slot& sl, int reach, bool strip, const float* q_dev,
-                                      cudaStream_t rs)
+                                      cudaStream_t rs, int kk = 1)
 {
+    KnnState* knn = kk > 1 ? sl.knn : nullptr;
     const int n = idx->n;
     const int npad = (n + 3) & ~3;
     const size_t qsm = (size_t)npad * sizeof(float);
     bool launched = false;
     if (strip) {
-        TRY(launch_strip(idx, sl, n, reach, q_dev, rs));
+        TRY(launch_strip(idx, sl, n, reach, q_dev, rs, knn, kk));
         launched = true;
     }
 #define LAUNCH_R(R)                                                                                           \
@@ -829,7 +824,7 @@ static messi_status launch_dtw_refine(messi_index* idx, Slot& sl, int reach, boo
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_dtw<R>, 128, 3 * qsm));               \
         k_refine_dtw<R><<<idx->sms * (occ > 0 ? occ : 1), 128, 3 * qsm, rs>>>(idx->rows, n, q_dev, sl.U, sl.L, \
                                                                             sl.list2, (unsigned)idx->N, sl.st, \
-                                                                            sl.near);                         \
+                                                                            sl.near, knn, kk);                \
         launched = true;                                                                                      \
     }
     MESSI_DTW_REACHES(LAUNCH_R)
@@ -837,13 +832,25 @@ static messi_status launch_dtw_refine(messi_index* idx, Slot& sl, int reach, boo
     if (!launched) {
         const int wr = warps_for((size_t)4 * npad * sizeof(float), 8);
         k_refine_dtw_warp<<<idx->sms * 4, 32 * wr, qsm + (size_t)wr * 4 * npad * sizeof(float), rs>>>(
-            idx->rows, n, reach, q_dev, sl.list2, (unsigned)idx->N, sl.st, sl.near);
+            idx->rows, n, reach, q_dev, sl.list2, (unsigned)idx->N, sl.st, sl.near, knn, kk);
     }
     LAUNCHED(idx);
     return MESSI_OK;
 }
 
-static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, messi_result* res, messi_stats* stats)
+static messi_status ensure_dtw_knn(messi_index* idx)
+{
+    for (Slot& sl : idx->slot) {
+        if (!sl.knn) TRY(dalloc(&sl.knn, 1));
+        if (!sl.seedd) TRY(dalloc(&sl.seedd, (size_t)idx->window));
+    }
+    return MESSI_OK;
+}
+
+// One DTW query (k = 1: 1-NN; k > 1: k-NN, results res[k]) on the next slot, staged over the
+// library's streams (serial: all on the caller's stream).
+static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, messi_result* res, messi_stats* stats,
+                            int kk = 1)
 {
     Slot& sl = idx->slot[idx->qcount++ % MESSI_DTW_SLOTS];
     const bool ser = serial_mode(idx);
@@ -860,14 +867,22 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     CK(cudaStreamWaitEvent(side, sl.ev_done, 0));
     // arm the slot for this query (whatever the previous query on it did, e.g. a launch that
     // failed part-way): BSF +inf, every counter 0
-    k_arm<<<1, 1, 0, side>>>(sl.st);
+    if (kk > 1) k_arm_knn<<<1, 1, 0, side>>>(sl.st, sl.knn);
+    else k_arm<<<1, 1, 0, side>>>(sl.st);
     LAUNCHED(idx);
     {
         ProfScope ps(idx, K_SEED, side);
         k_seed_dtw<<<seed_grid, 32 * wf, qsm + wf * seed_warp, side>>>(
             q_dev, n, reach, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32, idx->lo_w, idx->hi_w,
-            sl.lut, sl.tab, sl.U, sl.L, sl.st);
+            sl.lut, sl.tab, sl.U, sl.L, sl.st, kk > 1 ? sl.seedd : nullptr);
         LAUNCHED(idx);
+        if (kk > 1) {  // BSF0 = the k-th smallest window distance
+            int np = 1;
+            while (np < len) np <<= 1;
+            PeerSet none{nullptr, 0, 0u};
+            k_seed_select<<<1, 1024, (size_t)np * sizeof(float), side>>>(sl.seedd, idx->window, kk, sl.st, none);
+            LAUNCHED(idx);
+        }
         TRY(launch_tile_filter(idx, sl, side));
     }
     CK(cudaEventRecord(sl.ev_seed, side));
@@ -884,7 +899,7 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     CK(cudaStreamWaitEvent(rs, sl.ev_lbk, 0));
     {
         ProfScope ps(idx, K_REFINE, rs);
-        TRY(launch_dtw_refine(idx, sl, reach, strip, q_dev, rs));
+        TRY(launch_dtw_refine(idx, sl, reach, strip, q_dev, rs, kk));
     }
     // the exact resolve of this query overlaps the next query's refine (another slot)
     CK(cudaEventRecord(sl.ev_refined, rs));
@@ -895,8 +910,13 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
         const int wr = resolve_warps(n, reach, &gb);
         if (gb && !sl.rbuf) TRY(dalloc(&sl.rbuf, (size_t)8 * 3 * n));
         ProfScope ps(idx, K_RESOLVE, rs);
-        k_resolve_dtw<<<1, 32 * wr, wr * resolve_warp_bytes(n, reach, gb), rs>>>(
-            idx->rows, n, reach, q_dev, sl.near, sl.st, idx->N, idx->row_begin, res, stats, gb ? sl.rbuf : nullptr);
+        if (kk > 1)
+            k_resolve_dtw_knn<<<1, 32 * wr, wr * resolve_warp_bytes(n, reach, gb), rs>>>(
+                idx->rows, n, reach, q_dev, sl.near, sl.st, idx->N, idx->row_begin, res, stats, gb ? sl.rbuf : nullptr,
+                reinterpret_cast<double2*>(sl.list2), kk);
+        else
+            k_resolve_dtw<<<1, 32 * wr, wr * resolve_warp_bytes(n, reach, gb), rs>>>(
+                idx->rows, n, reach, q_dev, sl.near, sl.st, idx->N, idx->row_begin, res, stats, gb ? sl.rbuf : nullptr);
         LAUNCHED(idx);
     }
     CK(cudaEventRecord(sl.ev_done, rs));
@@ -1006,6 +1026,52 @@ extern "C" messi_status messi_query_ed_knn_batch(messi_index* idx, const float* 
     TRY(join_streams(idx));
     if (nq == 0) return MESSI_OK;
     return run_ed_batch(idx, queries_dev, nq, results_dev, stats_dev, k);
+}
+
+static messi_status check_dtw_k(const messi_index* idx, int32_t k)
+{
+    if (k < 1 || k > MESSI_MAX_K) return fail(MESSI_EINVAL, "k = %d outside [1, %d]", k, MESSI_MAX_K);
+    if (k > 1 && idx->window > 4096) return fail(MESSI_EINVAL, "k-NN needs an approximate-search window <= 4096");
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_query_dtw_knn(messi_index* idx, const float* query, int32_t reach, int32_t k,
+                                            messi_result* results, messi_stats* stats)
+{
+    g_err[0] = 0;
+    if (!idx || !query || !results) return fail(MESSI_EINVAL, "NULL argument");
+    if (reach < 0 || reach > idx->n) return fail(MESSI_EINVAL, "reach %d outside [0, %d]", reach, idx->n);
+    TRY(check_dtw_k(idx, k));
+    CK(cudaSetDevice(idx->device));
+    TRY(ensure_dtw_buffers(idx));
+    if (k > 1) TRY(ensure_dtw_knn(idx));
+    if (!idx->resk) TRY(dalloc(&idx->resk, MESSI_MAX_K));
+    const float* q = nullptr;
+    TRY(stage_query(idx, query, &q));
+    TRY(fork_streams(idx));
+    TRY(run_dtw(idx, q, reach, idx->resk, idx->stats1, k));
+    TRY(join_streams(idx));
+    CK(cudaMemcpyAsync(results, idx->resk, sizeof(messi_result) * k, cudaMemcpyDeviceToHost, idx->stream));
+    if (stats) CK(cudaMemcpyAsync(stats, idx->stats1, sizeof(messi_stats), cudaMemcpyDeviceToHost, idx->stream));
+    CK(cudaStreamSynchronize(idx->stream));
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_query_dtw_knn_batch(messi_index* idx, const float* queries_dev, int32_t nq, int32_t reach,
+                                                  int32_t k, messi_result* results_dev, messi_stats* stats_dev)
+{
+    g_err[0] = 0;
+    if (!idx || !queries_dev || !results_dev || nq < 0) return fail(MESSI_EINVAL, "bad argument");
+    if (reach < 0 || reach > idx->n) return fail(MESSI_EINVAL, "reach %d outside [0, %d]", reach, idx->n);
+    TRY(check_dtw_k(idx, k));
+    CK(cudaSetDevice(idx->device));
+    TRY(ensure_dtw_buffers(idx));
+    if (k > 1) TRY(ensure_dtw_knn(idx));
+    TRY(fork_streams(idx));
+    for (int i = 0; i < nq; ++i)
+        TRY(run_dtw(idx, queries_dev + (size_t)i * idx->n, reach, results_dev + (size_t)i * k,
+                    stats_dev ? stats_dev + i : nullptr, k));
+    return join_streams(idx);
 }
 
 extern "C" messi_status messi_query_dtw_batch(messi_index* idx, const float* queries_dev, int32_t nq, int32_t reach,
@@ -1171,7 +1237,7 @@ extern "C" messi_status messi_debug_order(messi_index* idx, const uint64_t** ske
 // k_lbk_filter_q8 / k_lbk_filter and the strip / band / warp DTW refine (frozen: no BSF update,
 // no abandon) for LB_Keogh and the fp32 DTW.  Only the ED refine's inner passes, which sit
 // inside the fused kernel, are reached through a small kernel that calls the same device
-// functions (q8_bound_pass, ed2_group, ed2_exact_g).
+// functions (q8i_bound_pass, ed2_group, ed2_exact_g).
 __global__ void k_dbg_invert(const unsigned* __restrict__ perm, long long N, unsigned* __restrict__ inv)
 {
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1220,11 +1286,6 @@ __global__ void k_dbg_scatter_dtw(const uint4* __restrict__ list2, const NearEnt
         if (lbk && i < nl) lbk[map[list2[i].x]] = __uint_as_float(list2[i].y);
         if (d32 && i < nn) d32[map[near[i].id]] = near[i].d32;
     }
-}
-__global__ void k_dbg_col(const float4* __restrict__ v, int k, int c, float* __restrict__ out)
-{
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < k) out[t] = c == 0 ? v[t].x : (c == 1 ? v[t].y : v[t].z);
 }
 // Box bound of every super-tile (16 consecutive tiles) with the filter's own code (box_lb,
 // same lane mapping: lane = super-tile mod 32), from query 0's filter table of a batch set.
@@ -1276,7 +1337,7 @@ static messi_status debug_prologue(messi_index* idx, const float* query_dev, int
     k_seed_dtw<<<1, 32, 2 * qsm + 3 * (size_t)n * sizeof(float), st>>>(query_dev, n, reach < 0 ? 0 : reach, idx->rows,
                                                                       idx->skey, idx->perm, idx->N, 1, idx->beta32,
                                                                       idx->lo_w, idx->hi_w, sl.lut, sl.tab, sl.U, sl.L,
-                                                                      sl.st);
+                                                                      sl.st, nullptr);
     LAUNCHED(idx);
     k_arm<<<1, 1, 0, st>>>(sl.st);
     LAUNCHED(idx);
@@ -1291,7 +1352,8 @@ static messi_status debug_prologue_ed(messi_index* idx, const float* query_dev)
     const auto& bs = idx->bset[0];
     const size_t qsm = (size_t)((idx->n + 3) & ~3) * sizeof(float);
     k_prologue_batch<<<1, 256, qsm, idx->stream>>>(query_dev, idx->n, idx->beta32, idx->lo_w, idx->hi_w, idx->skey,
-                                                   idx->N, idx->window, bs.lutc, bs.lutx, bs.lutf, bs.bst, nullptr);
+                                                   idx->N, idx->window, bs.lutc, bs.lutx, bs.lutf, bs.bst, nullptr,
+                                                   bs.qc);
     LAUNCHED(idx);
     return MESSI_OK;
 }
@@ -1404,21 +1466,19 @@ extern "C" messi_status messi_debug_super_bounds(messi_index* idx, const float* 
 }
 
 extern "C" messi_status messi_debug_ed_refine(messi_index* idx, const float* query_dev, const uint32_t* ids_dev,
-                                              int32_t k, float* out4_dev, double* d64_dev)
+                                              int32_t k, double* q8_dev, float* d32_dev, double* d64_dev)
 {
-    if ((!ids_dev && k > 0) || k < 0 || !out4_dev || !d64_dev) return fail(MESSI_EINVAL, "bad argument");
+    if ((!ids_dev && k > 0) || k < 0 || !q8_dev || !d32_dev || !d64_dev) return fail(MESSI_EINVAL, "bad argument");
     TRY(debug_begin(idx, query_dev, -1));
     if (k == 0) return MESSI_OK;
     cudaStream_t s = idx->stream;
-    Slot& sl = idx->slot[0];
-    k_dbg_state<<<1, 1, 0, s>>>(sl.st, 0u, 0u, 0u);  // BSF +inf: nothing pruned
-    LAUNCHED(idx);
+    TRY(debug_prologue_ed(idx, query_dev));  // the quantised query of the batch path (set 0, query 0)
     const int wpb = 8;
     unsigned grid = (unsigned)((k + 32 * wpb - 1) / (32 * wpb));
     if (grid > (unsigned)idx->sms * 8) grid = idx->sms * 8;
-    k_debug_ed_refine<<<grid, 32 * wpb, fused_qpad(idx->n) * sizeof(float), s>>>(
-        idx->rows, idx->n, query_dev, idx->rows8, idx->meta8, idx->q8_omd, idx->dbg_inv, sl.st, ids_dev, k,
-        reinterpret_cast<float4*>(out4_dev), d64_dev);
+    k_debug_ed_refine<<<grid, 32 * wpb, fused_qpad(idx->n) * sizeof(float) + idx->n, s>>>(
+        idx->rows, idx->n, query_dev, idx->rows8, idx->meta8, idx->bset[0].qc, idx->bset[0].bst, idx->dbg_inv, ids_dev,
+        k, reinterpret_cast<double2*>(q8_dev), d32_dev, d64_dev);
     LAUNCHED(idx);
     CK(cudaStreamSynchronize(s));
     return MESSI_OK;
@@ -1463,24 +1523,16 @@ extern "C" messi_status messi_debug_distances(messi_index* idx, const float* que
     if (k == 0) return MESSI_OK;
     cudaStream_t s = idx->stream;
     const int n = idx->n;
-    if (reach < 0) {
-        if ((size_t)k > idx->dbg_out4_cap) {
-            cudaFree(idx->dbg_out4);
-            idx->dbg_out4 = nullptr;
-            idx->dbg_out4_cap = 0;
-            TRY(dalloc(&idx->dbg_out4, (size_t)k));
-            idx->dbg_out4_cap = (size_t)k;
-        }
-        double* d64 = d64_dev;
-        if (!d64) TRY(dalloc(&d64, (size_t)k));
-        messi_status st = messi_debug_ed_refine(idx, query_dev, ids_dev, k, reinterpret_cast<float*>(idx->dbg_out4), d64);
-        if (st == MESSI_OK && d32_dev) {
-            k_dbg_col<<<grid_of(k, 256), 256, 0, s>>>(idx->dbg_out4, k, 2, d32_dev);
-            ++idx->launches;
-            if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
-                st = fail(MESSI_ECUDA, "k_dbg_col");
-        }
+    if (reach < 0) {  // scratch for the outputs the caller did not ask for
+        double *q8 = nullptr, *d64 = d64_dev;
+        float* d32 = d32_dev;
+        messi_status st = dalloc(&q8, 2 * (size_t)k);
+        if (st == MESSI_OK && !d64) st = dalloc(&d64, (size_t)k);
+        if (st == MESSI_OK && !d32) st = dalloc(&d32, (size_t)k);
+        if (st == MESSI_OK) st = messi_debug_ed_refine(idx, query_dev, ids_dev, k, q8, d32, d64);
+        cudaFree(q8);
         if (!d64_dev) cudaFree(d64);
+        if (!d32_dev) cudaFree(d32);
         return st;
     }
     if (d64_dev) {  // the resolve kernel's fp64 engine

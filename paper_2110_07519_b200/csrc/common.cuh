@@ -48,6 +48,12 @@ struct QState {
     unsigned char zlo[16], zhi[16];  // batch ED: per segment, the symbols whose table entry is 0
     unsigned lbk_thr_bits;  // DTW: the scan's threshold (BSF0), used by the LB_Keogh filter
     unsigned list2_back;    // DTW: LB_Keogh survivors appended from the back of list2 (larger LBK)
+    // batch ED: the query quantised like the rows ("quantised-row bound"):
+    // c_q = rint(q / s_q) in [-127, 127], s_q a power of two; q8e >= ||q - s_q c_q||;
+    // q8sum = sum c_q, q8s2ss = s_q^2 sum c_q^2 (exact in fp64); the words go to qc_all
+    float q8s;
+    int q8sum;
+    double q8e, q8s2ss;
     unsigned frozen;        // inspection only (messi_debug_dtw_stages): the DTW refine kernels keep
                             // their threshold at its start value and never lower the BSF, so every
                             // candidate runs to completion (no abandon) and reports its fp32 DTW
@@ -131,6 +137,20 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c)
         : "=f"(r.x), "=f"(r.y)
         : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
     return r;
+}
+
+// Four-way byte dot products with 32-bit accumulation (IDP.4A): exact integer arithmetic.
+__device__ __forceinline__ int dp4a_us(unsigned a, unsigned b, int c)  // a: 4 x u8, b: 4 x s8
+{
+    int d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ unsigned dp4a_uu(unsigned a, unsigned b, unsigned c)  // a, b: 4 x u8
+{
+    unsigned d;
+    asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
 }
 
 __device__ __forceinline__ float warp_sum(float v)

@@ -37,13 +37,73 @@ constexpr int kFilterQ = 2;              // queries per filter CTA
 // [zlo_s, zhi_s] of T (T[s][.] is non-increasing, zero on one run, non-decreasing: the box
 // of a symbol moves monotonically past the query mean), and locates the query's key in the
 // sorted keys (the approximate-search window, reading R14).
+// The query quantised like the rows (k_quantise's recipe): s_q the smallest power of two with
+// max |q_i| <= 127 s_q, c_q = rint(q / s_q); e_q >= ||q - s_q c_q|| (fp64 sum, sqrt inflated by
+// 2^-30 and rounded up); words qc[n/4] = 4 x s8 each.  A query that cannot be quantised (non-
+// finite values, scale outside 2^+-100) gets e_q = +inf: the quantised bound then never prunes.
+__device__ void quantise_query_block(const float* q_s, int n, unsigned* __restrict__ qc, QState* st)
+{
+    __shared__ float mx_s[32];
+    __shared__ double er_s[32];
+    __shared__ int sm_s[32], ss_s[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    float mx = 0.0f;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) mx = fmaxf(mx, fabsf(q_s[i]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) mx_s[w] = mx;
+    __syncthreads();
+    mx = mx_s[0];
+    for (int k = 1; k < nw; ++k) mx = fmaxf(mx, mx_s[k]);
+    bool usable = isfinite(mx);
+    int kq = 0;
+    if (usable && mx > 0.0f) {
+        int e;
+        const float f = frexpf(mx, &e);
+        kq = (f * 128.0f <= 127.0f) ? e - 7 : e - 6;
+        if (kq < -100 || kq > 100) usable = false;
+    }
+    const float sq = ldexpf(1.0f, kq);
+    double err = 0.0;
+    int sum = 0, ss = 0;
+    for (int wd = threadIdx.x; wd < n / 4; wd += blockDim.x) {
+        unsigned word = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float x = q_s[4 * wd + j];
+            const int c = usable ? (int)rintf(ldexpf(x, -kq)) : 0;
+            const double r = __dsub_rn((double)x, (double)c * (double)sq);
+            err = __dadd_rn(err, __dmul_rn(r, r));
+            sum += c;
+            ss += c * c;
+            word |= (unsigned)(c & 255) << (8 * j);
+        }
+        qc[wd] = word;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        err = __dadd_rn(err, __shfl_xor_sync(0xffffffffu, err, o));
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    }
+    if (lane == 0) { er_s[w] = err; sm_s[w] = sum; ss_s[w] = ss; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < nw; ++k) { err = __dadd_rn(err, er_s[k]); sum += sm_s[k]; ss += ss_s[k]; }
+        st->q8s = sq;
+        st->q8sum = sum;
+        st->q8s2ss = (double)sq * (double)sq * (double)ss;
+        st->q8e = usable ? sqrt(err) * (1.0 + 0x1p-30) : (double)INFINITY;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_prologue_batch(const float* __restrict__ queries, int n,
                                                         const float* __restrict__ beta_g, const float* __restrict__ lo_w,
                                                         const float* __restrict__ hi_w,
                                                         const unsigned long long* __restrict__ skey, long long N,
                                                         int window, float* __restrict__ lutc_all,
                                                         float* __restrict__ lutx_all, float* __restrict__ lutf_all,
-                                                        QState* st_all, KnnState* knn)
+                                                        QState* st_all, KnnState* knn, unsigned* __restrict__ qc_all)
 {
     extern __shared__ __align__(16) float q_s[];
     __shared__ unsigned long long qkey_s;
@@ -56,6 +116,7 @@ __global__ void __launch_bounds__(256) k_prologue_batch(const float* __restrict_
         if (knn) knn[b].n32 = knn[b].n64 = 0;
     }
     __syncthreads();
+    if (qc_all) quantise_query_block(q_s, n, qc_all + (size_t)b * (n / 4), st);
     float* lutc = lutc_all + (size_t)b * (MESSI_W * MESSI_CARD);
     prologue_block(q_s, n, -1, beta_g, lo_w, hi_w, lutc, lutx_all + (size_t)b * kLutX, nullptr, nullptr, &qkey_s, st);
     __syncthreads();
@@ -479,11 +540,14 @@ __device__ __forceinline__ void ed2_group(const unsigned (&id)[kRefineGroup], co
     for (int g = 0; g < kRefineGroup; ++g) acc[g] = warp_sum(acc[g]);
 }
 
+// Returns (every lane) the smallest fp32 distance this call accepted (+inf if none): the
+// caller lowers its cached threshold with it.
 template <bool LINKED, bool KNN>
-__device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __restrict__ perm,
-                           const float* __restrict__ rows, int n, const float* __restrict__ q_p, QState* st,
-                           PeerSet ps, int b, KnnState* knn, int k, int lane)
+__device__ float exact_pass(unsigned keep, unsigned my_pos, const unsigned* __restrict__ perm,
+                            const float* __restrict__ rows, int n, const float* __restrict__ q_p, QState* st,
+                            PeerSet ps, int b, KnnState* knn, int k, int lane)
 {
+    float dmin = INFINITY;
     while (keep) {
         unsigned id[kRefineGroup];
         bool ok[kRefineGroup];
@@ -530,6 +594,7 @@ __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __res
                         if (LINKED) bsf_publish(st, ps, b, acc[g]);
                         else bsf_update(st, acc[g]);
                         best_update(st, d64, (long long)id[g]);
+                        dmin = fminf(dmin, acc[g]);
                     }
                     atomicAdd(&st->near_count, 1u);
                 }
@@ -537,15 +602,17 @@ __device__ void exact_pass(unsigned keep, unsigned my_pos, const unsigned* __res
         }
         __syncwarp();
     }
+    return __shfl_sync(0xffffffffu, dmin, 0);
 }
 
-// Dynamic shared memory of k_scan_refine_ed: scan table, padded query, per-warp coarse
-// survivor lists (current + previous tile) and fine-survivor buffer (n = 256: 92.2 KB ->
-// 2 CTAs of 12 warps per SM).
+// Dynamic shared memory of k_scan_refine_ed: scan table, padded query, the quantised query
+// (n bytes), per-warp coarse survivor lists (current + previous tile) and fine-survivor
+// buffer (n = 256: 92.5 KB -> 2 CTAs of 12 warps per SM).
 __host__ __device__ inline size_t fused_qpad(int n) { return (size_t)(n + 4 * ((n + 31) / 32) + 4) & ~(size_t)3; }
 __host__ __device__ inline size_t fused_smem(int n)
 {
-    return (size_t)kLutX * 4 + fused_qpad(n) * 4 + (size_t)kFusedWarps * (2 * MESSI_TILE_ROWS * 2 + kCandBuf * 4);
+    return (size_t)kLutX * 4 + fused_qpad(n) * 4 + (size_t)n +
+           (size_t)kFusedWarps * (2 * MESSI_TILE_ROWS * 2 + kCandBuf * 4);
 }
 
 // Writes query b's result and stats (finish_query's layout) from its state.
@@ -611,87 +678,201 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// Quantised-row bound with integer dot products: the query quantised like the
+// rows (q^ = s_q c_q, e_q >= ||q - q^||, k_prologue_batch) and row x^ = s_x c_x (e_x >= ||x - x^||):
+//     ||q - x|| >= ||q^ - x^|| - e_q - e_x,
+//     ||q^ - x^||^2 = s_q^2 sum c_q^2 + s_x^2 sum c_x^2 - 2 s_q s_x sum c_q c_x,
+// the sums exact in int32 (IDP.4A over the row's bytes b = c_x + 128: sum b c_q, sum b^2, sum b),
+// the combination in fp64 with an error margin, so L below is a rigorous lower bound of ||q - x||.
+// A candidate with L > 0 and L^2 > thr cannot be the nearest neighbour; the others come back
+// (bit set) for the exact fp32 refine.  Groups of 4 lanes take one row each (8 rows per pass);
+// lane gl of a group reads the row's 16-byte chunks gl, gl + 4, ... with the query's chunk from
+// shared memory (qc_s).  DBG (inspection): dbg[src lane] = (dh2 lower bound, L).
+struct Q8Query {
+    double sq, e, s2ss;  // s_q, e_q, s_q^2 sum c_q^2
+    int sum;             // sum c_q
+};
+
+template <bool DBG = false>
+__device__ __forceinline__ unsigned q8i_bound_pass(unsigned pass, unsigned my_pos, const unsigned char* __restrict__ rows8,
+                                                   const float2* __restrict__ meta8, int n, const uint4* qc_s,
+                                                   const Q8Query& qq, float thr, int lane, double2* dbg = nullptr)
+{
+    const int g = lane >> 2, gl = lane & 3;
+    const int nch = n >> 4;
+    unsigned keep = 0;
+    while (pass) {
+        int src[8];
+        bool okj[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            okj[j] = pass != 0;
+            src[j] = okj[j] ? __ffs(pass) - 1 : 0;
+            pass &= pass - 1;
+        }
+        int ms = src[0];
+        bool ok = okj[0];
+#pragma unroll
+        for (int j = 1; j < 8; ++j)
+            if (g == j) { ms = src[j]; ok = okj[j]; }
+        const unsigned pos = __shfl_sync(0xffffffffu, my_pos, ms);
+        const uint4* row = reinterpret_cast<const uint4*>(rows8 + (long long)pos * n);
+        int dbq = 0;
+        unsigned sbb = 0, sb = 0;
+#pragma unroll 4
+        for (int c = gl; c < nch; c += 4) {
+            const uint4 w = ok ? __ldg(row + c) : make_uint4(0u, 0u, 0u, 0u);
+            const uint4 qv = qc_s[c];
+            dbq = dp4a_us(w.x, qv.x, dbq); dbq = dp4a_us(w.y, qv.y, dbq);
+            dbq = dp4a_us(w.z, qv.z, dbq); dbq = dp4a_us(w.w, qv.w, dbq);
+            sbb = dp4a_uu(w.x, w.x, sbb); sbb = dp4a_uu(w.y, w.y, sbb);
+            sbb = dp4a_uu(w.z, w.z, sbb); sbb = dp4a_uu(w.w, w.w, sbb);
+            sb = dp4a_uu(w.x, 0x01010101u, sb); sb = dp4a_uu(w.y, 0x01010101u, sb);
+            sb = dp4a_uu(w.z, 0x01010101u, sb); sb = dp4a_uu(w.w, 0x01010101u, sb);
+        }
+#pragma unroll
+        for (int o = 1; o <= 2; o <<= 1) {
+            dbq += __shfl_xor_sync(0xffffffffu, dbq, o);
+            sbb += __shfl_xor_sync(0xffffffffu, sbb, o);
+            sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        }
+        bool survives = true;
+        if (gl == 0 && ok) {
+            const float2 mt = meta8[pos];
+            const double sx = (double)mt.x;  // a power of two
+            const long long dqx = (long long)dbq - 128LL * qq.sum;                          // sum c_x c_q
+            const long long ssx = (long long)sbb - 256LL * (long long)sb + 16384LL * n;    // sum c_x^2
+            const double t2 = sx * sx * (double)ssx, t3 = 2.0 * qq.sq * sx * (double)dqx;  // exact products
+            const double d2 = (qq.s2ss + t2) - t3;
+            // two roundings of magnitude <= 2^-53 (s2ss + t2 + |t3|) each; margin 2^-50
+            const double d2lo = d2 - 0x1p-50 * (qq.s2ss + t2 + fabs(t3));
+            const double L = (d2lo > 0.0 ? sqrt(d2lo) * (1.0 - 0x1p-50) : 0.0) - (double)mt.y - qq.e;
+            survives = !(L > 0.0 && L * L * (1.0 - 0x1p-40) > (double)thr);
+            if constexpr (DBG) dbg[ms] = make_double2(d2lo, L);
+        }
+        const unsigned bits = __ballot_sync(0xffffffffu, gl == 0 && ok && survives);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (bits & (1u << (4 * j))) keep |= 1u << src[j];
+    }
+    return keep;
+}
+
 // Fine pass + refine of the coarse survivors of one tile (list surv, m entries, warp-
-// uniform).  Round 0 uses the 8-bit words the warp preloaded (w0 / pos0) one tile earlier,
-// later rounds load theirs.  Fine survivors (LB8 <= current thr) wait in the warp's buffer
-// cbuf (prefetched into L2); every full round of 32 goes through the quantised bound and
-// the exact passes.
+// uniform), against the warp's cached threshold thr (updated when the refine finds a better
+// distance).  Round 0 uses the 8-bit words the warp preloaded (w0 / pos0) one tile earlier;
+// each round loads the next round's words before evaluating its own.  Fine survivors
+// (LB8 <= thr) wait in the warp's buffer cbuf (prefetched into L2); every full round of 32
+// goes through the quantised bound and the exact passes.
 struct WarpCounts { unsigned tiles, coarse, cand, exact; };
 
+struct FusedCtx {
+    const uint4* sym8;
+    const unsigned char* rows8;
+    const float2* meta8;
+    const unsigned* perm;
+    const float* rows;
+    const float* q_p;
+    const uint4* qc_s;
+    const char* lbase;
+    QState* st;
+    KnnState* knn;
+    PeerSet ps;
+    Q8Query qq;
+    int n, b, k;
+};
+
 template <bool LINKED, bool KNN>
-__device__ __forceinline__ void fine_and_refine(long long tile, int m, const unsigned short* surv, uint4 w0, unsigned pos0,
-                                                const uint4* __restrict__ sym8, const char* lbase, unsigned* cbuf,
-                                                unsigned& ncb, const unsigned char* __restrict__ rows8,
-                                                const float2* __restrict__ meta8, int n, const float* q_p,
-                                                float one_minus_delta, const unsigned* __restrict__ perm,
-                                                const float* __restrict__ rows, QState* st, PeerSet ps, int b,
-                                                KnnState* knn, int k, WarpCounts& wc, int lane)
+__device__ __forceinline__ void refine_round(const FusedCtx& cx, unsigned cp, unsigned pass, float& thr,
+                                             WarpCounts& wc, int lane)
 {
+    const unsigned keep = q8i_bound_pass(pass, cp, cx.rows8, cx.meta8, cx.n, cx.qc_s, cx.qq, thr, lane);
+    wc.exact += __popc(keep);
+    if (keep) thr = fminf(thr, slack_up(exact_pass<LINKED, KNN>(keep, cp, cx.perm, cx.rows, cx.n, cx.q_p, cx.st,
+                                                                   cx.ps, cx.b, cx.knn, cx.k, lane)));
+}
+
+template <bool LINKED, bool KNN>
+__device__ __forceinline__ void fine_and_refine(const FusedCtx& cx, long long tile, int m, const unsigned short* surv,
+                                                uint4 w0, unsigned pos0, unsigned* cbuf, unsigned& ncb, float& thr,
+                                                WarpCounts& wc, int lane)
+{
+    unsigned pos = pos0;
+    uint4 w = w0;
     for (int i0 = 0; i0 < m; i0 += 32) {
         const bool v = i0 + lane < m;
-        unsigned pos = pos0;
-        uint4 w = w0;
-        if (i0 > 0) {
-            pos = v ? (unsigned)(tile * MESSI_TILE_ROWS + surv[i0 + lane]) : 0u;
-            if (v) w = sym8[pos];
+        // the next round's words, loaded before this round's bounds
+        unsigned pos_n = 0;
+        uint4 w_n = make_uint4(0u, 0u, 0u, 0u);
+        if (i0 + 32 < m) {
+            const bool vn = i0 + 32 + lane < m;
+            pos_n = vn ? (unsigned)(tile * MESSI_TILE_ROWS + surv[i0 + 32 + lane]) : 0u;
+            if (vn) w_n = cx.sym8[pos_n];
         }
         float lb = INFINITY;
-        if (v) lb = fine_lb(w, lbase, lane);
-        const bool ok = v && lb <= slack_up(ld_bsf_l<LINKED>(st, ps.epoch));
+        if (v) lb = fine_lb(w, cx.lbase, lane);
+        const bool ok = v && lb <= thr;
         const unsigned pass = __ballot_sync(0xffffffffu, ok);
-        if (!pass) continue;
-        if (ok) {
-            cbuf[ncb + __popc(pass & ((1u << lane) - 1))] = pos;
-            prefetch_l2_bulk(rows8 + (long long)pos * n, (unsigned)n);
-        }
-        ncb += __popc(pass);
-        wc.cand += __popc(pass);
-        __syncwarp();
-        if (ncb >= 32) {
-            const unsigned cp = cbuf[lane];
-            const unsigned rest = ncb - 32 > (unsigned)lane ? cbuf[32 + lane] : 0u;
+        if (pass) {
+            if (ok) {
+                cbuf[ncb + __popc(pass & ((1u << lane) - 1))] = pos;
+                prefetch_l2_bulk(cx.rows8 + (long long)pos * cx.n, (unsigned)cx.n);
+            }
+            ncb += __popc(pass);
+            wc.cand += __popc(pass);
             __syncwarp();
-            if (ncb - 32 > (unsigned)lane) cbuf[lane] = rest;
-            ncb -= 32;
-            __syncwarp();
-            const unsigned keep =
-                q8_bound_pass<LINKED>(0xffffffffu, cp, rows8, meta8, n, q_p, one_minus_delta, st, ps.epoch, lane);
-            wc.exact += __popc(keep);
-            exact_pass<LINKED, KNN>(keep, cp, perm, rows, n, q_p, st, ps, b, knn, k, lane);
+            if (ncb >= 32) {
+                const unsigned cp = cbuf[lane];
+                const unsigned rest = ncb - 32 > (unsigned)lane ? cbuf[32 + lane] : 0u;
+                __syncwarp();
+                if (ncb - 32 > (unsigned)lane) cbuf[lane] = rest;
+                ncb -= 32;
+                __syncwarp();
+                refine_round<LINKED, KNN>(cx, cp, 0xffffffffu, thr, wc, lane);
+            }
         }
+        pos = pos_n;
+        w = w_n;
     }
 }
 
 // Persistent.  CTA j starts at query j mod B and walks the batch's queries cyclically once;
-// at a query with listed tiles left it loads the query's scan table and padded query into
-// shared memory, then its warps take pairs of tiles from the query's list with one
-// atomicAdd (claimed one pair ahead; the next tiles are bulk-prefetched into L2), re-check
-// each tile's box bound against the CURRENT BSF (Alg. 7's node pruning), run the coarse
-// pass of the tile (A5), and the fine pass + refine of the PREVIOUS tile's coarse survivors
-// (whose 8-bit words were loaded before this tile's coarse pass, hiding the gather), as
-// Alg. 9's workers do.  When a query's list runs dry the CTA joins the next
-// one: light queries finish early and their CTAs help the heavy ones.  k_finalise_batch
-// writes the results.  KNN = true adds the warp-cooperative k-NN insert (k > 16).
+// at a query with listed tiles left it loads the query's scan table, padded query and
+// quantised query into shared memory, then its warps take pairs of tiles from the query's
+// list (Alg. 9's Fetch&Inc chunks), re-check each tile's box bound against the best-so-far
+// (Alg. 7's node pruning), run the coarse pass of the tile (A5), and the fine pass + refine of
+// the PREVIOUS tile's coarse survivors (whose 8-bit words were loaded before this tile's
+// coarse pass, hiding the gather), as Alg. 9's workers do.
+// Software pipeline per warp, one pair ahead: while pair i is processed, lane 0 has already
+// claimed pair i + 2 (atomicAdd), read the best-so-far and loaded pair i + 1's list entries,
+// and, after pair i's first tile, bulk-prefetches pair i + 1's tiles into L2.  The warp's
+// threshold is the best-so-far read one pair earlier (a stale, i.e. larger, value is a valid
+// threshold: it only prunes less), lowered at once by the distances the warp itself accepts.
+// When a query's list runs dry the CTA joins the next one: light queries finish early and
+// their CTAs help the heavy ones.  k_finalise_batch writes the results.  KNN = true adds the
+// warp-cooperative k-NN insert (k > 16).
 template <bool LINKED, bool KNN>
 __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
     const uint4* __restrict__ tiles, const uint4* __restrict__ sym8, long long ntiles, long long N, int n,
     const float* __restrict__ queries, const float* __restrict__ lutx_all, const uint2* __restrict__ tlist_all,
-    QState* st_all, int B,
-    const unsigned char* __restrict__ rows8, const float2* __restrict__ meta8, float one_minus_delta,
-    const unsigned* __restrict__ perm, const float* __restrict__ rows, PeerSet ps, KnnState* knn_arg, int k_arg)
+    QState* st_all, int B, const unsigned char* __restrict__ rows8, const float2* __restrict__ meta8,
+    const unsigned* __restrict__ qc_all, const unsigned* __restrict__ perm, const float* __restrict__ rows, PeerSet ps,
+    KnnState* knn_arg, int k_arg)
 {
-    KnnState* const knn = knn_arg;
-    const int k = k_arg;
     extern __shared__ __align__(16) float smem[];
     float* lut_s = smem;
     float* q_p = lut_s + kLutX;
-    unsigned short* surv_all = reinterpret_cast<unsigned short*>(q_p + fused_qpad(n));
+    unsigned* qc_w = reinterpret_cast<unsigned*>(q_p + fused_qpad(n));
+    unsigned short* surv_all = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(qc_w) + n);
     unsigned* cbuf_all = reinterpret_cast<unsigned*>(surv_all + kFusedWarps * 2 * MESSI_TILE_ROWS);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned short* survb = surv_all + warp * 2 * MESSI_TILE_ROWS;  // two lists: current / previous tile
     unsigned* cbuf = cbuf_all + warp * kCandBuf;
     __shared__ int s_has;
-    const char* lbase = reinterpret_cast<const char*>(lut_s);
+    FusedCtx cx;
+    cx.sym8 = sym8; cx.rows8 = rows8; cx.meta8 = meta8; cx.perm = perm; cx.rows = rows; cx.q_p = q_p;
+    cx.qc_s = reinterpret_cast<const uint4*>(qc_w); cx.lbase = reinterpret_cast<const char*>(lut_s);
+    cx.knn = knn_arg; cx.ps = ps; cx.n = n; cx.k = k_arg;
     int b = (int)(blockIdx.x % (unsigned)B);
     for (int visited = 0; visited < B; ++visited, b = (b + 1 == B ? 0 : b + 1)) {
         QState* st = st_all + b;
@@ -707,50 +888,71 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
             for (int i = threadIdx.x; i < kLutX / 4; i += blockDim.x) reinterpret_cast<float4*>(lut_s)[i] = src[i];
             const float* q = queries + (size_t)b * n;
             for (int i = threadIdx.x; i < n; i += blockDim.x) q_p[i + 4 * (i >> 5)] = q[i];
+            const unsigned* qc = qc_all + (size_t)b * (n / 4);
+            for (int i = threadIdx.x; i < n / 4; i += blockDim.x) qc_w[i] = qc[i];
         }
+        cx.st = st;
+        cx.b = b;
+        cx.qq.sq = (double)st->q8s;
+        cx.qq.e = st->q8e;
+        cx.qq.s2ss = st->q8s2ss;
+        cx.qq.sum = st->q8sum;
         __syncthreads();
         const uint2* tl = tlist_all + (size_t)b * ntiles;
+        // list position of claim k: the front bin, then the back bin from its far end
+        auto at = [&](unsigned kk) { return tl[kk < c0 ? kk : (unsigned)ntiles - 1u - (kk - c0)]; };
         WarpCounts wc{0, 0, 0, 0};
         unsigned ncb = 0;        // fine survivors pending in cbuf (warp-uniform)
         int pm = 0, cur = 0;     // previous tile's coarse survivors (list survb[cur ^ 1])
         long long ptile = 0;
         uint4 pw = make_uint4(0, 0, 0, 0);
         unsigned ppos = 0;
-        unsigned k_next = 0;
-        if (lane == 0) k_next = atomicAdd(&st->next_tile, 1u) * 2u;
-        k_next = __shfl_sync(0xffffffffu, k_next, 0);
-        while (k_next < count) {
-            const unsigned k0 = k_next;
-            // list position of claim k: the front bin, then the back bin from its far end
-            auto at = [&](unsigned k) { return tl[k < c0 ? k : (unsigned)ntiles - 1u - (k - c0)]; };
-            const uint2 te0 = at(k0);
-            const uint2 te1 = k0 + 1 < count ? at(k0 + 1) : make_uint2(0u, 0u);
-            // claim the following pair now and prefetch its tiles into L2
+        // pipeline start: claims of pairs 0 and 1, the first threshold, pair 0's entries
+        unsigned kc = 0, kn = 0;
+        float thr = 0.0f;
+        if (lane == 0) {
+            kc = atomicAdd(&st->next_tile, 1u) * 2u;
+            kn = atomicAdd(&st->next_tile, 1u) * 2u;
+            thr = slack_up(ld_bsf_l<LINKED>(st, ps.epoch));
+        }
+        kc = __shfl_sync(0xffffffffu, kc, 0);
+        kn = __shfl_sync(0xffffffffu, kn, 0);
+        thr = __shfl_sync(0xffffffffu, thr, 0);
+        uint2 te0 = kc < count ? at(kc) : make_uint2(0u, 0x7f800000u);
+        uint2 te1 = kc + 1 < count ? at(kc + 1) : make_uint2(0u, 0x7f800000u);
+        while (kc < count) {
+            // lane 0: claim pair i + 2, read the best-so-far, load pair i + 1's entries (used later)
+            unsigned k2 = 0;
+            float thr_n = 0.0f;
+            uint2 ne0 = make_uint2(0u, 0x7f800000u), ne1 = make_uint2(0u, 0x7f800000u);
             if (lane == 0) {
-                k_next = atomicAdd(&st->next_tile, 1u) * 2u;
-                const float pthr = slack_up(ld_bsf_l<LINKED>(st, ps.epoch));
-                for (unsigned kk = k_next; kk < min(k_next + 2u, count); ++kk) {
-                    const uint2 tn = at(kk);
-                    if (__uint_as_float(tn.y) <= pthr)  // not already box-pruned
-                        prefetch_l2_bulk(tiles + (long long)tn.x * (MESSI_TILE_BYTES / 16), MESSI_TILE_BYTES);
+                if (kn < count) {
+                    k2 = atomicAdd(&st->next_tile, 1u) * 2u;
+                    ne0 = at(kn);
+                    if (kn + 1 < count) ne1 = at(kn + 1);
+                } else {
+                    k2 = kn;
                 }
+                thr_n = slack_up(ld_bsf_l<LINKED>(st, ps.epoch));
             }
-            k_next = __shfl_sync(0xffffffffu, k_next, 0);
 #pragma unroll 1
             for (int u = 0; u < 2; ++u) {
-                if (k0 + u >= count) break;
+                if (u == 1 && lane == 0) {  // pair i + 1's tiles into L2, unless already box-pruned
+                    if (__uint_as_float(ne0.y) <= thr_n)
+                        prefetch_l2_bulk(tiles + (long long)ne0.x * (MESSI_TILE_BYTES / 16), MESSI_TILE_BYTES);
+                    if (__uint_as_float(ne1.y) <= thr_n)
+                        prefetch_l2_bulk(tiles + (long long)ne1.x * (MESSI_TILE_BYTES / 16), MESSI_TILE_BYTES);
+                }
                 const uint2 te = u == 0 ? te0 : te1;
-                // warp-uniform decision: lane 0's reading of the BSF
-                const float bthr = __shfl_sync(0xffffffffu, slack_up(ld_bsf_l<LINKED>(st, ps.epoch)), 0);
-                if (__uint_as_float(te.y) > bthr) continue;  // box pruned by the current BSF
+                if (kc + u >= count || __uint_as_float(te.y) > thr) continue;  // box pruned (warp-uniform)
                 ++wc.tiles;
                 const long long tile = te.x;
                 unsigned short* surv = survb + cur * MESSI_TILE_ROWS;
-                const int m = scan_tile_coarse(tiles, tile, lbase, slack_up(ld_bsf_l<LINKED>(st, ps.epoch)), N, surv, lane);
+                const int m = scan_tile_coarse(tiles, tile, cx.lbase, thr, N, surv, lane);
                 wc.coarse += m;
                 if (pm)
-                    fine_and_refine<LINKED, KNN>(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb,
-                                    rows8, meta8, n, q_p, one_minus_delta, perm, rows, st, ps, b, knn, k, wc, lane);
+                    fine_and_refine<LINKED, KNN>(cx, ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, cbuf, ncb,
+                                                 thr, wc, lane);
                 // preload the 8-bit words of this tile's first 32 coarse survivors
                 ppos = lane < m ? (unsigned)(tile * MESSI_TILE_ROWS + surv[lane]) : 0u;
                 pw = lane < m ? sym8[ppos] : make_uint4(0, 0, 0, 0);
@@ -758,18 +960,21 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
                 ptile = tile;
                 cur ^= 1;
             }
+            // advance the pipeline
+            kc = kn;
+            kn = __shfl_sync(0xffffffffu, k2, 0);
+            thr = fminf(thr, __shfl_sync(0xffffffffu, thr_n, 0));
+            te0 = make_uint2(__shfl_sync(0xffffffffu, ne0.x, 0), __shfl_sync(0xffffffffu, ne0.y, 0));
+            te1 = make_uint2(__shfl_sync(0xffffffffu, ne1.x, 0), __shfl_sync(0xffffffffu, ne1.y, 0));
         }
         if (pm)
-            fine_and_refine<LINKED, KNN>(ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, sym8, lbase, cbuf, ncb, rows8,
-                            meta8, n, q_p, one_minus_delta, perm, rows, st, ps, b, knn, k, wc, lane);
+            fine_and_refine<LINKED, KNN>(cx, ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, cbuf, ncb, thr,
+                                         wc, lane);
         if (ncb) {  // the query's last fine survivors
             const unsigned cp = (unsigned)lane < ncb ? cbuf[lane] : 0u;
             const unsigned pass = ncb >= 32 ? 0xffffffffu : (1u << ncb) - 1u;
             __syncwarp();
-            const unsigned keep =
-                q8_bound_pass<LINKED>(pass, cp, rows8, meta8, n, q_p, one_minus_delta, st, ps.epoch, lane);
-            wc.exact += __popc(keep);
-            exact_pass<LINKED, KNN>(keep, cp, perm, rows, n, q_p, st, ps, b, knn, k, lane);
+            refine_round<LINKED, KNN>(cx, cp, pass, thr, wc, lane);
             ncb = 0;
         }
         if (lane == 0) {
@@ -785,29 +990,40 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
 
 // ------------------------------------------------------------------------ inspection
 // Inspection of the ED refine (messi_debug_ed_refine): for `k` local row ids, one warp per 32
-// of them, the query path's own device code -- q8_bound_pass (quantised-row fp32 distance dh2
-// and its lower bound L of ||q - x||), ed2_group (the exact pass's fp32 squared ED) and
-// ed2_exact_g (the fp64 re-rank) -- with the threshold at +inf (st armed), nothing pruned.
-// inv: sorted position of every row (the inverse of perm).  out4[t] = (dh2, L, d32, 0).
+// of them, the query path's own device code -- q8i_bound_pass (the lower bound dh2 of the
+// squared distance between the quantised query and row, and L, its lower bound of ||q - x||),
+// ed2_group (the exact pass's fp32 squared ED) and ed2_exact_g (the fp64 re-rank) -- nothing
+// pruned.  The quantised query and its parameters come from query 0 of a batch set
+// (k_prologue_batch).  inv: sorted position of every row (the inverse of perm).
 __global__ void __launch_bounds__(256) k_debug_ed_refine(const float* __restrict__ rows, int n,
                                                          const float* __restrict__ q_g,
                                                          const unsigned char* __restrict__ rows8,
-                                                         const float2* __restrict__ meta8, float one_minus_delta,
-                                                         const unsigned* __restrict__ inv, QState* st,
+                                                         const float2* __restrict__ meta8,
+                                                         const unsigned* __restrict__ qc_g, const QState* qst,
+                                                         const unsigned* __restrict__ inv,
                                                          const unsigned* __restrict__ ids, int k,
-                                                         float4* __restrict__ out4, double* __restrict__ d64)
+                                                         double2* __restrict__ q8out, float* __restrict__ d32,
+                                                         double* __restrict__ d64)
 {
     extern __shared__ __align__(16) float q_p[];
-    __shared__ float2 dbg_s[8][32];
+    __shared__ double2 dbg_s[8][32];
+    unsigned* qc_w = reinterpret_cast<unsigned*>(q_p + fused_qpad(n));
     for (int i = threadIdx.x; i < n; i += blockDim.x) q_p[i + 4 * (i >> 5)] = q_g[i];
+    for (int i = threadIdx.x; i < n / 4; i += blockDim.x) qc_w[i] = qc_g[i];
     __syncthreads();
+    Q8Query qq;
+    qq.sq = (double)qst->q8s;
+    qq.e = qst->q8e;
+    qq.s2ss = qst->q8s2ss;
+    qq.sum = qst->q8sum;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     for (int t0 = (blockIdx.x * wpb + w) * 32; t0 < k; t0 += gridDim.x * wpb * 32) {
         const bool v = t0 + lane < k;
         const unsigned id = v ? ids[t0 + lane] : 0u;
         const unsigned pos = v ? inv[id] : 0u;
         const unsigned mask = __ballot_sync(0xffffffffu, v);
-        q8_bound_pass<false, true>(mask, pos, rows8, meta8, n, q_p, one_minus_delta, st, 0u, lane, dbg_s[w]);
+        q8i_bound_pass<true>(mask, pos, rows8, meta8, n, reinterpret_cast<const uint4*>(qc_w), qq, INFINITY, lane,
+                             dbg_s[w]);
         __syncwarp();
         float mine = 0.0f;
         unsigned rest = mask;
@@ -829,8 +1045,8 @@ __global__ void __launch_bounds__(256) k_debug_ed_refine(const float* __restrict
                 if (ok[g] && lane == src[g]) mine = acc[g];
         }
         if (v) {
-            const float2 qd = dbg_s[w][lane];
-            out4[t0 + lane] = make_float4(qd.x, qd.y, mine, 0.0f);
+            q8out[t0 + lane] = dbg_s[w][lane];
+            d32[t0 + lane] = mine;
             d64[t0 + lane] = ed2_exact_g(q_p, rows + (long long)id * n, n);
         }
         __syncwarp();

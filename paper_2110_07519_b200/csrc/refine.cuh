@@ -37,109 +37,46 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 // Rows in flight per warp in the fp32 distance loops (four 1 KB rows at n = 256).
 constexpr int kRefineGroup = 4;
 
-// Quantised-row bound (DESIGN.md §5/§7): for the candidates of `pass` (lane bit = candidate
-// held by that lane at sorted position my_pos), the fp32 squared distance dh2 between the
-// query and the dequantised row s*c (n bytes from rows8, biased by 128) gives
-//     ||q - x|| >= ||q - s c|| - e >= sqrt_rd(dh2) * (1 - delta) - e   (= L),
-// delta bounding the relative fp32 error of sqrt(dh2) (s*c exact: s is a power of two).  A
-// candidate with L > 0 and L^2 > thr cannot be the nearest neighbour; the others are
-// returned (bit set) for the exact fp32 refine.  Groups of 8 lanes take one row each, two
-// rows per group in flight (8 rows = 8n bytes per warp); lane gl of a group reads the 16 B
-// chunks gl, gl+8, ... of its rows; the query comes from q_p, a padded copy (element i at
-// i + 4 (i >> 5)).  Bytes convert exactly with the 2^23 trick:
-// float(0x4B000000 | b) = 2^23 + b.
-// L = sqrt_rd(dh2) * (1 - delta) - e, rounded down: the quantised-row lower bound of ||q - x||.
-__device__ __forceinline__ float q8_lower(float dh2, float e, float one_minus_delta)
-{
-    return __fsub_rd(__fmul_rd(__fsqrt_rd(dh2), one_minus_delta), e);
-}
-
-// DBG (inspection, messi_debug_ed_refine): also writes dbg[src lane] = (dh2, L) of every
-// candidate -- the same instructions as the query path, plus two stores.
-template <bool LINKED, bool DBG = false>
-__device__ __forceinline__ unsigned q8_bound_pass(unsigned pass, unsigned my_pos, const unsigned char* __restrict__ rows8,
-                                                  const float2* __restrict__ meta8, int n, const float* __restrict__ q_p,
-                                                  float one_minus_delta, QState* st, unsigned epoch, int lane,
-                                                  float2* dbg = nullptr)
-{
-    const int g = lane >> 3, gl = lane & 7;
-    unsigned keep = 0;
-    while (pass) {
-        int src[8];
-        bool ok[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            ok[j] = pass != 0;
-            src[j] = ok[j] ? __ffs(pass) - 1 : 0;
-            pass &= pass - 1;
-        }
-        // this group's two rows: slots g and g + 4
-        const int sa = g == 0 ? src[0] : g == 1 ? src[1] : g == 2 ? src[2] : src[3];
-        const int sb = g == 0 ? src[4] : g == 1 ? src[5] : g == 2 ? src[6] : src[7];
-        const bool oa = g == 0 ? ok[0] : g == 1 ? ok[1] : g == 2 ? ok[2] : ok[3];
-        const bool ob = g == 0 ? ok[4] : g == 1 ? ok[5] : g == 2 ? ok[6] : ok[7];
-        const unsigned pa = __shfl_sync(0xffffffffu, my_pos, sa);
-        const unsigned pb = __shfl_sync(0xffffffffu, my_pos, sb);
-        const float2 ma = oa ? meta8[pa] : make_float2(0.0f, 0.0f);
-        const float2 mb = ob ? meta8[pb] : make_float2(0.0f, 0.0f);
-        const unsigned char* ra = rows8 + (long long)pa * n;
-        const unsigned char* rb = rows8 + (long long)pb * n;
-        // paired fp32 (FADD2 / FFMA2): bytes (0,1) and (2,3) of every word in one op each
-        float2 qsa = make_float2(0.0f, 0.0f), qsb = make_float2(0.0f, 0.0f);
-        const float2 nsa = make_float2(-ma.x, -ma.x), nsb = make_float2(-mb.x, -mb.x);
-        const float2 bias = make_float2(-8388736.0f, -8388736.0f);  // - (2^23 + 128)
-        for (int c = gl * 16; c < n; c += 128) {
-            const uint4 wa = oa ? __ldg(reinterpret_cast<const uint4*>(ra + c)) : make_uint4(0, 0, 0, 0);
-            const uint4 wb = ob ? __ldg(reinterpret_cast<const uint4*>(rb + c)) : make_uint4(0, 0, 0, 0);
-            const unsigned xa[4] = {wa.x, wa.y, wa.z, wa.w}, xb[4] = {wb.x, wb.y, wb.z, wb.w};
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                // q_p: element i at i + 4 (i >> 5) -- the eight lanes of a group then read
-                // 8 x 16 B from 32 distinct banks
-                const float4 qv = *reinterpret_cast<const float4*>(q_p + c + 4 * w + 4 * (c >> 5));
-#pragma unroll
-                for (int b = 0; b < 4; b += 2) {
-                    // byte b of x, then 0x4B000000's bytes: float(2^23 + byte)
-                    const unsigned s0 = 0x7650u | (unsigned)b, s1 = 0x7650u | (unsigned)(b + 1);
-                    const float2 qq = b == 0 ? make_float2(qv.x, qv.y) : make_float2(qv.z, qv.w);
-                    const float2 ca = fadd2(make_float2(__uint_as_float(__byte_perm(xa[w], 0x4B000000u, s0)),
-                                                        __uint_as_float(__byte_perm(xa[w], 0x4B000000u, s1))), bias);
-                    const float2 cb = fadd2(make_float2(__uint_as_float(__byte_perm(xb[w], 0x4B000000u, s0)),
-                                                        __uint_as_float(__byte_perm(xb[w], 0x4B000000u, s1))), bias);
-                    const float2 da = ffma2(nsa, ca, qq);
-                    const float2 db = ffma2(nsb, cb, qq);
-                    qsa = ffma2(da, da, qsa);
-                    qsb = ffma2(db, db, qsb);
-                }
-            }
-        }
-        float acc_a = qsa.x + qsa.y, acc_b = qsb.x + qsb.y;
-#pragma unroll
-        for (int o = 4; o; o >>= 1) {
-            acc_a += __shfl_xor_sync(0xffffffffu, acc_a, o);
-            acc_b += __shfl_xor_sync(0xffffffffu, acc_b, o);
-        }
-        const float thr = slack_up(ld_bsf_l<LINKED>(st, epoch));
-        const float La = q8_lower(acc_a, ma.y, one_minus_delta), Lb = q8_lower(acc_b, mb.y, one_minus_delta);
-        const bool ka = oa && !(La > 0.0f && __fmul_rd(La, La) > thr);
-        const bool kb = ob && !(Lb > 0.0f && __fmul_rd(Lb, Lb) > thr);
-        if constexpr (DBG) {
-            if (gl == 0 && oa) dbg[sa] = make_float2(acc_a, La);
-            if (gl == 0 && ob) dbg[sb] = make_float2(acc_b, Lb);
-        }
-        // lane gl == 0 of each group reports; collect the source-lane bits
-        const unsigned ba = __ballot_sync(0xffffffffu, gl == 0 && ka);
-        const unsigned bb = __ballot_sync(0xffffffffu, gl == 0 && kb);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (ba & (1u << (8 * j))) keep |= 1u << src[j];
-            if (bb & (1u << (8 * j))) keep |= 1u << src[j + 4];
-        }
-    }
-    return keep;
-}
-
 struct Best { double d; long long id; };
+
+// DTW k-NN (the paper's k-NN: the BSF becomes the k-th best distance): a refined
+// candidate's fp32 distance into the query's list of the k smallest fp32 distances so far,
+// under the query's lock (one thread; completions within the threshold are rare).  Once the
+// list holds k distances its k-th is a distance k distinct rows achieve -- a valid threshold
+// for the k-th neighbour -- and lowers the BSF.
+__device__ __noinline__ void knn32_insert(QState* st, KnnState* kn, int k, float d)
+{
+    while (atomicCAS(&st->lock, 0u, 1u) != 0u) __nanosleep(32);
+    __threadfence();
+    volatile KnnState* v = kn;
+    int cnt = v->n32;
+    if (cnt < k || d < v->d32[k - 1]) {
+        int i = cnt < k ? cnt : k - 1;
+        while (i > 0 && v->d32[i - 1] > d) { v->d32[i] = v->d32[i - 1]; --i; }
+        v->d32[i] = d;
+        if (cnt < k) v->n32 = ++cnt;
+    }
+    const float kth = cnt == k ? v->d32[k - 1] : -1.0f;
+    __threadfence();
+    atomicExch(&st->lock, 0u);
+    if (kth >= 0.0f) bsf_update(st, kth);
+}
+
+// The refine's acceptance of a completed candidate at fp32 distance d <= thr: the near-best
+// list, and (unless inspecting, frozen) the BSF -- 1-NN: d itself (the thread's own threshold
+// drops with it); k-NN: the k-th of the list.
+__device__ __forceinline__ void dtw_accept(QState* st, NearEntry* near, KnnState* knn, int kk, bool frozen,
+                                           unsigned id, float d, float& thr)
+{
+    append_near(st, near, id, d);
+    if (frozen) return;
+    if (knn) {
+        knn32_insert(st, knn, kk, d);
+    } else {
+        bsf_update(st, d);
+        thr = fminf(thr, slack_up(d));
+    }
+}
 
 // DTW step 1 (Alg. 10 line LB_Keogh): the scan's candidates (sorted position,
 // envelope-PAA bound) whose bound still does not exceed the BSF get the raw LB_Keogh
@@ -398,7 +335,7 @@ template <int R>
 __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
                                                     const float* __restrict__ U_g, const float* __restrict__ L_g,
                                                     const uint4* __restrict__ list2, unsigned cap, QState* st,
-                                                    NearEntry* near)
+                                                    NearEntry* near, KnnState* knn, int kk)
 {
     extern __shared__ __align__(16) float dsm[];
     const int npad = (n + 3) & ~3;
@@ -470,13 +407,7 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
                 running = false;
                 cells += band_cells(n, R, n);
                 const float d = dp.result();
-                if (d <= thr) {
-                    append_near(st, near, id, d);
-                    if (!frozen) {
-                        bsf_update(st, d);
-                        thr = fminf(thr, slack_up(d));
-                    }
-                }
+                if (d <= thr) dtw_accept(st, near, knn, kk, frozen, id, d, thr);
             }
         }
     }
@@ -520,7 +451,7 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
                                                                    const float* __restrict__ U_g,
                                                                    const float* __restrict__ L_g,
                                                                    const uint4* __restrict__ list2, unsigned cap,
-                                                                   QState* st, NearEntry* near)
+                                                                   QState* st, NearEntry* near, KnnState* knn, int kk)
 {
     extern __shared__ __align__(16) float dsm[];
     const int npad = (n + 3) & ~3;
@@ -629,13 +560,7 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
                 running = false;
                 cells += band_cells(n, R, n);
                 const float d = Bt[R * T];  // D(n-1, n-1): column n-1 of the last row
-                if (d <= thr) {
-                    append_near(st, near, id, d);
-                    if (!frozen) {
-                        bsf_update(st, d);
-                        thr = fminf(thr, slack_up(d));
-                    }
-                }
+                if (d <= thr) dtw_accept(st, near, knn, kk, frozen, id, d, thr);
             }
         }
     }
@@ -661,7 +586,8 @@ __device__ __forceinline__ void stage_row(float* dst, const float* __restrict__ 
 // fp32 anti-diagonal wavefront (dtw_warp<float>) over the row staged in shared memory.
 // Per-warp shared memory: n floats of row + 3n floats of anti-diagonals.
 __global__ void k_refine_dtw_warp(const float* __restrict__ rows, int n, int reach, const float* __restrict__ q_g,
-                                  const uint4* __restrict__ list2, unsigned cap, QState* st, NearEntry* near)
+                                  const uint4* __restrict__ list2, unsigned cap, QState* st, NearEntry* near,
+                                  KnnState* knn, int kk)
 {
     extern __shared__ __align__(16) float dsm[];
     const int npad = (n + 3) & ~3;
@@ -679,11 +605,9 @@ __global__ void k_refine_dtw_warp(const float* __restrict__ rows, int n, int rea
         stage_row(c_s, rows + (long long)id * n, n, lane);
         const float d = dtw_warp_any<float>(q_s, c_s, n, reach, buf, lane);
         ++refined;
-        const float thr = slack_up(ld_bsf(st));
-        if (lane == 0 && d <= thr) {
-            if (!*(volatile const unsigned*)&st->frozen) bsf_update(st, d);
-            append_near(st, near, id, d);
-        }
+        float thr = slack_up(ld_bsf(st));
+        if (lane == 0 && d <= thr)
+            dtw_accept(st, near, knn, kk, *(volatile const unsigned*)&st->frozen != 0u, id, d, thr);
     }
     if (lane == 0 && refined) {
         atomicAdd(&st->refined, refined);
@@ -792,7 +716,92 @@ __global__ void k_resolve_dtw(const float* __restrict__ rows, int n, int reach, 
     if (threadIdx.x == 0) finish_query(b, (unsigned)cnt, st, N, row_begin, result, stats);
 }
 
+// DTW k-NN exact resolution: every near-best entry with d32 <= BSF_final * (1 + eps) (BSF =
+// the k-th smallest fp32 distance) is recomputed in fp64 (warp wavefront, as k_resolve_dtw)
+// into scratch (d64, id) pairs; then k rounds of a block-wide lexicographic argmin, each over
+// the pairs strictly greater than the previous pick (ids are distinct), give the k smallest
+// (d64, id) in order: results[k] (fewer rows -> (inf, -1)), stats, and the slot is re-armed.
+// Same per-warp memory layout as k_resolve_dtw.
+__global__ void k_resolve_dtw_knn(const float* __restrict__ rows, int n, int reach, const float* __restrict__ q_g,
+                                  const NearEntry* __restrict__ near, QState* st, long long N, long long row_begin,
+                                  void* result, void* stats, double* gbuf, double2* __restrict__ scratch, int kk)
+{
+    extern __shared__ __align__(16) double dbuf[];
+    __shared__ unsigned cnt_s;
+    __shared__ double rd[MESSI_MAX_K];
+    __shared__ long long ri[MESSI_MAX_K];
+    __shared__ double wd[32];
+    __shared__ long long wi[32];
+    const int npad = (n + 3) & ~3;
+    const float thr = slack_up(ld_bsf(st));
+    const unsigned total = *(volatile unsigned*)&st->near_count;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    if (threadIdx.x == 0) cnt_s = 0;
+    __syncthreads();
+    char* mine = reinterpret_cast<char*>(dbuf) + (size_t)w * resolve_warp_bytes(n, reach, gbuf != nullptr);
+    float* qc = reinterpret_cast<float*>(mine);
+    double* buf = gbuf ? gbuf + (size_t)w * 3 * n : reinterpret_cast<double*>(mine + 2 * (size_t)npad * sizeof(float));
+    for (int i = lane; i < n; i += 32) qc[i] = q_g[i];
+    for (unsigned k = w; k < total; k += wpb) {
+        const NearEntry e = near[k];
+        if (!(e.d32 <= thr)) continue;
+        stage_row(qc + npad, rows + (long long)e.id * n, n, lane);
+        const double d = dtw_warp_any<double>(qc, qc + npad, n, reach, buf, lane);
+        if (lane == 0) scratch[atomicAdd(&cnt_s, 1u)] = make_double2(d, __longlong_as_double((long long)e.id));
+    }
+    for (int r = threadIdx.x; r < kk; r += blockDim.x) { rd[r] = (double)INFINITY; ri[r] = -1; }
+    __syncthreads();
+    const unsigned cnt = cnt_s;
+    double pd = -1.0;
+    long long pi = -1;
+    for (int r = 0; r < kk && r < (int)cnt; ++r) {
+        double bd = (double)INFINITY;
+        long long bi = -1;
+        for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const double2 e = scratch[i];
+            const long long id = __double_as_longlong(e.y);
+            const bool after = e.x > pd || (e.x == pd && id > pi);
+            if (after && (e.x < bd || (e.x == bd && (bi < 0 || id < bi)))) { bd = e.x; bi = id; }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+            const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (better(od, oi, bd, bi)) { bd = od; bi = oi; }
+        }
+        if (lane == 0) { wd[w] = bd; wi[w] = bi; }
+        __syncthreads();
+        bd = wd[0];
+        bi = wi[0];
+        for (int j = 1; j < wpb; ++j)
+            if (better(wd[j], wi[j], bd, bi)) { bd = wd[j]; bi = wi[j]; }
+        if (threadIdx.x == 0) { rd[r] = bd; ri[r] = bi; }
+        __syncthreads();
+        pd = bd;
+        pi = bi;
+    }
+    if (threadIdx.x == 0) {
+        struct Rr { double dist; long long id; double d2; long long reserved; };
+        Rr* res = reinterpret_cast<Rr*>(result);
+        for (int r = 1; r < kk; ++r) {
+            const bool have = ri[r] >= 0;
+            res[r].dist = have ? sqrt(rd[r]) : (double)INFINITY;
+            res[r].id = have ? row_begin + ri[r] : -1;
+            res[r].d2 = have ? rd[r] : (double)INFINITY;
+            res[r].reserved = 0;
+        }
+        finish_query(Best{ri[0] >= 0 ? rd[0] : (double)INFINITY, ri[0]}, cnt, st, N, row_begin, result, stats);
+    }
+}
+
 __global__ void k_arm(QState* st) { arm_state(st); }
+
+__global__ void k_arm_knn(QState* st, KnnState* kn)
+{
+    arm_state(st);
+    kn->n32 = 0;
+    kn->n64 = 0;
+}
 
 // --------------------------------------------------------------------- inspection
 // fp64 DTW of `k` local row ids with the resolve kernel's engine (dtw_warp_any<double>,

@@ -157,13 +157,15 @@ __global__ void __launch_bounds__(256) k_seed_ed(const float* __restrict__ q_g, 
 
 // DTW seed: prologue (envelope, envelope PAA, table) in CTA 0, then the window rows' fp32
 // banded DTW, one warp per row (anti-diagonal wavefront, dtw.cuh) over the row staged in
-// shared memory.  Dynamic shared memory: q (npad) + per warp row (npad) + 3n floats.
+// shared memory; BSF0 = their minimum (1-NN) or, with seed_d, every distance goes to seed_d
+// for k_seed_select (k-NN: BSF0 = the k-th smallest).  Dynamic shared memory: q (npad) + per
+// warp row (npad) + 3n floats.
 __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, const float* __restrict__ rows,
                            const unsigned long long* __restrict__ skey, const unsigned* __restrict__ perm,
                            long long N, int window, const float* __restrict__ beta_g,
                            const float* __restrict__ lo_w, const float* __restrict__ hi_w,
                            float* __restrict__ lut_g, float* __restrict__ tab, float* __restrict__ U_g,
-                           float* __restrict__ L_g, QState* st)
+                           float* __restrict__ L_g, QState* st, float* __restrict__ seed_d)
 {
     extern __shared__ __align__(16) float dsm[];
     float* q_s = dsm;
@@ -194,9 +196,11 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
             *reinterpret_cast<float4*>(c_s + j) =
                 __ldg(reinterpret_cast<const float4*>(rows + (long long)perm[start + k] * n + j));
         __syncwarp();
-        best = fminf(best, dtw_warp_any<float>(q_s, c_s, n, reach, buf, lane));
+        const float d = dtw_warp_any<float>(q_s, c_s, n, reach, buf, lane);
+        best = fminf(best, d);
+        if (seed_d && lane == 0) seed_d[k] = d;  // k-NN: every window distance (k_seed_select)
     }
-    if (lane == 0 && best < INFINITY) {
+    if (!seed_d && lane == 0 && best < INFINITY) {
         bsf_update(st, best);
         atomicMin(&st->seed_bits, __float_as_uint(best));
     }
@@ -321,11 +325,13 @@ __device__ __forceinline__ int scan_tile_coarse(const uint4* __restrict__ tiles,
 {
     float acc[16];
     coarse_acc(tiles, tile, lbase, lane, acc);
-    const long long id0 = tile * MESSI_TILE_ROWS + lane * 16;
     unsigned mask = 0;
 #pragma unroll
     for (int k = 0; k < 16; ++k)
-        if (acc[k] <= thr && id0 + k < N) mask |= 1u << k;
+        if (acc[k] <= thr) mask |= 1u << k;
+    // series past the end of the collection (the last tile only): one 64-bit test per lane
+    const long long left = N - (tile * MESSI_TILE_ROWS + lane * 16);
+    if (left < 16) mask &= left > 0 ? (1u << left) - 1u : 0u;
     const int cnt = __popc(mask);
     int incl = cnt;
 #pragma unroll

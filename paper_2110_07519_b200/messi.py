@@ -71,9 +71,10 @@ def lib():
         L.messi_query_dtw.argtypes = [vp, vp, i32, ctypes.POINTER(Result), vp]
         L.messi_query_ed_batch.argtypes = [vp, vp, i32, vp, vp]
         L.messi_query_dtw_batch.argtypes = [vp, vp, i32, i32, vp, vp]
-        if hasattr(L, "messi_query_ed_knn"):
-            L.messi_query_ed_knn.argtypes = [vp, vp, i32, vp, vp]
-            L.messi_query_ed_knn_batch.argtypes = [vp, vp, i32, i32, vp, vp]
+        L.messi_query_ed_knn.argtypes = [vp, vp, i32, vp, vp]
+        L.messi_query_ed_knn_batch.argtypes = [vp, vp, i32, i32, vp, vp]
+        L.messi_query_dtw_knn.argtypes = [vp, vp, i32, i32, vp, vp]
+        L.messi_query_dtw_knn_batch.argtypes = [vp, vp, i32, i32, i32, vp, vp]
         L.messi_free.argtypes = [vp]
         L.messi_free.restype = None
         L.messi_last_error.restype = ctypes.c_char_p
@@ -97,7 +98,7 @@ def lib():
         L.messi_debug_tile_bounds.argtypes = [vp, vp, i32, vp]
         L.messi_debug_distances.argtypes = [vp, vp, i32, vp, i32, vp, vp, vp]
         L.messi_debug_super_bounds.argtypes = [vp, vp, vp]
-        L.messi_debug_ed_refine.argtypes = [vp, vp, vp, i32, vp, vp]
+        L.messi_debug_ed_refine.argtypes = [vp, vp, vp, i32, vp, vp, vp]
         L.messi_debug_dtw_stages.argtypes = [vp, vp, i32, vp, i32, vp, vp, ctypes.POINTER(i32)]
         for f in ("messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_batch",
                   "messi_query_dtw_batch", "messi_profile_enable", "messi_profile_read", "messi_debug_breakpoints", "messi_debug_summaries",
@@ -117,7 +118,8 @@ EXPORTED = ["messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_
             "messi_debug_scan_repeat", "messi_debug_tile_bounds", "messi_debug_quantised",
             "messi_debug_coarse_bounds", "messi_batch_state_ipc", "messi_link_peers_ipc",
             "messi_link_peers_local", "messi_query_ed_knn", "messi_query_ed_knn_batch", "messi_debug_super_bounds",
-            "messi_debug_ed_refine", "messi_debug_dtw_stages", "messi_build_times"]
+            "messi_debug_ed_refine", "messi_debug_dtw_stages", "messi_build_times", "messi_query_dtw_knn",
+            "messi_query_dtw_knn_batch"]
 
 
 def _check(status: int):
@@ -235,6 +237,26 @@ def messi_query_ed_knn(handle, query, k: int, with_stats: bool = False):
     return (dist, ids, d2, st.as_dict()) if with_stats else (dist, ids, d2)
 
 
+def messi_query_dtw_knn(handle, query, reach: int, k: int, with_stats: bool = False):
+    """Exact k-NN (DTW, reach points) of one query: (dist float64[k], id int64[k], d2 float64[k][, stats])."""
+    import numpy as np
+    q, keep = _query_ptr(query)
+    res = (Result * k)()
+    st = Stats()
+    _check(lib().messi_query_dtw_knn(handle, q, int(reach), int(k), res, ctypes.byref(st) if with_stats else None))
+    dist = np.array([r.dist for r in res]); ids = np.array([r.id for r in res], dtype=np.int64)
+    d2 = np.array([r.d2 for r in res])
+    return (dist, ids, d2, st.as_dict()) if with_stats else (dist, ids, d2)
+
+
+def messi_query_dtw_knn_batch(handle, queries_dev: torch.Tensor, reach: int, k: int, results_dev: torch.Tensor,
+                              stats_dev=None, n=None):
+    """results_dev: uint8 CUDA tensor of nq*k*32 bytes (result_buffer(nq * k))."""
+    nq = _check_batch(queries_dev, results_dev, stats_dev, max(1, int(k)), n)
+    _check(lib().messi_query_dtw_knn_batch(handle, _ptr(queries_dev), nq, int(reach), int(k), _ptr(results_dev),
+                                           _ptr(stats_dev)))
+
+
 def messi_query_ed_knn_batch(handle, queries_dev: torch.Tensor, k: int, results_dev: torch.Tensor, stats_dev=None,
                              n=None):
     """results_dev: uint8 CUDA tensor of nq*k*32 bytes (result_buffer(nq * k))."""
@@ -340,13 +362,15 @@ def messi_debug_super_bounds(handle, query_dev: torch.Tensor, nsuper: int):
 
 
 def messi_debug_ed_refine(handle, query_dev: torch.Tensor, ids_dev: torch.Tensor):
-    """(dh2, L, d32) float32 [k] each and d64 float64 [k] of the ED refine's device code."""
+    """(dh2 float64 [k], L float64 [k], d32 float32 [k], d64 float64 [k]) of the ED refine's device code."""
     ids = ids_dev.to(torch.int32).contiguous()
     k = ids.numel()
-    out4 = torch.empty((k, 4), dtype=torch.float32, device=query_dev.device)
-    d64 = torch.empty(k, dtype=torch.float64, device=query_dev.device)
-    _check(lib().messi_debug_ed_refine(handle, _ptr(query_dev), _ptr(ids), k, _ptr(out4), _ptr(d64)))
-    return out4[:, 0], out4[:, 1], out4[:, 2], d64
+    dev = query_dev.device
+    q8 = torch.empty((k, 2), dtype=torch.float64, device=dev)
+    d32 = torch.empty(k, dtype=torch.float32, device=dev)
+    d64 = torch.empty(k, dtype=torch.float64, device=dev)
+    _check(lib().messi_debug_ed_refine(handle, _ptr(query_dev), _ptr(ids), k, _ptr(q8), _ptr(d32), _ptr(d64)))
+    return q8[:, 0], q8[:, 1], d32, d64
 
 
 def messi_debug_dtw_stages(handle, query_dev: torch.Tensor, reach: int, ids_dev: torch.Tensor):
@@ -457,12 +481,19 @@ class Index:
     def query_knn(self, q, k: int, with_stats=False):
         return messi_query_ed_knn(self.handle, q, k, with_stats)
 
-    def query_batch_knn(self, queries_dev: torch.Tensor, k: int, results=None, stats=None):
-        """Enqueue nq exact k-NN (ED) queries; results: nq*k entries (decode_results -> [nq*k])."""
+    def query_batch_knn(self, queries_dev: torch.Tensor, k: int, results=None, stats=None, reach: int | None = None):
+        """Enqueue nq exact k-NN queries (ED, or DTW with `reach`); results: nq*k entries
+        (decode_results -> [nq*k])."""
         nq = queries_dev.shape[0]
         results = results if results is not None else result_buffer(nq * k, self.device)
-        messi_query_ed_knn_batch(self.handle, queries_dev, k, results, stats, n=self.n)
+        if reach is None:
+            messi_query_ed_knn_batch(self.handle, queries_dev, k, results, stats, n=self.n)
+        else:
+            messi_query_dtw_knn_batch(self.handle, queries_dev, reach, k, results, stats, n=self.n)
         return results, stats
+
+    def query_dtw_knn(self, q, reach: int, k: int, with_stats=False):
+        return messi_query_dtw_knn(self.handle, q, reach, k, with_stats)
 
     def launches(self) -> int:
         return messi_launch_count(self.handle)

@@ -218,13 +218,27 @@ def test_lower_bounds_dtw(c1):
 
 
 # -------------------------------------------------------------- real distances (A7-A9)
+def _quantise_like_rows(q):
+    """The quantisation recipe of the rows, restated for one fp32 vector: s the
+    smallest power of two with max|q| <= 127 s, c = rint(q / s)."""
+    q = np.asarray(q, dtype=np.float32)
+    mx = float(np.abs(q).max())
+    if mx == 0.0:
+        return 1.0, np.zeros(q.shape, np.int64)
+    m, e = np.frexp(np.float32(mx))
+    k = e - 7 if m * 128.0 <= 127.0 else e - 6
+    s = float(np.ldexp(1.0, int(k)))
+    return s, np.rint(q.astype(np.float64) / s).astype(np.int64)
+
+
 def test_ed_refine_stages_every_row(c1):
     """The ED refine's own device code on EVERY C1 row (messi_debug_ed_refine):
-      * q8_bound_pass: dh2 = fp32 ||q - s c||^2 over the GPU's quantised row within its fp32
-        error ((n + 16) u relative) of the fp64 value, and its bound L never exceeds the true
-        distance ||q - x|| (oracle ED, triangle inequality; DESIGN.md 5): the prune is safe;
-      * ed2_group (the exact pass): fp32 squared ED within (n/32 + 5 + 2) u relative of the
-        oracle's (8 sequential fma per lane, a 5-level butterfly);
+      * q8i_bound_pass: dh2 is a lower bound of ||q^ - x^||^2 (query and row quantised with the
+        same recipe; the sums are exact integers, so it is within 2^-40 of it), and its bound L
+        never exceeds the true distance ||q - x|| (oracle ED; triangle inequality):
+        the prune is safe; and L is tight (>= ||q^ - x^|| - e_x - ||q - q^|| up to the margins);
+      * ed2_group (the exact pass): fp32 squared ED within (n/32 + 9) u relative of the
+        oracle's (8 sequential fma per lane, a 5-level butterfly, the rounding of q - x);
       * ed2_exact_g (the re-rank): bit-identical to the oracle's fp64 ED^2."""
     X, Q, idx, Xh, Qh = c1
     N, n = X.shape
@@ -237,12 +251,15 @@ def test_ed_refine_stages_every_row(c1):
     for qi in range(2):
         dh2, L, d32, d64 = messi().messi_debug_ed_refine(idx.handle, Q[qi].contiguous(), ids)
         dh2, L, d32, d64 = (t.cpu().numpy() for t in (dh2, L, d32, d64))
-        q = Qh[qi].astype(np.float64)
-        ref_dh2 = ((xq - q) ** 2).sum(axis=1)
-        assert np.all(np.abs(dh2 - ref_dh2) <= (n + 16) * U32 * ref_dh2 + 1e-30)
+        sq, cq = _quantise_like_rows(Qh[qi])
+        qhat = sq * cq.astype(np.float64)
+        eq = np.sqrt(((Qh[qi].astype(np.float64) - qhat) ** 2).sum())
+        ref_dh2 = ((xq - qhat) ** 2).sum(axis=1)
+        assert np.all(dh2 <= ref_dh2 * (1 + 1e-15))
+        assert np.all(dh2 >= ref_dh2 * (1 - 2.0 ** -40) - 1e-12)
         ed = oracle.ed2_rows(Xh, Qh[qi])
-        assert np.all(L.astype(np.float64) <= np.sqrt(ed))
-        assert np.all(L >= np.sqrt(ref_dh2) * (1 - 2.0 ** -11) - e - 1e-6)  # and it is tight
+        assert np.all(L <= np.sqrt(ed))
+        assert np.all(L >= np.sqrt(ref_dh2) * (1 - 2.0 ** -40) - e - eq * (1 + 2.0 ** -20) - 1e-9)
         assert np.all(np.abs(d32 - ed) <= (n // 32 + 9) * U32 * ed + 1e-30)
         assert np.array_equal(d64, ed)
 
