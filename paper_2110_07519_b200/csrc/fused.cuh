@@ -694,35 +694,30 @@ struct Q8Query {
 };
 
 template <bool DBG = false>
-__device__ __forceinline__ unsigned q8i_bound_pass(unsigned pass, unsigned my_pos, const unsigned char* __restrict__ rows8,
+__device__ __forceinline__ unsigned q8i_bound_pass(int count, unsigned my_pos, const unsigned char* __restrict__ rows8,
                                                    const float2* __restrict__ meta8, int n, const uint4* qc_s,
                                                    const Q8Query& qq, float thr, int lane, double2* dbg = nullptr)
 {
+    // candidates: lanes 0 .. count-1 (a prefix), lane l's at sorted position my_pos.  Pass p
+    // streams candidates 8p .. 8p+7, group g = lane >> 2 the row of candidate 8p + g; the
+    // group's integer sums then go to the candidate's own lane, and every lane finishes its
+    // candidate's bound at once.
     const int g = lane >> 2, gl = lane & 3;
     const int nch = n >> 4;
-    unsigned keep = 0;
-    while (pass) {
-        int src[8];
-        bool okj[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            okj[j] = pass != 0;
-            src[j] = okj[j] ? __ffs(pass) - 1 : 0;
-            pass &= pass - 1;
-        }
-        int ms = src[0];
-        bool ok = okj[0];
-#pragma unroll
-        for (int j = 1; j < 8; ++j)
-            if (g == j) { ms = src[j]; ok = okj[j]; }
-        const unsigned pos = __shfl_sync(0xffffffffu, my_pos, ms);
-        const uint4* row = reinterpret_cast<const uint4*>(rows8 + (long long)pos * n);
+    int my_dq = 0;
+    unsigned my_bb = 0, my_b = 0;
+#pragma unroll 1
+    for (int p = 0; 8 * p < count; ++p) {
+        const int c = 8 * p + g;
+        const bool ok = c < count;
+        const unsigned pos = __shfl_sync(0xffffffffu, my_pos, c & 31);
+        const uint4* row = reinterpret_cast<const uint4*>(rows8 + (size_t)pos * (size_t)n);
         int dbq = 0;
         unsigned sbb = 0, sb = 0;
 #pragma unroll 4
-        for (int c = gl; c < nch; c += 4) {
-            const uint4 w = ok ? __ldg(row + c) : make_uint4(0u, 0u, 0u, 0u);
-            const uint4 qv = qc_s[c];
+        for (int ch = gl; ch < nch; ch += 4) {
+            const uint4 w = ok ? __ldg(row + ch) : make_uint4(0u, 0u, 0u, 0u);
+            const uint4 qv = qc_s[ch];
             dbq = dp4a_us(w.x, qv.x, dbq); dbq = dp4a_us(w.y, qv.y, dbq);
             dbq = dp4a_us(w.z, qv.z, dbq); dbq = dp4a_us(w.w, qv.w, dbq);
             sbb = dp4a_uu(w.x, w.x, sbb); sbb = dp4a_uu(w.y, w.y, sbb);
@@ -736,26 +731,33 @@ __device__ __forceinline__ unsigned q8i_bound_pass(unsigned pass, unsigned my_po
             sbb += __shfl_xor_sync(0xffffffffu, sbb, o);
             sb += __shfl_xor_sync(0xffffffffu, sb, o);
         }
-        bool survives = true;
-        if (gl == 0 && ok) {
-            const float2 mt = meta8[pos];
-            const double sx = (double)mt.x;  // a power of two
-            const long long dqx = (long long)dbq - 128LL * qq.sum;                          // sum c_x c_q
-            const long long ssx = (long long)sbb - 256LL * (long long)sb + 16384LL * n;    // sum c_x^2
-            const double t2 = sx * sx * (double)ssx, t3 = 2.0 * qq.sq * sx * (double)dqx;  // exact products
-            const double d2 = (qq.s2ss + t2) - t3;
-            // two roundings of magnitude <= 2^-53 (s2ss + t2 + |t3|) each; margin 2^-50
-            const double d2lo = d2 - 0x1p-50 * (qq.s2ss + t2 + fabs(t3));
-            const double L = (d2lo > 0.0 ? sqrt(d2lo) * (1.0 - 0x1p-50) : 0.0) - (double)mt.y - qq.e;
-            survives = !(L > 0.0 && L * L * (1.0 - 0x1p-40) > (double)thr);
-            if constexpr (DBG) dbg[ms] = make_double2(d2lo, L);
-        }
-        const unsigned bits = __ballot_sync(0xffffffffu, gl == 0 && ok && survives);
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (bits & (1u << (4 * j))) keep |= 1u << src[j];
+        const int src = 4 * (lane & 7);
+        const int v_dq = __shfl_sync(0xffffffffu, dbq, src);
+        const unsigned v_bb = __shfl_sync(0xffffffffu, sbb, src), v_b = __shfl_sync(0xffffffffu, sb, src);
+        if ((lane >> 3) == p) { my_dq = v_dq; my_bb = v_bb; my_b = v_b; }
     }
-    return keep;
+    bool survives = true;
+    if (lane < count) {
+        const float2 mt = meta8[my_pos];
+        const double sx = (double)mt.x;  // a power of two
+        const long long dqx = (long long)my_dq - 128LL * qq.sum;                         // sum c_x c_q
+        const long long ssx = (long long)my_bb - 256LL * (long long)my_b + 16384LL * n;  // sum c_x^2
+        const double t2 = sx * sx * (double)ssx, t3 = 2.0 * qq.sq * sx * (double)dqx;  // exact products
+        const double d2 = (qq.s2ss + t2) - t3;
+        // two roundings of magnitude <= 2^-53 (s2ss + t2 + |t3|) each; margin 2^-50
+        const double d2lo = d2 - 0x1p-50 * (qq.s2ss + t2 + fabs(t3));
+        const double L = (d2lo > 0.0 ? sqrt(d2lo) * (1.0 - 0x1p-50) : 0.0) - (double)mt.y - qq.e;
+        survives = !(L > 0.0 && L * L * (1.0 - 0x1p-40) > (double)thr);
+        if constexpr (DBG) dbg[lane] = make_double2(d2lo, L);
+    }
+    return __ballot_sync(0xffffffffu, lane < count && survives);
+}
+
+// L2 prefetch of the n bytes at p (128-byte lines, one instruction per line and lane).
+__device__ __forceinline__ void prefetch_l2_lines(const void* p, int bytes)
+{
+    const char* c = static_cast<const char*>(p);
+    for (int off = 0; off < bytes; off += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(c + off));
 }
 
 // Fine pass + refine of the coarse survivors of one tile (list surv, m entries, warp-
@@ -783,10 +785,10 @@ struct FusedCtx {
 };
 
 template <bool LINKED, bool KNN>
-__device__ __forceinline__ void refine_round(const FusedCtx& cx, unsigned cp, unsigned pass, float& thr,
+__device__ __forceinline__ void refine_round(const FusedCtx& cx, unsigned cp, int count, float& thr,
                                              WarpCounts& wc, int lane)
 {
-    const unsigned keep = q8i_bound_pass(pass, cp, cx.rows8, cx.meta8, cx.n, cx.qc_s, cx.qq, thr, lane);
+    const unsigned keep = q8i_bound_pass(count, cp, cx.rows8, cx.meta8, cx.n, cx.qc_s, cx.qq, thr, lane);
     wc.exact += __popc(keep);
     if (keep) thr = fminf(thr, slack_up(exact_pass<LINKED, KNN>(keep, cp, cx.perm, cx.rows, cx.n, cx.q_p, cx.st,
                                                                    cx.ps, cx.b, cx.knn, cx.k, lane)));
@@ -816,7 +818,7 @@ __device__ __forceinline__ void fine_and_refine(const FusedCtx& cx, long long ti
         if (pass) {
             if (ok) {
                 cbuf[ncb + __popc(pass & ((1u << lane) - 1))] = pos;
-                prefetch_l2_bulk(cx.rows8 + (long long)pos * cx.n, (unsigned)cx.n);
+                prefetch_l2_lines(cx.rows8 + (long long)pos * cx.n, cx.n);
             }
             ncb += __popc(pass);
             wc.cand += __popc(pass);
@@ -828,7 +830,7 @@ __device__ __forceinline__ void fine_and_refine(const FusedCtx& cx, long long ti
                 if (ncb - 32 > (unsigned)lane) cbuf[lane] = rest;
                 ncb -= 32;
                 __syncwarp();
-                refine_round<LINKED, KNN>(cx, cp, 0xffffffffu, thr, wc, lane);
+                refine_round<LINKED, KNN>(cx, cp, 32, thr, wc, lane);
             }
         }
         pos = pos_n;
@@ -972,9 +974,8 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
                                          wc, lane);
         if (ncb) {  // the query's last fine survivors
             const unsigned cp = (unsigned)lane < ncb ? cbuf[lane] : 0u;
-            const unsigned pass = ncb >= 32 ? 0xffffffffu : (1u << ncb) - 1u;
             __syncwarp();
-            refine_round<LINKED, KNN>(cx, cp, pass, thr, wc, lane);
+            refine_round<LINKED, KNN>(cx, cp, (int)ncb, thr, wc, lane);
             ncb = 0;
         }
         if (lane == 0) {
@@ -1022,8 +1023,8 @@ __global__ void __launch_bounds__(256) k_debug_ed_refine(const float* __restrict
         const unsigned id = v ? ids[t0 + lane] : 0u;
         const unsigned pos = v ? inv[id] : 0u;
         const unsigned mask = __ballot_sync(0xffffffffu, v);
-        q8i_bound_pass<true>(mask, pos, rows8, meta8, n, reinterpret_cast<const uint4*>(qc_w), qq, INFINITY, lane,
-                             dbg_s[w]);
+        q8i_bound_pass<true>(min(32, k - t0), pos, rows8, meta8, n, reinterpret_cast<const uint4*>(qc_w), qq, INFINITY,
+                             lane, dbg_s[w]);
         __syncwarp();
         float mine = 0.0f;
         unsigned rest = mask;
