@@ -206,9 +206,9 @@ messi_status messi_debug_breakpoints(int32_t device, float* beta32_host);
  * de-tiled into caller device buffers (paa_dev may be NULL). */
 messi_status messi_debug_summaries(messi_index* idx, uint8_t* sym_dev, float* paa_dev);
 
-/* The quantised copy of the rows used by the ED refine's distance bound (DESIGN.md §5/§7),
- * back in row order: q8_dev[count][n] bytes b = c + 128 (c = rint(x / s) in [-127, 127]) and
- * meta_dev[count][2] fp32 {s, e}: s a power of two, e >= ||x - s c||_2.  Device buffers. */
+/* The quantised copy of the rows used by the refine's distance bounds (DESIGN.md §5/§7),
+ * back in row order: q8_dev[count][n] int8 c = rint(x / s) in [-127, 127] and meta_dev[count][2]
+ * fp32 {s, e}: s a power of two, e >= ||x - s c||_2.  Device buffers. */
 messi_status messi_debug_quantised(messi_index* idx, uint8_t* q8_dev, float* meta_dev);
 
 /* Sorted approximate-search keys and the row permutation (device pointers owned by idx). */

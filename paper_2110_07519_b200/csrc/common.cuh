@@ -146,6 +146,12 @@ __device__ __forceinline__ int dp4a_us(unsigned a, unsigned b, int c)  // a: 4 x
     asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
     return d;
 }
+__device__ __forceinline__ int dp4a_ss(unsigned a, unsigned b, int c)  // a, b: 4 x s8
+{
+    int d;
+    asm("dp4a.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
 __device__ __forceinline__ unsigned dp4a_uu(unsigned a, unsigned b, unsigned c)  // a, b: 4 x u8
 {
     unsigned d;

@@ -612,7 +612,7 @@ __host__ __device__ inline size_t fused_qpad(int n) { return (size_t)(n + 4 * ((
 __host__ __device__ inline size_t fused_smem(int n)
 {
     return (size_t)kLutX * 4 + fused_qpad(n) * 4 + (size_t)n +
-           (size_t)kFusedWarps * (2 * MESSI_TILE_ROWS * 2 + kCandBuf * 4);
+           (size_t)kFusedWarps * (2 * MESSI_TILE_ROWS * 2 + kCandBuf * 4 + 4);
 }
 
 // Writes query b's result and stats (finish_query's layout) from its state.
@@ -682,7 +682,7 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes)
 // rows (q^ = s_q c_q, e_q >= ||q - q^||, k_prologue_batch) and row x^ = s_x c_x (e_x >= ||x - x^||):
 //     ||q - x|| >= ||q^ - x^|| - e_q - e_x,
 //     ||q^ - x^||^2 = s_q^2 sum c_q^2 + s_x^2 sum c_x^2 - 2 s_q s_x sum c_q c_x,
-// the sums exact in int32 (IDP.4A over the row's bytes b = c_x + 128: sum b c_q, sum b^2, sum b),
+// the sums exact in int32 (IDP.4A over the row's int8 bytes: sum c_x c_q, sum c_x^2),
 // the combination in fp64 with an error margin, so L below is a rigorous lower bound of ||q - x||.
 // A candidate with L > 0 and L^2 > thr cannot be the nearest neighbour; the others come back
 // (bit set) for the exact fp32 refine.  Groups of 4 lanes take one row each (8 rows per pass);
@@ -690,7 +690,6 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes)
 // shared memory (qc_s).  DBG (inspection): dbg[src lane] = (dh2 lower bound, L).
 struct Q8Query {
     double sq, e, s2ss;  // s_q, e_q, s_q^2 sum c_q^2
-    int sum;             // sum c_q
 };
 
 template <bool DBG = false>
@@ -704,45 +703,37 @@ __device__ __forceinline__ unsigned q8i_bound_pass(int count, unsigned my_pos, c
     // candidate's bound at once.
     const int g = lane >> 2, gl = lane & 3;
     const int nch = n >> 4;
-    int my_dq = 0;
-    unsigned my_bb = 0, my_b = 0;
+    int my_dq = 0, my_ss = 0;  // sum c_x c_q, sum c_x^2 of this lane's candidate (exact int32)
 #pragma unroll 1
     for (int p = 0; 8 * p < count; ++p) {
         const int c = 8 * p + g;
         const bool ok = c < count;
         const unsigned pos = __shfl_sync(0xffffffffu, my_pos, c & 31);
         const uint4* row = reinterpret_cast<const uint4*>(rows8 + (size_t)pos * (size_t)n);
-        int dbq = 0;
-        unsigned sbb = 0, sb = 0;
+        int dq = 0, ss = 0;
 #pragma unroll 4
         for (int ch = gl; ch < nch; ch += 4) {
             const uint4 w = ok ? __ldg(row + ch) : make_uint4(0u, 0u, 0u, 0u);
             const uint4 qv = qc_s[ch];
-            dbq = dp4a_us(w.x, qv.x, dbq); dbq = dp4a_us(w.y, qv.y, dbq);
-            dbq = dp4a_us(w.z, qv.z, dbq); dbq = dp4a_us(w.w, qv.w, dbq);
-            sbb = dp4a_uu(w.x, w.x, sbb); sbb = dp4a_uu(w.y, w.y, sbb);
-            sbb = dp4a_uu(w.z, w.z, sbb); sbb = dp4a_uu(w.w, w.w, sbb);
-            sb = dp4a_uu(w.x, 0x01010101u, sb); sb = dp4a_uu(w.y, 0x01010101u, sb);
-            sb = dp4a_uu(w.z, 0x01010101u, sb); sb = dp4a_uu(w.w, 0x01010101u, sb);
+            dq = dp4a_ss(w.x, qv.x, dq); dq = dp4a_ss(w.y, qv.y, dq);
+            dq = dp4a_ss(w.z, qv.z, dq); dq = dp4a_ss(w.w, qv.w, dq);
+            ss = dp4a_ss(w.x, w.x, ss); ss = dp4a_ss(w.y, w.y, ss);
+            ss = dp4a_ss(w.z, w.z, ss); ss = dp4a_ss(w.w, w.w, ss);
         }
 #pragma unroll
         for (int o = 1; o <= 2; o <<= 1) {
-            dbq += __shfl_xor_sync(0xffffffffu, dbq, o);
-            sbb += __shfl_xor_sync(0xffffffffu, sbb, o);
-            sb += __shfl_xor_sync(0xffffffffu, sb, o);
+            dq += __shfl_xor_sync(0xffffffffu, dq, o);
+            ss += __shfl_xor_sync(0xffffffffu, ss, o);
         }
         const int src = 4 * (lane & 7);
-        const int v_dq = __shfl_sync(0xffffffffu, dbq, src);
-        const unsigned v_bb = __shfl_sync(0xffffffffu, sbb, src), v_b = __shfl_sync(0xffffffffu, sb, src);
-        if ((lane >> 3) == p) { my_dq = v_dq; my_bb = v_bb; my_b = v_b; }
+        const int v_dq = __shfl_sync(0xffffffffu, dq, src), v_ss = __shfl_sync(0xffffffffu, ss, src);
+        if ((lane >> 3) == p) { my_dq = v_dq; my_ss = v_ss; }
     }
     bool survives = true;
     if (lane < count) {
         const float2 mt = meta8[my_pos];
         const double sx = (double)mt.x;  // a power of two
-        const long long dqx = (long long)my_dq - 128LL * qq.sum;                         // sum c_x c_q
-        const long long ssx = (long long)my_bb - 256LL * (long long)my_b + 16384LL * n;  // sum c_x^2
-        const double t2 = sx * sx * (double)ssx, t3 = 2.0 * qq.sq * sx * (double)dqx;  // exact products
+        const double t2 = sx * sx * (double)my_ss, t3 = 2.0 * qq.sq * sx * (double)my_dq;  // exact products
         const double d2 = (qq.s2ss + t2) - t3;
         // two roundings of magnitude <= 2^-53 (s2ss + t2 + |t3|) each; margin 2^-50
         const double d2lo = d2 - 0x1p-50 * (qq.s2ss + t2 + fabs(t3));
@@ -867,9 +858,11 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
     unsigned* qc_w = reinterpret_cast<unsigned*>(q_p + fused_qpad(n));
     unsigned short* surv_all = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(qc_w) + n);
     unsigned* cbuf_all = reinterpret_cast<unsigned*>(surv_all + kFusedWarps * 2 * MESSI_TILE_ROWS);
+    unsigned* wcnt_all = cbuf_all + kFusedWarps * kCandBuf;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned short* survb = surv_all + warp * 2 * MESSI_TILE_ROWS;  // two lists: current / previous tile
     unsigned* cbuf = cbuf_all + warp * kCandBuf;
+    unsigned* wcnt = wcnt_all + warp;
     __shared__ int s_has;
     FusedCtx cx;
     cx.sym8 = sym8; cx.rows8 = rows8; cx.meta8 = meta8; cx.perm = perm; cx.rows = rows; cx.q_p = q_p;
@@ -898,7 +891,6 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
         cx.qq.sq = (double)st->q8s;
         cx.qq.e = st->q8e;
         cx.qq.s2ss = st->q8s2ss;
-        cx.qq.sum = st->q8sum;
         __syncthreads();
         const uint2* tl = tlist_all + (size_t)b * ntiles;
         // list position of claim k: the front bin, then the back bin from its far end
@@ -950,7 +942,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
                 ++wc.tiles;
                 const long long tile = te.x;
                 unsigned short* surv = survb + cur * MESSI_TILE_ROWS;
-                const int m = scan_tile_coarse(tiles, tile, cx.lbase, thr, N, surv, lane);
+                const int m = scan_tile_coarse(tiles, tile, cx.lbase, thr, N, surv, wcnt, lane);
                 wc.coarse += m;
                 if (pm)
                     fine_and_refine<LINKED, KNN>(cx, ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, cbuf, ncb,
@@ -1016,7 +1008,6 @@ __global__ void __launch_bounds__(256) k_debug_ed_refine(const float* __restrict
     qq.sq = (double)qst->q8s;
     qq.e = qst->q8e;
     qq.s2ss = qst->q8s2ss;
-    qq.sum = qst->q8sum;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     for (int t0 = (blockIdx.x * wpb + w) * 32; t0 < k; t0 += gridDim.x * wpb * 32) {
         const bool v = t0 + lane < k;

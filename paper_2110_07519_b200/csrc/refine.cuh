@@ -237,13 +237,15 @@ __global__ void __launch_bounds__(128) k_lbk_filter_q8(const uint2* __restrict__
                 uint4 raw4[4];
 #pragma unroll
                 for (int h = 0; h < 4; ++h)
-                    raw4[h] = j0 + 16 * h < n ? __ldg(src + (j0 >> 4) + h) : make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
+                    raw4[h] = j0 + 16 * h < n ? __ldg(src + (j0 >> 4) + h) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
                 const int j = j0 + 16 * h;
                 if (j >= n) break;
                 const uint4 raw = raw4[h];
-                const unsigned wd[4] = {raw.x, raw.y, raw.z, raw.w};
+                // int8 c -> biased byte c + 128 (flip each sign bit), for the 2^23 conversion below
+                const unsigned wd[4] = {raw.x ^ 0x80808080u, raw.y ^ 0x80808080u, raw.z ^ 0x80808080u,
+                                        raw.w ^ 0x80808080u};
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
                     const float4 uu = *reinterpret_cast<const float4*>(U + j + 4 * g);

@@ -321,7 +321,7 @@ __device__ __forceinline__ void coarse_acc(const uint4* __restrict__ tiles, long
 }
 
 __device__ __forceinline__ int scan_tile_coarse(const uint4* __restrict__ tiles, long long tile, const char* lbase,
-                                                float thr, long long N, unsigned short* surv, int lane)
+                                                float thr, long long N, unsigned short* surv, unsigned* wcnt, int lane)
 {
     float acc[16];
     coarse_acc(tiles, tile, lbase, lane, acc);
@@ -332,15 +332,14 @@ __device__ __forceinline__ int scan_tile_coarse(const uint4* __restrict__ tiles,
     // series past the end of the collection (the last tile only): one 64-bit test per lane
     const long long left = N - (tile * MESSI_TILE_ROWS + lane * 16);
     if (left < 16) mask &= left > 0 ? (1u << left) - 1u : 0u;
+    // compaction: each lane reserves its survivors' slots with one shared-memory atomic on the
+    // warp's counter (the list order across lanes is free: every later pass is order-free)
     const int cnt = __popc(mask);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    const int m = __shfl_sync(0xffffffffu, incl, 31);
-    int off = incl - cnt;
+    if (lane == 0) *wcnt = 0u;
+    __syncwarp();
+    int off = cnt ? (int)atomicAdd(wcnt, (unsigned)cnt) : 0;
+    __syncwarp();
+    const int m = (int)*(volatile unsigned*)wcnt;
     while (mask) {
         const int k = __ffs(mask) - 1;
         mask &= mask - 1;
@@ -379,6 +378,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 3) k_scan(const uint4* __rest
 {
     extern __shared__ __align__(16) float tab_s[];
     __shared__ unsigned short surv_all[kScanWarps][MESSI_TILE_ROWS];
+    __shared__ unsigned wcnt_all[kScanWarps];
     for (int i = threadIdx.x; i < kScanTab / 4; i += blockDim.x)
         reinterpret_cast<float4*>(tab_s)[i] = reinterpret_cast<const float4*>(tab_g)[i];
     __syncthreads();
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 3) k_scan(const uint4* __rest
     const long long count = (long long)*(volatile unsigned*)&st->tile_count;
     for (long long it = (long long)blockIdx.x * kScanWarps + warp; it < count; it += (long long)gridDim.x * kScanWarps) {
         const long long tl = (long long)tlist[it];
-        const int m = scan_tile_coarse(tiles, tl, lbase, thr, N, surv, lane);
+        const int m = scan_tile_coarse(tiles, tl, lbase, thr, N, surv, &wcnt_all[warp], lane);
         if (lane == 0 && m) atomicAdd(&st->coarse_count, (unsigned)m);
         // rounds of 32 coarse survivors; the next round's 8-bit words are loaded before this
         // round's bounds are evaluated (DTW: ~40% of a tile survives the coarse bound)

@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(512) k_layout(const uint4* __restrict__ symrow
 
 // Quantised copy of the rows for the refine's distance bound (DESIGN.md §7 "quantised
 // rows"; not in the paper, whose refine reads every candidate's raw series, Alg. 9).
-// Sorted position p (row perm[p]) gets n bytes b_i = c_i + 128 with c_i = rint(x_i / s),
+// Sorted position p (row perm[p]) gets n bytes c_i (two's-complement int8), c_i = rint(x_i / s),
 // s = the smallest power of two with max_i |x_i| <= 127 s (so x_i / s and s * c_i are exact
 // in fp32), and meta[p] = {s, e}, e >= ||x - s c||_2 (fp64 sum, rounded up).  By the triangle
 // inequality ||q - x|| >= ||q - s c|| - e: a lower bound of the true ED from n bytes instead
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(256) k_quantise(const float* __restrict__ rows
                     const float c = usable ? rintf(ldexpf(xv[b], -k)) : 0.0f;  // |c| <= 127
                     const double r = __dsub_rn((double)xv[b], (double)c * (double)s);
                     err = __dadd_rn(err, __dmul_rn(r, r));
-                    word |= (unsigned)((int)c + 128) << (8 * b);
+                    word |= ((unsigned)(int)c & 255u) << (8 * b);
                 }
                 w[g] = word;
             }

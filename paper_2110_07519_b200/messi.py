@@ -318,7 +318,8 @@ def messi_debug_summaries(handle, count: int, device, with_paa: bool = False):
 
 
 def messi_debug_quantised(handle, count: int, n: int, device):
-    """(q8 uint8 [count, n] biased by 128, meta float32 [count, 2] = {scale, error bound}), row order."""
+    """(q8 [count, n] int8 c stored in a uint8 tensor (view as int8), meta float32 [count, 2] =
+    {scale, error bound}), row order."""
     q8 = torch.empty((count, n), dtype=torch.uint8, device=device)
     meta = torch.empty((count, 2), dtype=torch.float32, device=device)
     _check(lib().messi_debug_quantised(handle, _ptr(q8), _ptr(meta)))

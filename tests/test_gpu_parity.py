@@ -243,7 +243,7 @@ def test_ed_refine_stages_every_row(c1):
     X, Q, idx, Xh, Qh = c1
     N, n = X.shape
     q8, meta = messi().messi_debug_quantised(idx.handle, N, n, X.device)
-    c = q8.cpu().numpy().astype(np.float64) - 128.0
+    c = q8.cpu().numpy().view(np.int8).astype(np.float64)
     s = meta[:, 0].cpu().numpy().astype(np.float64)
     e = meta[:, 1].cpu().numpy().astype(np.float64)
     xq = s[:, None] * c
@@ -292,7 +292,7 @@ def test_dtw_stages_elementwise(c1, reach):
     assert np.all(raw <= ref * (1 + 1e-12))
     if quantised:
         q8, meta = messi().messi_debug_quantised(idx.handle, N, n, X.device)
-        cq = q8[ids].cpu().numpy().astype(np.float64) - 128.0
+        cq = q8[ids].cpu().numpy().view(np.int8).astype(np.float64)
         sc = meta[ids, 0].cpu().numpy().astype(np.float64)
         e = meta[ids, 1].cpu().numpy().astype(np.float64)
         xq = sc[:, None] * cq
@@ -351,7 +351,7 @@ def test_quantised_rows_and_bound(c1):
     for every C1 query, and the kernel's own fp32 evaluation is covered by the 1-NN parity."""
     X, Q, idx, Xh, Qh = c1
     q8, meta = messi().messi_debug_quantised(idx.handle, X.shape[0], X.shape[1], X.device)
-    c = q8.cpu().numpy().astype(np.int64) - 128
+    c = q8.cpu().numpy().view(np.int8).astype(np.int64)
     s = meta[:, 0].cpu().numpy().astype(np.float64)
     e = meta[:, 1].cpu().numpy().astype(np.float64)
     x = Xh.astype(np.float64)
@@ -380,7 +380,7 @@ def test_quantised_lb_keogh_bound(c1):
     X, Q, idx, Xh, Qh = c1
     rows = 3000
     q8, meta = messi().messi_debug_quantised(idx.handle, X.shape[0], X.shape[1], X.device)
-    c = q8[:rows].cpu().numpy().astype(np.float64) - 128.0
+    c = q8[:rows].cpu().numpy().view(np.int8).astype(np.float64)
     s = meta[:rows, 0].cpu().numpy().astype(np.float64)
     e = meta[:rows, 1].cpu().numpy().astype(np.float64)
     x = Xh[:rows].astype(np.float64)
