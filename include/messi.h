@@ -161,6 +161,16 @@ messi_status messi_query_dtw_knn(messi_index* idx, const float* query, int32_t r
 messi_status messi_query_dtw_knn_batch(messi_index* idx, const float* queries_dev, int32_t nq, int32_t reach, int32_t k,
                                        messi_result* results_dev, messi_stats* stats_dev);
 
+/* Exact 1-NN under ED of nq queries [nq][n] (device) by the tensor-core pass (SURVEY 8(f) f4:
+ * one stream of the quantised rows per <= 256 queries; tcgen05.mma kind::i8 computes every
+ * (row, query) int8 dot product exactly, the epilogue keeps the rows whose quantised-row bound
+ * does not exceed the approximate search's BSF0, and those are re-refined exactly:
+ * fp32 ED on the raw row, fp64 re-rank).  Same answers as messi_query_ed_batch.  n must be 128
+ * or 256 (EINVAL otherwise).  results_dev[nq], stats_dev[nq] (nullable) device arrays;
+ * asynchronous on cfg.stream. */
+messi_status messi_query_ed_tc_batch(messi_index* idx, const float* queries_dev, int32_t nq, messi_result* results_dev,
+                                     messi_stats* stats_dev);
+
 /* Release everything the library allocated for idx.  NULL-safe. */
 void messi_free(messi_index* idx);
 

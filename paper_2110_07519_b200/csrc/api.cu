@@ -26,6 +26,7 @@
 #include "scan.cuh"
 #include "summarise.cuh"
 #include "fused.cuh"
+#include "tc.cuh"
 
 using namespace messi;
 
@@ -99,6 +100,14 @@ struct messi_index {
     int* dbg_map = nullptr;
     unsigned* dbg_iota = nullptr;
     double* dbg_gbuf = nullptr;
+    // tensor-core batched path (tc.cuh), allocated on its first use
+    struct TcSet {
+        QState* bst = nullptr;     // per-query state of a pass (<= kTcMaxQ queries)
+        unsigned* qc = nullptr;    // quantised queries [kTcMaxQ][n] int8 (the MMA's B operand)
+        unsigned* cand = nullptr;  // survivors [kTcMaxQ][kTcCandCap] (sorted positions)
+        float4* tcm = nullptr;     // per sorted position: the row's share of the survival test
+        CUtensorMap tmA, tmB;      // TMA maps of rows8 and qc (128 B x 128 / 256 rows, 128-byte swizzle)
+    } tc;
     // per-query scratch
     Slot slot[MESSI_DTW_SLOTS];
     unsigned long long qcount = 0;
@@ -160,6 +169,12 @@ template <typename T> static messi_status dalloc(T** p, size_t count)
     if (count == 0) count = 1;
     CK(cudaMalloc((void**)p, count * sizeof(T)));
     return MESSI_OK;
+}
+
+static unsigned grid_of_rows(long long n, int threads)
+{
+    long long g = (n + threads - 1) / threads;
+    return (unsigned)(g < 1 ? 1 : g);
 }
 
 static cudaEvent_t pool_get(messi_index* idx)
@@ -289,6 +304,7 @@ static messi_status setup_kernels(int device)
     CK(cudaFuncSetAttribute(k_lbk_filter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_lbk_filter_q8, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_debug_dtw64, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_ed_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes(256)));
     CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_refine_dtw_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_resolve_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -469,7 +485,8 @@ extern "C" void messi_free(messi_index* idx)
     else cudaDeviceSynchronize();
     void* ptrs[] = {idx->tiles, idx->sym8, idx->boxes, idx->sboxes, idx->paa, idx->skey, idx->perm, idx->beta32, idx->lo_w,
                     idx->hi_w,  idx->qbuf,  idx->res1, idx->resk, idx->stats1, idx->rows8, idx->meta8,
-                    idx->dbg_inv, idx->dbg_map, idx->dbg_iota, idx->dbg_gbuf};
+                    idx->dbg_inv, idx->dbg_map, idx->dbg_iota, idx->dbg_gbuf, idx->tc.bst, idx->tc.qc, idx->tc.cand,
+                    idx->tc.tcm};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& row : idx->peer_ipc)
@@ -1086,6 +1103,112 @@ extern "C" messi_status messi_query_dtw_batch(messi_index* idx, const float* que
     for (int i = 0; i < nq; ++i)
         TRY(run_dtw(idx, queries_dev + (size_t)i * idx->n, reach, results_dev + i, stats_dev ? stats_dev + i : nullptr));
     return join_streams(idx);
+}
+
+// ----------------------------------------------------------------- tensor-core ED path
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// A 2-D uint8 TMA map over `rows` rows of `inner` bytes: boxes of 128 bytes x box_rows rows,
+// 128-byte swizzle (the UMMA K-major SWIZZLE_128B operand layout).
+static messi_status encode_u8_map(CUtensorMap* m, const void* base, unsigned long long inner, unsigned long long rows,
+                                  unsigned box_rows)
+{
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) return fail(MESSI_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    const cuuint64_t dims[2] = {inner, rows};
+    const cuuint64_t strides[1] = {inner};
+    const cuuint32_t box[2] = {128u, box_rows};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(MESSI_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return MESSI_OK;
+}
+
+static messi_status ensure_tc(messi_index* idx)
+{
+    if (idx->n != 128 && idx->n != 256)
+        return fail(MESSI_EINVAL, "the tensor-core path serves n = 128 or 256 (got %d)", idx->n);
+    auto& tc = idx->tc;
+    if (tc.bst) return MESSI_OK;
+    const size_t npad = (size_t)idx->ntiles * MESSI_TILE_ROWS;
+    TRY(dalloc(&tc.bst, kTcMaxQ));
+    CK(cudaMemset(tc.bst, 0, sizeof(QState) * kTcMaxQ));
+    TRY(dalloc(&tc.qc, (size_t)kTcMaxQ * (idx->n / 4)));
+    CK(cudaMemset(tc.qc, 0, (size_t)kTcMaxQ * idx->n));
+    TRY(dalloc(&tc.cand, (size_t)kTcMaxQ * kTcCandCap));
+    TRY(dalloc(&tc.tcm, npad));
+    k_tc_rowmeta<<<grid_of_rows(npad, 256), 256, 0, idx->stream>>>(idx->rows8, idx->meta8, (long long)npad, idx->n, tc.tcm);
+    LAUNCHED(idx);
+    TRY(encode_u8_map(&tc.tmA, idx->rows8, (unsigned long long)idx->n, (unsigned long long)npad, kTcRows));
+    TRY(encode_u8_map(&tc.tmB, tc.qc, (unsigned long long)idx->n, (unsigned long long)kTcMaxQ, kTcMaxQ));
+    return MESSI_OK;
+}
+
+// The batched tensor-core path for nq queries [nq][n] on the device: passes of <= kTcMaxQ
+// queries, each one stream of the quantised rows through k_ed_tc.
+static messi_status run_ed_tc(messi_index* idx, const float* queries_dev, int nq, messi_result* results_dev,
+                              messi_stats* stats_dev)
+{
+    TRY(ensure_tc(idx));
+    auto& tc = idx->tc;
+    const int n = idx->n;
+    const size_t qsm = (size_t)((n + 3) & ~3) * sizeof(float);
+    const int len = (int)(idx->window < idx->N ? idx->window : idx->N);
+    const long long ntc = idx->ntiles * (MESSI_TILE_ROWS / kTcRows);
+    cudaStream_t st = idx->stream;
+    PeerSet none{nullptr, 0, 0u};
+    for (int g0 = 0; g0 < nq; g0 += kTcMaxQ) {
+        const int B = nq - g0 < kTcMaxQ ? nq - g0 : kTcMaxQ;
+        const float* q = queries_dev + (size_t)g0 * n;
+        {
+            ProfScope ps(idx, K_SEED, st);
+            k_prologue_tc<<<B, 256, qsm, st>>>(q, n, idx->beta32, idx->lo_w, idx->hi_w, idx->skey, idx->N, idx->window,
+                                               tc.bst, tc.qc);
+            LAUNCHED(idx);
+            dim3 sg((unsigned)((len + kSeedRowsPerCta - 1) / kSeedRowsPerCta), (unsigned)B);
+            k_seed_batch<<<sg, 256, qsm, st>>>(q, n, idx->rows, idx->perm, tc.bst, none, nullptr, idx->window);
+            LAUNCHED(idx);
+        }
+        {
+            ProfScope ps(idx, K_SCAN, st);
+            const long long grid = ntc < idx->sms ? ntc : idx->sms;
+            k_ed_tc<<<(unsigned)grid, kTcThreads, tc_smem_bytes(n), st>>>(tc.tmA, tc.tmB, ntc, idx->N, n, B, tc.tcm,
+                                                                          tc.bst, tc.cand);
+            LAUNCHED(idx);
+        }
+        {
+            ProfScope ps(idx, K_REFINE, st);
+            const size_t per_warp = (fused_qpad(n) + (size_t)n / 4) * sizeof(float);
+            k_tc_verify<<<(B + 3) / 4, 128, 4 * per_warp, st>>>(q, n, B, tc.cand, idx->rows8, idx->meta8, tc.qc, idx->perm,
+                                                              idx->rows, idx->N, tc.bst);
+            LAUNCHED(idx);
+            k_finalise_batch<<<(B + 127) / 128, 128, 0, st>>>(tc.bst, B, idx->N, idx->row_begin, results_dev + g0,
+                                                              stats_dev ? stats_dev + g0 : nullptr, nullptr, 1);
+            LAUNCHED(idx);
+        }
+    }
+    return MESSI_OK;
+}
+
+extern "C" messi_status messi_query_ed_tc_batch(messi_index* idx, const float* queries_dev, int32_t nq,
+                                                messi_result* results_dev, messi_stats* stats_dev)
+{
+    g_err[0] = 0;
+    if (!idx || !queries_dev || !results_dev || nq < 0) return fail(MESSI_EINVAL, "bad argument");
+    CK(cudaSetDevice(idx->device));
+    TRY(join_streams(idx));
+    if (nq == 0) return MESSI_OK;
+    return run_ed_tc(idx, queries_dev, nq, results_dev, stats_dev);
 }
 
 // ------------------------------------------------------------ shared best-so-far (shards)

@@ -74,6 +74,7 @@ def lib():
         L.messi_query_ed_knn.argtypes = [vp, vp, i32, vp, vp]
         L.messi_query_ed_knn_batch.argtypes = [vp, vp, i32, i32, vp, vp]
         L.messi_query_dtw_knn.argtypes = [vp, vp, i32, i32, vp, vp]
+        L.messi_query_ed_tc_batch.argtypes = [vp, vp, i32, vp, vp]
         L.messi_query_dtw_knn_batch.argtypes = [vp, vp, i32, i32, i32, vp, vp]
         L.messi_free.argtypes = [vp]
         L.messi_free.restype = None
@@ -119,7 +120,7 @@ EXPORTED = ["messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_
             "messi_debug_coarse_bounds", "messi_batch_state_ipc", "messi_link_peers_ipc",
             "messi_link_peers_local", "messi_query_ed_knn", "messi_query_ed_knn_batch", "messi_debug_super_bounds",
             "messi_debug_ed_refine", "messi_debug_dtw_stages", "messi_build_times", "messi_query_dtw_knn",
-            "messi_query_dtw_knn_batch"]
+            "messi_query_dtw_knn_batch", "messi_query_ed_tc_batch"]
 
 
 def _check(status: int):
@@ -235,6 +236,12 @@ def messi_query_ed_knn(handle, query, k: int, with_stats: bool = False):
     dist = np.array([r.dist for r in res]); ids = np.array([r.id for r in res], dtype=np.int64)
     d2 = np.array([r.d2 for r in res])
     return (dist, ids, d2, st.as_dict()) if with_stats else (dist, ids, d2)
+
+
+def messi_query_ed_tc_batch(handle, queries_dev: torch.Tensor, results_dev: torch.Tensor, stats_dev=None, n=None):
+    """Exact 1-NN (ED) of nq queries by the tensor-core pass (n = 128 or 256); asynchronous like the batch call."""
+    nq = _check_batch(queries_dev, results_dev, stats_dev, 1, n)
+    _check(lib().messi_query_ed_tc_batch(handle, _ptr(queries_dev), nq, _ptr(results_dev), _ptr(stats_dev)))
 
 
 def messi_query_dtw_knn(handle, query, reach: int, k: int, with_stats: bool = False):
@@ -491,6 +498,13 @@ class Index:
             messi_query_ed_knn_batch(self.handle, queries_dev, k, results, stats, n=self.n)
         else:
             messi_query_dtw_knn_batch(self.handle, queries_dev, reach, k, results, stats, n=self.n)
+        return results, stats
+
+    def query_batch_tc(self, queries_dev: torch.Tensor, results=None, stats=None):
+        """Enqueue nq exact 1-NN (ED) queries on the tensor-core path."""
+        nq = queries_dev.shape[0]
+        results = results if results is not None else result_buffer(nq, self.device)
+        messi_query_ed_tc_batch(self.handle, queries_dev, results, stats, n=self.n)
         return results, stats
 
     def query_dtw_knn(self, q, reach: int, k: int, with_stats=False):
