@@ -365,11 +365,56 @@ def run_arm(cfg, args, world, rank, dev, stream, time_steps, warmup, repeats=1):
     return out
 
 
+def tc_compare(idx, Q, dev, stream, reps=5):
+    """The tensor-core batched path (SURVEY 8(f) f4 (i)+(ii)) against the LUT batch path on one
+    index and query set: q/s of each, the TC kernel's own time, its rows8 stream rate (of the
+    measured HBM peak) and int8 tensor rate (of 2 x the measured bf16 peak: the guide's nominal
+    int8 / bf16 ratio), and whether both paths return the same answers."""
+    import torch
+    from paper_2110_07519_b200 import messi as M
+    nq = Q.shape[0]
+    r1, r2, st = M.result_buffer(nq, dev), M.result_buffer(nq, dev), M.stats_buffer(nq, dev)
+    out = {"queries": nq}
+    with torch.cuda.stream(stream):
+        for name, fn in (("lut", lambda: idx.query_batch(Q, None, r1)), ("tc", lambda: idx.query_batch_tc(Q, r2, st))):
+            for _ in range(2):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            out[name] = {"ms": ms, "qps": nq / (ms / 1e3)}
+        M.messi_profile_enable(idx.handle, True)
+        idx.query_batch_tc(Q, r2, st)
+        kms = M.messi_profile_read(idx.handle, "scan")[0]
+        M.messi_profile_enable(idx.handle, False)
+        torch.cuda.synchronize()
+    a, b = M.decode_results(r1), M.decode_results(r2)
+    sts = M.decode_stats(st)
+    pk = peaks()
+    N, n = idx.count, idx.n
+    gbs = N * (n + 16) / (kms / 1e3) / 1e9  # rows8 + the 16 B row term per row
+    tops = 2.0 * N * n * nq / (kms / 1e3) / 1e12
+    int8_peak = 2.0 * pk.get("bf16_tflops", 1590.0)
+    out["tc"].update({"kernel": "k_ed_tc (TMA ring of int8 rows -> tcgen05.mma kind::i8 -> TMEM -> epilogue test)",
+                      "kernel_ms": kms, "hbm_gbs": gbs, "hbm_frac": gbs / pk.get("hbm_gbs", 6650.0),
+                      "int8_tops": tops, "int8_peak_tops": int8_peak, "tensor_frac": tops / int8_peak,
+                      "candidates_mean": sum(x["candidates"] for x in sts) / nq,
+                      "exact_mean": sum(x["exact"] for x in sts) / nq,
+                      "same_answers_as_lut": bool(torch.equal(a[1], b[1]) and torch.equal(a[2], b[2]))})
+    return out
+
+
 def build_split(args, dev, stream):
     """Index build of config 2 (10M x 256) on this GPU, phase by phase (device events inside
     messi_build): summarise (A1: 4n B read + 24 B written per series, the HBM-bound pass SURVEY
     8(d) prices at 1,104 B/series), key sort, sorted layout, quantised rows."""
     import torch
+    import datagen
     from paper_2110_07519_b200 import messi as M
     c2 = CONFIGS["c2"]
     X, _, _ = gen_collection(dict(c2, Q=1), 0, 1, dev)
@@ -380,7 +425,13 @@ def build_split(args, dev, stream):
         idx = M.Index(X, stream=stream, window=args.window)
         torch.cuda.synchronize()
         ph = M.messi_build_times(idx.handle)
-        idx.close()
+    tc = {}
+    for nq in (100, 256):  # C2's query set, and a full tensor-core pass
+        Q = torch.empty((nq, c2["n"]), dtype=torch.float32, device=dev)
+        datagen.walks_cuda(Q, 0, seed=datagen.QUERY_SEED)
+        torch.cuda.synchronize()
+        tc[f"q{nq}"] = tc_compare(idx, Q, dev, stream)
+    idx.close()
     del X
     torch.cuda.empty_cache()
     N, n = c2["N"], c2["n"]
@@ -392,7 +443,8 @@ def build_split(args, dev, stream):
                           "achieved_gbs": summ_bytes / (ph["summarise"] / 1e3) / 1e9,
                           "frac": summ_bytes / (ph["summarise"] / 1e3) / 1e9 / pk,
                           "algorithmic_bytes": summ_bytes,
-                          "what": "per series: 4n B of rows read; 16 B of symbols, 8 B of key, 4 B of row id written"}}
+                          "what": "per series: 4n B of rows read; 16 B of symbols, 8 B of key, 4 B of row id written"},
+            "tc_vs_lut": tc}
 
 
 # DTW band DP roofline: a cell costs one FADD + one FFMA on the FMA pipe (plus

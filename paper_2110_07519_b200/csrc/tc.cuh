@@ -13,16 +13,17 @@
 // the raw row, the fp64 canonical re-rank of every near tie (k_tc_verify: q8i_bound_pass +
 // exact_pass of the fused path), i.e. "exactly re-refined in fp32" (north_star).
 //
-// Kernel k_ed_tc (persistent, one CTA per SM, 6 warps):
+// Kernel k_ed_tc (persistent, one CTA per SM, 10 warps):
 //   warp 0      TMA producer: 128-row tiles of rows8 (SWIZZLE_128B, n/128 boxes of 128 x 128
 //               bytes per tile) into a kTcStages-deep shared-memory ring; the queries' int8
 //               block (<= 256 x n bytes) once.
 //   warp 1      MMA issuer (one lane): M = 128 rows x N = nq (padded to 16) queries, K = 32
 //               bytes per tcgen05.mma, into one of two TMEM accumulators (2 x 256 columns).
-//   warps 2..5  epilogue: tcgen05.ld of the tile's dot products (thread = TMEM lane = row),
-//               the survival test in fp32 with directed rounding (every quantity that enters
-//               the threshold is rounded towards keeping), survivors appended to the query's
-//               candidate list.
+//   warps 2..9  epilogue (two groups of four, one per TMEM accumulator, i.e. alternate tiles;
+//               warp & 3 = its TMEM lane quarter): tcgen05.ld
+//               of the tile's dot products (thread = TMEM lane = row), the survival test in
+//               paired fp32 with directed rounding (every quantity that enters the threshold
+//               is rounded towards keeping), survivors appended to the query's candidate list.
 // Shapes: n = 128 or 256 (one or two 128-byte K chunks); <= 256 queries per pass.
 #pragma once
 #include <cuda.h>
@@ -35,14 +36,15 @@ namespace messi {
 constexpr int kTcRows = 128;     // rows per tile (UMMA M)
 constexpr int kTcMaxQ = 256;     // queries per pass (UMMA N <= 256)
 constexpr int kTcStages = 4;     // A-tile ring depth
-constexpr int kTcThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue
+constexpr int kTcEpiWarps = 8;   // two groups of four (one per accumulator, alternate tiles)
+constexpr int kTcThreads = 32 * (2 + kTcEpiWarps);  // warp 0 TMA, warp 1 MMA, then the epilogue
 constexpr unsigned kTcCandCap = 65536;  // candidates per query; more -> exhaustive fallback
 
 __host__ __device__ inline size_t tc_smem_bytes(int n)
 {
     const size_t kch = (size_t)n / 128;
-    // 1024 B alignment slack + B block + A ring + per-query parameters (float4 x 256)
-    return 1024 + kch * kTcMaxQ * 128 + (size_t)kTcStages * kch * kTcRows * 128 + (size_t)kTcMaxQ * 16;
+    // 1024 B alignment slack + B block + A ring
+    return 1024 + kch * kTcMaxQ * 128 + (size_t)kTcStages * kch * kTcRows * 128;
 }
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -60,15 +62,18 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* b)
 {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// Waits for the phase of parity `parity` to complete; the suspend-time hint lets the hardware
+// park the waiting thread until then instead of spinning on issue slots the epilogue needs.
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity)
 {
     const unsigned a = smem_u32(b);
     unsigned ok = 0;
     while (!ok) {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-                     : "=r"(ok)
-                     : "r"(a), "r"(parity)
-                     : "memory");
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
     }
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, unsigned long long* bar)
@@ -108,6 +113,31 @@ __device__ __forceinline__ void umma_i8(unsigned d_tmem, unsigned long long a_de
 __device__ __forceinline__ void umma_commit(unsigned long long* bar)
 {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+// tcgen05.ld of 32 columns without the wait (the registers are valid only after tmem_wait).
+__device__ __forceinline__ void tmem_ld32_async(unsigned taddr, int (&v)[32])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+// tcgen05.wait::ld, with v as read-write operands so no use of v is scheduled before it.
+__device__ __forceinline__ void tmem_wait(int (&v)[32])
+{
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]),
+                   "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]),
+                   "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]),
+                   "+r"(v[30]), "+r"(v[31])
+                 :
                  : "memory");
 }
 
@@ -199,6 +229,61 @@ __device__ __forceinline__ float4 tc_query_params(const QState* st)
                        0.0f);
 }
 
+// The survival test of a row against two columns (queries j, j+1) at once, paired fp32 ops with
+// directed rounding.  With X = float(D + C) (C = 1.5 * 2^23: exact for |D| < 2^22, n <= 256),
+//   t1 = fma_rd(nw, b_j, a_j) <= a_j + nw b_j,   T2 = fma_rd(v, r_j, u C) <= v r_j + u C,
+//   diff = (u X - T2) - t1  (round to nearest),
+// u X - T2 >= u D - v r_j exactly, so whenever the exact test u D >= a_j + v r_j + nw b_j holds,
+// the rounded diff is >= 0 (rounding is monotone and t1 is representable).  UNIFORM_R: every
+// query of the pass has the same scale, so T2 is one value per row (hoisted).
+constexpr float kTcMagic = 12582912.0f;  // 1.5 * 2^23
+template <bool UNIFORM_R>
+__device__ __forceinline__ float2 tc_diff2(int d0, int d1, float2 a, float2 r, float2 bq, float u, float v, float nw,
+                                           float uC, float T2u)
+{
+    const float2 t1 = ffma2_rd(make_float2(nw, nw), bq, a);
+    const float2 T2 = UNIFORM_R ? make_float2(T2u, T2u) : ffma2_rd(make_float2(v, v), r, make_float2(uC, uC));
+    const float2 X = make_float2(__int_as_float(d0 + 0x4B400000), __int_as_float(d1 + 0x4B400000));
+    const float2 y = ffma2(make_float2(u, u), X, make_float2(-T2.x, -T2.y));
+    return fadd2(y, make_float2(-t1.x, -t1.y));
+}
+
+// Epilogue of one 32-column chunk: the chunk's max diff over its columns; survivors (diff >= 0,
+// rare) appended to their queries' candidate lists.
+template <bool UNIFORM_R>
+__device__ __forceinline__ void tc_chunk(const int (&d)[32], int c0, const float* qa, const float* qr, const float* qb,
+                                        float u, float v, float nw, float uC, float T2u, bool valid, long long pos, int nq,
+                                        QState* st_all, unsigned* __restrict__ cand)
+{
+    float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+    for (int jj = 0; jj < 32; jj += 4) {
+        const float2 df0 = tc_diff2<UNIFORM_R>(d[jj], d[jj + 1], *reinterpret_cast<const float2*>(qa + c0 + jj),
+                                               *reinterpret_cast<const float2*>(qr + c0 + jj),
+                                               *reinterpret_cast<const float2*>(qb + c0 + jj), u, v, nw, uC, T2u);
+        const float2 df1 = tc_diff2<UNIFORM_R>(d[jj + 2], d[jj + 3], *reinterpret_cast<const float2*>(qa + c0 + jj + 2),
+                                               *reinterpret_cast<const float2*>(qr + c0 + jj + 2),
+                                               *reinterpret_cast<const float2*>(qb + c0 + jj + 2), u, v, nw, uC, T2u);
+        m0 = max3f(m0, df0.x, df0.y);
+        m1 = max3f(m1, df1.x, df1.y);
+    }
+    if (valid && fmaxf(m0, m1) >= 0.0f) {  // rare: a survivor in this chunk -- find and append it
+        for (int jj = 0; jj < 32; jj += 2) {
+            const float2 df = tc_diff2<UNIFORM_R>(d[jj], d[jj + 1], *reinterpret_cast<const float2*>(qa + c0 + jj),
+                                                  *reinterpret_cast<const float2*>(qr + c0 + jj),
+                                                  *reinterpret_cast<const float2*>(qb + c0 + jj), u, v, nw, uC, T2u);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = c0 + jj + h;
+                if ((h ? df.y : df.x) >= 0.0f && j < nq) {
+                    const unsigned slot = atomicAdd(&st_all[j].cand_count, 1u);
+                    if (slot < kTcCandCap) cand[(size_t)j * kTcCandCap + slot] = (unsigned)pos;
+                }
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kTcThreads, 1) k_ed_tc(const __grid_constant__ CUtensorMap tmA,
                                                           const __grid_constant__ CUtensorMap tmB, long long ntc,
                                                           long long N, int n, int nq, const float4* __restrict__ tcm,
@@ -207,19 +292,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_ed_tc(const __grid_constant__
     extern __shared__ __align__(16) unsigned char tc_dsm[];
     __shared__ unsigned long long full_a[kTcStages], empty_a[kTcStages], full_b, tm_full[2], tm_empty[2];
     __shared__ unsigned tmem_base_s;
+    __shared__ __align__(16) float qa_s[kTcMaxQ], qr_s[kTcMaxQ], qb_s[kTcMaxQ];  // a_j, r_j, b_j
+    __shared__ int nonuniform_s;
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<size_t>(tc_dsm) + 1023) & ~(size_t)1023);
     const int kch = n / 128;
     unsigned char* B_s = base;                                   // kch x [256 rows x 128 B]
     unsigned char* A_s = B_s + (size_t)kch * kTcMaxQ * 128;      // kTcStages x kch x [128 rows x 128 B]
-    float4* qp_s = reinterpret_cast<float4*>(A_s + (size_t)kTcStages * kch * kTcRows * 128);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int Nm = max(16, (nq + 15) & ~15);  // MMA N
     const unsigned stage_bytes = (unsigned)kch * kTcRows * 128;
 
     if (threadIdx.x == 0) {
+        nonuniform_s = 0;
         for (int s = 0; s < kTcStages; ++s) { mbar_init(&full_a[s], 1); mbar_init(&empty_a[s], 1); }
         mbar_init(&full_b, 1);
-        for (int a = 0; a < 2; ++a) { mbar_init(&tm_full[a], 1); mbar_init(&tm_empty[a], 4); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tm_full[a], 1); mbar_init(&tm_empty[a], kTcEpiWarps / 2); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {  // two accumulators of 256 columns
@@ -228,12 +315,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_ed_tc(const __grid_constant__
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    for (int j = threadIdx.x; j < kTcMaxQ; j += blockDim.x)
-        qp_s[j] = j < nq ? tc_query_params(st_all + j) : make_float4(INFINITY, 1.0f, 0.0f, 0.0f);
+    for (int j = threadIdx.x; j < kTcMaxQ; j += blockDim.x) {
+        // columns past the batch: a = +inf makes rhs +inf, diff -inf (never kept)
+        const float4 qp = j < nq ? tc_query_params(st_all + j) : make_float4(INFINITY, 1.0f, 0.0f, 0.0f);
+        qa_s[j] = qp.x;
+        qr_s[j] = qp.y;
+        qb_s[j] = qp.z;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < nq; j += blockDim.x)
+        if (qr_s[j] != qr_s[0]) nonuniform_s = 1;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const unsigned tmem = tmem_base_s;
+    const bool uniform_r = nonuniform_s == 0;
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
@@ -275,39 +371,48 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_ed_tc(const __grid_constant__
                 umma_commit(&tm_full[acc]);
             }
         }
-    } else {  // ---------------- epilogue: warps 2..5, TMEM lane quarter warp & 3
-        const int qtr = warp & 3;
-        long long it = 0;
-        for (long long t = blockIdx.x; t < ntc; t += gridDim.x, ++it) {
-            const int acc = (int)(it & 1);
+    } else {  // ---------------- epilogue: group g = (warp - 2) / 4 takes the tiles of accumulator g (every
+              // other tile), warp & 3 is its TMEM lane quarter; the two groups overlap their tiles
+        const int qtr = warp & 3, grp = (warp - 2) >> 2;
+        const int nchunks = (Nm + 31) / 32;
+        long long it = grp;
+        long long t = (long long)blockIdx.x + (long long)grp * gridDim.x;
+        const long long step = 2LL * gridDim.x;
+        // the row terms (u, v, nw, 0) of this thread's row, loaded one tile ahead
+        float4 rm_next = t < ntc ? tcm[t * kTcRows + qtr * 32 + lane] : make_float4(0, 0, 0, 0);
+        for (; t < ntc; t += step, it += 2) {
+            const int acc = grp;
             const unsigned aph = (unsigned)((it >> 1) & 1);
-            mbar_wait(&tm_full[acc], aph);
-            tc_fence_after();
             const long long pos = t * kTcRows + qtr * 32 + lane;
             const bool valid = pos < N;
-            const float4 rm = tcm[pos];
+            const float4 rm = rm_next;
+            if (t + step < ntc) rm_next = tcm[(t + step) * kTcRows + qtr * 32 + lane];
+            const float u = rm.x, v = rm.y, nw = rm.z, uC = rm.x * kTcMagic;
+            const float T2u = __fmaf_rd(v, qr_s[0], uC);  // the row's T2 when every query has scale 1/qr_s[0]
+            mbar_wait(&tm_full[acc], aph);
+            tc_fence_after();
             const unsigned taddr = tmem + ((unsigned)(qtr * 32) << 16) + (unsigned)acc * 256u;
-            for (int c0 = 0; c0 < Nm; c0 += 32) {
-                int v[32];
-                tmem_ld32(taddr + (unsigned)c0, v);
-                unsigned hit = 0;
-#pragma unroll
-                for (int jj = 0; jj < 32; ++jj) {
-                    const float4 qp = qp_s[c0 + jj];
-                    const float rhs = __fmaf_rd(rm.y, qp.y, __fmaf_rd(rm.z, qp.z, qp.x));
-                    hit |= (rm.x * (float)v[jj] >= rhs ? 1u : 0u) << jj;
-                }
-                if (hit && valid) {
-                    while (hit) {
-                        const int jj = __ffs(hit) - 1;
-                        hit &= hit - 1;
-                        const int j = c0 + jj;
-                        if (j < nq) {
-                            const unsigned slot = atomicAdd(&st_all[j].cand_count, 1u);
-                            if (slot < kTcCandCap) cand[(size_t)j * kTcCandCap + slot] = (unsigned)pos;
-                        }
-                    }
-                }
+            // two chunks in flight: the next chunk's tcgen05.ld overlaps this chunk's test
+            int dA[32], dB[32];
+            auto test = [&](const int (&d)[32], int c0) {
+                if (uniform_r)
+                    tc_chunk<true>(d, c0, qa_s, qr_s, qb_s, u, v, nw, uC, T2u, valid, pos, nq, st_all, cand);
+                else
+                    tc_chunk<false>(d, c0, qa_s, qr_s, qb_s, u, v, nw, uC, T2u, valid, pos, nq, st_all, cand);
+            };
+            tmem_ld32_async(taddr, dA);
+            tmem_wait(dA);
+            for (int ch = 0; ch < nchunks; ch += 2) {
+                const bool more = ch + 1 < nchunks;
+                if (more) tmem_ld32_async(taddr + (unsigned)((ch + 1) * 32), dB);
+                test(dA, ch * 32);
+                if (!more) break;
+                tmem_wait(dB);
+                const bool more2 = ch + 2 < nchunks;
+                if (more2) tmem_ld32_async(taddr + (unsigned)((ch + 2) * 32), dA);
+                test(dB, (ch + 1) * 32);
+                if (!more2) break;
+                tmem_wait(dA);
             }
             tc_fence_before();
             __syncwarp();
