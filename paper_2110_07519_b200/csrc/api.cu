@@ -87,13 +87,15 @@ struct messi_index {
     // shards sharing each query's best-so-far (PeerSet): their per-set state arrays, the
     // IPC mappings to close, and the launch epoch (identical on every shard for the same
     // sequence of calls)
-    QState* peer_st[2][MESSI_MAX_PEERS] = {};
-    void* peer_ipc[2][MESSI_MAX_PEERS] = {};
+    QState* peer_st[3][MESSI_MAX_PEERS] = {};   // sets 0, 1: ED batch states; 2: DTW slot states
+    void* peer_ipc[3][MESSI_MAX_PEERS] = {};
     QState** d_peers = nullptr;  // device copy of peer_st
     int npeers = 0;
     unsigned epoch = 0;
     int fused_grid = 0;
     unsigned link_gen = 0;  // links made so far (the high byte of every epoch: see launch_ed_group)
+    unsigned dtw_epoch = 0;  // DTW queries since the link (the low bits of the DTW path's epoch)
+    QState* slot_st = nullptr;  // the DTW slots' states, contiguous (one IPC handle for all)
     // inspection scratch (messi_debug_*, allocated on first use): inverse permutation, row ->
     // index map of the ids being inspected, tile iota, per-id outputs
     unsigned* dbg_inv = nullptr;
@@ -258,7 +260,7 @@ static bool use_strip(int n, int R, bool have_band)
 }
 
 static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R, const float* q_dev, cudaStream_t rs,
-                                 KnnState* knn, int kk)
+                                 KnnState* knn, int kk, PeerSet ps, int slot)
 {
     const int H = strip_rows(R);
     const int rem = (2 * R - 2 * H + 3) % H;
@@ -273,7 +275,7 @@ static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R,
         const char* oe = getenv("MESSI_DTW_REFINE_OCC"); /* experiments: CTAs per SM */                          \
         if (oe && atoi(oe) > 0 && atoi(oe) < occ) occ = atoi(oe);                                                \
         k_refine_dtw_strip<HH, REM, KK, TT><<<idx->sms * (occ > 0 ? occ : 1), TT, smem, rs>>>(                   \
-            idx->rows, n, R, q_dev, sl.U, sl.L, sl.list2, (unsigned)idx->N, sl.st, sl.near, knn, kk);            \
+            idx->rows, n, R, q_dev, sl.U, sl.L, sl.list2, (unsigned)idx->N, sl.st, sl.near, knn, kk, ps, slot);  \
         launched = true;                                                                                         \
     }
     MESSI_STRIP_VARIANTS(LAUNCH_S)
@@ -376,8 +378,12 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     if ((s = dalloc(&idx->rows8, npadrows * (size_t)n)) || (s = dalloc(&idx->meta8, npadrows))) return bail(s);
     if ((s = dalloc(&idx->skey, (size_t)N)) || (s = dalloc(&idx->perm, (size_t)N))) return bail(s);
     if ((s = dalloc(&idx->beta32, 256)) || (s = dalloc(&idx->lo_w, 256)) || (s = dalloc(&idx->hi_w, 256))) return bail(s);
+    if ((s = dalloc(&idx->slot_st, MESSI_DTW_SLOTS))) return bail(s);
+    if (cudaMemset(idx->slot_st, 0, sizeof(QState) * MESSI_DTW_SLOTS) != cudaSuccess)  // gbsf = 0: no epoch
+        return bail(fail(MESSI_ECUDA, "memset"));
+    for (int i = 0; i < MESSI_DTW_SLOTS; ++i) idx->slot[i].st = idx->slot_st + i;
     for (Slot& sl : idx->slot) {
-        if ((s = dalloc(&sl.st, 1)) || (s = dalloc(&sl.lut, MESSI_W * MESSI_CARD)) || (s = dalloc(&sl.tab, kScanTab)) ||
+        if ((s = dalloc(&sl.lut, MESSI_W * MESSI_CARD)) || (s = dalloc(&sl.tab, kScanTab)) ||
             (s = dalloc(&sl.U, n)) || (s = dalloc(&sl.L, n)) || (s = dalloc(&sl.tlist, (size_t)idx->ntiles)))
             return bail(s);
         if (cudaEventCreateWithFlags(&sl.ev_seed, cudaEventDisableTiming) != cudaSuccess ||
@@ -486,7 +492,7 @@ extern "C" void messi_free(messi_index* idx)
     void* ptrs[] = {idx->tiles, idx->sym8, idx->boxes, idx->sboxes, idx->paa, idx->skey, idx->perm, idx->beta32, idx->lo_w,
                     idx->hi_w,  idx->qbuf,  idx->res1, idx->resk, idx->stats1, idx->rows8, idx->meta8,
                     idx->dbg_inv, idx->dbg_map, idx->dbg_iota, idx->dbg_gbuf, idx->tc.bst, idx->tc.qc, idx->tc.cand,
-                    idx->tc.tcm};
+                    idx->tc.tcm, idx->slot_st};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& row : idx->peer_ipc)
@@ -499,7 +505,7 @@ extern "C" void messi_free(messi_index* idx)
             if (p) cudaFree(p);
     }
     for (Slot& sl : idx->slot) {
-        void* sp[] = {sl.st, sl.lut, sl.tab, sl.U, sl.L, sl.cand, sl.list2, sl.near, sl.tlist, sl.rbuf, sl.knn, sl.seedd};
+        void* sp[] = {sl.lut, sl.tab, sl.U, sl.L, sl.cand, sl.list2, sl.near, sl.tlist, sl.rbuf, sl.knn, sl.seedd};
         for (void* p : sp)
             if (p) cudaFree(p);
         cudaEvent_t es[] = {sl.ev_seed, sl.ev_scan, sl.ev_lbk, sl.ev_refined, sl.ev_done};
@@ -666,21 +672,21 @@ static int filter_grid(const messi_index* idx)
 }
 
 // Box filter of every tile (side stream, right after the seed: needs BSF0 and the query PAA).
-static messi_status launch_tile_filter(messi_index* idx, Slot& sl, cudaStream_t st)
+static messi_status launch_tile_filter(messi_index* idx, Slot& sl, cudaStream_t st, PeerSet ps = PeerSet{nullptr, 0, 0u})
 {
     k_tile_filter<<<filter_grid(idx), 256, 0, st>>>(idx->boxes, idx->ntiles, idx->n / MESSI_W, idx->lo_w, idx->hi_w,
-                                                   sl.st, sl.tlist, nullptr);
+                                                   sl.st, sl.tlist, nullptr, ps.epoch);
     LAUNCHED(idx);
     return MESSI_OK;
 }
 
-static messi_status launch_scan(messi_index* idx, Slot& sl, cudaStream_t next)
+static messi_status launch_scan(messi_index* idx, Slot& sl, cudaStream_t next, PeerSet peers)
 {
     CK(cudaStreamWaitEvent(idx->stream, sl.ev_seed, 0));
     {
         ProfScope ps(idx, K_SCAN, idx->stream);
         k_scan<<<scan_grid(idx), 32 * kScanWarps, scan_smem(), idx->stream>>>(idx->tiles, idx->sym8, idx->N, sl.tab,
-                                                                              sl.st, sl.cand, sl.tlist);
+                                                                              sl.st, sl.cand, sl.tlist, peers.epoch);
         LAUNCHED(idx);
     }
     CK(cudaEventRecord(sl.ev_scan, idx->stream));
@@ -691,8 +697,8 @@ static messi_status launch_scan(messi_index* idx, Slot& sl, cudaStream_t next)
 static messi_status ensure_batch_buffers(messi_index* idx)
 {
     if (idx->bset[0].bst) return MESSI_OK;
-    TRY(dalloc(&idx->d_peers, 2 * MESSI_MAX_PEERS));
-    CK(cudaMemset(idx->d_peers, 0, sizeof(QState*) * 2 * MESSI_MAX_PEERS));
+    TRY(dalloc(&idx->d_peers, 3 * MESSI_MAX_PEERS));
+    CK(cudaMemset(idx->d_peers, 0, sizeof(QState*) * 3 * MESSI_MAX_PEERS));
     for (auto& bs : idx->bset) {
         TRY(dalloc(&bs.bst, kBatchMax));
         CK(cudaMemset(bs.bst, 0, sizeof(QState) * kBatchMax));  // gbsf = 0: no epoch
@@ -740,7 +746,7 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
         if (knn) {
             int np = 1;
             while (np < len) np <<= 1;
-            k_seed_select<<<B, 1024, (size_t)np * sizeof(float), st>>>(seed_d, idx->window, k, bs.bst, peers);
+            k_seed_select<<<B, 1024, (size_t)np * sizeof(float), st>>>(seed_d, idx->window, k, bs.bst, peers, -1);
             LAUNCHED(idx);
         }
         const long long nsuper = (idx->ntiles + kSuperTiles - 1) / kSuperTiles;
@@ -824,7 +830,7 @@ static messi_status launch_lbk_filter(messi_index* idx, Slot& sl, int reach, boo
 
 // DTW step 2: banded fp32 DTW of the list2 entries (near-best entries to sl.near).
 static messi_status launch_dtw_refine(messi_index* idx, Slot& sl, int reach, bool strip, const float* q_dev,
-                                      cudaStream_t rs, int kk = 1)
+                                      cudaStream_t rs, int kk = 1, PeerSet ps = PeerSet{nullptr, 0, 0u}, int slot = 0)
 {
     KnnState* knn = kk > 1 ? sl.knn : nullptr;
     const int n = idx->n;
@@ -832,7 +838,7 @@ static messi_status launch_dtw_refine(messi_index* idx, Slot& sl, int reach, boo
     const size_t qsm = (size_t)npad * sizeof(float);
     bool launched = false;
     if (strip) {
-        TRY(launch_strip(idx, sl, n, reach, q_dev, rs, knn, kk));
+        TRY(launch_strip(idx, sl, n, reach, q_dev, rs, knn, kk, ps, slot));
         launched = true;
     }
 #define LAUNCH_R(R)                                                                                           \
@@ -841,7 +847,7 @@ static messi_status launch_dtw_refine(messi_index* idx, Slot& sl, int reach, boo
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_dtw<R>, 128, 3 * qsm));               \
         k_refine_dtw<R><<<idx->sms * (occ > 0 ? occ : 1), 128, 3 * qsm, rs>>>(idx->rows, n, q_dev, sl.U, sl.L, \
                                                                             sl.list2, (unsigned)idx->N, sl.st, \
-                                                                            sl.near, knn, kk);                \
+                                                                            sl.near, knn, kk, ps, slot);      \
         launched = true;                                                                                      \
     }
     MESSI_DTW_REACHES(LAUNCH_R)
@@ -849,7 +855,7 @@ static messi_status launch_dtw_refine(messi_index* idx, Slot& sl, int reach, boo
     if (!launched) {
         const int wr = warps_for((size_t)4 * npad * sizeof(float), 8);
         k_refine_dtw_warp<<<idx->sms * 4, 32 * wr, qsm + (size_t)wr * 4 * npad * sizeof(float), rs>>>(
-            idx->rows, n, reach, q_dev, sl.list2, (unsigned)idx->N, sl.st, sl.near, knn, kk);
+            idx->rows, n, reach, q_dev, sl.list2, (unsigned)idx->N, sl.st, sl.near, knn, kk, ps, slot);
     }
     LAUNCHED(idx);
     return MESSI_OK;
@@ -869,8 +875,18 @@ static messi_status ensure_dtw_knn(messi_index* idx)
 static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, messi_result* res, messi_stats* stats,
                             int kk = 1)
 {
-    Slot& sl = idx->slot[idx->qcount++ % MESSI_DTW_SLOTS];
+    const int slot = (int)(idx->qcount++ % MESSI_DTW_SLOTS);
+    Slot& sl = idx->slot[slot];
     const bool ser = serial_mode(idx);
+    // shards linked: the slot's best-so-far is shared with the peers' same slot (the same
+    // query when the shards make the same DTW calls since the link), tagged like the ED path
+    PeerSet peers{nullptr, 0, 0u};
+    if (idx->npeers > 0) {
+        idx->dtw_epoch = (idx->dtw_epoch + 1) & 0xffffffu;
+        peers.st = idx->d_peers + 2 * MESSI_MAX_PEERS;
+        peers.n = idx->npeers;
+        peers.epoch = ((idx->link_gen & 0xffu) << 24) | idx->dtw_epoch;
+    }
     cudaStream_t side = ser ? idx->stream : idx->side;
     cudaStream_t rs = ser ? idx->stream : idx->rstr;
     const int n = idx->n;
@@ -891,19 +907,18 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
         ProfScope ps(idx, K_SEED, side);
         k_seed_dtw<<<seed_grid, 32 * wf, qsm + wf * seed_warp, side>>>(
             q_dev, n, reach, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32, idx->lo_w, idx->hi_w,
-            sl.lut, sl.tab, sl.U, sl.L, sl.st, kk > 1 ? sl.seedd : nullptr);
+            sl.lut, sl.tab, sl.U, sl.L, sl.st, kk > 1 ? sl.seedd : nullptr, peers, slot);
         LAUNCHED(idx);
         if (kk > 1) {  // BSF0 = the k-th smallest window distance
             int np = 1;
             while (np < len) np <<= 1;
-            PeerSet none{nullptr, 0, 0u};
-            k_seed_select<<<1, 1024, (size_t)np * sizeof(float), side>>>(sl.seedd, idx->window, kk, sl.st, none);
+            k_seed_select<<<1, 1024, (size_t)np * sizeof(float), side>>>(sl.seedd, idx->window, kk, sl.st, peers, slot);
             LAUNCHED(idx);
         }
-        TRY(launch_tile_filter(idx, sl, side));
+        TRY(launch_tile_filter(idx, sl, side, peers));
     }
     CK(cudaEventRecord(sl.ev_seed, side));
-    TRY(launch_scan(idx, sl, rs));
+    TRY(launch_scan(idx, sl, rs, peers));
     const bool strip = dtw_uses_strip(n, reach);
     {
         ProfScope ps(idx, K_LBK, rs);
@@ -916,7 +931,7 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     CK(cudaStreamWaitEvent(rs, sl.ev_lbk, 0));
     {
         ProfScope ps(idx, K_REFINE, rs);
-        TRY(launch_dtw_refine(idx, sl, reach, strip, q_dev, rs, kk));
+        TRY(launch_dtw_refine(idx, sl, reach, strip, q_dev, rs, kk, peers, slot));
     }
     // the exact resolve of this query overlaps the next query's refine (another slot)
     CK(cudaEventRecord(sl.ev_refined, rs));
@@ -1215,11 +1230,11 @@ extern "C" messi_status messi_query_ed_tc_batch(messi_index* idx, const float* q
 extern "C" messi_status messi_batch_state_ipc(messi_index* idx, int32_t set, void* handle_out)
 {
     g_err[0] = 0;
-    if (!idx || !handle_out || set < 0 || set > 1) return fail(MESSI_EINVAL, "bad argument");
+    if (!idx || !handle_out || set < 0 || set > 2) return fail(MESSI_EINVAL, "bad argument");
     CK(cudaSetDevice(idx->device));
     TRY(ensure_batch_buffers(idx));
     cudaIpcMemHandle_t h;
-    CK(cudaIpcGetMemHandle(&h, idx->bset[set].bst));
+    CK(cudaIpcGetMemHandle(&h, set < 2 ? idx->bset[set].bst : idx->slot_st));
     memcpy(handle_out, &h, sizeof h);
     return MESSI_OK;
 }
@@ -1240,7 +1255,7 @@ static messi_status unlink_peers(messi_index* idx)
 
 static messi_status upload_peers(messi_index* idx)
 {
-    CK(cudaMemcpy(idx->d_peers, &idx->peer_st[0][0], sizeof(QState*) * 2 * MESSI_MAX_PEERS, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(idx->d_peers, &idx->peer_st[0][0], sizeof(QState*) * 3 * MESSI_MAX_PEERS, cudaMemcpyHostToDevice));
     return MESSI_OK;
 }
 
@@ -1254,9 +1269,9 @@ extern "C" messi_status messi_link_peers_ipc(messi_index* idx, const void* handl
     TRY(unlink_peers(idx));
     const unsigned char* h = static_cast<const unsigned char*>(handles);
     for (int i = 0; i < npeers; ++i)
-        for (int set = 0; set < 2; ++set) {
+        for (int set = 0; set < 3; ++set) {
             cudaIpcMemHandle_t mh;
-            memcpy(&mh, h + ((size_t)i * 2 + set) * sizeof(cudaIpcMemHandle_t), sizeof mh);
+            memcpy(&mh, h + ((size_t)i * 3 + set) * sizeof(cudaIpcMemHandle_t), sizeof mh);
             void* p = nullptr;
             cudaError_t e = cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess);
             if (e != cudaSuccess) {
@@ -1269,6 +1284,7 @@ extern "C" messi_status messi_link_peers_ipc(messi_index* idx, const void* handl
     idx->npeers = npeers;
     idx->link_gen = (idx->link_gen + 1) % 255 + 1;  // never 0: epoch 0 means unlinked
     idx->epoch = 0;
+    idx->dtw_epoch = 0;
     return upload_peers(idx);
 }
 
@@ -1292,10 +1308,12 @@ extern "C" messi_status messi_link_peers_local(messi_index* idx, messi_index* co
         TRY(ensure_batch_buffers(peers[i]));
         CK(cudaSetDevice(idx->device));
         for (int set = 0; set < 2; ++set) idx->peer_st[set][i] = peers[i]->bset[set].bst;
+        idx->peer_st[2][i] = peers[i]->slot_st;
     }
     idx->npeers = npeers;
     idx->link_gen = (idx->link_gen + 1) % 255 + 1;
     idx->epoch = 0;
+    idx->dtw_epoch = 0;
     return upload_peers(idx);
 }
 
@@ -1460,7 +1478,7 @@ static messi_status debug_prologue(messi_index* idx, const float* query_dev, int
     k_seed_dtw<<<1, 32, 2 * qsm + 3 * (size_t)n * sizeof(float), st>>>(query_dev, n, reach < 0 ? 0 : reach, idx->rows,
                                                                       idx->skey, idx->perm, idx->N, 1, idx->beta32,
                                                                       idx->lo_w, idx->hi_w, sl.lut, sl.tab, sl.U, sl.L,
-                                                                      sl.st, nullptr);
+                                                                      sl.st, nullptr, PeerSet{nullptr, 0, 0u}, 0);
     LAUNCHED(idx);
     k_arm<<<1, 1, 0, st>>>(sl.st);
     LAUNCHED(idx);
@@ -1522,7 +1540,7 @@ extern "C" messi_status messi_debug_lower_bounds(messi_index* idx, const float* 
     LAUNCHED(idx);
     CK(cudaMemsetAsync(lb_dev, 0xff, sizeof(float) * (size_t)idx->N, s));  // NaN: not written
     k_scan<<<scan_grid(idx), 32 * kScanWarps, scan_smem(), s>>>(idx->tiles, idx->sym8, idx->N, tab, st, sl.cand,
-                                                                idx->dbg_iota);
+                                                                idx->dbg_iota, 0u);
     LAUNCHED(idx);
     k_dbg_scatter_cand<<<idx->sms * 8, 256, 0, s>>>(sl.cand, st, idx->perm, lb_dev);
     LAUNCHED(idx);
@@ -1568,7 +1586,7 @@ extern "C" messi_status messi_debug_tile_bounds(messi_index* idx, const float* q
         TRY(debug_prologue(idx, query_dev, reach));
         Slot& sl = idx->slot[0];
         k_tile_filter<<<filter_grid(idx), 256, 0, s>>>(idx->boxes, idx->ntiles, idx->n / MESSI_W, idx->lo_w, idx->hi_w,
-                                                      sl.st, nullptr, lb_dev);
+                                                      sl.st, nullptr, lb_dev, 0u);
         LAUNCHED(idx);
     }
     CK(cudaStreamSynchronize(s));
@@ -1704,7 +1722,7 @@ extern "C" messi_status messi_debug_scan_repeat(messi_index* idx, const float* q
         k_reset_cand<<<1, 1, 0, st>>>(sl.st);
         CK(cudaEventRecord(ev[2 * r], st));
         k_scan<<<scan_grid(idx), 32 * kScanWarps, scan_smem(), st>>>(idx->tiles, idx->sym8, idx->N, sl.tab, sl.st, sl.cand,
-                                                                     sl.tlist);
+                                                                     sl.tlist, 0u);
         CK(cudaEventRecord(ev[2 * r + 1], st));
     }
     idx->launches += 2 * reps;

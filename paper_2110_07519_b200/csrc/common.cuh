@@ -11,6 +11,24 @@
 #define MESSI_MAX_N 8192
 #define MESSI_MAX_PEERS 8          // shards that share each query's best-so-far (batched ED)
 
+// Bounds checks of the checked build (-DMESSI_CHECKED, tools/checked.sh): every computed
+// index into a list, buffer or shared array is asserted against its capacity and a violation
+// traps the kernel (the CUDA call then fails loudly).  No code in the normal build.
+#ifdef MESSI_CHECKED
+#define MESSI_CHECK(cond)                                                                                         \
+    do {                                                                                                          \
+        if (!(cond)) {                                                                                            \
+            printf("MESSI_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, blockIdx.x,   \
+                   threadIdx.x);                                                                                  \
+            __trap();                                                                                             \
+        }                                                                                                         \
+    } while (0)
+#else
+#define MESSI_CHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
+
 namespace messi {
 
 // Relative slack on every prune / abandon / near-tie test:

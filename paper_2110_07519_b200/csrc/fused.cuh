@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(256) k_seed_batch(const float* __restrict__ qu
 // k-NN seed: the k-th smallest fp32 distance of the window (a distance k rows achieve) is
 // BSF0; one CTA per query sorts the window's distances in shared memory (bitonic).
 __global__ void __launch_bounds__(1024) k_seed_select(const float* __restrict__ seed_d, int seed_cap, int k,
-                                                      QState* st_all, PeerSet ps)
+                                                      QState* st_all, PeerSet ps, int slot)
 {
     extern __shared__ float sv[];
     const int b = blockIdx.x;
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(1024) k_seed_select(const float* __restrict__ 
             __syncthreads();
         }
     if (threadIdx.x == 0 && len >= k && sv[k - 1] < INFINITY) {
-        bsf_publish(st, ps, b, sv[k - 1]);
+        bsf_publish(st, ps, slot >= 0 ? slot : b, sv[k - 1]);  // slot: a DTW slot (its peers' index)
         atomicMin(&st->seed_bits, __float_as_uint(sv[k - 1]));
     }
 }
@@ -346,6 +346,8 @@ __global__ void __launch_bounds__(256) k_filter_batch(const uint4* __restrict__ 
                     basef = __shfl_sync(0xffffffffu, basef, 0);
                     baseb = __shfl_sync(0xffffffffu, baseb, 0);
                     uint2* tl = tlist_all + (size_t)(b0 + qq) * ntiles;
+                    MESSI_CHECK(!(keep && near) || basef + __popc(mf & ((1u << lane) - 1)) + baseb < (unsigned)ntiles);
+                    MESSI_CHECK(!(keep && !near) || baseb + __popc(mb & ((1u << lane) - 1)) + basef < (unsigned)ntiles);
                     if (keep && near)
                         tl[basef + __popc(mf & ((1u << lane) - 1))] = make_uint2((unsigned)t, __float_as_uint(lb));
                     if (keep && !near)
@@ -773,6 +775,7 @@ struct FusedCtx {
     PeerSet ps;
     Q8Query qq;
     int n, b, k;
+    long long npad;  // sorted positions (checked build)
 };
 
 template <bool LINKED, bool KNN>
@@ -808,6 +811,8 @@ __device__ __forceinline__ void fine_and_refine(const FusedCtx& cx, long long ti
         const unsigned pass = __ballot_sync(0xffffffffu, ok);
         if (pass) {
             if (ok) {
+                MESSI_CHECK(ncb + __popc(pass & ((1u << lane) - 1)) < (unsigned)kCandBuf);
+                MESSI_CHECK(pos < (unsigned)(cx.npad));
                 cbuf[ncb + __popc(pass & ((1u << lane) - 1))] = pos;
                 prefetch_l2_lines(cx.rows8 + (long long)pos * cx.n, cx.n);
             }
@@ -867,7 +872,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
     FusedCtx cx;
     cx.sym8 = sym8; cx.rows8 = rows8; cx.meta8 = meta8; cx.perm = perm; cx.rows = rows; cx.q_p = q_p;
     cx.qc_s = reinterpret_cast<const uint4*>(qc_w); cx.lbase = reinterpret_cast<const char*>(lut_s);
-    cx.knn = knn_arg; cx.ps = ps; cx.n = n; cx.k = k_arg;
+    cx.knn = knn_arg; cx.ps = ps; cx.n = n; cx.k = k_arg; cx.npad = ntiles * MESSI_TILE_ROWS;
     int b = (int)(blockIdx.x % (unsigned)B);
     for (int visited = 0; visited < B; ++visited, b = (b + 1 == B ? 0 : b + 1)) {
         QState* st = st_all + b;
@@ -938,6 +943,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
                         prefetch_l2_bulk(tiles + (long long)ne1.x * (MESSI_TILE_BYTES / 16), MESSI_TILE_BYTES);
                 }
                 const uint2 te = u == 0 ? te0 : te1;
+                MESSI_CHECK(kc + u >= count || te.x < (unsigned)ntiles);
                 if (kc + u >= count || __uint_as_float(te.y) > thr) continue;  // box pruned (warp-uniform)
                 ++wc.tiles;
                 const long long tile = te.x;

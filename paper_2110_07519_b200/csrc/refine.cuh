@@ -44,7 +44,7 @@ struct Best { double d; long long id; };
 // under the query's lock (one thread; completions within the threshold are rare).  Once the
 // list holds k distances its k-th is a distance k distinct rows achieve -- a valid threshold
 // for the k-th neighbour -- and lowers the BSF.
-__device__ __noinline__ void knn32_insert(QState* st, KnnState* kn, int k, float d)
+__device__ __noinline__ void knn32_insert(QState* st, KnnState* kn, int k, float d, PeerSet ps, int slot)
 {
     while (atomicCAS(&st->lock, 0u, 1u) != 0u) __nanosleep(32);
     __threadfence();
@@ -59,21 +59,21 @@ __device__ __noinline__ void knn32_insert(QState* st, KnnState* kn, int k, float
     const float kth = cnt == k ? v->d32[k - 1] : -1.0f;
     __threadfence();
     atomicExch(&st->lock, 0u);
-    if (kth >= 0.0f) bsf_update(st, kth);
+    if (kth >= 0.0f) bsf_publish(st, ps, slot, kth);
 }
 
 // The refine's acceptance of a completed candidate at fp32 distance d <= thr: the near-best
 // list, and (unless inspecting, frozen) the BSF -- 1-NN: d itself (the thread's own threshold
 // drops with it); k-NN: the k-th of the list.
 __device__ __forceinline__ void dtw_accept(QState* st, NearEntry* near, KnnState* knn, int kk, bool frozen,
-                                           unsigned id, float d, float& thr)
+                                           unsigned id, float d, float& thr, PeerSet ps, int slot)
 {
     append_near(st, near, id, d);
     if (frozen) return;
     if (knn) {
-        knn32_insert(st, knn, kk, d);
+        knn32_insert(st, knn, kk, d, ps, slot);
     } else {
-        bsf_update(st, d);
+        bsf_publish(st, ps, slot, d);
         thr = fminf(thr, slack_up(d));
     }
 }
@@ -184,6 +184,8 @@ __global__ void __launch_bounds__(G == 8 ? 256 : 128, G == 8 ? 1 : 8) k_lbk_filt
             bb = __shfl_sync(0xffffffffu, bb, 0);
             const unsigned lt = (1u << lane) - 1u;
             const uint4 e = make_uint4(rid, __float_as_uint(mylbk), __float_as_uint(myhead), 0u);
+            MESSI_CHECK(!(frontmask & (1u << lane)) || fb + __popc(frontmask & lt) + bb < cap);
+            MESSI_CHECK(!(backmask & (1u << lane)) || bb + __popc(backmask & lt) + fb < cap);
             if (frontmask & (1u << lane)) list2[fb + __popc(frontmask & lt)] = e;
             if (backmask & (1u << lane)) list2[cap - 1u - (bb + __popc(backmask & lt))] = e;
         }
@@ -206,8 +208,11 @@ __device__ __forceinline__ float q8_lbk_bound(float tq, float e)
 // instead of 4n bytes), kept when q8_lbk_bound(LBK(x^), e) <= BSF0 -- a lower bound of
 // the raw LB_Keogh, hence of DTW.  list2 entries: (row id, LBK(x^), s, e);
 // the strip refine computes its tail bound from the same quantised terms.  One lane per
-// candidate: a lane streams its row's bytes 16 at a time (all lanes read the same U, L
-// words: shared-memory broadcasts); two best-first bins as k_lbk_filter.
+// candidate: a lane streams its row's bytes 64 at a time (all lanes read the same U, L
+// words: shared-memory broadcasts); two best-first bins as k_lbk_filter.  (G lanes per
+// candidate with coalesced 16-byte chunks, G = 2..16, measured slower on C4: 22-64 ms vs
+// 15.5 ms per 100 queries in the serial pass -- the four 16-byte loads a lane keeps in flight
+// here matter more than the lines a warp load touches.)
 __global__ void __launch_bounds__(128) k_lbk_filter_q8(const uint2* __restrict__ cand, const unsigned* __restrict__ perm,
                                                        const unsigned char* __restrict__ rows8,
                                                        const float2* __restrict__ meta8, int n,
@@ -282,6 +287,7 @@ __global__ void __launch_bounds__(128) k_lbk_filter_q8(const uint2* __restrict__
             const unsigned lt = (1u << lane) - 1u;
             if (pass) {
                 const uint4 e = make_uint4(perm[ce.x], __float_as_uint(a), __float_as_uint(meta.x), __float_as_uint(meta.y));
+                MESSI_CHECK(fb + __popc(frontmask & lt) + bb + __popc(backmask & lt) < cap);
                 if (fr) list2[fb + __popc(frontmask & lt)] = e;
                 else list2[cap - 1u - (bb + __popc(backmask & lt))] = e;
             }
@@ -337,7 +343,7 @@ template <int R>
 __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ rows, int n, const float* __restrict__ q_g,
                                                     const float* __restrict__ U_g, const float* __restrict__ L_g,
                                                     const uint4* __restrict__ list2, unsigned cap, QState* st,
-                                                    NearEntry* near, KnnState* knn, int kk)
+                                                    NearEntry* near, KnnState* knn, int kk, PeerSet ps, int slot)
 {
     extern __shared__ __align__(16) float dsm[];
     const int npad = (n + 3) & ~3;
@@ -367,7 +373,7 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
     unsigned id = 0, refined = 0, abandoned = 0, skipped = 0;
     unsigned long long cells = 0;
     float lbk_total = 0.0f;
-    float thr = slack_up(ld_bsf(st));
+    float thr = slack_up(ld_bsf_eff(st, ps.epoch));  // linked shards: the shared BSF too
     const bool frozen = *(volatile const unsigned*)&st->frozen != 0u;  // inspection: no BSF updates
     bool running = false;
     for (;;) {
@@ -396,9 +402,9 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
         }
         if (!__any_sync(0xffffffffu, running || nxt.x != 0xffffffffu)) break;
         if (running) {
-            const unsigned bsf_bits = *(volatile const unsigned*)&st->bsf_bits;  // consumed after the step
+            const float bsf_now = ld_bsf_eff(st, ps.epoch);  // consumed after the step
             const float rowmin = dp.step4(c, n, q_s, U, L);
-            thr = fminf(thr, slack_up(__uint_as_float(bsf_bits)));
+            thr = fminf(thr, slack_up(bsf_now));
             const float tail = fmaxf(0.0f, lbk_total * 0.9990234375f - dp.seen_lo * 1.0009765625f);
             const float bound = (rowmin + tail) * 0.9990234375f;
             if (bound > thr) {
@@ -409,7 +415,7 @@ __global__ void __launch_bounds__(128) k_refine_dtw(const float* __restrict__ ro
                 running = false;
                 cells += band_cells(n, R, n);
                 const float d = dp.result();
-                if (d <= thr) dtw_accept(st, near, knn, kk, frozen, id, d, thr);
+                if (d <= thr) dtw_accept(st, near, knn, kk, frozen, id, d, thr, ps, slot);
             }
         }
     }
@@ -453,7 +459,8 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
                                                                    const float* __restrict__ U_g,
                                                                    const float* __restrict__ L_g,
                                                                    const uint4* __restrict__ list2, unsigned cap,
-                                                                   QState* st, NearEntry* near, KnnState* knn, int kk)
+                                                                   QState* st, NearEntry* near, KnnState* knn, int kk,
+                                                                   PeerSet ps, int slot)
 {
     extern __shared__ __align__(16) float dsm[];
     const int npad = (n + 3) & ~3;
@@ -506,7 +513,7 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
     // tail bound uses the quantised terms of the rows not done yet (q8_lbk_bound), with
     // x^_j = s rint(x_j / s) recomputed from the raw point (bit-identical to k_quantise)
     float lbk_total = 0.0f, seen = 0.0f, qs = 1.0f, qinv = 1.0f, qe = INFINITY;
-    float thr = slack_up(ld_bsf(st));
+    float thr = slack_up(ld_bsf_eff(st, ps.epoch));  // linked shards: the shared BSF too
     const bool frozen = *(volatile const unsigned*)&st->frozen != 0u;  // inspection: no BSF updates
     bool running = false;
     for (;;) {
@@ -539,7 +546,7 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
         }
         if (!__any_sync(0xffffffffu, running || nxt.x != 0xffffffffu)) break;
         if (running) {
-            const unsigned bsf_bits = *(volatile const unsigned*)&st->bsf_bits;  // consumed after the strip
+            const float bsf_now = ld_bsf_eff(st, ps.epoch);  // consumed after the strip
 #pragma unroll
             for (int u = 0; u < H; ++u) dp.cv[u] = cnext[u];
             if (j0 + H < n) load_h(c, j0 + H, cnext);  // the next strip's points, one strip ahead
@@ -551,7 +558,7 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
                 seen = fmaf(d, d, seen);
             }
             j0 += H;
-            thr = fminf(thr, slack_up(__uint_as_float(bsf_bits)));
+            thr = fminf(thr, slack_up(bsf_now));
             const float tail = q8_lbk_bound(fmaxf(0.0f, lbk_total - seen * 1.0009765625f), qe);
             const float bound = (dp.rmin + tail) * 0.9990234375f;
             if (bound > thr) {
@@ -562,7 +569,7 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
                 running = false;
                 cells += band_cells(n, R, n);
                 const float d = Bt[R * T];  // D(n-1, n-1): column n-1 of the last row
-                if (d <= thr) dtw_accept(st, near, knn, kk, frozen, id, d, thr);
+                if (d <= thr) dtw_accept(st, near, knn, kk, frozen, id, d, thr, ps, slot);
             }
         }
     }
@@ -589,7 +596,7 @@ __device__ __forceinline__ void stage_row(float* dst, const float* __restrict__ 
 // Per-warp shared memory: n floats of row + 3n floats of anti-diagonals.
 __global__ void k_refine_dtw_warp(const float* __restrict__ rows, int n, int reach, const float* __restrict__ q_g,
                                   const uint4* __restrict__ list2, unsigned cap, QState* st, NearEntry* near,
-                                  KnnState* knn, int kk)
+                                  KnnState* knn, int kk, PeerSet ps, int slot)
 {
     extern __shared__ __align__(16) float dsm[];
     const int npad = (n + 3) & ~3;
@@ -607,9 +614,9 @@ __global__ void k_refine_dtw_warp(const float* __restrict__ rows, int n, int rea
         stage_row(c_s, rows + (long long)id * n, n, lane);
         const float d = dtw_warp_any<float>(q_s, c_s, n, reach, buf, lane);
         ++refined;
-        float thr = slack_up(ld_bsf(st));
+        float thr = slack_up(ld_bsf_eff(st, ps.epoch));
         if (lane == 0 && d <= thr)
-            dtw_accept(st, near, knn, kk, *(volatile const unsigned*)&st->frozen != 0u, id, d, thr);
+            dtw_accept(st, near, knn, kk, *(volatile const unsigned*)&st->frozen != 0u, id, d, thr, ps, slot);
     }
     if (lane == 0 && refined) {
         atomicAdd(&st->refined, refined);

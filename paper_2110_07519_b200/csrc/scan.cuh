@@ -165,7 +165,7 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
                            long long N, int window, const float* __restrict__ beta_g,
                            const float* __restrict__ lo_w, const float* __restrict__ hi_w,
                            float* __restrict__ lut_g, float* __restrict__ tab, float* __restrict__ U_g,
-                           float* __restrict__ L_g, QState* st, float* __restrict__ seed_d)
+                           float* __restrict__ L_g, QState* st, float* __restrict__ seed_d, PeerSet ps, int slot)
 {
     extern __shared__ __align__(16) float dsm[];
     float* q_s = dsm;
@@ -201,7 +201,7 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
         if (seed_d && lane == 0) seed_d[k] = d;  // k-NN: every window distance (k_seed_select)
     }
     if (!seed_d && lane == 0 && best < INFINITY) {
-        bsf_update(st, best);
+        bsf_publish(st, ps, slot, best);  // linked shards: also the peers' same slot
         atomicMin(&st->seed_bits, __float_as_uint(best));
     }
 }
@@ -215,14 +215,14 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
 // BSF0 * (1 + eps) are skipped; the others are listed (one thread per tile) for the scan.
 __global__ void k_tile_filter(const unsigned char* __restrict__ boxes, long long ntiles, int m,
                               const float* __restrict__ lo_w, const float* __restrict__ hi_w, QState* st,
-                              unsigned* __restrict__ list, float* __restrict__ lb_all)
+                              unsigned* __restrict__ list, float* __restrict__ lb_all, unsigned epoch)
 {
     __shared__ float lo[256], hi[256];
     __shared__ double ub[16], lb[16];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) { lo[i] = lo_w[i]; hi[i] = hi_w[i]; }
     if (threadIdx.x < 16) { ub[threadIdx.x] = st->ubar[threadIdx.x]; lb[threadIdx.x] = st->lbar[threadIdx.x]; }
     __syncthreads();
-    const double thr = (double)slack_up(ld_bsf(st));
+    const double thr = (double)slack_up(ld_bsf_eff(st, epoch));  // linked shards: the shared BSF too
     const int lane = threadIdx.x & 31;
     for (long long t0 = (long long)blockIdx.x * blockDim.x; t0 < ntiles; t0 += (long long)gridDim.x * blockDim.x) {
         const long long t = t0 + threadIdx.x;
@@ -343,6 +343,7 @@ __device__ __forceinline__ int scan_tile_coarse(const uint4* __restrict__ tiles,
     while (mask) {
         const int k = __ffs(mask) - 1;
         mask &= mask - 1;
+        MESSI_CHECK(off < MESSI_TILE_ROWS);
         surv[off++] = (unsigned short)(lane * 16 + k);
     }
     __syncwarp();
@@ -374,7 +375,8 @@ __device__ __forceinline__ float fine_lb(uint4 w, const char* lbase, int lane)
 // position, LB8) with one atomicAdd per warp-round.
 __global__ void __launch_bounds__(32 * kScanWarps, 3) k_scan(const uint4* __restrict__ tiles, const uint4* __restrict__ sym8,
                                                              long long N, const float* __restrict__ tab_g, QState* st,
-                                                             uint2* __restrict__ out, const unsigned* __restrict__ tlist)
+                                                             uint2* __restrict__ out, const unsigned* __restrict__ tlist,
+                                                             unsigned epoch)
 {
     extern __shared__ __align__(16) float tab_s[];
     __shared__ unsigned short surv_all[kScanWarps][MESSI_TILE_ROWS];
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 3) k_scan(const uint4* __rest
     for (int i = threadIdx.x; i < kScanTab / 4; i += blockDim.x)
         reinterpret_cast<float4*>(tab_s)[i] = reinterpret_cast<const float4*>(tab_g)[i];
     __syncthreads();
-    const float thr = slack_up(ld_bsf(st));
+    const float thr = slack_up(ld_bsf_eff(st, epoch));  // linked shards: the shared BSF too
     if (blockIdx.x == 0 && threadIdx.x == 0) st->lbk_thr_bits = __float_as_uint(thr);  // for the DTW filter
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned short* surv = surv_all[warp];
@@ -413,6 +415,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 3) k_scan(const uint4* __rest
             unsigned base = 0;
             if (lane == 0) base = atomicAdd(&st->cand_count, (unsigned)__popc(msk));
             base = __shfl_sync(0xffffffffu, base, 0);
+            MESSI_CHECK(!ok || base + __popc(msk & ((1u << lane) - 1)) < (unsigned)N);
             if (ok) out[base + __popc(msk & ((1u << lane) - 1))] = make_uint2(pos, __float_as_uint(lb));
         }
         __syncwarp();

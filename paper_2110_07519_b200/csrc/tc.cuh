@@ -277,6 +277,7 @@ __device__ __forceinline__ void tc_chunk(const int (&d)[32], int c0, const float
                 const int j = c0 + jj + h;
                 if ((h ? df.y : df.x) >= 0.0f && j < nq) {
                     const unsigned slot = atomicAdd(&st_all[j].cand_count, 1u);
+                    MESSI_CHECK(j < kTcMaxQ);
                     if (slot < kTcCandCap) cand[(size_t)j * kTcCandCap + slot] = (unsigned)pos;
                 }
             }

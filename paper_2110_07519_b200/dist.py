@@ -47,13 +47,15 @@ def merge_results(d2: torch.Tensor, gid: torch.Tensor, group=None):
 
 def link_shards(index, group=None):
     """Let the shards of this process group share each query's best-so-far during the
-    batched ED kernels (include/messi.h, messi_link_peers_ipc): every rank publishes the CUDA
-    IPC handles of its per-query state arrays, and opens those of all other ranks (their
-    GPUs' memory, reached over NVLink).  Collective: every rank calls it, once per index."""
+    batched ED kernels and the DTW path (include/messi.h, messi_link_peers_ipc): every rank
+    publishes the CUDA IPC handles of its per-query state arrays, and opens those of all other
+    ranks (their GPUs' memory, reached over NVLink).  Collective: every rank calls it, once per
+    index; afterwards the ranks make the same query calls."""
     from . import messi as M
     world = dist.get_world_size(group)
     me = dist.get_rank(group)
-    mine = (M.messi_batch_state_ipc(index.handle, 0), M.messi_batch_state_ipc(index.handle, 1))
+    # sets 0, 1: the batched ED path's per-query states; 2: the DTW path's slot states
+    mine = tuple(M.messi_batch_state_ipc(index.handle, s) for s in (0, 1, 2))
     allh = [None] * world
     dist.all_gather_object(allh, mine, group=group)
     peers = [allh[r] for r in range(world) if r != me]

@@ -208,15 +208,16 @@ def messi_query_dtw_batch(handle, queries_dev: torch.Tensor, reach: int, results
 
 
 def messi_batch_state_ipc(handle, set_index: int) -> bytes:
-    """The 64-byte CUDA IPC handle of the index's per-query state array `set_index` (0/1)."""
+    """The 64-byte CUDA IPC handle of the index's state array `set_index` (0/1: the batched
+    ED path's two query sets, 2: the DTW slots)."""
     buf = ctypes.create_string_buffer(64)
     _check(lib().messi_batch_state_ipc(handle, int(set_index), buf))
     return buf.raw
 
 
 def messi_link_peers_ipc(handle, peer_handles):
-    """peer_handles: list over peers of (set-0 handle, set-1 handle) byte strings."""
-    blob = b"".join(h0 + h1 for h0, h1 in peer_handles)
+    """peer_handles: list over peers of (set-0, set-1, set-2 handle) byte strings."""
+    blob = b"".join(b"".join(h) for h in peer_handles)
     buf = ctypes.create_string_buffer(blob, len(blob)) if blob else None
     _check(lib().messi_link_peers_ipc(handle, buf, len(peer_handles)))
 

@@ -29,7 +29,7 @@ def _gen(N, n, seed, row_begin=0):
     return x
 
 
-def _run_shards(X, Q, link, nshards=2, rounds=2):
+def _run_shards(X, Q, link, nshards=2, rounds=2, reach=None, k=1):
     from paper_2110_07519_b200 import messi as M
     from paper_2110_07519_b200.dist import lexmin, shard_range
     N = X.shape[0]
@@ -45,11 +45,23 @@ def _run_shards(X, Q, link, nshards=2, rounds=2):
             M.messi_link_peers_local(idxs[g].handle, [idxs[h].handle for h in range(nshards) if h != g])
     out = []
     for _ in range(rounds):  # several launch epochs
-        res = [M.result_buffer(Q.shape[0], DEV) for _ in range(nshards)]
+        res = [M.result_buffer(Q.shape[0] * k, DEV) for _ in range(nshards)]
         sts = [M.stats_buffer(Q.shape[0], DEV) for _ in range(nshards)]
         for g in range(nshards):
-            idxs[g].query_batch(Q, None, res[g], sts[g])
+            if k > 1:
+                idxs[g].query_batch_knn(Q, k, res[g], sts[g], reach=reach)
+            else:
+                idxs[g].query_batch(Q, reach, res[g], sts[g])
         torch.cuda.synchronize()
+        if k > 1:
+            from paper_2110_07519_b200.dist import merge_knn  # noqa: F401 (host merge below)
+            d2 = torch.cat([M.decode_results(r)[2].view(-1, k) for r in res], dim=1)
+            gid = torch.cat([M.decode_results(r)[1].view(-1, k) for r in res], dim=1)
+            order = [np.lexsort((g_.numpy(), np.where(g_.numpy() < 0, np.inf, d_.numpy())))[:k]
+                     for d_, g_ in zip(d2, gid)]
+            out.append((np.stack([d2[i].numpy()[o] for i, o in enumerate(order)]),
+                        np.stack([gid[i].numpy()[o] for i, o in enumerate(order)]), None))
+            continue
         d2 = torch.stack([M.decode_results(r)[2] for r in res])
         gid = torch.stack([M.decode_results(r)[1] for r in res])
         best, bid = lexmin(d2, gid)
@@ -72,6 +84,29 @@ def test_linked_shards_exact(link):
             for shard in stats:
                 for s in shard:
                     assert s["bsf_d2"] >= 0
+
+
+@pytest.mark.parametrize("link", [False, True])
+@pytest.mark.parametrize("reach", [25, 5])
+def test_linked_shards_dtw_exact(link, reach):
+    """DTW with linked shards (the shards share BSF0 and every later best of the
+    same query through their DTW slots): the merged answers equal the oracle's, and linking
+    only reduces the refine work of the shards."""
+    X = _gen(30_000, 128, datagen.DATA_SEED)
+    Q = _gen(6, 128, datagen.QUERY_SEED)
+    torch.cuda.synchronize()
+    d2, ids = oracle.nn("dtw", X.cpu().numpy(), Q.cpu().numpy(), r=reach)
+    for best, bid, stats in _run_shards(X, Q, link, nshards=3, rounds=2, reach=reach):
+        assert np.array_equal(bid, ids) and np.array_equal(best, d2)
+
+
+def test_linked_shards_dtw_knn_exact():
+    X = _gen(20_000, 128, datagen.DATA_SEED)
+    Q = _gen(4, 128, datagen.QUERY_SEED)
+    torch.cuda.synchronize()
+    d2, ids = oracle.knn("dtw", X.cpu().numpy(), Q.cpu().numpy(), 5, r=12)
+    for best, bid, _ in _run_shards(X, Q, True, nshards=2, rounds=1, reach=12, k=5):
+        assert np.array_equal(bid, ids) and np.array_equal(best, d2)
 
 
 def test_linked_shards_with_duplicates_across_shards():
@@ -117,8 +152,14 @@ def _ipc_worker(rank, world, port, out_path):
         torch.cuda.synchronize()
         _, gid, d2 = M.decode_results_device(res)
         best, bid = merge_results(d2, gid)
+    dist.barrier()
+    idx.query_batch(Q[:3].contiguous(), 12, res, None)  # DTW, shared through the slots
+    torch.cuda.synchronize()
+    _, gid, d2 = M.decode_results_device(res)
+    dbest, dbid = merge_results(d2[:3].contiguous(), gid[:3].contiguous())
     if rank == 0:
-        np.savez(out_path, best=best.cpu().numpy(), bid=bid.cpu().numpy(), npeers=npeers)
+        np.savez(out_path, best=best.cpu().numpy(), bid=bid.cpu().numpy(), npeers=npeers,
+                 dbest=dbest.cpu().numpy(), dbid=dbid.cpu().numpy())
     dist.barrier()
     idx.close()
     dist.destroy_process_group()
@@ -136,3 +177,5 @@ def test_ipc_linked_shards_two_processes(tmp_path):
     d2, ids = oracle.nn("ed", X.cpu().numpy(), Q.cpu().numpy())
     assert int(r["npeers"]) == 1
     assert np.array_equal(r["bid"], ids) and np.array_equal(r["best"], d2)
+    dd2, dids = oracle.nn("dtw", X.cpu().numpy(), Q[:3].cpu().numpy(), r=12)
+    assert np.array_equal(r["dbid"], dids) and np.array_equal(r["dbest"], dd2)

@@ -31,6 +31,8 @@ idx.query_batch_knn(Q[:4].contiguous(), 20, res)         # ED k-NN, warp insert
 for r in (25, 5, 0):                                      # strip, register band, warp refine
     idx.query_batch(Q[:6].contiguous(), r, res, st)
 idx.query_batch_knn(Q[:4].contiguous(), 7, res, reach=12)  # DTW k-NN
+if os.environ.get("SAN_TC", "1") == "1":
+    idx.query_batch_tc(Q, res, st)                        # tensor-core batched path
 torch.cuda.synchronize()
 print("single:", idx.query_ed(Q[0])[1], idx.query_dtw(Q[1], 25)[1], idx.query_knn(Q[2], 3)[1][0])
 # inspection calls (the same kernels with thresholds at +inf)
