@@ -264,7 +264,9 @@ static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R,
 {
     const int H = strip_rows(R);
     const int rem = (2 * R - 2 * H + 3) % H;
-    const int K = strip_qcopies(n, R);
+    int K = strip_qcopies(n, R);
+    if (const char* e = getenv("MESSI_DTW_QCOPIES"))  // experiments: 8 query-pair copies (H = 8 only)
+        if (atoi(e) == 8 && K == 16 && H == 8) K = 8;
     const int T = strip_threads(n, R);
     const size_t smem = strip_smem(n, R, K, T);
     bool launched = false;
@@ -456,7 +458,10 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
             ++idx->launches;
         }
         cudaEventRecord(bev[3], st);
-        k_quantise<<<(unsigned)(idx->sms * 8), 256, 0, st>>>(rows_dev, idx->perm, N, (int64_t)npadrows, n, idx->rows8,
+        // the sort's row-id input is free now: the inverse permutation for the row-order quantise
+        k_invert_perm<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(idx->perm, N, ids_in);
+        ++idx->launches;
+        k_quantise<<<(unsigned)(idx->sms * 8), 256, 0, st>>>(rows_dev, ids_in, N, (int64_t)npadrows, n, idx->rows8,
                                                             idx->meta8);
         ++idx->launches;
         cudaEventRecord(bev[4], st);
@@ -752,7 +757,9 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
         const long long nsuper = (idx->ntiles + kSuperTiles - 1) / kSuperTiles;
         const int npairs = (B + kFilterQ - 1) / kFilterQ;
         long long fx = (nsuper + 255) / 256;
-        const long long fcap = (long long)idx->sms * 8 / npairs + 1;
+        long long fcap = (long long)idx->sms * 8 / npairs + 1;
+        if (const char* e = getenv("MESSI_FILTER_CTAS"))  // experiments: filter CTAs per query pair
+            fcap = atoi(e) > 0 ? atoi(e) : fcap;
         if (fx > fcap) fx = fcap;
         dim3 fg((unsigned)fx, (unsigned)npairs);
         k_filter_batch<<<fg, 256, kFilterQ * kLutF * 4, st>>>(reinterpret_cast<const uint4*>(idx->boxes), idx->sboxes,

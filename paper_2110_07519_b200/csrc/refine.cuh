@@ -517,32 +517,37 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
     const bool frozen = *(volatile const unsigned*)&st->frozen != 0u;  // inspection: no BSF updates
     bool running = false;
     for (;;) {
-        const bool need = !running && nxt.x != 0xffffffffu;
-        const unsigned m = __ballot_sync(0xffffffffu, need);
-        if (m) {
+        // lanes without a candidate take list2 entries until one passes its bound (up to four
+        // rounds: a lane whose entry is skipped does not sit out a whole strip), then start it
+        bool start = false;
+#pragma unroll 1
+        for (int tries = 0; tries < 4; ++tries) {
+            const bool need = !running && !start && nxt.x != 0xffffffffu;
+            const unsigned m = __ballot_sync(0xffffffffu, need);
+            if (!m) break;
             const unsigned k = wc.take(ctr, m, lane);
             if (need) {
                 id = nxt.x;
                 lbk_total = __uint_as_float(nxt.y);
                 qs = __uint_as_float(nxt.z);
                 qe = __uint_as_float(nxt.w);
-                qinv = __frcp_rn(qs);  // exact: s is a power of two
                 nxt = nxt2;
                 nxt2 = fetch(k);
                 if (nxt.x != 0xffffffffu) prefetch_row(nxt.x);
-                if (q8_lbk_bound(lbk_total, qe) <= thr) {
-                    c = rows + (long long)id * n;
-                    load_h(c, 0, cnext);
-                    // virtual row -1: D(-1, -1) = 0 (slot R), +inf elsewhere
-                    for (int x = 0; x < 2 * R + 2; ++x) Bt[x * T] = x == R ? 0.0f : INFINITY;
-                    j0 = 0;
-                    seen = 0.0f;
-                    ++refined;
-                    running = true;
-                } else {
-                    ++skipped;
-                }
+                if (q8_lbk_bound(lbk_total, qe) <= thr) start = true;
+                else ++skipped;
             }
+        }
+        if (start) {
+            qinv = __frcp_rn(qs);  // exact: s is a power of two
+            c = rows + (long long)id * n;
+            load_h(c, 0, cnext);
+            // virtual row -1: D(-1, -1) = 0 (slot R), +inf elsewhere
+            for (int x = 0; x < 2 * R + 2; ++x) Bt[x * T] = x == R ? 0.0f : INFINITY;
+            j0 = 0;
+            seen = 0.0f;
+            ++refined;
+            running = true;
         }
         if (!__any_sync(0xffffffffu, running || nxt.x != 0xffffffffu)) break;
         if (running) {

@@ -160,24 +160,35 @@ __global__ void __launch_bounds__(512) k_layout(const uint4* __restrict__ symrow
 // rows"; not in the paper, whose refine reads every candidate's raw series, Alg. 9).
 // Sorted position p (row perm[p]) gets n bytes c_i (two's-complement int8), c_i = rint(x_i / s),
 // s = the smallest power of two with max_i |x_i| <= 127 s (so x_i / s and s * c_i are exact
-// in fp32), and meta[p] = {s, e}, e >= ||x - s c||_2 (fp64 sum, rounded up).  By the triangle
+// in fp32), and meta[p] = {s, e}, e >= ||x - s c||_2 (round-up fp32 sum of exact terms).  By the triangle
 // inequality ||q - x|| >= ||q - s c|| - e: a lower bound of the true ED from n bytes instead
 // of 4n.  Rows whose scale would leave the normal range, or with non-finite values, get
 // e = +inf (never pruned by the bound).  One warp per position.
-__global__ void __launch_bounds__(256) k_quantise(const float* __restrict__ rows, const unsigned* __restrict__ perm,
+// The rows are read in ROW order (inv: sorted position of every row), so the 4n-byte reads
+// stream linearly and only the n-byte writes scatter (round 1 gathered the rows in sorted
+// order: 1.3 TB/s).
+__global__ void k_invert_perm(const unsigned* __restrict__ perm, int64_t N, unsigned* __restrict__ inv)
+{
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < N) inv[perm[p]] = (unsigned)p;
+}
+
+__global__ void __launch_bounds__(256) k_quantise(const float* __restrict__ rows, const unsigned* __restrict__ inv,
                                                   int64_t N, int64_t npad, int n, unsigned char* __restrict__ rows8,
                                                   float2* __restrict__ meta8)
 {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < npad; p += warps) {
-        unsigned char* dst = rows8 + p * n;
-        if (p >= N) {  // padding positions: never candidates; zero them for determinism
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < npad; r += warps) {
+        if (r >= N) {  // padding positions (N .. npad-1): never candidates; zero them for determinism
+            unsigned char* dst = rows8 + r * n;
             for (int j = lane * 16; j < n; j += 512) *reinterpret_cast<uint4*>(dst + j) = make_uint4(0, 0, 0, 0);
-            if (lane == 0) meta8[p] = make_float2(1.0f, INFINITY);
+            if (lane == 0) meta8[r] = make_float2(1.0f, INFINITY);
             continue;
         }
-        const float* x = rows + (int64_t)perm[p] * n;
+        const int64_t p = inv[r];
+        unsigned char* dst = rows8 + p * n;
+        const float* x = rows + r * n;
         float mx = 0.0f;
         for (int j = lane * 4; j < n; j += 128) {
             const float4 v = __ldg(reinterpret_cast<const float4*>(x + j));
@@ -193,33 +204,26 @@ __global__ void __launch_bounds__(256) k_quantise(const float* __restrict__ rows
             k = (f * 128.0f <= 127.0f) ? e - 7 : e - 6;  // 127 * 2^k >= mx, smallest k
             if (k < -100 || k > 100) usable = false;
         }
-        const float s = ldexpf(1.0f, k);
-        double err = 0.0;
-        for (int j = lane * 16; j < n; j += 512) {
-            unsigned w[4];
+        const float s = ldexpf(1.0f, k), sinv = ldexpf(1.0f, -k);  // exact powers of two
+        // r = x - c s is exact in fp32 (|r| <= s / 2 and c s within a factor 2 of x when c != 0:
+        // Sterbenz), and summing r^2 with round-UP fmas / adds gives a value >= the exact sum
+        float err = 0.0f;
+        for (int j = lane * 4; j < n; j += 128) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(x + j));
+            const float xv[4] = {v.x, v.y, v.z, v.w};
+            unsigned word = 0;
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                const float4 v = __ldg(reinterpret_cast<const float4*>(x + j + 4 * g));
-                const float xv[4] = {v.x, v.y, v.z, v.w};
-                unsigned word = 0;
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const float c = usable ? rintf(ldexpf(xv[b], -k)) : 0.0f;  // |c| <= 127
-                    const double r = __dsub_rn((double)xv[b], (double)c * (double)s);
-                    err = __dadd_rn(err, __dmul_rn(r, r));
-                    word |= ((unsigned)(int)c & 255u) << (8 * b);
-                }
-                w[g] = word;
+            for (int b = 0; b < 4; ++b) {
+                const float c = usable ? rintf(xv[b] * sinv) : 0.0f;  // |c| <= 127
+                const float rr = xv[b] - c * s;
+                err = __fmaf_ru(rr, rr, err);
+                word |= ((unsigned)(int)c & 255u) << (8 * b);
             }
-            *reinterpret_cast<uint4*>(dst + j) = make_uint4(w[0], w[1], w[2], w[3]);
+            *reinterpret_cast<unsigned*>(dst + j) = word;
         }
 #pragma unroll
-        for (int o = 16; o; o >>= 1) err = __dadd_rn(err, __shfl_xor_sync(0xffffffffu, err, o));
-        if (lane == 0) {
-            // sqrt in fp64, inflated by 2^-30 (covers its rounding and the fp64 sum's, n <= 8192)
-            const float eu = usable ? __double2float_ru(sqrt(err) * (1.0 + 0x1p-30)) : INFINITY;
-            meta8[p] = make_float2(s, eu);
-        }
+        for (int o = 16; o; o >>= 1) err = __fadd_ru(err, __shfl_xor_sync(0xffffffffu, err, o));
+        if (lane == 0) meta8[p] = make_float2(s, usable ? __fsqrt_ru(err) : INFINITY);
     }
 }
 
