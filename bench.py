@@ -576,8 +576,9 @@ def cpu_baseline(cfg, args, dev, kind):
 
 def ours(args):
     import torch
-    if os.environ.get("MESSI_LIB"):
-        raise SystemExit("bench.py: MESSI_LIB is set; the bench only times the in-tree libmessi.so")
+    if os.environ.get("MESSI_LIB") and os.environ.get("MESSI_AB") != "1":
+        raise SystemExit("bench.py: MESSI_LIB is set; the bench only times the in-tree libmessi.so "
+                         "(A/B experiments set MESSI_AB=1 too, and the line then names the library)")
     world, rank, local = dist_init(args)
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
@@ -666,6 +667,7 @@ def ours(args):
         "e2e": {"value": K * nq / (e2e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": main["h2d"],
                 "d2h_bytes_per_step": main["d2h"]},
         "gpu_launches": main["launches"],
+        "lib": os.environ.get("MESSI_LIB") or "paper_2110_07519_b200/libmessi.so",
         "clocks": main["clocks"],
         "build": {"ms": main["build_ms"], "rows_per_s": main["N_local"] / (main["build_ms"] / 1e3),
                   "phases_ms": main["build_phases"],

@@ -25,7 +25,10 @@ namespace messi {
 constexpr int kLutX = MESSI_CARD * 64;   // expanded scan table: word v*64 + 16h + s (64 KB)
 constexpr int kLutF = MESSI_CARD * 32;   // filter table: word v*32 + 16h + s (32 KB)
 constexpr int kChunkTiles = 16;          // tiles per work chunk (2 per warp)
-constexpr int kFusedWarps = 12;         // 2 CTAs of 12 warps per SM (64 KB table each)
+#ifndef MESSI_FUSED_WARPS
+#define MESSI_FUSED_WARPS 12
+#endif
+constexpr int kFusedWarps = MESSI_FUSED_WARPS;  // 2 CTAs of 12 warps per SM (64 KB table each)
 constexpr int kCandBuf = 64;            // per-warp buffer of fine survivors awaiting the refine
 constexpr int kBatchMax = 128;           // queries per launch group
 constexpr int kFilterQ = 2;              // queries per filter CTA
