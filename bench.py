@@ -534,9 +534,9 @@ def _oracle_time(cfg, Xh, Qh, threads):
 
 def oracle_sample_size(cfg):
     """Rows of the oracle's bounded sample (the same for cpu_baseline and the reference arm):
-    2M rows for ED (about 10-30 core-seconds for 32 queries), 20K for DTW (each DTW row costs
-    n(2r+1) - r(r+1) = 12,406 fp64 cells at C4)."""
-    return min(cfg["N"], 2_000_000 if cfg["reach"] is None else 20_000)
+    4M rows for ED (about 25 core-seconds for 32 queries on 16 host threads), 20K for DTW (each
+    DTW row costs n(2r+1) - r(r+1) = 12,406 fp64 cells at C4)."""
+    return min(cfg["N"], 4_000_000 if cfg["reach"] is None else 20_000)
 
 
 def cpu_baseline(cfg, args, dev, kind):
@@ -566,9 +566,10 @@ def cpu_baseline(cfg, args, dev, kind):
     single["c2_1m_s_per_query"] = t2 / 4
     single["c2_1m_what"] = "C2 ED, 4 queries over the first 1,000,000 rows, one core; seconds per query"
     return {"value": qps, "unit": "queries/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
-            "sample": f"{nq} queries x first {rows:,} of {cfg['N']:,} rows in {dt:.2f} s, linearly scaled to the "
-                      f"full collection; plain fp64 brute force ({kind}), one serial call per row chunk on "
-                      f"{cores} threads", "seconds": dt, "single_core": single,
+            "sample": f"{nq} queries x first {rows:,} of {cfg['N']:,} rows in {dt:.2f} s wall "
+                      f"({dt * cores:.0f} core-seconds), linearly scaled to the full collection; plain fp64 "
+                      f"brute force ({kind}), one serial call per row chunk on {cores} threads",
+            "seconds": dt, "core_seconds": dt * cores, "single_core": single,
             "paper_context": "MESSI (CPU, 2x Xeon E5-2650 v4, 24 cores / 48 threads): ~50 ms per exact ED query "
                              "on 100M x 256 (~20 q/s, P:58, P:137, P:2881); DTW 679.3 ms RD time per query "
                              "(P:2718)"}

@@ -262,9 +262,12 @@ messi_status messi_debug_ed_refine(messi_index* idx, const float* query_dev, con
  * (frozen: threshold +inf, no BSF update, no abandon).  lbk_dev[k] (nullable) = the filter's
  * LB_Keogh -- of the QUANTISED row x^ = s c at reaches served by the strip refine
  * (*quantised = 1), of the raw row otherwise (*quantised = 0); d32_dev[k] (nullable) = the
- * refine kernel's fp32 DTW^2.  quantised may be NULL. */
+ * refine kernel's fp32 DTW^2; lbrev_dev[k] (nullable) = the filter's lower bound of the
+ * REVERSE LB_Keogh (the query's points against the candidate's envelope, from the quantised
+ * row; lbk_rev_q8) where the filter computes one -- strip reaches with (n, reach) in
+ * MESSI_REV_SPECS (refine.cuh) -- else NaN (all bits set).  quantised may be NULL. */
 messi_status messi_debug_dtw_stages(messi_index* idx, const float* query_dev, int32_t reach, const uint32_t* ids_dev,
-                                    int32_t k, float* lbk_dev, float* d32_dev, int32_t* quantised);
+                                    int32_t k, float* lbk_dev, float* d32_dev, int32_t* quantised, float* lbrev_dev);
 
 /* For `k` local row ids: d32 = the refine's fp32 squared distance (ED: ed2_group; DTW: the
  * refine kernel via messi_debug_dtw_stages), d64 = the exact fp64 re-rank (ED: ed2_exact_g;

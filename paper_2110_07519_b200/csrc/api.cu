@@ -57,6 +57,7 @@ struct messi_index {
     cudaStream_t dstr = nullptr;    // library-owned: DTW refine (overlaps the next query's filter)
     cudaStream_t dstr2 = nullptr;   // library-owned: DTW refine of the other slot (its start overlaps
                                     // the tail of the previous query's refine)
+    cudaStream_t dstr3 = nullptr, dstr4 = nullptr;  // MESSI_REFINE_STREAMS=4 (experiments)
     cudaStream_t xstr = nullptr;    // library-owned: DTW exact resolve (overlaps the next query's refine)
     cudaEvent_t ev_fork = nullptr;
     int n = 0, window = 2000, keep_paa = 0;
@@ -403,6 +404,8 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
         cudaStreamCreateWithPriority(&idx->rstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&idx->dstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&idx->dstr2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&idx->dstr3, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&idx->dstr4, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&idx->xstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&idx->ev_fork, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(MESSI_ECUDA, "stream creation failed"));
@@ -491,6 +494,8 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->rstr) cudaStreamSynchronize(idx->rstr);
     if (idx->dstr) cudaStreamSynchronize(idx->dstr);
     if (idx->dstr2) cudaStreamSynchronize(idx->dstr2);
+    if (idx->dstr3) cudaStreamSynchronize(idx->dstr3);
+    if (idx->dstr4) cudaStreamSynchronize(idx->dstr4);
     if (idx->xstr) cudaStreamSynchronize(idx->xstr);
     if (idx->stream) cudaStreamSynchronize(idx->stream);
     else cudaDeviceSynchronize();
@@ -522,6 +527,8 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->rstr && idx->rstr != idx->stream) cudaStreamDestroy(idx->rstr);
     if (idx->dstr && idx->dstr != idx->stream) cudaStreamDestroy(idx->dstr);
     if (idx->dstr2 && idx->dstr2 != idx->stream) cudaStreamDestroy(idx->dstr2);
+    if (idx->dstr3) cudaStreamDestroy(idx->dstr3);
+    if (idx->dstr4) cudaStreamDestroy(idx->dstr4);
     if (idx->xstr && idx->xstr != idx->stream) cudaStreamDestroy(idx->xstr);
     for (auto& e : idx->evs) {
         cudaEventDestroy(e.a);
@@ -549,6 +556,8 @@ static messi_status sync_all(messi_index* idx)
     CK(cudaStreamSynchronize(idx->rstr));
     CK(cudaStreamSynchronize(idx->dstr));
     CK(cudaStreamSynchronize(idx->dstr2));
+    CK(cudaStreamSynchronize(idx->dstr3));
+    CK(cudaStreamSynchronize(idx->dstr4));
     CK(cudaStreamSynchronize(idx->xstr));
     return MESSI_OK;
 }
@@ -635,6 +644,8 @@ static messi_status fork_streams(messi_index* idx)
     CK(cudaStreamWaitEvent(idx->rstr, idx->ev_fork, 0));
     CK(cudaStreamWaitEvent(idx->dstr, idx->ev_fork, 0));
     CK(cudaStreamWaitEvent(idx->dstr2, idx->ev_fork, 0));
+    CK(cudaStreamWaitEvent(idx->dstr3, idx->ev_fork, 0));
+    CK(cudaStreamWaitEvent(idx->dstr4, idx->ev_fork, 0));
     CK(cudaStreamWaitEvent(idx->xstr, idx->ev_fork, 0));
     return MESSI_OK;
 }
@@ -822,10 +833,30 @@ static bool dtw_uses_strip(int n, int reach)
 // DTW step 1: the LB_Keogh filter of the slot's candidates (list sl.cand, count and threshold
 // in sl.st) into list2 -- over the quantised rows at strip reaches (the strip refine's tail
 // bound uses the same terms), else over the raw rows.
-static messi_status launch_lbk_filter(messi_index* idx, Slot& sl, int reach, bool strip, cudaStream_t rs)
+// MESSI_NO_REV=1 (experiments): the forward-only filter k_lbk_filter_q8 at every reach.
+static bool no_rev_env()
+{
+    static int v = -1;
+    if (v < 0) v = getenv("MESSI_NO_REV") ? 1 : 0;
+    return v == 1;
+}
+
+static messi_status launch_lbk_filter(messi_index* idx, Slot& sl, int reach, bool strip, const float* q_dev,
+                                      cudaStream_t rs, float* rev_out = nullptr)
 {
     const int n = idx->n;
-    if (strip)
+    bool rev = false;
+#define LAUNCH_REV(NN, RR)                                                                                        \
+    if (strip && !rev && n == NN && reach == RR && !no_rev_env()) {                                \
+        k_lbk_filter_q8r<NN, RR><<<idx->sms * 8, 128, 0, rs>>>(sl.cand, idx->perm, idx->rows8, idx->meta8, sl.U, \
+                                                                sl.L, q_dev, sl.st, sl.list2, (unsigned)idx->N,     \
+                                                                dtw_front(), rev_out);                              \
+        rev = true;                                                                                               \
+    }
+    MESSI_REV_SPECS(LAUNCH_REV)
+#undef LAUNCH_REV
+    if (rev) {
+    } else if (strip)
         k_lbk_filter_q8<<<idx->sms * 8, 128, 2 * (size_t)((n + 15) & ~15) * sizeof(float), rs>>>(
             sl.cand, idx->perm, idx->rows8, idx->meta8, n, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N, dtw_front());
     else
@@ -929,12 +960,16 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     const bool strip = dtw_uses_strip(n, reach);
     {
         ProfScope ps(idx, K_LBK, rs);
-        TRY(launch_lbk_filter(idx, sl, reach, strip, rs));
+        TRY(launch_lbk_filter(idx, sl, reach, strip, q_dev, rs));
     }
     // the refine and the resolve run on their own stream: the LB_Keogh filter of the next
     // query (bandwidth-bound) overlaps this query's band DP (latency / ALU-bound)
     CK(cudaEventRecord(sl.ev_lbk, rs));
-    if (!ser) rs = (idx->qcount & 1) ? idx->dstr : idx->dstr2;  // qcount was advanced for this query
+    if (!ser) {  // qcount was advanced for this query
+        static const int nref = getenv("MESSI_REFINE_STREAMS") ? atoi(getenv("MESSI_REFINE_STREAMS")) : 2;
+        const cudaStream_t rst[4] = {idx->dstr, idx->dstr2, idx->dstr3, idx->dstr4};
+        rs = rst[idx->qcount % (nref == 4 ? 4 : 2)];
+    }
     CK(cudaStreamWaitEvent(rs, sl.ev_lbk, 0));
     {
         ProfScope ps(idx, K_REFINE, rs);
@@ -1634,7 +1669,7 @@ extern "C" messi_status messi_debug_ed_refine(messi_index* idx, const float* que
 
 extern "C" messi_status messi_debug_dtw_stages(messi_index* idx, const float* query_dev, int32_t reach,
                                                const uint32_t* ids_dev, int32_t k, float* lbk_dev, float* d32_dev,
-                                               int32_t* quantised)
+                                               int32_t* quantised, float* rev_dev)
 {
     if ((!ids_dev && k > 0) || k < 0 || reach < 0) return fail(MESSI_EINVAL, "bad argument");
     TRY(debug_begin(idx, query_dev, reach));
@@ -1648,7 +1683,8 @@ extern "C" messi_status messi_debug_dtw_stages(messi_index* idx, const float* qu
     LAUNCHED(idx);
     k_dbg_map<<<grid_of(k, 256), 256, 0, s>>>(ids_dev, k, idx->dbg_map, idx->dbg_inv, sl.cand, 1);
     LAUNCHED(idx);
-    TRY(launch_lbk_filter(idx, sl, reach, strip, s));
+    if (rev_dev) CK(cudaMemsetAsync(rev_dev, 0xff, sizeof(float) * (size_t)k, s));
+    TRY(launch_lbk_filter(idx, sl, reach, strip, query_dev, s, rev_dev));
     TRY(launch_dtw_refine(idx, sl, reach, strip, query_dev, s));
     if (lbk_dev) CK(cudaMemsetAsync(lbk_dev, 0xff, sizeof(float) * (size_t)k, s));
     if (d32_dev) CK(cudaMemsetAsync(d32_dev, 0xff, sizeof(float) * (size_t)k, s));
@@ -1694,7 +1730,7 @@ extern "C" messi_status messi_debug_distances(messi_index* idx, const float* que
                                                                                  gb ? idx->dbg_gbuf : nullptr);
         LAUNCHED(idx);
     }
-    if (d32_dev || lbk_dev) TRY(messi_debug_dtw_stages(idx, query_dev, reach, ids_dev, k, lbk_dev, d32_dev, nullptr));
+    if (d32_dev || lbk_dev) TRY(messi_debug_dtw_stages(idx, query_dev, reach, ids_dev, k, lbk_dev, d32_dev, nullptr, nullptr));
     CK(cudaStreamSynchronize(s));
     return MESSI_OK;
 }

@@ -227,6 +227,8 @@ __global__ void __launch_bounds__(128) k_lbk_filter_q8(const uint2* __restrict__
     const unsigned total = *(volatile unsigned*)&st->cand_count;
     const int lane = threadIdx.x & 31;
     const float thr = __uint_as_float(st->lbk_thr_bits);
+    unsigned mf;  // 0x4B000000 (2^23) in a register the compiler cannot fold: PRMT keeps an immediate selector
+    asm volatile("mov.b32 %0, 0x4B000000;" : "=r"(mf));
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k - lane < total; k += gridDim.x * blockDim.x) {
         const bool valid = k < total;
         const uint2 ce = valid ? cand[k] : make_uint2(0u, 0x7f800000u);
@@ -260,7 +262,7 @@ __global__ void __launch_bounds__(128) k_lbk_filter_q8(const uint2* __restrict__
 #pragma unroll
                     for (int b = 0; b < 4; ++b) {
                         // 2^23 + byte via PRMT, then (2^23 + byte - 2^23 - 128) * s in one exact FFMA
-                        const float fm = __uint_as_float(__byte_perm(wd[g], 0x4B000000u, 0x7650u | b));
+                        const float fm = __uint_as_float(__byte_perm(wd[g], mf, 0x7650u | b));
                         const float xq = fmaf(fm, meta.x, qoff);
                         d[b] = xq - fminf(fmaxf(xq, ls[b]), us[b]);
                     }
@@ -273,6 +275,216 @@ __global__ void __launch_bounds__(128) k_lbk_filter_q8(const uint2* __restrict__
         }
         const float bnd = q8_lbk_bound(a, meta.y);
         const bool pass = ok && bnd <= thr;
+        const bool fr = pass && bnd <= thr * front;
+        const unsigned passmask = __ballot_sync(0xffffffffu, pass), frontmask = __ballot_sync(0xffffffffu, fr);
+        if (passmask) {
+            const unsigned backmask = passmask & ~frontmask;
+            unsigned fb = 0, bb = 0;
+            if (lane == 0) {
+                if (frontmask) fb = atomicAdd(&st->list2_count, (unsigned)__popc(frontmask));
+                if (backmask) bb = atomicAdd(&st->list2_back, (unsigned)__popc(backmask));
+            }
+            fb = __shfl_sync(0xffffffffu, fb, 0);
+            bb = __shfl_sync(0xffffffffu, bb, 0);
+            const unsigned lt = (1u << lane) - 1u;
+            if (pass) {
+                const uint4 e = make_uint4(perm[ce.x], __float_as_uint(a), __float_as_uint(meta.x), __float_as_uint(meta.y));
+                MESSI_CHECK(fb + __popc(frontmask & lt) + bb + __popc(backmask & lt) < cap);
+                if (fr) list2[fb + __popc(frontmask & lt)] = e;
+                else list2[cap - 1u - (bb + __popc(backmask & lt))] = e;
+            }
+        }
+    }
+}
+
+// Reverse LB_Keogh of a quantised row ("reverse LB_Keogh"): LB_Keogh is
+// defined for either series against the envelope of the other (every point of
+// a series lies on the warping path, matched to a point of the other within the reach), so
+//     LBrev(x) = sum_i dist(q_i, [L^x_i, U^x_i])^2 <= DTW(q, x),
+// U^x_i / L^x_i = max / min of x over |k - i| <= R (clipped to [0, n)).  From the quantised
+// row x^ = s c (|x_k - x^_k| <= s/2 per point, k_quantise): U^x <= U^x^ + s/2 and
+// L^x >= L^x^ - s/2, so in code units (q' = q / s, exact: s is a power of two)
+//     dist(q_i, [L^x_i, U^x_i]) / s >= max(q'_i - Uc_i - 1/2, Lc_i - q'_i - 1/2, 0),
+// Uc / Lc the max / min code over the window.  Every rounding is DOWNWARD, so the result
+// (times s^2, exact) lower-bounds LBrev(x) with no margin.
+//
+// Envelope: the codes as biased bytes b = c + 128 paired with their complements in one
+// u16x2 word (b * 257, (255 - b) * 257), so ONE lanewise max (VIMNMX.U16x2) updates the
+// max of b and the min of b (as 255 - max(255 - b)); absent points are 0 in both lanes.
+// Points go in blocks of 8: the window of point 8b + t covers the suffix of block
+// b - A - [t < R0] from offset (t - R0) mod 8, the whole blocks between, and the prefix of
+// block b + A + [t + R0 >= 8] to offset (t + R0) mod 8 (A = R / 8, R0 = R mod 8), so each
+// block's prefix / suffix maxima are computed once, when the block is loaded (A + 1 blocks
+// ahead), into a ring of P = 2A + 3 register slots (the loop body is P blocks: the slot of a
+// block is static), and every envelope value is one 3-input max.
+// Term, per point: the byte pairs into floats 2^15 + b (PRMT into a magic exponent), then
+// (RD(q' + 2^15 + 127.5) - (2^15 + Ub), RD(2^15 + 126.5 - q') - (2^15 + 255 - Lb)) --
+// = (q' - Uc - 1/2, Lc - q' - 1/2), rounded down -- in one FFMA2 + one FSUB2.
+template <int NN, int RR>
+__device__ __forceinline__ float lbk_rev_q8(const unsigned* row, float s, const float* __restrict__ Q, unsigned mg)
+{
+    static_assert(NN % 16 == 0 && RR >= 8 && 2 * RR + 1 < NN, "lbk_rev_q8: unsupported (n, reach)");
+    constexpr int NB = NN / 8, A = RR / 8, R0 = RR % 8, P = 2 * A + 3;
+    unsigned pre[P][8], suf[P][8];
+    auto vmax = [](unsigned x, unsigned y) { return __vmaxu2(x, y); };
+    // block k (runtime, uniform) into ring slot SL: its pairs, prefix and suffix maxima
+    auto load = [&](int k, auto SL) {
+        constexpr int sl = decltype(SL)::value;
+        unsigned x[8];
+        if (k >= 0 && k < NB) {
+            unsigned w0, w1;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                         : "=r"(w0), "=r"(w1)
+                         : "r"((unsigned)__cvta_generic_to_shared(row + 2 * k)));
+            const unsigned b0 = w0 ^ 0x80808080u, b1 = w1 ^ 0x80808080u;
+            const unsigned c0 = ~b0, c1 = ~b1;
+            static_for<4>([&](auto T) {
+                constexpr int t = decltype(T)::value;
+                constexpr unsigned sel = t | (t << 4) | ((4 + t) << 8) | ((4 + t) << 12);
+                x[t] = __byte_perm(b0, c0, sel);
+                x[4 + t] = __byte_perm(b1, c1, sel);
+            });
+        } else {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) x[t] = 0u;
+        }
+        pre[sl][0] = x[0];
+#pragma unroll
+        for (int t = 1; t < 8; ++t) pre[sl][t] = vmax(pre[sl][t - 1], x[t]);
+        suf[sl][7] = x[7];
+#pragma unroll
+        for (int t = 6; t >= 0; --t) suf[sl][t] = vmax(suf[sl][t + 1], x[t]);
+    };
+    static_for<2 * A + 2>([&](auto I) {  // blocks -A-1 .. A
+        constexpr int k = decltype(I)::value - A - 1;
+        load(k, std::integral_constant<int, (k + P) % P>{});
+    });
+    const float inv = __frcp_rn(s);  // exact: s is a power of two
+    const float2 sc2 = make_float2(inv, -inv), kk2 = make_float2(32895.5f, 32894.5f);
+    float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll 1
+    for (int b0 = 0; b0 < NB; b0 += P) {
+        static_for<P>([&](auto J) {
+            constexpr int j = decltype(J)::value;
+            const int b = b0 + j;
+            if (b < NB) {
+                load(b + A + 1, std::integral_constant<int, (j + A + 1) % P>{});
+                unsigned core = pre[(j - A + 1 + P) % P][7];
+                static_for<2 * A - 2>([&](auto D) {
+                    constexpr int d = decltype(D)::value - A + 2;
+                    core = vmax(core, pre[(j + d + P) % P][7]);
+                });
+                const unsigned ml = vmax(core, pre[(j - A + P) % P][7]), mr = vmax(core, pre[(j + A) % P][7]);
+                const unsigned mlr = vmax(ml, pre[(j + A) % P][7]);
+                const float4 qa = *reinterpret_cast<const float4*>(Q + 8 * b);
+                const float4 qb = *reinterpret_cast<const float4*>(Q + 8 * b + 4);
+                const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+                float dd[8];
+                static_for<8>([&](auto T) {
+                    constexpr int t = decltype(T)::value;
+                    constexpr bool lft = t < R0, rgt = t + R0 >= 8;
+                    constexpr int sl_l = (j - A - (lft ? 1 : 0) + 2 * P) % P, ol = (t - R0 + 8) % 8;
+                    constexpr int sl_h = (j + A + (rgt ? 1 : 0)) % P, oh = (t + R0) % 8;
+                    const unsigned mid = lft ? (rgt ? mlr : ml) : (rgt ? mr : core);
+                    const unsigned e = __vimax3_u16x2(suf[sl_l][ol], mid, pre[sl_h][oh]);
+                    // (2^15 + Ub, 2^15 + 255 - Lb) as floats
+                    float2 f;
+                    asm("prmt.b32 %0, %1, %2, 0x7614;" : "=r"(*reinterpret_cast<unsigned*>(&f.x)) : "r"(e), "r"(mg));
+                    asm("prmt.b32 %0, %1, %2, 0x7634;" : "=r"(*reinterpret_cast<unsigned*>(&f.y)) : "r"(e), "r"(mg));
+                    const float2 qk = ffma2_rd(make_float2(qv[t], qv[t]), sc2, kk2);
+                    const float2 ac = fsub2_rd(qk, f);
+                    dd[t] = max3f(ac.x, ac.y, 0.0f);
+                });
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+                    acc = ffma2_rd(make_float2(dd[2 * p], dd[2 * p + 1]), make_float2(dd[2 * p], dd[2 * p + 1]), acc);
+            }
+        });
+    }
+    return __fmul_rd(__fadd_rd(acc.x, acc.y), s * s);
+}
+
+// k_lbk_filter_q8 with the reverse bound, for the (n, reach) pairs it is compiled for
+// (MESSI_REV_SPECS): a lane loads its whole row (n bytes in flight), computes the forward
+// quantised LB_Keogh exactly as k_lbk_filter_q8, and -- when that passes -- lbk_rev_q8; the
+// candidate is kept when both bounds are <= the threshold (rev_out, inspection only: the
+// reverse bound per candidate position, +inf when not computed).
+#define MESSI_REV_SPECS(X) X(256, 12) X(256, 25) X(256, 51)
+template <int NN, int RR>
+__global__ void __launch_bounds__(128) k_lbk_filter_q8r(const uint2* __restrict__ cand, const unsigned* __restrict__ perm,
+                                                        const unsigned char* __restrict__ rows8,
+                                                        const float2* __restrict__ meta8, const float* __restrict__ U_g,
+                                                        const float* __restrict__ L_g, const float* __restrict__ q_g,
+                                                        QState* st, uint4* __restrict__ list2, unsigned cap, float front,
+                                                        float* __restrict__ rev_out)
+{
+    __shared__ __align__(16) float U[NN], L[NN], Q[NN];
+    // per-thread row copies, NN + 8 bytes apart: the 8-byte loads of a half-warp hit 16
+    // distinct bank pairs
+    __shared__ __align__(16) unsigned rowbuf[128 * (NN / 4 + 2)];
+    unsigned* myrow = rowbuf + threadIdx.x * (NN / 4 + 2);
+    // the PRMT magic exponents read back from shared memory, so the compiler cannot fold them
+    // into PRMT's immediate (which would put each byte selector in a register instead)
+    __shared__ unsigned magic[2];
+    if (threadIdx.x == 0) { magic[0] = 0x4B000000u; magic[1] = 0x47000000u; }
+    for (int i = threadIdx.x; i < NN; i += blockDim.x) { U[i] = U_g[i]; L[i] = L_g[i]; Q[i] = q_g[i]; }
+    __syncthreads();
+    const unsigned mf = magic[0], mg = magic[1];
+    const unsigned total = *(volatile unsigned*)&st->cand_count;
+    const int lane = threadIdx.x & 31;
+    const float thr = __uint_as_float(st->lbk_thr_bits);
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k - lane < total; k += gridDim.x * blockDim.x) {
+        const bool valid = k < total;
+        const uint2 ce = valid ? cand[k] : make_uint2(0u, 0x7f800000u);
+        const bool ok = valid && __uint_as_float(ce.y) <= thr;
+        float a = 0.0f, rev = INFINITY;
+        float2 meta = make_float2(1.0f, INFINITY);
+        if (ok) {
+            meta = __ldg(meta8 + ce.x);
+            const float qoff = -8388736.0f * meta.x;
+            const uint4* src = reinterpret_cast<const uint4*>(rows8 + (long long)ce.x * NN);
+            uint4 raw[NN / 16];
+#pragma unroll
+            for (int h = 0; h < NN / 16; ++h) raw[h] = __ldg(src + h);
+#pragma unroll
+            for (int h = 0; h < NN / 16; ++h) {  // this thread's copy for the reverse bound
+                *reinterpret_cast<uint2*>(myrow + 4 * h) = make_uint2(raw[h].x, raw[h].y);
+                *reinterpret_cast<uint2*>(myrow + 4 * h + 2) = make_uint2(raw[h].z, raw[h].w);
+            }
+            float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll 4
+            for (int h = 0; h < NN / 16; ++h) {
+                // back from the thread's copy (volatile: the registers of the loads are free)
+                uint4 rw;
+                asm volatile("ld.shared.v2.u32 {%0, %1}, [%4];\n\tld.shared.v2.u32 {%2, %3}, [%4+8];"
+                             : "=r"(rw.x), "=r"(rw.y), "=r"(rw.z), "=r"(rw.w)
+                             : "r"((unsigned)__cvta_generic_to_shared(myrow + 4 * h)));
+                const unsigned wd[4] = {rw.x ^ 0x80808080u, rw.y ^ 0x80808080u, rw.z ^ 0x80808080u, rw.w ^ 0x80808080u};
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const float4 uu = *reinterpret_cast<const float4*>(U + 16 * h + 4 * g);
+                    const float4 ll = *reinterpret_cast<const float4*>(L + 16 * h + 4 * g);
+                    const float us[4] = {uu.x, uu.y, uu.z, uu.w}, ls[4] = {ll.x, ll.y, ll.z, ll.w};
+                    float d[4];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const float fm = __uint_as_float(__byte_perm(wd[g], mf, 0x7650u | b));
+                        const float xq = fmaf(fm, meta.x, qoff);
+                        d[b] = xq - fminf(fmaxf(xq, ls[b]), us[b]);
+                    }
+                    acc = ffma2(make_float2(d[0], d[1]), make_float2(d[0], d[1]), acc);
+                    acc = ffma2(make_float2(d[2], d[3]), make_float2(d[2], d[3]), acc);
+                }
+            }
+            a = acc.x + acc.y;
+            // the reverse bound where the forward one passes (an unusable row, e = +inf, has
+            // all-zero codes: no per-point bound, so it is not filtered here)
+            if (q8_lbk_bound(a, meta.y) <= thr) rev = (isinf(meta.y) || !(meta.x >= 0x1p-60f && meta.x <= 0x1p60f))
+                          ? 0.0f : lbk_rev_q8<NN, RR>(myrow, meta.x, Q, mg);
+        }
+        if (rev_out && valid) rev_out[k] = rev;
+        const float bnd = q8_lbk_bound(a, meta.y);
+        const bool pass = ok && bnd <= thr && rev <= thr;
         const bool fr = pass && bnd <= thr * front;
         const unsigned passmask = __ballot_sync(0xffffffffu, pass), frontmask = __ballot_sync(0xffffffffu, fr);
         if (passmask) {

@@ -100,7 +100,7 @@ def lib():
         L.messi_debug_distances.argtypes = [vp, vp, i32, vp, i32, vp, vp, vp]
         L.messi_debug_super_bounds.argtypes = [vp, vp, vp]
         L.messi_debug_ed_refine.argtypes = [vp, vp, vp, i32, vp, vp, vp]
-        L.messi_debug_dtw_stages.argtypes = [vp, vp, i32, vp, i32, vp, vp, ctypes.POINTER(i32)]
+        L.messi_debug_dtw_stages.argtypes = [vp, vp, i32, vp, i32, vp, vp, ctypes.POINTER(i32), vp]
         for f in ("messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_batch",
                   "messi_query_dtw_batch", "messi_profile_enable", "messi_profile_read", "messi_debug_breakpoints", "messi_debug_summaries",
                   "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances",
@@ -382,16 +382,19 @@ def messi_debug_ed_refine(handle, query_dev: torch.Tensor, ids_dev: torch.Tensor
     return q8[:, 0], q8[:, 1], d32, d64
 
 
-def messi_debug_dtw_stages(handle, query_dev: torch.Tensor, reach: int, ids_dev: torch.Tensor):
-    """(lbk float32 [k], d32 float32 [k], quantised: bool) of the DTW filter and refine kernels."""
+def messi_debug_dtw_stages(handle, query_dev: torch.Tensor, reach: int, ids_dev: torch.Tensor, rev: bool = False):
+    """(lbk float32 [k], d32 float32 [k], quantised: bool) of the DTW filter and refine kernels;
+    with rev=True also the filter's reverse LB_Keogh bound (float32 [k], NaN where the filter
+    computes none)."""
     ids = ids_dev.to(torch.int32).contiguous()
     k = ids.numel()
     lbk = torch.empty(k, dtype=torch.float32, device=query_dev.device)
     d32 = torch.empty(k, dtype=torch.float32, device=query_dev.device)
+    lbr = torch.empty(k, dtype=torch.float32, device=query_dev.device) if rev else None
     qz = ctypes.c_int32()
     _check(lib().messi_debug_dtw_stages(handle, _ptr(query_dev), int(reach), _ptr(ids), k, _ptr(lbk), _ptr(d32),
-                                        ctypes.byref(qz)))
-    return lbk, d32, bool(qz.value)
+                                        ctypes.byref(qz), _ptr(lbr) if rev else None))
+    return (lbk, d32, bool(qz.value), lbr) if rev else (lbk, d32, bool(qz.value))
 
 
 def messi_debug_distances(handle, query_dev: torch.Tensor, reach: int, ids_dev: torch.Tensor):

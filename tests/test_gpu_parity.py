@@ -264,6 +264,9 @@ def test_ed_refine_stages_every_row(c1):
         assert np.array_equal(d64, ed)
 
 
+REV_REACHES = (12, 25, 51)  # MESSI_REV_SPECS (refine.cuh) at n = 256
+
+
 @pytest.mark.parametrize("reach", [0, 2, 5, 7, 12, 25, 51])
 def test_dtw_stages_elementwise(c1, reach):
     """The DTW filter and refine KERNELS of the query path on 1,500 C1 rows (the ids handed
@@ -272,6 +275,9 @@ def test_dtw_stages_elementwise(c1, reach):
         within fp32 summation error of its fp64 value, and (sqrt(LBK(x^)(1 - 2^-10)) - e)^2
         <= the oracle's raw LB_Keogh <= DTW; at other reaches the raw LB_Keogh within fp32
         error of the oracle's;
+      * reverse LB_Keogh (r = 12, 25, 51: the query's points against the candidate's
+        envelope): the filter's bound from the quantised row within rounding below its fp64
+        value, <= the oracle's raw reverse LB_Keogh <= DTW (NaN, not computed, elsewhere);
       * refine (strip kernel r >= 7, register band r = 2, 5, warp wavefront r = 0): fp32 DTW^2
         within (2n + 2) u relative of the oracle's fp64 DTW^2 (the error of a sum along one
         warping path of <= 2n - 1 cells)."""
@@ -281,8 +287,9 @@ def test_dtw_stages_elementwise(c1, reach):
     ids_np = rng.choice(20_000, 1500, replace=False).astype(np.int32)
     ids = torch.from_numpy(ids_np).to(DEV)
     q = Q[2].contiguous()
-    lbk, d32, quantised = messi().messi_debug_dtw_stages(idx.handle, q, reach, ids)
+    lbk, d32, quantised, lbr = messi().messi_debug_dtw_stages(idx.handle, q, reach, ids, rev=True)
     lbk, d32 = lbk.cpu().numpy().astype(np.float64), d32.cpu().numpy().astype(np.float64)
+    lbr = lbr.cpu().numpy().astype(np.float64)
     assert not np.isnan(lbk).any() and not np.isnan(d32).any()
     assert quantised == (reach >= 7)
     ref = oracle.dtw2_rows(Xh[ids_np], Qh[2], reach)
@@ -301,7 +308,35 @@ def test_dtw_stages_elementwise(c1, reach):
         assert np.all(np.abs(lbk - tq) <= (n + 4) * U32 * tq + 1e-30)
         bnd = np.maximum(0.0, np.sqrt(lbk * (1 - 2.0 ** -10)) - e) ** 2
         assert np.all(bnd <= raw * (1 + 1e-12))
+        if reach in REV_REACHES and n == 256:
+            # the filter's reverse bound (lbk_rev_q8): the query against the quantised row's
+            # envelope widened by s/2, rounded down -- <= its fp64 value, >= that value less
+            # the kernel's 2^-8 code-unit carry of q / s and fp32 rounding, <= the oracle's
+            # raw reverse LB_Keogh <= DTW
+            xq32 = xq.astype(np.float32)
+            assert np.array_equal(xq32.astype(np.float64), xq)
+            qd = Qh[2].astype(np.float64)
+            T = np.empty(len(ids_np))
+            T_lo = np.empty(len(ids_np))
+            rawrev = np.empty(len(ids_np))
+            for j, i in enumerate(ids_np):
+                Uq, Lq = oracle.envelope(xq32[j], reach)
+                m = np.maximum(np.maximum(qd - Uq, Lq - qd), sc[j] / 2) - sc[j] / 2
+                T[j] = (m * m).sum()
+                mlo = np.maximum(m - sc[j] * 2.0 ** -8, 0.0)  # q / s carried to 2^-8 (down)
+                T_lo[j] = (mlo * mlo).sum()
+                Ux, Lx = oracle.envelope(Xh[i], reach)
+                rawrev[j] = oracle.lb_keogh2(Ux, Lx, Qh[2])
+            assert not np.isnan(lbr).any()
+            assert np.all(lbr <= T * (1 + 1e-12))
+            assert np.all(lbr >= T_lo * (1 - (2 * n + 8) * U32))
+            assert np.all(lbr <= rawrev * (1 + 1e-12))
+            assert np.all(rawrev <= ref * (1 + 1e-12))
+            assert (lbr > lbk).any()  # the reverse bound is the larger one for some rows
+        else:
+            assert np.isnan(lbr).all()
     else:
+        assert np.isnan(lbr).all()
         assert np.all(np.abs(lbk - raw) <= (n // 32 + 8) * U32 * raw + 1e-30)
 
 

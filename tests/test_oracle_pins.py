@@ -267,6 +267,34 @@ def test_lower_bound_chain_dtw():
         assert oracle.lb_env_paa2(Up, Lp, S[k], 256) == oracle.mindist2(qp, S[k], 256)
 
 
+def test_lb_keogh_reverse_lower_bounds_dtw():
+    """LB_Keogh with the roles swapped -- the query's points against the CANDIDATE's envelope
+    -- lower-bounds DTW too (the argument of P:1392-1405 is symmetric in the two series: every
+    query point lies on the warping path, matched to a candidate point within the reach; the
+    DTW refine's reverse filter): against brute force over every warping path on
+    tiny inputs, and on 2,500 random-walk pairs at r = 25, where it is often the larger bound."""
+    rng = np.random.default_rng(31)
+    for trial in range(60):
+        n = int(rng.integers(1, 8))
+        q = rng.standard_normal(n).astype(np.float32)
+        c = rng.standard_normal(n).astype(np.float32)
+        for r in range(0, n + 1):
+            Uc, Lc = oracle.envelope(c, r)
+            assert oracle.lb_keogh2(Uc, Lc, q) <= brute_dtw(q, c, r) * (1 + 1e-12) + 1e-12
+    X = zwalks(50, 256, 14)
+    Q = zwalks(50, 256, 15)
+    larger = 0
+    for q in Q:
+        U, L = oracle.envelope(q, 25)
+        for k in range(X.shape[0]):
+            Uc, Lc = oracle.envelope(X[k], 25)
+            fwd = oracle.lb_keogh2(U, L, X[k])
+            rev = oracle.lb_keogh2(Uc, Lc, q)
+            assert rev <= oracle.dtw2(q, X[k], 25)
+            larger += rev > fwd
+    assert 0 < larger < 2500
+
+
 def test_lb_env_paa_hand_value_reach1():
     """O11 at r > 0 on a worked example (Fig. fig:dtwsimd's ABOVE / BELOW / IN cases
     P:1471-1486), cardinality 4 (breakpoints -b, 0, b with b = Phi^-1(3/4), fp32):
