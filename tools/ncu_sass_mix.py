@@ -10,6 +10,9 @@ def load(rep):
     out = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'sass'],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
+    # several kernels in the report: keep the LAST kernel's section (header row repeated per kernel)
+    starts = [i for i, r in enumerate(rows) if 'Address' in r and 'Source' in r]
+    rows = rows[starts[-1] - 1:]
     hdr = rows[1]
     ix = {h: i for i, h in enumerate(hdr)}
     recs = []
