@@ -41,6 +41,7 @@ struct Slot {
     float *lut = nullptr, *tab = nullptr, *U = nullptr, *L = nullptr;  // tab: 64 KB scan table
     uint2* cand = nullptr;    // scan survivors (sorted position, 8-bit LB)                      [lazy]
     uint4* list2 = nullptr;   // DTW: LB_Keogh survivors (id, LBK, LBK of the first window, 0)  [lazy]
+    uint4* rlist = nullptr;   // DTW: forward survivors queued for the reverse bound               [lazy]
     unsigned* tlist = nullptr;  // tiles surviving the box filter
     NearEntry* near = nullptr;  // near-best (id, d32) of the DTW refine                          [lazy]
     double* rbuf = nullptr;     // DTW resolve: global wavefront scratch for long series         [lazy]
@@ -518,7 +519,7 @@ extern "C" void messi_free(messi_index* idx)
             if (p) cudaFree(p);
     }
     for (Slot& sl : idx->slot) {
-        void* sp[] = {sl.lut, sl.tab, sl.U, sl.L, sl.cand, sl.list2, sl.near, sl.tlist, sl.rbuf, sl.knn, sl.seedd};
+        void* sp[] = {sl.lut, sl.tab, sl.U, sl.L, sl.cand, sl.list2, sl.rlist, sl.near, sl.tlist, sl.rbuf, sl.knn, sl.seedd};
         for (void* p : sp)
             if (p) cudaFree(p);
         cudaEvent_t es[] = {sl.ev_seed, sl.ev_scan, sl.ev_lbk, sl.ev_refined, sl.ev_done};
@@ -671,6 +672,7 @@ static messi_status ensure_dtw_buffers(messi_index* idx)
         if (!sl.cand) TRY(dalloc(&sl.cand, (size_t)idx->N));
         if (!sl.near) TRY(dalloc(&sl.near, (size_t)idx->N));
         if (!sl.list2) TRY(dalloc(&sl.list2, (size_t)idx->N));
+        if (!sl.rlist) TRY(dalloc(&sl.rlist, (size_t)idx->N));
     }
     return MESSI_OK;
 }
@@ -847,16 +849,46 @@ static bool no_rev_env()
     return v == 1;
 }
 
+// The reverse bound (n, reach in MESSI_REV_SPECS, strip reaches): the forward filter
+// k_lbk_filter_q8 queues its survivors with forward bound <= rho * BSF0 (MESSI_REV_RHO,
+// default 1: all of them) and k_lbk_rev_q8 evaluates the queue with every lane busy
+// (MESSI_REV_MODE=fused, experiments: both bounds in one kernel, k_lbk_filter_q8r).
+static float rev_rho()
+{
+    static float v = -1.0f;
+    if (v < 0.0f) {
+        const char* e = getenv("MESSI_REV_RHO");
+        v = e ? (float)atof(e) : 1.0f;
+    }
+    return v;
+}
+static bool rev_fused()
+{
+    static int v = -1;
+    if (v < 0) v = (getenv("MESSI_REV_MODE") && !strcmp(getenv("MESSI_REV_MODE"), "fused")) ? 1 : 0;
+    return v == 1;
+}
+
 static messi_status launch_lbk_filter(messi_index* idx, Slot& sl, int reach, bool strip, const float* q_dev,
                                       cudaStream_t rs, float* rev_out = nullptr)
 {
     const int n = idx->n;
     bool rev = false;
 #define LAUNCH_REV(NN, RR)                                                                                        \
-    if (strip && !rev && n == NN && reach == RR && !no_rev_env()) {                                \
-        k_lbk_filter_q8r<NN, RR><<<idx->sms * 8, 128, 0, rs>>>(sl.cand, idx->perm, idx->rows8, idx->meta8, sl.U, \
-                                                                sl.L, q_dev, sl.st, sl.list2, (unsigned)idx->N,     \
-                                                                dtw_front(), rev_out);                              \
+    if (strip && !rev && n == NN && reach == RR && !no_rev_env()) {                                             \
+        if (rev_fused()) {                                                                                        \
+            k_lbk_filter_q8r<NN, RR><<<idx->sms * 8, 128, 0, rs>>>(sl.cand, idx->perm, idx->rows8, idx->meta8,   \
+                                                                    sl.U, sl.L, q_dev, sl.st, sl.list2,         \
+                                                                    (unsigned)idx->N, dtw_front(), rev_out);    \
+        } else {                                                                                                  \
+            k_lbk_filter_q8<<<idx->sms * 8, 128, 2 * (size_t)((n + 15) & ~15) * sizeof(float), rs>>>(             \
+                sl.cand, idx->perm, idx->rows8, idx->meta8, n, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N,     \
+                dtw_front(), sl.rlist, rev_rho());                                                               \
+            LAUNCHED(idx);                                                                                        \
+            k_lbk_rev_q8<NN, RR><<<idx->sms * 8, 128, 0, rs>>>(sl.rlist, idx->perm, idx->rows8, q_dev, sl.st,     \
+                                                                sl.list2, (unsigned)idx->N, dtw_front(), rev_out, \
+                                                                rev_out ? idx->dbg_map : nullptr);               \
+        }                                                                                                         \
         rev = true;                                                                                               \
     }
     MESSI_REV_SPECS(LAUNCH_REV)
@@ -864,7 +896,8 @@ static messi_status launch_lbk_filter(messi_index* idx, Slot& sl, int reach, boo
     if (rev) {
     } else if (strip)
         k_lbk_filter_q8<<<idx->sms * 8, 128, 2 * (size_t)((n + 15) & ~15) * sizeof(float), rs>>>(
-            sl.cand, idx->perm, idx->rows8, idx->meta8, n, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N, dtw_front());
+            sl.cand, idx->perm, idx->rows8, idx->meta8, n, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N, dtw_front(),
+            nullptr, 0.0f);
     else
         k_lbk_filter<4><<<refine_grid(idx, 1024) * 2, 128, lbk_smem(n), rs>>>(
             sl.cand, idx->perm, idx->rows, n, sl.U, sl.L, reach, sl.st, sl.list2, (unsigned)idx->N, dtw_front());
@@ -881,6 +914,8 @@ static messi_status launch_dtw_refine(messi_index* idx, Slot& sl, int reach, boo
     const int npad = (n + 3) & ~3;
     const size_t qsm = (size_t)npad * sizeof(float);
     bool launched = false;
+    static const bool skip = getenv("MESSI_TIMING_SKIP_REFINE") != nullptr;  // timing experiments only: WRONG answers
+    if (skip) return MESSI_OK;
     if (strip) {
         TRY(launch_strip(idx, sl, n, reach, q_dev, rs, knn, kk, ps, slot));
         launched = true;
@@ -964,13 +999,14 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     CK(cudaEventRecord(sl.ev_seed, side));
     TRY(launch_scan(idx, sl, rs, peers));
     const bool strip = dtw_uses_strip(n, reach);
+    static const bool skipf = getenv("MESSI_TIMING_SKIP_FILTER") != nullptr;  // timing experiments only: WRONG answers
     if (!ser && (idx->qcount & 1)) {  // filters of consecutive queries on two streams (C4: +2%)
         rs = idx->fstr;
         CK(cudaStreamWaitEvent(rs, sl.ev_scan, 0));
     }
     {
         ProfScope ps(idx, K_LBK, rs);
-        TRY(launch_lbk_filter(idx, sl, reach, strip, q_dev, rs));
+        if (!skipf) TRY(launch_lbk_filter(idx, sl, reach, strip, q_dev, rs));
     }
     // the refine and the resolve run on their own stream: the LB_Keogh filter of the next
     // query (bandwidth-bound) overlaps this query's band DP (latency / ALU-bound)

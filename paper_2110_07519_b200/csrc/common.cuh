@@ -66,6 +66,7 @@ struct QState {
     unsigned char zlo[16], zhi[16];  // batch ED: per segment, the symbols whose table entry is 0
     unsigned lbk_thr_bits;  // DTW: the scan's threshold (BSF0), used by the LB_Keogh filter
     unsigned list2_back;    // DTW: LB_Keogh survivors appended from the back of list2 (larger LBK)
+    unsigned rev_count;     // DTW: forward survivors queued for the reverse LB_Keogh (rlist)
     // batch ED: the query quantised like the rows ("quantised-row bound"):
     // c_q = rint(q / s_q) in [-127, 127], s_q a power of two; q8e >= ||q - s_q c_q||;
     // q8sum = sum c_q, q8s2ss = s_q^2 sum c_q^2 (exact in fp64); the words go to qc_all
@@ -109,6 +110,7 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->cand_count = 0;
     st->list2_count = 0;
     st->list2_back = 0;
+    st->rev_count = 0;
     st->near_count = 0;
     st->refined = 0;
     st->abandoned = 0;

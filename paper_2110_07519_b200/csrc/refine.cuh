@@ -217,7 +217,8 @@ __global__ void __launch_bounds__(128) k_lbk_filter_q8(const uint2* __restrict__
                                                        const unsigned char* __restrict__ rows8,
                                                        const float2* __restrict__ meta8, int n,
                                                        const float* __restrict__ U_g, const float* __restrict__ L_g,
-                                                       QState* st, uint4* __restrict__ list2, unsigned cap, float front)
+                                                       QState* st, uint4* __restrict__ list2, unsigned cap, float front,
+                                                       uint4* __restrict__ rlist, float rho)
 {
     extern __shared__ __align__(16) float env[];
     float* U = env;
@@ -274,7 +275,20 @@ __global__ void __launch_bounds__(128) k_lbk_filter_q8(const uint2* __restrict__
             a = acc.x + acc.y;
         }
         const float bnd = q8_lbk_bound(a, meta.y);
-        const bool pass = ok && bnd <= thr;
+        bool pass = ok && bnd <= thr;
+        // survivors whose forward bound is <= rho * BSF0 (the ones the refine would run longest)
+        // queue for the reverse bound (k_lbk_rev_q8) instead of going to list2
+        const bool rq = rlist && pass && bnd <= rho * thr;
+        const unsigned rmask = __ballot_sync(0xffffffffu, rq);
+        if (rmask) {
+            unsigned rb = 0;
+            if (lane == 0) rb = atomicAdd(&st->rev_count, (unsigned)__popc(rmask));
+            rb = __shfl_sync(0xffffffffu, rb, 0);
+            MESSI_CHECK(!rq || rb + __popc(rmask & ((1u << lane) - 1u)) < cap);
+            if (rq) rlist[rb + __popc(rmask & ((1u << lane) - 1u))] =
+                make_uint4(ce.x, __float_as_uint(a), __float_as_uint(meta.x), __float_as_uint(meta.y));
+            pass = pass && !rq;
+        }
         const bool fr = pass && bnd <= thr * front;
         const unsigned passmask = __ballot_sync(0xffffffffu, pass), frontmask = __ballot_sync(0xffffffffu, fr);
         if (passmask) {
@@ -402,6 +416,74 @@ __device__ __forceinline__ float lbk_rev_q8(const unsigned* row, float s, const 
         });
     }
     return __fmul_rd(__fadd_rd(acc.x, acc.y), s * s);
+}
+
+// The reverse LB_Keogh over the forward filter's queue (rlist: sorted position, LBK(x^), s, e;
+// QState::rev_count entries), one thread per entry with every lane busy: the row's n bytes in
+// flight, a copy in this thread's shared-memory slot for lbk_rev_q8; entries whose reverse
+// bound is <= the threshold join list2 (front bin by the larger of the two bounds).
+// rev_out / dbg_map: inspection only (the bound per inspected id).
+template <int NN, int RR>
+__global__ void __launch_bounds__(128) k_lbk_rev_q8(const uint4* __restrict__ rlist, const unsigned* __restrict__ perm,
+                                                    const unsigned char* __restrict__ rows8, const float* __restrict__ q_g,
+                                                    QState* st, uint4* __restrict__ list2, unsigned cap, float front,
+                                                    float* __restrict__ rev_out, const int* __restrict__ dbg_map)
+{
+    __shared__ __align__(16) float Q[NN];
+    __shared__ __align__(16) unsigned rowbuf[128 * (NN / 4 + 2)];
+    unsigned* myrow = rowbuf + threadIdx.x * (NN / 4 + 2);
+    __shared__ unsigned magic;
+    if (threadIdx.x == 0) magic = 0x47000000u;
+    for (int i = threadIdx.x; i < NN; i += blockDim.x) Q[i] = q_g[i];
+    __syncthreads();
+    const unsigned mg = magic;
+    const unsigned total = *(volatile unsigned*)&st->rev_count;
+    const int lane = threadIdx.x & 31;
+    const float thr = __uint_as_float(st->lbk_thr_bits);
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k - lane < total; k += gridDim.x * blockDim.x) {
+        const bool valid = k < total;
+        const uint4 e = valid ? rlist[k] : make_uint4(0u, 0u, 0x3f800000u, 0x7f800000u);
+        const float a = __uint_as_float(e.y), s = __uint_as_float(e.z), ee = __uint_as_float(e.w);
+        float rev = INFINITY;
+        if (valid) {
+            if (isinf(ee) || !(s >= 0x1p-60f && s <= 0x1p60f)) {
+                rev = 0.0f;  // an unusable row (all-zero codes): not filtered here
+            } else {
+                const uint4* src = reinterpret_cast<const uint4*>(rows8 + (long long)e.x * NN);
+                uint4 raw[NN / 16];
+#pragma unroll
+                for (int h = 0; h < NN / 16; ++h) raw[h] = __ldg(src + h);
+#pragma unroll
+                for (int h = 0; h < NN / 16; ++h) {
+                    *reinterpret_cast<uint2*>(myrow + 4 * h) = make_uint2(raw[h].x, raw[h].y);
+                    *reinterpret_cast<uint2*>(myrow + 4 * h + 2) = make_uint2(raw[h].z, raw[h].w);
+                }
+                rev = lbk_rev_q8<NN, RR>(myrow, s, Q, mg);
+            }
+            if (rev_out) rev_out[dbg_map[perm[e.x]]] = rev;
+        }
+        const float bnd = q8_lbk_bound(a, ee);
+        const bool pass = valid && rev <= thr;
+        const bool fr = pass && fmaxf(bnd, rev) <= thr * front;
+        const unsigned passmask = __ballot_sync(0xffffffffu, pass), frontmask = __ballot_sync(0xffffffffu, fr);
+        if (passmask) {
+            const unsigned backmask = passmask & ~frontmask;
+            unsigned fb = 0, bb = 0;
+            if (lane == 0) {
+                if (frontmask) fb = atomicAdd(&st->list2_count, (unsigned)__popc(frontmask));
+                if (backmask) bb = atomicAdd(&st->list2_back, (unsigned)__popc(backmask));
+            }
+            fb = __shfl_sync(0xffffffffu, fb, 0);
+            bb = __shfl_sync(0xffffffffu, bb, 0);
+            const unsigned lt = (1u << lane) - 1u;
+            if (pass) {
+                const uint4 o = make_uint4(perm[e.x], e.y, e.z, e.w);
+                MESSI_CHECK(fb + __popc(frontmask & lt) + bb + __popc(backmask & lt) < cap);
+                if (fr) list2[fb + __popc(frontmask & lt)] = o;
+                else list2[cap - 1u - (bb + __popc(backmask & lt))] = o;
+            }
+        }
+    }
 }
 
 // k_lbk_filter_q8 with the reverse bound, for the (n, reach) pairs it is compiled for
