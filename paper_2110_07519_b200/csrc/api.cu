@@ -310,6 +310,7 @@ static messi_status setup_kernels(int device)
     CK(cudaFuncSetAttribute(k_lbk_filter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_lbk_filter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_lbk_filter_q8, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_lbk_filter_q8b<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbkb_smem<256>()));
     CK(cudaFuncSetAttribute(k_debug_dtw64, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_ed_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes(256)));
     CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -862,6 +863,12 @@ static float rev_rho()
     }
     return v;
 }
+static bool lbk_bulk()  // MESSI_LBK_BULK=0 (experiments): the LDG forward filter instead of the bulk-copy one
+{
+    static int v = -1;
+    if (v < 0) v = (getenv("MESSI_LBK_BULK") && !strcmp(getenv("MESSI_LBK_BULK"), "0")) ? 0 : 1;
+    return v == 1;
+}
 static bool rev_fused()
 {
     static int v = -1;
@@ -881,9 +888,14 @@ static messi_status launch_lbk_filter(messi_index* idx, Slot& sl, int reach, boo
                                                                     sl.U, sl.L, q_dev, sl.st, sl.list2,         \
                                                                     (unsigned)idx->N, dtw_front(), rev_out);    \
         } else {                                                                                                  \
-            k_lbk_filter_q8<<<idx->sms * 8, 128, 2 * (size_t)((n + 15) & ~15) * sizeof(float), rs>>>(             \
-                sl.cand, idx->perm, idx->rows8, idx->meta8, n, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N,     \
-                dtw_front(), sl.rlist, rev_rho());                                                               \
+            if (lbk_bulk())                                                                                       \
+                k_lbk_filter_q8b<NN><<<idx->sms * 3, 128, lbkb_smem<NN>(), rs>>>(                                \
+                    sl.cand, idx->perm, idx->rows8, idx->meta8, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N,    \
+                    dtw_front(), sl.rlist, rev_rho(), 0x4B000000u);                                              \
+            else                                                                                                  \
+                k_lbk_filter_q8<<<idx->sms * 8, 128, 2 * (size_t)((n + 15) & ~15) * sizeof(float), rs>>>(         \
+                    sl.cand, idx->perm, idx->rows8, idx->meta8, n, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N, \
+                    dtw_front(), sl.rlist, rev_rho());                                                           \
             LAUNCHED(idx);                                                                                        \
             k_lbk_rev_q8<NN, RR><<<idx->sms * 8, 128, 0, rs>>>(sl.rlist, idx->perm, idx->rows8, q_dev, sl.st,     \
                                                                 sl.list2, (unsigned)idx->N, dtw_front(), rev_out, \

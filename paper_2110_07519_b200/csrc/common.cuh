@@ -129,6 +129,36 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->frozen = 0;
 }
 
+// mbarrier (TMA / bulk-copy completion) wrappers.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// Waits for the phase of parity `parity` to complete; the suspend-time hint lets the hardware
+// park the waiting thread until then instead of spinning on issue slots the epilogue needs.
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity)
+{
+    const unsigned a = smem_u32(b);
+    unsigned ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
+
 // Paired fp32 arithmetic (Blackwell FADD2 / FFMA2: two lanes of fp32 per instruction on the
 // FMA pipe -- half the issue slots of two scalar ops).
 __device__ __forceinline__ float2 fadd2_rd(float2 a, float2 b)

@@ -440,9 +440,24 @@ __global__ void __launch_bounds__(128) k_lbk_rev_q8(const uint4* __restrict__ rl
     const unsigned total = *(volatile unsigned*)&st->rev_count;
     const int lane = threadIdx.x & 31;
     const float thr = __uint_as_float(st->lbk_thr_bits);
-    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k - lane < total; k += gridDim.x * blockDim.x) {
+    const unsigned stride = gridDim.x * blockDim.x;
+    const uint4 none = make_uint4(0u, 0u, 0x3f800000u, 0x7f800000u);
+    // the next entry's row is prefetched into L1 while this one is evaluated
+    auto prefetch = [&](const uint4& e) {
+        const char* r = reinterpret_cast<const char*>(rows8) + (long long)e.x * NN;
+#pragma unroll
+        for (int c = 0; c < NN; c += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(r + c));
+    };
+    unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k + stride < total) prefetch(rlist[k + stride]);
+    uint4 nxt;
+    for (; k - lane < total; k += stride) {
         const bool valid = k < total;
-        const uint4 e = valid ? rlist[k] : make_uint4(0u, 0u, 0x3f800000u, 0x7f800000u);
+        const uint4 e = valid ? rlist[k] : none;
+        if (k + 2 * stride < total) {  // the entry after next: its row to L1
+            nxt = rlist[k + 2 * stride];
+            prefetch(nxt);
+        }
         const float a = __uint_as_float(e.y), s = __uint_as_float(e.z), ee = __uint_as_float(e.w);
         float rev = INFINITY;
         if (valid) {
@@ -587,6 +602,159 @@ __global__ void __launch_bounds__(128) k_lbk_filter_q8r(const uint2* __restrict_
             }
         }
     }
+}
+
+// k_lbk_filter_q8 for compile-time n with the rows brought in by the bulk-copy (TMA) engine:
+// each lane of a warp issues one cp.async.bulk of its candidate's n bytes into its own slot
+// of a per-warp double buffer in shared memory (completion on the warp's mbarrier), so a
+// row costs one instruction and no L1 wavefronts (one lane per row, n/16 LDG.128 per lane,
+// made the L1 the limiter), and the next 32 rows are in flight while these are evaluated.
+// Same values, list2 / rlist appends and result as k_lbk_filter_q8 (the per-point term as
+// max(x^ - U, L - x^, 0), paired FADD2 + one FMNMX3, instead of x^ - clamp(x^, L, U)).
+// mf = 0x4B000000 as a parameter: a value the compiler cannot fold into PRMT's immediate,
+// which would leave every byte selector in a register.
+template <int NN>
+__host__ __device__ constexpr size_t lbkb_smem()
+{
+    return (size_t)2 * NN * 4 + 8 * 8 + (size_t)2 * 128 * (NN + 16);
+}
+template <int NN>
+__global__ void __launch_bounds__(128) k_lbk_filter_q8b(const uint2* __restrict__ cand, const unsigned* __restrict__ perm,
+                                                        const unsigned char* __restrict__ rows8,
+                                                        const float2* __restrict__ meta8, const float* __restrict__ U_g,
+                                                        const float* __restrict__ L_g, QState* st,
+                                                        uint4* __restrict__ list2, unsigned cap, float front,
+                                                        uint4* __restrict__ rlist, float rho, unsigned mf)
+{
+    constexpr int RS = NN + 16;  // slot stride: 16-byte aligned, LDS.128 quarter-warps conflict-free
+    extern __shared__ __align__(128) unsigned char lsm[];
+    float* U = reinterpret_cast<float*>(lsm);
+    float* L = U + NN;
+    unsigned long long* mb = reinterpret_cast<unsigned long long*>(L + NN);  // [warp][buffer]
+    unsigned char* rowsm = reinterpret_cast<unsigned char*>(mb + 8);           // [buffer][thread][RS]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+        mbar_init(&mb[2 * w], 1);
+        mbar_init(&mb[2 * w + 1], 1);
+    }
+    for (int i = threadIdx.x; i < NN; i += blockDim.x) { U[i] = U_g[i]; L[i] = L_g[i]; }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    const unsigned total = *(volatile unsigned*)&st->cand_count;
+    const float thr = __uint_as_float(st->lbk_thr_bits);
+    const uint2 none = make_uint2(0u, 0x7f800000u);
+    struct Cur { uint2 ce; bool ok; float2 meta; unsigned id; };
+    // warp-uniform: rows of the candidates ce (k0 + lane, loaded one batch earlier) into
+    // buffer b (lanes without a usable one copy nothing; the warp's mbarrier expects the
+    // bytes of the others); their scale / error bound and row id load meanwhile
+    auto issue = [&](uint2 ce, unsigned k0, int b) {
+        Cur c;
+        c.ce = ce;
+        c.ok = k0 + lane < total && __uint_as_float(ce.y) <= thr;
+        const unsigned cnt = __popc(__ballot_sync(0xffffffffu, c.ok));
+        unsigned long long* bar = &mb[2 * w + b];
+        if (lane == 0) mbar_expect_tx(bar, cnt * NN);
+        __syncwarp();
+        if (c.ok) {
+            const unsigned dst = smem_u32(rowsm + ((size_t)b * 128 + threadIdx.x) * RS);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                "l"(rows8 + (long long)ce.x * NN), "r"(NN), "r"(smem_u32(bar))
+                : "memory");
+        }
+        c.meta = c.ok ? __ldg(meta8 + ce.x) : make_float2(1.0f, INFINITY);
+        c.id = c.ok ? __ldg(perm + ce.x) : 0u;
+        return c;
+    };
+    // appends of one batch: the atomics are issued after its evaluation and their results
+    // consumed after the NEXT batch's (their latency hidden behind it)
+    struct Pend { unsigned rmask, passmask, frontmask, rb, fb, bb; uint4 e; bool rq, pass, fr; };
+    auto flush = [&](const Pend& pd) {
+        const unsigned lt = (1u << lane) - 1u;
+        if (pd.rmask) {
+            const unsigned rb = __shfl_sync(0xffffffffu, pd.rb, 0);
+            MESSI_CHECK(!pd.rq || rb + __popc(pd.rmask & lt) < cap);
+            if (pd.rq) rlist[rb + __popc(pd.rmask & lt)] = pd.e;
+        }
+        if (pd.passmask) {
+            const unsigned backmask = pd.passmask & ~pd.frontmask;
+            const unsigned fb = __shfl_sync(0xffffffffu, pd.fb, 0), bb = __shfl_sync(0xffffffffu, pd.bb, 0);
+            MESSI_CHECK(!pd.pass || fb + __popc(pd.frontmask & lt) + bb + __popc(backmask & lt) < cap);
+            if (pd.fr) list2[fb + __popc(pd.frontmask & lt)] = pd.e;
+            else if (pd.pass) list2[cap - 1u - (bb + __popc(backmask & lt))] = pd.e;
+        }
+    };
+    const unsigned kstep = gridDim.x * blockDim.x;
+    unsigned k0 = (blockIdx.x * 4 + w) * 32;
+    auto entry = [&](unsigned kb) { return kb + lane < total ? cand[kb + lane] : none; };
+    Cur cur = {none, false, make_float2(1.0f, INFINITY), 0u};
+    if (k0 < total) cur = issue(entry(k0), k0, 0);
+    uint2 ce_n = entry(k0 + kstep);  // candidates of the next batch (their rows issued next iteration)
+    Pend pend = {0u, 0u, 0u, 0u, 0u, 0u, make_uint4(0u, 0u, 0u, 0u), false, false, false};
+    for (int it = 0; k0 < total; ++it, k0 += kstep) {
+        const int b = it & 1;
+        Cur nxt = {none, false, make_float2(1.0f, INFINITY), 0u};
+        if (k0 + kstep < total) nxt = issue(ce_n, k0 + kstep, b ^ 1);
+        ce_n = entry(k0 + 2 * kstep);
+        mbar_wait(&mb[2 * w + b], (it >> 1) & 1);
+        const bool ok = cur.ok;
+        const float2 meta = cur.meta;
+        float a = 0.0f;
+        if (ok) {
+            const unsigned char* row = rowsm + ((size_t)b * 128 + threadIdx.x) * RS;
+            const float qoff = -8388736.0f * meta.x;  // -(2^23 + 128) s, exact (s a power of two)
+            const float2 s2 = make_float2(meta.x, meta.x), qoff2 = make_float2(qoff, qoff);
+            float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll 4
+            for (int h = 0; h < NN / 16; ++h) {
+                const uint4 raw = *reinterpret_cast<const uint4*>(row + 16 * h);
+                const unsigned wd[4] = {raw.x ^ 0x80808080u, raw.y ^ 0x80808080u, raw.z ^ 0x80808080u,
+                                        raw.w ^ 0x80808080u};
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const float4 uu = *reinterpret_cast<const float4*>(U + 16 * h + 4 * g);
+                    const float4 ll = *reinterpret_cast<const float4*>(L + 16 * h + 4 * g);
+                    float fm[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) fm[q] = __uint_as_float(__byte_perm(wd[g], mf, 0x7650u | q));
+#pragma unroll
+                    for (int p = 0; p < 2; ++p) {
+                        // x^ = (2^23 + byte - 2^23 - 128) s exactly; dist = max(x^ - U, L - x^, 0)
+                        const float2 xq = ffma2(make_float2(fm[2 * p], fm[2 * p + 1]), s2, qoff2);
+                        const float2 up = p ? make_float2(uu.z, uu.w) : make_float2(uu.x, uu.y);
+                        const float2 lo = p ? make_float2(ll.z, ll.w) : make_float2(ll.x, ll.y);
+                        const float2 da = fadd2(xq, make_float2(-up.x, -up.y));
+                        const float2 db = fadd2(lo, make_float2(-xq.x, -xq.y));
+                        const float2 d = make_float2(max3f(da.x, db.x, 0.0f), max3f(da.y, db.y, 0.0f));
+                        acc = ffma2(d, d, acc);
+                    }
+                }
+            }
+            a = acc.x + acc.y;
+        }
+        flush(pend);  // the previous batch's appends (its atomics have long returned)
+        const float bnd = q8_lbk_bound(a, meta.y);
+        Pend pd;
+        pd.pass = ok && bnd <= thr;
+        pd.rq = rlist && pd.pass && bnd <= rho * thr;
+        pd.pass = pd.pass && !pd.rq;
+        pd.fr = pd.pass && bnd <= thr * front;
+        pd.rmask = __ballot_sync(0xffffffffu, pd.rq);
+        pd.passmask = __ballot_sync(0xffffffffu, pd.pass);
+        pd.frontmask = __ballot_sync(0xffffffffu, pd.fr);
+        pd.rb = pd.fb = pd.bb = 0u;
+        if (lane == 0) {
+            if (pd.rmask) pd.rb = atomicAdd(&st->rev_count, (unsigned)__popc(pd.rmask));
+            if (pd.frontmask) pd.fb = atomicAdd(&st->list2_count, (unsigned)__popc(pd.frontmask));
+            if (pd.passmask & ~pd.frontmask) pd.bb = atomicAdd(&st->list2_back, (unsigned)__popc(pd.passmask & ~pd.frontmask));
+        }
+        pd.e = pd.rq ? make_uint4(cur.ce.x, __float_as_uint(a), __float_as_uint(meta.x), __float_as_uint(meta.y))
+                     : make_uint4(cur.id, __float_as_uint(a), __float_as_uint(meta.x), __float_as_uint(meta.y));
+        pend = pd;
+        __syncwarp();  // every lane is done with buffer b before the next issue refills it
+        cur = nxt;
+    }
+    flush(pend);
 }
 
 // Work distribution of the per-thread refine kernels: a lane that finishes (or skips) a
