@@ -468,10 +468,13 @@ def dtw_roofline(run, steps):
     achieved = cells / (ms / 1e3)
     peak = dtw_cell_peak(run["clocks"].get("sm_max_mhz", 1965.0) or 1965.0)
     lbk_ms, _ = run["prof"]["lbk"]
-    # strip refine reaches (r >= 7): the filter reads the quantised rows (n bytes + 8 B of
-    # scale / error per candidate); register-band reaches: the raw rows (4n bytes)
-    per_cand = run["n"] + 8 if (run.get("reach") or 0) >= 7 else 4 * run["n"]
-    lbk_bytes = sum(per_cand * s["candidates"] + 16 * s["lbk_pass"] for s in st) * steps
+    # strip refine reaches (r >= 7): the forward filter reads the candidate entry (8 B), the
+    # quantised row (n bytes) and its scale / error (8 B); the reverse bound (stats "exact":
+    # its evaluations) writes and reads a 16 B queue entry, reads the row again and its id
+    # (4 B); every survivor is a 16 B list2 entry.  Register-band reaches: raw rows (4n bytes)
+    n = run["n"]
+    per_cand = n + 16 if (run.get("reach") or 0) >= 7 else 4 * n + 8
+    lbk_bytes = sum(per_cand * s["candidates"] + (n + 36) * s["exact"] + 16 * s["lbk_pass"] for s in st) * steps
     return {"bound": "alu", "kernel": "k_refine_dtw_strip<8,REM> (fp32 banded DTW, one thread per candidate; "
                                       "k_refine_dtw<R> at R = 2, 5)",
             "achieved": achieved, "peak": peak, "unit": "cells/s", "frac": achieved / peak,
@@ -480,7 +483,9 @@ def dtw_roofline(run, steps):
             "peak_source": "derived (DESIGN.md 6): issue limit 1 warp-instr / cycle / SMSP at >= 2 instr per cell "
                            "(FMNMX3 + paired FADD2/FFMA2), 148 SMs x 4 SMSP, max SM clock",
             "time": "CUDA events around the refine launches in a serial pass of the same steps (no stage overlap)",
-            "lbk_filter": {"bound": "hbm", "achieved_gbs": lbk_bytes / (lbk_ms / 1e3) / 1e9 if lbk_ms > 0 else None,
+            "lbk_filter": {"bound": "hbm", "kernels": "k_lbk_filter_q8b (forward, bulk-copy rows) + k_lbk_rev_q8 "
+                                                      "(reverse over the forward survivors)",
+                           "achieved_gbs": lbk_bytes / (lbk_ms / 1e3) / 1e9 if lbk_ms > 0 else None,
                            "frac": lbk_bytes / (lbk_ms / 1e3) / 1e9 / peaks().get("hbm_gbs", 6650.0)
                            if lbk_ms > 0 else None,
                            "ms_per_step": lbk_ms / steps, "bytes_per_query": lbk_bytes / steps / len(st)}}

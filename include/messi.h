@@ -74,15 +74,17 @@ typedef struct {
     int64_t candidates;   /* series whose iSAX bound <= BSF0 * (1 + eps) */
     int64_t lbk_pass;     /* DTW: candidates passing the LB_Keogh filter against BSF0: the bound
                              from the quantised row, (sqrt(LBK(x^)) - e)^2, at reaches served by
-                             the strip refine (r >= 7), the raw LB_Keogh otherwise */
+                             the strip refine (r >= 7), the raw LB_Keogh otherwise; where the
+                             filter has the reverse bound (n, reach in MESSI_REV_SPECS) that too */
     int64_t refined;      /* real distances computed (fp32) in the refine step */
     int64_t abandoned;    /* real distance computations abandoned early */
     int64_t near_best;    /* fp32 near-ties re-ranked exactly in fp64 */
     int64_t dtw_cells;    /* DTW: valid band cells (|i - j| <= r inside the n x n matrix) of the rows the
                              fp32 refine evaluated -- n(2r+1) - r(r+1) per completed candidate, the
                              rows done for an abandoned one */
-    int64_t exact;        /* real distances over the raw fp32 rows: ED = candidates whose
-                             quantised-row bound did not prune them; DTW = refined */
+    int64_t exact;        /* ED: real distances over the raw fp32 rows = candidates whose
+                             quantised-row bound did not prune them; DTW: reverse
+                             LB_Keogh bounds evaluated (forward survivors; 0 without that filter) */
     int64_t tiles_listed; /* tiles whose box bound <= BSF0 * (1 + eps) (the filter's list); ED scans
                              those still within the CURRENT BSF when reached (tiles_scanned) */
     int64_t coarse;       /* series whose cardinality-16 bound passed (their 8-bit bound evaluated) */

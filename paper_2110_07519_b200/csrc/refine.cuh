@@ -1119,7 +1119,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
         s->abandoned = st->abandoned;
         s->near = nb;
         s->cells = (long long)st->dtw_cells;
-        s->exact = st->exact ? st->exact : st->refined;
+        s->exact = st->rev_count;  // DTW: reverse LB_Keogh evaluations
         s->listed = st->tile_count;
         s->coarse = st->coarse_count;
         s->seed = (double)__uint_as_float(st->seed_bits);

@@ -518,6 +518,10 @@ def test_nn_dtw(c1, reach, strip, monkeypatch):
             check_nn(got, d2[qi], ids[qi])
             st = got[3]
             assert st["candidates"] >= st["lbk_pass"] >= 1
+            if reach in REV_REACHES:  # the reverse bound ran on the forward survivors
+                assert st["candidates"] >= st["exact"] >= st["lbk_pass"]
+            else:
+                assert st["exact"] == 0
         res = messi().result_buffer(3, DEV)
         idx2.query_batch(Q[:3].contiguous(), reach, res)
         torch.cuda.synchronize()
