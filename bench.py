@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-dtw", action="store_true", help="skip the secondary DTW measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
     ap.add_argument("--cpu-queries", type=int, default=32, help="queries of the oracle timing sample")
+    ap.add_argument("--steady", type=int, default=500000,
+                    help="DTW: candidates of the steady-state refine measurement (0: skip)")
     ap.add_argument("--window", type=int, default=0, help="approximate-search window (0: library default 2000)")
     ap.add_argument("--knn", type=int, default=10, help="ED: also time exact k-NN with this k (<= 1: skip)")
     ap.add_argument("--latency", type=int, default=20,
@@ -355,10 +357,27 @@ def run_arm(cfg, args, world, rank, dev, stream, time_steps, warmup, repeats=1):
                 l1.record(stream)
                 torch.cuda.synchronize()
                 lat.append(l0.elapsed_time(l1))
+        # DTW refine kernel at steady state: the query path's refine kernel over a long list of
+        # candidates in its inspection mode (frozen: every candidate runs all n rows, no abandon)
+        # -- its cell rate without the per-query tail of a short list; CUDA events around the
+        # refine launch (messi_debug_dtw_stages, profiling on)
+        steady = None
+        if world == 1 and reach is not None and args.steady > 0:
+            ids = torch.arange(min(args.steady, X.shape[0]), dtype=torch.int32, device=dev)
+            M.messi_debug_dtw_stages(idx.handle, Q[0].contiguous(), reach, ids)  # warm-up
+            torch.cuda.synchronize()
+            M.messi_profile_enable(idx.handle, True)
+            M.messi_debug_dtw_stages(idx.handle, Q[0].contiguous(), reach, ids)
+            torch.cuda.synchronize()
+            sms, _ = M.messi_profile_read(idx.handle, "refine")
+            M.messi_profile_enable(idx.handle, False)
+            n_, r_ = cfg["n"], min(reach, cfg["n"] - 1)
+            cells = ids.numel() * (n_ * (2 * r_ + 1) - r_ * (r_ + 1))
+            steady = {"candidates": ids.numel(), "cells": cells, "ms": sms}
     out = dict(ms=ms, rep_ms=rep_ms, build_ms=build_ms, build_phases=build_phases, launches=launches, prof=prof,
                prof_ms=prof_ms, stats=st, clocks=clk_all[0].summary(), e2e_ms=e2e_ms, knn_ms=knn, nq=nq,
                N_local=X.shape[0], n=cfg["n"], reach=reach, h2d=qh.numel() * 4, d2h=rh.numel(), latency_ms=lat,
-               last=last)
+               last=last, steady=steady)
     idx.close()
     del X, Q
     torch.cuda.empty_cache()
@@ -455,6 +474,20 @@ def dtw_cell_peak(sm_mhz=1965.0, sms=148):
     return sms * 4 * 32 / 2.0 * sm_mhz * 1e6
 
 
+def steady_refine(run):
+    """The refine kernel's cell rate on a long frozen candidate list (run["steady"])."""
+    sd = run.get("steady")
+    if not sd or sd["ms"] <= 0:
+        return None
+    peak = dtw_cell_peak(run["clocks"].get("sm_max_mhz", 1965.0) or 1965.0)
+    rate = sd["cells"] / (sd["ms"] / 1e3)
+    return {"achieved": rate, "peak": peak, "unit": "cells/s", "frac": rate / peak,
+            "candidates": sd["candidates"], "ms": sd["ms"],
+            "what": "the same refine kernel over the first %d rows as candidates in its inspection mode "
+                    "(frozen: every candidate runs all n rows), CUDA events around its launch: the kernel's "
+                    "rate without the per-query tail of a short candidate list" % sd["candidates"]}
+
+
 def dtw_roofline(run, steps):
     """Roofline of the DTW refine: valid band cells (counted by the kernels, SURVEY 8(d):
     n(2r+1) - r(r+1) per completed candidate, the rows done for an abandoned one) over the
@@ -483,6 +516,7 @@ def dtw_roofline(run, steps):
             "peak_source": "derived (DESIGN.md 6): issue limit 1 warp-instr / cycle / SMSP at >= 2 instr per cell "
                            "(FMNMX3 + paired FADD2/FFMA2), 148 SMs x 4 SMSP, max SM clock",
             "time": "CUDA events around the refine launches in a serial pass of the same steps (no stage overlap)",
+            "steady_state": steady_refine(run),
             "lbk_filter": {"bound": "hbm", "kernels": "k_lbk_filter_q8b (forward, bulk-copy rows) + k_lbk_rev_q8 "
                                                       "(reverse over the forward survivors)",
                            "achieved_gbs": lbk_bytes / (lbk_ms / 1e3) / 1e9 if lbk_ms > 0 else None,

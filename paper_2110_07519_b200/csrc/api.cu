@@ -1743,7 +1743,10 @@ extern "C" messi_status messi_debug_dtw_stages(messi_index* idx, const float* qu
     LAUNCHED(idx);
     if (rev_dev) CK(cudaMemsetAsync(rev_dev, 0xff, sizeof(float) * (size_t)k, s));
     TRY(launch_lbk_filter(idx, sl, reach, strip, query_dev, s, rev_dev));
-    TRY(launch_dtw_refine(idx, sl, reach, strip, query_dev, s));
+    {
+        ProfScope ps(idx, K_REFINE, s);  // profiling on: the frozen refine's own time (bench steady-state rate)
+        TRY(launch_dtw_refine(idx, sl, reach, strip, query_dev, s));
+    }
     if (lbk_dev) CK(cudaMemsetAsync(lbk_dev, 0xff, sizeof(float) * (size_t)k, s));
     if (d32_dev) CK(cudaMemsetAsync(d32_dev, 0xff, sizeof(float) * (size_t)k, s));
     k_dbg_scatter_dtw<<<grid_of(k, 256), 256, 0, s>>>(sl.list2, sl.near, sl.st, idx->dbg_map, lbk_dev, d32_dev);
