@@ -341,11 +341,12 @@ __device__ __forceinline__ float lbk_rev_q8(const unsigned* row, float s, const 
     constexpr int NB = NN / 8, A = RR / 8, R0 = RR % 8, P = 2 * A + 3;
     unsigned pre[P][8], suf[P][8];
     auto vmax = [](unsigned x, unsigned y) { return __vmaxu2(x, y); };
-    // block k (runtime, uniform) into ring slot SL: its pairs, prefix and suffix maxima
-    auto load = [&](int k, auto SL) {
+    // block k into ring slot SL: its pairs, prefix and suffix maxima; VALID (compile-time)
+    // says whether k is inside [0, NB) -- outside, the block is absent (all pairs 0)
+    auto load = [&](int k, auto SL, auto VALID) {
         constexpr int sl = decltype(SL)::value;
         unsigned x[8];
-        if (k >= 0 && k < NB) {
+        if constexpr (decltype(VALID)::value) {
             unsigned w0, w1;
             asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
                          : "=r"(w0), "=r"(w1)
@@ -371,50 +372,57 @@ __device__ __forceinline__ float lbk_rev_q8(const unsigned* row, float s, const 
     };
     static_for<2 * A + 2>([&](auto I) {  // blocks -A-1 .. A
         constexpr int k = decltype(I)::value - A - 1;
-        load(k, std::integral_constant<int, (k + P) % P>{});
+        load(k, std::integral_constant<int, (k + P) % P>{}, std::integral_constant<bool, (k >= 0 && k < NB)>{});
     });
     const float inv = __frcp_rn(s);  // exact: s is a power of two
     const float2 sc2 = make_float2(inv, -inv), kk2 = make_float2(32895.5f, 32894.5f);
     float2 acc = make_float2(0.0f, 0.0f);
-#pragma unroll 1
-    for (int b0 = 0; b0 < NB; b0 += P) {
-        static_for<P>([&](auto J) {
-            constexpr int j = decltype(J)::value;
-            const int b = b0 + j;
-            if (b < NB) {
-                load(b + A + 1, std::integral_constant<int, (j + A + 1) % P>{});
-                unsigned core = pre[(j - A + 1 + P) % P][7];
-                static_for<2 * A - 2>([&](auto D) {
-                    constexpr int d = decltype(D)::value - A + 2;
-                    core = vmax(core, pre[(j + d + P) % P][7]);
-                });
-                const unsigned ml = vmax(core, pre[(j - A + P) % P][7]), mr = vmax(core, pre[(j + A) % P][7]);
-                const unsigned mlr = vmax(ml, pre[(j + A) % P][7]);
-                const float4 qa = *reinterpret_cast<const float4*>(Q + 8 * b);
-                const float4 qb = *reinterpret_cast<const float4*>(Q + 8 * b + 4);
-                const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-                float dd[8];
-                static_for<8>([&](auto T) {
-                    constexpr int t = decltype(T)::value;
-                    constexpr bool lft = t < R0, rgt = t + R0 >= 8;
-                    constexpr int sl_l = (j - A - (lft ? 1 : 0) + 2 * P) % P, ol = (t - R0 + 8) % 8;
-                    constexpr int sl_h = (j + A + (rgt ? 1 : 0)) % P, oh = (t + R0) % 8;
-                    const unsigned mid = lft ? (rgt ? mlr : ml) : (rgt ? mr : core);
-                    const unsigned e = __vimax3_u16x2(suf[sl_l][ol], mid, pre[sl_h][oh]);
-                    // (2^15 + Ub, 2^15 + 255 - Lb) as floats
-                    float2 f;
-                    asm("prmt.b32 %0, %1, %2, 0x7614;" : "=r"(*reinterpret_cast<unsigned*>(&f.x)) : "r"(e), "r"(mg));
-                    asm("prmt.b32 %0, %1, %2, 0x7634;" : "=r"(*reinterpret_cast<unsigned*>(&f.y)) : "r"(e), "r"(mg));
-                    const float2 qk = ffma2_rd(make_float2(qv[t], qv[t]), sc2, kk2);
-                    const float2 ac = fsub2_rd(qk, f);
-                    dd[t] = max3f(ac.x, ac.y, 0.0f);
-                });
-#pragma unroll
-                for (int p = 0; p < 4; ++p)
-                    acc = ffma2_rd(make_float2(dd[2 * p], dd[2 * p + 1]), make_float2(dd[2 * p], dd[2 * p + 1]), acc);
-            }
+    // output block b (ring position j = b mod P): loads block b + A + 1 (present iff LV), then
+    // the envelope and terms of points 8b .. 8b+7
+    auto step = [&](int b, auto J, auto LV) {
+        constexpr int j = decltype(J)::value;
+        load(b + A + 1, std::integral_constant<int, (j + A + 1) % P>{}, LV);
+        unsigned core = pre[(j - A + 1 + P) % P][7];
+        static_for<2 * A - 2>([&](auto D) {
+            constexpr int d = decltype(D)::value - A + 2;
+            core = vmax(core, pre[(j + d + P) % P][7]);
         });
-    }
+        const unsigned ml = vmax(core, pre[(j - A + P) % P][7]), mr = vmax(core, pre[(j + A) % P][7]);
+        const unsigned mlr = vmax(ml, pre[(j + A) % P][7]);
+        const float4 qa = *reinterpret_cast<const float4*>(Q + 8 * b);
+        const float4 qb = *reinterpret_cast<const float4*>(Q + 8 * b + 4);
+        const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+        float dd[8];
+        static_for<8>([&](auto T) {
+            constexpr int t = decltype(T)::value;
+            constexpr bool lft = t < R0, rgt = t + R0 >= 8;
+            constexpr int sl_l = (j - A - (lft ? 1 : 0) + 2 * P) % P, ol = (t - R0 + 8) % 8;
+            constexpr int sl_h = (j + A + (rgt ? 1 : 0)) % P, oh = (t + R0) % 8;
+            const unsigned mid = lft ? (rgt ? mlr : ml) : (rgt ? mr : core);
+            const unsigned e = __vimax3_u16x2(suf[sl_l][ol], mid, pre[sl_h][oh]);
+            // (2^15 + Ub, 2^15 + 255 - Lb) as floats
+            float2 f;
+            asm("prmt.b32 %0, %1, %2, 0x7614;" : "=r"(*reinterpret_cast<unsigned*>(&f.x)) : "r"(e), "r"(mg));
+            asm("prmt.b32 %0, %1, %2, 0x7634;" : "=r"(*reinterpret_cast<unsigned*>(&f.y)) : "r"(e), "r"(mg));
+            const float2 qk = ffma2_rd(make_float2(qv[t], qv[t]), sc2, kk2);
+            const float2 ac = fsub2_rd(qk, f);
+            dd[t] = max3f(ac.x, ac.y, 0.0f);
+        });
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+            acc = ffma2_rd(make_float2(dd[2 * p], dd[2 * p + 1]), make_float2(dd[2 * p], dd[2 * p + 1]), acc);
+    };
+    // ring periods whose every step is inside [0, NB) and loads a present block run as a
+    // loop; the rest (the last < 2P steps) are unrolled with their bounds known at compile time
+    constexpr int CLEAN = NB - A - P > 0 ? (NB - A - P + P - 1) / P : 0;  // periods b0 < NB - A - P
+#pragma unroll 1
+    for (int b0 = 0; b0 < CLEAN * P; b0 += P)
+        static_for<P>([&](auto J) { step(b0 + decltype(J)::value, J, std::true_type{}); });
+    static_for<2 * P>([&](auto I) {
+        constexpr int b = CLEAN * P + decltype(I)::value;
+        if constexpr (b < NB)
+            step(b, std::integral_constant<int, b % P>{}, std::integral_constant<bool, (b + A + 1 < NB)>{});
+    });
     return __fmul_rd(__fadd_rd(acc.x, acc.y), s * s);
 }
 
