@@ -754,9 +754,10 @@ def ours(args):
                        "steps": k4, "ms_per_step": dms / k4,
                        "kernel_ms_per_step_serial": {k: v[0] / k4 for k, v in d["prof"].items()},
                        "serial_pass_ms_per_step": d["prof_ms"] / k4,
-                       "stats_mean": {k: dm(k) for k in ("lb_computed", "tiles_scanned", "candidates", "lbk_pass",
-                                                         "refined", "abandoned", "near_best", "dtw_cells",
-                                                         "coarse", "seed_d2", "bsf_d2")},
+                       "stats_mean": {**{k: dm(k) for k in ("lb_computed", "tiles_scanned", "candidates", "lbk_pass",
+                                                            "refined", "abandoned", "near_best", "dtw_cells",
+                                                            "coarse", "seed_d2", "bsf_d2")},
+                                      "reverse_evaluated": dm("exact")},
                        "gpu_launches": d["launches"], "roofline": dtw_roofline(d, k4),
                        "stats_dist": dist_of(dst)}
         if d.get("latency_ms"):
