@@ -29,6 +29,9 @@ constexpr int kChunkTiles = 16;          // tiles per work chunk (2 per warp)
 #define MESSI_FUSED_WARPS 12
 #endif
 constexpr int kFusedWarps = MESSI_FUSED_WARPS;  // 2 CTAs of 12 warps per SM (64 KB table each)
+#ifndef MESSI_FUSED_MINB
+#define MESSI_FUSED_MINB 2
+#endif
 constexpr int kCandBuf = 64;            // per-warp buffer of fine survivors awaiting the refine
 constexpr int kBatchMax = 128;           // queries per launch group
 constexpr int kFilterQ = 2;              // queries per filter CTA
@@ -617,7 +620,7 @@ __host__ __device__ inline size_t fused_qpad(int n) { return (size_t)(n + 4 * ((
 __host__ __device__ inline size_t fused_smem(int n)
 {
     return (size_t)kLutX * 4 + fused_qpad(n) * 4 + (size_t)n +
-           (size_t)kFusedWarps * (2 * MESSI_TILE_ROWS * 2 + kCandBuf * 4 + 4);
+           (size_t)kFusedWarps * (2 * MESSI_TILE_ROWS * 2 + kCandBuf * 4 + 4 + 16);
 }
 
 // Writes query b's result and stats (finish_query's layout) from its state.
@@ -709,6 +712,8 @@ __device__ __forceinline__ unsigned q8i_bound_pass(int count, unsigned my_pos, c
     const int g = lane >> 2, gl = lane & 3;
     const int nch = n >> 4;
     int my_dq = 0, my_ss = 0;  // sum c_x c_q, sum c_x^2 of this lane's candidate (exact int32)
+    // the row's (scale, error), issued before the row passes (a random 8-byte gather)
+    const float2 mt = lane < count ? meta8[my_pos] : make_float2(0.0f, 0.0f);
 #pragma unroll 1
     for (int p = 0; 8 * p < count; ++p) {
         const int c = 8 * p + g;
@@ -736,7 +741,6 @@ __device__ __forceinline__ unsigned q8i_bound_pass(int count, unsigned my_pos, c
     }
     bool survives = true;
     if (lane < count) {
-        const float2 mt = meta8[my_pos];
         const double sx = (double)mt.x;  // a power of two
         const double t2 = sx * sx * (double)my_ss, t3 = 2.0 * qq.sq * sx * (double)my_dq;  // exact products
         const double d2 = (qq.s2ss + t2) - t3;
@@ -762,7 +766,12 @@ __device__ __forceinline__ void prefetch_l2_lines(const void* p, int bytes)
 // each round loads the next round's words before evaluating its own.  Fine survivors
 // (LB8 <= thr) wait in the warp's buffer cbuf (prefetched into L2); every full round of 32
 // goes through the quantised bound and the exact passes.
-struct WarpCounts { unsigned tiles, coarse, cand, exact; };
+// The warp's per-query counters live in shared memory (lane 0 updates them; registers are
+// the fused kernel's occupancy limit): c[0] tiles, c[1] coarse, c[2] cand, c[3] exact.
+struct WarpCounts {
+    unsigned* c;
+    __device__ __forceinline__ void add(int i, unsigned v, int lane) const { if (lane == 0) c[i] += v; }
+};
 
 struct FusedCtx {
     const uint4* sym8;
@@ -786,7 +795,7 @@ __device__ __forceinline__ void refine_round(const FusedCtx& cx, unsigned cp, in
                                              WarpCounts& wc, int lane)
 {
     const unsigned keep = q8i_bound_pass(count, cp, cx.rows8, cx.meta8, cx.n, cx.qc_s, cx.qq, thr, lane);
-    wc.exact += __popc(keep);
+    wc.add(3, __popc(keep), lane);
     if (keep) thr = fminf(thr, slack_up(exact_pass<LINKED, KNN>(keep, cp, cx.perm, cx.rows, cx.n, cx.q_p, cx.st,
                                                                    cx.ps, cx.b, cx.knn, cx.k, lane)));
 }
@@ -820,7 +829,7 @@ __device__ __forceinline__ void fine_and_refine(const FusedCtx& cx, long long ti
                 prefetch_l2_lines(cx.rows8 + (long long)pos * cx.n, cx.n);
             }
             ncb += __popc(pass);
-            wc.cand += __popc(pass);
+            wc.add(2, __popc(pass), lane);
             __syncwarp();
             if (ncb >= 32) {
                 const unsigned cp = cbuf[lane];
@@ -835,6 +844,18 @@ __device__ __forceinline__ void fine_and_refine(const FusedCtx& cx, long long ti
         pos = pos_n;
         w = w_n;
     }
+}
+
+// A claim of the next work item (one lane): atom.inc with limit 2^31 - 1 (a counter of tile
+// pairs never gets there), which ptxas keeps as one ATOMG.E.INC -- an add (or an inc with
+// limit 2^32 - 1, which it turns into an add) becomes a warp-aggregated atomic whose result
+// is broadcast with a shuffle right after it, so the warp would wait for the round trip at
+// the claim instead of where the value is first used.
+__device__ __forceinline__ unsigned claim_next(unsigned* p)
+{
+    unsigned r;
+    asm volatile("atom.global.inc.u32 %0, [%1], 2147483647;" : "=r"(r) : "l"(p) : "memory");
+    return r;
 }
 
 // Persistent.  CTA j starts at query j mod B and walks the batch's queries cyclically once;
@@ -853,7 +874,7 @@ __device__ __forceinline__ void fine_and_refine(const FusedCtx& cx, long long ti
 // their CTAs help the heavy ones.  k_finalise_batch writes the results.  KNN = true adds the
 // warp-cooperative k-NN insert (k > 16).
 template <bool LINKED, bool KNN>
-__global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
+__global__ void __launch_bounds__(32 * kFusedWarps, MESSI_FUSED_MINB) k_scan_refine_ed(
     const uint4* __restrict__ tiles, const uint4* __restrict__ sym8, long long ntiles, long long N, int n,
     const float* __restrict__ queries, const float* __restrict__ lutx_all, const uint2* __restrict__ tlist_all,
     QState* st_all, int B, const unsigned char* __restrict__ rows8, const float2* __restrict__ meta8,
@@ -871,6 +892,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
     unsigned short* survb = surv_all + warp * 2 * MESSI_TILE_ROWS;  // two lists: current / previous tile
     unsigned* cbuf = cbuf_all + warp * kCandBuf;
     unsigned* wcnt = wcnt_all + warp;
+    unsigned* wcs = wcnt_all + kFusedWarps + 4 * warp;  // the warp's per-query counters
     __shared__ int s_has;
     FusedCtx cx;
     cx.sym8 = sym8; cx.rows8 = rows8; cx.meta8 = meta8; cx.perm = perm; cx.rows = rows; cx.q_p = q_p;
@@ -903,7 +925,8 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
         const uint2* tl = tlist_all + (size_t)b * ntiles;
         // list position of claim k: the front bin, then the back bin from its far end
         auto at = [&](unsigned kk) { return tl[kk < c0 ? kk : (unsigned)ntiles - 1u - (kk - c0)]; };
-        WarpCounts wc{0, 0, 0, 0};
+        WarpCounts wc{wcs};
+        if (lane == 0) wcs[0] = wcs[1] = wcs[2] = wcs[3] = 0u;
         unsigned ncb = 0;        // fine survivors pending in cbuf (warp-uniform)
         int pm = 0, cur = 0;     // previous tile's coarse survivors (list survb[cur ^ 1])
         long long ptile = 0;
@@ -924,22 +947,26 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
         uint2 te1 = kc + 1 < count ? at(kc + 1) : make_uint2(0u, 0x7f800000u);
         while (kc < count) {
             // lane 0: claim pair i + 2, read the best-so-far, load pair i + 1's entries (used later)
+            // (lane 0's block only issues the atomic and the loads; their results are first
+            // used after pair i's first tile, so no instruction in the divergent block waits
+            // on them and the warp reconverges at once)
             unsigned k2 = 0;
             float thr_n = 0.0f;
             uint2 ne0 = make_uint2(0u, 0x7f800000u), ne1 = make_uint2(0u, 0x7f800000u);
             if (lane == 0) {
                 if (kn < count) {
-                    k2 = atomicAdd(&st->next_tile, 1u) * 2u;
+                    k2 = claim_next(&st->next_tile);  // pair index: x2 when consumed
                     ne0 = at(kn);
                     if (kn + 1 < count) ne1 = at(kn + 1);
                 } else {
-                    k2 = kn;
+                    k2 = kn >> 1;
                 }
-                thr_n = slack_up(ld_bsf_l<LINKED>(st, ps.epoch));
+                thr_n = ld_bsf_l<LINKED>(st, ps.epoch);  // raw: slack_up when consumed
             }
 #pragma unroll 1
             for (int u = 0; u < 2; ++u) {
                 if (u == 1 && lane == 0) {  // pair i + 1's tiles into L2, unless already box-pruned
+                    thr_n = slack_up(thr_n);
                     if (__uint_as_float(ne0.y) <= thr_n)
                         prefetch_l2_bulk(tiles + (long long)ne0.x * (MESSI_TILE_BYTES / 16), MESSI_TILE_BYTES);
                     if (__uint_as_float(ne1.y) <= thr_n)
@@ -948,11 +975,11 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
                 const uint2 te = u == 0 ? te0 : te1;
                 MESSI_CHECK(kc + u >= count || te.x < (unsigned)ntiles);
                 if (kc + u >= count || __uint_as_float(te.y) > thr) continue;  // box pruned (warp-uniform)
-                ++wc.tiles;
+                wc.add(0, 1u, lane);
                 const long long tile = te.x;
                 unsigned short* surv = survb + cur * MESSI_TILE_ROWS;
                 const int m = scan_tile_coarse(tiles, tile, cx.lbase, thr, N, surv, wcnt, lane);
-                wc.coarse += m;
+                wc.add(1, (unsigned)m, lane);
                 if (pm)
                     fine_and_refine<LINKED, KNN>(cx, ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, cbuf, ncb,
                                                  thr, wc, lane);
@@ -965,7 +992,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
             }
             // advance the pipeline
             kc = kn;
-            kn = __shfl_sync(0xffffffffu, k2, 0);
+            kn = __shfl_sync(0xffffffffu, k2, 0) * 2u;
             thr = fminf(thr, __shfl_sync(0xffffffffu, thr_n, 0));
             te0 = make_uint2(__shfl_sync(0xffffffffu, ne0.x, 0), __shfl_sync(0xffffffffu, ne0.y, 0));
             te1 = make_uint2(__shfl_sync(0xffffffffu, ne1.x, 0), __shfl_sync(0xffffffffu, ne1.y, 0));
@@ -980,11 +1007,11 @@ __global__ void __launch_bounds__(32 * kFusedWarps, 2) k_scan_refine_ed(
             ncb = 0;
         }
         if (lane == 0) {
-            if (wc.tiles) atomicAdd(&st->tiles_scanned, wc.tiles);
-            if (wc.cand) atomicAdd(&st->cand_count, wc.cand);
-            if (wc.cand) atomicAdd(&st->refined, wc.cand);
-            if (wc.coarse) atomicAdd(&st->coarse_count, wc.coarse);
-            if (wc.exact) atomicAdd(&st->exact, wc.exact);
+            if (wcs[0]) atomicAdd(&st->tiles_scanned, wcs[0]);
+            if (wcs[2]) atomicAdd(&st->cand_count, wcs[2]);
+            if (wcs[2]) atomicAdd(&st->refined, wcs[2]);
+            if (wcs[1]) atomicAdd(&st->coarse_count, wcs[1]);
+            if (wcs[3]) atomicAdd(&st->exact, wcs[3]);
         }
         __syncthreads();  // every warp is done with b's table before it is overwritten
     }
