@@ -83,7 +83,8 @@ struct messi_index {
         QState* bst = nullptr;
         float *lutc = nullptr, *lutx = nullptr, *lutf = nullptr;
         unsigned* qc = nullptr;   // quantised queries [kBatchMax][n / 4] (4 x s8 per word)
-        uint2* btlist = nullptr;
+        uint2* btlist = nullptr;  // listed tiles, best-first (k_order_tiles)
+        uint2* tstage = nullptr;  // listed tiles as the filter appends them
         KnnState* knn = nullptr;  // k-NN state (lazy)
         float* seedd = nullptr;   // k-NN: the window distances of every query (lazy)
     } bset[2];
@@ -515,7 +516,7 @@ extern "C" void messi_free(messi_index* idx)
             if (p) cudaIpcCloseMemHandle(p);
     if (idx->d_peers) cudaFree(idx->d_peers);
     for (auto& bs : idx->bset) {
-        void* bp[] = {bs.bst, bs.lutc, bs.lutx, bs.lutf, bs.qc, bs.btlist, bs.knn, bs.seedd};
+        void* bp[] = {bs.bst, bs.lutc, bs.lutx, bs.lutf, bs.qc, bs.btlist, bs.tstage, bs.knn, bs.seedd};
         for (void* p : bp)
             if (p) cudaFree(p);
     }
@@ -732,6 +733,7 @@ static messi_status ensure_batch_buffers(messi_index* idx)
         TRY(dalloc(&bs.lutf, (size_t)kBatchMax * kLutF));
         TRY(dalloc(&bs.qc, (size_t)kBatchMax * (idx->n / 4)));
         TRY(dalloc(&bs.btlist, (size_t)kBatchMax * (size_t)idx->ntiles));
+        TRY(dalloc(&bs.tstage, (size_t)kBatchMax * (size_t)idx->ntiles));
     }
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan_refine_ed<false, false>, 32 * kFusedWarps, fused_smem(idx->n)));
@@ -783,8 +785,10 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
         if (fx > fcap) fx = fcap;
         dim3 fg((unsigned)fx, (unsigned)npairs);
         k_filter_batch<<<fg, 256, kFilterQ * kLutF * 4, st>>>(reinterpret_cast<const uint4*>(idx->boxes), idx->sboxes,
-                                                              idx->ntiles, nsuper, bs.lutf, bs.bst, B, bs.btlist,
+                                                              idx->ntiles, nsuper, bs.lutf, bs.bst, B, bs.tstage,
                                                               peers.epoch);
+        LAUNCHED(idx);
+        k_order_tiles<<<B, 1024, 0, st>>>(bs.tstage, bs.bst, idx->ntiles, bs.btlist);
         LAUNCHED(idx);
     }
     {

@@ -55,6 +55,7 @@ struct QState {
     unsigned next_tile;     // batch ED: next pair of listed tiles to hand out
     unsigned tiles_done;    // batch ED: listed tiles finished (the warp finishing the last finalises)
     unsigned lock;          // batch ED: guards best_d / best_id
+    unsigned tile_hist[16]; // batch ED: listed tiles per best-first bin (k_filter_batch -> k_order_tiles)
     unsigned long long dtw_cells;  // DTW band cells evaluated in fp32 (refine)
     unsigned long long gbsf; // batch ED: the epoch-tagged best-so-far of all shards (PeerSet)
     double best_d;          // batch ED: lexicographic min (d64, id) over the fp64 re-ranked rows
@@ -122,6 +123,7 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->next_tile = 0;
     st->coarse_count = 0;
     st->tiles_done = 0;
+    for (int j = 0; j < 16; ++j) st->tile_hist[j] = 0;
     st->lock = 0;
     st->best_d = (double)INFINITY;
     st->best_id = -1;

@@ -35,6 +35,25 @@ constexpr int kFusedWarps = MESSI_FUSED_WARPS;  // 2 CTAs of 12 warps per SM (64
 constexpr int kCandBuf = 64;            // per-warp buffer of fine survivors awaiting the refine
 constexpr int kBatchMax = 128;           // queries per launch group
 constexpr int kFilterQ = 2;              // queries per filter CTA
+constexpr int kTileBins = 16;            // best-first bins of a query's tile list (k_order_tiles)
+constexpr unsigned kTileMask = 0x0fffffffu;    // list entry .x: tile | bin << 28
+constexpr unsigned kClaimsDone = 0x40000000u;  // next_tile raised to this: no listed pair left
+
+// Best-first bins of a query's listed tiles: bin j = min(15, (int)fl(lb * sc)) with sc = 16 /
+// (BSF0 (1 + eps)) from the query's local seed (the same value in every kernel: the filter
+// keeps lb <= BSF (1 + eps) <= that, so bins cover [0, 15]); sc = 0 (no finite seed): bin 0.
+__device__ __forceinline__ float tile_bin_scale(const QState* st)
+{
+    const float t = slack_up(__uint_as_float(*(volatile const unsigned*)&st->seed_bits));
+    return (t > 0.0f && t < INFINITY) ? (float)kTileBins / t : 0.0f;
+}
+__device__ __forceinline__ int tile_bin(float lb, float sc) { return min(kTileBins - 1, (int)(lb * sc)); }
+// A lower bound of every bound in bin j: fl(lb sc) >= j, so lb sc >= j (1 - 2^-24) and
+// lb >= j / sc (1 - 2^-24) >= fl_rd(j / sc) (1 - 2^-20).
+__device__ __forceinline__ float tile_bin_floor(int j, float sc)
+{
+    return (j == 0 || sc == 0.0f) ? 0.0f : __fdiv_rd((float)j, sc) * (1.0f - 0x1p-20f);
+}
 
 // ------------------------------------------------------------------------ prologue
 // One CTA per query: arms the query's state, runs the prologue (prologue_block: PAA in fp64,
@@ -286,7 +305,8 @@ __global__ void k_superbox(const uint4* __restrict__ boxes, long long ntiles, ui
 
 // Two-level filter, kFilterQ queries per CTA: a warp tests 32 super-tiles (one per lane);
 // the tiles of every super-tile that passes are tested 16 at a time (half-warps), and the
-// kept tiles are appended as (tile, bound) to the query's list.
+// kept tiles are appended as (tile, bound) to the query's staging list (k_order_tiles then
+// lays the list out best-first for the fused kernel).
 __global__ void __launch_bounds__(256) k_filter_batch(const uint4* __restrict__ boxes, const uint4* __restrict__ sboxes,
                                                       long long ntiles, long long nsuper,
                                                       const float* __restrict__ lutf_all, QState* st_all, int B,
@@ -294,7 +314,8 @@ __global__ void __launch_bounds__(256) k_filter_batch(const uint4* __restrict__ 
 {
     extern __shared__ __align__(16) float lutf_s[];  // kFilterQ * kLutF
     __shared__ unsigned char zlo[kFilterQ][16], zhi[kFilterQ][16];
-    __shared__ float thr_s[kFilterQ];
+    __shared__ float thr_s[kFilterQ], sc_s[kFilterQ];
+    __shared__ unsigned hist_s[kFilterQ][kTileBins];
     const int b0 = blockIdx.y * kFilterQ;
     const int nq = min(kFilterQ, B - b0);
     for (int i = threadIdx.x; i < nq * kLutF / 4; i += blockDim.x)
@@ -304,7 +325,11 @@ __global__ void __launch_bounds__(256) k_filter_batch(const uint4* __restrict__ 
         zlo[qq][s] = st_all[b0 + qq].zlo[s];
         zhi[qq][s] = st_all[b0 + qq].zhi[s];
     }
-    if (threadIdx.x < nq) thr_s[threadIdx.x] = slack_up(ld_bsf_eff(st_all + b0 + threadIdx.x, epoch));
+    if (threadIdx.x < nq) {
+        thr_s[threadIdx.x] = slack_up(ld_bsf_eff(st_all + b0 + threadIdx.x, epoch));
+        sc_s[threadIdx.x] = tile_bin_scale(st_all + b0 + threadIdx.x);
+    }
+    if (threadIdx.x < kFilterQ * kTileBins) hist_s[threadIdx.x / kTileBins][threadIdx.x % kTileBins] = 0u;
     __syncthreads();
     const int lane = threadIdx.x & 31, r = lane & 15, h = lane >> 4;
     const int wpb = blockDim.x >> 5;
@@ -338,30 +363,69 @@ __global__ void __launch_bounds__(256) k_filter_batch(const uint4* __restrict__ 
                     lb = box_lb(mn, mx, T, zlo[qq], zhi[qq], r);
                     keep = lb <= thr;
                 }
-                // best-first in two bins: tiles with bound <= thr / 2 fill the list from the
-                // front, the others from the back; the fused kernel hands out the front first
-                const bool near = lb <= 0.5f * thr;
-                const unsigned mf = __ballot_sync(0xffffffffu, keep && near);
-                const unsigned mb = __ballot_sync(0xffffffffu, keep && !near);
-                if (mf | mb) {
-                    unsigned basef = 0, baseb = 0;
-                    if (lane == 0) {
-                        if (mf) basef = atomicAdd(&st->tile_count, (unsigned)__popc(mf));
-                        if (mb) baseb = atomicAdd(&st->tile_back, (unsigned)__popc(mb));
-                    }
-                    basef = __shfl_sync(0xffffffffu, basef, 0);
-                    baseb = __shfl_sync(0xffffffffu, baseb, 0);
+                // kept tiles are appended (tile, bound) to the query's staging list; k_order_tiles
+                // then lays them out best-first
+                const unsigned mk = __ballot_sync(0xffffffffu, keep);
+                if (mk) {
+                    unsigned base = 0;
+                    if (lane == 0) base = atomicAdd(&st->tile_count, (unsigned)__popc(mk));
+                    base = __shfl_sync(0xffffffffu, base, 0);
                     uint2* tl = tlist_all + (size_t)(b0 + qq) * ntiles;
-                    MESSI_CHECK(!(keep && near) || basef + __popc(mf & ((1u << lane) - 1)) + baseb < (unsigned)ntiles);
-                    MESSI_CHECK(!(keep && !near) || baseb + __popc(mb & ((1u << lane) - 1)) + basef < (unsigned)ntiles);
-                    if (keep && near)
-                        tl[basef + __popc(mf & ((1u << lane) - 1))] = make_uint2((unsigned)t, __float_as_uint(lb));
-                    if (keep && !near)
-                        tl[ntiles - 1 - (baseb + __popc(mb & ((1u << lane) - 1)))] =
-                            make_uint2((unsigned)t, __float_as_uint(lb));
+                    MESSI_CHECK(!keep || base + __popc(mk & ((1u << lane) - 1)) < (unsigned)ntiles);
+                    if (keep) {
+                        tl[base + __popc(mk & ((1u << lane) - 1))] = make_uint2((unsigned)t, __float_as_uint(lb));
+                        atomicAdd(&hist_s[qq][tile_bin(lb, sc_s[qq])], 1u);
+                    }
                 }
             }
         }
+    }
+    __syncthreads();
+    if (threadIdx.x < nq * kTileBins) {
+        const unsigned c = hist_s[threadIdx.x / kTileBins][threadIdx.x % kTileBins];
+        if (c) atomicAdd(&st_all[b0 + threadIdx.x / kTileBins].tile_hist[threadIdx.x % kTileBins], c);
+    }
+}
+
+// Best-first layout of a query's listed tiles (one CTA per query): a counting sort of the
+// staging list by bin (tile_bin; bin sizes from the filter's histogram): bin 0, bin 1, ...
+// (order inside a bin arbitrary), each entry (tile | j << 28, lb).  fl(lb sc) is monotone in
+// lb, so every tile of a later bin has a larger bound than any tile of an earlier one: once
+// the best-so-far drops below tile_bin_floor(j) for the bin j of a claimed tile, every tile
+// from there on is box-pruned and the fused kernel voids the query's remaining claims.
+// Scatter: lanes with the same bin take consecutive slots with one shared-memory atomic
+// (__match_any_sync).  Tiles are < 2^28 (sorted positions are 32-bit: ntiles < 2^23).
+__global__ void __launch_bounds__(1024) k_order_tiles(const uint2* __restrict__ stage_all, QState* st_all,
+                                                      long long ntiles, uint2* __restrict__ tlist_all)
+{
+    __shared__ unsigned cur[kTileBins];
+    const int b = blockIdx.x;
+    QState* st = st_all + b;
+    const unsigned count = st->tile_count;
+    const float sc = tile_bin_scale(st);
+    const uint2* in = stage_all + (size_t)b * ntiles;
+    uint2* out = tlist_all + (size_t)b * ntiles;
+    if (threadIdx.x == 0) {
+        unsigned acc = 0;
+        for (int j = 0; j < kTileBins; ++j) {
+            cur[j] = acc;
+            acc += st->tile_hist[j];
+        }
+        MESSI_CHECK(acc == count);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    for (unsigned i0 = threadIdx.x & ~31u; i0 < count; i0 += blockDim.x) {
+        const unsigned i = i0 + lane;
+        const bool v = i < count;
+        const uint2 e = v ? in[i] : make_uint2(0u, 0u);
+        const int j = v ? tile_bin(__uint_as_float(e.y), sc) : kTileBins;
+        const unsigned peers = __match_any_sync(0xffffffffu, j);
+        const int leader = __ffs(peers) - 1;
+        unsigned base = 0;
+        if (v && lane == leader) base = atomicAdd(&cur[j], (unsigned)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (v) out[base + __popc(peers & ((1u << lane) - 1))] = make_uint2(e.x | ((unsigned)j << 28), e.y);
     }
 }
 
@@ -785,7 +849,7 @@ struct FusedCtx {
     QState* st;
     KnnState* knn;
     PeerSet ps;
-    Q8Query qq;
+    const Q8Query* qq;  // the current query's, in shared memory (registers are the occupancy limit)
     int n, b, k;
     long long npad;  // sorted positions (checked build)
 };
@@ -794,7 +858,7 @@ template <bool LINKED, bool KNN>
 __device__ __forceinline__ void refine_round(const FusedCtx& cx, unsigned cp, int count, float& thr,
                                              WarpCounts& wc, int lane)
 {
-    const unsigned keep = q8i_bound_pass(count, cp, cx.rows8, cx.meta8, cx.n, cx.qc_s, cx.qq, thr, lane);
+    const unsigned keep = q8i_bound_pass(count, cp, cx.rows8, cx.meta8, cx.n, cx.qc_s, *cx.qq, thr, lane);
     wc.add(3, __popc(keep), lane);
     if (keep) thr = fminf(thr, slack_up(exact_pass<LINKED, KNN>(keep, cp, cx.perm, cx.rows, cx.n, cx.q_p, cx.st,
                                                                    cx.ps, cx.b, cx.knn, cx.k, lane)));
@@ -894,15 +958,17 @@ __global__ void __launch_bounds__(32 * kFusedWarps, MESSI_FUSED_MINB) k_scan_ref
     unsigned* wcnt = wcnt_all + warp;
     unsigned* wcs = wcnt_all + kFusedWarps + 4 * warp;  // the warp's per-query counters
     __shared__ int s_has;
+    __shared__ float s_binfloor[kTileBins];
+    __shared__ Q8Query s_qq;
     FusedCtx cx;
     cx.sym8 = sym8; cx.rows8 = rows8; cx.meta8 = meta8; cx.perm = perm; cx.rows = rows; cx.q_p = q_p;
     cx.qc_s = reinterpret_cast<const uint4*>(qc_w); cx.lbase = reinterpret_cast<const char*>(lut_s);
-    cx.knn = knn_arg; cx.ps = ps; cx.n = n; cx.k = k_arg; cx.npad = ntiles * MESSI_TILE_ROWS;
+    cx.knn = knn_arg; cx.ps = ps; cx.n = n; cx.k = k_arg; cx.npad = ntiles * MESSI_TILE_ROWS; cx.qq = &s_qq;
     int b = (int)(blockIdx.x % (unsigned)B);
     for (int visited = 0; visited < B; ++visited, b = (b + 1 == B ? 0 : b + 1)) {
         QState* st = st_all + b;
-        const unsigned c0 = *(volatile unsigned*)&st->tile_count;   // front bin
-        const unsigned count = c0 + *(volatile unsigned*)&st->tile_back;
+        // listed tiles, best-first (k_order_tiles)
+        const unsigned count = *(volatile unsigned*)&st->tile_count;
         if (threadIdx.x == 0) s_has = *(volatile unsigned*)&st->next_tile * 2u < count;
         __syncthreads();
         const bool has = s_has;
@@ -915,16 +981,18 @@ __global__ void __launch_bounds__(32 * kFusedWarps, MESSI_FUSED_MINB) k_scan_ref
             for (int i = threadIdx.x; i < n; i += blockDim.x) q_p[i + 4 * (i >> 5)] = q[i];
             const unsigned* qc = qc_all + (size_t)b * (n / 4);
             for (int i = threadIdx.x; i < n / 4; i += blockDim.x) qc_w[i] = qc[i];
+            if (threadIdx.x < kTileBins) s_binfloor[threadIdx.x] = tile_bin_floor(threadIdx.x, tile_bin_scale(st));
         }
         cx.st = st;
         cx.b = b;
-        cx.qq.sq = (double)st->q8s;
-        cx.qq.e = st->q8e;
-        cx.qq.s2ss = st->q8s2ss;
+        if (threadIdx.x == 0) {
+            s_qq.sq = (double)st->q8s;
+            s_qq.e = st->q8e;
+            s_qq.s2ss = st->q8s2ss;
+        }
         __syncthreads();
         const uint2* tl = tlist_all + (size_t)b * ntiles;
-        // list position of claim k: the front bin, then the back bin from its far end
-        auto at = [&](unsigned kk) { return tl[kk < c0 ? kk : (unsigned)ntiles - 1u - (kk - c0)]; };
+        auto at = [&](unsigned kk) { return tl[kk]; };
         WarpCounts wc{wcs};
         if (lane == 0) wcs[0] = wcs[1] = wcs[2] = wcs[3] = 0u;
         unsigned ncb = 0;        // fine survivors pending in cbuf (warp-uniform)
@@ -968,15 +1036,21 @@ __global__ void __launch_bounds__(32 * kFusedWarps, MESSI_FUSED_MINB) k_scan_ref
                 if (u == 1 && lane == 0) {  // pair i + 1's tiles into L2, unless already box-pruned
                     thr_n = slack_up(thr_n);
                     if (__uint_as_float(ne0.y) <= thr_n)
-                        prefetch_l2_bulk(tiles + (long long)ne0.x * (MESSI_TILE_BYTES / 16), MESSI_TILE_BYTES);
+                        prefetch_l2_bulk(tiles + (long long)(ne0.x & kTileMask) * (MESSI_TILE_BYTES / 16), MESSI_TILE_BYTES);
                     if (__uint_as_float(ne1.y) <= thr_n)
-                        prefetch_l2_bulk(tiles + (long long)ne1.x * (MESSI_TILE_BYTES / 16), MESSI_TILE_BYTES);
+                        prefetch_l2_bulk(tiles + (long long)(ne1.x & kTileMask) * (MESSI_TILE_BYTES / 16), MESSI_TILE_BYTES);
                 }
                 const uint2 te = u == 0 ? te0 : te1;
-                MESSI_CHECK(kc + u >= count || te.x < (unsigned)ntiles);
-                if (kc + u >= count || __uint_as_float(te.y) > thr) continue;  // box pruned (warp-uniform)
+                MESSI_CHECK(kc + u >= count || (te.x & kTileMask) < (unsigned)ntiles);
+                if (kc + u >= count) continue;
+                if (__uint_as_float(te.y) > thr) {  // box pruned (warp-uniform)
+                    // every bound of this tile's bin above thr too, so every later bin's: the
+                    // query's remaining claims are void
+                    if (lane == 0 && s_binfloor[te.x >> 28] > thr) atomicMax(&st->next_tile, kClaimsDone);
+                    continue;
+                }
                 wc.add(0, 1u, lane);
-                const long long tile = te.x;
+                const long long tile = te.x & kTileMask;
                 unsigned short* surv = survb + cur * MESSI_TILE_ROWS;
                 const int m = scan_tile_coarse(tiles, tile, cx.lbase, thr, N, surv, wcnt, lane);
                 wc.add(1, (unsigned)m, lane);
