@@ -788,7 +788,7 @@ static messi_status launch_ed_group(messi_index* idx, const messi_index::BatchSe
                                                               idx->ntiles, nsuper, bs.lutf, bs.bst, B, bs.tstage,
                                                               peers.epoch);
         LAUNCHED(idx);
-        k_order_tiles<<<B, 1024, 0, st>>>(bs.tstage, bs.bst, idx->ntiles, bs.btlist);
+        k_order_tiles<<<dim3(kOrderCtas, B), 256, 0, st>>>(bs.tstage, bs.bst, idx->ntiles, bs.btlist);
         LAUNCHED(idx);
     }
     {

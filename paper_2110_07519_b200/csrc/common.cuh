@@ -56,6 +56,7 @@ struct QState {
     unsigned tiles_done;    // batch ED: listed tiles finished (the warp finishing the last finalises)
     unsigned lock;          // batch ED: guards best_d / best_id
     unsigned tile_hist[16]; // batch ED: listed tiles per best-first bin (k_filter_batch -> k_order_tiles)
+    unsigned tile_cur[16];  // batch ED: k_order_tiles' per-bin fill cursors
     unsigned long long dtw_cells;  // DTW band cells evaluated in fp32 (refine)
     unsigned long long gbsf; // batch ED: the epoch-tagged best-so-far of all shards (PeerSet)
     double best_d;          // batch ED: lexicographic min (d64, id) over the fp64 re-ranked rows
@@ -123,7 +124,7 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->next_tile = 0;
     st->coarse_count = 0;
     st->tiles_done = 0;
-    for (int j = 0; j < 16; ++j) st->tile_hist[j] = 0;
+    for (int j = 0; j < 16; ++j) st->tile_hist[j] = st->tile_cur[j] = 0;
     st->lock = 0;
     st->best_d = (double)INFINITY;
     st->best_id = -1;
@@ -158,6 +159,19 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
             : "=r"(ok)
             : "r"(a), "r"(parity)
             : "memory");
+    }
+}
+
+// Bulk copy (TMA, non-tensor) of `bytes` (a multiple of 16, 16-byte aligned ends) from global
+// to shared memory, completing on mbarrier b, in chunks of at most 32 KB; one thread issues.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b)
+{
+    for (unsigned off = 0; off < bytes; off += 32768u) {
+        const unsigned len = min(32768u, bytes - off);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(static_cast<char*>(dst) + off)),
+                     "l"(static_cast<const char*>(src) + off), "r"(len), "r"(smem_u32(b))
+                     : "memory");
     }
 }
 

@@ -316,10 +316,15 @@ __global__ void __launch_bounds__(256) k_filter_batch(const uint4* __restrict__ 
     __shared__ unsigned char zlo[kFilterQ][16], zhi[kFilterQ][16];
     __shared__ float thr_s[kFilterQ], sc_s[kFilterQ];
     __shared__ unsigned hist_s[kFilterQ][kTileBins];
+    __shared__ __align__(8) unsigned long long tab_bar;
     const int b0 = blockIdx.y * kFilterQ;
     const int nq = min(kFilterQ, B - b0);
-    for (int i = threadIdx.x; i < nq * kLutF / 4; i += blockDim.x)
-        reinterpret_cast<float4*>(lutf_s)[i] = reinterpret_cast<const float4*>(lutf_all + (size_t)b0 * kLutF)[i];
+    if (threadIdx.x == 0) {  // the queries' tables: one bulk copy, overlapped with the set-up below
+        mbar_init(&tab_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(&tab_bar, (unsigned)(nq * kLutF * 4));
+        bulk_g2s(lutf_s, lutf_all + (size_t)b0 * kLutF, (unsigned)(nq * kLutF * 4), &tab_bar);
+    }
     if (threadIdx.x < nq * 16) {
         const int qq = threadIdx.x >> 4, s = threadIdx.x & 15;
         zlo[qq][s] = st_all[b0 + qq].zlo[s];
@@ -331,6 +336,7 @@ __global__ void __launch_bounds__(256) k_filter_batch(const uint4* __restrict__ 
     }
     if (threadIdx.x < kFilterQ * kTileBins) hist_s[threadIdx.x / kTileBins][threadIdx.x % kTileBins] = 0u;
     __syncthreads();
+    mbar_wait(&tab_bar, 0);
     const int lane = threadIdx.x & 31, r = lane & 15, h = lane >> 4;
     const int wpb = blockDim.x >> 5;
     for (long long s0 = ((long long)blockIdx.x * wpb + (threadIdx.x >> 5)) * 32; s0 < nsuper;
@@ -387,37 +393,50 @@ __global__ void __launch_bounds__(256) k_filter_batch(const uint4* __restrict__ 
     }
 }
 
-// Best-first layout of a query's listed tiles (one CTA per query): a counting sort of the
-// staging list by bin (tile_bin; bin sizes from the filter's histogram): bin 0, bin 1, ...
-// (order inside a bin arbitrary), each entry (tile | j << 28, lb).  fl(lb sc) is monotone in
-// lb, so every tile of a later bin has a larger bound than any tile of an earlier one: once
-// the best-so-far drops below tile_bin_floor(j) for the bin j of a claimed tile, every tile
-// from there on is box-pruned and the fused kernel voids the query's remaining claims.
-// Scatter: lanes with the same bin take consecutive slots with one shared-memory atomic
-// (__match_any_sync).  Tiles are < 2^28 (sorted positions are 32-bit: ntiles < 2^23).
-__global__ void __launch_bounds__(1024) k_order_tiles(const uint2* __restrict__ stage_all, QState* st_all,
-                                                      long long ntiles, uint2* __restrict__ tlist_all)
+// Best-first layout of a query's listed tiles (kOrderCtas CTAs per query, each a contiguous
+// slice of the staging list): a counting sort by bin (tile_bin; bin sizes from the filter's
+// histogram): bin 0, bin 1, ... (order inside a bin arbitrary), each entry (tile | j << 28,
+// lb).  fl(lb sc) is monotone in lb, so every tile of a later bin has a larger bound than any
+// tile of an earlier one: once the best-so-far drops below tile_bin_floor(j) for the bin j of
+// a claimed tile, every tile from there on is box-pruned and the fused kernel voids the
+// query's remaining claims.  A CTA counts its slice per bin (shared memory), reserves one
+// range per bin in the query's list (global cursor), then scatters its slice; lanes of one
+// warp with the same bin take consecutive slots (__match_any_sync).  Tiles are < 2^28
+// (sorted positions are 32-bit: ntiles < 2^23).
+constexpr int kOrderCtas = 8;
+__global__ void __launch_bounds__(256) k_order_tiles(const uint2* __restrict__ stage_all, QState* st_all,
+                                                     long long ntiles, uint2* __restrict__ tlist_all)
 {
-    __shared__ unsigned cur[kTileBins];
-    const int b = blockIdx.x;
+    __shared__ unsigned cnt[kTileBins], cur[kTileBins];
+    const int b = blockIdx.y;
     QState* st = st_all + b;
     const unsigned count = st->tile_count;
+    const unsigned per = (count + kOrderCtas - 1) / kOrderCtas;
+    const unsigned lo = min(count, blockIdx.x * per), hi = min(count, lo + per);
+    if (lo >= hi) return;
     const float sc = tile_bin_scale(st);
     const uint2* in = stage_all + (size_t)b * ntiles;
     uint2* out = tlist_all + (size_t)b * ntiles;
-    if (threadIdx.x == 0) {
-        unsigned acc = 0;
-        for (int j = 0; j < kTileBins; ++j) {
-            cur[j] = acc;
-            acc += st->tile_hist[j];
-        }
-        MESSI_CHECK(acc == count);
-    }
+    if (threadIdx.x < kTileBins) cnt[threadIdx.x] = 0u;
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    for (unsigned i0 = threadIdx.x & ~31u; i0 < count; i0 += blockDim.x) {
+    for (unsigned i0 = lo + (threadIdx.x & ~31u); i0 < hi; i0 += blockDim.x) {
         const unsigned i = i0 + lane;
-        const bool v = i < count;
+        const int j = i < hi ? tile_bin(__uint_as_float(in[i].y), sc) : kTileBins;
+        const unsigned peers = __match_any_sync(0xffffffffu, j);
+        if (j < kTileBins && lane == __ffs(peers) - 1) atomicAdd(&cnt[j], (unsigned)__popc(peers));
+    }
+    __syncthreads();
+    if (threadIdx.x < kTileBins) {
+        const int j = threadIdx.x;
+        unsigned start = 0;
+        for (int jj = 0; jj < j; ++jj) start += st->tile_hist[jj];
+        cur[j] = cnt[j] ? start + atomicAdd(&st->tile_cur[j], cnt[j]) : 0u;
+    }
+    __syncthreads();
+    for (unsigned i0 = lo + (threadIdx.x & ~31u); i0 < hi; i0 += blockDim.x) {
+        const unsigned i = i0 + lane;
+        const bool v = i < hi;
         const uint2 e = v ? in[i] : make_uint2(0u, 0u);
         const int j = v ? tile_bin(__uint_as_float(e.y), sc) : kTileBins;
         const unsigned peers = __match_any_sync(0xffffffffu, j);
@@ -425,6 +444,7 @@ __global__ void __launch_bounds__(1024) k_order_tiles(const uint2* __restrict__ 
         unsigned base = 0;
         if (v && lane == leader) base = atomicAdd(&cur[j], (unsigned)__popc(peers));
         base = __shfl_sync(0xffffffffu, base, leader);
+        MESSI_CHECK(!v || base + __popc(peers & ((1u << lane) - 1)) < count);
         if (v) out[base + __popc(peers & ((1u << lane) - 1))] = make_uint2(e.x | ((unsigned)j << 28), e.y);
     }
 }

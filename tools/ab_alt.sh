@@ -9,7 +9,7 @@ import json, sys
 try:
     d = json.loads(open("gpurun_out/ab.log").read().strip().splitlines()[-1])
     print("AB", sys.argv[1], "rep", sys.argv[2], "value %.0f" % d["value"], "mean %.0f" % d["repeats"]["mean"],
-          "frac %.4f" % d["roofline"]["frac"], "scan_ms %.4f" % d["kernel_ms_per_step"]["scan"],
+          "frac %.4f" % d["roofline"]["frac"], "scan_ms %.4f" % d["kernel_ms_per_step"]["scan"], "pre_ms %.4f" % d["kernel_ms_per_step"]["seed"], "ms/step %.4f" % d["ms_per_step"],
           "traffic", d["roofline"].get("traffic"), "clk", d["clocks"]["sm_mhz"])
 except Exception as e:
     print("AB", sys.argv[1], "FAILED", e); print(open("gpurun_out/ab.log").read()[-2000:])
