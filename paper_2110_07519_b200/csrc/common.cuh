@@ -52,11 +52,15 @@ struct QState {
     unsigned exact;         // ED: fp32 distances over the raw rows (quantised bound passed)
     unsigned tiles_scanned; // batch ED: tiles whose box bound still passed the CURRENT BSF
     unsigned coarse_count;  // series whose cardinality-16 bound passed (fine bound evaluated)
-    unsigned next_tile;     // batch ED: next pair of listed tiles to hand out
     unsigned tiles_done;    // batch ED: listed tiles finished (the warp finishing the last finalises)
     unsigned lock;          // batch ED: guards best_d / best_id
     unsigned tile_hist[16]; // batch ED: listed tiles per best-first bin (k_filter_batch -> k_order_tiles)
     unsigned tile_cur[16];  // batch ED: k_order_tiles' per-bin fill cursors
+    // batch ED: next pair of listed tiles to hand out -- the fused kernel's hot claim counter,
+    // alone on its 128-byte line: loads of the fields above (the BSF every warp reads once per
+    // pair) would otherwise queue behind the claims at the L2 slice that owns the line
+    alignas(128) unsigned next_tile;
+    unsigned next_tile_pad[31];
     unsigned long long dtw_cells;  // DTW band cells evaluated in fp32 (refine)
     unsigned long long gbsf; // batch ED: the epoch-tagged best-so-far of all shards (PeerSet)
     double best_d;          // batch ED: lexicographic min (d64, id) over the fp64 re-ranked rows
@@ -276,10 +280,20 @@ __device__ __forceinline__ void bsf_update(QState* st, float d)
 
 // The threshold source of the batched ED path: the local BSF, lowered by the shards' shared
 // one when it carries this launch's epoch (epoch 0 = unlinked: gbsf is not read).
+// (GPU-scope relaxed load: a stale value is a valid, larger threshold; a volatile load
+// compiles to a system-scope strong load, which was measured to wait behind the warp's
+// in-flight claim atomic.)
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p)
+{
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 template <bool LINKED>
 __device__ __forceinline__ float ld_bsf_l(const QState* st, unsigned epoch)
 {
-    if (!LINKED) return __uint_as_float(*(volatile const unsigned*)&st->bsf_bits);
+    if (!LINKED) return __uint_as_float(ld_relaxed_gpu(&st->bsf_bits));
     const float loc = __uint_as_float(*(volatile const unsigned*)&st->bsf_bits);
     const unsigned long long g = *(volatile const unsigned long long*)&st->gbsf;
     if ((unsigned)(g >> 32) == epoch) return fminf(loc, __uint_as_float(0xffffffffu - (unsigned)g));
