@@ -704,7 +704,7 @@ __host__ __device__ inline size_t fused_qpad(int n) { return (size_t)(n + 4 * ((
 __host__ __device__ inline size_t fused_smem(int n)
 {
     return (size_t)kLutX * 4 + fused_qpad(n) * 4 + (size_t)n +
-           (size_t)kFusedWarps * (2 * MESSI_TILE_ROWS * 2 + kCandBuf * 4 + 4 + 16);
+           (size_t)kFusedWarps * (MESSI_TILE_ROWS * 2 + kCandBuf * 4 + 4 + 16);
 }
 
 // Writes query b's result and stats (finish_query's layout) from its state.
@@ -970,10 +970,10 @@ __global__ void __launch_bounds__(32 * kFusedWarps, MESSI_FUSED_MINB) k_scan_ref
     float* q_p = lut_s + kLutX;
     unsigned* qc_w = reinterpret_cast<unsigned*>(q_p + fused_qpad(n));
     unsigned short* surv_all = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(qc_w) + n);
-    unsigned* cbuf_all = reinterpret_cast<unsigned*>(surv_all + kFusedWarps * 2 * MESSI_TILE_ROWS);
+    unsigned* cbuf_all = reinterpret_cast<unsigned*>(surv_all + kFusedWarps * MESSI_TILE_ROWS);
     unsigned* wcnt_all = cbuf_all + kFusedWarps * kCandBuf;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned short* survb = surv_all + warp * 2 * MESSI_TILE_ROWS;  // two lists: current / previous tile
+    unsigned short* surv = surv_all + warp * MESSI_TILE_ROWS;  // coarse survivors of the previous tile
     unsigned* cbuf = cbuf_all + warp * kCandBuf;
     unsigned* wcnt = wcnt_all + warp;
     unsigned* wcs = wcnt_all + kFusedWarps + 4 * warp;  // the warp's per-query counters
@@ -1016,7 +1016,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, MESSI_FUSED_MINB) k_scan_ref
         WarpCounts wc{wcs};
         if (lane == 0) wcs[0] = wcs[1] = wcs[2] = wcs[3] = 0u;
         unsigned ncb = 0;        // fine survivors pending in cbuf (warp-uniform)
-        int pm = 0, cur = 0;     // previous tile's coarse survivors (list survb[cur ^ 1])
+        int pm = 0;              // previous tile's coarse survivors (list surv)
         long long ptile = 0;
         uint4 pw = make_uint4(0, 0, 0, 0);
         unsigned ppos = 0;
@@ -1071,18 +1071,20 @@ __global__ void __launch_bounds__(32 * kFusedWarps, MESSI_FUSED_MINB) k_scan_ref
                 }
                 wc.add(0, 1u, lane);
                 const long long tile = te.x & kTileMask;
-                unsigned short* surv = survb + cur * MESSI_TILE_ROWS;
-                const int m = scan_tile_coarse(tiles, tile, cx.lbase, thr, N, surv, wcnt, lane);
-                wc.add(1, (unsigned)m, lane);
+                // coarse pass of this tile (its survivors stay a per-lane mask until the previous
+                // tile's fine pass has released the warp's list)
+                float acc[16];
+                coarse_acc(tiles, tile, cx.lbase, lane, acc);
+                const unsigned cmask = coarse_mask(acc, thr, N, tile, lane);
                 if (pm)
-                    fine_and_refine<LINKED, KNN>(cx, ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, cbuf, ncb,
-                                                 thr, wc, lane);
+                    fine_and_refine<LINKED, KNN>(cx, ptile, pm, surv, pw, ppos, cbuf, ncb, thr, wc, lane);
+                const int m = compact_mask(cmask, surv, wcnt, lane);
+                wc.add(1, (unsigned)m, lane);
                 // preload the 8-bit words of this tile's first 32 coarse survivors
                 ppos = lane < m ? (unsigned)(tile * MESSI_TILE_ROWS + surv[lane]) : 0u;
                 pw = lane < m ? sym8[ppos] : make_uint4(0, 0, 0, 0);
                 pm = m;
                 ptile = tile;
-                cur ^= 1;
             }
             // advance the pipeline
             kc = kn;
@@ -1091,9 +1093,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps, MESSI_FUSED_MINB) k_scan_ref
             te0 = make_uint2(__shfl_sync(0xffffffffu, ne0.x, 0), __shfl_sync(0xffffffffu, ne0.y, 0));
             te1 = make_uint2(__shfl_sync(0xffffffffu, ne1.x, 0), __shfl_sync(0xffffffffu, ne1.y, 0));
         }
-        if (pm)
-            fine_and_refine<LINKED, KNN>(cx, ptile, pm, survb + (cur ^ 1) * MESSI_TILE_ROWS, pw, ppos, cbuf, ncb, thr,
-                                         wc, lane);
+        if (pm) fine_and_refine<LINKED, KNN>(cx, ptile, pm, surv, pw, ppos, cbuf, ncb, thr, wc, lane);
         if (ncb) {  // the query's last fine survivors
             const unsigned cp = (unsigned)lane < ncb ? cbuf[lane] : 0u;
             __syncwarp();

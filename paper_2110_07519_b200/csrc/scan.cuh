@@ -286,17 +286,10 @@ constexpr int kScanWarps = 8;
 constexpr int kScanTab = MESSI_CARD * 64;                 // floats per scan table
 constexpr size_t kScanLutBytes = (size_t)kScanTab * sizeof(float);
 
-// Coarse bounds of the 512 series of tile `tile`; the series with LB16 <= thr are written to
-// the warp's list surv (tile-local index) in ascending order; returns their number
-// (warp-uniform).
-// Coarse bounds acc[k] of the lane's 16 series 16*lane + k of tile `tile`.
-__device__ __forceinline__ void coarse_acc(const uint4* __restrict__ tiles, long long tile, const char* lbase, int lane,
-                                           float acc[16])
+// Coarse bounds acc[k] of the lane's 16 series 16*lane + k of a tile from its 8 rows
+// (data[t] = tile row t, 16 bytes per lane).
+__device__ __forceinline__ void coarse_acc_data(const uint4 (&data)[8], const char* lbase, int lane, float acc[16])
 {
-    const uint4* tp = tiles + tile * (MESSI_TILE_BYTES / 16) + lane;
-    uint4 data[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) data[t] = __ldcs(tp + t * 32);
 #pragma unroll
     for (int k = 0; k < 16; ++k) acc[k] = 0.0f;
     const int bl = lane & 7, cp = lane >> 3;
@@ -320,20 +313,36 @@ __device__ __forceinline__ void coarse_acc(const uint4* __restrict__ tiles, long
     }
 }
 
-__device__ __forceinline__ int scan_tile_coarse(const uint4* __restrict__ tiles, long long tile, const char* lbase,
-                                                float thr, long long N, unsigned short* surv, unsigned* wcnt, int lane)
+// Coarse bounds acc[k] of the lane's 16 series 16*lane + k of tile `tile`.
+__device__ __forceinline__ void coarse_acc(const uint4* __restrict__ tiles, long long tile, const char* lbase, int lane,
+                                           float acc[16])
 {
-    float acc[16];
-    coarse_acc(tiles, tile, lbase, lane, acc);
+    const uint4* tp = tiles + tile * (MESSI_TILE_BYTES / 16) + lane;
+    uint4 data[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) data[t] = __ldcs(tp + t * 32);
+    coarse_acc_data(data, lbase, lane, acc);
+}
+
+// The lane's survivors (bit k: series 16*lane + k has LB16 <= thr and lies inside the
+// collection -- series past the end exist in the last tile only: one 64-bit test per lane).
+__device__ __forceinline__ unsigned coarse_mask(const float acc[16], float thr, long long N, long long tile, int lane)
+{
     unsigned mask = 0;
 #pragma unroll
     for (int k = 0; k < 16; ++k)
         if (acc[k] <= thr) mask |= 1u << k;
-    // series past the end of the collection (the last tile only): one 64-bit test per lane
     const long long left = N - (tile * MESSI_TILE_ROWS + lane * 16);
     if (left < 16) mask &= left > 0 ? (1u << left) - 1u : 0u;
-    // compaction: each lane reserves its survivors' slots with one shared-memory atomic on the
-    // warp's counter (the list order across lanes is free: every later pass is order-free)
+    return mask;
+}
+
+// Compaction of the lanes' survivor masks into the warp's list surv (tile-local indices):
+// each lane reserves its survivors' slots with one shared-memory atomic on the warp's counter
+// (the list order across lanes is free: every later pass is order-free); returns their
+// number (warp-uniform).
+__device__ __forceinline__ int compact_mask(unsigned mask, unsigned short* surv, unsigned* wcnt, int lane)
+{
     const int cnt = __popc(mask);
     if (lane == 0) *wcnt = 0u;
     __syncwarp();
@@ -348,6 +357,16 @@ __device__ __forceinline__ int scan_tile_coarse(const uint4* __restrict__ tiles,
     }
     __syncwarp();
     return m;
+}
+
+// Coarse bounds of the 512 series of tile `tile`; the series with LB16 <= thr are written to
+// the warp's list surv (tile-local index); returns their number (warp-uniform).
+__device__ __forceinline__ int scan_tile_coarse(const uint4* __restrict__ tiles, long long tile, const char* lbase,
+                                                float thr, long long N, unsigned short* surv, unsigned* wcnt, int lane)
+{
+    float acc[16];
+    coarse_acc(tiles, tile, lbase, lane, acc);
+    return compact_mask(coarse_mask(acc, thr, N, tile, lane), surv, wcnt, lane);
 }
 
 // Fine bound of one series from its 8-bit word (16 symbols, segment s in byte s); the lane
