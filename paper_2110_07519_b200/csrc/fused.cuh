@@ -307,7 +307,7 @@ __global__ void k_superbox(const uint4* __restrict__ boxes, long long ntiles, ui
 // the tiles of every super-tile that passes are tested 16 at a time (half-warps), and the
 // kept tiles are appended as (tile, bound) to the query's staging list (k_order_tiles then
 // lays the list out best-first for the fused kernel).
-__global__ void __launch_bounds__(256) k_filter_batch(const uint4* __restrict__ boxes, const uint4* __restrict__ sboxes,
+__global__ void __launch_bounds__(256, 3) k_filter_batch(const uint4* __restrict__ boxes, const uint4* __restrict__ sboxes,
                                                       long long ntiles, long long nsuper,
                                                       const float* __restrict__ lutf_all, QState* st_all, int B,
                                                       uint2* __restrict__ tlist_all, unsigned epoch)
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(256) k_filter_batch(const uint4* __restrict__ 
 // range per bin in the query's list (global cursor), then scatters its slice; lanes of one
 // warp with the same bin take consecutive slots (__match_any_sync).  Tiles are < 2^28
 // (sorted positions are 32-bit: ntiles < 2^23).
-constexpr int kOrderCtas = 8;
+constexpr int kOrderCtas = 64;
 __global__ void __launch_bounds__(256) k_order_tiles(const uint2* __restrict__ stage_all, QState* st_all,
                                                      long long ntiles, uint2* __restrict__ tlist_all)
 {
