@@ -374,6 +374,7 @@ def run_arm(cfg, args, world, rank, dev, stream, time_steps, warmup, repeats=1):
             n_, r_ = cfg["n"], min(reach, cfg["n"] - 1)
             cells = ids.numel() * (n_ * (2 * r_ + 1) - r_ * (r_ + 1))
             steady = {"candidates": ids.numel(), "cells": cells, "ms": sms}
+    build_phases = {**build_phases, "renv": M.messi_build_times(idx.handle)["renv"]}  # DTW: after its first query
     out = dict(ms=ms, rep_ms=rep_ms, build_ms=build_ms, build_phases=build_phases, launches=launches, prof=prof,
                prof_ms=prof_ms, stats=st, clocks=clk_all[0].summary(), e2e_ms=e2e_ms, knn_ms=knn, nq=nq,
                N_local=X.shape[0], n=cfg["n"], reach=reach, h2d=qh.numel() * 4, d2h=rh.numel(), latency_ms=lat,
@@ -501,13 +502,18 @@ def dtw_roofline(run, steps):
     achieved = cells / (ms / 1e3)
     peak = dtw_cell_peak(run["clocks"].get("sm_max_mhz", 1965.0) or 1965.0)
     lbk_ms, _ = run["prof"]["lbk"]
-    # strip refine reaches (r >= 7): the forward filter reads the candidate entry (8 B), the
-    # quantised row (n bytes) and its scale / error (8 B); the reverse bound (stats "exact":
-    # its evaluations) writes and reads a 16 B queue entry, reads the row again and its id
-    # (4 B); every survivor is a 16 B list2 entry.  Register-band reaches: raw rows (4n bytes)
+    # strip refine reaches (r >= 7): the reverse envelope-PAA filter reads every scan candidate's
+    # entry (8 B) and envelope symbols (32 B) and writes its survivors (8 B, stats
+    # "rev_paa_pass"); the forward filter reads those survivors' entries (8 B), quantised rows
+    # (n bytes) and scale / error (8 B); the reverse bound (stats "exact": its evaluations)
+    # writes and reads a 16 B queue entry, reads the row again and its id (4 B); every survivor
+    # is a 16 B list2 entry.  Register-band reaches: raw rows (4n bytes) of every candidate
     n = run["n"]
-    per_cand = n + 16 if (run.get("reach") or 0) >= 7 else 4 * n + 8
-    lbk_bytes = sum(per_cand * s["candidates"] + (n + 36) * s["exact"] + 16 * s["lbk_pass"] for s in st) * steps
+    strip = (run.get("reach") or 0) >= 7
+    renv = strip and not os.environ.get("MESSI_NO_RENV")
+    per_cand = n + 16 if strip else 4 * n + 8
+    lbk_bytes = sum((40 * s["candidates"] + (8 + per_cand) * s["rev_paa_pass"] if renv else per_cand * s["candidates"])
+                    + (n + 36) * s["exact"] + 16 * s["lbk_pass"] for s in st) * steps
     return {"bound": "alu", "kernel": "k_refine_dtw_strip<8,REM> (fp32 banded DTW, one thread per candidate; "
                                       "k_refine_dtw<R> at R = 2, 5)",
             "achieved": achieved, "peak": peak, "unit": "cells/s", "frac": achieved / peak,
@@ -517,8 +523,9 @@ def dtw_roofline(run, steps):
                            "(FMNMX3 + paired FADD2/FFMA2), 148 SMs x 4 SMSP, max SM clock",
             "time": "CUDA events around the refine launches in a serial pass of the same steps (no stage overlap)",
             "steady_state": steady_refine(run),
-            "lbk_filter": {"bound": "hbm", "kernels": "k_lbk_filter_q8b (forward, bulk-copy rows) + k_lbk_rev_q8 "
-                                                      "(reverse over the forward survivors)",
+            "lbk_filter": {"bound": "hbm", "kernels": "k_rev_paa_filter (reverse envelope-PAA bound over the scan's "
+                                                      "candidates) + k_lbk_filter_q8b (forward LB_Keogh, bulk-copy "
+                                                      "rows) + k_lbk_rev_q8 (reverse LB_Keogh over the forward survivors)",
                            "achieved_gbs": lbk_bytes / (lbk_ms / 1e3) / 1e9 if lbk_ms > 0 else None,
                            "frac": lbk_bytes / (lbk_ms / 1e3) / 1e9 / peaks().get("hbm_gbs", 6650.0)
                            if lbk_ms > 0 else None,
@@ -713,7 +720,7 @@ def ours(args):
                   "phases_ms": main["build_phases"],
                   "what": "messi_build per GPU: breakpoints + summarise (PAA, iSAX, key) + CUB key sort + sorted "
                           "layout + quantised rows"},
-        "stats_mean": {k: mean(k) for k in ("lb_computed", "tiles_scanned", "candidates", "lbk_pass", "refined",
+        "stats_mean": {k: mean(k) for k in ("lb_computed", "tiles_scanned", "candidates", "rev_paa_pass", "lbk_pass", "refined",
                                              "abandoned", "near_best", "dtw_cells", "exact", "tiles_listed", "coarse",
                                              "seed_d2", "bsf_d2")},
     }
@@ -754,11 +761,12 @@ def ours(args):
                        "steps": k4, "ms_per_step": dms / k4,
                        "kernel_ms_per_step_serial": {k: v[0] / k4 for k, v in d["prof"].items()},
                        "serial_pass_ms_per_step": d["prof_ms"] / k4,
-                       "stats_mean": {**{k: dm(k) for k in ("lb_computed", "tiles_scanned", "candidates", "lbk_pass",
-                                                            "refined", "abandoned", "near_best", "dtw_cells",
-                                                            "coarse", "seed_d2", "bsf_d2")},
+                       "stats_mean": {**{k: dm(k) for k in ("lb_computed", "tiles_scanned", "candidates",
+                                                            "rev_paa_pass", "lbk_pass", "refined", "abandoned",
+                                                            "near_best", "dtw_cells", "coarse", "seed_d2", "bsf_d2")},
                                       "reverse_evaluated": dm("exact")},
                        "gpu_launches": d["launches"], "roofline": dtw_roofline(d, k4),
+                       "renv_build_ms": d["build_phases"].get("renv"),
                        "stats_dist": dist_of(dst)}
         if d.get("latency_ms"):
             lt = sorted(d["latency_ms"])

@@ -90,6 +90,9 @@ typedef struct {
     int64_t coarse;       /* series whose cardinality-16 bound passed (their 8-bit bound evaluated) */
     double seed_d2;       /* BSF0: squared distance found by the approximate search */
     double bsf_d2;        /* final fp32 best-so-far (squared) before the exact re-rank */
+    int64_t rev_paa_pass; /* DTW at strip reaches: candidates that also passed the reverse envelope-PAA
+                             bound (the rows' envelope-PAA symbols against the query PAA, DESIGN.md
+                             5) -- the series the LB_Keogh filter reads; otherwise = candidates */
 } messi_stats;
 
 /* Build the index over `count` rows of length cfg->length (device pointer, borrowed: the
@@ -194,9 +197,11 @@ int64_t messi_launch_count(const messi_index* idx);
 messi_status messi_profile_enable(messi_index* idx, int32_t enable);
 messi_status messi_profile_read(messi_index* idx, int32_t kind, double* total_ms, int64_t* launches);
 
-/* Device time of the build phases (CUDA events on cfg.stream inside messi_build), ms_out[4]:
+/* Device time of the build phases (CUDA events on cfg.stream inside messi_build), ms_out[5]:
  * 0 breakpoints + summarisation (PAA, symbols, keys: Alg. 3), 1 the CUB key sort,
- * 2 sorted layout (tiles, 8-bit words, boxes, super-boxes), 3 quantised rows. */
+ * 2 sorted layout (tiles, 8-bit words, boxes, super-boxes), 3 quantised rows; 4 the last
+ * reverse-envelope symbol pass of the DTW path (k_renv, per reach, run by the first strip-reach
+ * DTW query of that reach; 0 if none). */
 messi_status messi_build_times(const messi_index* idx, double* ms_out);
 
 /* Scan throughput in isolation: one query's prologue and tile filter, then `reps` scans back
@@ -234,6 +239,12 @@ messi_status messi_debug_order(messi_index* idx, const uint64_t** skey_dev, cons
  * (reach >= 0) -> the envelope-PAA bound from k_seed_dtw's.  Squared, fp32, table
  * entries rounded down and summed rounding down. */
 messi_status messi_debug_lower_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
+/* The reverse envelope-PAA bound (the DTW path's filter between the scan and
+ * LB_Keogh at strip reaches) of every row for `reach` >= 1, lb_dev[N] in row order:
+ * m sum_s max(0, qbar_s - hi(u_s), lo(l_s) - qbar_s)^2 in fp32 rounded down, u_s / l_s the
+ * row's envelope-PAA symbols (k_renv).  Reverse LB_Keogh (P:1392-1405 with the series' roles
+ * swapped) reduced by PAA as P:1411 does for the query envelope: <= DTW(q, x). */
+messi_status messi_debug_rev_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev);
 
 /* Coarse (cardinality-16, the top 4 bits of every symbol) bound of every row against one
  * query with the scan kernel's own arithmetic (coarse_acc, called by scan_tile_coarse):

@@ -71,6 +71,14 @@ def lib():
         L.oracle_lb_keogh2.restype = _c_d
         L.oracle_lb_env_paa2.argtypes = [_f64p, _f64p, _u8p, _c_int, _c_int, _f32p, _c_int]
         L.oracle_lb_env_paa2.restype = _c_d
+        L.oracle_renv_sym.argtypes = [_f32p, _c_int, _c_int, _c_int, _f32p, _c_int, _u8p, _u8p]
+        L.oracle_renv_sym.restype = _c_int
+        L.oracle_renv_sym_rows.argtypes = [_f32p, _c_i64, _c_int, _c_int, _c_int, _f32p, _c_int, _u8p, _u8p]
+        L.oracle_renv_sym_rows.restype = _c_int
+        L.oracle_lb_rev_paa2.argtypes = [_f64p, _u8p, _u8p, _c_int, _c_int, _f32p, _c_int]
+        L.oracle_lb_rev_paa2.restype = _c_d
+        L.oracle_lb_rev_paa2_rows.argtypes = [_f64p, _u8p, _u8p, _c_i64, _c_int, _c_int, _f32p, _c_int, _f64p]
+        L.oracle_lb_rev_paa2_rows.restype = None
         L.oracle_dtw2.argtypes = [_f32p, _f32p, _c_int, _c_int]
         L.oracle_dtw2.restype = _c_d
         vp = ctypes.c_void_p
@@ -182,6 +190,47 @@ def lb_env_paa2(Upaa64, Lpaa64, sym, n: int, card: int = 256, beta32=None) -> fl
     return lib().oracle_lb_env_paa2(np.ascontiguousarray(Upaa64, np.float64),
                                     np.ascontiguousarray(Lpaa64, np.float64), sym, sym.size, n,
                                     _f32(beta32), card)
+
+
+def renv_sym(x, r: int, w: int = 16, card: int = 256, beta32=None):
+    """(usym, lsym): symbols of the per-segment means of x's envelope of reach r (O11b)."""
+    x = _f32(x)
+    if beta32 is None:
+        beta32 = breakpoints(card)[1]
+    u = np.zeros(w, np.uint8)
+    l = np.zeros(w, np.uint8)
+    if lib().oracle_renv_sym(x, x.size, int(r), w, _f32(beta32), card, u, l):
+        raise ValueError("need 0 < w, n % w == 0, 0 <= r <= n")
+    return u, l
+
+
+def renv_sym_rows(data, r: int, w: int = 16, card: int = 256):
+    data = _f32(data)
+    beta32 = breakpoints(card)[1]
+    U = np.zeros((data.shape[0], w), np.uint8)
+    L = np.zeros((data.shape[0], w), np.uint8)
+    if lib().oracle_renv_sym_rows(data, data.shape[0], data.shape[1], int(r), w, _f32(beta32), card, U, L):
+        raise ValueError("need 0 < w, n % w == 0, 0 <= r <= n")
+    return U, L
+
+
+def lb_rev_paa2(qpaa64, usym, lsym, n: int, card: int = 256, beta32=None) -> float:
+    """Reverse envelope-PAA bound (O11b) of one row from its envelope symbols."""
+    usym = np.ascontiguousarray(usym, np.uint8)
+    lsym = np.ascontiguousarray(lsym, np.uint8)
+    if beta32 is None:
+        beta32 = breakpoints(card)[1]
+    return lib().oracle_lb_rev_paa2(np.ascontiguousarray(qpaa64, np.float64), usym, lsym, usym.size, n,
+                                    _f32(beta32), card)
+
+
+def lb_rev_paa2_rows(qpaa64, usym, lsym, n: int, card: int = 256):
+    usym = np.ascontiguousarray(usym, np.uint8)
+    lsym = np.ascontiguousarray(lsym, np.uint8)
+    out = np.zeros(usym.shape[0], np.float64)
+    lib().oracle_lb_rev_paa2_rows(np.ascontiguousarray(qpaa64, np.float64), usym, lsym, usym.shape[0],
+                                  usym.shape[1], n, _f32(breakpoints(card)[1]), card, out)
+    return out
 
 
 def dtw2(q, c, r: int) -> float:

@@ -216,6 +216,73 @@ double oracle_lb_env_paa2(const double* Upaa, const double* Lpaa, const uint8_t*
     return m * sum;
 }
 
+/* O11b.  Reverse envelope-PAA bound (reading R19).  LB_Keogh holds with
+ * the roles of the two series swapped (the query against the envelope of the
+ * candidate), and the PAA reduction of P:1411 applies to that envelope as it does to the
+ * query's.  oracle_renv_sym: the candidate's envelope (O9), the mean of U and of L over
+ * each segment (fp64), and the symbol of the box containing each mean (O4's rule,
+ * #{k : beta32_k <= mean}). */
+int oracle_renv_sym(const float* x, int n, int r, int w, const float* beta32, int card, uint8_t* usym,
+                    uint8_t* lsym)
+{
+    if (w <= 0 || n % w || r < 0 || r > n) return -1;
+    float* U = (float*)malloc(sizeof(float) * (size_t)n);
+    float* L = (float*)malloc(sizeof(float) * (size_t)n);
+    if (!U || !L) { free(U); free(L); return -1; }
+    oracle_envelope(x, n, r, U, L);
+    int m = n / w;
+    for (int s = 0; s < w; ++s) {
+        double su = 0.0, sl = 0.0;
+        for (int j = 0; j < m; ++j) {
+            su = su + (double)U[s * m + j];
+            sl = sl + (double)L[s * m + j];
+        }
+        double ubar = su / (double)m, lbar = sl / (double)m;
+        int cu = 0, cl = 0;
+        for (int k = 0; k < card - 1; ++k) {
+            if ((double)beta32[k] <= ubar) cu = cu + 1;
+            if ((double)beta32[k] <= lbar) cl = cl + 1;
+        }
+        usym[s] = (uint8_t)cu;
+        lsym[s] = (uint8_t)cl;
+    }
+    free(U);
+    free(L);
+    return 0;
+}
+
+int oracle_renv_sym_rows(const float* data, int64_t rows, int n, int r, int w, const float* beta32, int card,
+                         uint8_t* usym, uint8_t* lsym)
+{
+    for (int64_t i = 0; i < rows; ++i)
+        if (oracle_renv_sym(data + i * n, n, r, w, beta32, card, usym + i * w, lsym + i * w)) return -1;
+    return 0;
+}
+
+/* LB^2 = m * sum_s max(0, qpaa_s - hi(usym_s), lo(lsym_s) - qpaa_s)^2: the distance of the
+ * query's segment mean to the box spanning [lo(lsym_s), hi(usym_s)] (O5's boxes), which
+ * contains [Lbar_s, Ubar_s]. */
+double oracle_lb_rev_paa2(const double* qpaa, const uint8_t* usym, const uint8_t* lsym, int w, int n,
+                          const float* beta32, int card)
+{
+    double m = (double)(n / w);
+    double sum = 0.0;
+    for (int s = 0; s < w; ++s) {
+        double hi = box_hi(usym[s], beta32, card), lo = box_lo(lsym[s], beta32);
+        double d = 0.0;                       /* inside */
+        if (qpaa[s] > hi) d = qpaa[s] - hi;   /* query mean above the upper envelope's box */
+        else if (qpaa[s] < lo) d = lo - qpaa[s]; /* below the lower envelope's box */
+        sum = sum + d * d;
+    }
+    return m * sum;
+}
+
+void oracle_lb_rev_paa2_rows(const double* qpaa, const uint8_t* usym, const uint8_t* lsym, int64_t rows, int w,
+                             int n, const float* beta32, int card, double* out)
+{
+    for (int64_t i = 0; i < rows; ++i) out[i] = oracle_lb_rev_paa2(qpaa, usym + i * w, lsym + i * w, w, n, beta32, card);
+}
+
 /* ----------------------------------------------------------------------- DTW --
  * O12.  DTW with a Sakoe-Chiba band of reach r ("reach ... allowed
  * range of warping"; reading R8): D(0,0) = c(0,0); D(i,j) = c(i,j) + min(D(i-1,j-1),

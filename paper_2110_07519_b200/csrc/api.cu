@@ -42,6 +42,7 @@ struct Slot {
     uint2* cand = nullptr;    // scan survivors (sorted position, 8-bit LB)                      [lazy]
     uint4* list2 = nullptr;   // DTW: LB_Keogh survivors (id, LBK, LBK of the first window, 0)  [lazy]
     uint4* rlist = nullptr;   // DTW: forward survivors queued for the reverse bound               [lazy]
+    uint2* cand2 = nullptr;   // DTW: scan survivors passing the reverse envelope-PAA bound         [lazy]
     unsigned* tlist = nullptr;  // tiles surviving the box filter
     NearEntry* near = nullptr;  // near-best (id, d32) of the DTW refine                          [lazy]
     double* rbuf = nullptr;     // DTW resolve: global wavefront scratch for long series         [lazy]
@@ -77,6 +78,11 @@ struct messi_index {
     unsigned long long* skey = nullptr;
     unsigned* perm = nullptr;
     float *beta32 = nullptr, *lo_w = nullptr, *hi_w = nullptr;
+    // DTW: the rows' envelope-PAA symbols for reach renv_reach (k_renv, 32 B per sorted
+    // position), built on the first strip-reach DTW query and rebuilt when the reach changes
+    uint4* renv = nullptr;
+    int renv_reach = -1;
+    float renv_ms = 0.0f;
     // batched ED path (fused.cuh): per-query state, tables and tile lists of a launch group
     // (two sets, alternating between consecutive groups of one call)
     struct BatchSet {
@@ -132,7 +138,7 @@ struct messi_index {
 };
 
 static_assert(sizeof(messi_result) == 32, "messi_result layout");
-static_assert(sizeof(messi_stats) == 104, "messi_stats layout");
+static_assert(sizeof(messi_stats) == kStatsBytes, "messi_stats layout");
 
 enum { K_SEED = 0, K_SCAN = 1, K_REFINE = 2, K_LBK = 3, K_RESOLVE = 4, K_KINDS = 5 };
 
@@ -315,6 +321,8 @@ static messi_status setup_kernels(int device)
     CK(cudaFuncSetAttribute(k_debug_dtw64, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_ed_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes(256)));
     CK(cudaFuncSetAttribute(k_seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_renv, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_rev_paa_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, kRevTabBytes));
     CK(cudaFuncSetAttribute(k_refine_dtw_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_resolve_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_resolve_dtw_knn, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -508,7 +516,7 @@ extern "C" void messi_free(messi_index* idx)
     void* ptrs[] = {idx->tiles, idx->sym8, idx->boxes, idx->sboxes, idx->paa, idx->skey, idx->perm, idx->beta32, idx->lo_w,
                     idx->hi_w,  idx->qbuf,  idx->res1, idx->resk, idx->stats1, idx->rows8, idx->meta8,
                     idx->dbg_inv, idx->dbg_map, idx->dbg_iota, idx->dbg_gbuf, idx->tc.bst, idx->tc.qc, idx->tc.cand,
-                    idx->tc.tcm, idx->slot_st};
+                    idx->tc.tcm, idx->slot_st, idx->renv};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& row : idx->peer_ipc)
@@ -521,7 +529,8 @@ extern "C" void messi_free(messi_index* idx)
             if (p) cudaFree(p);
     }
     for (Slot& sl : idx->slot) {
-        void* sp[] = {sl.lut, sl.tab, sl.U, sl.L, sl.cand, sl.list2, sl.rlist, sl.near, sl.tlist, sl.rbuf, sl.knn, sl.seedd};
+        void* sp[] = {sl.lut, sl.tab, sl.U, sl.L, sl.cand, sl.cand2, sl.list2, sl.rlist, sl.near, sl.tlist, sl.rbuf, sl.knn,
+                      sl.seedd};
         for (void* p : sp)
             if (p) cudaFree(p);
         cudaEvent_t es[] = {sl.ev_seed, sl.ev_scan, sl.ev_lbk, sl.ev_refined, sl.ev_done};
@@ -551,6 +560,7 @@ extern "C" messi_status messi_build_times(const messi_index* idx, double* ms_out
 {
     if (!idx || !ms_out) return fail(MESSI_EINVAL, "NULL argument");
     for (int i = 0; i < 4; ++i) ms_out[i] = idx->build_ms[i];
+    ms_out[4] = idx->renv_ms;
     return MESSI_OK;
 }
 
@@ -880,11 +890,66 @@ static bool rev_fused()
     return v == 1;
 }
 
+// The reverse envelope-PAA filter (k_rev_paa_filter) between the scan and the LB_Keogh
+// filter, at the strip reaches >= 1 (MESSI_NO_RENV=1, experiments: off).
+static bool renv_env_off()
+{
+    static int v = -1;
+    if (v < 0) v = getenv("MESSI_NO_RENV") ? 1 : 0;
+    return v == 1;
+}
+static bool renv_on(const messi_index* idx, int reach)
+{
+    return !renv_env_off() && reach >= 1 && idx->renv && idx->renv_reach == reach;
+}
+
+// The rows' envelope-PAA symbols for `reach` (k_renv over every sorted position, on the
+// caller's stream ahead of the query's scan), built when the reach differs from the last
+// built one; earlier queries (which may read the old symbols) are joined first.
+static messi_status ensure_renv(messi_index* idx, int reach)
+{
+    if (renv_env_off() || reach < 1 || idx->renv_reach == reach) return MESSI_OK;
+    if (!idx->renv) TRY(dalloc(&idx->renv, 2 * (size_t)idx->N));
+    for (Slot& sl : idx->slot)
+        if (!sl.cand2) TRY(dalloc(&sl.cand2, (size_t)idx->N));
+    TRY(join_streams(idx));
+    const int n = idx->n;
+    int wr = (int)((96 * 1024) / ((size_t)12 * n));
+    wr = wr < 1 ? 1 : (wr > 8 ? 8 : wr);
+    long long need = (idx->N + wr - 1) / wr, cap = (long long)idx->sms * 16;
+    cudaEvent_t a = nullptr, b = nullptr;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, idx->stream));
+    k_renv<<<(int)(need < cap ? need : cap), 32 * wr, (size_t)wr * 12 * n, idx->stream>>>(idx->rows, idx->perm, idx->N, n,
+                                                                                       reach, idx->beta32, idx->renv);
+    LAUNCHED(idx);
+    CK(cudaEventRecord(b, idx->stream));
+    CK(cudaEventSynchronize(b));
+    float ms = 0.0f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    idx->renv_ms = ms;
+    idx->renv_reach = reach;
+    return MESSI_OK;
+}
+
 static messi_status launch_lbk_filter(messi_index* idx, Slot& sl, int reach, bool strip, const float* q_dev,
                                       cudaStream_t rs, float* rev_out = nullptr)
 {
     const int n = idx->n;
     bool rev = false;
+    // the scan's candidates, or those of them passing the reverse envelope-PAA bound
+    const uint2* cand = sl.cand;
+    const unsigned* cnt_p = &sl.st->cand_count;
+    if (strip && renv_on(idx, reach)) {
+        k_rev_paa_filter<<<idx->sms * 3, 256, kRevTabBytes, rs>>>(sl.cand, idx->renv, idx->lo_w, idx->hi_w, n / MESSI_W,
+                                                                  sl.st, sl.cand2, 0);
+        LAUNCHED(idx);
+        cand = sl.cand2;
+        cnt_p = &sl.st->rcand_count;
+    }
 #define LAUNCH_REV(NN, RR)                                                                                        \
     if (strip && !rev && n == NN && reach == RR && !no_rev_env()) {                                             \
         if (rev_fused()) {                                                                                        \
@@ -894,12 +959,12 @@ static messi_status launch_lbk_filter(messi_index* idx, Slot& sl, int reach, boo
         } else {                                                                                                  \
             if (lbk_bulk())                                                                                       \
                 k_lbk_filter_q8b<NN><<<idx->sms * 3, 128, lbkb_smem<NN>(), rs>>>(                                \
-                    sl.cand, idx->perm, idx->rows8, idx->meta8, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N,    \
-                    dtw_front(), sl.rlist, rev_rho(), 0x4B000000u);                                              \
+                    cand, idx->perm, idx->rows8, idx->meta8, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N,       \
+                    dtw_front(), sl.rlist, rev_rho(), 0x4B000000u, cnt_p);                                       \
             else                                                                                                  \
                 k_lbk_filter_q8<<<idx->sms * 8, 128, 2 * (size_t)((n + 15) & ~15) * sizeof(float), rs>>>(         \
-                    sl.cand, idx->perm, idx->rows8, idx->meta8, n, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N, \
-                    dtw_front(), sl.rlist, rev_rho());                                                           \
+                    cand, idx->perm, idx->rows8, idx->meta8, n, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N,    \
+                    dtw_front(), sl.rlist, rev_rho(), cnt_p);                                                    \
             LAUNCHED(idx);                                                                                        \
             k_lbk_rev_q8<NN, RR><<<idx->sms * 8, 128, 0, rs>>>(sl.rlist, idx->perm, idx->rows8, q_dev, sl.st,     \
                                                                 sl.list2, (unsigned)idx->N, dtw_front(), rev_out, \
@@ -912,8 +977,8 @@ static messi_status launch_lbk_filter(messi_index* idx, Slot& sl, int reach, boo
     if (rev) {
     } else if (strip)
         k_lbk_filter_q8<<<idx->sms * 8, 128, 2 * (size_t)((n + 15) & ~15) * sizeof(float), rs>>>(
-            sl.cand, idx->perm, idx->rows8, idx->meta8, n, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N, dtw_front(),
-            nullptr, 0.0f);
+            cand, idx->perm, idx->rows8, idx->meta8, n, sl.U, sl.L, sl.st, sl.list2, (unsigned)idx->N, dtw_front(),
+            nullptr, 0.0f, cnt_p);
     else
         k_lbk_filter<4><<<refine_grid(idx, 1024) * 2, 128, lbk_smem(n), rs>>>(
             sl.cand, idx->perm, idx->rows, n, sl.U, sl.L, reach, sl.st, sl.list2, (unsigned)idx->N, dtw_front());
@@ -970,6 +1035,7 @@ static messi_status ensure_dtw_knn(messi_index* idx)
 static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, messi_result* res, messi_stats* stats,
                             int kk = 1)
 {
+    if (dtw_uses_strip(idx->n, reach)) TRY(ensure_renv(idx, reach));
     const int slot = (int)(idx->qcount++ % MESSI_DTW_SLOTS);
     Slot& sl = idx->slot[slot];
     const bool ser = serial_mode(idx);
@@ -1511,9 +1577,9 @@ __global__ void k_dbg_map(const unsigned* __restrict__ ids, int k, int* map, con
     if (cand) cand[t] = make_uint2(inv[ids[t]], 0u);  // (sorted position, 8-bit bound 0)
 }
 __global__ void k_dbg_scatter_cand(const uint2* __restrict__ cand, const QState* st, const unsigned* __restrict__ perm,
-                                   float* __restrict__ out)
+                                   float* __restrict__ out, int rev = 0)
 {
-    const unsigned total = st->cand_count;
+    const unsigned total = rev ? st->rcand_count : st->cand_count;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x)
         out[perm[cand[i].x]] = __uint_as_float(cand[i].y);
 }
@@ -1654,6 +1720,37 @@ extern "C" messi_status messi_debug_lower_bounds(messi_index* idx, const float* 
     return MESSI_OK;
 }
 
+// The reverse envelope-PAA bound of every row (k_renv for `reach`, then k_scan with every
+// tile listed and the threshold at +inf, then k_rev_paa_filter in its rev_only mode).
+extern "C" messi_status messi_debug_rev_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev)
+{
+    if (!lb_dev) return fail(MESSI_EINVAL, "NULL argument");
+    if (reach < 1) return fail(MESSI_EINVAL, "reach %d: the reverse envelope-PAA bound serves reaches >= 1", reach);
+    if (renv_env_off()) return fail(MESSI_EINVAL, "the reverse envelope-PAA filter is off (MESSI_NO_RENV)");
+    TRY(debug_begin(idx, query_dev, reach));
+    TRY(ensure_renv(idx, reach));
+    const float* tab = nullptr;
+    QState* st = nullptr;
+    TRY(debug_tables(idx, query_dev, reach, &tab, &st));
+    Slot& sl = idx->slot[0];
+    cudaStream_t s = idx->stream;
+    k_dbg_state<<<1, 1, 0, s>>>(st, (unsigned)idx->ntiles, 0u, 0u);  // every tile listed, BSF +inf
+    LAUNCHED(idx);
+    CK(cudaMemsetAsync(lb_dev, 0xff, sizeof(float) * (size_t)idx->N, s));  // NaN: not written
+    k_scan<<<scan_grid(idx), 32 * kScanWarps, scan_smem(), s>>>(idx->tiles, idx->sym8, idx->N, tab, st, sl.cand,
+                                                                idx->dbg_iota, 0u);
+    LAUNCHED(idx);
+    k_rev_paa_filter<<<idx->sms * 3, 256, kRevTabBytes, s>>>(sl.cand, idx->renv, idx->lo_w, idx->hi_w, idx->n / MESSI_W,
+                                                             st, sl.cand2, 1);
+    LAUNCHED(idx);
+    k_dbg_scatter_cand<<<idx->sms * 8, 256, 0, s>>>(sl.cand2, st, idx->perm, lb_dev, 1);
+    LAUNCHED(idx);
+    k_arm<<<1, 1, 0, s>>>(st);
+    LAUNCHED(idx);
+    CK(cudaStreamSynchronize(s));
+    return MESSI_OK;
+}
+
 extern "C" messi_status messi_debug_coarse_bounds(messi_index* idx, const float* query_dev, int32_t reach, float* lb_dev)
 {
     if (!lb_dev) return fail(MESSI_EINVAL, "NULL argument");
@@ -1736,6 +1833,7 @@ extern "C" messi_status messi_debug_dtw_stages(messi_index* idx, const float* qu
     if ((!ids_dev && k > 0) || k < 0 || reach < 0) return fail(MESSI_EINVAL, "bad argument");
     TRY(debug_begin(idx, query_dev, reach));
     const bool strip = dtw_uses_strip(idx->n, reach);
+    if (strip) TRY(ensure_renv(idx, reach));  // the query path's filter chain (threshold +inf here)
     if (quantised) *quantised = strip ? 1 : 0;
     if (k == 0) return MESSI_OK;
     cudaStream_t s = idx->stream;

@@ -73,6 +73,11 @@ struct QState {
     unsigned lbk_thr_bits;  // DTW: the scan's threshold (BSF0), used by the LB_Keogh filter
     unsigned list2_back;    // DTW: LB_Keogh survivors appended from the back of list2 (larger LBK)
     unsigned rev_count;     // DTW: forward survivors queued for the reverse LB_Keogh (rlist)
+    // DTW: the query's own PAA per segment, fp32 bounds below / above (directed fp64 sums), for
+    // the scan's reverse envelope-PAA bound against the rows' envelope symbols (renv)
+    float qlo[16], qhi[16];
+    unsigned rcand_count;   // DTW: scan candidates that also passed the reverse envelope-PAA bound
+    unsigned rev_paa;       // DTW: 1 when k_rev_paa_filter ran for this query
     // batch ED: the query quantised like the rows ("quantised-row bound"):
     // c_q = rint(q / s_q) in [-127, 127], s_q a power of two; q8e >= ||q - s_q c_q||;
     // q8sum = sum c_q, q8s2ss = s_q^2 sum c_q^2 (exact in fp64); the words go to qc_all
@@ -90,6 +95,7 @@ struct NearEntry { unsigned id; float d32; };
 // fp32 distances of the rows refined so far (their k-th is the pruning threshold, held in
 // bsf_bits) and the k lexicographically smallest (fp64 d2, id) of the rows re-ranked.
 #define MESSI_MAX_K 64
+constexpr size_t kStatsBytes = 112;  // sizeof(messi_stats) (include/messi.h; asserted in api.cu)
 struct KnnState {
     float d32[MESSI_MAX_K];
     double d64[MESSI_MAX_K];
@@ -117,6 +123,8 @@ __device__ __forceinline__ void arm_state(QState* st)
     st->list2_count = 0;
     st->list2_back = 0;
     st->rev_count = 0;
+    st->rcand_count = 0;
+    st->rev_paa = 0;
     st->near_count = 0;
     st->refined = 0;
     st->abandoned = 0;

@@ -711,7 +711,7 @@ __host__ __device__ inline size_t fused_smem(int n)
 __device__ void fused_finalise(const QState* st, long long N, long long row_begin, void* result, void* stats)
 {
     struct R { double dist; long long id; double d2; long long reserved; };
-    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells, exact, listed, coarse; double seed, bsf; };
+    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells, exact, listed, coarse; double seed, bsf; long long rpaa; };
     const double bd = st->best_d;
     const long long bi = st->best_id;
     R* res = reinterpret_cast<R*>(result);
@@ -735,6 +735,7 @@ __device__ void fused_finalise(const QState* st, long long N, long long row_begi
         s->cells = 0;
         s->seed = (double)__uint_as_float(st->seed_bits);
         s->bsf = (double)__uint_as_float(st->bsf_bits);
+        s->rpaa = s->cand;  // ED: no reverse bound
     }
 }
 
@@ -748,11 +749,11 @@ __global__ void k_finalise_batch(const QState* __restrict__ st_all, int B, long 
     if (b >= B) return;
     if (!knn) {
         fused_finalise(st_all + b, N, row_begin, reinterpret_cast<char*>(results) + (size_t)b * 32,
-                       stats ? reinterpret_cast<char*>(stats) + (size_t)b * 104 : nullptr);
+                       stats ? reinterpret_cast<char*>(stats) + (size_t)b * kStatsBytes : nullptr);
         return;
     }
     fused_finalise(st_all + b, N, row_begin, reinterpret_cast<char*>(results) + (size_t)b * k * 32,
-                   stats ? reinterpret_cast<char*>(stats) + (size_t)b * 104 : nullptr);
+                   stats ? reinterpret_cast<char*>(stats) + (size_t)b * kStatsBytes : nullptr);
     struct R { double dist; long long id; double d2; long long reserved; };
     R* res = reinterpret_cast<R*>(results) + (size_t)b * k;
     const KnnState* kn = knn + b;

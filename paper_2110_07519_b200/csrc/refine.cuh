@@ -218,14 +218,14 @@ __global__ void __launch_bounds__(128) k_lbk_filter_q8(const uint2* __restrict__
                                                        const float2* __restrict__ meta8, int n,
                                                        const float* __restrict__ U_g, const float* __restrict__ L_g,
                                                        QState* st, uint4* __restrict__ list2, unsigned cap, float front,
-                                                       uint4* __restrict__ rlist, float rho)
+                                                       uint4* __restrict__ rlist, float rho, const unsigned* cnt_p)
 {
     extern __shared__ __align__(16) float env[];
     float* U = env;
     float* L = U + ((n + 15) & ~15);
     for (int i = threadIdx.x; i < n; i += blockDim.x) { U[i] = U_g[i]; L[i] = L_g[i]; }
     __syncthreads();
-    const unsigned total = *(volatile unsigned*)&st->cand_count;
+    const unsigned total = *(volatile const unsigned*)cnt_p;  // QState::cand_count or ::rcand_count
     const int lane = threadIdx.x & 31;
     const float thr = __uint_as_float(st->lbk_thr_bits);
     unsigned mf;  // 0x4B000000 (2^23) in a register the compiler cannot fold: PRMT keeps an immediate selector
@@ -632,7 +632,8 @@ __global__ void __launch_bounds__(128) k_lbk_filter_q8b(const uint2* __restrict_
                                                         const float2* __restrict__ meta8, const float* __restrict__ U_g,
                                                         const float* __restrict__ L_g, QState* st,
                                                         uint4* __restrict__ list2, unsigned cap, float front,
-                                                        uint4* __restrict__ rlist, float rho, unsigned mf)
+                                                        uint4* __restrict__ rlist, float rho, unsigned mf,
+                                                        const unsigned* cnt_p)
 {
     constexpr int RS = NN + 16;  // slot stride: 16-byte aligned, LDS.128 quarter-warps conflict-free
     extern __shared__ __align__(128) unsigned char lsm[];
@@ -648,7 +649,7 @@ __global__ void __launch_bounds__(128) k_lbk_filter_q8b(const uint2* __restrict_
     for (int i = threadIdx.x; i < NN; i += blockDim.x) { U[i] = U_g[i]; L[i] = L_g[i]; }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
-    const unsigned total = *(volatile unsigned*)&st->cand_count;
+    const unsigned total = *(volatile const unsigned*)cnt_p;  // QState::cand_count or ::rcand_count
     const float thr = __uint_as_float(st->lbk_thr_bits);
     const uint2 none = make_uint2(0u, 0x7f800000u);
     struct Cur { uint2 ce; bool ok; float2 meta; unsigned id; };
@@ -1111,7 +1112,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
                              void* result, void* stats)
 {
     struct R { double dist; long long id; double d2; long long reserved; };
-    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells, exact, listed, coarse; double seed, bsf; };
+    struct S { long long lb, tiles, cand, lbk, refined, abandoned, near, cells, exact, listed, coarse; double seed, bsf; long long rpaa; };
     R* res = reinterpret_cast<R*>(result);
     res->dist = b.id >= 0 ? sqrt(b.d) : (double)INFINITY;
     res->id = b.id >= 0 ? row_begin + b.id : -1;
@@ -1132,6 +1133,7 @@ __device__ void finish_query(Best b, unsigned nb, QState* st, long long N, long 
         s->coarse = st->coarse_count;
         s->seed = (double)__uint_as_float(st->seed_bits);
         s->bsf = (double)__uint_as_float(st->bsf_bits);
+        s->rpaa = st->rev_paa ? st->rcand_count : st->cand_count;
     }
     arm_state(st);
 }

@@ -52,6 +52,15 @@ __device__ void prologue_block(const float* __restrict__ q, int n, int reach, co
                 st->ubar[s] = ubar[s];
                 st->lbar[s] = lbar[s];
             }
+            if (lut_g && reach >= 0) {  // the reverse envelope-PAA bound: qlo <= mean(q_seg) <= qhi
+                double lo = 0.0, hi = 0.0;
+                for (int j = 0; j < m; ++j) {
+                    lo = __dadd_rd(lo, (double)q[s * m + j]);
+                    hi = __dadd_ru(hi, (double)q[s * m + j]);
+                }
+                st->qlo[s] = __double2float_rd(__ddiv_rd(lo, (double)m));
+                st->qhi[s] = __double2float_ru(__ddiv_ru(hi, (double)m));
+            }
             sym = symbol_of(__double2float_rn(qbar), beta);
         }
         unsigned long long key = 0;
@@ -392,13 +401,18 @@ __device__ __forceinline__ float fine_lb(uint4 w, const char* lbase, int lane)
 // Per-query scan for the DTW path (and the scan-throughput probe): the tiles the box filter
 // listed, coarse + fine bounds, survivors (LB8 <= BSF0 * (1 + eps)) appended as (sorted
 // position, LB8) with one atomicAdd per warp-round.
-__global__ void __launch_bounds__(32 * kScanWarps, 3) k_scan(const uint4* __restrict__ tiles, const uint4* __restrict__ sym8,
+// Latency structure (a warp's tile is a chain of dependent loads: list entry -> tile rows ->
+// 8-bit words -> append): the next tile's rows are loaded while this tile's fine pass runs,
+// the list entry two tiles ahead; a tile's fine survivors are compacted in place in the
+// warp's shared list and appended with ONE atomic per tile (not one per 32-series round).
+__global__ void __launch_bounds__(32 * kScanWarps, 2) k_scan(const uint4* __restrict__ tiles, const uint4* __restrict__ sym8,
                                                              long long N, const float* __restrict__ tab_g, QState* st,
                                                              uint2* __restrict__ out, const unsigned* __restrict__ tlist,
                                                              unsigned epoch)
 {
     extern __shared__ __align__(16) float tab_s[];
     __shared__ unsigned short surv_all[kScanWarps][MESSI_TILE_ROWS];
+    __shared__ float lbs_all[kScanWarps][MESSI_TILE_ROWS];
     __shared__ unsigned wcnt_all[kScanWarps];
     for (int i = threadIdx.x; i < kScanTab / 4; i += blockDim.x)
         reinterpret_cast<float4*>(tab_s)[i] = reinterpret_cast<const float4*>(tab_g)[i];
@@ -407,16 +421,39 @@ __global__ void __launch_bounds__(32 * kScanWarps, 3) k_scan(const uint4* __rest
     if (blockIdx.x == 0 && threadIdx.x == 0) st->lbk_thr_bits = __float_as_uint(thr);  // for the DTW filter
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned short* surv = surv_all[warp];
+    float* lbs = lbs_all[warp];
     const char* lbase = reinterpret_cast<const char*>(tab_s);
     const long long count = (long long)*(volatile unsigned*)&st->tile_count;
-    for (long long it = (long long)blockIdx.x * kScanWarps + warp; it < count; it += (long long)gridDim.x * kScanWarps) {
-        const long long tl = (long long)tlist[it];
-        const int m = scan_tile_coarse(tiles, tl, lbase, thr, N, surv, &wcnt_all[warp], lane);
-        if (lane == 0 && m) atomicAdd(&st->coarse_count, (unsigned)m);
+    const long long stride = (long long)gridDim.x * kScanWarps;
+    long long it = (long long)blockIdx.x * kScanWarps + warp;
+    if (it >= count) return;
+    long long tl = (long long)tlist[it];
+    long long tl_n = it + stride < count ? (long long)tlist[it + stride] : 0;
+    uint4 data[8];
+    {
+        const uint4* tp = tiles + tl * (MESSI_TILE_BYTES / 16) + lane;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) data[t] = __ldcs(tp + t * 32);
+    }
+    unsigned coarse = 0;
+    for (; it < count; it += stride) {
+        float acc[16];
+        coarse_acc_data(data, lbase, lane, acc);
+        const int m = compact_mask(coarse_mask(acc, thr, N, tl, lane), surv, &wcnt_all[warp], lane);
+        coarse += (unsigned)m;
+        // the next tile's rows and the list entry after it, in flight during the fine pass
+        if (it + stride < count) {
+            const uint4* tp = tiles + tl_n * (MESSI_TILE_BYTES / 16) + lane;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) data[t] = __ldcs(tp + t * 32);
+        }
+        const long long tl_nn = it + 2 * stride < count ? (long long)tlist[it + 2 * stride] : 0;
         // rounds of 32 coarse survivors; the next round's 8-bit words are loaded before this
-        // round's bounds are evaluated (DTW: ~40% of a tile survives the coarse bound)
+        // round's bounds are evaluated (DTW: ~40% of a tile survives the coarse bound); the
+        // survivors of a round overwrite list slots already read (cnt <= i0)
         unsigned pos_n = lane < m ? (unsigned)(tl * MESSI_TILE_ROWS + surv[lane]) : 0u;
         uint4 w_n = lane < m ? sym8[pos_n] : make_uint4(0u, 0u, 0u, 0u);
+        int cnt = 0;
         for (int i0 = 0; i0 < m; i0 += 32) {
             const bool v = i0 + lane < m;
             const unsigned pos = pos_n;
@@ -430,12 +467,171 @@ __global__ void __launch_bounds__(32 * kScanWarps, 3) k_scan(const uint4* __rest
             if (v) lb = fine_lb(w, lbase, lane);
             const bool ok = v && lb <= thr;
             const unsigned msk = __ballot_sync(0xffffffffu, ok);
-            if (!msk) continue;
+            __syncwarp();  // every lane read its slot i0 + lane before the slots below are rewritten
+            if (ok) {
+                const int o = cnt + __popc(msk & ((1u << lane) - 1));
+                surv[o] = (unsigned short)(pos - (unsigned)(tl * MESSI_TILE_ROWS));
+                lbs[o] = lb;
+            }
+            cnt += __popc(msk);
+        }
+        if (cnt) {
             unsigned base = 0;
-            if (lane == 0) base = atomicAdd(&st->cand_count, (unsigned)__popc(msk));
+            if (lane == 0) base = atomicAdd(&st->cand_count, (unsigned)cnt);
             base = __shfl_sync(0xffffffffu, base, 0);
-            MESSI_CHECK(!ok || base + __popc(msk & ((1u << lane) - 1)) < (unsigned)N);
-            if (ok) out[base + __popc(msk & ((1u << lane) - 1))] = make_uint2(pos, __float_as_uint(lb));
+            __syncwarp();
+            MESSI_CHECK(base + (unsigned)cnt <= (unsigned)N);
+            for (int i = lane; i < cnt; i += 32)
+                out[base + i] = make_uint2((unsigned)(tl * MESSI_TILE_ROWS + surv[i]), __float_as_uint(lbs[i]));
+        }
+        __syncwarp();  // the list is rewritten by the next tile's compaction
+        tl = tl_n;
+        tl_n = tl_nn;
+    }
+    if (lane == 0 && coarse) atomicAdd(&st->coarse_count, coarse);
+}
+
+// ------------------------------------------------- reverse envelope-PAA bound (DTW)
+// LB_Keogh holds for either series against the envelope of the other (every
+// point of a series lies on the warping path, matched to a point of the other within the
+// reach), and the envelope-PAA reduction of P:1411 applies to either side too: per segment s
+// of m points, Jensen on the convex f(q, L, U)^2 = max(0, q - U, L - q)^2 gives
+//     sum_{i in s} dist(q_i, [L^x_i, U^x_i])^2 >= m dist(qbar_s, [Lbar^x_s, Ubar^x_s])^2,
+// and the left side summed over s is the reverse LB_Keogh (<= DTW).  The rows' envelope PAA
+// is kept per reach as 8-bit symbols whose regions contain it (renv, k_renv), so
+//     LBrp(x) = m sum_s max(0, qbar_s - hi(u_s), lo(l_s) - qbar_s)^2 <= DTW(q, x).
+//
+// k_renv: for the row at sorted position p, u_s = symbol of an fp32 value >= mean(U^x over s)
+// and l_s = symbol of one <= mean(L^x over s) (fp64 sums and quotient rounded up / down), so
+// hi_w(u_s) > Ubar and lo_w(l_s) < Lbar (symbol_of puts x in [beta_{v-1}, beta_v)).
+// out[2p] = u_0..u_15, out[2p+1] = l_0..l_15.  One warp per row staged in shared memory
+// (row, U, L: 3n floats per warp), a lane per point for the clipped-window max / min.
+__global__ void __launch_bounds__(256) k_renv(const float* __restrict__ rows, const unsigned* __restrict__ perm,
+                                              long long N, int n, int R, const float* __restrict__ beta_g,
+                                              uint4* __restrict__ out)
+{
+    extern __shared__ __align__(16) float rsm[];
+    __shared__ float beta[256];
+    for (int i = threadIdx.x; i < 255; i += blockDim.x) beta[i] = beta_g[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    float* x = rsm + (size_t)w * 3 * n;
+    float* U = x + n;
+    float* L = U + n;
+    const int m = n / MESSI_W;
+    for (long long p = (long long)blockIdx.x * nw + w; p < N; p += (long long)gridDim.x * nw) {
+        const float* src = rows + (long long)perm[p] * n;
+        for (int j = lane * 4; j < n; j += 128)
+            *reinterpret_cast<float4*>(x + j) = __ldg(reinterpret_cast<const float4*>(src + j));
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) {
+            const int a = max(0, i - R), b = min(n - 1, i + R);
+            float u = x[a], l = x[a];
+            for (int j = a + 1; j <= b; ++j) { u = fmaxf(u, x[j]); l = fminf(l, x[j]); }
+            U[i] = u;
+            L[i] = l;
+        }
+        __syncwarp();
+        const int s = lane & 15;
+        double acc = 0.0;
+        float v;
+        if (lane < 16) {
+            for (int j = 0; j < m; ++j) acc = __dadd_ru(acc, (double)U[s * m + j]);
+            v = __double2float_ru(__ddiv_ru(acc, (double)m));
+        } else {
+            for (int j = 0; j < m; ++j) acc = __dadd_rd(acc, (double)L[s * m + j]);
+            v = __double2float_rd(__ddiv_rd(acc, (double)m));
+        }
+        unsigned word = (unsigned)symbol_of(v, beta) << (8 * (lane & 3));
+        word |= __shfl_xor_sync(0xffffffffu, word, 1);
+        word |= __shfl_xor_sync(0xffffffffu, word, 2);
+        if ((lane & 3) == 0) reinterpret_cast<unsigned*>(out)[8 * p + (lane >> 2)] = word;
+        __syncwarp();  // x, U, L are rewritten by the next row
+    }
+}
+
+// The reverse envelope-PAA filter over the scan's candidates (cand, QState::cand_count): the
+// ones with LBrp(x) <= the threshold go to out (QState::rcand_count) with LB = max(scan LB,
+// LBrp) (rev_only, inspection: LBrp, every candidate kept).  Table per CTA (64 KB), word
+// v * 64 + c: c = 16x + s: TU[s][v] = m max(0, qlo_s - hi_w(v))^2, c = 32 + 16x + s:
+// TL[s][v] = m max(0, lo_w(v) - qhi_s)^2 (two copies x; fp32 rounded down, qlo / qhi the
+// query's segment means rounded down / up) -- lane l reads segment (s + l) mod 16 of copy
+// l >> 4, 32 distinct banks for any symbols.  At most one of TU, TL is nonzero per segment
+// (u_s >= l_s), so TU + TL is the max form exactly.  A warp takes 128 candidates at a time
+// (their rows' 32-byte words all in flight) and appends its survivors with one atomic.
+constexpr int kRevTabBytes = 256 * 64 * 4;
+__global__ void __launch_bounds__(256) k_rev_paa_filter(const uint2* __restrict__ cand, const uint4* __restrict__ renv,
+                                                        const float* __restrict__ lo_w, const float* __restrict__ hi_w,
+                                                        int m, QState* st, uint2* __restrict__ out, int rev_only)
+{
+    extern __shared__ __align__(16) float rtab[];
+    __shared__ uint2 buf_all[8][128];
+    for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) {
+        const int v = i >> 4, s = i & 15;
+        const float du = fmaxf(0.0f, __fsub_rd(st->qlo[s], hi_w[v]));  // hi_w(255) = +inf: 0
+        const float dl = fmaxf(0.0f, __fsub_rd(lo_w[v], st->qhi[s]));  // lo_w(0) = -inf: 0
+        const float tu = __fmul_rd((float)m, __fmul_rd(du, du)), tl = __fmul_rd((float)m, __fmul_rd(dl, dl));
+        rtab[v * 64 + s] = tu;
+        rtab[v * 64 + 16 + s] = tu;
+        rtab[v * 64 + 32 + s] = tl;
+        rtab[v * 64 + 48 + s] = tl;
+    }
+    __syncthreads();
+    const float thr = __uint_as_float(st->lbk_thr_bits);
+    const unsigned total = *(volatile unsigned*)&st->cand_count;
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->rev_paa = 1u;
+    const int lane = threadIdx.x & 31, r = lane & 15;
+    uint2* buf = buf_all[threadIdx.x >> 5];
+    const char* tb = reinterpret_cast<const char*>(rtab);
+    const unsigned cbase = 64u * (unsigned)(lane >> 4);  // byte offset of copy x
+    const unsigned nwarp = gridDim.x * (blockDim.x >> 5);
+    for (unsigned k0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 128u; k0 < total; k0 += nwarp * 128u) {
+        uint2 ce[4];
+        bool ok[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const unsigned k = k0 + 32u * b + lane;
+            ce[b] = k < total ? cand[k] : make_uint2(0u, 0x7f800000u);
+            ok[b] = k < total && (rev_only || __uint_as_float(ce[b].y) <= thr);
+        }
+        uint4 wu[4], wl[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            wu[b] = ok[b] ? renv[2 * (size_t)ce[b].x] : make_uint4(0u, 0u, 0u, 0u);
+            wl[b] = ok[b] ? renv[2 * (size_t)ce[b].x + 1] : make_uint4(0u, 0u, 0u, 0u);
+        }
+        int cnt = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const uint4 xu = rotate_bytes(wu[b], r), xl = rotate_bytes(wl[b], r);
+            const unsigned uv[4] = {xu.x, xu.y, xu.z, xu.w}, lv[4] = {xl.x, xl.y, xl.z, xl.w};
+            float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int s = 0; s < 16; s += 2) {
+                // byte address of (symbol, column): symbol * 256 + (copy + segment) * 4
+                const unsigned c0 = cbase + 4u * (unsigned)((s + r) & 15), c1 = cbase + 4u * (unsigned)((s + 1 + r) & 15);
+                const unsigned au0 = __byte_perm(uv[s >> 2], c0, 0x5504 | ((s & 3) << 4));
+                const unsigned au1 = __byte_perm(uv[s >> 2], c1, 0x5504 | (((s + 1) & 3) << 4));
+                const unsigned al0 = __byte_perm(lv[s >> 2], c0 + 128u, 0x5504 | ((s & 3) << 4));
+                const unsigned al1 = __byte_perm(lv[s >> 2], c1 + 128u, 0x5504 | (((s + 1) & 3) << 4));
+                const float2 tu = make_float2(*reinterpret_cast<const float*>(tb + au0), *reinterpret_cast<const float*>(tb + au1));
+                const float2 tl = make_float2(*reinterpret_cast<const float*>(tb + al0), *reinterpret_cast<const float*>(tb + al1));
+                acc = fadd2_rd(fadd2_rd(acc, tu), tl);
+            }
+            const float rb = __fadd_rd(acc.x, acc.y);
+            const bool pass = ok[b] && (rev_only || rb <= thr);
+            const unsigned msk = __ballot_sync(0xffffffffu, pass);
+            if (pass)
+                buf[cnt + __popc(msk & ((1u << lane) - 1u))] =
+                    make_uint2(ce[b].x, __float_as_uint(rev_only ? rb : fmaxf(__uint_as_float(ce[b].y), rb)));
+            cnt += __popc(msk);
+        }
+        __syncwarp();
+        if (cnt) {
+            unsigned o = 0;
+            if (lane == 0) o = atomicAdd(&st->rcand_count, (unsigned)cnt);
+            o = __shfl_sync(0xffffffffu, o, 0);
+            for (int i = lane; i < cnt; i += 32) out[o + i] = buf[i];
         }
         __syncwarp();
     }

@@ -47,7 +47,7 @@ class Stats(ctypes.Structure):
                 ("refined", ctypes.c_int64), ("abandoned", ctypes.c_int64), ("near_best", ctypes.c_int64),
                 ("dtw_cells", ctypes.c_int64), ("exact", ctypes.c_int64), ("tiles_listed", ctypes.c_int64),
                 ("coarse", ctypes.c_int64),
-                ("seed_d2", ctypes.c_double), ("bsf_d2", ctypes.c_double)]
+                ("seed_d2", ctypes.c_double), ("bsf_d2", ctypes.c_double), ("rev_paa_pass", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -96,6 +96,8 @@ def lib():
             L.messi_link_peers_local.argtypes = [vp, ctypes.POINTER(vp), i32]
         L.messi_debug_order.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]
         L.messi_debug_lower_bounds.argtypes = [vp, vp, i32, vp]
+        if hasattr(L, "messi_debug_rev_bounds"):  # (MESSI_LIB may name an older build in A/B runs)
+            L.messi_debug_rev_bounds.argtypes = [vp, vp, i32, vp]
         L.messi_debug_tile_bounds.argtypes = [vp, vp, i32, vp]
         L.messi_debug_distances.argtypes = [vp, vp, i32, vp, i32, vp, vp, vp]
         L.messi_debug_super_bounds.argtypes = [vp, vp, vp]
@@ -108,6 +110,8 @@ def lib():
                   "messi_debug_ed_refine", "messi_debug_dtw_stages", "messi_debug_coarse_bounds",
                   "messi_debug_quantised"):
             getattr(L, f).restype = ctypes.c_int
+        if hasattr(L, "messi_debug_rev_bounds"):
+            L.messi_debug_rev_bounds.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -115,7 +119,7 @@ def lib():
 EXPORTED = ["messi_build", "messi_query_ed", "messi_query_dtw", "messi_query_ed_batch", "messi_query_dtw_batch",
             "messi_free", "messi_last_error", "messi_launch_count", "messi_profile_enable", "messi_profile_read",
             "messi_debug_breakpoints",
-            "messi_debug_summaries", "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_distances",
+            "messi_debug_summaries", "messi_debug_order", "messi_debug_lower_bounds", "messi_debug_rev_bounds", "messi_debug_distances",
             "messi_debug_scan_repeat", "messi_debug_tile_bounds", "messi_debug_quantised",
             "messi_debug_coarse_bounds", "messi_batch_state_ipc", "messi_link_peers_ipc",
             "messi_link_peers_local", "messi_query_ed_knn", "messi_query_ed_knn_batch", "messi_debug_super_bounds",
@@ -196,7 +200,7 @@ def _check_batch(queries_dev, results_dev, stats_dev, per_query_results=1, n=Non
 
 def messi_query_ed_batch(handle, queries_dev: torch.Tensor, results_dev: torch.Tensor, stats_dev=None, n=None):
     """Asynchronous on the build stream.  results_dev: uint8 CUDA tensor of nq*32 bytes (see
-    ``result_buffer``); stats_dev: optional nq*104 bytes (``stats_buffer``)."""
+    ``result_buffer``); stats_dev: optional nq*112 bytes (``stats_buffer``)."""
     nq = _check_batch(queries_dev, results_dev, stats_dev, 1, n)
     _check(lib().messi_query_ed_batch(handle, _ptr(queries_dev), nq, _ptr(results_dev), _ptr(stats_dev)))
 
@@ -290,10 +294,11 @@ def messi_profile_enable(handle, enable: bool = True, serial: bool = False):
 
 
 def messi_build_times(handle):
-    """Device ms of the build phases: summarise, key sort, layout, quantise."""
-    out = (ctypes.c_double * 4)()
+    """Device ms of the build phases: summarise, key sort, layout, quantise; renv = the last
+    DTW reverse-envelope symbol pass (per reach, built on the first strip-reach DTW query)."""
+    out = (ctypes.c_double * 5)()
     _check(lib().messi_build_times(handle, out))
-    return {"summarise": out[0], "sort": out[1], "layout": out[2], "quantise": out[3]}
+    return {"summarise": out[0], "sort": out[1], "layout": out[2], "quantise": out[3], "renv": out[4]}
 
 
 def messi_profile_read(handle, kind):
@@ -349,6 +354,13 @@ def messi_debug_order(handle, count: int, device):
 def messi_debug_lower_bounds(handle, query_dev: torch.Tensor, reach: int, count: int):
     lb = torch.empty(count, dtype=torch.float32, device=query_dev.device)
     _check(lib().messi_debug_lower_bounds(handle, _ptr(query_dev), int(reach), _ptr(lb)))
+    return lb
+
+
+def messi_debug_rev_bounds(handle, query_dev: torch.Tensor, reach: int, count: int):
+    """The DTW path's reverse envelope-PAA bound of every row (row order) for reach >= 1."""
+    lb = torch.empty(count, dtype=torch.float32, device=query_dev.device)
+    _check(lib().messi_debug_rev_bounds(handle, _ptr(query_dev), int(reach), _ptr(lb)))
     return lb
 
 
@@ -429,7 +441,7 @@ def _wrap_dev(ptr: int, nbytes: int, device):
     return torch.as_tensor(_Arr(), device=device)
 
 
-RESULT_BYTES, STATS_BYTES = 32, 104
+RESULT_BYTES, STATS_BYTES = 32, 112
 
 
 def result_buffer(nq: int, device) -> torch.Tensor:
@@ -456,10 +468,11 @@ def decode_results_device(buf: torch.Tensor):
 
 def decode_stats(buf: torch.Tensor):
     raw = buf.view(-1, STATS_BYTES).cpu()
-    ints = raw[:, :88].contiguous().view(torch.int64)
-    dbl = raw[:, 88:].contiguous().view(torch.float64)
-    return [dict(zip(STATS_FIELDS, list(map(int, i.tolist())) + list(map(float, d.tolist()))))
-            for i, d in zip(ints, dbl)]
+    ints = raw[:, :88].contiguous().view(torch.int64)       # lb_computed .. coarse
+    dbl = raw[:, 88:104].contiguous().view(torch.float64)   # seed_d2, bsf_d2
+    tail = raw[:, 104:].contiguous().view(torch.int64)      # rev_paa_pass
+    return [dict(zip(STATS_FIELDS, list(map(int, i.tolist())) + list(map(float, d.tolist())) + list(map(int, t.tolist()))))
+            for i, d, t in zip(ints, dbl, tail)]
 
 
 class Index:

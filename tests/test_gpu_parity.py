@@ -217,6 +217,30 @@ def test_lower_bounds_dtw(c1):
         assert np.all(lbk <= oracle.dtw2_rows(Xh[::50], Qh[qi], r))
 
 
+@pytest.mark.parametrize("r", [7, 25, 51])
+def test_rev_paa_bounds_dtw(c1, r):
+    """The DTW path's reverse envelope-PAA filter (k_renv + k_rev_paa_filter, the query path's
+    own kernels, threshold +inf) on EVERY C1 row: GPU <= the oracle's lb_rev_paa2 (O11b) of the
+    row's envelope symbols (safe: the kernel's symbols take rounded-up / -down means and its
+    fp32 sums round down), GPU within 1e-4 of it on >= 99.9 % of the rows (tight), and the
+    chain GPU <= reverse LB_Keogh <= DTW on a row sample."""
+    X, Q, idx, Xh, Qh = c1
+    Us, Ls = oracle.renv_sym_rows(Xh, r)
+    for qi in range(2):
+        lb = messi().messi_debug_rev_bounds(idx.handle, Q[qi].contiguous(), r, X.shape[0]).cpu().numpy()
+        assert not np.isnan(lb).any()
+        ref = oracle.lb_rev_paa2_rows(oracle.paa64(Qh[qi]), Us, Ls, Xh.shape[1])
+        assert np.all(lb <= ref * (1 + 1e-9) + 1e-12)
+        close = np.abs(lb - ref) <= 1e-4 * np.maximum(ref, 1.0)
+        assert close.mean() >= 0.999, close.mean()
+        assert (lb > 0).mean() > 0.5  # prunes something at all
+        for k in range(0, Xh.shape[0], 997):
+            Ux, Lx = oracle.envelope(Xh[k], r)
+            rev = oracle.lb_keogh2(Ux, Lx, Qh[qi])
+            assert lb[k] <= rev * (1 + 1e-9)
+            assert rev <= oracle.dtw2(Qh[qi], Xh[k], r) * (1 + 1e-12)
+
+
 # -------------------------------------------------------------- real distances (A7-A9)
 def _quantise_like_rows(q):
     """The quantisation recipe of the rows, restated for one fp32 vector: s the
@@ -517,9 +541,9 @@ def test_nn_dtw(c1, reach, strip, monkeypatch):
             got = idx2.query_dtw(Q[qi], reach, with_stats=True)
             check_nn(got, d2[qi], ids[qi])
             st = got[3]
-            assert st["candidates"] >= st["lbk_pass"] >= 1
+            assert st["candidates"] >= st["rev_paa_pass"] >= st["lbk_pass"] >= 1
             if reach in REV_REACHES:  # the reverse bound ran on the forward survivors
-                assert st["candidates"] >= st["exact"] >= st["lbk_pass"]
+                assert st["rev_paa_pass"] >= st["exact"] >= st["lbk_pass"]
             else:
                 assert st["exact"] == 0
         res = messi().result_buffer(3, DEV)

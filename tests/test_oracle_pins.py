@@ -324,6 +324,68 @@ def test_lb_env_paa_hand_value_reach1():
     assert oracle.lb_env_paa2(Up, Lp, np.array([0, 3, 0, 0], np.uint8), 8, card=4) < lb
 
 
+def test_lb_rev_paa_hand_value_reach1():
+    """O11b on a worked example (reading R19: LB_Keogh with the series' roles
+    swapped, reduced by PAA as P:1411), cardinality 4 (breakpoints -b, 0, b,
+    b = fp32(Phi^-1(3/4)) = 0.6744897365570068):
+      candidate x = [0, 1, 0, 0, 2, 0, -1, 0], r = 1 -> U^x = [1,1,1,2,2,2,0,0],
+      L^x = [0,0,0,0,0,-1,-1,-1]; w = 4 (m = 2): Ubar = [1, 1.5, 2, 0], Lbar = [0, 0, -0.5, -1]
+      usym = [3, 3, 3, 2] (hi = +inf, +inf, +inf, b), lsym = [2, 2, 1, 0] (lo = 0, 0, -b, -inf)
+      query q = [-1,-1, 1,1, -1,-1, 1,1], qbar = [-1, 1, -1, 1]:
+      seg 0 below lo = 0 by 1; seg 1 inside; seg 2 below lo = -b by 1 - b; seg 3 above hi = b
+      by 1 - b  ->  LB = m (1 + 0 + (1 - b)^2 + (1 - b)^2) = 2.4238277264269072 (fp64, summed in
+      segment order).
+    The reverse LB_Keogh of the pair is 5 (points 0, 1, 4 below L^x by 1; 6, 7 above U^x by
+    1), so LB <= reverse LB_Keogh <= DTW."""
+    x = np.array([0, 1, 0, 0, 2, 0, -1, 0], np.float32)
+    q = np.array([-1, -1, 1, 1, -1, -1, 1, 1], np.float32)
+    u, l = oracle.renv_sym(x, 1, 4, 4)
+    assert u.tolist() == [3, 3, 3, 2] and l.tolist() == [2, 2, 1, 0]
+    qp = oracle.paa64(q, 4)
+    assert qp.tolist() == [-1.0, 1.0, -1.0, 1.0]
+    lb = oracle.lb_rev_paa2(qp, u, l, 8, card=4)
+    assert lb == 2.4238277264269072
+    Ux, Lx = oracle.envelope(x, 1)
+    assert oracle.lb_keogh2(Ux, Lx, q) == 5.0
+    assert lb <= 5.0 <= oracle.dtw2(q, x, 1)
+    # each case is live: moving one box so the query mean falls inside lowers the value
+    assert oracle.lb_rev_paa2(qp, np.array([3, 3, 3, 3], np.uint8), l, 8, card=4) < lb
+    assert oracle.lb_rev_paa2(qp, u, np.array([0, 2, 1, 0], np.uint8), 8, card=4) < lb
+    assert oracle.lb_rev_paa2(qp, u, np.array([2, 2, 0, 0], np.uint8), 8, card=4) < lb
+
+
+def test_lb_rev_paa_chain_and_r0_identity():
+    """O11b lower-bounds the reverse LB_Keogh (hence DTW) on random walks at several reaches;
+    at r = 0 (envelope = the series) it equals O6's mindist of the series' own symbols
+    wherever O4's fp32-PAA symbols agree with O11b's fp64-mean symbols."""
+    X = zwalks(60, 128, 41)
+    Q = zwalks(6, 128, 42)
+    tight = 0
+    for r in (1, 5, 12):
+        for q in Q:
+            qp = oracle.paa64(q, 16)
+            for x in X:
+                u, l = oracle.renv_sym(x, r, 16)
+                lb = oracle.lb_rev_paa2(qp, u, l, 128)
+                Ux, Lx = oracle.envelope(x, r)
+                rev = oracle.lb_keogh2(Ux, Lx, q)
+                assert lb <= rev * (1 + 1e-12) + 1e-12
+                assert rev <= oracle.dtw2(q, x, r) * (1 + 1e-12)
+                tight += lb > 0.25 * rev
+    assert tight > 0.1 * 3 * 6 * 60  # not a vacuous bound
+    agree = 0
+    for q in Q:
+        qp = oracle.paa64(q, 16)
+        for x in X:
+            u, l = oracle.renv_sym(x, 0, 16)
+            assert u.tolist() == l.tolist()
+            _, sym = oracle.isax(x, 16)
+            if sym.tolist() == u.tolist():
+                agree += 1
+                assert oracle.lb_rev_paa2(qp, u, l, 128) == oracle.mindist2(qp, sym, 128)
+    assert agree >= 0.9 * len(Q) * len(X)
+
+
 # ------------------------------------------------------------------------- 1-NN (O8/O13)
 def test_nn_ed_vs_numpy_scan_and_threads():
     X = zwalks(3000, 256, 31)
