@@ -296,6 +296,39 @@ static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R,
     return MESSI_OK;
 }
 
+// The DTW seed's distances at strip reaches (k_seed_rows, one thread per window row); seed_d:
+// k-NN (every window distance), else 1-NN (BSF0 published).
+static messi_status launch_seed_rows(messi_index* idx, const Slot& sl, int n, int R, const float* q_dev,
+                                     cudaStream_t s, float* seed_d, PeerSet ps, int slot, int len)
+{
+    const int H = strip_rows(R);
+    const int rem = (2 * R - 2 * H + 3) % H;
+    const int K = strip_qcopies(n, R);
+    const int T = strip_threads(n, R);
+    const size_t smem = strip_smem(n, R, K, T);
+    const int grid = (len + T - 1) / T;
+    bool launched = false;
+#define LAUNCH_SR(HH, REM, KK, TT)                                                                              \
+    if (!launched && H == HH && rem == REM && K == KK && T == TT) {                                            \
+        k_seed_rows<HH, REM, KK, TT><<<grid > 0 ? grid : 1, TT, smem, s>>>(idx->rows, n, R, q_dev, idx->perm,  \
+                                                                          sl.st, seed_d, ps, slot);             \
+        launched = true;                                                                                        \
+    }
+    MESSI_STRIP_VARIANTS(LAUNCH_SR)
+#undef LAUNCH_SR
+    if (!launched) return fail(MESSI_EINVAL, "no strip DTW variant for reach %d", R);
+    return MESSI_OK;
+}
+
+// The DTW seed runs one thread per window row (k_seed_prologue + k_seed_rows) at the strip
+// reaches (MESSI_SEED_ROWS=0, experiments: the warp-wavefront k_seed_dtw everywhere).
+static bool seed_rows_on()
+{
+    static int v = -1;
+    if (v < 0) v = (getenv("MESSI_SEED_ROWS") && !strcmp(getenv("MESSI_SEED_ROWS"), "0")) ? 0 : 1;
+    return v == 1;
+}
+
 static size_t scan_smem() { return kScanLutBytes; }
 static size_t lbk_smem(int n) { return 2 * (size_t)((n + 3) & ~3) * sizeof(float); }
 
@@ -326,7 +359,8 @@ static messi_status setup_kernels(int device)
     CK(cudaFuncSetAttribute(k_refine_dtw_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_resolve_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(k_resolve_dtw_knn, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-#define SET_ATTR_S(H, REM, K, T) CK(cudaFuncSetAttribute(k_refine_dtw_strip<H, REM, K, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStripSmemMax));
+#define SET_ATTR_S(H, REM, K, T) CK(cudaFuncSetAttribute(k_refine_dtw_strip<H, REM, K, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStripSmemMax)); \
+    CK(cudaFuncSetAttribute(k_seed_rows<H, REM, K, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStripSmemMax));
     MESSI_STRIP_VARIANTS(SET_ATTR_S)
 #undef SET_ATTR_S
 #define SET_ATTR_R(R) CK(cudaFuncSetAttribute(k_refine_dtw<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
@@ -1066,9 +1100,16 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     LAUNCHED(idx);
     {
         ProfScope ps(idx, K_SEED, side);
-        k_seed_dtw<<<seed_grid, 32 * wf, qsm + wf * seed_warp, side>>>(
-            q_dev, n, reach, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32, idx->lo_w, idx->hi_w,
-            sl.lut, sl.tab, sl.U, sl.L, sl.st, kk > 1 ? sl.seedd : nullptr, peers, slot);
+        if (dtw_uses_strip(n, reach) && seed_rows_on()) {  // one thread per window row
+            k_seed_prologue<<<1, 256, qsm, side>>>(q_dev, n, reach, idx->skey, idx->N, idx->window, idx->beta32,
+                                                   idx->lo_w, idx->hi_w, sl.lut, sl.tab, sl.U, sl.L, sl.st);
+            LAUNCHED(idx);
+            TRY(launch_seed_rows(idx, sl, n, reach, q_dev, side, kk > 1 ? sl.seedd : nullptr, peers, slot, len));
+        } else {
+            k_seed_dtw<<<seed_grid, 32 * wf, qsm + wf * seed_warp, side>>>(
+                q_dev, n, reach, idx->rows, idx->skey, idx->perm, idx->N, idx->window, idx->beta32, idx->lo_w,
+                idx->hi_w, sl.lut, sl.tab, sl.U, sl.L, sl.st, kk > 1 ? sl.seedd : nullptr, peers, slot);
+        }
         LAUNCHED(idx);
         if (kk > 1) {  // BSF0 = the k-th smallest window distance
             int np = 1;

@@ -1059,6 +1059,66 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
     }
 }
 
+// DTW seed, step 2, at the strip reaches: ONE THREAD PER WINDOW ROW (k_seed_prologue's
+// window, R14; BSF0 rule as k_seed_dtw): the strip DP of k_refine_dtw_strip (DtwStrip<H>) over
+// the row, abandoned once the strip's row minimum exceeds the best finished window distance
+// (every warping path crosses that row, and costs are >= 0: the row cannot be the window's
+// minimum); finished rows publish their fp32 DTW (1-NN) or, with seed_d (k-NN), every row runs
+// to the end and its distance goes to seed_d for k_seed_select.  The DP costs ~2.5
+// instructions per cell where the warp wavefront (k_seed_dtw) spends ~45 per anti-diagonal
+// step, so the seed holds ceil(window / T) CTAs instead of the whole GPU.
+template <int H, int REM, int K, int T>
+__global__ void __launch_bounds__(T) k_seed_rows(const float* __restrict__ rows, int n, int R,
+                                                 const float* __restrict__ q_g, const unsigned* __restrict__ perm,
+                                                 QState* st, float* __restrict__ seed_d, PeerSet ps, int slot)
+{
+    extern __shared__ __align__(16) float dsm[];
+    float2* qrep = reinterpret_cast<float2*>(dsm + (size_t)(2 * R + 2) * T);
+    for (int x = threadIdx.x; x < (n + 2 * R) * K; x += T) {
+        const int i = x / K - R;
+        qrep[x] = make_float2((i >= 0 && i < n) ? q_g[i] : INFINITY, (i >= 1 && i <= n) ? q_g[i - 1] : INFINITY);
+    }
+    __syncthreads();
+    const int len = st->window_len;
+    const int k = blockIdx.x * T + threadIdx.x;
+    if (k >= len) return;
+    const int lane = threadIdx.x & 31;
+    float* Bt = dsm + threadIdx.x;
+    const float2* qlane = qrep + (lane & (K - 1));
+    const int nfull = (2 * R - 2 * H + 3) / H;
+    const float* c = rows + (long long)perm[st->window_start + k] * n;
+    for (int x = 0; x < 2 * R + 2; ++x) Bt[x * T] = x == R ? 0.0f : INFINITY;  // virtual row -1
+    auto load_h = [&](int j, float (&dst)[H]) {
+        if constexpr (H % 4 == 0) {
+#pragma unroll
+            for (int b = 0; b < H / 4; ++b) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(c + j) + b);
+                dst[4 * b] = v.x; dst[4 * b + 1] = v.y; dst[4 * b + 2] = v.z; dst[4 * b + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < H; ++u) dst[u] = __ldg(c + j + u);
+        }
+    };
+    DtwStrip<H> dp;
+    float cnext[H];
+    load_h(0, cnext);
+    for (int j0 = 0; j0 < n; j0 += H) {
+#pragma unroll
+        for (int u = 0; u < H; ++u) dp.cv[u] = cnext[u];
+        if (j0 + H < n) load_h(j0 + H, cnext);
+        dp.template run<REM, K, T>(Bt, qlane + (size_t)j0 * K, R, nfull);
+        if (!seed_d && dp.rmin * 0.9990234375f > slack_up(ld_bsf_eff(st, ps.epoch))) return;
+    }
+    const float d = Bt[R * T];  // D(n-1, n-1)
+    if (seed_d) {
+        seed_d[k] = d;
+    } else {
+        bsf_publish(st, ps, slot, d);
+        atomicMin(&st->seed_bits, __float_as_uint(d));
+    }
+}
+
 // Stage one row into a warp's shared buffer (float4, n % 4 == 0).
 __device__ __forceinline__ void stage_row(float* dst, const float* __restrict__ src, int n, int lane)
 {

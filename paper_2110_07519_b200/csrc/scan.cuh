@@ -215,6 +215,31 @@ __global__ void k_seed_dtw(const float* __restrict__ q_g, int n, int reach, cons
     }
 }
 
+// DTW seed, step 1 (k_seed_rows does the distances): one CTA runs k_seed_dtw's prologue
+// (envelope, tables) and window search and records the window in the query state.
+__global__ void __launch_bounds__(256) k_seed_prologue(const float* __restrict__ q_g, int n, int reach,
+                                                       const unsigned long long* __restrict__ skey, long long N,
+                                                       int window, const float* __restrict__ beta_g,
+                                                       const float* __restrict__ lo_w, const float* __restrict__ hi_w,
+                                                       float* __restrict__ lut_g, float* __restrict__ tab,
+                                                       float* __restrict__ U_g, float* __restrict__ L_g, QState* st)
+{
+    extern __shared__ __align__(16) float q_s[];
+    __shared__ unsigned long long qkey_s;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) q_s[i] = q_g[i];
+    __syncthreads();
+    prologue_block(q_s, n, reach, beta_g, lo_w, hi_w, lut_g, tab, U_g, L_g, &qkey_s, st);
+    __syncthreads();
+    const unsigned long long qkey = qkey_s;
+    const long long a = block_lower_bound(skey, N, qkey);
+    const int len = (int)min((long long)window, N);
+    if (threadIdx.x == 0) {
+        st->qkey = qkey;
+        st->window_start = (int)max(0LL, min(a - len / 2, N - len));
+        st->window_len = len;
+    }
+}
+
 // ---------------------------------------------------------------------- tile filter
 // MESSI's node pruning (Alg. 7 TraverseRootSubtree: "if FindDist(node) > BSF then prune",
 // P:1117-1143) on the flat tile array: the box of a tile (per segment the min and max
