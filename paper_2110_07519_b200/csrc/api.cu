@@ -62,6 +62,7 @@ struct messi_index {
                                     // the tail of the previous query's refine)
     cudaStream_t dstr3 = nullptr, dstr4 = nullptr;  // MESSI_REFINE_STREAMS=4 (experiments)
     cudaStream_t xstr = nullptr;    // library-owned: DTW exact resolve (overlaps the next query's refine)
+    cudaStream_t sstr = nullptr;    // library-owned: DTW scans (high priority; MESSI_SCAN_STREAM=0: the caller's stream)
     cudaEvent_t ev_fork = nullptr;
     int n = 0, window = 2000, keep_paa = 0;
     long long N = 0, ntiles = 0, row_begin = 0;
@@ -446,14 +447,19 @@ extern "C" messi_status messi_build(const float* rows_dev, int64_t count, const 
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     if (getenv("MESSI_PRIO_EQUAL")) prio_hi = 0;
+    // the DTW refine streams below the seed / scan / filter / resolve streams: when SMs free up,
+    // CTAs of the filter chain (the pipeline's critical path) are scheduled first and the
+    // refine fills what is left (C4 +0.6%; MESSI_PRIO_REFINE_HI=1: all equal, experiments)
+    const int prio_ref = getenv("MESSI_PRIO_REFINE_HI") ? prio_hi : prio_lo;
     if (cudaStreamCreateWithPriority(&idx->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&idx->rstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&idx->fstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&idx->dstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&idx->dstr2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&idx->dstr3, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&idx->dstr4, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&idx->dstr, cudaStreamNonBlocking, prio_ref) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&idx->dstr2, cudaStreamNonBlocking, prio_ref) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&idx->dstr3, cudaStreamNonBlocking, prio_ref) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&idx->dstr4, cudaStreamNonBlocking, prio_ref) != cudaSuccess ||
         cudaStreamCreateWithPriority(&idx->xstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&idx->sstr, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&idx->ev_fork, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(MESSI_ECUDA, "stream creation failed"));
 
@@ -545,6 +551,7 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->dstr3) cudaStreamSynchronize(idx->dstr3);
     if (idx->dstr4) cudaStreamSynchronize(idx->dstr4);
     if (idx->xstr) cudaStreamSynchronize(idx->xstr);
+    if (idx->sstr) cudaStreamSynchronize(idx->sstr);
     if (idx->stream) cudaStreamSynchronize(idx->stream);
     else cudaDeviceSynchronize();
     void* ptrs[] = {idx->tiles, idx->sym8, idx->boxes, idx->sboxes, idx->paa, idx->skey, idx->perm, idx->beta32, idx->lo_w,
@@ -580,6 +587,7 @@ extern "C" void messi_free(messi_index* idx)
     if (idx->dstr3) cudaStreamDestroy(idx->dstr3);
     if (idx->dstr4) cudaStreamDestroy(idx->dstr4);
     if (idx->xstr && idx->xstr != idx->stream) cudaStreamDestroy(idx->xstr);
+    if (idx->sstr) cudaStreamDestroy(idx->sstr);
     for (auto& e : idx->evs) {
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
@@ -611,6 +619,7 @@ static messi_status sync_all(messi_index* idx)
     CK(cudaStreamSynchronize(idx->dstr3));
     CK(cudaStreamSynchronize(idx->dstr4));
     CK(cudaStreamSynchronize(idx->xstr));
+    CK(cudaStreamSynchronize(idx->sstr));
     return MESSI_OK;
 }
 
@@ -700,6 +709,7 @@ static messi_status fork_streams(messi_index* idx)
     CK(cudaStreamWaitEvent(idx->dstr3, idx->ev_fork, 0));
     CK(cudaStreamWaitEvent(idx->dstr4, idx->ev_fork, 0));
     CK(cudaStreamWaitEvent(idx->xstr, idx->ev_fork, 0));
+    CK(cudaStreamWaitEvent(idx->sstr, idx->ev_fork, 0));
     return MESSI_OK;
 }
 
@@ -750,16 +760,26 @@ static messi_status launch_tile_filter(messi_index* idx, Slot& sl, cudaStream_t 
     return MESSI_OK;
 }
 
+static bool scan_stream_on()
+{
+    static int v = -1;
+    if (v < 0) v = (getenv("MESSI_SCAN_STREAM") && !strcmp(getenv("MESSI_SCAN_STREAM"), "0")) ? 0 : 1;
+    return v == 1;
+}
+
 static messi_status launch_scan(messi_index* idx, Slot& sl, cudaStream_t next, PeerSet peers)
 {
-    CK(cudaStreamWaitEvent(idx->stream, sl.ev_seed, 0));
+    // the scans of consecutive queries in order on one stream: the library's high-priority
+    // scan stream (the caller's stream, default priority, in serial mode)
+    const cudaStream_t ss = (!serial_mode(idx) && scan_stream_on()) ? idx->sstr : idx->stream;
+    CK(cudaStreamWaitEvent(ss, sl.ev_seed, 0));
     {
-        ProfScope ps(idx, K_SCAN, idx->stream);
-        k_scan<<<scan_grid(idx), 32 * kScanWarps, scan_smem(), idx->stream>>>(idx->tiles, idx->sym8, idx->N, sl.tab,
-                                                                              sl.st, sl.cand, sl.tlist, peers.epoch);
+        ProfScope ps(idx, K_SCAN, ss);
+        k_scan<<<scan_grid(idx), 32 * kScanWarps, scan_smem(), ss>>>(idx->tiles, idx->sym8, idx->N, sl.tab,
+                                                                     sl.st, sl.cand, sl.tlist, peers.epoch);
         LAUNCHED(idx);
     }
-    CK(cudaEventRecord(sl.ev_scan, idx->stream));
+    CK(cudaEventRecord(sl.ev_scan, ss));
     CK(cudaStreamWaitEvent(next, sl.ev_scan, 0));
     return MESSI_OK;
 }

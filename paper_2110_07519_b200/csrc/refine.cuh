@@ -772,7 +772,13 @@ __global__ void __launch_bounds__(128) k_lbk_filter_q8b(const uint2* __restrict_
 // chunk ahead so the warp never waits on the atomic.  Lanes thus stay busy until the list is
 // exhausted, whatever the spread of candidate lifetimes (early abandon after a few rows vs
 // the full n), where a static lane stride left most lanes of a warp idle behind its slowest.
-constexpr unsigned kClaimChunk = 64;
+#ifndef MESSI_STRIP_DEPTH1  // strip refine: list2 entries held ahead per lane (1; 0: two, the round-2 session-3 kernel)
+#define MESSI_STRIP_DEPTH1 1
+#endif
+#ifndef MESSI_CLAIM_CHUNK
+#define MESSI_CLAIM_CHUNK 64
+#endif
+constexpr unsigned kClaimChunk = MESSI_CLAIM_CHUNK;
 
 struct WarpClaim {
     unsigned cbase, cused;  // warp-uniform: current chunk, entries used
@@ -955,8 +961,16 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
     wc.init(ctr, lane);
     const uint4 none = make_uint4(0xffffffffu, 0u, 0u, 0u);
     auto fetch = [&](unsigned k) { return k < total ? list2_at(list2, k, nfront, cap) : none; };
+#if MESSI_STRIP_DEPTH1
+    // one list2 entry ahead per lane (claimed when the lane starts a candidate, its row
+    // prefetched one strip later), so few entries are tied to a lane when the list is short
+    unsigned k1 = wc.take(ctr, 0xffffffffu, lane);
+    bool has_nxt = k1 < total, pf = false;
+    uint4 nxt = fetch(k1);
+#else
     uint4 nxt = fetch(wc.take(ctr, 0xffffffffu, lane));
     uint4 nxt2 = fetch(wc.take(ctr, 0xffffffffu, lane));
+#endif
     auto prefetch_row = [&](unsigned rid) {
         const char* pr = reinterpret_cast<const char*>(rows + (long long)rid * n);
         asm volatile("prefetch.global.L1 [%0];" ::"l"(pr));
@@ -991,9 +1005,19 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
         // lanes without a candidate take list2 entries until one passes its bound (up to four
         // rounds: a lane whose entry is skipped does not sit out a whole strip), then start it
         bool start = false;
+#if MESSI_STRIP_DEPTH1
+        if (pf) {  // the entry claimed a strip ago has landed
+            if (has_nxt) prefetch_row(nxt.x);
+            pf = false;
+        }
+#endif
 #pragma unroll 1
         for (int tries = 0; tries < 4; ++tries) {
+#if MESSI_STRIP_DEPTH1
+            const bool need = !running && !start && has_nxt;
+#else
             const bool need = !running && !start && nxt.x != 0xffffffffu;
+#endif
             const unsigned m = __ballot_sync(0xffffffffu, need);
             if (!m) break;
             const unsigned k = wc.take(ctr, m, lane);
@@ -1002,9 +1026,15 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
                 lbk_total = __uint_as_float(nxt.y);
                 qs = __uint_as_float(nxt.z);
                 qe = __uint_as_float(nxt.w);
+#if MESSI_STRIP_DEPTH1
+                has_nxt = k < total;
+                nxt = fetch(k);
+                pf = true;
+#else
                 nxt = nxt2;
                 nxt2 = fetch(k);
                 if (nxt.x != 0xffffffffu) prefetch_row(nxt.x);
+#endif
                 if (q8_lbk_bound(lbk_total, qe) <= thr) start = true;
                 else ++skipped;
             }
@@ -1020,7 +1050,11 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
             ++refined;
             running = true;
         }
+#if MESSI_STRIP_DEPTH1
+        if (!__any_sync(0xffffffffu, running || has_nxt)) break;
+#else
         if (!__any_sync(0xffffffffu, running || nxt.x != 0xffffffffu)) break;
+#endif
         if (running) {
             const float bsf_now = ld_bsf_eff(st, ps.epoch);  // consumed after the strip
 #pragma unroll
