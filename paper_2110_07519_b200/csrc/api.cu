@@ -32,9 +32,6 @@ using namespace messi;
 
 // Per-query state sets of the DTW path: queries in flight at once (the stages of
 // consecutive queries overlap across the library's streams).
-#ifndef MESSI_PROBE_DEFAULT
-#define MESSI_PROBE_DEFAULT 0  // candidates of the DTW probe pass (0: off)
-#endif
 #ifndef MESSI_DTW_SLOTS
 #define MESSI_DTW_SLOTS 4  // C4: 2 -> 1136, 3 -> 1232, 4 -> 1281, 6 -> 1303, 8 -> 1307 q/s
 #endif
@@ -46,7 +43,6 @@ struct Slot {
     uint4* list2 = nullptr;   // DTW: LB_Keogh survivors (id, LBK, LBK of the first window, 0)  [lazy]
     uint4* rlist = nullptr;   // DTW: forward survivors queued for the reverse bound               [lazy]
     uint2* cand2 = nullptr;   // DTW: scan survivors passing the reverse envelope-PAA bound         [lazy]
-    unsigned* probe = nullptr;  // DTW probe pass: bound histogram, picked count, picked positions  [lazy]
     unsigned* tlist = nullptr;  // tiles surviving the box filter
     NearEntry* near = nullptr;  // near-best (id, d32) of the DTW refine                          [lazy]
     double* rbuf = nullptr;     // DTW resolve: global wavefront scratch for long series         [lazy]
@@ -304,8 +300,7 @@ static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R,
 // The DTW seed's distances at strip reaches (k_seed_rows, one thread per window row); seed_d:
 // k-NN (every window distance), else 1-NN (BSF0 published).
 static messi_status launch_seed_rows(messi_index* idx, const Slot& sl, int n, int R, const float* q_dev,
-                                     cudaStream_t s, float* seed_d, PeerSet ps, int slot, int len,
-                                     const unsigned* probe = nullptr)
+                                     cudaStream_t s, float* seed_d, PeerSet ps, int slot, int len)
 {
     const int H = strip_rows(R);
     const int rem = (2 * R - 2 * H + 3) % H;
@@ -317,7 +312,7 @@ static messi_status launch_seed_rows(messi_index* idx, const Slot& sl, int n, in
 #define LAUNCH_SR(HH, REM, KK, TT)                                                                              \
     if (!launched && H == HH && rem == REM && K == KK && T == TT) {                                            \
         k_seed_rows<HH, REM, KK, TT><<<grid > 0 ? grid : 1, TT, smem, s>>>(idx->rows, n, R, q_dev, idx->perm,  \
-                                                                          sl.st, seed_d, ps, slot, probe);      \
+                                                                          sl.st, seed_d, ps, slot);             \
         launched = true;                                                                                        \
     }
     MESSI_STRIP_VARIANTS(LAUNCH_SR)
@@ -576,7 +571,7 @@ extern "C" void messi_free(messi_index* idx)
     }
     for (Slot& sl : idx->slot) {
         void* sp[] = {sl.lut, sl.tab, sl.U, sl.L, sl.cand, sl.cand2, sl.list2, sl.rlist, sl.near, sl.tlist, sl.rbuf, sl.knn,
-                      sl.seedd, sl.probe};
+                      sl.seedd};
         for (void* p : sp)
             if (p) cudaFree(p);
         cudaEvent_t es[] = {sl.ev_seed, sl.ev_scan, sl.ev_lbk, sl.ev_refined, sl.ev_done};
@@ -971,8 +966,6 @@ static messi_status ensure_renv(messi_index* idx, int reach)
     if (!idx->renv) TRY(dalloc(&idx->renv, 2 * (size_t)idx->N));
     for (Slot& sl : idx->slot)
         if (!sl.cand2) TRY(dalloc(&sl.cand2, (size_t)idx->N));
-    for (Slot& sl : idx->slot)
-        if (!sl.probe) TRY(dalloc(&sl.probe, kProbeWords));
     TRY(join_streams(idx));
     const int n = idx->n;
     int wr = (int)((96 * 1024) / ((size_t)12 * n));
@@ -996,18 +989,8 @@ static messi_status ensure_renv(messi_index* idx, int reach)
     return MESSI_OK;
 }
 
-// The probe pass (refine.cuh, "DTW probe pass"): candidates probed per 1-NN query before the
-// LB_Keogh filters (MESSI_PROBE=0, experiments: off).
-static int probe_want()
-{
-    static int v = -1;
-    if (v < 0) v = getenv("MESSI_PROBE") ? atoi(getenv("MESSI_PROBE")) : MESSI_PROBE_DEFAULT;
-    return v < 0 ? 0 : (v > kProbeCap ? kProbeCap : v);
-}
-
 static messi_status launch_lbk_filter(messi_index* idx, Slot& sl, int reach, bool strip, const float* q_dev,
-                                      cudaStream_t rs, float* rev_out = nullptr, bool probe = false,
-                                      PeerSet peers = PeerSet{nullptr, 0, 0u}, int slot = 0)
+                                      cudaStream_t rs, float* rev_out = nullptr)
 {
     const int n = idx->n;
     bool rev = false;
@@ -1020,17 +1003,6 @@ static messi_status launch_lbk_filter(messi_index* idx, Slot& sl, int reach, boo
         LAUNCHED(idx);
         cand = sl.cand2;
         cnt_p = &sl.st->rcand_count;
-        if (probe && probe_want() > 0 && sl.probe) {
-            CK(cudaMemsetAsync(sl.probe, 0, sizeof(unsigned) * kProbeList, rs));
-            k_probe_hist<<<idx->sms, 256, 0, rs>>>(cand, cnt_p, sl.st, sl.probe);
-            LAUNCHED(idx);
-            k_probe_pick<<<idx->sms, 256, 0, rs>>>(cand, cnt_p, sl.st, sl.probe, (unsigned)probe_want());
-            LAUNCHED(idx);
-            TRY(launch_seed_rows(idx, sl, n, reach, q_dev, rs, nullptr, peers, slot, kProbeCap, sl.probe));
-            LAUNCHED(idx);
-            k_probe_thr<<<1, 1, 0, rs>>>(sl.st, peers.epoch);
-            LAUNCHED(idx);
-        }
     }
 #define LAUNCH_REV(NN, RR)                                                                                        \
     if (strip && !rev && n == NN && reach == RR && !no_rev_env()) {                                             \
@@ -1177,7 +1149,7 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     }
     {
         ProfScope ps(idx, K_LBK, rs);
-        if (!skipf) TRY(launch_lbk_filter(idx, sl, reach, strip, q_dev, rs, nullptr, kk == 1, peers, slot));
+        if (!skipf) TRY(launch_lbk_filter(idx, sl, reach, strip, q_dev, rs));
     }
     // the refine and the resolve run on their own stream: the LB_Keogh filter of the next
     // query (bandwidth-bound) overlaps this query's band DP (latency / ALU-bound)

@@ -1093,86 +1093,6 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
     }
 }
 
-// ------------------------------------------------------------------------ DTW probe pass
-// Best-first step of the DTW path (the paper's priority queues hand out the leaves with the
-// smallest lower bounds first so that the BSF tightens early): the
-// candidates with the smallest bounds after the scan and the reverse envelope-PAA filter run
-// their DTW BEFORE the LB_Keogh filters, and the filters then prune against the BSF those
-// distances reached instead of the approximate search's BSF0.  Only ever LOWERS the threshold
-// to the fp32 DTW of a real row (the same rule as the seed), so no answer is lost; the probed
-// rows stay in the candidate list and are refined again with the rest.
-// Per-slot probe buffer (unsigned words): [0, 256) histogram of LB / thr in 1/256 steps,
-// [kProbeCount] picked entries, [kProbeList, +kProbeCap) their sorted positions.
-constexpr int kProbeBins = 256;
-constexpr int kProbeCount = 256;
-constexpr int kProbeList = 264;
-constexpr int kProbeCap = 2048;
-constexpr size_t kProbeWords = kProbeList + kProbeCap;
-
-__device__ __forceinline__ int probe_bin(float lb, float scale)
-{
-    const float b = lb * scale;  // NaN-free: lb >= 0, scale finite
-    return b >= (float)(kProbeBins - 1) ? kProbeBins - 1 : (int)b;
-}
-
-__global__ void __launch_bounds__(256) k_probe_hist(const uint2* __restrict__ cand, const unsigned* __restrict__ cnt_p,
-                                                    const QState* st, unsigned* __restrict__ probe)
-{
-    __shared__ unsigned h[kProbeBins];
-    h[threadIdx.x] = 0u;
-    __syncthreads();
-    const unsigned total = *cnt_p;
-    const float thr = __uint_as_float(st->lbk_thr_bits);
-    const float scale = thr > 0.0f && thr < INFINITY ? (float)kProbeBins / thr : 0.0f;
-    for (unsigned k = blockIdx.x * 256u + threadIdx.x; k < total; k += gridDim.x * 256u)
-        atomicAdd(&h[probe_bin(__uint_as_float(cand[k].y), scale)], 1u);
-    __syncthreads();
-    if (h[threadIdx.x]) atomicAdd(&probe[threadIdx.x], h[threadIdx.x]);
-}
-
-// Picks the entries of the lowest histogram bins that together hold >= want candidates.
-__global__ void __launch_bounds__(256) k_probe_pick(const uint2* __restrict__ cand, const unsigned* __restrict__ cnt_p,
-                                                    const QState* st, unsigned* __restrict__ probe, unsigned want)
-{
-    __shared__ int s_cut;
-    if (threadIdx.x < 32) {  // the cut bin: first b with cum(b) >= want
-        unsigned run = 0;
-        int cut = kProbeBins - 1;
-        bool found = false;
-        for (int b0 = 0; b0 < kProbeBins && !found; b0 += 32) {
-            const unsigned v = probe[b0 + threadIdx.x];
-            unsigned inc = v;
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
-                if ((int)threadIdx.x >= o) inc += t;
-            }
-            const unsigned hit = __ballot_sync(0xffffffffu, run + inc >= want);
-            if (hit) { cut = b0 + __ffs(hit) - 1; found = true; }
-            run += __shfl_sync(0xffffffffu, inc, 31);
-        }
-        if (threadIdx.x == 0) s_cut = cut;
-    }
-    __syncthreads();
-    const int cut = s_cut;
-    const unsigned total = *cnt_p;
-    const float thr = __uint_as_float(st->lbk_thr_bits);
-    const float scale = thr > 0.0f && thr < INFINITY ? (float)kProbeBins / thr : 0.0f;
-    for (unsigned k = blockIdx.x * 256u + threadIdx.x; k < total; k += gridDim.x * 256u) {
-        const uint2 e = cand[k];
-        if (probe_bin(__uint_as_float(e.y), scale) <= cut) {
-            const unsigned o = atomicAdd(&probe[kProbeCount], 1u);
-            if (o < (unsigned)kProbeCap) probe[kProbeList + o] = e.x;
-        }
-    }
-}
-
-// The LB_Keogh filters' threshold after the probe: the BSF the probed rows reached.
-__global__ void k_probe_thr(QState* st, unsigned epoch)
-{
-    const float thr = slack_up(ld_bsf_eff(st, epoch));
-    if (thr < __uint_as_float(st->lbk_thr_bits)) st->lbk_thr_bits = __float_as_uint(thr);
-}
-
 // DTW seed, step 2, at the strip reaches: ONE THREAD PER WINDOW ROW (k_seed_prologue's
 // window, R14; BSF0 rule as k_seed_dtw): the strip DP of k_refine_dtw_strip (DtwStrip<H>) over
 // the row, abandoned once the strip's row minimum exceeds the best finished window distance
@@ -1184,26 +1104,23 @@ __global__ void k_probe_thr(QState* st, unsigned epoch)
 template <int H, int REM, int K, int T>
 __global__ void __launch_bounds__(T) k_seed_rows(const float* __restrict__ rows, int n, int R,
                                                  const float* __restrict__ q_g, const unsigned* __restrict__ perm,
-                                                 QState* st, float* __restrict__ seed_d, PeerSet ps, int slot,
-                                                 const unsigned* __restrict__ probe = nullptr)
+                                                 QState* st, float* __restrict__ seed_d, PeerSet ps, int slot)
 {
     extern __shared__ __align__(16) float dsm[];
-    // probe pass (k_probe_pick's list of the smallest-bound candidates): nothing picked, no work
-    if (probe && blockIdx.x * T >= min(probe[kProbeCount], (unsigned)kProbeCap)) return;
     float2* qrep = reinterpret_cast<float2*>(dsm + (size_t)(2 * R + 2) * T);
     for (int x = threadIdx.x; x < (n + 2 * R) * K; x += T) {
         const int i = x / K - R;
         qrep[x] = make_float2((i >= 0 && i < n) ? q_g[i] : INFINITY, (i >= 1 && i <= n) ? q_g[i - 1] : INFINITY);
     }
     __syncthreads();
-    const int len = probe ? (int)min(probe[kProbeCount], (unsigned)kProbeCap) : st->window_len;
+    const int len = st->window_len;
     const int k = blockIdx.x * T + threadIdx.x;
     if (k >= len) return;
     const int lane = threadIdx.x & 31;
     float* Bt = dsm + threadIdx.x;
     const float2* qlane = qrep + (lane & (K - 1));
     const int nfull = (2 * R - 2 * H + 3) / H;
-    const float* c = rows + (long long)perm[probe ? probe[kProbeList + k] : (unsigned)(st->window_start + k)] * n;
+    const float* c = rows + (long long)perm[st->window_start + k] * n;
     for (int x = 0; x < 2 * R + 2; ++x) Bt[x * T] = x == R ? 0.0f : INFINITY;  // virtual row -1
     auto load_h = [&](int j, float (&dst)[H]) {
         if constexpr (H % 4 == 0) {
@@ -1232,7 +1149,7 @@ __global__ void __launch_bounds__(T) k_seed_rows(const float* __restrict__ rows,
         seed_d[k] = d;
     } else {
         bsf_publish(st, ps, slot, d);
-        if (!probe) atomicMin(&st->seed_bits, __float_as_uint(d));
+        atomicMin(&st->seed_bits, __float_as_uint(d));
     }
 }
 
