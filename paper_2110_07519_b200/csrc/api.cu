@@ -1049,8 +1049,10 @@ static messi_status launch_dtw_refine(messi_index* idx, Slot& sl, int reach, boo
     const int npad = (n + 3) & ~3;
     const size_t qsm = (size_t)npad * sizeof(float);
     bool launched = false;
-    static const bool skip = getenv("MESSI_TIMING_SKIP_REFINE") != nullptr;  // timing experiments only: WRONG answers
+#ifdef MESSI_TIMING_KNOBS  // critical-path experiments only (WRONG answers): never in the default build
+    static const bool skip = getenv("MESSI_TIMING_SKIP_REFINE") != nullptr;
     if (skip) return MESSI_OK;
+#endif
     if (strip) {
         TRY(launch_strip(idx, sl, n, reach, q_dev, rs, knn, kk, ps, slot));
         launched = true;
@@ -1142,7 +1144,11 @@ static messi_status run_dtw(messi_index* idx, const float* q_dev, int reach, mes
     CK(cudaEventRecord(sl.ev_seed, side));
     TRY(launch_scan(idx, sl, rs, peers));
     const bool strip = dtw_uses_strip(n, reach);
-    static const bool skipf = getenv("MESSI_TIMING_SKIP_FILTER") != nullptr;  // timing experiments only: WRONG answers
+#ifdef MESSI_TIMING_KNOBS  // critical-path experiments only (WRONG answers): never in the default build
+    static const bool skipf = getenv("MESSI_TIMING_SKIP_FILTER") != nullptr;
+#else
+    constexpr bool skipf = false;
+#endif
     if (!ser && (idx->qcount & 1)) {  // filters of consecutive queries on two streams (C4: +2%)
         rs = idx->fstr;
         CK(cudaStreamWaitEvent(rs, sl.ev_scan, 0));

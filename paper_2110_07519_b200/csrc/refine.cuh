@@ -775,6 +775,9 @@ __global__ void __launch_bounds__(128) k_lbk_filter_q8b(const uint2* __restrict_
 #ifndef MESSI_STRIP_DEPTH1  // strip refine: list2 entries held ahead per lane (1; 0: two, the round-2 session-3 kernel)
 #define MESSI_STRIP_DEPTH1 1
 #endif
+#ifndef MESSI_STRIP_INTERLEAVE  // strip refine: chunk halves from the two ends of list2 (see k_refine_dtw_strip)
+#define MESSI_STRIP_INTERLEAVE 1
+#endif
 #ifndef MESSI_CLAIM_CHUNK
 #define MESSI_CLAIM_CHUNK 64
 #endif
@@ -960,12 +963,33 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
     WarpClaim wc;
     wc.init(ctr, lane);
     const uint4 none = make_uint4(0xffffffffu, 0u, 0u, 0u);
+#if MESSI_STRIP_INTERLEAVE
+    // Hand-out order: the first half of every 64-entry chunk comes from the START of the list
+    // (the front bin: small LB_Keogh, the candidates that run deep), the second half from its
+    // END (large LB_Keogh: abandoned after a strip or two).  A warp's first claim gives every
+    // lane one entry of each half -- its current candidate and the one it holds ahead -- so no
+    // lane starts with two deep candidates in a row while other warps run out of work (the
+    // front bin then set the kernel's time: two full DPs back to back on ~F/64 warps).
+    // Entry k: a = 32 (k / 64) + k mod 32; k mod 64 < 32: position a (a < ceil(total/2)),
+    // else position total-1-a (a < floor(total/2)); other k below kmax are holes (skipped).
+    static_assert(kClaimChunk == 64, "the interleaved hand-out splits 64-entry chunks in halves");
+    static_assert(MESSI_STRIP_DEPTH1 == 1, "holes of the interleaved order need the has_nxt flag");
+    const unsigned kmax = ((total + 63u) >> 6) << 6, half_lo = (total + 1u) >> 1, half_hi = total >> 1;
+    auto fetch = [&](unsigned k) {
+        const unsigned a = ((k >> 6) << 5) | (k & 31u);
+        const bool hi = (k & 32u) != 0u;
+        if (k >= kmax || a >= (hi ? half_hi : half_lo)) return none;
+        return list2_at(list2, hi ? total - 1u - a : a, nfront, cap);
+    };
+#else
+    const unsigned kmax = total;
     auto fetch = [&](unsigned k) { return k < total ? list2_at(list2, k, nfront, cap) : none; };
+#endif
 #if MESSI_STRIP_DEPTH1
     // one list2 entry ahead per lane (claimed when the lane starts a candidate, its row
     // prefetched one strip later), so few entries are tied to a lane when the list is short
     unsigned k1 = wc.take(ctr, 0xffffffffu, lane);
-    bool has_nxt = k1 < total, pf = false;
+    bool has_nxt = k1 < kmax, pf = false;
     uint4 nxt = fetch(k1);
 #else
     uint4 nxt = fetch(wc.take(ctr, 0xffffffffu, lane));
@@ -1007,7 +1031,7 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
         bool start = false;
 #if MESSI_STRIP_DEPTH1
         if (pf) {  // the entry claimed a strip ago has landed
-            if (has_nxt) prefetch_row(nxt.x);
+            if (has_nxt && nxt.x != 0xffffffffu) prefetch_row(nxt.x);
             pf = false;
         }
 #endif
@@ -1027,7 +1051,7 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
                 qs = __uint_as_float(nxt.z);
                 qe = __uint_as_float(nxt.w);
 #if MESSI_STRIP_DEPTH1
-                has_nxt = k < total;
+                has_nxt = k < kmax;
                 nxt = fetch(k);
                 pf = true;
 #else
@@ -1035,7 +1059,8 @@ __global__ void __launch_bounds__(T) k_refine_dtw_strip(const float* __restrict_
                 nxt2 = fetch(k);
                 if (nxt.x != 0xffffffffu) prefetch_row(nxt.x);
 #endif
-                if (q8_lbk_bound(lbk_total, qe) <= thr) start = true;
+                if (id == 0xffffffffu) {  // a hole of the interleaved order: nothing to refine
+                } else if (q8_lbk_bound(lbk_total, qe) <= thr) start = true;
                 else ++skipped;
             }
         }

@@ -1,4 +1,5 @@
 # Round 2 (session 4): DTW critical-path probe at HEAD (skip runs give WRONG answers; timing only)
+# needs a library built with -DMESSI_TIMING_KNOBS (the skip knobs are compiled out of the default build)
 # and the C4 launch list (ncu, cold / serialised per-launch times)
 run() {
   timeout 300 python bench.py --mode dtw --steps 3 --warmup 3 --no-cpu --latency 0 --repeats 2 > gpurun_out/sab.log 2>/dev/null

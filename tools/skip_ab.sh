@@ -1,4 +1,5 @@
 # timing sensitivity of the DTW pipeline to each stage (answers are wrong in the skip runs)
+# needs a library built with -DMESSI_TIMING_KNOBS (the skip knobs are compiled out of the default build)
 run() {
   timeout 300 python bench.py --mode dtw --steps 3 --warmup 3 --no-cpu --latency 0 --repeats 2 > gpurun_out/sab.log 2>/dev/null
   python -c "
