@@ -270,6 +270,13 @@ static bool use_strip(int n, int R, bool have_band)
     return fits && (!have_band || R >= 7);
 }
 
+static bool strip_trim_on()
+{
+    static int v = -1;
+    if (v < 0) v = (getenv("MESSI_DTW_TRIM") && !strcmp(getenv("MESSI_DTW_TRIM"), "0")) ? 0 : 1;
+    return v == 1;
+}
+
 static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R, const float* q_dev, cudaStream_t rs,
                                  KnnState* knn, int kk, PeerSet ps, int slot)
 {
@@ -287,8 +294,12 @@ static messi_status launch_strip(messi_index* idx, const Slot& sl, int n, int R,
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_dtw_strip<HH, REM, KK, TT>, TT, smem));  \
         const char* oe = getenv("MESSI_DTW_REFINE_OCC"); /* experiments: CTAs per SM */                          \
         if (oe && atoi(oe) > 0 && atoi(oe) < occ) occ = atoi(oe);                                                \
-        k_refine_dtw_strip<HH, REM, KK, TT><<<idx->sms * (occ > 0 ? occ : 1), TT, smem, rs>>>(                   \
-            idx->rows, n, R, q_dev, sl.U, sl.L, sl.list2, (unsigned)idx->N, sl.st, sl.near, knn, kk, ps, slot);  \
+        const unsigned grid = (unsigned)(idx->sms * (occ > 0 ? occ : 1));                                        \
+        /* lists under 4 entries per thread run on 2 of 3 CTAs per SM (MESSI_DTW_TRIM=0, experiments: off) */   \
+        const unsigned full_min = (occ == 3 && strip_trim_on()) ? 4u * grid * TT : 0u;                           \
+        k_refine_dtw_strip<HH, REM, KK, TT><<<grid, TT, smem, rs>>>(idx->rows, n, R, q_dev, sl.U, sl.L, sl.list2, \
+                                                                    (unsigned)idx->N, sl.st, sl.near, knn, kk, ps, \
+                                                                    slot, full_min);                              \
         launched = true;                                                                                         \
     }
     MESSI_STRIP_VARIANTS(LAUNCH_S)
