@@ -174,7 +174,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.nv:
@@ -249,6 +249,10 @@ def run_arm(cfg, args, world, rank, dev, stream, time_steps, warmup, repeats=1):
                 dist_, gid, d2 = M.decode_results_device(res)
                 merged["d2"], merged["gid"] = merge_results(d2, gid)
 
+        # NVML comes up BEFORE the warm-up (its first init takes tens of ms of host time, during
+        # which the GPU would sit idle between the warm-up and the timed steps: the first repeat
+        # then ran 2-3 % below the others)
+        samplers = [ClockSampler(dev.index or 0) for _ in range(max(1, repeats))]
         for _ in range(warmup):
             step()
         torch.cuda.synchronize()
@@ -261,7 +265,7 @@ def run_arm(cfg, args, world, rank, dev, stream, time_steps, warmup, repeats=1):
             launches0 = idx.launches()
             ev0 = torch.cuda.Event(enable_timing=True)
             ev1 = torch.cuda.Event(enable_timing=True)
-            with ClockSampler(dev.index or 0) as clk:
+            with samplers[rpt] as clk:
                 ev0.record(stream)
                 for _ in range(time_steps):
                     step()
