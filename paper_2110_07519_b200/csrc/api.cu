@@ -250,11 +250,12 @@ static int strip_rows(int R)
     return R >= 7 ? 8 : (R >= 3 ? 4 : 2);
 }
 
-// Which refine kernel serves reach R: the strip kernel for R >= 7 (measured faster than
-// the register band from R = 12 on: 3084 vs 2999 q/s at R = 12, 1174 vs 1099 at R = 25,
-// profiles/r01_sweeps_dtw.jsonl) and wherever no register band is instantiated, as long as
-// its shared memory fits; the register band (DtwThread<R>) for R = 2, 5; else the warp
-// wavefront.  MESSI_DTW_STRIP=1 / 0 forces the strip kernel on / off (experiments).
+// Which refine kernel serves reach R: the strip kernel (and with it the strip pipeline: the
+// reverse envelope-PAA filter and the quantised LB_Keogh) for every R >= 1 whose shared
+// memory fits -- also at R = 2, 5 where a register band (DtwThread<R>) is instantiated: the
+// strip pipeline's filters make it 7.5K vs 4.5K q/s at R = 2 on 10M x 256
+// (profiles/r02s5_strip_small_reach.txt); else the warp wavefront.  MESSI_DTW_STRIP=0
+// (experiments, tests) keeps the register bands and the raw LB_Keogh filter reachable.
 // Threads per strip CTA: 128 when the CTA's shared memory fits, else 64 (large reaches).
 static int strip_threads(int n, int R) { return strip_qcopies(n, R) == 1 ? 64 : 128; }
 
@@ -267,7 +268,8 @@ static bool use_strip(int n, int R, bool have_band)
                       strip_smem(n, R, strip_qcopies(n, R), T) <= (size_t)kStripSmemMax;
     if (force == 0) return false;
     if (force == 1) return fits;
-    return fits && (!have_band || R >= 7);
+    (void)have_band;  // the register bands (R = 2, 5) stay reachable with MESSI_DTW_STRIP=0
+    return fits;
 }
 
 static bool strip_trim_on()

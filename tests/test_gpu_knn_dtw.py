@@ -33,9 +33,13 @@ def coll():
     idx.close()
 
 
-@pytest.mark.parametrize("reach,k", [(12, 5), (12, 64), (5, 10), (2, 3), (0, 7), (25, 2)])
-def test_dtw_knn_batch_exact(coll, reach, k):
+@pytest.mark.parametrize("reach,k,strip", [(12, 5, None), (12, 64, None), (5, 10, None), (2, 3, None), (0, 7, None),
+                                           (25, 2, None), (5, 10, "0"), (2, 3, "0")])
+def test_dtw_knn_batch_exact(coll, reach, k, strip, monkeypatch):
+    """strip "0": the register-band refine (MESSI_DTW_STRIP=0) instead of the default strip kernel."""
     from paper_2110_07519_b200 import messi as M
+    if strip is not None:
+        monkeypatch.setenv("MESSI_DTW_STRIP", strip)
     X, Q, idx, Xh, Qh = coll
     d2, ids = oracle.knn("dtw", Xh, Qh, k, r=reach)
     res, st = M.result_buffer(Q.shape[0] * k, DEV), M.stats_buffer(Q.shape[0], DEV)

@@ -291,20 +291,24 @@ def test_ed_refine_stages_every_row(c1):
 REV_REACHES = (12, 25, 51)  # MESSI_REV_SPECS (refine.cuh) at n = 256
 
 
-@pytest.mark.parametrize("reach", [0, 2, 5, 7, 12, 25, 51])
-def test_dtw_stages_elementwise(c1, reach):
+@pytest.mark.parametrize("reach,strip", [(0, None), (2, None), (5, None), (7, None), (12, None), (25, None),
+                                         (51, None), (2, "0"), (5, "0")])
+def test_dtw_stages_elementwise(c1, reach, strip, monkeypatch):
     """The DTW filter and refine KERNELS of the query path on 1,500 C1 rows (the ids handed
     to them as candidates, threshold +inf, refine frozen: no abandon):
-      * LB_Keogh: at strip reaches (r >= 7) the filter's LB_Keogh of the quantised row x^
+      * LB_Keogh: at strip reaches (r >= 1 by default) the filter's LB_Keogh of the quantised row x^
         within fp32 summation error of its fp64 value, and (sqrt(LBK(x^)(1 - 2^-10)) - e)^2
         <= the oracle's raw LB_Keogh <= DTW; at other reaches the raw LB_Keogh within fp32
         error of the oracle's;
       * reverse LB_Keogh (r = 12, 25, 51: the query's points against the candidate's
         envelope): the filter's bound from the quantised row within rounding below its fp64
         value, <= the oracle's raw reverse LB_Keogh <= DTW (NaN, not computed, elsewhere);
-      * refine (strip kernel r >= 7, register band r = 2, 5, warp wavefront r = 0): fp32 DTW^2
+      * refine (strip kernel r >= 1, register band r = 2, 5 under MESSI_DTW_STRIP=0, warp
+        wavefront r = 0): fp32 DTW^2
         within (2n + 2) u relative of the oracle's fp64 DTW^2 (the error of a sum along one
         warping path of <= 2n - 1 cells)."""
+    if strip is not None:  # "0": the register-band path (raw LB_Keogh filter, DtwThread<R>)
+        monkeypatch.setenv("MESSI_DTW_STRIP", strip)
     X, Q, idx, Xh, Qh = c1
     N, n = X.shape
     rng = np.random.default_rng(100 + reach)
@@ -315,7 +319,7 @@ def test_dtw_stages_elementwise(c1, reach):
     lbk, d32 = lbk.cpu().numpy().astype(np.float64), d32.cpu().numpy().astype(np.float64)
     lbr = lbr.cpu().numpy().astype(np.float64)
     assert not np.isnan(lbk).any() and not np.isnan(d32).any()
-    assert quantised == (reach >= 7)
+    assert quantised == (reach >= 1 and strip != "0")
     ref = oracle.dtw2_rows(Xh[ids_np], Qh[2], reach)
     assert np.all(np.abs(d32 - ref) <= (2 * n + 2) * U32 * ref + 1e-30)
     U, L = oracle.envelope(Qh[2], reach)
@@ -524,11 +528,11 @@ def test_nn_ed_batch_spans_launch_groups(c1):
 
 
 @pytest.mark.parametrize("reach,strip", [(25, None), (7, None), (1, None), (3, None), (9, None), (51, None),
-                                         (2, "1"), (5, "1"), (12, "1"), (25, "1")])
+                                         (2, None), (5, None), (2, "0"), (5, "0"), (12, "0"), (25, "0")])
 def test_nn_dtw(c1, reach, strip, monkeypatch):
-    """Exact DTW 1-NN against the oracle.  Reaches 1/3/7/9/51 take the strip kernel
-    (k_refine_dtw_strip, any reach); MESSI_DTW_STRIP=1 forces it where a register-band
-    instantiation exists too."""
+    """Exact DTW 1-NN against the oracle.  Every reach >= 1 takes the strip kernel
+    (k_refine_dtw_strip) by default; MESSI_DTW_STRIP=0 takes the register bands where they are
+    instantiated (2, 5, 12, 25) with the raw LB_Keogh filter."""
     if strip is not None:
         monkeypatch.setenv("MESSI_DTW_STRIP", strip)
     X, Q, idx, Xh, Qh = c1
@@ -542,7 +546,7 @@ def test_nn_dtw(c1, reach, strip, monkeypatch):
             check_nn(got, d2[qi], ids[qi])
             st = got[3]
             assert st["candidates"] >= st["rev_paa_pass"] >= st["lbk_pass"] >= 1
-            if reach in REV_REACHES:  # the reverse bound ran on the forward survivors
+            if reach in REV_REACHES and strip != "0":  # the reverse bound ran on the forward survivors
                 assert st["rev_paa_pass"] >= st["exact"] >= st["lbk_pass"]
             else:
                 assert st["exact"] == 0
