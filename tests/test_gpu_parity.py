@@ -368,6 +368,25 @@ def test_dtw_stages_elementwise(c1, reach, strip, monkeypatch):
         assert np.all(np.abs(lbk - raw) <= (n // 32 + 8) * U32 * raw + 1e-30)
 
 
+@pytest.mark.parametrize("count", [1, 2, 31, 32, 33, 63, 64, 65, 97, 127, 128, 129, 191, 193, 1000])
+def test_dtw_refine_handout_counts(c1, count):
+    """The strip refine's hand-out order (chunks of 64 entries, first half from the start of the
+    list, second half from its end, holes past the middle) reaches EVERY list entry exactly
+    once for list lengths around the chunk and half-chunk boundaries: the frozen refine over
+    `count` candidates returns each one's fp32 DTW^2 (NaN where a candidate was never run)."""
+    X, Q, idx, Xh, Qh = c1
+    n = X.shape[1]
+    reach = 25
+    ids_np = np.random.default_rng(500 + count).choice(20_000, count, replace=False).astype(np.int32)
+    ids = torch.from_numpy(ids_np).to(DEV)
+    q = Q[1].contiguous()
+    lbk, d32, quantised, _ = messi().messi_debug_dtw_stages(idx.handle, q, reach, ids, rev=True)
+    d32 = d32.cpu().numpy().astype(np.float64)
+    assert quantised and not np.isnan(d32).any()
+    ref = oracle.dtw2_rows(Xh[ids_np], Qh[1], reach)
+    assert np.all(np.abs(d32 - ref) <= (2 * n + 2) * U32 * ref + 1e-30)
+
+
 def test_dtw_stages_long_series():
     """The strip refine at n = 2048 with r = 204 (10%) and r = 100 (64-thread CTAs, one query
     copy: the boundary rows fill shared memory), against the oracle's DTW on 160 rows each."""
